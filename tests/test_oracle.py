@@ -1,0 +1,94 @@
+"""Pin the oracle (oracle/) against the golden vectors generated from the
+reference (tests/golden/make_golden.py).  CPU only."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import reference as R
+
+
+def _load(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        return json.load(f)
+
+
+def _traj(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        lines = [json.loads(l) for l in f if l.strip()]
+    return lines[0], [l for l in lines if l["record"] == "step"], lines[-1]
+
+
+def test_fnv_vectors(golden_dir):
+    v = _load(golden_dir, "fnv.json")
+    assert R.digest_hex(R.fnv1a(b"")) == v["empty"] == "cbf29ce484222325"
+    assert R.digest_hex(R.fnv1a(b"a")) == v["a"]
+    assert R.digest_hex(R.fnv1a(b"foobar")) == v["foobar"]
+    assert R.digest_hex(R.digest_text("params")) == v["params"]
+    assert R.digest_hex(R.digest_array(np.arange(8, dtype=np.float64))) == v["arange8"]
+    assert R.digest_hex(R.digest_array(np.array([1.5, -2.25]), R.digest_text("blk0.qkv"))) == v["chain"]
+
+
+def test_stream_keys_and_samples(golden_dir):
+    for s in _load(golden_dir, "streams.json"):
+        assert f"{R.digest_text(s['layer_id']):016x}" == s["lid_hash"]
+        k = R.stream_key(s["seed"], s["step"], s["layer_id"], s["role"])
+        assert [f"{k[0]:016x}", f"{k[1]:016x}"] == s["key"], s
+        x, used = R.gaussian_consumed(k, s["rows"] * s["cols"])
+        assert used == s["u64_consumed"]
+        assert R.digest_hex(R.digest_array(x)) == s["digest"], s
+        assert [float(v).hex() for v in x[:6]] == s["head"]
+
+
+def test_stream_grid_covers_slow_paths(golden_dir):
+    # the golden grid must exercise the ziggurat tail (log1p) path
+    assert sum(s["n_tail"] for s in _load(golden_dir, "streams.json")) > 100
+
+
+@pytest.mark.parametrize("name", ["micro", "small"])
+def test_forward_nll_vs_reference(golden_dir, name):
+    g = _load(golden_dir, f"forward_{name}.json")
+    cfg = R.ModelCfg(**g["model"])
+    params = R.init_params(cfg)
+    assert R.params_digest(params) == g["params_digest"]
+    tokens = np.asarray(g["tokens"], dtype=np.int64)
+    gold = tokens[:, cfg.prompt_len:]
+    shapes = {k: v.shape for k, v in params.items() if v.ndim == 2}
+    for key, ref in g["nll"].items():
+        prec, sign = key.split(":")
+        eff = dict(params)
+        for lid, (m, n) in shapes.items():
+            u = R.gaussian(g["zseed"], g["step"], lid, R.ROLE_U, m, g["rank"])
+            v = R.gaussian(g["zseed"], (g["step"] // 50) * 50, lid, R.ROLE_V, n, g["rank"])
+            a = g["a_scale"] * R.gaussian(g["a_seed"], g["step"], lid, R.ROLE_U, m, g["rank"])
+            eff[lid] = R.compose(params[lid], a, v, u, int(sign), g["epsilon"])
+        dt = np.float64 if prec == "real64" else np.float32
+        nll = R.forward_nll(eff, cfg, tokens, gold, dt).astype(np.float64)
+        tol = 1e-11 if prec == "real64" else 2e-4
+        np.testing.assert_allclose(nll, ref, rtol=0, atol=tol)
+
+
+@pytest.mark.parametrize("name", ["micro_lozo", "micro_fact", "small_lozo"])
+def test_trajectory_vs_reference(golden_dir, name):
+    h, recs, fin = _traj(golden_dir, f"traj_{name}.jsonl")
+    cfg = R.ModelCfg(**h["model"])
+    splits = R.generate_task(R.TaskCfg(**h["task"]))
+    z = R.ZoCfg(**h["zo"])
+    assert R.params_digest(R.init_params(cfg)) == h["model_digest"]
+    mine, params, _ = R.run_serving(cfg, splits, z, h["steps"])
+    for a, b in zip(recs, mine):
+        assert (a["u_digest"], a["v_digest"], a["minibatch_id"]) == (b.u_digest, b.v_digest, b.minibatch_id)
+        assert abs(a["loss_plus"] - b.loss_plus) <= 1e-12
+        assert abs(a["loss_minus"] - b.loss_minus) <= 1e-12
+    if all(a["loss_plus"] == b.loss_plus and a["loss_minus"] == b.loss_minus for a, b in zip(recs, mine)):
+        assert R.params_digest(params) == fin["final_params_digest"]
+
+
+def test_canonical_mean_pairwise_order():
+    v = np.array([1e16, 1.0, -1e16, 1.0, 3.0])
+    # ((1e16 + 1) + (-1e16 + (1 + 3))) / 5, evaluated pairwise
+    left = 1e16 + 1.0
+    right = -1e16 + (1.0 + 3.0)
+    assert R.canonical_mean(v) == (left + right) / 5
+    assert R.canonical_mean(np.concatenate([v, v])) == R.canonical_mean(v)
