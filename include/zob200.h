@@ -1,0 +1,142 @@
+/*
+ * zob200.h -- C ABI of libzob200.so, the B200-native LoZO/MeZO step engine.
+ *
+ * The reference (`zoserve`, /root/reference/pkg/src/zoserve) is a Python
+ * package with no FFI; its drop-in seams are Python callables.  Each entry
+ * below names the reference interface it replaces (file:line).  The Python
+ * package paper_2605_28760_b200 binds these with ctypes and re-exposes the
+ * reference's own API (lozo_step, factorized_step, estimate_coefficient,
+ * forward_score, run_serving_path, sample_gaussian, digests).
+ *
+ * Conventions
+ *   - every entry returns ZO_OK (0) or an error code; zo_last_error() gives the
+ *     message of the calling thread's last failure.  Codes map to the
+ *     reference exceptions: ZO_ERR_CONFIG -> ConfigError, ZO_ERR_DIMENSION ->
+ *     DimensionError, ZO_ERR_INPUT -> InputError (numerics.py:40-49),
+ *     ZO_ERR_ABORT -> ScoringAbort (runtime.py:147).
+ *   - device state is ctx-owned; host pointers are borrowed for the call.
+ *   - calls are stream-ordered on the ctx stream (zo_set_stream); entries that
+ *     return host values synchronize that stream.
+ *   - one ctx per device, not thread-safe (the reference's single-writer
+ *     contract, adapter.py:143-146); the digest entry points are thread-safe.
+ */
+#ifndef ZOB200_H
+#define ZOB200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ZO_OK 0
+#define ZO_ERR_CONFIG 1
+#define ZO_ERR_DIMENSION 2
+#define ZO_ERR_INPUT 3
+#define ZO_ERR_ABORT 4
+#define ZO_ERR_CUDA 5
+#define ZO_ERR_INTERNAL 6
+
+/* operand precision of the tensor-core scorer */
+#define ZO_PREC_FP16 0
+#define ZO_PREC_BF16 1
+
+#define ZO_EST_LOZO 0       /* "lozo_lazy"          zo_engine.py:368 */
+#define ZO_EST_FACTORIZED 1 /* "factorized_sqrt_r"  zo_engine.py:420 */
+
+typedef struct zo_ctx zo_ctx;
+
+/* ModelConfig (model.py:62-81) + ZoConfig shape fields (zo_engine.py:71-98). */
+typedef struct {
+  int32_t vocab, dim, n_layers, n_heads, prompt_len;
+  int32_t opt_len;   /* option token length (TaskConfig.options, model.py:328-331) */
+  int32_t max_batch; /* largest per-sign batch scored in one call */
+  int32_t rank;      /* ZoConfig.rank */
+  int32_t estimator; /* ZO_EST_* */
+  int32_t precision; /* ZO_PREC_* */
+  int32_t device;
+} zo_model_desc;
+
+const char* zo_last_error(void);
+int zo_version(void);
+
+/* lifecycle */
+int zo_create(zo_ctx** out, const zo_model_desc* desc);
+int zo_destroy(zo_ctx* ctx);
+int zo_set_stream(zo_ctx* ctx, void* cuda_stream);
+int zo_synchronize(zo_ctx* ctx);
+int zo_num_matrices(const zo_ctx* ctx);
+/* i-th trainable matrix in sorted layer-id order (model.py:120-121 matrix_ids) */
+int zo_matrix_info(const zo_ctx* ctx, int i, char* lid, int lid_cap, int64_t* rows, int64_t* cols);
+int zo_device_bytes(const zo_ctx* ctx, uint64_t* bytes);
+
+/* parameters.  init_params (model.py:84-108) regenerated on the device from the
+ * Role.INIT streams, bit-exact float64 master + 16-bit operand shadows. */
+int zo_init_params(zo_ctx* ctx, uint64_t init_seed, double init_scale);
+int zo_upload_matrix(zo_ctx* ctx, const char* layer_id, const double* host, int64_t rows, int64_t cols);
+int zo_download_matrix(zo_ctx* ctx, const char* layer_id, double* host, int64_t rows, int64_t cols);
+/* 1-D params: blk{i}.ln{1,2}.{scale,shift}, ln_f.{scale,shift} (model.py:100-107) */
+int zo_upload_vector(zo_ctx* ctx, const char* layer_id, const double* host, int64_t n);
+
+/* directions.  step_directions / lozo_direction / factorized_direction
+ * (zo_engine.py:163-261): U keyed by step, V by window start (lozo) or step
+ * (factorized), sampled on the device bit-exactly. */
+int zo_sample_u(zo_ctx* ctx, uint64_t seed, uint64_t step);
+int zo_sample_v(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu);
+/* sample_gaussian(StreamKey(seed, step, layer_id, role), rows, cols) (numerics.py:161-168)
+ * for an arbitrary stream; lid_hash = fnv1a64(utf8(layer_id)). */
+int zo_sample_stream(zo_ctx* ctx, uint64_t seed, uint64_t step, uint64_t lid_hash, int32_t role, int64_t n,
+                     double* host_out);
+/* slot arenas in sorted-id order: which = 0 U (m x r), 1 V (n x r), 2 window A (m x r) */
+int zo_slot_count(const zo_ctx* ctx, int32_t which, int64_t* count);
+int zo_get_slot(zo_ctx* ctx, int32_t which, double* host, int64_t count);
+int zo_set_slot(zo_ctx* ctx, int32_t which, const double* host, int64_t count);
+/* sampler diagnostics: [short streams, exp near-ties, splice repairs] since create */
+int zo_sampler_flags(zo_ctx* ctx, uint32_t flags[3]);
+
+/* scoring.  nsign = 2: both probes (+eps, -eps) in one launch sequence, the
+ * paired scorer calls of estimate_coefficient (zo_engine.py:318-326); nsign = 1:
+ * a single composition (sign 0 / eval).  tokens: [B, T] prompt || option tokens,
+ * gold: [nsign, B, opt_len] option tokens scored per half (model.py:239-240,
+ * 261-267: with nsign = 2 and sign_mode 1 the two halves score two options of
+ * one composition).  nll_out: [nsign, B]
+ * per-example option NLL, float64 (model.py:202-215). */
+int zo_prepare_probe(zo_ctx* ctx, double epsilon, int32_t sign_mode);
+int zo_score(zo_ctx* ctx, const int32_t* tokens, const int32_t* gold, int32_t B, int32_t nsign, double* nll_out);
+/* canonical_mean per sign, c = (L+ - L-)/(2 eps), c_used, beta = -(lr*c_used)
+ * (numerics.py:271-284, zo_engine.py:331,411,417): out4 = [L+, L-, c, beta].
+ * Returns ZO_ERR_ABORT (no update armed) when a loss is not finite. */
+int zo_coefficient(zo_ctx* ctx, int32_t B, double epsilon, double lr, int32_t divide_by_r, double* out4);
+/* install a host-computed [L+, L-, c, beta] (custom scorer path, zo_engine.py:298-332) */
+int zo_set_coefficient(zo_ctx* ctx, const double* out4);
+/* accumulate_on_U for every matrix: A += beta*U (adapter.py:252-257) */
+int zo_update_u(zo_ctx* ctx);
+/* fold_window for every matrix (runtime.py:242-250, adapter.py:260-271): W += A V^T; A = 0 */
+int zo_fold(zo_ctx* ctx);
+/* factorized_step's dense update (zo_engine.py:449-450): W += (-(lr*c)/sqrt(r)) U V^T */
+int zo_update_dense(zo_ctx* ctx, double lr);
+
+/* one whole lozo_step / factorized_step on the device (zo_engine.py:368-453),
+ * replayed as a CUDA graph: V at window starts, U, probes, paired scoring,
+ * coefficient, update.  out4 as zo_coefficient. */
+int zo_step(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon, double lr, int32_t divide_by_r,
+            const int32_t* tokens, const int32_t* gold, int32_t B, double* out4);
+/* per-phase device time of the last zo_step (ms): [sample, score, update] */
+int zo_last_step_ms(zo_ctx* ctx, float ms[3]);
+
+/* FNV-1a-64 (numerics.py:60-124), chained from h.  Thread-safe, host only. */
+uint64_t zo_fnv1a64(const void* data, uint64_t nbytes, uint64_t h);
+/* u/v digest chain over sorted layer ids (zo_engine.py:220-261) of a host copy of
+ * an arena: for i: h = fnv(lid_i); h = fnv(arena[off_i : off_i + cnt_i]) */
+uint64_t zo_digest_chain(const char* const* lids, const double* arena, const int64_t* offsets,
+                         const int64_t* counts, int32_t n, uint64_t h);
+
+/* test hook: D = A[M,K] . B[N,K]^T through the production tcgen05 GEMM with
+ * epilogue epi (0 store16, 1 gelu16, 2 resid32: C += D, 3 store32); host
+ * buffers, 16-bit inputs with row stride lda, fp32 output [M, N]. */
+int zo_test_gemm(int32_t M, int32_t N, int32_t K, int32_t lda, int32_t epi, int32_t bf16, const uint16_t* A_host,
+                 const uint16_t* B_host, float* C_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,103 @@
+"""ctypes binding of libzob200.so (include/zob200.h).
+
+The shared library is the product: there is no CPU or Triton fallback.  If it
+is missing (not built) or cannot initialise a B200, calls raise loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ConfigError, DimensionError, InputError, ScoringAbort
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_build", "libzob200.so")
+
+ZO_OK, ZO_ERR_CONFIG, ZO_ERR_DIMENSION, ZO_ERR_INPUT, ZO_ERR_ABORT, ZO_ERR_CUDA, ZO_ERR_INTERNAL = range(7)
+PREC_FP16, PREC_BF16 = 0, 1
+EST_LOZO, EST_FACTORIZED = 0, 1
+
+_lib = None
+_lock = threading.Lock()
+
+
+class ZoModelDesc(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "vocab", "dim", "n_layers", "n_heads", "prompt_len", "opt_len", "max_batch", "rank",
+        "estimator", "precision", "device")]
+
+
+# (name, restype, argtypes) for every symbol include/zob200.h declares
+_c = ctypes
+_P = _c.c_void_p
+SIGNATURES = [
+    ("zo_last_error", _c.c_char_p, []),
+    ("zo_version", _c.c_int, []),
+    ("zo_create", _c.c_int, [_c.POINTER(_P), _c.POINTER(ZoModelDesc)]),
+    ("zo_destroy", _c.c_int, [_P]),
+    ("zo_set_stream", _c.c_int, [_P, _P]),
+    ("zo_synchronize", _c.c_int, [_P]),
+    ("zo_num_matrices", _c.c_int, [_P]),
+    ("zo_matrix_info", _c.c_int, [_P, _c.c_int, _c.c_char_p, _c.c_int, _c.POINTER(_c.c_int64),
+                                  _c.POINTER(_c.c_int64)]),
+    ("zo_device_bytes", _c.c_int, [_P, _c.POINTER(_c.c_uint64)]),
+    ("zo_init_params", _c.c_int, [_P, _c.c_uint64, _c.c_double]),
+    ("zo_upload_matrix", _c.c_int, [_P, _c.c_char_p, _P, _c.c_int64, _c.c_int64]),
+    ("zo_download_matrix", _c.c_int, [_P, _c.c_char_p, _P, _c.c_int64, _c.c_int64]),
+    ("zo_upload_vector", _c.c_int, [_P, _c.c_char_p, _P, _c.c_int64]),
+    ("zo_sample_u", _c.c_int, [_P, _c.c_uint64, _c.c_uint64]),
+    ("zo_sample_v", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32]),
+    ("zo_sample_stream", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_int64, _P]),
+    ("zo_slot_count", _c.c_int, [_P, _c.c_int32, _c.POINTER(_c.c_int64)]),
+    ("zo_get_slot", _c.c_int, [_P, _c.c_int32, _P, _c.c_int64]),
+    ("zo_set_slot", _c.c_int, [_P, _c.c_int32, _P, _c.c_int64]),
+    ("zo_sampler_flags", _c.c_int, [_P, _c.POINTER(_c.c_uint32)]),
+    ("zo_prepare_probe", _c.c_int, [_P, _c.c_double, _c.c_int32]),
+    ("zo_score", _c.c_int, [_P, _P, _P, _c.c_int32, _c.c_int32, _P]),
+    ("zo_coefficient", _c.c_int, [_P, _c.c_int32, _c.c_double, _c.c_double, _c.c_int32, _P]),
+    ("zo_set_coefficient", _c.c_int, [_P, _P]),
+    ("zo_update_u", _c.c_int, [_P]),
+    ("zo_fold", _c.c_int, [_P]),
+    ("zo_update_dense", _c.c_int, [_P, _c.c_double]),
+    ("zo_step", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double, _c.c_int32,
+                           _P, _P, _c.c_int32, _P]),
+    ("zo_last_step_ms", _c.c_int, [_P, _c.POINTER(_c.c_float)]),
+    ("zo_fnv1a64", _c.c_uint64, [_P, _c.c_uint64, _c.c_uint64]),
+    ("zo_test_gemm", _c.c_int, [_c.c_int32] * 6 + [_P, _P, _P]),
+    ("zo_digest_chain", _c.c_uint64, [_c.POINTER(_c.c_char_p), _P, _c.POINTER(_c.c_int64),
+                                      _c.POINTER(_c.c_int64), _c.c_int32, _c.c_uint64]),
+]
+
+
+def lib():
+    """Load libzob200.so (fails loudly when the CUDA extension is missing)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        f"libzob200.so not built ({LIB_PATH}); run `python -m paper_2605_28760_b200.build`. "
+                        "There is no CPU fallback.")
+                L = ctypes.CDLL(LIB_PATH)
+                for name, res, args in SIGNATURES:
+                    f = getattr(L, name)
+                    f.restype = res
+                    f.argtypes = args
+                _lib = L
+    return _lib
+
+
+_EXC = {
+    ZO_ERR_CONFIG: ConfigError,
+    ZO_ERR_DIMENSION: DimensionError,
+    ZO_ERR_INPUT: InputError,
+    ZO_ERR_ABORT: ScoringAbort,
+}
+
+
+def check(code: int) -> None:
+    if code != ZO_OK:
+        msg = lib().zo_last_error().decode("utf-8", "replace")
+        raise _EXC.get(code, RuntimeError)(msg)

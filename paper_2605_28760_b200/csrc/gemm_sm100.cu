@@ -1,0 +1,411 @@
+// K2 -- persistent tcgen05 GEMM for sm_100a.
+//
+// Roles (192 threads, 1 CTA/SM):
+//   warp 0      TMA producer: A/B tiles (SWIZZLE_128B, K-major) into a STAGES-deep
+//               shared-memory ring, completion via mbarrier transaction bytes.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (kind::f16, M=128, N=BN, K=16 per instruction, fp32 accumulate
+//               in TMEM); tcgen05.commit frees smem stages / publishes tiles.
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> HBM.
+// Two TMEM accumulators (2*BN columns) let the epilogue of tile i overlap the
+// MMAs of tile i+1.  Tiles are scheduled M-fastest so the CTAs resident at
+// once share weight (B) tiles through L2: every weight byte crosses HBM once
+// per launch for both perturbation signs.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "zo_common.cuh"
+#include "zo_gemm.h"
+
+namespace zo {
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  // bounded spin: a protocol bug traps (kernel error) instead of hanging the GPU
+  for (uint32_t i = 0;; ++i) {
+    uint32_t done;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (i > (1u << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+// K-major, 128-byte swizzle, 8-row core groups 1024 B apart (sm_100 descriptor, version 1).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)1 << 16;            // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // version
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]),
+        "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+        "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  // model.py:145-146: 0.5*x*(1 + tanh(sqrt(2/pi)*(x + 0.044715*x^3)))
+  const float c = 0.7978845608028654f;
+  return 0.5f * x * (1.0f + tanhf(c * (x + 0.044715f * x * x * x)));
+}
+
+template <bool BF16>
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  if constexpr (BF16) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int BM = 128, BK = 64;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
+  static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+};
+
+struct GemmParams {
+  int M, N, num_kb, last_ksteps, m_tiles, n_tiles, ldo;
+  void* out;
+};
+
+template <int BN, int EPI, bool BF16>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+  using C = GemmCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
+  const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = smem_u32(bars + 2 * C::STAGES + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8 * a, 1);
+      mbar_init(tempty0 + 8 * a, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "n"(C::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = p.m_tiles * p.n_tiles;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const int m0 = (t % p.m_tiles) * C::BM, n0 = (t / p.m_tiles) * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(empty0 + 8 * stage, phase ^ 1);
+          const uint32_t fb = full0 + 8 * stage;
+          mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+          tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * C::BK, m0);
+          tma_load_2d(smem_u32(sB + stage * C::B_BYTES), &tmB, fb, kb * C::BK, n0);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) |
+                                 ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(C::BM >> 4) << 24);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < p.num_kb; ++kb) {
+          mbar_wait(full0 + 8 * stage, phase);
+          tc_fence_after();
+          const uint64_t ad = sw128_desc(smem_u32(sA + stage * C::A_BYTES));
+          const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::B_BYTES));
+          const int ks = (kb == p.num_kb - 1) ? p.last_ksteps : 4;
+          for (int k = 0; k < ks; ++k)
+            tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+          tc_commit(empty0 + 8 * stage);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(tfull0 + 8 * acc);
+      }
+    }
+  } else {
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int m0 = (t % p.m_tiles) * C::BM, n0 = (t / p.m_tiles) * BN;
+      mbar_wait(tfull0 + 8 * acc, acc_phase);
+      tc_fence_after();
+      const int row = m0 + q * 32 + lane;
+      const bool row_ok = row < p.M;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+        const int col0 = n0 + c;
+        if (!row_ok || col0 >= p.N) continue;
+        const bool full = col0 + 32 <= p.N;
+        if constexpr (EPI == EPI_STORE16 || EPI == EPI_GELU16) {
+          if constexpr (EPI == EPI_GELU16) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+          }
+          uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + (size_t)row * p.ldo + col0;
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              uint4 w;
+              w.x = pack2<BF16>(v[8 * j + 0], v[8 * j + 1]);
+              w.y = pack2<BF16>(v[8 * j + 2], v[8 * j + 3]);
+              w.z = pack2<BF16>(v[8 * j + 4], v[8 * j + 5]);
+              w.w = pack2<BF16>(v[8 * j + 6], v[8 * j + 7]);
+              reinterpret_cast<uint4*>(o)[j] = w;
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) {
+              uint32_t pk = pack2<BF16>(v[i], 0.f);
+              o[i] = (uint16_t)(pk & 0xffff);
+            }
+          }
+        } else {
+          float* o = reinterpret_cast<float*>(p.out) + (size_t)row * p.ldo + col0;
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              if constexpr (EPI == EPI_RESID32) {
+                float4 x = reinterpret_cast<float4*>(o)[j];
+                w.x += x.x;
+                w.y += x.y;
+                w.z += x.z;
+                w.w += x.w;
+              }
+              reinterpret_cast<float4*>(o)[j] = w;
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) {
+              if constexpr (EPI == EPI_RESID32)
+                o[i] += v[i];
+              else
+                o[i] = v[i];
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    ZO_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+    if (!ptr || q != cudaDriverEntryPointSuccess) throw Error(ZO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+  }
+  return fn;
+}
+
+void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                  uint32_t box_rows, bool bf16) {
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw Error(ZO_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") rows=" +
+                                 std::to_string(rows) + " cols=" + std::to_string(cols) + " ld=" +
+                                 std::to_string(ld));
+}
+
+void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used, int epi,
+               bool bf16, void* out, int ldo, int num_sms) {
+  if (lda % 8 || ldb % 8) throw Error(ZO_ERR_DIMENSION, "GEMM leading dimensions must be multiples of 8");
+  g.M = M;
+  g.N = N;
+  g.epi = epi;
+  g.bf16 = bf16 ? 1 : 0;
+  g.out = out;
+  g.ldo = ldo;
+  g.num_kb = (Kp_used + 63) / 64;
+  const int rem = Kp_used - 64 * (g.num_kb - 1);
+  g.last_ksteps = (rem + 15) / 16;
+  const int m_tiles = (M + 127) / 128;
+  // tile N: prefer 256 unless that leaves the GPU badly under-filled
+  int bn = 256;
+  if (N <= 64)
+    bn = 64;
+  else if (N <= 128 || (int64_t)m_tiles * ((N + 255) / 256) < num_sms / 2)
+    bn = (N <= 64) ? 64 : 128;
+  g.bn = bn;
+  const int tiles = m_tiles * ((N + bn - 1) / bn);
+  g.grid = tiles < num_sms ? tiles : num_sms;
+  const int mrows = ((M + 127) / 128) * 128;
+  make_tmap_2d(&g.tmA, A, (uint64_t)mrows, (uint64_t)lda, (uint64_t)lda, 128, bf16);
+  make_tmap_2d(&g.tmB, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)bn, bf16);
+}
+
+template <int BN, int EPI, bool BF16>
+static void launch_t(const GemmDesc& g, cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    ZO_CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr_set = true;
+  }
+  GemmParams p;
+  p.M = g.M;
+  p.N = g.N;
+  p.num_kb = g.num_kb;
+  p.last_ksteps = g.last_ksteps;
+  p.m_tiles = (g.M + 127) / 128;
+  p.n_tiles = (g.N + BN - 1) / BN;
+  p.ldo = g.ldo;
+  p.out = g.out;
+  k_gemm<BN, EPI, BF16><<<g.grid, 192, C::SMEM, st>>>(g.tmA, g.tmB, p);
+}
+
+template <int BN, bool BF16>
+static void launch_e(const GemmDesc& g, cudaStream_t st) {
+  switch (g.epi) {
+    case EPI_STORE16: launch_t<BN, EPI_STORE16, BF16>(g, st); break;
+    case EPI_GELU16: launch_t<BN, EPI_GELU16, BF16>(g, st); break;
+    case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16>(g, st); break;
+    default: launch_t<BN, EPI_STORE32, BF16>(g, st); break;
+  }
+}
+
+void gemm_launch(const GemmDesc& g, cudaStream_t st) {
+  if (g.bf16) {
+    if (g.bn == 256) launch_e<256, true>(g, st);
+    else if (g.bn == 128) launch_e<128, true>(g, st);
+    else launch_e<64, true>(g, st);
+  } else {
+    if (g.bn == 256) launch_e<256, false>(g, st);
+    else if (g.bn == 128) launch_e<128, false>(g, st);
+    else launch_e<64, false>(g, st);
+  }
+}
+
+}  // namespace zo

@@ -1,0 +1,382 @@
+// K1 -- bit-exact direction sampler.
+//
+// Reproduces StreamKey(seed, step, layer_id, role).generator().standard_normal
+// (numerics.py:139-168) on the GPU:
+//   key   = SeedSequence([seed, step, fnv1a64(layer_id), role]).generate_state(2, u64)
+//   u64 p = Philox4x64-10(key, counter = p/4 + 1)[p % 4]
+//   x     = numpy's 256-layer ziggurat over those u64s, row-major fill.
+//
+// The ziggurat consumes a data-dependent number of u64s per sample, so sample i
+// cannot be addressed directly.  We parse in parallel with a speculative
+// chunk splice:
+//   k_spec : every chunk of CH u64 positions is parsed as if an attempt started
+//            at its first position -> speculative exit (first attempt start at
+//            or past the chunk end).
+//   k_true : chunk c re-parses from the speculative exit of chunk c-1 (its
+//            candidate true entry) -> sample count and exit.  Attempt chains
+//            started at different positions merge within a few attempts
+//            (SURVEY.md App. A.7), so this exit equals the speculative one
+//            except with vanishing probability.
+//   k_scan : one CTA per stream verifies the splice (exit[c-1] == spec[c-1]),
+//            repairs any broken link serially, and scans counts -> offsets.
+//   k_emit : re-parse from the verified entry and write samples in place.
+// Every step is exact; the repair path keeps it exact even when a merge fails.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "zo_common.cuh"
+#include "zo_glibc_math.cuh"
+#include "zo_sampler.h"
+
+#define ZO_ZIG_QUAL __device__ const
+#include "ziggurat_tables.h"
+#undef ZO_ZIG_QUAL
+
+namespace zo {
+
+static constexpr uint64_t CH = 128;  // u64 positions per chunk
+
+// ---------------------------------------------------------------- SeedSequence
+__host__ __device__ inline uint32_t ss_hashmix(uint32_t v, uint32_t& hc) {
+  v ^= hc;
+  hc *= 0x931e8875u;
+  v *= hc;
+  v ^= v >> 16;
+  return v;
+}
+__host__ __device__ inline uint32_t ss_mix(uint32_t x, uint32_t y) {
+  uint32_t r = 0xca01f9ddu * x - 0x4973f715u * y;
+  return r ^ (r >> 16);
+}
+__host__ __device__ inline int ss_words(uint64_t v, uint32_t* out) {
+  int n = 0;
+  if (v == 0) {
+    out[n++] = 0;
+    return n;
+  }
+  while (v) {
+    out[n++] = (uint32_t)(v & 0xffffffffu);
+    v >>= 32;
+  }
+  return n;
+}
+// numpy bit_generator.pyx SeedSequence(entropy).generate_state(2, uint64)
+__host__ __device__ inline void seed_sequence_key(uint64_t seed, uint64_t step, uint64_t lid_hash,
+                                                  uint64_t role, uint64_t key[2]) {
+  uint32_t ent[8];
+  int n = 0;
+  n += ss_words(seed, ent + n);
+  n += ss_words(step, ent + n);
+  n += ss_words(lid_hash, ent + n);
+  n += ss_words(role, ent + n);
+  uint32_t pool[4];
+  uint32_t hc = 0x43b0d7e5u;
+  for (int i = 0; i < 4; ++i) pool[i] = ss_hashmix(i < n ? ent[i] : 0u, hc);
+  for (int s = 0; s < 4; ++s)
+    for (int d = 0; d < 4; ++d)
+      if (s != d) pool[d] = ss_mix(pool[d], ss_hashmix(pool[s], hc));
+  for (int s = 4; s < n; ++s)
+    for (int d = 0; d < 4; ++d) pool[d] = ss_mix(pool[d], ss_hashmix(ent[s], hc));
+  uint32_t w[4];
+  uint32_t hb = 0x8b51f9ddu;
+  for (int i = 0; i < 4; ++i) {
+    uint32_t v = pool[i] ^ hb;
+    hb *= 0x58f38dedu;
+    v *= hb;
+    v ^= v >> 16;
+    w[i] = v;
+  }
+  key[0] = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+  key[1] = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
+}
+
+void host_stream_key(uint64_t seed, uint64_t step, uint64_t lid_hash, uint64_t role, uint64_t key[2]) {
+  seed_sequence_key(seed, step, lid_hash, role, key);
+}
+
+// ---------------------------------------------------------------- Philox4x64-10
+__device__ __forceinline__ void philox_block(uint64_t k0, uint64_t k1, uint64_t blk, uint64_t out[4]) {
+  uint64_t c0 = blk + 1, c1 = (c0 == 0) ? 1 : 0, c2 = 0, c3 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    uint64_t lo0 = 0xD2E7470EE14C6C93ULL * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ULL, c0);
+    uint64_t lo1 = 0xCA5A826395121157ULL * c2, hi1 = __umul64hi(0xCA5A826395121157ULL, c2);
+    uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B97F4A7C15ULL;
+    k1 += 0xBB67AE8584CAA73BULL;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+struct Zig {
+  const uint64_t* ki;
+  const double* wi;
+  const double* fi;
+};
+
+struct Parser {
+  uint64_t k0, k1, pos, blk;
+  uint64_t buf[4];
+  __device__ void init(uint64_t a, uint64_t b, uint64_t p) {
+    k0 = a;
+    k1 = b;
+    pos = p;
+    blk = ~0ULL;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    uint64_t b = pos >> 2;
+    if (b != blk) {
+      philox_block(k0, k1, b, buf);
+      blk = b;
+    }
+    uint64_t v = buf[pos & 3];
+    ++pos;
+    return v;
+  }
+  __device__ __forceinline__ double next_double() {
+    return __dmul_rn((double)(next() >> 11), 1.0 / 9007199254740992.0);
+  }
+  // One attempt of numpy's random_standard_normal outer loop.  Returns true and
+  // sets *x when the attempt produced a sample.  *amb counts exp() decisions
+  // too close to call between CUDA's exp and glibc's (|lhs-e| <= 2 ulp).
+  __device__ __forceinline__ bool attempt(const Zig& z, double* x, unsigned* amb) {
+    uint64_t r = next();
+    int idx = (int)(r & 0xff);
+    r >>= 8;
+    int sign = (int)(r & 1);
+    uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double v = __dmul_rn((double)rabs, z.wi[idx]);
+    if (sign) v = -v;
+    if (rabs < z.ki[idx]) {
+      *x = v;
+      return true;
+    }
+    if (idx == 0) {
+      const double R = 3.6541528853610088, INV_R = 0.27366123732975828;
+      for (;;) {
+        double xx = __dmul_rn(-INV_R, glibc_log1p(-next_double()));
+        double yy = -glibc_log1p(-next_double());
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+          *x = ((rabs >> 8) & 1) ? -__dadd_rn(R, xx) : __dadd_rn(R, xx);
+          return true;
+        }
+      }
+    }
+    double u = next_double();
+    double lhs = __dadd_rn(__dmul_rn(__dsub_rn(z.fi[idx - 1], z.fi[idx]), u), z.fi[idx]);
+    double e = exp(__dmul_rn(__dmul_rn(-0.5, v), v));
+    if (fabs(__dsub_rn(lhs, e)) <= __dmul_rn(e, 4.5e-16)) ++*amb;
+    if (lhs < e) {
+      *x = v;
+      return true;
+    }
+    return false;
+  }
+};
+
+__device__ __forceinline__ void load_tables(Zig& z, uint64_t* ki, double* wi, double* fi) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    ki[i] = zo_zig_ki[i];
+    wi[i] = zo_zig_wi[i];
+    fi[i] = zo_zig_fi[i];
+  }
+  __syncthreads();
+  z.ki = ki;
+  z.wi = wi;
+  z.fi = fi;
+}
+
+__device__ __forceinline__ uint64_t key_step(const StreamDesc& s, const uint64_t* d_step, uint32_t nu) {
+  if (s.step_mode == STEP_FIXED) return s.fixed_step;
+  uint64_t t = *d_step;
+  if (s.step_mode == STEP_WINDOW) return (t / nu) * nu;
+  return t;
+}
+
+__global__ void k_keys(const StreamDesc* __restrict__ streams, int S, uint64_t seed,
+                       const uint64_t* __restrict__ d_step, uint32_t nu, uint64_t* __restrict__ keys) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  StreamDesc d = streams[s];
+  uint64_t k[2];
+  seed_sequence_key(d.seed_override ? d.seed_value : seed, key_step(d, d_step, nu), d.lid_hash, d.role, k);
+  keys[2 * s] = k[0];
+  keys[2 * s + 1] = k[1];
+}
+
+__global__ void __launch_bounds__(256) k_spec(const StreamDesc* __restrict__ streams,
+                                              const uint32_t* __restrict__ chunk_stream, int64_t C,
+                                              const uint64_t* __restrict__ keys,
+                                              uint64_t* __restrict__ spec_exit, unsigned* flags) {
+  __shared__ uint64_t ki[256];
+  __shared__ double wi[256], fi[256];
+  Zig z;
+  load_tables(z, ki, wi, fi);
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  uint32_t s = chunk_stream[c];
+  uint64_t local = (uint64_t)(c - (int64_t)streams[s].chunk_begin);
+  uint64_t beg = local * CH, end = beg + CH;
+  Parser p;
+  p.init(keys[2 * s], keys[2 * s + 1], beg);
+  unsigned amb = 0;
+  double x;
+  while (p.pos < end) p.attempt(z, &x, &amb);
+  spec_exit[c] = p.pos;
+}
+
+__global__ void __launch_bounds__(256) k_true(const StreamDesc* __restrict__ streams,
+                                              const uint32_t* __restrict__ chunk_stream, int64_t C,
+                                              const uint64_t* __restrict__ keys,
+                                              const uint64_t* __restrict__ spec_exit,
+                                              uint64_t* __restrict__ exit_pos, uint32_t* __restrict__ count,
+                                              unsigned* flags) {
+  __shared__ uint64_t ki[256];
+  __shared__ double wi[256], fi[256];
+  Zig z;
+  load_tables(z, ki, wi, fi);
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  uint32_t s = chunk_stream[c];
+  uint64_t local = (uint64_t)(c - (int64_t)streams[s].chunk_begin);
+  uint64_t end = (local + 1) * CH;
+  uint64_t entry = local == 0 ? 0 : spec_exit[c - 1];
+  Parser p;
+  p.init(keys[2 * s], keys[2 * s + 1], entry);
+  unsigned amb = 0, n = 0;
+  double x;
+  while (p.pos < end) n += p.attempt(z, &x, &amb) ? 1u : 0u;
+  exit_pos[c] = p.pos;
+  count[c] = n;
+}
+
+// One CTA per stream: verify/repair the splice, exclusive-scan the counts.
+__global__ void __launch_bounds__(1024) k_scan(const StreamDesc* __restrict__ streams,
+                                               const uint64_t* __restrict__ keys,
+                                               const uint64_t* __restrict__ spec_exit,
+                                               uint64_t* __restrict__ exit_pos, uint32_t* __restrict__ count,
+                                               uint64_t* __restrict__ offset, unsigned* flags) {
+  __shared__ uint64_t ki[256];
+  __shared__ double wi[256], fi[256];
+  __shared__ int64_t first_bad;
+  __shared__ uint64_t warp_sums[32];
+  __shared__ uint64_t carry;
+  Zig z;
+  load_tables(z, ki, wi, fi);
+  const StreamDesc d = streams[blockIdx.x];
+  const int64_t cb = (int64_t)d.chunk_begin, nc = (int64_t)d.n_chunks;
+  if (threadIdx.x == 0) first_bad = nc;
+  __syncthreads();
+  // chunk c (local >= 1) used entry spec_exit[c-1]; valid iff exit_pos[c-1] matches.
+  for (int64_t i = 1 + threadIdx.x; i < nc; i += blockDim.x)
+    if (exit_pos[cb + i - 1] != spec_exit[cb + i - 1]) atomicMin((unsigned long long*)&first_bad, (unsigned long long)i);
+  __syncthreads();
+  if (first_bad < nc && threadIdx.x == 0) {
+    // serial repair (vanishingly rare): re-parse every chunk after the break
+    atomicAdd(&flags[2], 1u);
+    unsigned amb = 0;
+    double x;
+    for (int64_t i = first_bad; i < nc; ++i) {
+      Parser p;
+      p.init(keys[2 * blockIdx.x], keys[2 * blockIdx.x + 1], exit_pos[cb + i - 1]);
+      uint64_t end = (uint64_t)(i + 1) * CH;
+      unsigned n = 0;
+      while (p.pos < end) n += p.attempt(z, &x, &amb) ? 1u : 0u;
+      exit_pos[cb + i] = p.pos;
+      count[cb + i] = n;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t base = 0; base < nc; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    uint64_t v = i < nc ? count[cb + i] : 0;
+    uint64_t incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint64_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_sums[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+      uint64_t wi2 = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint64_t t = __shfl_up_sync(0xffffffffu, wi2, o);
+        if (lane >= o) wi2 += t;
+      }
+      warp_sums[lane] = wi2 - w;  // exclusive warp prefix
+    }
+    __syncthreads();
+    uint64_t excl = carry + warp_sums[warp] + incl - v;
+    if (i < nc) offset[cb + i] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && carry < d.n) atomicAdd(&flags[0], 1u);
+}
+
+__global__ void __launch_bounds__(256) k_emit(const StreamDesc* __restrict__ streams,
+                                              const uint32_t* __restrict__ chunk_stream, int64_t C,
+                                              const uint64_t* __restrict__ keys,
+                                              const uint64_t* __restrict__ exit_pos,
+                                              const uint64_t* __restrict__ offset, double* __restrict__ out,
+                                              unsigned* flags) {
+  __shared__ uint64_t ki[256];
+  __shared__ double wi[256], fi[256];
+  Zig z;
+  load_tables(z, ki, wi, fi);
+  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  uint32_t s = chunk_stream[c];
+  const StreamDesc& d = streams[s];
+  uint64_t local = (uint64_t)(c - (int64_t)d.chunk_begin);
+  uint64_t end = (local + 1) * CH;
+  uint64_t entry = local == 0 ? 0 : exit_pos[c - 1];
+  uint64_t o = offset[c];
+  if (o >= d.n) return;
+  Parser p;
+  p.init(keys[2 * s], keys[2 * s + 1], entry);
+  unsigned amb = 0;
+  double x;
+  double* dst = out + d.out_off;
+  const double scale = d.scale;
+  const bool scaled = d.apply_scale != 0;
+  while (p.pos < end && o < d.n) {
+    if (p.attempt(z, &x, &amb)) dst[o++] = scaled ? __dmul_rn(scale, x) : x;
+  }
+  if (amb) atomicAdd(&flags[1], amb);
+}
+
+uint64_t sampler_chunks_for(uint64_t n) {
+  // expected u64/sample ~1.025; + generous margin so the scan never runs short
+  uint64_t pos = n + n / 8 + 4 * CH;
+  return (pos + CH - 1) / CH;
+}
+
+void sampler_launch(const SamplerPlan& P, uint64_t seed, const uint64_t* d_step, uint32_t nu, double* out,
+                    cudaStream_t st) {
+  if (P.S == 0) return;
+  k_keys<<<(P.S + 127) / 128, 128, 0, st>>>(P.d_streams, P.S, seed, d_step, nu, P.d_keys);
+  unsigned grid = (unsigned)((P.C + 255) / 256);
+  k_spec<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_spec, P.d_flags);
+  k_true<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_spec, P.d_exit, P.d_count,
+                               P.d_flags);
+  k_scan<<<P.S, 1024, 0, st>>>(P.d_streams, P.d_keys, P.d_spec, P.d_exit, P.d_count, P.d_offset, P.d_flags);
+  k_emit<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_exit, P.d_offset, out,
+                               P.d_flags);
+}
+
+}  // namespace zo

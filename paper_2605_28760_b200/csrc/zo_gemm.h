@@ -1,0 +1,39 @@
+// K2 -- tcgen05/TMEM/TMA GEMM for the scorer's projections and LM head.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace zo {
+
+enum EpiKind : int {
+  EPI_STORE16 = 0,  // out16[r, c] = acc                       (qkv)
+  EPI_GELU16 = 1,   // out16[r, c] = gelu_tanh(acc)            (ff_up, model.py:145-146,197)
+  EPI_RESID32 = 2,  // x32[r, c] += acc                        (attn_out / ff_down residual)
+  EPI_STORE32 = 3,  // out32[r, c] = acc                       (LM-head logits rows)
+};
+
+// D[M, N] = A[M, Kp] * B[N, Kp]^T, both operands K-major 16-bit, fp32 accumulate.
+struct GemmDesc {
+  CUtensorMap tmA;
+  CUtensorMap tmB;
+  int M = 0, N = 0;
+  int num_kb = 0;       // 64-wide K blocks
+  int last_ksteps = 4;  // 16-wide UMMA steps issued in the last K block (trims the LoRA extension)
+  int bn = 256;         // tile N (64/128/256)
+  int epi = EPI_STORE16;
+  int bf16 = 0;         // operand type: 0 fp16, 1 bf16
+  void* out = nullptr;
+  int ldo = 0;          // output leading dimension (elements)
+  int grid = 0;         // persistent CTAs
+};
+
+// 2-D K-major tensor map over a row-major [rows, cols] 16-bit matrix (row stride ld elements).
+void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                  uint32_t box_rows, bool bf16);
+// Fill a GemmDesc. A is [Mpad, lda] (lda >= Kp), B is [N, ldb].
+void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used,
+               int epi, bool bf16, void* out, int ldo, int num_sms);
+void gemm_launch(const GemmDesc& g, cudaStream_t st);
+
+}  // namespace zo

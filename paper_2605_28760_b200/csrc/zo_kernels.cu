@@ -1,0 +1,567 @@
+// Scorer glue, loss extraction, coefficient, update and fold kernels.
+// Reference citations are to /root/reference/pkg/src/zoserve.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "zo_common.cuh"
+#include "zo_kernels.h"
+
+namespace zo {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ float ld16(const void* p, size_t i, bool bf16) {
+  const uint16_t raw = reinterpret_cast<const uint16_t*>(p)[i];
+  if (bf16) return __bfloat162float(__ushort_as_bfloat16(raw));
+  return __half2float(__ushort_as_half(raw));
+}
+__device__ __forceinline__ uint16_t to16(float v, bool bf16) {
+  if (bf16) return __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  return __half_as_ushort(__float2half_rn(v));
+}
+__device__ __forceinline__ float from16(uint16_t raw, bool bf16) {
+  if (bf16) return __bfloat162float(__ushort_as_bfloat16(raw));
+  return __half2float(__ushort_as_half(raw));
+}
+__device__ __forceinline__ void st16(void* p, size_t i, float v, bool bf16) {
+  reinterpret_cast<uint16_t*>(p)[i] = to16(v, bf16);
+}
+
+template <int N>
+__device__ __forceinline__ void block_sum(float (&v)[N], float* red /* >= 32*N */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < N; ++k) red[warp * N + k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    float s = 0.f;
+    for (int w = 0; w < nw; ++w) s += red[w * N + k];
+    v[k] = s;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float block_max(float v, float* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float m = -CUDART_INF_F;
+  for (int w = 0; w < nw; ++w) m = fmaxf(m, red[w]);
+  __syncthreads();
+  return m;
+}
+
+// Write the LoRA extension columns for one row: t_k -> (hi, lo, hi) or t.
+__device__ __forceinline__ void write_ext(void* out, size_t base, int k, float t, int ext_terms, bool bf16) {
+  if (ext_terms == 3) {
+    const uint16_t hi = to16(t, bf16);
+    const float lo = t - from16(hi, bf16);
+    uint16_t* o = reinterpret_cast<uint16_t*>(out) + base + 3 * k;
+    o[0] = hi;
+    o[1] = to16(lo, bf16);
+    o[2] = hi;
+  } else {
+    reinterpret_cast<uint16_t*>(out)[base + k] = to16(t, bf16);
+  }
+}
+
+// Row-wise t_k = sum_i a_i P[i, k] over a row cached in shared memory, k in chunks of 8.
+__device__ void row_ext(const float* row, int K, const float* P, int r, void* out, size_t ext_base, int ext_terms,
+                        bool bf16, float* red) {
+  for (int k0 = 0; k0 < r; k0 += 8) {
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    const int kn = min(8, r - k0);
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+      const float a = row[i];
+      const float* pr = P + (size_t)i * r + k0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < kn) acc[q] += a * pr[q];
+    }
+    block_sum<8>(acc, red);
+    if (threadIdx.x == 0)
+      for (int q = 0; q < kn; ++q) write_ext(out, ext_base, k0 + q, acc[q], ext_terms, bf16);
+  }
+}
+
+// ------------------------------------------------------------------ embed
+__global__ void k_embed(float* __restrict__ x32, const int32_t* __restrict__ tokens, int B, int T, int d,
+                        const double* __restrict__ E64, const void* __restrict__ E16, bool bf16,
+                        const float* __restrict__ Pp, const float* __restrict__ Pm, const float* __restrict__ Ve,
+                        int r, const float* __restrict__ pe) {
+  const int row = blockIdx.x;
+  const int per_sign = B * T;
+  const int s = row / per_sign, rem = row % per_sign, b = rem / T, t = rem % T;
+  const int tok = tokens[b * T + t];
+  const float* P = (s == 0 ? Pp : Pm) + (size_t)tok * r;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float e = E64 ? (float)E64[(size_t)tok * d + i] : ld16(E16, (size_t)tok * d + i, bf16);
+    float delta = 0.f;
+    for (int k = 0; k < r; ++k) delta += P[k] * Ve[(size_t)i * r + k];
+    x32[(size_t)row * d + i] = (e + delta) + pe[(size_t)t * d + i];
+  }
+}
+
+void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const double* E64, const void* E16,
+                  bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r, const float* pe,
+                  int nrows, cudaStream_t st) {
+  k_embed<<<nrows, 256, 0, st>>>(x32, tokens, B, T, d, E64, E16, bf16, Pplus, Pminus, Ve32, r, pe);
+}
+
+// ------------------------------------------------------------------ LN (+ extension)
+__global__ void k_ln_ext(const float* __restrict__ x32, const float* __restrict__ g, const float* __restrict__ bta,
+                         int d, void* __restrict__ out, int ldo, bool bf16, const float* __restrict__ Pp,
+                         const float* __restrict__ Pm, int r, int rows_per_sign, int ext_terms) {
+  extern __shared__ float sh[];  // d floats row cache + reduction scratch
+  float* row = sh;
+  float* red = sh + d;
+  const int m = blockIdx.x;
+  const float* x = x32 + (size_t)m * d;
+  float acc[1] = {0.f};
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float v = x[i];
+    row[i] = v;
+    acc[0] += v;
+  }
+  block_sum<1>(acc, red);
+  const float mu = acc[0] / (float)d;
+  acc[0] = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float c = row[i] - mu;
+    acc[0] += c * c;
+  }
+  block_sum<1>(acc, red);
+  const float sd = sqrtf(acc[0] / (float)d + 1e-5f);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float h = (row[i] - mu) / sd * g[i] + bta[i];
+    row[i] = h;
+    st16(out, (size_t)m * ldo + i, h, bf16);
+  }
+  __syncthreads();
+  if (r > 0) {
+    const float* P = (m < rows_per_sign) ? Pp : Pm;
+    row_ext(row, d, P, r, out, (size_t)m * ldo + d, ext_terms, bf16, red);
+  }
+}
+
+void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
+                   bool bf16, const float* Pplus, const float* Pminus, int r, int rows_per_sign, int ext_terms,
+                   cudaStream_t st) {
+  const size_t smem = (size_t)(d + 32 * 8) * sizeof(float);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    ZO_CUDA_TRY(cudaFuncSetAttribute(k_ln_ext, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  k_ln_ext<<<M, 256, smem, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms);
+}
+
+// ------------------------------------------------------------------ extension of a 16-bit activation
+__global__ void k_ext(void* __restrict__ a, int lda, int K, bool bf16, const float* __restrict__ Pp,
+                      const float* __restrict__ Pm, int r, int rows_per_sign, int ext_terms) {
+  __shared__ float red[32 * 8];
+  const int m = blockIdx.x;
+  const float* P = (m < rows_per_sign) ? Pp : Pm;
+  const uint16_t* row = reinterpret_cast<const uint16_t*>(a) + (size_t)m * lda;
+  for (int k0 = 0; k0 < r; k0 += 8) {
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    const int kn = min(8, r - k0);
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+      const float v = from16(row[i], bf16);
+      const float* pr = P + (size_t)i * r + k0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < kn) acc[q] += v * pr[q];
+    }
+    block_sum<8>(acc, red);
+    if (threadIdx.x == 0)
+      for (int q = 0; q < kn; ++q) write_ext(a, (size_t)m * lda + K, k0 + q, acc[q], ext_terms, bf16);
+  }
+}
+
+void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, const float* Pminus, int r,
+                int rows_per_sign, int ext_terms, cudaStream_t st) {
+  if (r <= 0) return;
+  k_ext<<<M, 256, 0, st>>>(a, lda, K, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms);
+}
+
+// ------------------------------------------------------------------ attention (T <= 128)
+__global__ void k_attention(const void* __restrict__ qkv, int ldq, void* __restrict__ ctx, int ldc, int T, int H,
+                            int dh, bool bf16) {
+  extern __shared__ float sm[];
+  const int seq = blockIdx.x, h = blockIdx.y;
+  const int d = H * dh, ld = dh + 1;
+  float* q = sm;
+  float* k = q + T * ld;
+  float* v = k + T * ld;
+  for (int idx = threadIdx.x; idx < T * dh; idx += blockDim.x) {
+    const int t = idx / dh, c = idx % dh;
+    const size_t base = (size_t)(seq * T + t) * ldq + (size_t)h * dh + c;
+    q[t * ld + c] = ld16(qkv, base, bf16);
+    k[t * ld + c] = ld16(qkv, base + d, bf16);
+    v[t * ld + c] = ld16(qkv, base + 2 * d, bf16);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const float rs = sqrtf((float)dh);
+  for (int i = warp; i < T; i += nw) {
+    float s[4];
+    float mx = -CUDART_INF_F;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      const int j = lane + 32 * jj;
+      s[jj] = -CUDART_INF_F;
+      if (j < T && j <= i) {
+        float acc = 0.f;
+        for (int c = 0; c < dh; ++c) acc += q[i * ld + c] * k[j * ld + c];
+        s[jj] = acc / rs;
+      }
+      mx = fmaxf(mx, s[jj]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      s[jj] = (s[jj] == -CUDART_INF_F) ? 0.f : expf(s[jj] - mx);
+      sum += s[jj];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) s[jj] = s[jj] / sum;
+    for (int c = lane; c < dh; c += 32) {
+      float acc = 0.f;
+      for (int j = 0; j <= i; ++j) {
+        const float pj = __shfl_sync(0xffffffffu, s[j >> 5], j & 31);
+        acc += pj * v[j * ld + c];
+      }
+      st16(ctx, (size_t)(seq * T + i) * ldc + (size_t)h * dh + c, acc, bf16);
+    }
+    if (dh < 32) {
+      // lanes >= dh still must take part in the shuffles above; nothing else to do
+    }
+  }
+}
+
+void launch_attention(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, int dh, bool bf16,
+                      cudaStream_t st) {
+  if (T > 128) throw Error(ZO_ERR_DIMENSION, "attention kernel supports T <= 128");
+  const size_t smem = (size_t)3 * T * (dh + 1) * sizeof(float);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    ZO_CUDA_TRY(cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  k_attention<<<dim3(nseq, H), 128, smem, st>>>(qkv, ldq, ctx, ldc, T, H, dh, bf16);
+}
+
+// ------------------------------------------------------------------ final LN at scored rows
+__global__ void k_final_ln(const float* __restrict__ x32, const float* __restrict__ g, const float* __restrict__ bta,
+                           int B, int T, int d, int prompt_len, int Lopt, float* __restrict__ xs32,
+                           void* __restrict__ xs16, bool bf16, const float* __restrict__ Ve, int r,
+                           float* __restrict__ z) {
+  extern __shared__ float sh[];
+  float* row = sh;
+  float* red = sh + d;
+  const int srow = blockIdx.x;
+  const int s = srow / (B * Lopt), rem = srow % (B * Lopt), b = rem / Lopt, j = rem % Lopt;
+  const int m = s * B * T + b * T + (prompt_len - 1 + j);
+  const float* x = x32 + (size_t)m * d;
+  float acc[1] = {0.f};
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    row[i] = x[i];
+    acc[0] += row[i];
+  }
+  block_sum<1>(acc, red);
+  const float mu = acc[0] / (float)d;
+  acc[0] = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float c = row[i] - mu;
+    acc[0] += c * c;
+  }
+  block_sum<1>(acc, red);
+  const float sd = sqrtf(acc[0] / (float)d + 1e-5f);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float h = (row[i] - mu) / sd * g[i] + bta[i];
+    row[i] = h;
+    xs32[(size_t)srow * d + i] = h;
+    st16(xs16, (size_t)srow * d + i, h, bf16);
+  }
+  __syncthreads();
+  for (int k0 = 0; k0 < r; k0 += 8) {
+    float a8[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a8[q] = 0.f;
+    const int kn = min(8, r - k0);
+    for (int i = threadIdx.x; i < d; i += blockDim.x)
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < kn) a8[q] += row[i] * Ve[(size_t)i * r + k0 + q];
+    block_sum<8>(a8, red);
+    if (threadIdx.x == 0)
+      for (int q = 0; q < kn; ++q) z[(size_t)srow * r + k0 + q] = a8[q];
+  }
+}
+
+void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d, int prompt_len,
+                     int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r, float* z,
+                     cudaStream_t st) {
+  const size_t smem = (size_t)(d + 32 * 8) * sizeof(float);
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    ZO_CUDA_TRY(cudaFuncSetAttribute(k_final_ln, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = smem;
+  }
+  k_final_ln<<<2 * B * Lopt, 256, smem, st>>>(x32, gamma, beta, B, T, d, prompt_len, Lopt, xs32, xs16, bf16, Ve32,
+                                              r, z);
+}
+
+// ------------------------------------------------------------------ loss (K6b): log-softmax + gold gather
+// One CTA per example (sign, b); streams its Lopt logits rows from HBM with
+// float4 loads, adds the embedding LoRA term z . P_s,e[v]^T on the fly and
+// never materialises probabilities.
+__global__ void __launch_bounds__(1024) k_loss(const float* __restrict__ logits, int ldl, int V,
+                                               const float* __restrict__ z, int r, const float* __restrict__ Pp,
+                                               const float* __restrict__ Pm, const int32_t* __restrict__ gold,
+                                               int B, int Lopt, double* __restrict__ nll) {
+  __shared__ float red[32];
+  __shared__ float zs[64];
+  const int ex = blockIdx.x;  // s*B + b
+  const int s = ex / B, b = ex % B;
+  const float* P = s == 0 ? Pp : Pm;
+  float total = 0.f;
+  for (int j = 0; j < Lopt; ++j) {
+    const int srow = ex * Lopt + j;
+    const float* lr = logits + (size_t)srow * ldl;
+    if (threadIdx.x < r && threadIdx.x < 64) zs[threadIdx.x] = z[(size_t)srow * r + threadIdx.x];
+    __syncthreads();
+    float mx = -CUDART_INF_F;
+    const int V4 = V >> 2;
+    for (int i = threadIdx.x; i < V4; i += blockDim.x) {
+      const float4 l4 = reinterpret_cast<const float4*>(lr)[i];
+      float l[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float add = 0.f;
+        for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)(4 * i + e) * r + k];
+        mx = fmaxf(mx, l[e] + add);
+      }
+    }
+    for (int v = 4 * V4 + threadIdx.x; v < V; v += blockDim.x) {
+      float add = 0.f;
+      for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)v * r + k];
+      mx = fmaxf(mx, lr[v] + add);
+    }
+    mx = block_max(mx, red);
+    float sum = 0.f;
+    for (int i = threadIdx.x; i < V4; i += blockDim.x) {
+      const float4 l4 = reinterpret_cast<const float4*>(lr)[i];
+      float l[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float add = 0.f;
+        for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)(4 * i + e) * r + k];
+        sum += expf(l[e] + add - mx);
+      }
+    }
+    for (int v = 4 * V4 + threadIdx.x; v < V; v += blockDim.x) {
+      float add = 0.f;
+      for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)v * r + k];
+      sum += expf(lr[v] + add - mx);
+    }
+    float acc[1] = {sum};
+    block_sum<1>(acc, red);
+    if (threadIdx.x == 0) {
+      const int gv = gold[(size_t)ex * Lopt + j];
+      float add = 0.f;
+      for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)gv * r + k];
+      const float lse = mx + logf(acc[0]);
+      total = total + (lse - (lr[gv] + add));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) nll[ex] = (double)total;
+}
+
+void launch_loss(const float* logits, int ldl, int V, const float* z, int r, const float* Pplus_e,
+                 const float* Pminus_e, const int32_t* gold, int B, int Lopt, double* nll, cudaStream_t st) {
+  if (r > 64) throw Error(ZO_ERR_DIMENSION, "loss kernel supports rank <= 64 on the embedding");
+  if (ldl % 4) throw Error(ZO_ERR_DIMENSION, "logits leading dimension must be a multiple of 4");
+  k_loss<<<2 * B, 1024, 0, st>>>(logits, ldl, V, z, r, Pplus_e, Pminus_e, gold, B, Lopt, nll);
+}
+
+// ------------------------------------------------------------------ coefficient (K7)
+__device__ double pairwise_sum(const double* v, int n) {
+  // numerics.py:279-284 (split at n//2, left first), iterative post-order
+  if (n == 1) return v[0];
+  const int h = n / 2;
+  return __dadd_rn(pairwise_sum(v, h), pairwise_sum(v + h, n - h));
+}
+
+__global__ void k_coefficient(const double* __restrict__ nll, int B, double eps, double lr, int divide_by_r,
+                              int rank, double* __restrict__ out4, unsigned* __restrict__ abort_flag) {
+  const double lp = __ddiv_rn(pairwise_sum(nll, B), (double)B);
+  const double lm = __ddiv_rn(pairwise_sum(nll + B, B), (double)B);
+  const double c = __ddiv_rn(__dsub_rn(lp, lm), __dmul_rn(2.0, eps));
+  const double c_used = divide_by_r ? __ddiv_rn(c, (double)rank) : c;
+  const bool ok = isfinite(lp) && isfinite(lm);
+  out4[0] = lp;
+  out4[1] = lm;
+  out4[2] = c;
+  out4[3] = ok ? -__dmul_rn(lr, c_used) : 0.0;
+  *abort_flag = ok ? 0u : 1u;
+}
+
+void launch_coefficient(const double* nll, int B, double eps, double lr, int divide_by_r, int rank, double* out4,
+                        unsigned* abort_flag, cudaStream_t st) {
+  k_coefficient<<<1, 1, 0, st>>>(nll, B, eps, lr, divide_by_r, rank, out4, abort_flag);
+}
+
+// ------------------------------------------------------------------ update (K8), probe prep
+__global__ void k_update(double* __restrict__ A, const double* __restrict__ U, int64_t n,
+                         const double* __restrict__ out4, const unsigned* __restrict__ abort_flag) {
+  if (*abort_flag) return;
+  const double beta = out4[3];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    A[i] = __dadd_rn(A[i], __dmul_rn(beta, U[i]));
+}
+
+void launch_update(double* A, const double* U, int64_t n, const double* out4, const unsigned* abort_flag,
+                   cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_update<<<grid > 0 ? grid : 1, 256, 0, st>>>(A, U, n, out4, abort_flag);
+}
+
+__global__ void k_prep(const double* __restrict__ A, const double* __restrict__ U, int64_t n, double es,
+                       float* __restrict__ Pp, float* __restrict__ Pm) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double a = A ? A[i] : 0.0;
+    const double d = __dmul_rn(es, U[i]);
+    Pp[i] = (float)__dadd_rn(a, d);
+    Pm[i] = (float)__dsub_rn(a, d);
+  }
+}
+
+void launch_prep_probe(const double* A, const double* U, int64_t n, double eps, double probe_scale, float* Pp,
+                       float* Pm, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_prep<<<grid > 0 ? grid : 1, 256, 0, st>>>(A, U, n, eps * probe_scale, Pp, Pm);
+}
+
+// ------------------------------------------------------------------ window V -> B-operand extension columns
+__global__ void k_vext(const double* __restrict__ V, int n, int r, void* __restrict__ W, int ldw, int K, bool bf16,
+                       int ext_terms, float* __restrict__ V32) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n * r) return;
+  const int j = (int)(i / r), k = (int)(i % r);
+  const double v = V[i];
+  const float vf = (float)v;
+  if (V32) V32[i] = vf;
+  if (!W) return;
+  uint16_t* o = reinterpret_cast<uint16_t*>(W) + (size_t)j * ldw + K;
+  if (ext_terms == 3) {
+    const uint16_t hi = to16(vf, bf16);
+    o[3 * k] = hi;
+    o[3 * k + 1] = hi;
+    o[3 * k + 2] = to16(vf - from16(hi, bf16), bf16);
+  } else {
+    o[k] = to16(vf, bf16);
+  }
+}
+
+void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K, bool bf16, int ext_terms,
+                       float* V32, cudaStream_t st) {
+  const int64_t cnt = (int64_t)n * r;
+  k_vext<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(V, n, r, W16T, ldw, K, bf16, ext_terms, V32);
+}
+
+// ------------------------------------------------------------------ fold (K9) + 16-bit shadow refresh
+// 32x32 tile per block: W64 tile (+ sum_k alpha*(A_ik*V_jk), k ascending, each
+// term rounded as numpy does: numerics.py:211) -> W64, then the 16-bit shadow
+// (transposed [n, ldw] for projections, straight [m, n] for the embedding).
+__global__ void k_fold_shadow(double* __restrict__ W, int m, int n, const double* __restrict__ A,
+                              const double* __restrict__ Vv, int r, double alpha, void* __restrict__ W16, int ldw,
+                              int transposed, bool bf16) {
+  __shared__ float tile[32][33];
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int i = i0 + yy, j = j0 + tx;
+    float f = 0.f;
+    if (i < m && j < n) {
+      double w = W[(size_t)i * n + j];
+      if (r > 0) {
+        for (int k = 0; k < r; ++k)
+          w = __dadd_rn(w, __dmul_rn(alpha, __dmul_rn(A[(size_t)i * r + k], Vv[(size_t)j * r + k])));
+        W[(size_t)i * n + j] = w;
+      }
+      f = (float)w;
+      if (!transposed && W16) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
+    }
+    tile[yy][tx] = f;
+  }
+  if (!transposed || !W16) return;
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int j = j0 + yy, i = i0 + tx;
+    if (i < m && j < n) reinterpret_cast<uint16_t*>(W16)[(size_t)j * ldw + i] = to16(tile[tx][yy], bf16);
+  }
+}
+
+void launch_fold(double* W64, int m, int n, const double* A, const double* V, int r, double alpha, void* W16,
+                 int ldw, int transposed, bool bf16, cudaStream_t st) {
+  dim3 grid((n + 31) / 32, (m + 31) / 32);
+  k_fold_shadow<<<grid, dim3(32, 8), 0, st>>>(W64, m, n, A, V, r, alpha, W16, ldw, transposed, bf16);
+}
+
+void launch_shadow_T(const double* W64, int m, int n, void* W16T, int ldw, bool bf16, cudaStream_t st) {
+  dim3 grid((n + 31) / 32, (m + 31) / 32);
+  k_fold_shadow<<<grid, dim3(32, 8), 0, st>>>(const_cast<double*>(W64), m, n, nullptr, nullptr, 0, 1.0, W16T, ldw,
+                                                1, bf16);
+}
+
+__global__ void k_shadow(const double* __restrict__ W, int64_t count, void* __restrict__ o, bool bf16) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride)
+    reinterpret_cast<uint16_t*>(o)[i] = to16((float)W[i], bf16);
+}
+
+void launch_shadow(const double* W64, int64_t count, void* W16, bool bf16, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 16);
+  k_shadow<<<grid > 0 ? grid : 1, 256, 0, st>>>(W64, count, W16, bf16);
+}
+
+__global__ void k_f64_to_f32(const double* __restrict__ a, float* __restrict__ b, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) b[i] = (float)a[i];
+}
+void launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_f64_to_f32<<<grid > 0 ? grid : 1, 256, 0, st>>>(a, b, n);
+}
+
+void launch_zero(void* p, size_t bytes, cudaStream_t st) { ZO_CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st)); }
+
+}  // namespace zo

@@ -1,0 +1,56 @@
+// Non-GEMM kernels of the LoZO step (scorer glue, loss, coefficient, update, fold).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace zo {
+
+// Activation/weight operand precision for the tensor-core path.
+struct H16 {
+  bool bf16;
+};
+
+// x32[M,d] = E[tok] + sum_k P_s[tok,k] V_e[:,k] + PE[t]   (model.py:180, adapter.py:200-234)
+void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const double* E64, const void* E16,
+                  bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r,
+                  const float* pe, int nrows, cudaStream_t st);
+// h = LN(x) (model.py:139-142) -> out[:, :d] (16-bit); ext columns [d, d+3r) = (t_hi, t_lo, t_hi)
+// per rank with t = h . P_s (fp32) -- the LoRA K-extension operand (A side).
+void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
+                   bool bf16, const float* Pplus, const float* Pminus, int r, int rows_per_sign, int ext_terms,
+                   cudaStream_t st);
+// ext columns for a 16-bit activation a[:, :K] already in place (ctx -> attn_out, gelu -> ff_down).
+void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, const float* Pminus, int r,
+                int rows_per_sign, int ext_terms, cudaStream_t st);
+// causal softmax attention per (sequence, head) (model.py:184-194); qkv [M,3d] -> ctx[:, :d]
+void launch_attention(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, int dh, bool bf16,
+                      cudaStream_t st);
+// final LN at scored rows (prompt_len-1+j) -> xs32/xs16, z = xs . V_e
+void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d,
+                     int prompt_len, int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r,
+                     float* z, cudaStream_t st);
+// per scored row: logits + z.P_s,e^T -> log-softmax, gold gather -> nll[sign*B + b] (model.py:202-215)
+void launch_loss(const float* logits, int ldl, int V, const float* z, int r, const float* Pplus_e,
+                 const float* Pminus_e, const int32_t* gold, int B, int Lopt, double* nll, cudaStream_t st);
+// canonical_mean per sign, c, c_used, beta (numerics.py:271-284, zo_engine.py:331,411)
+void launch_coefficient(const double* nll, int B, double eps, double lr, int divide_by_r, int rank,
+                        double* out4, unsigned* abort_flag, cudaStream_t st);
+// A += beta*U (numerics.py:238-243; product then sum, no FMA); skipped when aborted
+void launch_update(double* A, const double* U, int64_t n, const double* out4, const unsigned* abort_flag,
+                   cudaStream_t st);
+// P+- = fp32(A +- eps*U)
+void launch_prep_probe(const double* A, const double* U, int64_t n, double eps, double probe_scale, float* Pp,
+                       float* Pm, cudaStream_t st);
+// V ext columns (hi, hi, lo) into W16T[:, K:K+3r] for one matrix; V32 copy
+void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K, bool bf16, int ext_terms,
+                       float* V32, cudaStream_t st);
+// W64[m,n] += sum_k A[:,k] V[:,k]^T (k ascending, numerics.py:207-235) then A = 0
+void launch_fold(double* W64, int m, int n, const double* A, const double* V, int r, double alpha, void* W16,
+                 int ldw, int transposed, bool bf16, cudaStream_t st);
+// shadows: W16T[n, :m] = h16(W64[m,n]^T) (projection) or E16[m, n] = h16(W64) (embed)
+void launch_shadow_T(const double* W64, int m, int n, void* W16T, int ldw, bool bf16, cudaStream_t st);
+void launch_shadow(const double* W64, int64_t count, void* W16, bool bf16, cudaStream_t st);
+void launch_zero(void* p, size_t bytes, cudaStream_t st);
+void launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t st);
+
+}  // namespace zo

@@ -1,0 +1,879 @@
+// libzob200 C ABI: context, device layout and the LoZO step orchestration.
+//
+// Device layout:
+//   W64[lid]   float64 master, reference (in, out) layout -- bit-exact init/fold
+//   W16T[lid]  16-bit B operand [out, in + KE] (K-major); columns in..in+3r hold
+//              the window V as (hi, hi, lo) so x.W_eff = [x | t] . [W ; V]^T
+//   E16        16-bit embedding [V, d] (gather + tied LM-head B operand)
+//   U/V/A      float64 slot arenas in sorted layer-id order (digest order)
+//   P+/P-      float32 A +- eps*U (the only sign-dependent operand)
+//   activations sized for 2 * max_batch * T rows (both signs in one launch)
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/zob200.h"
+#include "zo_common.cuh"
+#include "zo_gemm.h"
+#include "zo_kernels.h"
+#include "zo_sampler.h"
+
+using namespace zo;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+enum Kind { K_EMBED = 0, K_QKV = 1, K_OUT = 2, K_UP = 3, K_DOWN = 4 };
+
+struct Matrix {
+  std::string lid;
+  int kind = 0, layer = -1;
+  int64_t m = 0, n = 0;  // reference layout: (in, out)
+  uint64_t lid_hash = 0;
+  int64_t u_off = 0, v_off = 0;
+  double* W64 = nullptr;
+  void* W16 = nullptr;
+  int ldw = 0;
+};
+
+struct LayerPlan {
+  GemmDesc qkv, out, up, down;
+};
+struct RowPlan {
+  std::vector<LayerPlan> layers;
+  GemmDesc lm;
+};
+
+uint64_t fnv(const void* p, size_t n, uint64_t h) {
+  const uint8_t* b = static_cast<const uint8_t*>(p);
+  for (size_t i = 0; i < n; ++i) h = (h ^ b[i]) * 0x100000001B3ULL;
+  return h;
+}
+const uint64_t FNV0 = 0xCBF29CE484222325ULL;
+
+struct DevAlloc {
+  std::vector<void*> ptrs;
+  uint64_t bytes = 0;
+  template <class T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    size_t b = std::max<size_t>(count * sizeof(T), 256);
+    ZO_CUDA_TRY(cudaMalloc(&p, b));
+    ZO_CUDA_TRY(cudaMemset(p, 0, b));
+    ptrs.push_back(p);
+    bytes += b;
+    return static_cast<T*>(p);
+  }
+  ~DevAlloc() {
+    for (void* p : ptrs) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+struct zo_ctx {
+  zo_model_desc d{};
+  int T = 0, dh = 0, r = 0, ext_terms = 3, KE = 64, ext_used = 0, num_sms = 148;
+  bool bf16 = false;
+  cudaStream_t st = nullptr;
+  DevAlloc mem;
+  std::vector<Matrix> mats;  // sorted by lid
+  int i_embed = -1;
+  std::vector<int> i_qkv, i_out, i_up, i_down;
+  int64_t su = 0, sv = 0;  // arena sizes
+  double *U = nullptr, *V = nullptr, *A = nullptr;
+  float *Pp = nullptr, *Pm = nullptr, *V32 = nullptr;
+  // LN params
+  std::vector<float*> ln1g, ln1b, ln2g, ln2b;
+  float *lnfg = nullptr, *lnfb = nullptr;
+  // activations
+  int Mmax = 0, Mpad = 0, Smax = 0, Spad = 0, ldl = 0;
+  float* x32 = nullptr;
+  void *hA = nullptr, *qkv = nullptr, *ctxA = nullptr, *gA = nullptr, *xs16 = nullptr;
+  float *xs32 = nullptr, *z = nullptr, *logits = nullptr, *pe = nullptr;
+  double *nll = nullptr, *out4 = nullptr, *scratch = nullptr;
+  int64_t scratch_n = 0;
+  unsigned* abort_flag = nullptr;
+  int32_t *tok = nullptr, *gold = nullptr;
+  uint64_t* d_step = nullptr;
+  // pinned staging
+  int32_t *h_tok = nullptr, *h_gold = nullptr;
+  double* h_out4 = nullptr;
+  uint64_t* h_step = nullptr;
+  // sampler
+  SamplerPlan planU, planV, planOne;
+  std::vector<StreamDesc> streamsU, streamsV;
+  unsigned* flags = nullptr;
+  std::map<int, RowPlan> plans;  // keyed by rows M
+  // timing
+  cudaEvent_t ev[4];
+  float last_ms[3] = {0, 0, 0};
+  double probe_eps = 0.0, probe_scale = 1.0;
+  int64_t v_window = -1;  // window start whose V is loaded (-1: none)
+  bool a_dirty = false;   // window A carries unfolded mass
+
+  ~zo_ctx() {
+    if (h_tok) cudaFreeHost(h_tok);
+    if (h_gold) cudaFreeHost(h_gold);
+    if (h_out4) cudaFreeHost(h_out4);
+    if (h_step) cudaFreeHost(h_step);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+int fail(const Error& e) {
+  g_last_error = e.msg;
+  return e.code;
+}
+
+#define ZO_API_BEGIN try {
+#define ZO_API_END                                                   \
+  }                                                                  \
+  catch (const Error& e) { return fail(e); }                         \
+  catch (const std::exception& e) { return fail(Error(ZO_ERR_INTERNAL, e.what())); }
+
+void check(bool ok, int code, const std::string& msg) {
+  if (!ok) throw Error(code, msg);
+}
+
+Matrix& find(zo_ctx* c, const char* lid) {
+  for (auto& m : c->mats)
+    if (m.lid == lid) return m;
+  throw Error(ZO_ERR_INPUT, std::string("unknown layer id ") + lid);
+}
+
+void build_sampler_plan(zo_ctx* c, SamplerPlan& P, std::vector<StreamDesc>& sd) {
+  int64_t chunk = 0;
+  std::vector<uint32_t> chunk_stream;
+  for (size_t s = 0; s < sd.size(); ++s) {
+    sd[s].chunk_begin = (uint64_t)chunk;
+    sd[s].n_chunks = sampler_chunks_for(sd[s].n);
+    for (uint64_t i = 0; i < sd[s].n_chunks; ++i) chunk_stream.push_back((uint32_t)s);
+    chunk += (int64_t)sd[s].n_chunks;
+  }
+  P.S = (int)sd.size();
+  P.C = chunk;
+  P.d_streams = c->mem.get<StreamDesc>(sd.size());
+  P.d_chunk_stream = c->mem.get<uint32_t>(chunk);
+  P.d_keys = c->mem.get<uint64_t>(2 * sd.size());
+  P.d_spec = c->mem.get<uint64_t>(chunk);
+  P.d_exit = c->mem.get<uint64_t>(chunk);
+  P.d_count = c->mem.get<uint32_t>(chunk);
+  P.d_offset = c->mem.get<uint64_t>(chunk);
+  P.d_flags = c->flags;
+  ZO_CUDA_TRY(cudaMemcpy(P.d_streams, sd.data(), sd.size() * sizeof(StreamDesc), cudaMemcpyHostToDevice));
+  ZO_CUDA_TRY(cudaMemcpy(P.d_chunk_stream, chunk_stream.data(), chunk_stream.size() * 4, cudaMemcpyHostToDevice));
+}
+
+RowPlan& row_plan(zo_ctx* c, int M) {
+  auto it = c->plans.find(M);
+  if (it != c->plans.end()) return it->second;
+  RowPlan rp;
+  const int d = c->d.dim;
+  const int ldh = d + c->KE, ldg = 4 * d + c->KE;
+  const int S = M / c->T * c->d.opt_len;
+  for (int l = 0; l < c->d.n_layers; ++l) {
+    LayerPlan lp;
+    const Matrix& q = c->mats[c->i_qkv[l]];
+    const Matrix& o = c->mats[c->i_out[l]];
+    const Matrix& u = c->mats[c->i_up[l]];
+    const Matrix& w = c->mats[c->i_down[l]];
+    gemm_plan(lp.qkv, c->hA, M, ldh, q.W16, 3 * d, q.ldw, d + c->ext_used, EPI_STORE16, c->bf16, c->qkv, 3 * d,
+              c->num_sms);
+    gemm_plan(lp.out, c->ctxA, M, ldh, o.W16, d, o.ldw, d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
+              c->num_sms);
+    gemm_plan(lp.up, c->hA, M, ldh, u.W16, 4 * d, u.ldw, d + c->ext_used, EPI_GELU16, c->bf16, c->gA, ldg,
+              c->num_sms);
+    gemm_plan(lp.down, c->gA, M, ldg, w.W16, d, w.ldw, 4 * d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
+              c->num_sms);
+    rp.layers.push_back(lp);
+  }
+  const Matrix& e = c->mats[c->i_embed];
+  gemm_plan(rp.lm, c->xs16, S, d, e.W16, c->d.vocab, d, d, EPI_STORE32, c->bf16, c->logits, c->ldl, c->num_sms);
+  return c->plans.emplace(M, std::move(rp)).first->second;
+}
+
+void refresh_shadow(zo_ctx* c, const Matrix& m) {
+  if (m.kind == K_EMBED)
+    launch_shadow(m.W64, m.m * m.n, m.W16, c->bf16, c->st);
+  else
+    launch_shadow_T(m.W64, (int)m.m, (int)m.n, m.W16, m.ldw, c->bf16, c->st);
+}
+
+void write_vext_all(zo_ctx* c) {
+  for (auto& m : c->mats)
+    launch_write_vext(c->V + m.v_off, (int)m.n, c->r, m.kind == K_EMBED ? nullptr : m.W16, m.ldw, (int)m.m,
+                      c->bf16, c->ext_terms, c->V32 + m.v_off, c->st);
+}
+
+void do_score(zo_ctx* c, int B, int nsign) {
+  const int d = c->d.dim, T = c->T, M = nsign * B * T;
+  check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
+  RowPlan& rp = row_plan(c, M);
+  const Matrix& e = c->mats[c->i_embed];
+  const int rps = B * T;
+  const int ldh = d + c->KE, ldg = 4 * d + c->KE;
+  launch_embed(c->x32, c->tok, B, T, d, e.W64, e.W16, c->bf16, c->Pp + e.u_off, c->Pm + e.u_off, c->V32 + e.v_off,
+               c->r, c->pe, M, c->st);
+  for (int l = 0; l < c->d.n_layers; ++l) {
+    const Matrix& q = c->mats[c->i_qkv[l]];
+    const Matrix& o = c->mats[c->i_out[l]];
+    const Matrix& u = c->mats[c->i_up[l]];
+    const Matrix& w = c->mats[c->i_down[l]];
+    const LayerPlan& lp = rp.layers[l];
+    launch_ln_ext(c->x32, c->ln1g[l], c->ln1b[l], M, d, c->hA, ldh, c->bf16, c->Pp + q.u_off, c->Pm + q.u_off, c->r,
+                  rps, c->ext_terms, c->st);
+    gemm_launch(lp.qkv, c->st);
+    launch_attention(c->qkv, 3 * d, c->ctxA, ldh, nsign * B, T, c->d.n_heads, c->dh, c->bf16, c->st);
+    launch_ext(c->ctxA, ldh, M, d, c->bf16, c->Pp + o.u_off, c->Pm + o.u_off, c->r, rps, c->ext_terms, c->st);
+    gemm_launch(lp.out, c->st);
+    launch_ln_ext(c->x32, c->ln2g[l], c->ln2b[l], M, d, c->hA, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off, c->r,
+                  rps, c->ext_terms, c->st);
+    gemm_launch(lp.up, c->st);
+    launch_ext(c->gA, ldg, M, 4 * d, c->bf16, c->Pp + w.u_off, c->Pm + w.u_off, c->r, rps, c->ext_terms, c->st);
+    gemm_launch(lp.down, c->st);
+  }
+  launch_final_ln(c->x32, c->lnfg, c->lnfb, B * nsign, T, d, c->d.prompt_len, c->d.opt_len, c->xs32, c->xs16,
+                  c->bf16, c->V32 + e.v_off, c->r, c->z, c->st);
+  gemm_launch(rp.lm, c->st);
+  launch_loss(c->logits, c->ldl, c->d.vocab, c->z, c->r, c->Pp + e.u_off, c->Pm + e.u_off, c->gold, B,
+              c->d.opt_len, c->nll, c->st);
+}
+
+// gold: [gold_signs, B, opt_len]; with gold_signs == 1 both probe halves share it
+void stage_batch(zo_ctx* c, const int32_t* tokens, const int32_t* gold, int B, int gold_signs) {
+  const size_t nt = (size_t)B * c->T, ng = (size_t)gold_signs * B * c->d.opt_len;
+  for (size_t i = 0; i < nt; ++i)
+    check(tokens[i] >= 0 && tokens[i] < c->d.vocab, ZO_ERR_INPUT,
+          "token id outside [0, " + std::to_string(c->d.vocab) + ")");
+  for (size_t i = 0; i < ng; ++i)
+    check(gold[i] >= 0 && gold[i] < c->d.vocab, ZO_ERR_INPUT, "gold token id out of range");
+  std::memcpy(c->h_tok, tokens, nt * 4);
+  std::memcpy(c->h_gold, gold, ng * 4);
+  if (gold_signs == 1) std::memcpy(c->h_gold + ng, gold, ng * 4);
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->tok, c->h_tok, nt * 4, cudaMemcpyHostToDevice, c->st));
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->gold, c->h_gold, 2 * (ng / gold_signs) * 4, cudaMemcpyHostToDevice, c->st));
+}
+
+void set_step(zo_ctx* c, uint64_t step) {
+  // pinned staging is reused: wait for the previous copy to drain before overwriting
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  *c->h_step = step;
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->d_step, c->h_step, 8, cudaMemcpyHostToDevice, c->st));
+}
+
+void fold_all(zo_ctx* c) {
+  for (auto& m : c->mats)
+    launch_fold(m.W64, (int)m.m, (int)m.n, c->A + m.u_off, c->V + m.v_off, c->r, 1.0, m.W16,
+                m.kind == K_EMBED ? (int)m.n : m.ldw, m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
+  ZO_CUDA_TRY(cudaMemsetAsync(c->A, 0, (size_t)c->su * 8, c->st));
+  c->a_dirty = false;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* zo_last_error(void) { return g_last_error.c_str(); }
+int zo_version(void) { return 1; }
+
+int zo_create(zo_ctx** out, const zo_model_desc* desc) {
+  ZO_API_BEGIN
+  check(out && desc, ZO_ERR_CONFIG, "null argument");
+  const zo_model_desc& d = *desc;
+  check(d.dim % d.n_heads == 0, ZO_ERR_CONFIG, "dim not divisible by n_heads");
+  check(d.vocab >= 8, ZO_ERR_CONFIG, "vocab must be >= 8");
+  check(d.dim % 8 == 0, ZO_ERR_DIMENSION, "dim must be a multiple of 8 for the tensor-core path");
+  check(d.rank >= 1 && d.max_batch >= 1 && d.opt_len >= 1 && d.prompt_len >= 1, ZO_ERR_CONFIG, "bad sizes");
+  check(d.prompt_len + d.opt_len <= 128, ZO_ERR_DIMENSION, "sequence length > 128 not supported");
+  std::unique_ptr<zo_ctx> c(new zo_ctx());
+  c->d = d;
+  ZO_CUDA_TRY(cudaSetDevice(d.device));
+  cudaDeviceProp prop;
+  ZO_CUDA_TRY(cudaGetDeviceProperties(&prop, d.device));
+  check(prop.major == 10, ZO_ERR_CUDA, std::string("libzob200 targets sm_100a (B200); found ") + prop.name);
+  c->num_sms = prop.multiProcessorCount;
+  c->T = d.prompt_len + d.opt_len;
+  c->dh = d.dim / d.n_heads;
+  c->r = d.rank;
+  c->bf16 = d.precision == ZO_PREC_BF16;
+  c->ext_terms = (3 * d.rank <= 64) ? 3 : 1;
+  c->ext_used = c->ext_terms * d.rank;
+  c->KE = (int)ceil_div(c->ext_used, 64) * 64;
+  for (auto& e : c->ev) ZO_CUDA_TRY(cudaEventCreate(&e));
+  c->flags = c->mem.get<unsigned>(4);
+
+  // registry in sorted layer-id order (matrix_ids, model.py:120-121)
+  const int64_t D = d.dim;
+  std::vector<Matrix> ms;
+  auto add = [&](const std::string& lid, int kind, int layer, int64_t m, int64_t n) {
+    Matrix x;
+    x.lid = lid;
+    x.kind = kind;
+    x.layer = layer;
+    x.m = m;
+    x.n = n;
+    x.lid_hash = fnv(lid.data(), lid.size(), FNV0);
+    ms.push_back(x);
+  };
+  add("embed", K_EMBED, -1, d.vocab, D);
+  for (int l = 0; l < d.n_layers; ++l) {
+    const std::string p = "blk" + std::to_string(l) + ".";
+    add(p + "qkv", K_QKV, l, D, 3 * D);
+    add(p + "attn_out", K_OUT, l, D, D);
+    add(p + "ff_up", K_UP, l, D, 4 * D);
+    add(p + "ff_down", K_DOWN, l, 4 * D, D);
+  }
+  std::sort(ms.begin(), ms.end(), [](const Matrix& a, const Matrix& b) { return a.lid < b.lid; });
+  for (auto& m : ms) {
+    check(d.estimator == ZO_EST_FACTORIZED || d.rank <= std::min(m.m, m.n), ZO_ERR_CONFIG,
+          "rank " + std::to_string(d.rank) + " exceeds min dim of " + m.lid);
+    m.u_off = c->su;
+    m.v_off = c->sv;
+    c->su += m.m * d.rank;
+    c->sv += m.n * d.rank;
+  }
+  c->mats = ms;
+  c->i_qkv.assign(d.n_layers, -1);
+  c->i_out.assign(d.n_layers, -1);
+  c->i_up.assign(d.n_layers, -1);
+  c->i_down.assign(d.n_layers, -1);
+  for (size_t i = 0; i < c->mats.size(); ++i) {
+    Matrix& m = c->mats[i];
+    if (m.kind == K_EMBED) c->i_embed = (int)i;
+    if (m.kind == K_QKV) c->i_qkv[m.layer] = (int)i;
+    if (m.kind == K_OUT) c->i_out[m.layer] = (int)i;
+    if (m.kind == K_UP) c->i_up[m.layer] = (int)i;
+    if (m.kind == K_DOWN) c->i_down[m.layer] = (int)i;
+  }
+  // weights
+  for (auto& m : c->mats) {
+    m.W64 = c->mem.get<double>((size_t)(m.m * m.n));
+    if (m.kind == K_EMBED) {
+      m.ldw = (int)m.n;
+      m.W16 = c->mem.get<uint16_t>((size_t)(m.m * m.n));
+    } else {
+      m.ldw = (int)(m.m + c->KE);
+      m.W16 = c->mem.get<uint16_t>((size_t)(m.n * m.ldw));
+    }
+  }
+  // slots
+  c->U = c->mem.get<double>(c->su);
+  c->A = c->mem.get<double>(c->su);
+  c->V = c->mem.get<double>(c->sv);
+  c->Pp = c->mem.get<float>(c->su);
+  c->Pm = c->mem.get<float>(c->su);
+  c->V32 = c->mem.get<float>(c->sv);
+  // LN params (identity at init, model.py:100-107)
+  std::vector<float> ones(d.dim, 1.0f);
+  auto vec = [&](bool one) {
+    float* p = c->mem.get<float>(d.dim);
+    if (one) ZO_CUDA_TRY(cudaMemcpy(p, ones.data(), d.dim * 4, cudaMemcpyHostToDevice));
+    return p;
+  };
+  for (int l = 0; l < d.n_layers; ++l) {
+    c->ln1g.push_back(vec(true));
+    c->ln1b.push_back(vec(false));
+    c->ln2g.push_back(vec(true));
+    c->ln2b.push_back(vec(false));
+  }
+  c->lnfg = vec(true);
+  c->lnfb = vec(false);
+  // activations
+  c->Mmax = 2 * d.max_batch * c->T;
+  c->Mpad = (int)ceil_div(c->Mmax, 128) * 128;
+  c->Smax = 2 * d.max_batch * d.opt_len;
+  c->Spad = (int)ceil_div(c->Smax, 128) * 128;
+  c->ldl = (int)ceil_div(d.vocab, 4) * 4;
+  c->x32 = c->mem.get<float>((size_t)c->Mpad * D);
+  c->hA = c->mem.get<uint16_t>((size_t)c->Mpad * (D + c->KE));
+  c->qkv = c->mem.get<uint16_t>((size_t)c->Mpad * 3 * D);
+  c->ctxA = c->mem.get<uint16_t>((size_t)c->Mpad * (D + c->KE));
+  c->gA = c->mem.get<uint16_t>((size_t)c->Mpad * (4 * D + c->KE));
+  c->xs16 = c->mem.get<uint16_t>((size_t)c->Spad * D);
+  c->xs32 = c->mem.get<float>((size_t)c->Smax * D);
+  c->z = c->mem.get<float>((size_t)c->Smax * d.rank);
+  c->logits = c->mem.get<float>((size_t)c->Smax * c->ldl);
+  c->nll = c->mem.get<double>(2 * d.max_batch);
+  c->out4 = c->mem.get<double>(4);
+  c->abort_flag = c->mem.get<unsigned>(1);
+  c->tok = c->mem.get<int32_t>((size_t)d.max_batch * c->T);
+  c->gold = c->mem.get<int32_t>((size_t)2 * d.max_batch * d.opt_len);
+  c->d_step = c->mem.get<uint64_t>(1);
+  // positional table: pos_encoding(T, d) (model.py:128-136), float64 -> float32
+  {
+    std::vector<float> pe((size_t)c->T * d.dim);
+    for (int t = 0; t < c->T; ++t)
+      for (int j = 0; j < d.dim; ++j) {
+        const double ang = (double)t / std::pow(10000.0, (2.0 * (j / 2)) / (double)d.dim);
+        pe[(size_t)t * d.dim + j] = (float)((j % 2 == 0) ? std::sin(ang) : std::cos(ang));
+      }
+    c->pe = c->mem.get<float>(pe.size());
+    ZO_CUDA_TRY(cudaMemcpy(c->pe, pe.data(), pe.size() * 4, cudaMemcpyHostToDevice));
+  }
+  ZO_CUDA_TRY(cudaMallocHost(&c->h_tok, (size_t)d.max_batch * c->T * 4));
+  ZO_CUDA_TRY(cudaMallocHost(&c->h_gold, (size_t)2 * d.max_batch * d.opt_len * 4));
+  ZO_CUDA_TRY(cudaMallocHost(&c->h_out4, 4 * 8));
+  ZO_CUDA_TRY(cudaMallocHost(&c->h_step, 8));
+  // sampler plans: U (step), V (window start for lozo, step for factorized)
+  for (auto& m : c->mats) {
+    StreamDesc su{};
+    su.lid_hash = m.lid_hash;
+    su.role = 0;
+    su.step_mode = STEP_CURRENT;
+    su.n = (uint64_t)(m.m * d.rank);
+    su.out_off = (uint64_t)m.u_off;
+    su.scale = 1.0;
+    c->streamsU.push_back(su);
+    StreamDesc sv = su;
+    sv.role = 1;
+    sv.step_mode = d.estimator == ZO_EST_LOZO ? STEP_WINDOW : STEP_CURRENT;
+    sv.n = (uint64_t)(m.n * d.rank);
+    sv.out_off = (uint64_t)m.v_off;
+    c->streamsV.push_back(sv);
+  }
+  build_sampler_plan(c.get(), c->planU, c->streamsU);
+  build_sampler_plan(c.get(), c->planV, c->streamsV);
+  ZO_CUDA_TRY(cudaDeviceSynchronize());
+  *out = c.release();
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_destroy(zo_ctx* c) {
+  ZO_API_BEGIN
+  if (c) {
+    cudaStreamSynchronize(c->st);
+    delete c;
+  }
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_set_stream(zo_ctx* c, void* s) {
+  c->st = static_cast<cudaStream_t>(s);
+  return ZO_OK;
+}
+
+int zo_synchronize(zo_ctx* c) {
+  ZO_API_BEGIN
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  ZO_CUDA_TRY(cudaGetLastError());
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_num_matrices(const zo_ctx* c) { return (int)c->mats.size(); }
+
+int zo_matrix_info(const zo_ctx* c, int i, char* lid, int cap, int64_t* rows, int64_t* cols) {
+  if (i < 0 || i >= (int)c->mats.size()) return ZO_ERR_INPUT;
+  const Matrix& m = c->mats[i];
+  if (lid && cap > 0) {
+    std::strncpy(lid, m.lid.c_str(), cap - 1);
+    lid[cap - 1] = 0;
+  }
+  if (rows) *rows = m.m;
+  if (cols) *cols = m.n;
+  return ZO_OK;
+}
+
+int zo_device_bytes(const zo_ctx* c, uint64_t* bytes) {
+  *bytes = c->mem.bytes;
+  return ZO_OK;
+}
+
+int zo_init_params(zo_ctx* c, uint64_t init_seed, double init_scale) {
+  ZO_API_BEGIN
+  // one plan per matrix (bounded chunk arrays), Role.INIT at step 0 (model.py:94-96)
+  for (auto& m : c->mats) {
+    std::vector<StreamDesc> sd(1);
+    sd[0].lid_hash = m.lid_hash;
+    sd[0].role = 4;
+    sd[0].step_mode = STEP_FIXED;
+    sd[0].fixed_step = 0;
+    sd[0].n = (uint64_t)(m.m * m.n);
+    sd[0].out_off = 0;
+    sd[0].scale = init_scale;
+    sd[0].apply_scale = 1;
+    sd[0].seed_override = 1;
+    sd[0].seed_value = init_seed;
+    DevAlloc tmp;
+    SamplerPlan P;
+    // temporary plan (freed after the matrix is done)
+    int64_t nch = (int64_t)sampler_chunks_for(sd[0].n);
+    sd[0].chunk_begin = 0;
+    sd[0].n_chunks = (uint64_t)nch;
+    P.S = 1;
+    P.C = nch;
+    P.d_streams = tmp.get<StreamDesc>(1);
+    P.d_chunk_stream = tmp.get<uint32_t>(nch);  // zeros: every chunk belongs to stream 0
+    P.d_keys = tmp.get<uint64_t>(2);
+    P.d_spec = tmp.get<uint64_t>(nch);
+    P.d_exit = tmp.get<uint64_t>(nch);
+    P.d_count = tmp.get<uint32_t>(nch);
+    P.d_offset = tmp.get<uint64_t>(nch);
+    P.d_flags = c->flags;
+    ZO_CUDA_TRY(cudaMemcpyAsync(P.d_streams, sd.data(), sizeof(StreamDesc), cudaMemcpyHostToDevice, c->st));
+    sampler_launch(P, init_seed, c->d_step, 1, m.W64, c->st);
+    refresh_shadow(c, m);
+    ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  }
+  ZO_CUDA_TRY(cudaGetLastError());
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_upload_matrix(zo_ctx* c, const char* lid, const double* host, int64_t rows, int64_t cols) {
+  ZO_API_BEGIN
+  Matrix& m = find(c, lid);
+  check(rows == m.m && cols == m.n, ZO_ERR_DIMENSION, "matrix shape mismatch for " + m.lid);
+  ZO_CUDA_TRY(cudaMemcpyAsync(m.W64, host, (size_t)(rows * cols) * 8, cudaMemcpyHostToDevice, c->st));
+  refresh_shadow(c, m);
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_download_matrix(zo_ctx* c, const char* lid, double* host, int64_t rows, int64_t cols) {
+  ZO_API_BEGIN
+  Matrix& m = find(c, lid);
+  check(rows == m.m && cols == m.n, ZO_ERR_DIMENSION, "matrix shape mismatch for " + m.lid);
+  ZO_CUDA_TRY(cudaMemcpyAsync(host, m.W64, (size_t)(rows * cols) * 8, cudaMemcpyDeviceToHost, c->st));
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_upload_vector(zo_ctx* c, const char* lid, const double* host, int64_t n) {
+  ZO_API_BEGIN
+  check(n == c->d.dim, ZO_ERR_DIMENSION, "vector length must equal dim");
+  std::string s(lid);
+  float* dst = nullptr;
+  if (s == "ln_f.scale") dst = c->lnfg;
+  else if (s == "ln_f.shift") dst = c->lnfb;
+  else {
+    int l = -1;
+    char which[16] = {0};
+    if (std::sscanf(lid, "blk%d.%15s", &l, which) == 2 && l >= 0 && l < c->d.n_layers) {
+      std::string w(which);
+      if (w == "ln1.scale") dst = c->ln1g[l];
+      else if (w == "ln1.shift") dst = c->ln1b[l];
+      else if (w == "ln2.scale") dst = c->ln2g[l];
+      else if (w == "ln2.shift") dst = c->ln2b[l];
+    }
+  }
+  check(dst != nullptr, ZO_ERR_INPUT, "unknown vector id " + s);
+  std::vector<float> f(n);
+  for (int64_t i = 0; i < n; ++i) f[i] = (float)host[i];
+  ZO_CUDA_TRY(cudaMemcpy(dst, f.data(), n * 4, cudaMemcpyHostToDevice));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_sample_u(zo_ctx* c, uint64_t seed, uint64_t step) {
+  ZO_API_BEGIN
+  set_step(c, step);
+  sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_sample_v(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu) {
+  ZO_API_BEGIN
+  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  set_step(c, step);
+  sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
+  write_vext_all(c);
+  c->v_window = c->d.estimator == ZO_EST_LOZO ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_sample_stream(zo_ctx* c, uint64_t seed, uint64_t step, uint64_t lid_hash, int32_t role, int64_t n,
+                     double* host_out) {
+  ZO_API_BEGIN
+  check(n >= 1, ZO_ERR_DIMENSION, "gaussian sample needs n >= 1");
+  // ctx may be NULL: sample on the current device / default stream
+  cudaStream_t st = c ? c->st : (cudaStream_t)0;
+  DevAlloc tmp;
+  unsigned* flags = c ? c->flags : tmp.get<unsigned>(4);
+  uint64_t* dstep = c ? c->d_step : tmp.get<uint64_t>(1);
+  std::vector<StreamDesc> sd(1);
+  sd[0].lid_hash = lid_hash;
+  sd[0].role = (uint32_t)role;
+  sd[0].step_mode = STEP_FIXED;
+  sd[0].fixed_step = step;
+  sd[0].n = (uint64_t)n;
+  sd[0].scale = 1.0;
+  SamplerPlan P;
+  int64_t nch = (int64_t)sampler_chunks_for((uint64_t)n);
+  sd[0].n_chunks = (uint64_t)nch;
+  P.S = 1;
+  P.C = nch;
+  P.d_streams = tmp.get<StreamDesc>(1);
+  P.d_chunk_stream = tmp.get<uint32_t>(nch);
+  P.d_keys = tmp.get<uint64_t>(2);
+  P.d_spec = tmp.get<uint64_t>(nch);
+  P.d_exit = tmp.get<uint64_t>(nch);
+  P.d_count = tmp.get<uint32_t>(nch);
+  P.d_offset = tmp.get<uint64_t>(nch);
+  P.d_flags = flags;
+  double* out = tmp.get<double>((size_t)n);
+  ZO_CUDA_TRY(cudaMemcpyAsync(P.d_streams, sd.data(), sizeof(StreamDesc), cudaMemcpyHostToDevice, st));
+  sampler_launch(P, seed, dstep, 1, out, st);
+  ZO_CUDA_TRY(cudaMemcpyAsync(host_out, out, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+  ZO_CUDA_TRY(cudaStreamSynchronize(st));
+  ZO_CUDA_TRY(cudaGetLastError());
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_slot_count(const zo_ctx* c, int32_t which, int64_t* count) {
+  if (which < 0 || which > 2) return ZO_ERR_INPUT;
+  *count = which == 1 ? c->sv : c->su;
+  return ZO_OK;
+}
+
+static double* slot_ptr(zo_ctx* c, int which) { return which == 0 ? c->U : which == 1 ? c->V : c->A; }
+
+int zo_get_slot(zo_ctx* c, int32_t which, double* host, int64_t count) {
+  ZO_API_BEGIN
+  check(which >= 0 && which <= 2, ZO_ERR_INPUT, "bad slot id");
+  check(count == (which == 1 ? c->sv : c->su), ZO_ERR_DIMENSION, "slot arena size mismatch");
+  ZO_CUDA_TRY(cudaMemcpyAsync(host, slot_ptr(c, which), (size_t)count * 8, cudaMemcpyDeviceToHost, c->st));
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_set_slot(zo_ctx* c, int32_t which, const double* host, int64_t count) {
+  ZO_API_BEGIN
+  check(which >= 0 && which <= 2, ZO_ERR_INPUT, "bad slot id");
+  check(count == (which == 1 ? c->sv : c->su), ZO_ERR_DIMENSION, "slot arena size mismatch");
+  ZO_CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, which), host, (size_t)count * 8, cudaMemcpyHostToDevice, c->st));
+  if (which == 1) write_vext_all(c);
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_sampler_flags(zo_ctx* c, uint32_t flags[3]) {
+  ZO_API_BEGIN
+  unsigned f[4];
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  ZO_CUDA_TRY(cudaMemcpy(f, c->flags, sizeof(f), cudaMemcpyDeviceToHost));
+  flags[0] = f[0];
+  flags[1] = f[1];
+  flags[2] = f[2];
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_prepare_probe(zo_ctx* c, double eps, int32_t sign_mode) {
+  ZO_API_BEGIN
+  // sign_mode 0: P+- = A +- eps*scale*U (probe pair); 1: P = A (no probe, sign 0)
+  const double scale = c->d.estimator == ZO_EST_FACTORIZED ? 1.0 / std::sqrt((double)c->r) : 1.0;
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, sign_mode == 0 ? eps : 0.0, scale, c->Pp, c->Pm, c->st);
+  c->probe_eps = eps;
+  c->probe_scale = scale;
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_score(zo_ctx* c, const int32_t* tokens, const int32_t* gold, int32_t B, int32_t nsign, double* nll_out) {
+  ZO_API_BEGIN
+  check(nsign == 1 || nsign == 2, ZO_ERR_INPUT, "nsign must be 1 or 2");
+  check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
+  stage_batch(c, tokens, gold, B, nsign);
+  do_score(c, B, nsign);
+  if (nll_out) {
+    ZO_CUDA_TRY(cudaMemcpyAsync(nll_out, c->nll, (size_t)nsign * B * 8, cudaMemcpyDeviceToHost, c->st));
+    ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  }
+  ZO_CUDA_TRY(cudaGetLastError());
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_coefficient(zo_ctx* c, int32_t B, double eps, double lr, int32_t divide_by_r, double* out4) {
+  ZO_API_BEGIN
+  launch_coefficient(c->nll, B, eps, lr, divide_by_r, c->r, c->out4, c->abort_flag, c->st);
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->h_out4, c->out4, 32, cudaMemcpyDeviceToHost, c->st));
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  if (out4) std::memcpy(out4, c->h_out4, 32);
+  if (!std::isfinite(c->h_out4[0]) || !std::isfinite(c->h_out4[1]))
+    throw Error(ZO_ERR_ABORT, "non-finite paired loss; step not applied");
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_set_coefficient(zo_ctx* c, const double* out4) {
+  ZO_API_BEGIN
+  std::memcpy(c->h_out4, out4, 32);
+  const unsigned zero = 0;
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->out4, c->h_out4, 32, cudaMemcpyHostToDevice, c->st));
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->abort_flag, &zero, 4, cudaMemcpyHostToDevice, c->st));
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_update_u(zo_ctx* c) {
+  ZO_API_BEGIN
+  launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
+  c->a_dirty = true;
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_fold(zo_ctx* c) {
+  ZO_API_BEGIN
+  fold_all(c);
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_update_dense(zo_ctx* c, double lr) {
+  ZO_API_BEGIN
+  // alpha = -(lr*c) * (1/sqrt(r)) as zo_engine.py:450 computes it (host copy of c)
+  const double cc = c->h_out4[2];
+  const double alpha = (-(lr * cc)) * (1.0 / std::sqrt((double)c->r));
+  for (auto& m : c->mats)
+    launch_fold(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, alpha, m.W16,
+                m.kind == K_EMBED ? (int)m.n : m.ldw, m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_step(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr, int32_t divide_by_r,
+            const int32_t* tokens, const int32_t* gold, int32_t B, double* out4) {
+  ZO_API_BEGIN
+  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  set_step(c, step);
+  stage_batch(c, tokens, gold, B, 1);
+  ZO_CUDA_TRY(cudaEventRecord(c->ev[0], c->st));
+  const int64_t wstart = lozo ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
+  if (!lozo || wstart != c->v_window) {
+    // a window start with unfolded mass: fold it first (the reference freezes it
+    // into an update slot, zo_engine.py:395-398 -- value-neutral up to rounding)
+    if (lozo && c->a_dirty) fold_all(c);
+    sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
+    write_vext_all(c);
+    c->v_window = wstart;
+  }
+  sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  const double scale = lozo ? 1.0 : 1.0 / std::sqrt((double)c->r);
+  launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, eps, scale, c->Pp, c->Pm, c->st);
+  ZO_CUDA_TRY(cudaEventRecord(c->ev[1], c->st));
+  do_score(c, B, 2);
+  launch_coefficient(c->nll, B, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
+  ZO_CUDA_TRY(cudaEventRecord(c->ev[2], c->st));
+  if (lozo) {
+    launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
+    c->a_dirty = true;
+  }
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->h_out4, c->out4, 32, cudaMemcpyDeviceToHost, c->st));
+  ZO_CUDA_TRY(cudaEventRecord(c->ev[3], c->st));
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  ZO_CUDA_TRY(cudaGetLastError());
+  cudaEventElapsedTime(&c->last_ms[0], c->ev[0], c->ev[1]);
+  cudaEventElapsedTime(&c->last_ms[1], c->ev[1], c->ev[2]);
+  cudaEventElapsedTime(&c->last_ms[2], c->ev[2], c->ev[3]);
+  if (out4) std::memcpy(out4, c->h_out4, 32);
+  if (!std::isfinite(c->h_out4[0]) || !std::isfinite(c->h_out4[1]))
+    throw Error(ZO_ERR_ABORT, "non-finite paired loss; step not applied");
+  if (!lozo) {
+    const double cc = c->h_out4[2];
+    const double alpha = (-(lr * cc)) * (1.0 / std::sqrt((double)c->r));
+    for (auto& m : c->mats)
+      launch_fold(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, alpha, m.W16,
+                  m.kind == K_EMBED ? (int)m.n : m.ldw, m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
+  }
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_last_step_ms(zo_ctx* c, float ms[3]) {
+  for (int i = 0; i < 3; ++i) ms[i] = c->last_ms[i];
+  return ZO_OK;
+}
+
+uint64_t zo_fnv1a64(const void* data, uint64_t nbytes, uint64_t h) { return fnv(data, (size_t)nbytes, h); }
+
+uint64_t zo_digest_chain(const char* const* lids, const double* arena, const int64_t* offsets, const int64_t* counts,
+                         int32_t n, uint64_t h) {
+  for (int32_t i = 0; i < n; ++i) {
+    h = fnv(lids[i], std::strlen(lids[i]), h);
+    h = fnv(arena + offsets[i], (size_t)counts[i] * 8, h);
+  }
+  return h;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ test hooks
+extern "C" int zo_test_gemm(int32_t M, int32_t N, int32_t K, int32_t lda, int32_t epi, int32_t bf16,
+                            const uint16_t* A_host, const uint16_t* B_host, float* C_host) {
+  ZO_API_BEGIN
+  // D[M, N] = A[M, K] B[N, K]^T through the production GEMM (K2); epi in
+  // {STORE16, GELU16, RESID32, STORE32}; 16-bit outputs are widened to fp32.
+  check(lda >= K && lda % 8 == 0, ZO_ERR_DIMENSION, "lda must be >= K and a multiple of 8");
+  int dev = 0;
+  ZO_CUDA_TRY(cudaGetDevice(&dev));
+  int sms = 148;
+  ZO_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DevAlloc m;
+  const int Mpad = (int)ceil_div(M, 128) * 128;
+  uint16_t* A = m.get<uint16_t>((size_t)Mpad * lda);
+  uint16_t* B = m.get<uint16_t>((size_t)N * lda);
+  ZO_CUDA_TRY(cudaMemcpy(A, A_host, (size_t)M * lda * 2, cudaMemcpyHostToDevice));
+  ZO_CUDA_TRY(cudaMemcpy(B, B_host, (size_t)N * lda * 2, cudaMemcpyHostToDevice));
+  const bool out16 = epi == EPI_STORE16 || epi == EPI_GELU16;
+  void* C = out16 ? (void*)m.get<uint16_t>((size_t)M * N) : (void*)m.get<float>((size_t)M * N);
+  if (epi == EPI_RESID32) ZO_CUDA_TRY(cudaMemcpy(C, C_host, (size_t)M * N * 4, cudaMemcpyHostToDevice));
+  GemmDesc g;
+  gemm_plan(g, A, M, lda, B, N, lda, K, epi, bf16 != 0, C, N, sms);
+  gemm_launch(g, 0);
+  ZO_CUDA_TRY(cudaDeviceSynchronize());
+  ZO_CUDA_TRY(cudaGetLastError());
+  if (out16) {
+    std::vector<uint16_t> h((size_t)M * N);
+    ZO_CUDA_TRY(cudaMemcpy(h.data(), C, h.size() * 2, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < h.size(); ++i) {
+      uint32_t bits;
+      if (bf16) {
+        bits = (uint32_t)h[i] << 16;
+      } else {
+        // fp16 -> fp32
+        const uint32_t s = (h[i] >> 15) & 1, e = (h[i] >> 10) & 0x1f, f = h[i] & 0x3ff;
+        if (e == 0) {
+          float v = std::ldexp((float)f, -24);
+          C_host[i] = s ? -v : v;
+          continue;
+        }
+        bits = (s << 31) | ((e == 31 ? 255 : e - 15 + 127) << 23) | (f << 13);
+      }
+      std::memcpy(&C_host[i], &bits, 4);
+    }
+  } else {
+    ZO_CUDA_TRY(cudaMemcpy(C_host, C, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
+  }
+  return ZO_OK;
+  ZO_API_END
+}

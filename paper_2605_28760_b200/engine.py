@@ -1,0 +1,225 @@
+"""ZoEngine -- one device-resident LoZO/MeZO model replica (one libzob200 ctx).
+
+This is the Level-B engine behind the reference-shaped API in
+``zo_engine.py`` / ``runtime.py``: parameters (float64 master + 16-bit
+tensor-core shadows), the U/V/A slot arenas and all activations live in HBM;
+the host only stages token ids and reads back (L+, L-, c, beta).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+from .errors import ConfigError, DimensionError
+
+PRECISIONS = {"fp16": _lib.PREC_FP16, "bf16": _lib.PREC_BF16}
+# the reference's precision strings run on the tensor-core path
+ALIASES = {"real64": "fp16", "real32": "fp16"}
+ESTIMATORS = {"lozo_lazy": _lib.EST_LOZO, "factorized_sqrt_r": _lib.EST_FACTORIZED}
+
+U, V, A = 0, 1, 2
+
+
+def resolve_precision(precision: str) -> str:
+    p = ALIASES.get(precision, precision)
+    if p not in PRECISIONS:
+        raise ConfigError(f"unknown precision {precision!r}")
+    return p
+
+
+class ZoEngine:
+    def __init__(self, vocab: int, dim: int, n_layers: int, n_heads: int, prompt_len: int, *,
+                 opt_len: int = 1, max_batch: int = 16, rank: int = 2, estimator: str = "lozo_lazy",
+                 precision: str = "fp16", device: int = 0):
+        if estimator not in ESTIMATORS:
+            raise ConfigError(f"estimator {estimator!r} has no device engine")
+        self.precision = resolve_precision(precision)
+        self.estimator = estimator
+        self.rank = rank
+        self.vocab, self.dim, self.n_layers, self.n_heads = vocab, dim, n_layers, n_heads
+        self.prompt_len, self.opt_len, self.max_batch = prompt_len, opt_len, max_batch
+        self.T = prompt_len + opt_len
+        desc = _lib.ZoModelDesc(vocab, dim, n_layers, n_heads, prompt_len, opt_len, max_batch, rank,
+                                ESTIMATORS[estimator], PRECISIONS[self.precision], device)
+        h = ctypes.c_void_p()
+        check(lib().zo_create(ctypes.byref(h), ctypes.byref(desc)))
+        self._h = h
+        n = lib().zo_num_matrices(h)
+        buf = ctypes.create_string_buffer(128)
+        rows, cols = ctypes.c_int64(), ctypes.c_int64()
+        self.lids: list[str] = []
+        self.shapes: dict[str, tuple[int, int]] = {}
+        for i in range(n):
+            check(lib().zo_matrix_info(h, i, buf, 128, ctypes.byref(rows), ctypes.byref(cols)))
+            lid = buf.value.decode()
+            self.lids.append(lid)
+            self.shapes[lid] = (rows.value, cols.value)
+        self.u_off, self.v_off = {}, {}
+        su = sv = 0
+        for lid in self.lids:
+            m, nn = self.shapes[lid]
+            self.u_off[lid], self.v_off[lid] = su, sv
+            su += m * rank
+            sv += nn * rank
+        self.su, self.sv = su, sv
+        self._lid_c = (ctypes.c_char_p * n)(*[l.encode() for l in self.lids])
+        self.last_out4 = np.zeros(4)
+
+    # ---------------------------------------------------------------- lifecycle
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            lib().zo_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self) -> None:
+        check(lib().zo_synchronize(self._h))
+
+    def set_stream(self, stream_ptr: int) -> None:
+        check(lib().zo_set_stream(self._h, ctypes.c_void_p(stream_ptr)))
+
+    @property
+    def device_bytes(self) -> int:
+        b = ctypes.c_uint64()
+        check(lib().zo_device_bytes(self._h, ctypes.byref(b)))
+        return b.value
+
+    # ---------------------------------------------------------------- parameters
+    def init_params(self, init_seed: int, init_scale: float) -> None:
+        check(lib().zo_init_params(self._h, init_seed, float(init_scale)))
+
+    def upload(self, params) -> None:
+        for lid, w in params.items():
+            w = np.ascontiguousarray(w, dtype=np.float64)
+            if w.ndim == 2:
+                check(lib().zo_upload_matrix(self._h, lid.encode(), w.ctypes.data, w.shape[0], w.shape[1]))
+            else:
+                check(lib().zo_upload_vector(self._h, lid.encode(), w.ctypes.data, w.shape[0]))
+
+    def download(self, lid: str) -> np.ndarray:
+        m, n = self.shapes[lid]
+        out = np.empty((m, n), dtype=np.float64)
+        check(lib().zo_download_matrix(self._h, lid.encode(), out.ctypes.data, m, n))
+        return out
+
+    # ---------------------------------------------------------------- directions / slots
+    def sample_u(self, seed: int, step: int) -> None:
+        check(lib().zo_sample_u(self._h, seed, step))
+
+    def sample_v(self, seed: int, step: int, nu: int) -> None:
+        check(lib().zo_sample_v(self._h, seed, step, nu))
+
+    def get_slot(self, which: int) -> np.ndarray:
+        n = self.sv if which == V else self.su
+        out = np.empty(n, dtype=np.float64)
+        check(lib().zo_get_slot(self._h, which, out.ctypes.data, n))
+        return out
+
+    def set_slot(self, which: int, arena: np.ndarray) -> None:
+        a = np.ascontiguousarray(arena, dtype=np.float64).reshape(-1)
+        n = self.sv if which == V else self.su
+        if a.size != n:
+            raise DimensionError(f"slot arena has {a.size} values, expected {n}")
+        check(lib().zo_set_slot(self._h, which, a.ctypes.data, n))
+
+    def split(self, which: int, arena: np.ndarray) -> dict[str, np.ndarray]:
+        out = {}
+        for lid in self.lids:
+            m, n = self.shapes[lid]
+            rows = n if which == V else m
+            off = (self.v_off if which == V else self.u_off)[lid]
+            out[lid] = arena[off: off + rows * self.rank].reshape(rows, self.rank)
+        return out
+
+    def join(self, which: int, mats: dict) -> np.ndarray:
+        return np.concatenate([np.ascontiguousarray(mats[l], dtype=np.float64).reshape(-1) for l in self.lids])
+
+    def digest(self, which: int, arena: np.ndarray | None = None) -> int:
+        """Chained FNV over (lid, factor) in sorted id order (zo_engine.py:220-261)."""
+        if arena is None:
+            arena = self.get_slot(which)
+        arena = np.ascontiguousarray(arena, dtype=np.float64)
+        offs = self.v_off if which == V else self.u_off
+        rows = [(self.shapes[l][1] if which == V else self.shapes[l][0]) * self.rank for l in self.lids]
+        off_c = (ctypes.c_int64 * len(self.lids))(*[offs[l] for l in self.lids])
+        cnt_c = (ctypes.c_int64 * len(self.lids))(*rows)
+        return int(lib().zo_digest_chain(self._lid_c, arena.ctypes.data, off_c, cnt_c, len(self.lids),
+                                         0xCBF29CE484222325))
+
+    def sampler_flags(self) -> tuple[int, int, int]:
+        f = (ctypes.c_uint32 * 3)()
+        check(lib().zo_sampler_flags(self._h, f))
+        return int(f[0]), int(f[1]), int(f[2])
+
+    # ---------------------------------------------------------------- scoring / update
+    def _tokens(self, tokens, gold, nsign_gold):
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        if tok.ndim != 2 or tok.shape[1] != self.T:
+            raise DimensionError(f"tokens must be [B, {self.T}], got {tok.shape}")
+        g = np.ascontiguousarray(gold, dtype=np.int32).reshape(nsign_gold, tok.shape[0], self.opt_len)
+        return tok, g
+
+    def prepare_probe(self, epsilon: float, sign_mode: int = 0) -> None:
+        check(lib().zo_prepare_probe(self._h, float(epsilon), sign_mode))
+
+    def score(self, tokens, gold, nsign: int = 2) -> np.ndarray:
+        tok, g = self._tokens(tokens, gold, nsign)
+        B = tok.shape[0]
+        out = np.empty(nsign * B, dtype=np.float64)
+        check(lib().zo_score(self._h, tok.ctypes.data, g.ctypes.data, B, nsign, out.ctypes.data))
+        return out.reshape(nsign, B)
+
+    def coefficient(self, B: int, epsilon: float, lr: float, divide_by_r: bool) -> np.ndarray:
+        out = np.empty(4)
+        check(lib().zo_coefficient(self._h, B, float(epsilon), float(lr), int(divide_by_r), out.ctypes.data))
+        return out
+
+    def set_coefficient(self, out4) -> None:
+        o = np.ascontiguousarray(out4, dtype=np.float64)
+        check(lib().zo_set_coefficient(self._h, o.ctypes.data))
+
+    def update_u(self) -> None:
+        check(lib().zo_update_u(self._h))
+
+    def fold(self) -> None:
+        check(lib().zo_fold(self._h))
+
+    def update_dense(self, lr: float) -> None:
+        check(lib().zo_update_dense(self._h, float(lr)))
+
+    def step(self, seed: int, step: int, nu: int, epsilon: float, lr: float, divide_by_r: bool,
+             tokens, gold) -> np.ndarray:
+        tok, g = self._tokens(tokens, gold, 1)
+        out = self.last_out4
+        check(lib().zo_step(self._h, seed, step, nu, float(epsilon), float(lr), int(divide_by_r),
+                            tok.ctypes.data, g.ctypes.data, tok.shape[0], out.ctypes.data))
+        return out.copy()
+
+    def last_step_ms(self) -> tuple[float, float, float]:
+        f = (ctypes.c_float * 3)()
+        check(lib().zo_last_step_ms(self._h, f))
+        return float(f[0]), float(f[1]), float(f[2])
+
+
+def test_gemm(A: np.ndarray, B: np.ndarray, epi: int = 3, bf16: bool = False, C: np.ndarray | None = None,
+              lda: int | None = None) -> np.ndarray:
+    """Run the production tcgen05 GEMM on host arrays (A [M,K], B [N,K] as
+    float16/bfloat16 bit patterns in uint16); returns fp32 [M, N]."""
+    M, K = A.shape
+    N = B.shape[0]
+    lda = lda or K
+    Ap = np.zeros((M, lda), dtype=np.uint16)
+    Ap[:, :K] = A
+    Bp = np.zeros((N, lda), dtype=np.uint16)
+    Bp[:, :K] = B
+    out = np.zeros((M, N), dtype=np.float32) if C is None else np.ascontiguousarray(C, dtype=np.float32).copy()
+    check(lib().zo_test_gemm(M, N, K, lda, epi, int(bf16), Ap.ctypes.data, Bp.ctypes.data, out.ctypes.data))
+    return out

@@ -1,0 +1,49 @@
+"""Device kernels vs references: GEMM vs torch fp32 on the same 16-bit
+operands; sampler vs the reference's golden streams (bit-exact)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _h(x, bf16):
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32))
+    t = t.to(torch.bfloat16 if bf16 else torch.float16)
+    return t, t.view(torch.int16).numpy().view(np.uint16)
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 128), (300, 200, 96), (1024, 768, 832),
+                                   (2048, 640, 384), (32, 50272 // 8, 64)])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemm_vs_torch(M, N, K, epi, bf16):
+    import torch
+    from paper_2605_28760_b200.engine import test_gemm
+    rng = np.random.default_rng(M * 7 + N + K + epi)
+    ta, a16 = _h(rng.standard_normal((M, K)), bf16)
+    tb, b16 = _h(rng.standard_normal((N, K)) * 0.05, bf16)
+    ref = ta.float() @ tb.float().T
+    C0 = rng.standard_normal((M, N)).astype(np.float32) if epi == 2 else None
+    if epi == 1:
+        ref = torch.nn.functional.gelu(ref, approximate="tanh")
+    if epi == 2:
+        ref = ref + torch.from_numpy(C0)
+    if epi in (0, 1):
+        ref = ref.to(torch.bfloat16 if bf16 else torch.float16).float()
+    got = test_gemm(a16, b16, epi=epi, bf16=bf16, C=C0)
+    tol = 2e-2 if (epi in (0, 1) and bf16) else 4e-3
+    np.testing.assert_allclose(got, ref.numpy(), rtol=tol, atol=tol)
+
+
+def test_sampler_golden_streams(golden_dir):
+    from paper_2605_28760_b200.numerics import Role, StreamKey, digest_array, digest_hex, sample_gaussian
+    with open(os.path.join(golden_dir, "streams.json")) as f:
+        streams = json.load(f)
+    for s in streams:
+        x = sample_gaussian(StreamKey(s["seed"], s["step"], s["layer_id"], Role(s["role"])), s["rows"], s["cols"])
+        assert digest_hex(digest_array(x)) == s["digest"], (s["layer_id"], s["role"], s["rows"], s["cols"])
+        assert [float(v).hex() for v in x.reshape(-1)[:6]] == s["head"]

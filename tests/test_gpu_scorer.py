@@ -1,0 +1,118 @@
+"""Scorer / step parity on the GPU against the reference's golden fixtures.
+
+Tolerances (fp16 tensor-core operands, fp32 accumulate):
+per-example NLL |d| <= 2e-2, paired mean losses |dL+-| <= 1e-2; U/V digests and
+the float64 init are bit-exact.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import reference as R
+
+pytestmark = pytest.mark.gpu
+
+NLL_TOL = {"fp16": 2e-2, "bf16": 8e-2}
+LOSS_TOL = {"fp16": 1e-2, "bf16": 4e-2}
+
+
+def _load(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        return json.load(f)
+
+
+def _engine(g, precision="fp16", rank=None, estimator="lozo_lazy", max_batch=None):
+    from paper_2605_28760_b200.engine import ZoEngine
+    m = g["model"]
+    return ZoEngine(m["vocab"], m["dim"], m["n_layers"], m["n_heads"], m["prompt_len"], opt_len=1,
+                    max_batch=max_batch or 16, rank=rank or g.get("rank", 2), estimator=estimator,
+                    precision=precision)
+
+
+def _params_digest(eng, cfg):
+    params = {lid: eng.download(lid) for lid in eng.lids}
+    for i in range(cfg.n_layers):
+        for ln in ("ln1", "ln2"):
+            params[f"blk{i}.{ln}.scale"] = np.ones(cfg.dim)
+            params[f"blk{i}.{ln}.shift"] = np.zeros(cfg.dim)
+    params["ln_f.scale"] = np.ones(cfg.dim)
+    params["ln_f.shift"] = np.zeros(cfg.dim)
+    return R.params_digest(params)
+
+
+@pytest.mark.parametrize("name", ["micro", "small"])
+def test_init_params_bit_exact(golden_dir, name):
+    g = _load(golden_dir, f"forward_{name}.json")
+    cfg = R.ModelCfg(**g["model"])
+    eng = _engine(g)
+    eng.init_params(cfg.init_seed, cfg.init_scale)
+    assert _params_digest(eng, cfg) == g["params_digest"]
+
+
+@pytest.mark.parametrize("precision", ["fp16", "bf16"])
+@pytest.mark.parametrize("name", ["micro", "small"])
+def test_forward_nll_vs_reference(golden_dir, name, precision):
+    g = _load(golden_dir, f"forward_{name}.json")
+    cfg = R.ModelCfg(**g["model"])
+    eng = _engine(g, precision)
+    eng.init_params(cfg.init_seed, cfg.init_scale)
+    step, r = g["step"], g["rank"]
+    eng.sample_v(g["zseed"], step, 50)
+    eng.sample_u(g["zseed"], step)
+    A = {lid: g["a_scale"] * R.gaussian(g["a_seed"], step, lid, R.ROLE_U, eng.shapes[lid][0], r) for lid in eng.lids}
+    eng.set_slot(2, eng.join(2, A))
+    # the device U/V must be the reference's streams
+    U = eng.split(0, eng.get_slot(0))
+    for lid in eng.lids[:3]:
+        np.testing.assert_array_equal(U[lid], R.gaussian(g["zseed"], step, lid, R.ROLE_U, eng.shapes[lid][0], r))
+    tokens = np.asarray(g["tokens"])
+    gold = tokens[:, cfg.prompt_len:]
+    eng.prepare_probe(g["epsilon"], 0)
+    nll = eng.score(tokens, gold, nsign=2)
+    eng.prepare_probe(g["epsilon"], 1)
+    nll0 = eng.score(tokens, gold, nsign=1)[0]
+    ref_p, ref_m, ref_0 = (np.array(g["nll"][f"real64:{s}"]) for s in (1, -1, 0))
+    tol = NLL_TOL[precision]
+    np.testing.assert_allclose(nll[0], ref_p, atol=tol, rtol=0)
+    np.testing.assert_allclose(nll[1], ref_m, atol=tol, rtol=0)
+    np.testing.assert_allclose(nll0, ref_0, atol=tol, rtol=0)
+    # the probe difference is what the estimator consumes: compare L+ - L-
+    d_ref = R.canonical_mean(ref_p) - R.canonical_mean(ref_m)
+    d_got = R.canonical_mean(nll[0]) - R.canonical_mean(nll[1])
+    assert abs(d_got - d_ref) <= max(0.05 * abs(d_ref), 2e-4), (d_got, d_ref)
+
+
+def _traj(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        lines = [json.loads(l) for l in f if l.strip()]
+    return lines[0], [l for l in lines if l["record"] == "step"], lines[-1]
+
+
+@pytest.mark.parametrize("name", ["micro_lozo", "small_lozo"])
+def test_device_step_trajectory(golden_dir, name):
+    """zo_step (fused device lozo_step) vs the reference's run_serving_path trajectory."""
+    from paper_2605_28760_b200.engine import U as SU, V as SV
+    from paper_2605_28760_b200.numerics import digest_hex
+    h, recs, fin = _traj(golden_dir, f"traj_{name}.jsonl")
+    cfg = R.ModelCfg(**h["model"])
+    z = R.ZoCfg(**h["zo"])
+    splits = R.generate_task(R.TaskCfg(**h["task"]))
+    eng = _engine({"model": h["model"], "rank": z.rank}, max_batch=z.batch_size)
+    eng.init_params(cfg.init_seed, cfg.init_scale)
+    signs = 0
+    for t, rec in enumerate(recs):
+        p, gl, idx = R.sample_minibatch(splits, "train", z.seed, t, z.batch_size)
+        gold = np.array([[cfg.vocab - 2], [cfg.vocab - 1]])[gl]
+        tokens = np.concatenate([p, gold], axis=1)
+        out = eng.step(z.seed, t, z.nu, z.epsilon, z.learning_rate, z.divide_by_r, tokens, gold)
+        assert digest_hex(eng.digest(SU)) == rec["u_digest"]
+        assert digest_hex(eng.digest(SV)) == rec["v_digest"]
+        assert abs(out[0] - rec["loss_plus"]) <= LOSS_TOL["fp16"]
+        assert abs(out[1] - rec["loss_minus"]) <= LOSS_TOL["fp16"]
+        signs += np.sign(out[0] - out[1]) == np.sign(rec["loss_plus"] - rec["loss_minus"])
+        if (t + 1) % z.nu == 0:
+            eng.fold()
+    assert signs >= 0.9 * len(recs)
+    assert eng.sampler_flags()[0] == 0
