@@ -245,7 +245,9 @@ __global__ void __launch_bounds__(192, 1)
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
         const int col0 = n0 + c;
         if (!row_ok || col0 >= p.N) continue;
-        const bool full = col0 + 32 <= p.N;
+        const size_t lin = (size_t)row * p.ldo + col0;
+        constexpr int VEC = (EPI == EPI_STORE16 || EPI == EPI_GELU16) ? 8 : 4;
+        const bool full = col0 + 32 <= p.N && (lin % VEC) == 0;
         if constexpr (EPI == EPI_STORE16 || EPI == EPI_GELU16) {
           if constexpr (EPI == EPI_GELU16) {
 #pragma unroll
@@ -263,9 +265,12 @@ __global__ void __launch_bounds__(192, 1)
               reinterpret_cast<uint4*>(o)[j] = w;
             }
           } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) {
-              uint32_t pk = pack2<BF16>(v[i], 0.f);
-              o[i] = (uint16_t)(pk & 0xffff);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (col0 + i < p.N) {
+                uint32_t pk = pack2<BF16>(v[i], 0.f);
+                o[i] = (uint16_t)(pk & 0xffff);
+              }
             }
           }
         } else {
@@ -284,11 +289,14 @@ __global__ void __launch_bounds__(192, 1)
               reinterpret_cast<float4*>(o)[j] = w;
             }
           } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) {
-              if constexpr (EPI == EPI_RESID32)
-                o[i] += v[i];
-              else
-                o[i] = v[i];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (col0 + i < p.N) {
+                if constexpr (EPI == EPI_RESID32)
+                  o[i] += v[i];
+                else
+                  o[i] = v[i];
+              }
             }
           }
         }

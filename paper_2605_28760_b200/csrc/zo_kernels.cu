@@ -249,16 +249,16 @@ __global__ void k_attention(const void* __restrict__ qkv, int ldq, void* __restr
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
 #pragma unroll
     for (int jj = 0; jj < 4; ++jj) s[jj] = s[jj] / sum;
-    for (int c = lane; c < dh; c += 32) {
+    // every lane takes part in every shuffle, also when dh < 32
+    for (int c0 = 0; c0 < dh; c0 += 32) {
+      const int c = c0 + lane;
+      const int cc = c < dh ? c : dh - 1;
       float acc = 0.f;
       for (int j = 0; j <= i; ++j) {
         const float pj = __shfl_sync(0xffffffffu, s[j >> 5], j & 31);
-        acc += pj * v[j * ld + c];
+        acc += pj * v[j * ld + cc];
       }
-      st16(ctx, (size_t)(seq * T + i) * ldc + (size_t)h * dh + c, acc, bf16);
-    }
-    if (dh < 32) {
-      // lanes >= dh still must take part in the shuffles above; nothing else to do
+      if (c < dh) st16(ctx, (size_t)(seq * T + i) * ldc + (size_t)h * dh + c, acc, bf16);
     }
   }
 }

@@ -215,7 +215,7 @@ def test_gemm(A: np.ndarray, B: np.ndarray, epi: int = 3, bf16: bool = False, C:
     float16/bfloat16 bit patterns in uint16); returns fp32 [M, N]."""
     M, K = A.shape
     N = B.shape[0]
-    lda = lda or K
+    lda = lda or ((K + 7) // 8) * 8
     Ap = np.zeros((M, lda), dtype=np.uint16)
     Ap[:, :K] = A
     Bp = np.zeros((N, lda), dtype=np.uint16)

@@ -1,0 +1,151 @@
+"""Serving-style driver of ``zoserve.runtime`` (runtime.py:253-359) on the engine.
+
+``run_serving_path`` keeps the reference's loop and return type: per step a
+host minibatch (16 indices), one fused device ``lozo_step``, a fold at every
+nu boundary and at run end, evals at the reference cadence (excluded from
+``train_wall_s``).  U/V digests are computed off the critical path by a host
+thread pool from device copies of the slot arenas.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import time
+from dataclasses import dataclass, field
+
+from .adapter import AdapterState
+from .engine import U as SLOT_U, V as SLOT_V
+from .errors import ConfigError, ScoringAbort
+from .model import (EvalPoint, ModelConfig, TaskData, as_device_params, evaluate_split, init_params,
+                    params_digest, sample_minibatch)
+from .numerics import digest_hex
+from .zo_engine import ZoConfig, ZoStepRecord, factorized_step, lozo_step
+
+__all__ = ["CostMeter", "ServingRun", "ScoringAbort", "run_serving_path"]
+
+
+@dataclass
+class CostMeter:
+    """Phase accounting (runtime.py:84-136).  Weight-write counts are a CPU
+    cost proxy in the reference; here the device phases are timed with CUDA
+    events (sample / score / update) and folds by wall clock."""
+    scoring_calls: int = 0
+    scoring_cost_units: int = 0
+    writes_probe: int = 0
+    time_sample_s: float = 0.0
+    time_scoring_s: float = 0.0
+    time_update_s: float = 0.0
+    time_fold_s: float = 0.0
+
+    def to_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+@dataclass
+class ServingRun:
+    config: ZoConfig
+    model_config: ModelConfig
+    trajectory: list[ZoStepRecord]
+    eval_curve: list[EvalPoint]
+    meter: CostMeter
+    final_params_digest: str
+    params: object
+    state: AdapterState
+    train_wall_s: float
+    precision: str
+    steps_completed: int
+    model_digest: str
+    task_digest: str
+    aborted: bool = False
+    kind: str = "serving-b200"
+    extra: dict = field(default_factory=dict)
+
+
+def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: int, precision: str = "real64",
+                     eval_every: int = 50, fold_on_eval: bool = False, abort_at: int | None = None,
+                     params=None, digests: bool = True, compute_param_digests: bool = True) -> ServingRun:
+    """ZO fine-tuning the serving way (runtime.py:253-359), device-resident."""
+    if steps < 1:
+        raise ConfigError("steps must be >= 1")
+    if zcfg.estimator == "dense_mezo":
+        raise ConfigError("dense_mezo has no serving-path form (no compact update factor); "
+                          "use the baseline path for it")
+    params = init_params(mcfg, precision=precision if precision in ("fp16", "bf16") else "fp16",
+                         max_batch=max(16, zcfg.batch_size)) if params is None else params
+    dp = as_device_params(params, mcfg)
+    opt_len = len(task.config.options[0])
+    eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, opt_len)
+    model_digest = params_digest(dp) if compute_param_digests else ""
+    state = AdapterState(epsilon=zcfg.epsilon)
+    state._bind(eng)
+    meter = CostMeter()
+    step_fn = lozo_step if zcfg.estimator == "lozo_lazy" else factorized_step
+    pool = cf.ThreadPoolExecutor(max_workers=4) if digests else None
+    pending: list[tuple[ZoStepRecord, cf.Future, cf.Future | None]] = []
+    vfut = {"key": None, "fut": None}
+    trajectory: list[ZoStepRecord] = []
+    evals: list[EvalPoint] = []
+    wall = 0.0
+    aborted = False
+
+    def do_eval(at: int) -> None:
+        if fold_on_eval and zcfg.estimator == "lozo_lazy":
+            eng.fold()
+            dp.invalidate()
+        loss, acc = evaluate_split(dp, mcfg, task, "dev", state.view(), precision)
+        evals.append(EvalPoint(at, wall * 1e3, loss, acc))
+
+    do_eval(0)
+    done = 0
+    for t in range(steps):
+        batch = sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
+        t0 = time.perf_counter()
+        try:
+            if abort_at is not None and t == abort_at:
+                raise ScoringAbort(f"injected failure at step {t}")
+            rec = step_fn(dp, mcfg, state, zcfg, t, batch, precision, digests="off")
+        except ScoringAbort:
+            aborted = True
+            break
+        wall += time.perf_counter() - t0
+        ms = eng.last_step_ms()
+        meter.time_sample_s += ms[0] * 1e-3
+        meter.time_scoring_s += ms[1] * 1e-3
+        meter.time_update_s += ms[2] * 1e-3
+        meter.scoring_calls += 2
+        meter.scoring_cost_units += 2 * zcfg.batch_size
+        if pool is not None:
+            u_arena = eng.get_slot(SLOT_U)
+            ufut = pool.submit(eng.digest, SLOT_U, u_arena)
+            wkey = (t // zcfg.nu) * zcfg.nu if zcfg.estimator == "lozo_lazy" else t
+            if vfut["key"] != wkey:
+                vfut["key"], vfut["fut"] = wkey, pool.submit(eng.digest, SLOT_V, eng.get_slot(SLOT_V))
+            pending.append((rec, ufut, vfut["fut"]))
+        trajectory.append(rec)
+        done = t + 1
+        if zcfg.estimator == "lozo_lazy" and (t + 1) % zcfg.nu == 0:
+            f0 = time.perf_counter()
+            eng.fold()
+            dp.invalidate()
+            dt = time.perf_counter() - f0
+            meter.time_fold_s += dt
+            wall += dt
+        if (t + 1) % eval_every == 0 and (t + 1) != steps:
+            do_eval(t + 1)
+    if not aborted and zcfg.estimator == "lozo_lazy":
+        f0 = time.perf_counter()
+        eng.fold()
+        dp.invalidate()
+        dt = time.perf_counter() - f0
+        meter.time_fold_s += dt
+        wall += dt
+    if not aborted:
+        do_eval(done)
+    for rec, uf, vf in pending:
+        rec.u_digest = digest_hex(uf.result())
+        rec.v_digest = digest_hex(vf.result())
+    if pool is not None:
+        pool.shutdown()
+    return ServingRun(config=zcfg, model_config=mcfg, trajectory=trajectory, eval_curve=evals, meter=meter,
+                      final_params_digest=params_digest(dp) if compute_param_digests else "", params=dp,
+                      state=state, train_wall_s=wall, precision=precision, steps_completed=done,
+                      model_digest=model_digest, task_digest=task.digest(), aborted=aborted)

@@ -18,7 +18,8 @@ def _h(x, bf16):
 
 @pytest.mark.parametrize("bf16", [False, True])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 128), (300, 200, 96), (1024, 768, 832),
-                                   (2048, 640, 384), (32, 50272 // 8, 64)])
+                                   (2048, 640, 384), (32, 50272 // 8, 64), (272, 96, 38), (16, 64, 32),
+                                   (272, 32, 134), (2048, 2304, 774)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
 def test_gemm_vs_torch(M, N, K, epi, bf16):
     import torch
