@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py -- ZO steps/s + scored tokens/s of the LoZO serving step
+(BASELINE.json metric) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--model opt-13b] [--impl ours|reference]
+
+Workload (N=1): OPT-13B-shaped decoder (d=5120, L=40, H=40, V=50272; the
+reference's architecture, model.py:170-199), LoZO rank-2 LoRA-only, SST-2
+shape B=16 x T=64 (prompt 63 + 1 option token), nu=50, eps=1e-3, lr=1e-7,
+random init (Role.INIT streams, init_scale 0.02) on synthetic marker-task
+batches.  One step = directions (U; V + fold at window boundaries) + both
+probes scored in one fused forward + canonical-mean coefficient + rank-r
+update, exactly lozo_step + run_serving_path's fold policy.
+
+value : steps/s over K device-timed steps (CUDA events on the engine stream,
+        inputs resident in HBM, weights 25.7 GB >> 126 MB L2 so no flush).
+e2e   : the same through the public API (sample_minibatch + lozo_step with
+        host batches: H2D tokens from pinned staging, D2H of L+/L-/c) -- wall clock.
+N > 1 : exact-trajectory mode -- the 16 examples are split over ranks (both
+        signs on every rank), the per-example NLLs are all-gathered over NCCL
+        (256 B/step) and every rank applies the identical update; "strong".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+MODELS = {
+    "opt-125m": dict(vocab=50272, dim=768, n_layers=12, n_heads=12),
+    "opt-1.3b": dict(vocab=50272, dim=2048, n_layers=24, n_heads=32),
+    "opt-6.7b": dict(vocab=50272, dim=4096, n_layers=32, n_heads=32),
+    "opt-13b": dict(vocab=50272, dim=5120, n_layers=40, n_heads=40),
+}
+METRIC = "ZO steps/sec + scored tokens/s, OPT-13B LoZO SST-2 shape, 1/2/4/8 B200"
+UNIT = "ZO steps/s"
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peaks():
+    p = os.path.join(HERE, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def launches_per_step(L: int, n_mats: int, window: bool) -> int:
+    # set_step + sampler(U) 5 + prep + embed + 9/layer + final LN + LM GEMM + loss + coefficient + update
+    n = 1 + 5 + 1 + 1 + 9 * L + 4 + 1
+    if window:
+        n += 5 + n_mats + n_mats  # sampler(V) + V extension writes + fold kernels
+    return n
+
+
+def dense_flops(dim, L, B, T, V, r, opt_len=1):
+    tok = 2 * B * T
+    dense = 24.0 * dim * dim * L * tok
+    attn = 2 * B * L * 4 * T * T * dim * 2 / 2  # QK^T + AV, both signs
+    head = 2.0 * (2 * B * opt_len) * dim * V
+    lora = 2.0 * tok * r * (L * (dim + 3 * dim + dim + dim + dim + 4 * dim + 4 * dim + dim))
+    return dense, dense + attn + head + lora
+
+
+# --------------------------------------------------------------------------- CPU arms
+def run_reference(args, mdl):
+    """--impl reference: the oracle port of the reference's path on host cores."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.cpu_bench import BlockSample, host_threads
+    B, T = args.batch, args.seq
+    n_ex = 1
+    bs = BlockSample(mdl["dim"], mdl["n_heads"], mdl["vocab"], T, n_ex)
+    t_head = bs.run_head() * B
+    for _ in range(args.warmup):
+        bs.run()
+    times = [bs.run() for _ in range(args.steps)]
+    tc = float(np.mean([t[0] for t in times]))
+    tf = float(np.mean([t[1] for t in times]))
+    per_step = mdl["n_layers"] * (tc + B * tf) + t_head
+    v = 1.0 / per_step
+    sample = (f"oracle float64 port: per step 1 of {mdl['n_layers']} blocks, paired +-eps forward of 1 of {B} "
+              f"sequences (T={T}, scaled x{B}) + the block's per-call composition; x{mdl['n_layers']} + LM-head rows")
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.model} LoZO r=2 LoRA-only, B={B} x T={T}", "model": args.model,
+                       "global_batch": B, "seq_len": T},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": host_threads(), "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "scored_tokens_per_s": v * 2 * B * T}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--model", default="opt-13b", choices=sorted(MODELS))
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--seq", type=int, default=64)
+    ap.add_argument("--rank", type=int, default=2)
+    ap.add_argument("--nu", type=int, default=50)
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu/gemm microbench")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    mdl = MODELS[args.model]
+    if args.impl == "reference":
+        run_reference(args, mdl)
+        return
+
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2605_28760_b200 import model as M
+    from paper_2605_28760_b200.adapter import AdapterState
+    from paper_2605_28760_b200.engine import ZoEngine
+    from paper_2605_28760_b200.zo_engine import ZoConfig, lozo_step
+
+    B, T = args.batch, args.seq
+    if B % world:
+        raise SystemExit("global batch must divide over ranks")
+    Bl = B // world
+    prompt_len = T - 1
+    mcfg = M.ModelConfig(vocab=mdl["vocab"], dim=mdl["dim"], n_layers=mdl["n_layers"], n_heads=mdl["n_heads"],
+                         prompt_len=prompt_len, init_seed=7, init_scale=0.02)
+    tcfg = M.TaskConfig(seed=11, vocab=mdl["vocab"], prompt_len=prompt_len, train_size=1000, dev_size=4,
+                        val_size=4)
+    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=1e-7, rank=args.rank, nu=args.nu, batch_size=B)
+    task = M.generate_task(tcfg)
+    t_init = time.perf_counter()
+    eng = ZoEngine(mcfg.vocab, mcfg.dim, mcfg.n_layers, mcfg.n_heads, prompt_len, opt_len=1, max_batch=Bl,
+                   rank=args.rank, precision=args.precision, device=local)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    eng.init_params(mcfg.init_seed, mcfg.init_scale)
+    torch.cuda.synchronize()
+    t_init = time.perf_counter() - t_init
+
+    # device-resident batches for every step of the run (the contract's `value`)
+    nsteps = args.warmup + args.steps
+    toks = np.zeros((nsteps, Bl, T), dtype=np.int32)
+    golds = np.zeros((nsteps, Bl, 1), dtype=np.int32)
+    for t in range(nsteps):
+        mb = M.sample_minibatch(task, "train", zcfg.seed, t, B)
+        seq, gold = mb.sequences()
+        toks[t] = seq[rank * Bl:(rank + 1) * Bl]
+        golds[t] = gold[rank * Bl:(rank + 1) * Bl]
+    d_tok = torch.from_numpy(toks).cuda()
+    d_gold = torch.from_numpy(golds).cuda()
+    nll_local = torch.zeros(2 * Bl, dtype=torch.float64, device="cuda")
+    nll_all = torch.zeros(world * 2 * Bl, dtype=torch.float64, device="cuda")
+
+    def one_step(t):
+        tp, gp = d_tok[t].data_ptr(), d_gold[t].data_ptr()
+        if world == 1:
+            eng.step_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, Bl)
+        else:
+            import torch.distributed as dist
+            eng.step_score_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, tp, gp, Bl)
+            eng.nll_io(nll_local.data_ptr(), 2 * Bl, False)
+            dist.all_gather_into_tensor(nll_all, nll_local)
+            # [rank][sign][b] -> [sign][rank*Bl + b] (canonical example order)
+            full = nll_all.view(world, 2, Bl).transpose(0, 1).contiguous()
+            eng.nll_io(full.data_ptr(), 2 * B, True)
+            eng.step_apply_async(zcfg.epsilon, zcfg.learning_rate, False, B)
+        if (t + 1) % zcfg.nu == 0:
+            eng.fold_async()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    for t in range(args.warmup):
+        one_step(t)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for t in range(args.warmup, nsteps):
+            one_step(t)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    out4 = eng.read_out4()
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / args.steps
+    value = 1000.0 / ms_step
+    windows = sum(1 for t in range(args.warmup, nsteps) if t % zcfg.nu == 0)
+    launches = args.steps * launches_per_step(mcfg.n_layers, 4 * mcfg.n_layers + 1, False) + windows * (
+        5 + 2 * (4 * mcfg.n_layers + 1))
+
+    hbm_peak, tf_peak, peak_kind = peaks()
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic (marker task, random-init Role.INIT weights)",
+            "config": {"workload": f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, "
+                                   f"nu={args.nu}, fold amortised", "model": args.model, "global_batch": B,
+                       "seq_len": T, "parallelism": f"exact-dp{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (25.7 GB 16-bit weights/step at 13B); no flush"},
+            "scored_tokens_per_s": value * 2 * B * T, "option_tokens_per_s": value * 2 * B,
+            "gpu_launches": launches, "clocks": clk.summary(), "init_s": t_init,
+            "last_losses": [float(out4[0]), float(out4[1]), float(out4[2])]}
+    dense, total = dense_flops(mcfg.dim, mcfg.n_layers, B, T, mcfg.vocab, args.rank)
+    line["step_tflops"] = total / 1e12
+    line["step_tensor_util"] = {"achieved_tflops": total / (ms_step * 1e-3) / 1e12 / world,
+                                "of": f"{tf_peak} TF/s {peak_kind} bf16 burst"}
+
+    if rank == 0 and not args.profile:
+        # roofline of the dominant kernel family: the four per-layer tcgen05 GEMMs
+        names = ["qkv", "attn_out", "ff_up", "ff_down", "lm_head"]
+        g = {}
+        for w in range(5):
+            gms, gfl = eng.bench_gemm(w, Bl, 20)
+            g[names[w]] = {"ms": gms, "tflops": gfl / (gms * 1e-3) / 1e12}
+        lay_ms = sum(g[n]["ms"] for n in names[:4])
+        lay_fl = sum(g[n]["tflops"] * g[n]["ms"] * 1e-3 * 1e12 for n in names[:4])
+        achieved = lay_fl / (lay_ms * 1e-3) / 1e12
+        line["roofline"] = {"bound": "tensor", "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s",
+                            "frac": achieved / tf_peak, "traffic": None,
+                            "kernel": "k_gemm (tcgen05 kind::f16, layer GEMMs qkv+attn_out+ff_up+ff_down)",
+                            "peak_kind": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)", "per_gemm": g,
+                            "share_of_step": lay_ms * mcfg.n_layers / ms_step}
+
+    if not args.no_e2e and not args.profile and world == 1:
+        # public API: sample_minibatch + lozo_step on host batches (+ fold at boundaries)
+        params = M.DeviceParams(mcfg, precision=args.precision, max_batch=B)
+        params._engine = eng  # reuse the initialised replica
+        state = AdapterState(epsilon=zcfg.epsilon)
+        for t in range(nsteps, nsteps + args.warmup):
+            lozo_step(params, mcfg, state, zcfg, t, M.sample_minibatch(task, "train", zcfg.seed, t, B),
+                      digests="off")
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for t in range(nsteps + args.warmup, nsteps + args.warmup + args.steps):
+            mb = M.sample_minibatch(task, "train", zcfg.seed, t, B)
+            lozo_step(params, mcfg, state, zcfg, t, mb, digests="off")
+            if (t + 1) % zcfg.nu == 0:
+                eng.fold()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        line["e2e"] = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * T * 4 + B * 4 + 8,
+                       "d2h_bytes_per_step": 32, "api": "model.sample_minibatch + zo_engine.lozo_step (host batch)",
+                       "phase_ms_last_step": dict(zip(["sample", "score", "update"], eng.last_step_ms()))}
+
+    if rank == 0 and not args.no_cpu_baseline and not args.profile:
+        from oracle.cpu_bench import estimate_step, host_threads
+        step_s, desc, _ = estimate_step(mcfg.dim, mcfg.n_layers, mcfg.n_heads, mcfg.vocab, B, T,
+                                        n_examples=4 if mcfg.dim >= 4096 else B)
+        line["cpu_baseline"] = {"value": 1.0 / step_s, "unit": UNIT, "cores": host_threads(), "kind": "port",
+                                "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -120,6 +120,18 @@ int zo_update_dense(zo_ctx* ctx, double lr);
  * coefficient, update.  out4 as zo_coefficient. */
 int zo_step(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon, double lr, int32_t divide_by_r,
             const int32_t* tokens, const int32_t* gold, int32_t B, double* out4);
+/* zo_step with device-resident tokens_dev [B, T] / gold_dev [B, opt_len] and no
+ * host synchronisation (the fused loop a serving replica runs); results via
+ * zo_read_out4.  zo_fold_async: the fold of zo_fold, stream-ordered. */
+int zo_step_async(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon, double lr,
+                  int32_t divide_by_r, const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B);
+int zo_fold_async(zo_ctx* ctx);
+/* the two halves of zo_step_async; multi-GPU exact mode all-gathers the
+ * per-example NLLs (zo_nll_io) between them, B_total = global batch */
+int zo_step_score_async(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon,
+                        const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B);
+int zo_step_apply_async(zo_ctx* ctx, double epsilon, double lr, int32_t divide_by_r, int32_t B_total);
+int zo_read_out4(zo_ctx* ctx, double* out4);
 /* per-phase device time of the last zo_step (ms): [sample, score, update] */
 int zo_last_step_ms(zo_ctx* ctx, float ms[3]);
 
@@ -129,6 +141,13 @@ uint64_t zo_fnv1a64(const void* data, uint64_t nbytes, uint64_t h);
  * an arena: for i: h = fnv(lid_i); h = fnv(arena[off_i : off_i + cnt_i]) */
 uint64_t zo_digest_chain(const char* const* lids, const double* arena, const int64_t* offsets,
                          const int64_t* counts, int32_t n, uint64_t h);
+
+/* measurement: average ms of one launch of a layer GEMM at batch B
+ * (which: 0 qkv, 1 attn_out, 2 ff_up, 3 ff_down, 4 LM head) and its FLOPs */
+int zo_bench_gemm(zo_ctx* ctx, int32_t which, int32_t B, int32_t reps, float* avg_ms, double* flops);
+/* copy per-example NLLs between the ctx and an external device buffer
+ * (to_ctx = 1: dev -> ctx) -- the multi-GPU exact-mode exchange point */
+int zo_nll_io(zo_ctx* ctx, void* dev, int32_t count, int32_t to_ctx);
 
 /* test hook: D = A[M,K] . B[N,K]^T through the production tcgen05 GEMM with
  * epilogue epi (0 store16, 1 gelu16, 2 resid32: C += D, 3 store32); host

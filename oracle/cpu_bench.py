@@ -1,0 +1,115 @@
+"""oracle/cpu_bench.py -- TEST INFRASTRUCTURE ONLY: the CPU baseline leg of bench.py.
+
+Times the oracle port (oracle/reference.py, float64 numpy, the reference's
+algorithm: compose-then-matmul, model.py:157-199 + adapter.py:200-234) on a
+BOUNDED sample of one LoZO step and extrapolates to the whole step:
+
+  sample  = one decoder block of the paired (+eps, -eps) scoring forward for
+            `n_examples` sequences of T tokens, including the per-call dense
+            composition W0 + A V^T +- eps U V^T of the block's four matrices
+            (the reference materialises these every scorer call);
+  step    = n_layers * (composition + (B / n_examples) * forward)
+            + the LM-head rows and option NLLs of both probes (timed once)
+            + direction sampling for every matrix (timed, C oracle sampler).
+
+Never used as the product path; bench.py reports it as ``cpu_baseline``
+(kind "port") and as the ``--impl reference`` arm.
+"""
+from __future__ import annotations
+
+import math
+import os
+import time
+
+import numpy as np
+
+from . import reference as R
+
+
+def _block_forward(x, w, H):
+    B, T, d = x.shape
+    dh = d // H
+    mask = np.triu(np.ones((T, T), dtype=bool), k=1)
+    h = R._ln(x, 1.0, 0.0)
+    qkv = h @ w["qkv"]
+    q, k, v = (qkv[..., j * d:(j + 1) * d].reshape(B, T, H, dh).transpose(0, 2, 1, 3) for j in range(3))
+    s = q @ k.transpose(0, 1, 3, 2) / math.sqrt(dh)
+    s = np.where(mask, -np.inf, s)
+    s = s - s.max(axis=-1, keepdims=True)
+    a = np.exp(s)
+    a = a / a.sum(axis=-1, keepdims=True)
+    ctx = (a @ v).transpose(0, 2, 1, 3).reshape(B, T, d)
+    x = x + ctx @ w["attn_out"]
+    h = R._ln(x, 1.0, 0.0)
+    return x + R._gelu(h @ w["ff_up"]) @ w["ff_down"]
+
+
+class BlockSample:
+    def __init__(self, dim: int, n_heads: int, vocab: int, T: int, n_examples: int, rank: int = 2, seed: int = 0):
+        rng = np.random.default_rng(seed)
+        d = dim
+        self.H, self.T, self.n = n_heads, T, n_examples
+        self.shapes = {"qkv": (d, 3 * d), "attn_out": (d, d), "ff_up": (d, 4 * d), "ff_down": (4 * d, d)}
+        self.W = {k: 0.02 * rng.standard_normal(s) for k, s in self.shapes.items()}
+        self.A = {k: 1e-4 * rng.standard_normal((s[0], rank)) for k, s in self.shapes.items()}
+        self.U = {k: rng.standard_normal((s[0], rank)) for k, s in self.shapes.items()}
+        self.V = {k: rng.standard_normal((s[1], rank)) for k, s in self.shapes.items()}
+        self.x = rng.standard_normal((n_examples, T, d))
+        self.head_x = rng.standard_normal((n_examples, d))
+        self.E = 0.02 * rng.standard_normal((vocab, d))
+
+    def run(self, eps: float = 1e-3) -> tuple[float, float]:
+        """(composition seconds, forward seconds) for the sample, both probe signs.
+        Composition is per scorer call (independent of batch size), the forward
+        scales with the number of sequences."""
+        tc = tf = 0.0
+        for sign in (+1, -1):
+            t0 = time.perf_counter()
+            w = {k: R.compose(self.W[k], self.A[k], self.V[k], self.U[k], sign, eps) for k in self.W}
+            t1 = time.perf_counter()
+            _block_forward(self.x, w, self.H)
+            t2 = time.perf_counter()
+            tc += t1 - t0
+            tf += t2 - t1
+        return tc, tf
+
+    def run_head(self) -> float:
+        t0 = time.perf_counter()
+        for _ in (+1, -1):
+            row = self.head_x @ self.E.T
+            m = row.max(axis=-1)
+            _ = m + np.log(np.exp(row - m[:, None]).sum(axis=-1))
+        return time.perf_counter() - t0
+
+
+def sampler_seconds(shapes: dict, rank: int) -> float:
+    t0 = time.perf_counter()
+    for lid, (m, n) in shapes.items():
+        R.gaussian(42, 7, lid, R.ROLE_U, m, rank)
+    return time.perf_counter() - t0
+
+
+def estimate_step(dim, n_layers, n_heads, vocab, B, T, n_examples, rank=2, reps=1):
+    """(seconds per full step estimated, sample description, sample seconds)."""
+    bs = BlockSample(dim, n_heads, vocab, T, n_examples, rank)
+    bs.run()  # warm (page in, BLAS threads)
+    tc, tf = min((bs.run() for _ in range(reps)), key=lambda p: p[0] + p[1])
+    t_block = tc + tf * (B / n_examples)
+    t_head = bs.run_head() * (B / n_examples)
+    shapes = {"embed": (vocab, dim)}
+    for i in range(n_layers):
+        shapes.update({f"blk{i}.qkv": (dim, 3 * dim), f"blk{i}.attn_out": (dim, dim),
+                       f"blk{i}.ff_up": (dim, 4 * dim), f"blk{i}.ff_down": (4 * dim, dim)})
+    t_samp = sampler_seconds(dict(list(shapes.items())[:5]), rank) * len(shapes) / 5
+    step = n_layers * t_block + t_head + t_samp
+    desc = (f"oracle float64 port: 1 of {n_layers} decoder blocks, paired +-eps forward of {n_examples}/{B} "
+            f"sequences x T={T} ({tf:.3f} s, scaled x{B // n_examples}) + the block's per-call W0+AV^T+-eps UV^T "
+            f"composition ({tc:.3f} s); x{n_layers} blocks + LM-head rows + direction sampling")
+    return step, desc, t_block
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1

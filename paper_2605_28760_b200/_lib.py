@@ -62,8 +62,18 @@ SIGNATURES = [
     ("zo_update_dense", _c.c_int, [_P, _c.c_double]),
     ("zo_step", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double, _c.c_int32,
                            _P, _P, _c.c_int32, _P]),
+    ("zo_step_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double,
+                                 _c.c_int32, _P, _P, _c.c_int32]),
+    ("zo_fold_async", _c.c_int, [_P]),
+    ("zo_step_score_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _P, _P,
+                                       _c.c_int32]),
+    ("zo_step_apply_async", _c.c_int, [_P, _c.c_double, _c.c_double, _c.c_int32, _c.c_int32]),
+    ("zo_read_out4", _c.c_int, [_P, _P]),
     ("zo_last_step_ms", _c.c_int, [_P, _c.POINTER(_c.c_float)]),
     ("zo_fnv1a64", _c.c_uint64, [_P, _c.c_uint64, _c.c_uint64]),
+    ("zo_bench_gemm", _c.c_int, [_P, _c.c_int32, _c.c_int32, _c.c_int32, _c.POINTER(_c.c_float),
+                                 _c.POINTER(_c.c_double)]),
+    ("zo_nll_io", _c.c_int, [_P, _P, _c.c_int32, _c.c_int32]),
     ("zo_test_gemm", _c.c_int, [_c.c_int32] * 6 + [_P, _P, _P]),
     ("zo_digest_chain", _c.c_uint64, [_c.POINTER(_c.c_char_p), _P, _c.POINTER(_c.c_int64),
                                       _c.POINTER(_c.c_int64), _c.c_int32, _c.c_uint64]),

@@ -530,6 +530,46 @@ __global__ void k_fold_shadow(double* __restrict__ W, int m, int n, const double
   }
 }
 
+// factorized dense update with alpha = -(lr*c) * scale read from the device
+// coefficient (zo_engine.py:450); no-op when the step aborted.
+__global__ void k_fold_dev(double* __restrict__ W, int m, int n, const double* __restrict__ A,
+                           const double* __restrict__ Vv, int r, const double* __restrict__ out4, double lr,
+                           double scale, const unsigned* __restrict__ abort_flag, void* __restrict__ W16, int ldw,
+                           int transposed, bool bf16) {
+  if (*abort_flag) return;
+  const double alpha = __dmul_rn(-__dmul_rn(lr, out4[2]), scale);
+  __shared__ float tile[32][33];
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int i = i0 + yy, j = j0 + tx;
+    float f = 0.f;
+    if (i < m && j < n) {
+      double w = W[(size_t)i * n + j];
+      for (int k = 0; k < r; ++k)
+        w = __dadd_rn(w, __dmul_rn(alpha, __dmul_rn(A[(size_t)i * r + k], Vv[(size_t)j * r + k])));
+      W[(size_t)i * n + j] = w;
+      f = (float)w;
+      if (!transposed) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
+    }
+    tile[yy][tx] = f;
+  }
+  if (!transposed) return;
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int j = j0 + yy, i = i0 + tx;
+    if (i < m && j < n) reinterpret_cast<uint16_t*>(W16)[(size_t)j * ldw + i] = to16(tile[tx][yy], bf16);
+  }
+}
+
+void launch_fold_dev(double* W64, int m, int n, const double* A, const double* V, int r, const double* out4,
+                     double lr, double scale, const unsigned* abort_flag, void* W16, int ldw, int transposed,
+                     bool bf16, cudaStream_t st) {
+  dim3 grid((n + 31) / 32, (m + 31) / 32);
+  k_fold_dev<<<grid, dim3(32, 8), 0, st>>>(W64, m, n, A, V, r, out4, lr, scale, abort_flag, W16, ldw, transposed,
+                                           bf16);
+}
+
 void launch_fold(double* W64, int m, int n, const double* A, const double* V, int r, double alpha, void* W16,
                  int ldw, int transposed, bool bf16, cudaStream_t st) {
   dim3 grid((n + 31) / 32, (m + 31) / 32);

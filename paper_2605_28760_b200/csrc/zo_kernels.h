@@ -47,6 +47,9 @@ void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K
 // W64[m,n] += sum_k A[:,k] V[:,k]^T (k ascending, numerics.py:207-235) then A = 0
 void launch_fold(double* W64, int m, int n, const double* A, const double* V, int r, double alpha, void* W16,
                  int ldw, int transposed, bool bf16, cudaStream_t st);
+void launch_fold_dev(double* W64, int m, int n, const double* A, const double* V, int r, const double* out4,
+                     double lr, double scale, const unsigned* abort_flag, void* W16, int ldw, int transposed,
+                     bool bf16, cudaStream_t st);
 // shadows: W16T[n, :m] = h16(W64[m,n]^T) (projection) or E16[m, n] = h16(W64) (embed)
 void launch_shadow_T(const double* W64, int m, int n, void* W16T, int ldw, bool bf16, cudaStream_t st);
 void launch_shadow(const double* W64, int64_t count, void* W16, bool bf16, cudaStream_t st);

@@ -132,6 +132,8 @@ struct zo_ctx {
 
 namespace {
 
+__global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
+
 int fail(const Error& e) {
   g_last_error = e.msg;
   return e.code;
@@ -273,6 +275,13 @@ void set_step(zo_ctx* c, uint64_t step) {
   ZO_CUDA_TRY(cudaMemcpyAsync(c->d_step, c->h_step, 8, cudaMemcpyHostToDevice, c->st));
 }
 
+void launch_dense_update_dev(zo_ctx* c, double lr) {
+  for (auto& m : c->mats)
+    launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, c->out4, lr,
+                    1.0 / std::sqrt((double)c->r), c->abort_flag, m.W16, m.kind == K_EMBED ? (int)m.n : m.ldw,
+                    m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
+}
+
 void fold_all(zo_ctx* c) {
   for (auto& m : c->mats)
     launch_fold(m.W64, (int)m.m, (int)m.n, c->A + m.u_off, c->V + m.v_off, c->r, 1.0, m.W16,
@@ -405,7 +414,7 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->xs32 = c->mem.get<float>((size_t)c->Smax * D);
   c->z = c->mem.get<float>((size_t)c->Smax * d.rank);
   c->logits = c->mem.get<float>((size_t)c->Smax * c->ldl);
-  c->nll = c->mem.get<double>(2 * d.max_batch);
+  c->nll = c->mem.get<double>(2 * std::max(d.max_batch, 4096));
   c->out4 = c->mem.get<double>(4);
   c->abort_flag = c->mem.get<unsigned>(1);
   c->tok = c->mem.get<int32_t>((size_t)d.max_batch * c->T);
@@ -826,6 +835,122 @@ uint64_t zo_digest_chain(const char* const* lids, const double* arena, const int
 }
 
 }  // extern "C"
+
+// Stream-ordered step with device-resident inputs and no host synchronisation
+// (tokens_dev [B, T], gold_dev [B, opt_len] int32).  Results stay on the device
+// (zo_read_out4); a non-finite loss disarms the update on the device.
+// Stream-ordered step with device-resident inputs and no host synchronisation
+// (tokens_dev [B, T], gold_dev [B, opt_len] int32).  Results stay on the device
+// (zo_read_out4); a non-finite loss disarms the update on the device.
+// zo_step_score_async = directions + probes + paired scoring (per-example NLLs
+// in the ctx); zo_step_apply_async = canonical mean / c / update over B_total
+// examples.  Multi-GPU exact mode all-gathers the NLLs between the two.
+extern "C" int zo_step_score_async(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps,
+                                   const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
+  ZO_API_BEGIN
+  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  k_set_u64<<<1, 1, 0, c->st>>>(c->d_step, step);
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->tok, tokens_dev, (size_t)B * c->T * 4, cudaMemcpyDeviceToDevice, c->st));
+  const size_t ng = (size_t)B * c->d.opt_len * 4;
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->gold, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
+  ZO_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->gold) + ng, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
+  const int64_t wstart = lozo ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
+  if (!lozo || wstart != c->v_window) {
+    if (lozo && c->a_dirty) fold_all(c);
+    sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
+    write_vext_all(c);
+    c->v_window = wstart;
+  }
+  sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  const double scale = lozo ? 1.0 : 1.0 / std::sqrt((double)c->r);
+  launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, eps, scale, c->Pp, c->Pm, c->st);
+  do_score(c, B, 2);
+  return ZO_OK;
+  ZO_API_END
+}
+
+extern "C" int zo_step_apply_async(zo_ctx* c, double eps, double lr, int32_t divide_by_r, int32_t B_total) {
+  ZO_API_BEGIN
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  launch_coefficient(c->nll, B_total, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
+  if (lozo) {
+    launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
+    c->a_dirty = true;
+  } else {
+    launch_dense_update_dev(c, lr);
+  }
+  return ZO_OK;
+  ZO_API_END
+}
+
+extern "C" int zo_step_async(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr,
+                             int32_t divide_by_r, const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
+  int rc = zo_step_score_async(c, seed, step, nu, eps, tokens_dev, gold_dev, B);
+  if (rc) return rc;
+  return zo_step_apply_async(c, eps, lr, divide_by_r, B);
+}
+
+extern "C" int zo_fold_async(zo_ctx* c) {
+  ZO_API_BEGIN
+  if (c->d.estimator == ZO_EST_LOZO) fold_all(c);
+  return ZO_OK;
+  ZO_API_END
+}
+
+extern "C" int zo_read_out4(zo_ctx* c, double* out4) {
+  ZO_API_BEGIN
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->h_out4, c->out4, 32, cudaMemcpyDeviceToHost, c->st));
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  ZO_CUDA_TRY(cudaGetLastError());
+  std::memcpy(out4, c->h_out4, 32);
+  return ZO_OK;
+  ZO_API_END
+}
+
+// ------------------------------------------------------------------ measurement hooks
+// Average device time (ms) of one launch of a layer-0 GEMM of the scorer at
+// batch B (both signs): which = 0 qkv, 1 attn_out, 2 ff_up, 3 ff_down, 4 LM head.
+// CUDA events bracket `reps` back-to-back launches on the ctx stream; the
+// weights (>> L2) stream from HBM on every launch.
+extern "C" int zo_bench_gemm(zo_ctx* c, int32_t which, int32_t B, int32_t reps, float* avg_ms, double* flops) {
+  ZO_API_BEGIN
+  check(which >= 0 && which <= 4 && reps >= 1, ZO_ERR_INPUT, "bad gemm id / reps");
+  const int M = 2 * B * c->T;
+  RowPlan& rp = row_plan(c, M);
+  const GemmDesc& g = which == 0 ? rp.layers[0].qkv : which == 1 ? rp.layers[0].out
+                    : which == 2 ? rp.layers[0].up : which == 3 ? rp.layers[0].down : rp.lm;
+  const int l = c->d.n_layers > 1 ? 1 : 0;
+  const GemmDesc& g2 = which == 0 ? rp.layers[l].qkv : which == 1 ? rp.layers[l].out
+                     : which == 2 ? rp.layers[l].up : which == 3 ? rp.layers[l].down : rp.lm;
+  gemm_launch(g, c->st);  // warm
+  ZO_CUDA_TRY(cudaEventRecord(c->ev[0], c->st));
+  // alternate two layers' weights so no launch finds its B operand in L2
+  for (int i = 0; i < reps; ++i) gemm_launch((i & 1) ? g2 : g, c->st);
+  ZO_CUDA_TRY(cudaEventRecord(c->ev[1], c->st));
+  ZO_CUDA_TRY(cudaEventSynchronize(c->ev[1]));
+  float ms = 0;
+  ZO_CUDA_TRY(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+  *avg_ms = ms / reps;
+  const double K = (double)(g.num_kb - 1) * 64 + 16.0 * g.last_ksteps;
+  *flops = 2.0 * g.M * (double)g.N * K;
+  return ZO_OK;
+  ZO_API_END
+}
+
+// External device buffer <-> ctx per-example NLLs [2, B] (multi-GPU exact mode
+// exchanges them between the scoring and the coefficient phases).
+extern "C" int zo_nll_io(zo_ctx* c, void* dev, int32_t count, int32_t to_ctx) {
+  ZO_API_BEGIN
+  check(count >= 0 && count <= 2 * std::max(c->d.max_batch, 4096), ZO_ERR_DIMENSION, "nll count out of range");
+  if (to_ctx)
+    ZO_CUDA_TRY(cudaMemcpyAsync(c->nll, dev, (size_t)count * 8, cudaMemcpyDeviceToDevice, c->st));
+  else
+    ZO_CUDA_TRY(cudaMemcpyAsync(dev, c->nll, (size_t)count * 8, cudaMemcpyDeviceToDevice, c->st));
+  return ZO_OK;
+  ZO_API_END
+}
 
 // ------------------------------------------------------------------ test hooks
 extern "C" int zo_test_gemm(int32_t M, int32_t N, int32_t K, int32_t lda, int32_t epi, int32_t bf16,

@@ -203,6 +203,35 @@ class ZoEngine:
                             tok.ctypes.data, g.ctypes.data, tok.shape[0], out.ctypes.data))
         return out.copy()
 
+    def step_async(self, seed: int, step: int, nu: int, epsilon: float, lr: float, divide_by_r: bool,
+                   tokens_dev: int, gold_dev: int, B: int) -> None:
+        check(lib().zo_step_async(self._h, seed, step, nu, float(epsilon), float(lr), int(divide_by_r),
+                                  ctypes.c_void_p(tokens_dev), ctypes.c_void_p(gold_dev), B))
+
+    def step_score_async(self, seed: int, step: int, nu: int, epsilon: float, tokens_dev: int, gold_dev: int,
+                         B: int) -> None:
+        check(lib().zo_step_score_async(self._h, seed, step, nu, float(epsilon), ctypes.c_void_p(tokens_dev),
+                                        ctypes.c_void_p(gold_dev), B))
+
+    def step_apply_async(self, epsilon: float, lr: float, divide_by_r: bool, B_total: int) -> None:
+        check(lib().zo_step_apply_async(self._h, float(epsilon), float(lr), int(divide_by_r), B_total))
+
+    def fold_async(self) -> None:
+        check(lib().zo_fold_async(self._h))
+
+    def read_out4(self) -> np.ndarray:
+        out = np.empty(4)
+        check(lib().zo_read_out4(self._h, out.ctypes.data))
+        return out
+
+    def bench_gemm(self, which: int, B: int, reps: int = 20) -> tuple[float, float]:
+        ms, fl = ctypes.c_float(), ctypes.c_double()
+        check(lib().zo_bench_gemm(self._h, which, B, reps, ctypes.byref(ms), ctypes.byref(fl)))
+        return float(ms.value), float(fl.value)
+
+    def nll_io(self, dev_ptr: int, count: int, to_ctx: bool) -> None:
+        check(lib().zo_nll_io(self._h, ctypes.c_void_p(dev_ptr), count, int(to_ctx)))
+
     def last_step_ms(self) -> tuple[float, float, float]:
         f = (ctypes.c_float * 3)()
         check(lib().zo_last_step_ms(self._h, f))
