@@ -332,7 +332,7 @@ void launch_final_ln(const float* x32, const float* gamma, const float* beta, in
     ZO_CUDA_TRY(cudaFuncSetAttribute(k_final_ln, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  k_final_ln<<<2 * B * Lopt, 256, smem, st>>>(x32, gamma, beta, B, T, d, prompt_len, Lopt, xs32, xs16, bf16, Ve32,
+  k_final_ln<<<B * Lopt, 256, smem, st>>>(x32, gamma, beta, B, T, d, prompt_len, Lopt, xs32, xs16, bf16, Ve32,
                                               r, z);
 }
 

@@ -25,7 +25,7 @@ void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, c
 // causal softmax attention per (sequence, head) (model.py:184-194); qkv [M,3d] -> ctx[:, :d]
 void launch_attention(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, int dh, bool bf16,
                       cudaStream_t st);
-// final LN at scored rows (prompt_len-1+j) -> xs32/xs16, z = xs . V_e
+// final LN at scored rows (prompt_len-1+j) of B sequences (both signs counted) -> xs32/xs16, z = xs . V_e
 void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d,
                      int prompt_len, int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r,
                      float* z, cudaStream_t st);
