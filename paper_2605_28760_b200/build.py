@@ -23,12 +23,12 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
           "-I" + os.path.join(os.path.dirname(PKG), "include")]
-# the sampler/update arithmetic must never be contracted into FMAs (bit-exact fp64)
+# the sampler must never contract its float64 arithmetic into FMAs (bit-exact ziggurat);
+# the update/fold/coefficient kernels spell every rounding with __dmul_rn/__dadd_rn
 PER_FILE = {
     "sampler.cu": ["-fmad=false"],
-    "zo_kernels.cu": ["-fmad=false"],
 }
-SOURCES = ["sampler.cu", "gemm_sm100.cu", "zo_kernels.cu", "zob200.cu"]
+SOURCES = ["sampler.cu", "gemm_sm100.cu", "attention.cu", "zo_kernels.cu", "zob200.cu"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

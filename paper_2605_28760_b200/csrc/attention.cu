@@ -1,0 +1,263 @@
+// K3 -- small-T causal attention per (sequence, head) (model.py:184-194).
+//
+// T <= 128 tokens and dh in {16, 32, 64, 128}: one CTA of ceil(T/16) warps per
+// (sequence, head); Q, K, V (16-bit, from the packed qkv GEMM output) are
+// staged in shared memory with 16-byte loads, S = Q K^T and O = P V run on the
+// tensor cores (mma.sync m16n8k16, fp32 accumulate) with the causal softmax
+// kept in registers between them (the S accumulator fragment is re-used as the
+// A fragment of P V).  Warp w owns query rows [16w, 16w+16) and only visits
+// key blocks <= its own (causal).  FLOPs are <0.3% of the step; the kernel is
+// bound by reading qkv once (HBM) -- the SIMT version was 35% of the step.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "zo_common.cuh"
+#include "zo_kernels.h"
+
+namespace zo {
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+template <bool BF16>
+__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  if constexpr (BF16) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  } else {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  }
+}
+template <bool BF16>
+__device__ __forceinline__ float unpack_f(uint32_t w, int hi) {
+  const uint16_t h = (uint16_t)(w >> (16 * hi));
+  if constexpr (BF16) return __bfloat162float(__ushort_as_bfloat16(h));
+  else return __half2float(__ushort_as_half(h));
+}
+template <bool BF16>
+__device__ __forceinline__ uint32_t pack_f2(float a, float b) {
+  if constexpr (BF16) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+}
+
+template <int DH, int TP, bool BF16>
+__global__ void __launch_bounds__(TP * 2)
+    k_attn_mma(const uint16_t* __restrict__ qkv, int ldq, uint16_t* __restrict__ ctx, int ldc, int T, int H,
+               AttnExt x) {
+  constexpr int LD = DH + 8;  // padded row (halves): conflict-free ldmatrix
+  constexpr int NT = TP / 8;  // key n-tiles
+  constexpr int DT = DH / 8;  // output n-tiles
+  extern __shared__ __align__(16) uint16_t sm[];
+  uint16_t* sq = sm;
+  uint16_t* sk = sq + TP * LD;
+  uint16_t* sv = sk + TP * LD;
+  const int seq = blockIdx.x, h = blockIdx.y;
+  const int d = H * DH;
+  // stage Q, K, V (16-byte vectors; rows >= T zero)
+  constexpr int VPR = DH / 8;
+  for (int idx = threadIdx.x; idx < TP * VPR; idx += blockDim.x) {
+    const int t = idx / VPR, c = (idx % VPR) * 8;
+    uint4 q = make_uint4(0, 0, 0, 0), k = q, v = q;
+    if (t < T) {
+      const uint16_t* src = qkv + (size_t)(seq * T + t) * ldq + (size_t)h * DH + c;
+      q = *reinterpret_cast<const uint4*>(src);
+      k = *reinterpret_cast<const uint4*>(src + d);
+      v = *reinterpret_cast<const uint4*>(src + 2 * d);
+    }
+    *reinterpret_cast<uint4*>(sq + t * LD + c) = q;
+    *reinterpret_cast<uint4*>(sk + t * LD + c) = k;
+    *reinterpret_cast<uint4*>(sv + t * LD + c) = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = warp * 16;
+  if (r0 >= T) return;
+  const int g = lane >> 2, tq = lane & 3;
+  const int kblocks = warp + 1;  // causal: key blocks of 16 up to this warp's rows
+  const uint32_t sq_a = static_cast<uint32_t>(__cvta_generic_to_shared(sq));
+  const uint32_t sk_a = static_cast<uint32_t>(__cvta_generic_to_shared(sk));
+  const uint32_t sv_a = static_cast<uint32_t>(__cvta_generic_to_shared(sv));
+
+  float s[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) s[n][0] = s[n][1] = s[n][2] = s[n][3] = 0.f;
+#pragma unroll
+  for (int kk = 0; kk < DH / 16; ++kk) {
+    uint32_t a0, a1, a2, a3;
+    ldsm_x4(sq_a + 2 * ((r0 + (lane & 15)) * LD + kk * 16 + (lane >> 4) * 8), a0, a1, a2, a3);
+#pragma unroll
+    for (int nb = 0; nb < NT / 2; ++nb) {
+      if (nb < kblocks) {
+        uint32_t b0, b1, b2, b3;
+        const int q = lane >> 3;
+        ldsm_x4(sk_a + 2 * ((nb * 16 + (q >> 1) * 8 + (lane & 7)) * LD + kk * 16 + (q & 1) * 8), b0, b1, b2, b3);
+        mma16816<BF16>(s[2 * nb], a0, a1, a2, a3, b0, b1);
+        mma16816<BF16>(s[2 * nb + 1], a0, a1, a2, a3, b2, b3);
+      }
+    }
+  }
+  // causal softmax on the fragments: rows r0+g and r0+g+8, cols 8n + 2tq (+1)
+  const float scale = rsqrtf((float)DH);
+  float mx[2] = {-CUDART_INF_F, -CUDART_INF_F};
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int row = r0 + g + ((e >> 1) << 3), col = n * 8 + 2 * tq + (e & 1);
+      const bool ok = (n / 2) < kblocks && col <= row && col < T;
+      s[n][e] = ok ? s[n][e] * scale : -CUDART_INF_F;
+      mx[e >> 1] = fmaxf(mx[e >> 1], s[n][e]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], 1));
+    mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], 2));
+  }
+  float sum[2] = {0.f, 0.f};
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float p = s[n][e] == -CUDART_INF_F ? 0.f : __expf(s[n][e] - mx[e >> 1]);
+      s[n][e] = p;
+      sum[e >> 1] += p;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    sum[i] += __shfl_xor_sync(0xffffffffu, sum[i], 1);
+    sum[i] += __shfl_xor_sync(0xffffffffu, sum[i], 2);
+  }
+  // O = P V
+  float o[DT][4];
+#pragma unroll
+  for (int n = 0; n < DT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+#pragma unroll
+  for (int kp = 0; kp < NT / 2; ++kp) {
+    if (kp < kblocks) {
+      const uint32_t a0 = pack_f2<BF16>(s[2 * kp][0], s[2 * kp][1]);
+      const uint32_t a1 = pack_f2<BF16>(s[2 * kp][2], s[2 * kp][3]);
+      const uint32_t a2 = pack_f2<BF16>(s[2 * kp + 1][0], s[2 * kp + 1][1]);
+      const uint32_t a3 = pack_f2<BF16>(s[2 * kp + 1][2], s[2 * kp + 1][3]);
+#pragma unroll
+      for (int nc = 0; nc < DT / 2; ++nc) {
+        uint32_t b0, b1, b2, b3;
+        const int q = lane >> 3;
+        ldsm_x4_t(sv_a + 2 * ((kp * 16 + (q & 1) * 8 + (lane & 7)) * LD + nc * 16 + (q >> 1) * 8), b0, b1, b2, b3);
+        mma16816<BF16>(o[2 * nc], a0, a1, a2, a3, b0, b1);
+        mma16816<BF16>(o[2 * nc + 1], a0, a1, a2, a3, b2, b3);
+      }
+    }
+  }
+  const float inv0 = 1.f / sum[0], inv1 = 1.f / sum[1];
+  const int row0 = r0 + g, row1 = r0 + g + 8;
+  const int m0 = seq * T + row0, m1 = seq * T + row1;
+  float t0[8], t1[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t0[k] = t1[k] = 0.f;
+  const float* P0 = x.tpart ? ((m0 < x.rps) ? x.Pp : x.Pm) : nullptr;
+  const float* P1 = x.tpart ? ((m1 < x.rps) ? x.Pp : x.Pm) : nullptr;
+#pragma unroll
+  for (int n = 0; n < DT; ++n) {
+    const int col = h * DH + n * 8 + 2 * tq;
+    const uint32_t w0 = pack_f2<BF16>(o[n][0] * inv0, o[n][1] * inv0);
+    const uint32_t w1 = pack_f2<BF16>(o[n][2] * inv1, o[n][3] * inv1);
+    if (row0 < T) *reinterpret_cast<uint32_t*>(ctx + (size_t)m0 * ldc + col) = w0;
+    if (row1 < T) *reinterpret_cast<uint32_t*>(ctx + (size_t)m1 * ldc + col) = w1;
+    if (x.tpart) {
+      // partial LoRA-extension dots of the stored ctx with the attn_out P+- (model.py:191-192)
+      const float a00 = unpack_f<BF16>(w0, 0), a01 = unpack_f<BF16>(w0, 1);
+      const float a10 = unpack_f<BF16>(w1, 0), a11 = unpack_f<BF16>(w1, 1);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (k < x.r) {
+          t0[k] += a00 * P0[(size_t)col * x.r + k] + a01 * P0[(size_t)(col + 1) * x.r + k];
+          t1[k] += a10 * P1[(size_t)col * x.r + k] + a11 * P1[(size_t)(col + 1) * x.r + k];
+        }
+      }
+    }
+  }
+  if (x.tpart) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      t0[k] += __shfl_xor_sync(0xffffffffu, t0[k], 1);
+      t0[k] += __shfl_xor_sync(0xffffffffu, t0[k], 2);
+      t1[k] += __shfl_xor_sync(0xffffffffu, t1[k], 1);
+      t1[k] += __shfl_xor_sync(0xffffffffu, t1[k], 2);
+    }
+    if (tq == 0) {
+      for (int k = 0; k < x.r; ++k) {
+        if (row0 < T) x.tpart[((size_t)h * x.ld + m0) * x.r + k] = t0[k];
+        if (row1 < T) x.tpart[((size_t)h * x.ld + m1) * x.r + k] = t1[k];
+      }
+    }
+  }
+}
+
+template <int DH, int TP, bool BF16>
+static void launch_t(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, const AttnExt& x,
+                     cudaStream_t st) {
+  const size_t smem = (size_t)3 * TP * (DH + 8) * 2;
+  static bool set = false;
+  if (!set) {
+    ZO_CUDA_TRY(cudaFuncSetAttribute(k_attn_mma<DH, TP, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    set = true;
+  }
+  k_attn_mma<DH, TP, BF16><<<dim3(nseq, H), TP * 2, smem, st>>>(static_cast<const uint16_t*>(qkv), ldq,
+                                                                 static_cast<uint16_t*>(ctx), ldc, T, H, x);
+}
+
+template <int DH, bool BF16>
+static void launch_dh(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, const AttnExt& x,
+                      cudaStream_t st) {
+  if (T <= 32) launch_t<DH, 32, BF16>(qkv, ldq, ctx, ldc, nseq, T, H, x, st);
+  else if (T <= 64) launch_t<DH, 64, BF16>(qkv, ldq, ctx, ldc, nseq, T, H, x, st);
+  else launch_t<DH, 128, BF16>(qkv, ldq, ctx, ldc, nseq, T, H, x, st);
+}
+
+void launch_attention(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, int dh, bool bf16,
+                      const AttnExt& x, cudaStream_t st) {
+  if (x.tpart && (x.r < 1 || x.r > 8)) throw Error(ZO_ERR_DIMENSION, "fused attention extension needs 1 <= r <= 8");
+  if (T > 128) throw Error(ZO_ERR_DIMENSION, "attention kernel supports T <= 128");
+  if (ldq % 8 || ldc % 2) throw Error(ZO_ERR_DIMENSION, "attention operands must be 16-byte aligned");
+#define ZO_DH(D)                                                                    \
+  case D:                                                                           \
+    if (bf16) launch_dh<D, true>(qkv, ldq, ctx, ldc, nseq, T, H, x, st);             \
+    else launch_dh<D, false>(qkv, ldq, ctx, ldc, nseq, T, H, x, st);                 \
+    return;
+  switch (dh) {
+    ZO_DH(16)
+    ZO_DH(32)
+    ZO_DH(64)
+    ZO_DH(128)
+    default: throw Error(ZO_ERR_DIMENSION, "head dim must be 16, 32, 64 or 128");
+  }
+#undef ZO_DH
+}
+
+}  // namespace zo

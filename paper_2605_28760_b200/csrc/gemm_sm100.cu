@@ -123,6 +123,13 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   }
 }
 
+template <bool BF16>
+__device__ __forceinline__ float unpack16(uint32_t w, int hi) {
+  const uint16_t h = (uint16_t)(w >> (16 * hi));
+  if constexpr (BF16) return __bfloat162float(__ushort_as_bfloat16(h));
+  else return __half2float(__ushort_as_half(h));
+}
+
 template <int BN>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;
@@ -137,6 +144,12 @@ struct GemmCfg {
 struct GemmParams {
   int M, N, num_kb, last_ksteps, m_tiles, n_tiles, ldo;
   void* out;
+  // EPI_GELU16_EXT: per-tile partial LoRA-extension dots of the stored 16-bit
+  // activation with the NEXT matrix's P+- (see zo_gemm.h)
+  const float* xPp;
+  const float* xPm;
+  int xr, xrps, tpart_ld;
+  float* tpart;
 };
 
 template <int BN, int EPI, bool BF16>
@@ -239,6 +252,13 @@ __global__ void __launch_bounds__(192, 1)
       tc_fence_after();
       const int row = m0 + q * 32 + lane;
       const bool row_ok = row < p.M;
+      constexpr bool GELU = (EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT);
+      constexpr bool OUT16 = (EPI == EPI_STORE16 || GELU);
+      float tp[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) tp[k] = 0.f;
+      const float* xP = nullptr;
+      if constexpr (EPI == EPI_GELU16_EXT) xP = (row < p.xrps) ? p.xPp : p.xPm;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
@@ -246,35 +266,41 @@ __global__ void __launch_bounds__(192, 1)
         const int col0 = n0 + c;
         if (!row_ok || col0 >= p.N) continue;
         const size_t lin = (size_t)row * p.ldo + col0;
-        constexpr int VEC = (EPI == EPI_STORE16 || EPI == EPI_GELU16) ? 8 : 4;
+        constexpr int VEC = OUT16 ? 8 : 4;
         const bool full = col0 + 32 <= p.N && (lin % VEC) == 0;
-        if constexpr (EPI == EPI_STORE16 || EPI == EPI_GELU16) {
-          if constexpr (EPI == EPI_GELU16) {
+        if constexpr (OUT16) {
+          if constexpr (GELU) {
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
           }
-          uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + (size_t)row * p.ldo + col0;
-          if (full) {
+          uint32_t pk[16];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint4 w;
-              w.x = pack2<BF16>(v[8 * j + 0], v[8 * j + 1]);
-              w.y = pack2<BF16>(v[8 * j + 2], v[8 * j + 3]);
-              w.z = pack2<BF16>(v[8 * j + 4], v[8 * j + 5]);
-              w.w = pack2<BF16>(v[8 * j + 6], v[8 * j + 7]);
-              reinterpret_cast<uint4*>(o)[j] = w;
-            }
-          } else {
+          for (int j = 0; j < 16; ++j) pk[j] = pack2<BF16>(v[2 * j], v[2 * j + 1]);
+          if constexpr (EPI == EPI_GELU16_EXT) {
+            // t_k += a16[row, col] * P[col, k] on the values the next GEMM reads
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               if (col0 + i < p.N) {
-                uint32_t pk = pack2<BF16>(v[i], 0.f);
-                o[i] = (uint16_t)(pk & 0xffff);
+                const float a = unpack16<BF16>(pk[i >> 1], i & 1);
+                const float* pr = xP + (size_t)(col0 + i) * p.xr;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                  if (k < p.xr) tp[k] += a * pr[k];
               }
             }
           }
+          uint16_t* o = reinterpret_cast<uint16_t*>(p.out) + lin;
+          if (full) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              reinterpret_cast<uint4*>(o)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.N) o[i] = (uint16_t)(pk[i >> 1] >> (16 * (i & 1)));
+          }
         } else {
-          float* o = reinterpret_cast<float*>(p.out) + (size_t)row * p.ldo + col0;
+          float* o = reinterpret_cast<float*>(p.out) + lin;
           if (full) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
@@ -299,6 +325,12 @@ __global__ void __launch_bounds__(192, 1)
               }
             }
           }
+        }
+      }
+      if constexpr (EPI == EPI_GELU16_EXT) {
+        if (row_ok) {
+          float* dst = p.tpart + ((size_t)(n0 / BN) * p.tpart_ld + row) * p.xr;
+          for (int k = 0; k < p.xr && k < 8; ++k) dst[k] = tp[k];
         }
       }
       tc_fence_before();
@@ -391,6 +423,12 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.n_tiles = (g.N + BN - 1) / BN;
   p.ldo = g.ldo;
   p.out = g.out;
+  p.xPp = g.xPp;
+  p.xPm = g.xPm;
+  p.xr = g.xr;
+  p.xrps = g.xrps;
+  p.tpart_ld = g.tpart_ld;
+  p.tpart = g.tpart;
   k_gemm<BN, EPI, BF16><<<g.grid, 192, C::SMEM, st>>>(g.tmA, g.tmB, p);
 }
 
@@ -399,6 +437,7 @@ static void launch_e(const GemmDesc& g, cudaStream_t st) {
   switch (g.epi) {
     case EPI_STORE16: launch_t<BN, EPI_STORE16, BF16>(g, st); break;
     case EPI_GELU16: launch_t<BN, EPI_GELU16, BF16>(g, st); break;
+    case EPI_GELU16_EXT: launch_t<BN, EPI_GELU16_EXT, BF16>(g, st); break;
     case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16>(g, st); break;
     default: launch_t<BN, EPI_STORE32, BF16>(g, st); break;
   }

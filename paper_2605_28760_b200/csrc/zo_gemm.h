@@ -11,6 +11,8 @@ enum EpiKind : int {
   EPI_GELU16 = 1,   // out16[r, c] = gelu_tanh(acc)            (ff_up, model.py:145-146,197)
   EPI_RESID32 = 2,  // x32[r, c] += acc                        (attn_out / ff_down residual)
   EPI_STORE32 = 3,  // out32[r, c] = acc                       (LM-head logits rows)
+  EPI_GELU16_EXT = 4,  // EPI_GELU16 + per-tile partial t_k = sum_c a16[r,c] P[c,k] for the
+                       // next GEMM's LoRA K-extension (tpart[n_tile][r][k], deterministic)
 };
 
 // D[M, N] = A[M, Kp] * B[N, Kp]^T, both operands K-major 16-bit, fp32 accumulate.
@@ -26,6 +28,11 @@ struct GemmDesc {
   void* out = nullptr;
   int ldo = 0;          // output leading dimension (elements)
   int grid = 0;         // persistent CTAs
+  // EPI_GELU16_EXT only
+  const float* xPp = nullptr;
+  const float* xPm = nullptr;
+  int xr = 0, xrps = 0, tpart_ld = 0;
+  float* tpart = nullptr;
 };
 
 // 2-D K-major tensor map over a row-major [rows, cols] 16-bit matrix (row stride ld elements).

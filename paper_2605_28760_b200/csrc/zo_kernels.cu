@@ -80,25 +80,20 @@ __device__ __forceinline__ void write_ext(void* out, size_t base, int k, float t
   }
 }
 
-// Row-wise t_k = sum_i a_i P[i, k] over a row cached in shared memory, k in chunks of 8.
-__device__ void row_ext(const float* row, int K, const float* P, int r, void* out, size_t ext_base, int ext_terms,
-                        bool bf16, float* red) {
-  for (int k0 = 0; k0 < r; k0 += 8) {
-    float acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-    const int kn = min(8, r - k0);
-    for (int i = threadIdx.x; i < K; i += blockDim.x) {
-      const float a = row[i];
-      const float* pr = P + (size_t)i * r + k0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < kn) acc[q] += a * pr[q];
-    }
-    block_sum<8>(acc, red);
-    if (threadIdx.x == 0)
-      for (int q = 0; q < kn; ++q) write_ext(out, ext_base, k0 + q, acc[q], ext_terms, bf16);
-  }
+// ------------------------------------------------------------------ fused-extension finalize
+__global__ void k_ext_finalize(const float* __restrict__ tpart, int ntiles, int ld, int M, int r, void* __restrict__ a,
+                               int lda, int K, int ext_terms, bool bf16) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M * r) return;
+  const int row = i / r, k = i % r;
+  float t = 0.f;
+  for (int j = 0; j < ntiles; ++j) t += tpart[((size_t)j * ld + row) * r + k];
+  write_ext(a, (size_t)row * lda + K, k, t, ext_terms, bf16);
+}
+
+void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
+                         int ext_terms, bool bf16, cudaStream_t st) {
+  k_ext_finalize<<<(M * r + 255) / 256, 256, 0, st>>>(tpart, ntiles, ld, M, r, a, lda, K, ext_terms, bf16);
 }
 
 // ------------------------------------------------------------------ embed
@@ -125,154 +120,119 @@ void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const 
   k_embed<<<nrows, 256, 0, st>>>(x32, tokens, B, T, d, E64, E16, bf16, Pplus, Pminus, Ve32, r, pe);
 }
 
-// ------------------------------------------------------------------ LN (+ extension)
-__global__ void k_ln_ext(const float* __restrict__ x32, const float* __restrict__ g, const float* __restrict__ bta,
-                         int d, void* __restrict__ out, int ldo, bool bf16, const float* __restrict__ Pp,
-                         const float* __restrict__ Pm, int r, int rows_per_sign, int ext_terms) {
-  extern __shared__ float sh[];  // d floats row cache + reduction scratch
-  float* row = sh;
-  float* red = sh + d;
-  const int m = blockIdx.x;
-  const float* x = x32 + (size_t)m * d;
-  float acc[1] = {0.f};
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float v = x[i];
-    row[i] = v;
-    acc[0] += v;
+// ------------------------------------------------------------------ LN (+ extension), warp per row
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void store4_16(void* out, size_t i, float a, float b, float c, float d, bool bf16) {
+  uint2 w;
+  w.x = (uint32_t)to16(a, bf16) | ((uint32_t)to16(b, bf16) << 16);
+  w.y = (uint32_t)to16(c, bf16) | ((uint32_t)to16(d, bf16) << 16);
+  *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(out) + i) = w;
+}
+
+// h = LN(x) -> out[:, :d] (16-bit), ext columns t = h . P_s (fp32 h), one warp per row,
+// float4 loads (the row stays in L1 across the three passes).
+__global__ void __launch_bounds__(256) k_ln_ext(const float* __restrict__ x32, const float* __restrict__ g,
+                                                const float* __restrict__ bta, int M, int d, void* __restrict__ out,
+                                                int ldo, bool bf16, const float* __restrict__ Pp,
+                                                const float* __restrict__ Pm, int r, int rows_per_sign,
+                                                int ext_terms) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float4* x = reinterpret_cast<const float4*>(x32 + (size_t)row * d);
+  const int n4 = d >> 2;
+  float s = 0.f;
+#pragma unroll 4
+  for (int i = lane; i < n4; i += 32) {
+    const float4 v = x[i];
+    s += (v.x + v.y) + (v.z + v.w);
   }
-  block_sum<1>(acc, red);
-  const float mu = acc[0] / (float)d;
-  acc[0] = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float c = row[i] - mu;
-    acc[0] += c * c;
+  const float mu = warp_sum(s) / (float)d;
+  s = 0.f;
+#pragma unroll 4
+  for (int i = lane; i < n4; i += 32) {
+    const float4 v = x[i];
+    const float a = v.x - mu, b = v.y - mu, c = v.z - mu, e = v.w - mu;
+    s += (a * a + b * b) + (c * c + e * e);
   }
-  block_sum<1>(acc, red);
-  const float sd = sqrtf(acc[0] / (float)d + 1e-5f);
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float h = (row[i] - mu) / sd * g[i] + bta[i];
-    row[i] = h;
-    st16(out, (size_t)m * ldo + i, h, bf16);
-  }
-  __syncthreads();
-  if (r > 0) {
-    const float* P = (m < rows_per_sign) ? Pp : Pm;
-    row_ext(row, d, P, r, out, (size_t)m * ldo + d, ext_terms, bf16, red);
+  const float rsd = 1.0f / sqrtf(warp_sum(s) / (float)d + 1e-5f);
+  const float* P = (row < rows_per_sign) ? Pp : Pm;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(bta);
+  for (int k0 = 0; k0 < (r > 0 ? r : 1); k0 += 8) {
+    float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int kn = min(8, r - k0);
+    for (int i = lane; i < n4; i += 32) {
+      const float4 v = x[i], gg = g4[i], bb = b4[i];
+      float h[4] = {(v.x - mu) * rsd * gg.x + bb.x, (v.y - mu) * rsd * gg.y + bb.y,
+                    (v.z - mu) * rsd * gg.z + bb.z, (v.w - mu) * rsd * gg.w + bb.w};
+      if (k0 == 0) store4_16(out, (size_t)row * ldo + 4 * i, h[0], h[1], h[2], h[3], bf16);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float* pr = P + (size_t)(4 * i + e) * r + k0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < kn) t[q] += h[e] * pr[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = warp_sum(t[q]);
+    if (lane == 0)
+      for (int q = 0; q < kn; ++q) write_ext(out, (size_t)row * ldo + d, k0 + q, t[q], ext_terms, bf16);
   }
 }
 
 void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
                    bool bf16, const float* Pplus, const float* Pminus, int r, int rows_per_sign, int ext_terms,
                    cudaStream_t st) {
-  const size_t smem = (size_t)(d + 32 * 8) * sizeof(float);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    ZO_CUDA_TRY(cudaFuncSetAttribute(k_ln_ext, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
-  k_ln_ext<<<M, 256, smem, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms);
+  if (d % 4 || ldo % 4) throw Error(ZO_ERR_DIMENSION, "LN rows must be multiples of 4");
+  k_ln_ext<<<(M + 7) / 8, 256, 0, st>>>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign,
+                                        ext_terms);
 }
 
 // ------------------------------------------------------------------ extension of a 16-bit activation
-__global__ void k_ext(void* __restrict__ a, int lda, int K, bool bf16, const float* __restrict__ Pp,
-                      const float* __restrict__ Pm, int r, int rows_per_sign, int ext_terms) {
-  __shared__ float red[32 * 8];
-  const int m = blockIdx.x;
-  const float* P = (m < rows_per_sign) ? Pp : Pm;
-  const uint16_t* row = reinterpret_cast<const uint16_t*>(a) + (size_t)m * lda;
+// t_k = a[row, :K] . P_s[:, k] -> ext columns, one warp per row, 16-byte loads.
+__global__ void __launch_bounds__(256) k_ext(void* __restrict__ a, int lda, int M, int K, bool bf16,
+                                             const float* __restrict__ Pp, const float* __restrict__ Pm, int r,
+                                             int rows_per_sign, int ext_terms) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float* P = (row < rows_per_sign) ? Pp : Pm;
+  const uint4* src = reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a) + (size_t)row * lda);
+  const int n8 = K >> 3;
   for (int k0 = 0; k0 < r; k0 += 8) {
-    float acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const int kn = min(8, r - k0);
-    for (int i = threadIdx.x; i < K; i += blockDim.x) {
-      const float v = from16(row[i], bf16);
-      const float* pr = P + (size_t)i * r + k0;
+    for (int i = lane; i < n8; i += 32) {
+      const uint4 w = src[i];
+      const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < kn) acc[q] += v * pr[q];
+      for (int e = 0; e < 8; ++e) {
+        const float v = from16((uint16_t)(ww[e >> 1] >> (16 * (e & 1))), bf16);
+        const float* pr = P + (size_t)(8 * i + e) * r + k0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < kn) t[q] += v * pr[q];
+      }
     }
-    block_sum<8>(acc, red);
-    if (threadIdx.x == 0)
-      for (int q = 0; q < kn; ++q) write_ext(a, (size_t)m * lda + K, k0 + q, acc[q], ext_terms, bf16);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t[q] = warp_sum(t[q]);
+    if (lane == 0)
+      for (int q = 0; q < kn; ++q) write_ext(a, (size_t)row * lda + K, k0 + q, t[q], ext_terms, bf16);
   }
 }
 
 void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, const float* Pminus, int r,
                 int rows_per_sign, int ext_terms, cudaStream_t st) {
   if (r <= 0) return;
-  k_ext<<<M, 256, 0, st>>>(a, lda, K, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms);
-}
-
-// ------------------------------------------------------------------ attention (T <= 128)
-__global__ void k_attention(const void* __restrict__ qkv, int ldq, void* __restrict__ ctx, int ldc, int T, int H,
-                            int dh, bool bf16) {
-  extern __shared__ float sm[];
-  const int seq = blockIdx.x, h = blockIdx.y;
-  const int d = H * dh, ld = dh + 1;
-  float* q = sm;
-  float* k = q + T * ld;
-  float* v = k + T * ld;
-  for (int idx = threadIdx.x; idx < T * dh; idx += blockDim.x) {
-    const int t = idx / dh, c = idx % dh;
-    const size_t base = (size_t)(seq * T + t) * ldq + (size_t)h * dh + c;
-    q[t * ld + c] = ld16(qkv, base, bf16);
-    k[t * ld + c] = ld16(qkv, base + d, bf16);
-    v[t * ld + c] = ld16(qkv, base + 2 * d, bf16);
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const float rs = sqrtf((float)dh);
-  for (int i = warp; i < T; i += nw) {
-    float s[4];
-    float mx = -CUDART_INF_F;
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      const int j = lane + 32 * jj;
-      s[jj] = -CUDART_INF_F;
-      if (j < T && j <= i) {
-        float acc = 0.f;
-        for (int c = 0; c < dh; ++c) acc += q[i * ld + c] * k[j * ld + c];
-        s[jj] = acc / rs;
-      }
-      mx = fmaxf(mx, s[jj]);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.f;
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) {
-      s[jj] = (s[jj] == -CUDART_INF_F) ? 0.f : expf(s[jj] - mx);
-      sum += s[jj];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) s[jj] = s[jj] / sum;
-    // every lane takes part in every shuffle, also when dh < 32
-    for (int c0 = 0; c0 < dh; c0 += 32) {
-      const int c = c0 + lane;
-      const int cc = c < dh ? c : dh - 1;
-      float acc = 0.f;
-      for (int j = 0; j <= i; ++j) {
-        const float pj = __shfl_sync(0xffffffffu, s[j >> 5], j & 31);
-        acc += pj * v[j * ld + cc];
-      }
-      if (c < dh) st16(ctx, (size_t)(seq * T + i) * ldc + (size_t)h * dh + c, acc, bf16);
-    }
-  }
-}
-
-void launch_attention(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, int dh, bool bf16,
-                      cudaStream_t st) {
-  if (T > 128) throw Error(ZO_ERR_DIMENSION, "attention kernel supports T <= 128");
-  const size_t smem = (size_t)3 * T * (dh + 1) * sizeof(float);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    ZO_CUDA_TRY(cudaFuncSetAttribute(k_attention, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
-  k_attention<<<dim3(nseq, H), 128, smem, st>>>(qkv, ldq, ctx, ldc, T, H, dh, bf16);
+  if (K % 8 || lda % 8) throw Error(ZO_ERR_DIMENSION, "extension rows must be multiples of 8");
+  k_ext<<<(M + 7) / 8, 256, 0, st>>>(a, lda, M, K, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms);
 }
 
 // ------------------------------------------------------------------ final LN at scored rows

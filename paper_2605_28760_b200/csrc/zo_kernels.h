@@ -22,9 +22,20 @@ void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int 
 // ext columns for a 16-bit activation a[:, :K] already in place (ctx -> attn_out, gelu -> ff_down).
 void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, const float* Pminus, int r,
                 int rows_per_sign, int ext_terms, cudaStream_t st);
+// Fused LoRA-extension partials of an activation producer: tpart[tile][row][k]
+// (tile = head for attention), finished by launch_ext_finalize.
+struct AttnExt {
+  const float* Pp = nullptr;
+  const float* Pm = nullptr;
+  int r = 0, rps = 0, ld = 0;  // rank, rows per sign, rows per tile slab
+  float* tpart = nullptr;      // nullptr: no fused extension
+};
 // causal softmax attention per (sequence, head) (model.py:184-194); qkv [M,3d] -> ctx[:, :d]
 void launch_attention(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, int dh, bool bf16,
-                      cudaStream_t st);
+                      const AttnExt& x, cudaStream_t st);
+// t_k = sum over tiles of tpart[tile][row][k] (fixed order) -> ext columns (hi, lo, hi) of a[:, K:]
+void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
+                         int ext_terms, bool bf16, cudaStream_t st);
 // final LN at scored rows (prompt_len-1+j) of B sequences (both signs counted) -> xs32/xs16, z = xs . V_e
 void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d,
                      int prompt_len, int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r,

@@ -112,7 +112,10 @@ struct zo_ctx {
   SamplerPlan planU, planV, planOne;
   std::vector<StreamDesc> streamsU, streamsV;
   unsigned* flags = nullptr;
-  std::map<int, RowPlan> plans;  // keyed by rows M
+  std::map<int, RowPlan> plans;  // keyed by 2*M + (nsign == 1)
+  float* tpart = nullptr;         // fused LoRA-extension partials [tiles][Mpad][r]
+  int tpart_tiles = 0;
+  bool fused_ext = true;
   // timing
   cudaEvent_t ev[4];
   float last_ms[3] = {0, 0, 0};
@@ -178,8 +181,9 @@ void build_sampler_plan(zo_ctx* c, SamplerPlan& P, std::vector<StreamDesc>& sd) 
   ZO_CUDA_TRY(cudaMemcpy(P.d_chunk_stream, chunk_stream.data(), chunk_stream.size() * 4, cudaMemcpyHostToDevice));
 }
 
-RowPlan& row_plan(zo_ctx* c, int M) {
-  auto it = c->plans.find(M);
+RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
+  const int key = 2 * M + (nsign == 1 ? 1 : 0);
+  auto it = c->plans.find(key);
   if (it != c->plans.end()) return it->second;
   RowPlan rp;
   const int d = c->d.dim;
@@ -195,15 +199,24 @@ RowPlan& row_plan(zo_ctx* c, int M) {
               c->num_sms);
     gemm_plan(lp.out, c->ctxA, M, ldh, o.W16, d, o.ldw, d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
               c->num_sms);
-    gemm_plan(lp.up, c->hA, M, ldh, u.W16, 4 * d, u.ldw, d + c->ext_used, EPI_GELU16, c->bf16, c->gA, ldg,
-              c->num_sms);
+    gemm_plan(lp.up, c->hA, M, ldh, u.W16, 4 * d, u.ldw, d + c->ext_used,
+              c->fused_ext ? EPI_GELU16_EXT : EPI_GELU16, c->bf16, c->gA, ldg, c->num_sms);
+    if (c->fused_ext) {
+      lp.up.xPp = c->Pp + w.u_off;
+      lp.up.xPm = c->Pm + w.u_off;
+      lp.up.xr = c->r;
+      lp.up.xrps = M / nsign;
+      lp.up.tpart_ld = c->Mpad;
+      lp.up.tpart = c->tpart;
+      check((4 * d + lp.up.bn - 1) / lp.up.bn <= c->tpart_tiles, ZO_ERR_INTERNAL, "tpart too small");
+    }
     gemm_plan(lp.down, c->gA, M, ldg, w.W16, d, w.ldw, 4 * d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
               c->num_sms);
     rp.layers.push_back(lp);
   }
   const Matrix& e = c->mats[c->i_embed];
   gemm_plan(rp.lm, c->xs16, S, d, e.W16, c->d.vocab, d, d, EPI_STORE32, c->bf16, c->logits, c->ldl, c->num_sms);
-  return c->plans.emplace(M, std::move(rp)).first->second;
+  return c->plans.emplace(key, std::move(rp)).first->second;
 }
 
 void refresh_shadow(zo_ctx* c, const Matrix& m) {
@@ -222,7 +235,7 @@ void write_vext_all(zo_ctx* c) {
 void do_score(zo_ctx* c, int B, int nsign) {
   const int d = c->d.dim, T = c->T, M = nsign * B * T;
   check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
-  RowPlan& rp = row_plan(c, M);
+  RowPlan& rp = row_plan(c, M, nsign);
   const Matrix& e = c->mats[c->i_embed];
   const int rps = B * T;
   const int ldh = d + c->KE, ldg = 4 * d + c->KE;
@@ -237,13 +250,29 @@ void do_score(zo_ctx* c, int B, int nsign) {
     launch_ln_ext(c->x32, c->ln1g[l], c->ln1b[l], M, d, c->hA, ldh, c->bf16, c->Pp + q.u_off, c->Pm + q.u_off, c->r,
                   rps, c->ext_terms, c->st);
     gemm_launch(lp.qkv, c->st);
-    launch_attention(c->qkv, 3 * d, c->ctxA, ldh, nsign * B, T, c->d.n_heads, c->dh, c->bf16, c->st);
-    launch_ext(c->ctxA, ldh, M, d, c->bf16, c->Pp + o.u_off, c->Pm + o.u_off, c->r, rps, c->ext_terms, c->st);
+    AttnExt ax;
+    if (c->fused_ext) {
+      ax.Pp = c->Pp + o.u_off;
+      ax.Pm = c->Pm + o.u_off;
+      ax.r = c->r;
+      ax.rps = rps;
+      ax.ld = c->Mpad;
+      ax.tpart = c->tpart;
+    }
+    launch_attention(c->qkv, 3 * d, c->ctxA, ldh, nsign * B, T, c->d.n_heads, c->dh, c->bf16, ax, c->st);
+    if (c->fused_ext)
+      launch_ext_finalize(c->tpart, c->d.n_heads, c->Mpad, M, c->r, c->ctxA, ldh, d, c->ext_terms, c->bf16, c->st);
+    else
+      launch_ext(c->ctxA, ldh, M, d, c->bf16, c->Pp + o.u_off, c->Pm + o.u_off, c->r, rps, c->ext_terms, c->st);
     gemm_launch(lp.out, c->st);
     launch_ln_ext(c->x32, c->ln2g[l], c->ln2b[l], M, d, c->hA, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off, c->r,
                   rps, c->ext_terms, c->st);
     gemm_launch(lp.up, c->st);
-    launch_ext(c->gA, ldg, M, 4 * d, c->bf16, c->Pp + w.u_off, c->Pm + w.u_off, c->r, rps, c->ext_terms, c->st);
+    if (c->fused_ext)
+      launch_ext_finalize(c->tpart, (4 * d + lp.up.bn - 1) / lp.up.bn, c->Mpad, M, c->r, c->gA, ldg, 4 * d,
+                          c->ext_terms, c->bf16, c->st);
+    else
+      launch_ext(c->gA, ldg, M, 4 * d, c->bf16, c->Pp + w.u_off, c->Pm + w.u_off, c->r, rps, c->ext_terms, c->st);
     gemm_launch(lp.down, c->st);
   }
   launch_final_ln(c->x32, c->lnfg, c->lnfb, B * nsign, T, d, c->d.prompt_len, c->d.opt_len, c->xs32, c->xs16,
@@ -420,6 +449,9 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->tok = c->mem.get<int32_t>((size_t)d.max_batch * c->T);
   c->gold = c->mem.get<int32_t>((size_t)2 * d.max_batch * d.opt_len);
   c->d_step = c->mem.get<uint64_t>(1);
+  c->fused_ext = d.rank <= 8;
+  c->tpart_tiles = std::max((int)ceil_div(4 * D, 64), d.n_heads);
+  if (c->fused_ext) c->tpart = c->mem.get<float>((size_t)c->tpart_tiles * c->Mpad * d.rank);
   // positional table: pos_encoding(T, d) (model.py:128-136), float64 -> float32
   {
     std::vector<float> pe((size_t)c->T * d.dim);
