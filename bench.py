@@ -110,6 +110,20 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(model):
+    """DRAM bytes (read + write) of one launch of each of the four layer GEMMs, from the
+    committed `ncu --set full` capture (profiles/), or None when not captured for this model."""
+    import csv
+    p = os.path.join(HERE, "profiles", "r01_ncu_full_gemm_opt13b_layer1.csv")
+    if model != "opt-13b" or not os.path.exists(p):
+        return None
+    tot = 0.0
+    with open(p) as f:
+        for row in csv.DictReader(f):
+            tot += (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e6  # MB
+    return tot
+
+
 def launches_per_step(L: int, n_mats: int, window: bool) -> int:
     # set_step + sampler(U) 5 + prep + embed + 9/layer + final LN + LM GEMM + loss + coefficient + update
     n = 1 + 5 + 1 + 1 + 9 * L + 4 + 1
@@ -302,7 +316,7 @@ def main():
         lay_fl = sum(g[n]["tflops"] * g[n]["ms"] * 1e-3 * 1e12 for n in names[:4])
         achieved = lay_fl / (lay_ms * 1e-3) / 1e12
         line["roofline"] = {"bound": "tensor", "achieved": achieved, "peak": tf_peak, "unit": "TFLOP/s",
-                            "frac": achieved / tf_peak, "traffic": None,
+                            "frac": achieved / tf_peak, "traffic": ncu_traffic(args.model),
                             "kernel": "k_gemm (tcgen05 kind::f16, layer GEMMs qkv+attn_out+ff_up+ff_down)",
                             "peak_kind": f"{peak_kind} bf16 burst (MEASURED_PEAKS.json)", "per_gemm": g,
                             "share_of_step": lay_ms * mcfg.n_layers / ms_step}

@@ -1,0 +1,134 @@
+"""Level-A drop-in: run the UNMODIFIED reference (zoserve) with the B200 scorer.
+
+* ``ReferenceScorer(params, mcfg, state)`` implements zoserve's ``scorer``
+  protocol (zo_engine.py:340-346) for ``zoserve.zo_engine.lozo_step(...,
+  scorer=...)`` / ``estimate_coefficient``: on the +1 call it uploads the
+  reference AdapterState's window slot (A, V) and probe (U) to the device,
+  scores both probes in one fused launch and returns L+; the -1 call returns
+  the cached L-.  Pure: it never writes the reference's params or state.
+* ``install_into_zoserve(zoserve)`` patches ``zoserve.runtime.forward_score``
+  (the name ``_MeteredScorer`` calls, runtime.py:28,168-177) and
+  ``zoserve.runtime._fold_all`` (runtime.py:242-250) so the unmodified
+  ``run_serving_path`` scores on the GPU; folds run on the host (the
+  reference's own arithmetic) and on the device replica with the same slot
+  values, so both copies stay bit-identical (k_fold_shadow restates
+  numerics.py:207-235 exactly).
+
+The reference state is duck-typed: ``entries[lid].window_slot/.perturb_slot``
+with ``.A, .B, .scale`` and ``perturb_sign``, ``epsilon`` (adapter.py:53-197).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .engine import A as SLOT_A, U as SLOT_U, V as SLOT_V, ZoEngine
+from .errors import ConfigError
+from .numerics import canonical_mean
+
+
+def _engine_from_reference(params, mcfg, rank: int, batch_size: int, precision: str) -> ZoEngine:
+    eng = ZoEngine(mcfg.vocab, mcfg.dim, mcfg.n_layers, mcfg.n_heads, mcfg.prompt_len, opt_len=1,
+                   max_batch=max(16, batch_size), rank=rank, precision=precision)
+    eng.upload(params)
+    return eng
+
+
+def upload_reference_slots(eng: ZoEngine, state, with_probe: bool) -> None:
+    """Window A/V and probe U of a reference AdapterState -> device arenas."""
+    r = eng.rank
+    A = {l: np.zeros((eng.shapes[l][0], r)) for l in eng.lids}
+    U = {l: np.zeros((eng.shapes[l][0], r)) for l in eng.lids}
+    V = eng.split(SLOT_V, eng.get_slot(SLOT_V))
+    for lid, e in state.entries.items():
+        if any(s.rank for s in getattr(e, "update_slots", [])):
+            raise ConfigError("frozen update slots present: fold before GPU scoring")
+        B = None
+        ws = e.window_slot
+        if ws is not None and ws.rank:
+            if ws.scale != 1.0:
+                raise ConfigError("window slot scale must be 1")
+            A[lid], B = ws.A, ws.B
+        ps = e.perturb_slot
+        if with_probe and ps is not None and ps.rank:
+            if ps.scale != 1.0:
+                raise ConfigError("probe scale must be 1 for the lozo device scorer")
+            U[lid] = ps.A
+            if B is not None and not np.array_equal(B, ps.B):
+                raise ConfigError("window slot and probe must share V")
+            B = ps.B
+        if B is not None:
+            V[lid] = B
+    eng.set_slot(SLOT_V, eng.join(SLOT_V, V))
+    eng.set_slot(SLOT_A, eng.join(SLOT_A, A))
+    eng.set_slot(SLOT_U, eng.join(SLOT_U, U))
+
+
+class ReferenceScorer:
+    """zoserve ``scorer`` on the B200 engine (fused +-eps pair, cached L-)."""
+
+    def __init__(self, params, mcfg, state, rank: int = 2, batch_size: int = 16, precision: str = "fp16",
+                 engine: ZoEngine | None = None):
+        self.state = state
+        self.eng = engine or _engine_from_reference(params, mcfg, rank, batch_size, precision)
+        self._cached = None
+
+    def _tokens(self, batch):
+        gold = batch.option_array()[batch.golds]
+        return np.concatenate([batch.prompts, gold], axis=1), gold
+
+    def __call__(self, batch) -> float:
+        sign = self.state.perturb_sign
+        key = batch.batch_id
+        if sign == -1 and self._cached is not None and self._cached[0] == key:
+            lm = self._cached[1]
+            self._cached = None
+            return lm
+        tokens, gold = self._tokens(batch)
+        probe = sign != 0 and any(e.perturb_slot is not None for e in self.state.entries.values())
+        upload_reference_slots(self.eng, self.state, probe)
+        if not probe:
+            self.eng.prepare_probe(self.state.epsilon, 1)
+            return canonical_mean(self.eng.score(tokens, gold, nsign=1)[0])
+        self.eng.prepare_probe(self.state.epsilon, 0)
+        nll = self.eng.score(tokens, np.stack([gold, gold]), nsign=2)
+        lp, lm = canonical_mean(nll[0]), canonical_mean(nll[1])
+        if sign == 1:
+            self._cached = (key, lm)
+            return lp
+        return lm
+
+
+def install_into_zoserve(zoserve, rank: int = 2, batch_size: int = 16, precision: str = "fp16"):
+    """Patch the unmodified reference so run_serving_path scores on the B200.
+    Returns an ``uninstall()`` callable."""
+    rt = zoserve.runtime
+    orig_fs, orig_fold = rt.forward_score, rt._fold_all
+    engines: dict[int, tuple[object, ReferenceScorer]] = {}
+
+    def scorer_for(params, cfg, state):
+        ent = engines.get(id(params))
+        if ent is None or ent[0] is not params:
+            ent = (params, ReferenceScorer(params, cfg, state, rank, batch_size, precision))
+            engines[id(params)] = ent
+        ent[1].state = state
+        return ent[1]
+
+    def forward_score(params, cfg, batch, view=None, precision_arg="real64"):
+        if view is None:
+            return orig_fs(params, cfg, batch, view, precision_arg)
+        state = view.__closure__[0].cell_contents  # AdapterState.view() closure (adapter.py:181-190)
+        return scorer_for(params, cfg, state)(batch)
+
+    def fold_all(state, params, meter):
+        ent = engines.get(id(params))
+        if ent is not None:
+            upload_reference_slots(ent[1].eng, state, with_probe=False)
+            ent[1].eng.fold()  # device replica: same k-ascending float64 arithmetic
+        return orig_fold(state, params, meter)
+
+    rt.forward_score, rt._fold_all = forward_score, fold_all
+
+    def uninstall():
+        rt.forward_score, rt._fold_all = orig_fs, orig_fold
+
+    return uninstall
