@@ -150,9 +150,62 @@ struct GemmParams {
   const float* xPm;
   int xr, xrps, tpart_ld;
   float* tpart;
+  // stream-K (sk = 1): CTA c owns global k-iterations [c*sk_w, min((c+1)*sk_w, tiles*num_kb));
+  // a tile split between CTAs c-1 (k-start part, owns the epilogue) and c (k-end part,
+  // publishes an fp32 partial in sk_ws[c] + sk_flags[c]) is summed in that fixed order.
+  int sk, sk_w, sk_dp;
+  float* sk_ws;
+  unsigned* sk_flags;
 };
 
-template <int BN, int EPI, bool BF16>
+// Work segments of one CTA: (tile, k-block range).  Data-parallel phase: whole
+// tiles blockIdx + i*grid below sk_dp (M-fastest order, so the CTAs resident at
+// once share weight tiles in L2); stream-K phase (sk = 1): the remaining tiles'
+// k-iterations split evenly, CTA c owning [sk_dp*kb + c*sk_w, +sk_w).
+struct SegIter {
+  int cursor, hi, dp;
+  __device__ __forceinline__ void init(const GemmParams& p) {
+    dp = 1;
+    cursor = blockIdx.x;
+    hi = p.sk ? p.sk_dp : p.m_tiles * p.n_tiles;
+  }
+  __device__ __forceinline__ bool next(const GemmParams& p, int& tile, int& k0, int& k1) {
+    if (dp) {
+      if (cursor < hi) {
+        tile = cursor;
+        k0 = 0;
+        k1 = p.num_kb;
+        cursor += gridDim.x;
+        return true;
+      }
+      if (!p.sk) return false;
+      dp = 0;
+      const int total = p.m_tiles * p.n_tiles * p.num_kb;
+      cursor = p.sk_dp * p.num_kb + blockIdx.x * p.sk_w;
+      hi = min(total, cursor + p.sk_w);
+    }
+    if (cursor >= hi) return false;
+    tile = cursor / p.num_kb;
+    k0 = cursor - tile * p.num_kb;
+    k1 = min(p.num_kb, hi - tile * p.num_kb);
+    cursor = tile * p.num_kb + k1;
+    return true;
+  }
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int BN, int EPI, bool BF16, int XR>
 __global__ void __launch_bounds__(192, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
   using C = GemmCfg<BN>;
@@ -196,9 +249,12 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      SegIter si;
+      si.init(p);
+      int t, k0, k1;
+      while (si.next(p, t, k0, k1)) {
         const int m0 = (t % p.m_tiles) * C::BM, n0 = (t / p.m_tiles) * BN;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
           mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
@@ -218,20 +274,23 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      SegIter si;
+      si.init(p);
+      int t, k0, k1;
+      for (; si.next(p, t, k0, k1); ++it) {
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
+        for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
           const uint64_t ad = sw128_desc(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::B_BYTES));
           const int ks = (kb == p.num_kb - 1) ? p.last_ksteps : 4;
           for (int k = 0; k < ks; ++k)
-            tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+            tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb > k0 || k > 0) ? 1u : 0u);
           tc_commit(empty0 + 8 * stage);
           if (++stage == C::STAGES) {
             stage = 0;
@@ -243,15 +302,44 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const int erow = q * 32 + lane;  // row within the 128-row tile
     int it = 0;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+    SegIter si;
+    si.init(p);
+    int t, k0, k1;
+    for (; si.next(p, t, k0, k1); ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       const int m0 = (t % p.m_tiles) * C::BM, n0 = (t / p.m_tiles) * BN;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
-      const int row = m0 + q * 32 + lane;
+      const int row = m0 + erow;
       const bool row_ok = row < p.M;
+      if (k0 > 0) {
+        // k-end part of a split tile: publish the raw fp32 partial for CTA blockIdx-1
+        float* ws = p.sk_ws + ((size_t)blockIdx.x * C::BM + erow) * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            reinterpret_cast<float4*>(ws + c)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) st_release(p.sk_flags + blockIdx.x, 1u);
+        continue;
+      }
+      const bool split = k1 < p.num_kb;  // k-start part: add the partial of CTA blockIdx+1
+      const float* wsin = split ? p.sk_ws + ((size_t)(blockIdx.x + 1) * C::BM + erow) * BN : nullptr;
+      if (split) {
+        for (uint32_t i = 0; ld_acquire(p.sk_flags + blockIdx.x + 1) == 0u; ++i)
+          if (i > (1u << 28)) __trap();
+      }
       constexpr bool GELU = (EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT);
       constexpr bool OUT16 = (EPI == EPI_STORE16 || GELU);
       float tp[8];
@@ -259,10 +347,59 @@ __global__ void __launch_bounds__(192, 1)
       for (int k = 0; k < 8; ++k) tp[k] = 0.f;
       const float* xP = nullptr;
       if constexpr (EPI == EPI_GELU16_EXT) xP = (row < p.xrps) ? p.xPp : p.xPm;
+      if constexpr (EPI == EPI_RESID32) {
+        // fast path: whole tile row in range -> residual loads for chunk c+1 are in
+        // flight while chunk c is added and stored
+        const size_t lin0 = (size_t)row * p.ldo + n0;
+        // warp-uniform (tcgen05.ld is .sync.aligned)
+        if (__all_sync(0xffffffffu, row_ok && n0 + BN <= p.N && (lin0 % 4) == 0)) {
+          float* o = reinterpret_cast<float*>(p.out) + lin0;
+          float4 xa[8], xb[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) xa[j] = reinterpret_cast<const float4*>(o)[j];
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            if (c + 32 < BN) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) xb[j] = reinterpret_cast<const float4*>(o + c + 32)[j];
+            }
+            float v[32];
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+            if (split) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 w = reinterpret_cast<const float4*>(wsin + c)[j];
+                v[4 * j] += w.x;
+                v[4 * j + 1] += w.y;
+                v[4 * j + 2] += w.z;
+                v[4 * j + 3] += w.w;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4*>(o + c)[j] =
+                  make_float4(v[4 * j] + xa[j].x, v[4 * j + 1] + xa[j].y, v[4 * j + 2] + xa[j].z,
+                              v[4 * j + 3] + xa[j].w);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) xa[j] = xb[j];
+          }
+          goto tile_done;
+        }
+      }
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+        if (split) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 w = reinterpret_cast<const float4*>(wsin + c)[j];
+            v[4 * j] += w.x;
+            v[4 * j + 1] += w.y;
+            v[4 * j + 2] += w.z;
+            v[4 * j + 3] += w.w;
+          }
+        }
         const int col0 = n0 + c;
         if (!row_ok || col0 >= p.N) continue;
         const size_t lin = (size_t)row * p.ldo + col0;
@@ -282,10 +419,16 @@ __global__ void __launch_bounds__(192, 1)
             for (int i = 0; i < 32; ++i) {
               if (col0 + i < p.N) {
                 const float a = unpack16<BF16>(pk[i >> 1], i & 1);
-                const float* pr = xP + (size_t)(col0 + i) * p.xr;
+                if constexpr (XR < 8) {
+                  const float* pr = xP + (size_t)(col0 + i) * XR;
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                  if (k < p.xr) tp[k] += a * pr[k];
+                  for (int k = 0; k < XR; ++k) tp[k] += a * pr[k];
+                } else {
+                  const float* pr = xP + (size_t)(col0 + i) * p.xr;
+#pragma unroll
+                  for (int k = 0; k < 8; ++k)
+                    if (k < p.xr) tp[k] += a * pr[k];
+                }
               }
             }
           }
@@ -302,15 +445,19 @@ __global__ void __launch_bounds__(192, 1)
         } else {
           float* o = reinterpret_cast<float*>(p.out) + lin;
           if (full) {
+            float4 xr4[8];
+            if constexpr (EPI == EPI_RESID32) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) xr4[j] = reinterpret_cast<const float4*>(o)[j];
+            }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
               if constexpr (EPI == EPI_RESID32) {
-                float4 x = reinterpret_cast<float4*>(o)[j];
-                w.x += x.x;
-                w.y += x.y;
-                w.z += x.z;
-                w.w += x.w;
+                w.x += xr4[j].x;
+                w.y += xr4[j].y;
+                w.z += xr4[j].z;
+                w.w += xr4[j].w;
               }
               reinterpret_cast<float4*>(o)[j] = w;
             }
@@ -326,6 +473,11 @@ __global__ void __launch_bounds__(192, 1)
             }
           }
         }
+      }
+    tile_done:
+      if (split) {
+        named_bar_sync(1, 128);
+        if (warp == 2 && lane == 0) p.sk_flags[blockIdx.x + 1] = 0u;  // re-arm for the next launch
       }
       if constexpr (EPI == EPI_GELU16_EXT) {
         if (row_ok) {
@@ -406,12 +558,13 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
   make_tmap_2d(&g.tmB, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)bn, bf16);
 }
 
-template <int BN, int EPI, bool BF16>
+template <int BN, int EPI, bool BF16, int XR>
 static void launch_t(const GemmDesc& g, cudaStream_t st) {
   using C = GemmCfg<BN>;
   static bool attr_set = false;
   if (!attr_set) {
-    ZO_CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    ZO_CUDA_TRY(
+        cudaFuncSetAttribute(k_gemm<BN, EPI, BF16, XR>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     attr_set = true;
   }
   GemmParams p;
@@ -429,18 +582,47 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.xrps = g.xrps;
   p.tpart_ld = g.tpart_ld;
   p.tpart = g.tpart;
-  k_gemm<BN, EPI, BF16><<<g.grid, 192, C::SMEM, st>>>(g.tmA, g.tmB, p);
+  p.sk = g.sk;
+  p.sk_w = g.sk_w;
+  p.sk_dp = g.sk_dp;
+  p.sk_ws = g.sk_ws;
+  p.sk_flags = g.sk_flags;
+  k_gemm<BN, EPI, BF16, XR><<<g.grid, 192, C::SMEM, st>>>(g.tmA, g.tmB, p);
 }
 
 template <int BN, bool BF16>
 static void launch_e(const GemmDesc& g, cudaStream_t st) {
   switch (g.epi) {
-    case EPI_STORE16: launch_t<BN, EPI_STORE16, BF16>(g, st); break;
-    case EPI_GELU16: launch_t<BN, EPI_GELU16, BF16>(g, st); break;
-    case EPI_GELU16_EXT: launch_t<BN, EPI_GELU16_EXT, BF16>(g, st); break;
-    case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16>(g, st); break;
-    default: launch_t<BN, EPI_STORE32, BF16>(g, st); break;
+    case EPI_STORE16: launch_t<BN, EPI_STORE16, BF16, 0>(g, st); break;
+    case EPI_GELU16: launch_t<BN, EPI_GELU16, BF16, 0>(g, st); break;
+    case EPI_GELU16_EXT:
+      if (g.xr == 1) launch_t<BN, EPI_GELU16_EXT, BF16, 1>(g, st);
+      else if (g.xr == 2) launch_t<BN, EPI_GELU16_EXT, BF16, 2>(g, st);
+      else if (g.xr == 4) launch_t<BN, EPI_GELU16_EXT, BF16, 4>(g, st);
+      else launch_t<BN, EPI_GELU16_EXT, BF16, 8>(g, st);
+      break;
+    case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16, 0>(g, st); break;
+    default: launch_t<BN, EPI_STORE32, BF16, 0>(g, st); break;
   }
+}
+
+void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
+  const int m_tiles = (g.M + 127) / 128, n_tiles = (g.N + g.bn - 1) / g.bn;
+  const int tiles = m_tiles * n_tiles;
+  // worth it when the last wave is ragged; keep >= one full wave in the stream-K phase so
+  // every CTA owns >= one tile of k-iterations (<= 2 segments per split tile)
+  if (tiles <= num_sms || tiles % num_sms == 0 || !ws || !flags) return;
+  const int dp_waves = tiles / num_sms - 1;
+  const int sk_tiles = tiles - dp_waves * num_sms;
+  const long sk_iters = (long)sk_tiles * g.num_kb;
+  const int w = (int)((sk_iters + num_sms - 1) / num_sms);
+  if (w < g.num_kb) return;
+  g.sk = 1;
+  g.sk_dp = dp_waves * num_sms;
+  g.sk_w = w;
+  g.sk_ws = ws;
+  g.sk_flags = flags;
+  g.grid = num_sms;
 }
 
 void gemm_launch(const GemmDesc& g, cudaStream_t st) {

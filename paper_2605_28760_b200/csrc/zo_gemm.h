@@ -33,7 +33,15 @@ struct GemmDesc {
   const float* xPm = nullptr;
   int xr = 0, xrps = 0, tpart_ld = 0;
   float* tpart = nullptr;
+  // stream-K split of the k-iteration space over the persistent CTAs (gemm_enable_streamk)
+  int sk = 0, sk_w = 0, sk_dp = 0;
+  float* sk_ws = nullptr;       // [grid][128][bn] fp32 partials of split tiles
+  unsigned* sk_flags = nullptr; // [grid], zero between launches
 };
+
+// workspace needed by gemm_enable_streamk: floats / flags
+inline size_t gemm_sk_ws_floats(int num_sms) { return (size_t)num_sms * 128 * 256; }
+void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms);
 
 // 2-D K-major tensor map over a row-major [rows, cols] 16-bit matrix (row stride ld elements).
 void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,

@@ -187,12 +187,87 @@ __global__ void __launch_bounds__(256) k_ln_ext(const float* __restrict__ x32, c
   }
 }
 
+// Register-resident variant: the whole row (NV float4 per lane) is loaded once
+// with NV independent 16-byte loads in flight per lane, then mean, variance
+// (two-pass, in registers), h and the extension dots.  One HBM read of x.
+template <int NV, int XR>
+__global__ void __launch_bounds__(256) k_ln_ext_reg(const float* __restrict__ x32, const float* __restrict__ g,
+                                                    const float* __restrict__ bta, int M, void* __restrict__ out,
+                                                    int ldo, bool bf16, const float* __restrict__ Pp,
+                                                    const float* __restrict__ Pm, int rows_per_sign,
+                                                    int ext_terms) {
+  constexpr int d = NV * 128;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const float4* x = reinterpret_cast<const float4*>(x32 + (size_t)row * d);
+  float4 v[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = x[lane + 32 * j];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+  const float mu = warp_sum(s) / (float)d;
+  s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const float a = v[j].x - mu, b = v[j].y - mu, c = v[j].z - mu, e = v[j].w - mu;
+    s += (a * a + b * b) + (c * c + e * e);
+  }
+  const float rsd = 1.0f / sqrtf(warp_sum(s) / (float)d + 1e-5f);
+  const float* P = (row < rows_per_sign) ? Pp : Pm;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(bta);
+  float t[XR > 0 ? XR : 1];
+#pragma unroll
+  for (int k = 0; k < (XR > 0 ? XR : 1); ++k) t[k] = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i = lane + 32 * j;
+    const float4 gg = g4[i], bb = b4[i];
+    const float h[4] = {(v[j].x - mu) * rsd * gg.x + bb.x, (v[j].y - mu) * rsd * gg.y + bb.y,
+                        (v[j].z - mu) * rsd * gg.z + bb.z, (v[j].w - mu) * rsd * gg.w + bb.w};
+    store4_16(out, (size_t)row * ldo + 4 * i, h[0], h[1], h[2], h[3], bf16);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int k = 0; k < XR; ++k) t[k] += h[e] * P[(size_t)(4 * i + e) * XR + k];
+  }
+#pragma unroll
+  for (int k = 0; k < XR; ++k) t[k] = warp_sum(t[k]);
+  if (lane == 0)
+    for (int k = 0; k < XR; ++k) write_ext(out, (size_t)row * ldo + d, k, t[k], ext_terms, bf16);
+}
+
+template <int NV>
+static bool ln_reg_dispatch(const float* x32, const float* gamma, const float* beta, int M, void* out, int ldo,
+                            bool bf16, const float* Pp, const float* Pm, int r, int rps, int ext_terms,
+                            cudaStream_t st) {
+  const int grid = (M + 7) / 8;
+  switch (r) {
+    case 1: k_ln_ext_reg<NV, 1><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
+    case 2: k_ln_ext_reg<NV, 2><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
+    case 4: k_ln_ext_reg<NV, 4><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
+    default: return false;
+  }
+}
+
 void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
                    bool bf16, const float* Pplus, const float* Pminus, int r, int rows_per_sign, int ext_terms,
                    cudaStream_t st) {
   if (d % 4 || ldo % 4) throw Error(ZO_ERR_DIMENSION, "LN rows must be multiples of 4");
-  k_ln_ext<<<(M + 7) / 8, 256, 0, st>>>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign,
-                                        ext_terms);
+  bool done = false;
+  switch (d) {
+    case 768: done = ln_reg_dispatch<6>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+    case 1024: done = ln_reg_dispatch<8>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+    case 2048: done = ln_reg_dispatch<16>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+    case 4096: done = ln_reg_dispatch<32>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+    case 5120: done = ln_reg_dispatch<40>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+    default: break;
+  }
+  if (!done)
+    k_ln_ext<<<(M + 7) / 8, 256, 0, st>>>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign,
+                                          ext_terms);
 }
 
 // ------------------------------------------------------------------ extension of a 16-bit activation

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -114,6 +115,9 @@ struct zo_ctx {
   unsigned* flags = nullptr;
   std::map<int, RowPlan> plans;  // keyed by 2*M + (nsign == 1)
   float* tpart = nullptr;         // fused LoRA-extension partials [tiles][Mpad][r]
+  float* sk_ws = nullptr;         // stream-K partial tiles
+  unsigned* sk_flags = nullptr;
+  bool streamk = false;  // ZO_STREAMK=1 enables the DP + stream-K tail schedule
   int tpart_tiles = 0;
   bool fused_ext = true;
   // timing
@@ -212,6 +216,8 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
     }
     gemm_plan(lp.down, c->gA, M, ldg, w.W16, d, w.ldw, 4 * d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
               c->num_sms);
+    if (c->streamk)
+      for (GemmDesc* g : {&lp.qkv, &lp.out, &lp.up, &lp.down}) gemm_enable_streamk(*g, c->sk_ws, c->sk_flags, c->num_sms);
     rp.layers.push_back(lp);
   }
   const Matrix& e = c->mats[c->i_embed];
@@ -449,6 +455,9 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->tok = c->mem.get<int32_t>((size_t)d.max_batch * c->T);
   c->gold = c->mem.get<int32_t>((size_t)2 * d.max_batch * d.opt_len);
   c->d_step = c->mem.get<uint64_t>(1);
+  c->sk_ws = c->mem.get<float>(gemm_sk_ws_floats(c->num_sms));
+  c->sk_flags = c->mem.get<unsigned>(c->num_sms + 1);
+  if (const char* e = std::getenv("ZO_STREAMK")) c->streamk = std::atoi(e) != 0;
   c->fused_ext = d.rank <= 8;
   c->tpart_tiles = std::max((int)ceil_div(4 * D, 64), d.n_heads);
   if (c->fused_ext) c->tpart = c->mem.get<float>((size_t)c->tpart_tiles * c->Mpad * d.rank);
@@ -1006,6 +1015,9 @@ extern "C" int zo_test_gemm(int32_t M, int32_t N, int32_t K, int32_t lda, int32_
   if (epi == EPI_RESID32) ZO_CUDA_TRY(cudaMemcpy(C, C_host, (size_t)M * N * 4, cudaMemcpyHostToDevice));
   GemmDesc g;
   gemm_plan(g, A, M, lda, B, N, lda, K, epi, bf16 != 0, C, N, sms);
+  const char* e = std::getenv("ZO_STREAMK");
+  if (!e || std::atoi(e) != 0)
+    gemm_enable_streamk(g, m.get<float>(gemm_sk_ws_floats(sms)), m.get<unsigned>(sms + 1), sms);
   gemm_launch(g, 0);
   ZO_CUDA_TRY(cudaDeviceSynchronize());
   ZO_CUDA_TRY(cudaGetLastError());

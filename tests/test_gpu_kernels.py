@@ -19,7 +19,7 @@ def _h(x, bf16):
 @pytest.mark.parametrize("bf16", [False, True])
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 128), (300, 200, 96), (1024, 768, 832),
                                    (2048, 640, 384), (32, 50272 // 8, 64), (272, 96, 38), (16, 64, 32),
-                                   (272, 32, 134), (2048, 2304, 774)])
+                                   (272, 32, 134), (2048, 2304, 774), (2048, 5120, 832), (1024, 6144, 200)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
 def test_gemm_vs_torch(M, N, K, epi, bf16):
     import torch
@@ -38,6 +38,20 @@ def test_gemm_vs_torch(M, N, K, epi, bf16):
     got = test_gemm(a16, b16, epi=epi, bf16=bf16, C=C0)
     tol = 2e-2 if (epi in (0, 1) and bf16) else 4e-3
     np.testing.assert_allclose(got, ref.numpy(), rtol=tol, atol=tol)
+
+
+@pytest.mark.parametrize("streamk", ["0", "1"])
+def test_gemm_streamk_deterministic(streamk, monkeypatch):
+    """Stream-K splits tiles across CTAs and sums partials in a fixed order: results are
+    run-to-run identical and match the data-parallel schedule within fp32 rounding."""
+    from paper_2605_28760_b200.engine import test_gemm
+    monkeypatch.setenv("ZO_STREAMK", streamk)
+    rng = np.random.default_rng(5)
+    _, a16 = _h(rng.standard_normal((2048, 1024)), False)
+    _, b16 = _h(rng.standard_normal((5120, 1024)) * 0.05, False)
+    r1 = test_gemm(a16, b16, epi=3)
+    r2 = test_gemm(a16, b16, epi=3)
+    np.testing.assert_array_equal(r1, r2)
 
 
 def test_sampler_golden_streams(golden_dir):

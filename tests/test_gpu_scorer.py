@@ -132,3 +132,43 @@ def test_device_step_trajectory(golden_dir, name):
     assert max(max(abs(r["dLp"]), abs(r["dLm"])) for r in rows) <= LOSS_TOL["fp16"] * 1.5, rows
     assert sum(r["sign_ok"] for r in rows) >= 0.9 * len(rows)
     assert eng.sampler_flags()[0] == 0
+
+
+@pytest.mark.parametrize("precision", ["fp16"])
+def test_forward_vs_oracle_streamk_shapes(precision):
+    """A config large enough that every layer GEMM runs stream-K and the fused extension
+    partials span many tiles (d=1024, dh=128, M=2048), against the float64 oracle."""
+    from paper_2605_28760_b200.engine import ZoEngine
+    cfg = R.ModelCfg(vocab=4096, dim=1024, n_layers=2, n_heads=8, prompt_len=63, init_seed=7, init_scale=0.02)
+    eng = ZoEngine(cfg.vocab, cfg.dim, cfg.n_layers, cfg.n_heads, cfg.prompt_len, max_batch=16, rank=2,
+                   precision=precision)
+    eng.init_params(cfg.init_seed, cfg.init_scale)
+    params = R.init_params(cfg)
+    eng.sample_v(42, 0, 50)
+    eng.sample_u(42, 3)
+    A = {lid: 1e-3 * R.gaussian(43, 3, lid, R.ROLE_U, eng.shapes[lid][0], 2) for lid in eng.lids}
+    eng.set_slot(2, eng.join(2, A))
+    splits = R.generate_task(R.TaskCfg(seed=11, vocab=cfg.vocab, prompt_len=63, train_size=64, dev_size=4,
+                                       val_size=4))
+    p, gl, idx = R.sample_minibatch(splits, "train", 42, 3, 16)
+    gold = np.array([[cfg.vocab - 2], [cfg.vocab - 1]])[gl]
+    tokens = np.concatenate([p, gold], axis=1)
+    eng.prepare_probe(1e-3, 0)
+    nll = eng.score(tokens, np.stack([gold, gold]), nsign=2)
+    ref = {}
+    for sign in (1, -1):
+        eff = dict(params)
+        for lid in eng.lids:
+            m, n = eng.shapes[lid]
+            u = R.gaussian(42, 3, lid, R.ROLE_U, m, 2)
+            v = R.gaussian(42, 0, lid, R.ROLE_V, n, 2)
+            eff[lid] = R.compose(params[lid], A[lid], v, u, sign, 1e-3)
+        ref[sign] = R.forward_nll(eff, cfg, tokens, gold)
+    d_ref = R.canonical_mean(ref[1]) - R.canonical_mean(ref[-1])
+    d_got = R.canonical_mean(nll[0]) - R.canonical_mean(nll[1])
+    _report(f"forward_oracle_d1024_{precision}", {
+        "max_abs_nll_plus": float(np.max(np.abs(nll[0] - ref[1]))),
+        "max_abs_nll_minus": float(np.max(np.abs(nll[1] - ref[-1]))), "dL_ref": d_ref, "dL_got": d_got})
+    np.testing.assert_allclose(nll[0], ref[1], atol=NLL_TOL[precision], rtol=0)
+    np.testing.assert_allclose(nll[1], ref[-1], atol=NLL_TOL[precision], rtol=0)
+    assert abs(d_got - d_ref) <= max(DL_REL[precision] * abs(d_ref), 2e-4), (d_got, d_ref)
