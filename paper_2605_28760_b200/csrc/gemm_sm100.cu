@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -62,6 +63,45 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
           dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 2-CTA TMA: both CTAs' bytes complete on the leader CTA's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_2d_cg2(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit_cg2(uint32_t bar) {
+  // arrive on the barrier at this offset in both CTAs of the pair
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accum) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -130,11 +170,11 @@ __device__ __forceinline__ float unpack16(uint32_t w, int hi) {
   else return __half2float(__ushort_as_half(h));
 }
 
-template <int BN>
+template <int BN, int CG = 1>
 struct GemmCfg {
-  static constexpr int BM = 128, BK = 64;
+  static constexpr int BM = 128, BK = 64;  // rows per CTA; a CTA pair (CG = 2) covers 256
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
@@ -163,10 +203,11 @@ struct GemmParams {
 // once share weight tiles in L2); stream-K phase (sk = 1): the remaining tiles'
 // k-iterations split evenly, CTA c owning [sk_dp*kb + c*sk_w, +sk_w).
 struct SegIter {
-  int cursor, hi, dp;
-  __device__ __forceinline__ void init(const GemmParams& p) {
+  int cursor, hi, dp, step;
+  __device__ __forceinline__ void init(const GemmParams& p, int cg = 1) {
     dp = 1;
-    cursor = blockIdx.x;
+    cursor = blockIdx.x / cg;  // CTA pairs share one tile when cg = 2
+    step = gridDim.x / cg;
     hi = p.sk ? p.sk_dp : p.m_tiles * p.n_tiles;
   }
   __device__ __forceinline__ bool next(const GemmParams& p, int& tile, int& k0, int& k1) {
@@ -175,7 +216,7 @@ struct SegIter {
         tile = cursor;
         k0 = 0;
         k1 = p.num_kb;
-        cursor += gridDim.x;
+        cursor += step;
         return true;
       }
       if (!p.sk) return false;
@@ -205,10 +246,12 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int BN, int EPI, bool BF16, int XR>
+template <int BN, int EPI, bool BF16, int XR, int CG>
 __global__ void __launch_bounds__(192, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, CG>;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // CTA within the pair
+  const bool leader = rank == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -228,19 +271,27 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 4);
+      mbar_init(tempty0 + 8 * a, 4 * CG);  // every epilogue warp of the pair arrives at the leader
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "n"(C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int num_tiles = p.m_tiles * p.n_tiles;
@@ -250,16 +301,23 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       SegIter si;
-      si.init(p);
+      si.init(p, CG);
       int t, k0, k1;
       while (si.next(p, t, k0, k1)) {
-        const int m0 = (t % p.m_tiles) * C::BM, n0 = (t / p.m_tiles) * BN;
+        const int m0 = (t % p.m_tiles) * (C::BM * CG) + (int)rank * C::BM;
+        const int n0 = (t / p.m_tiles) * BN + (int)rank * (BN / CG);
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
-          mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
-          tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * C::BK, m0);
-          tma_load_2d(smem_u32(sB + stage * C::B_BYTES), &tmB, fb, kb * C::BK, n0);
+          if constexpr (CG == 2) {
+            if (leader) mbar_arrive_expect_tx(fb, 2 * C::STAGE_BYTES);
+            tma_load_2d_cg2(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * C::BK, m0);
+            tma_load_2d_cg2(smem_u32(sB + stage * C::B_BYTES), &tmB, fb, kb * C::BK, n0);
+          } else {
+            mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+            tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * C::BK, m0);
+            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), &tmB, fb, kb * C::BK, n0);
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -268,14 +326,14 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       constexpr uint32_t idesc = (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) |
-                                 ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(C::BM >> 4) << 24);
+                                 ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((C::BM * CG) >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       SegIter si;
-      si.init(p);
+      si.init(p, CG);
       int t, k0, k1;
       for (; si.next(p, t, k0, k1); ++it) {
         const int acc = it & 1;
@@ -289,15 +347,25 @@ __global__ void __launch_bounds__(192, 1)
           const uint64_t ad = sw128_desc(smem_u32(sA + stage * C::A_BYTES));
           const uint64_t bd = sw128_desc(smem_u32(sB + stage * C::B_BYTES));
           const int ks = (kb == p.num_kb - 1) ? p.last_ksteps : 4;
-          for (int k = 0; k < ks; ++k)
-            tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb > k0 || k > 0) ? 1u : 0u);
-          tc_commit(empty0 + 8 * stage);
+          for (int k = 0; k < ks; ++k) {
+            if constexpr (CG == 2)
+              tc_mma_cg2(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb > k0 || k > 0) ? 1u : 0u);
+            else
+              tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb > k0 || k > 0) ? 1u : 0u);
+          }
+          if constexpr (CG == 2)
+            tc_commit_cg2(empty0 + 8 * stage);
+          else
+            tc_commit(empty0 + 8 * stage);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(tfull0 + 8 * acc);
+        if constexpr (CG == 2)
+          tc_commit_cg2(tfull0 + 8 * acc);
+        else
+          tc_commit(tfull0 + 8 * acc);
       }
     }
   } else {
@@ -305,12 +373,12 @@ __global__ void __launch_bounds__(192, 1)
     const int erow = q * 32 + lane;  // row within the 128-row tile
     int it = 0;
     SegIter si;
-    si.init(p);
+    si.init(p, CG);
     int t, k0, k1;
     for (; si.next(p, t, k0, k1); ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (t % p.m_tiles) * C::BM, n0 = (t / p.m_tiles) * BN;
+      const int m0 = (t % p.m_tiles) * (C::BM * CG) + (int)rank * C::BM, n0 = (t / p.m_tiles) * BN;
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       const int row = m0 + erow;
@@ -487,14 +555,24 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_remote(tempty0 + 8 * acc, 0);
+        else
+          mbar_arrive(tempty0 + 8 * acc);
+      }
     }
   }
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/epilogues are done before TMEM is freed
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
-                 : "memory");
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(C::TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -551,20 +629,28 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
   else if (N <= 128 || (int64_t)m_tiles * ((N + 255) / 256) < num_sms / 2)
     bn = (N <= 64) ? 64 : 128;
   g.bn = bn;
-  const int tiles = m_tiles * ((N + bn - 1) / bn);
-  g.grid = tiles < num_sms ? tiles : num_sms;
+  // CTA pairs (M = 256 per tile) halve the per-CTA B traffic and double the stages
+  static const bool cg2_on = [] {
+    const char* e = std::getenv("ZO_CG2");
+    return !e || std::atoi(e) != 0;
+  }();
+  g.cg = (cg2_on && bn >= 128 && M >= 512) ? 2 : 1;
+  const int mt = (M + 128 * g.cg - 1) / (128 * g.cg);
+  const int tiles = mt * ((N + bn - 1) / bn);
+  const int slots = num_sms / g.cg;
+  g.grid = (tiles < slots ? tiles : slots) * g.cg;
   const int mrows = ((M + 127) / 128) * 128;
   make_tmap_2d(&g.tmA, A, (uint64_t)mrows, (uint64_t)lda, (uint64_t)lda, 128, bf16);
-  make_tmap_2d(&g.tmB, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)bn, bf16);
+  make_tmap_2d(&g.tmB, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg), bf16);
 }
 
-template <int BN, int EPI, bool BF16, int XR>
+template <int BN, int EPI, bool BF16, int XR, int CG>
 static void launch_t(const GemmDesc& g, cudaStream_t st) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    ZO_CUDA_TRY(
-        cudaFuncSetAttribute(k_gemm<BN, EPI, BF16, XR>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    ZO_CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI, BF16, XR, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     C::SMEM));
     attr_set = true;
   }
   GemmParams p;
@@ -572,7 +658,7 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.N = g.N;
   p.num_kb = g.num_kb;
   p.last_ksteps = g.last_ksteps;
-  p.m_tiles = (g.M + 127) / 128;
+  p.m_tiles = (g.M + 128 * CG - 1) / (128 * CG);
   p.n_tiles = (g.N + BN - 1) / BN;
   p.ldo = g.ldo;
   p.out = g.out;
@@ -582,27 +668,43 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.xrps = g.xrps;
   p.tpart_ld = g.tpart_ld;
   p.tpart = g.tpart;
-  p.sk = g.sk;
+  p.sk = CG == 1 ? g.sk : 0;
   p.sk_w = g.sk_w;
   p.sk_dp = g.sk_dp;
   p.sk_ws = g.sk_ws;
   p.sk_flags = g.sk_flags;
-  k_gemm<BN, EPI, BF16, XR><<<g.grid, 192, C::SMEM, st>>>(g.tmA, g.tmB, p);
+  if constexpr (CG == 1) {
+    k_gemm<BN, EPI, BF16, XR, 1><<<g.grid, 192, C::SMEM, st>>>(g.tmA, g.tmB, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g.grid);
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ZO_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm<BN, EPI, BF16, XR, 2>, g.tmA, g.tmB, p));
+  }
 }
 
-template <int BN, bool BF16>
+template <int BN, bool BF16, int CG>
 static void launch_e(const GemmDesc& g, cudaStream_t st) {
   switch (g.epi) {
-    case EPI_STORE16: launch_t<BN, EPI_STORE16, BF16, 0>(g, st); break;
-    case EPI_GELU16: launch_t<BN, EPI_GELU16, BF16, 0>(g, st); break;
+    case EPI_STORE16: launch_t<BN, EPI_STORE16, BF16, 0, CG>(g, st); break;
+    case EPI_GELU16: launch_t<BN, EPI_GELU16, BF16, 0, CG>(g, st); break;
     case EPI_GELU16_EXT:
-      if (g.xr == 1) launch_t<BN, EPI_GELU16_EXT, BF16, 1>(g, st);
-      else if (g.xr == 2) launch_t<BN, EPI_GELU16_EXT, BF16, 2>(g, st);
-      else if (g.xr == 4) launch_t<BN, EPI_GELU16_EXT, BF16, 4>(g, st);
-      else launch_t<BN, EPI_GELU16_EXT, BF16, 8>(g, st);
+      if (g.xr == 1) launch_t<BN, EPI_GELU16_EXT, BF16, 1, CG>(g, st);
+      else if (g.xr == 2) launch_t<BN, EPI_GELU16_EXT, BF16, 2, CG>(g, st);
+      else if (g.xr == 4) launch_t<BN, EPI_GELU16_EXT, BF16, 4, CG>(g, st);
+      else launch_t<BN, EPI_GELU16_EXT, BF16, 8, CG>(g, st);
       break;
-    case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16, 0>(g, st); break;
-    default: launch_t<BN, EPI_STORE32, BF16, 0>(g, st); break;
+    case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16, 0, CG>(g, st); break;
+    default: launch_t<BN, EPI_STORE32, BF16, 0, CG>(g, st); break;
   }
 }
 
@@ -611,7 +713,7 @@ void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
   const int tiles = m_tiles * n_tiles;
   // worth it when the last wave is ragged; keep >= one full wave in the stream-K phase so
   // every CTA owns >= one tile of k-iterations (<= 2 segments per split tile)
-  if (tiles <= num_sms || tiles % num_sms == 0 || !ws || !flags) return;
+  if (g.cg != 1 || tiles <= num_sms || tiles % num_sms == 0 || !ws || !flags) return;
   const int dp_waves = tiles / num_sms - 1;
   const int sk_tiles = tiles - dp_waves * num_sms;
   const long sk_iters = (long)sk_tiles * g.num_kb;
@@ -626,14 +728,24 @@ void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
 }
 
 void gemm_launch(const GemmDesc& g, cudaStream_t st) {
+  if (g.cg == 2) {
+    if (g.bf16) {
+      if (g.bn == 256) launch_e<256, true, 2>(g, st);
+      else launch_e<128, true, 2>(g, st);
+    } else {
+      if (g.bn == 256) launch_e<256, false, 2>(g, st);
+      else launch_e<128, false, 2>(g, st);
+    }
+    return;
+  }
   if (g.bf16) {
-    if (g.bn == 256) launch_e<256, true>(g, st);
-    else if (g.bn == 128) launch_e<128, true>(g, st);
-    else launch_e<64, true>(g, st);
+    if (g.bn == 256) launch_e<256, true, 1>(g, st);
+    else if (g.bn == 128) launch_e<128, true, 1>(g, st);
+    else launch_e<64, true, 1>(g, st);
   } else {
-    if (g.bn == 256) launch_e<256, false>(g, st);
-    else if (g.bn == 128) launch_e<128, false>(g, st);
-    else launch_e<64, false>(g, st);
+    if (g.bn == 256) launch_e<256, false, 1>(g, st);
+    else if (g.bn == 128) launch_e<128, false, 1>(g, st);
+    else launch_e<64, false, 1>(g, st);
   }
 }
 

@@ -23,6 +23,7 @@ struct GemmDesc {
   int num_kb = 0;       // 64-wide K blocks
   int last_ksteps = 4;  // 16-wide UMMA steps issued in the last K block (trims the LoRA extension)
   int bn = 256;         // tile N (64/128/256)
+  int cg = 1;           // 2: CTA-pair tiles (tcgen05 cta_group::2, M = 256, B split across the pair)
   int epi = EPI_STORE16;
   int bf16 = 0;         // operand type: 0 fp16, 1 bf16
   void* out = nullptr;
