@@ -74,8 +74,13 @@ __global__ void __launch_bounds__(TP * 2)
   uint16_t* sq = sm;
   uint16_t* sk = sq + TP * LD;
   uint16_t* sv = sk + TP * LD;
+  float* sP = reinterpret_cast<float*>(sv + TP * LD);  // this head's P rows [DH][r] (one sign per sequence)
   const int seq = blockIdx.x, h = blockIdx.y;
   const int d = H * DH;
+  if (x.tpart) {
+    const float* Pg = ((seq * T) < x.rps ? x.Pp : x.Pm) + (size_t)h * DH * x.r;
+    for (int i = threadIdx.x; i < DH * x.r; i += blockDim.x) sP[i] = Pg[i];
+  }
   // stage Q, K, V (16-byte vectors; rows >= T zero)
   constexpr int VPR = DH / 8;
   for (int idx = threadIdx.x; idx < TP * VPR; idx += blockDim.x) {
@@ -179,11 +184,12 @@ __global__ void __launch_bounds__(TP * 2)
   float t0[8], t1[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) t0[k] = t1[k] = 0.f;
-  const float* P0 = x.tpart ? ((m0 < x.rps) ? x.Pp : x.Pm) : nullptr;
-  const float* P1 = x.tpart ? ((m1 < x.rps) ? x.Pp : x.Pm) : nullptr;
+  const float* P0 = sP;  // a sequence never straddles the two probe halves
+  const float* P1 = sP;
 #pragma unroll
   for (int n = 0; n < DT; ++n) {
     const int col = h * DH + n * 8 + 2 * tq;
+    const int lc = n * 8 + 2 * tq;  // column within the head (index into sP)
     const uint32_t w0 = pack_f2<BF16>(o[n][0] * inv0, o[n][1] * inv0);
     const uint32_t w1 = pack_f2<BF16>(o[n][2] * inv1, o[n][3] * inv1);
     if (row0 < T) *reinterpret_cast<uint32_t*>(ctx + (size_t)m0 * ldc + col) = w0;
@@ -195,8 +201,8 @@ __global__ void __launch_bounds__(TP * 2)
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         if (k < x.r) {
-          t0[k] += a00 * P0[(size_t)col * x.r + k] + a01 * P0[(size_t)(col + 1) * x.r + k];
-          t1[k] += a10 * P1[(size_t)col * x.r + k] + a11 * P1[(size_t)(col + 1) * x.r + k];
+          t0[k] += a00 * P0[lc * x.r + k] + a01 * P0[(lc + 1) * x.r + k];
+          t1[k] += a10 * P1[lc * x.r + k] + a11 * P1[(lc + 1) * x.r + k];
         }
       }
     }
@@ -221,7 +227,7 @@ __global__ void __launch_bounds__(TP * 2)
 template <int DH, int TP, bool BF16>
 static void launch_t(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int T, int H, const AttnExt& x,
                      cudaStream_t st) {
-  const size_t smem = (size_t)3 * TP * (DH + 8) * 2;
+  const size_t smem = (size_t)3 * TP * (DH + 8) * 2 + (size_t)DH * 8 * sizeof(float);
   static bool set = false;
   if (!set) {
     ZO_CUDA_TRY(cudaFuncSetAttribute(k_attn_mma<DH, TP, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,

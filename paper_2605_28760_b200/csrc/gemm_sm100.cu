@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -635,6 +636,7 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
     return !e || std::atoi(e) != 0;
   }();
   g.cg = (cg2_on && bn >= 128 && M >= 512) ? 2 : 1;
+  if (g.cg == 2) g.bn = bn = 256;  // N=128 pair tiles measured 1.4-1.5x slower (A re-reads, fixed costs)
   const int mt = (M + 128 * g.cg - 1) / (128 * g.cg);
   const int tiles = mt * ((N + bn - 1) / bn);
   const int slots = num_sms / g.cg;

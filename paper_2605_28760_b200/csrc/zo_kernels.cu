@@ -31,6 +31,12 @@ __device__ __forceinline__ void st16(void* p, size_t i, float v, bool bf16) {
   reinterpret_cast<uint16_t*>(p)[i] = to16(v, bf16);
 }
 
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int N>
 __device__ __forceinline__ void block_sum(float (&v)[N], float* red /* >= 32*N */) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -81,19 +87,24 @@ __device__ __forceinline__ void write_ext(void* out, size_t base, int k, float t
 }
 
 // ------------------------------------------------------------------ fused-extension finalize
-__global__ void k_ext_finalize(const float* __restrict__ tpart, int ntiles, int ld, int M, int r, void* __restrict__ a,
-                               int lda, int K, int ext_terms, bool bf16) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+// one warp per (row, k): lanes stride over the tiles, then a fixed xor-shuffle tree
+// (deterministic; independent of scheduling)
+__global__ void __launch_bounds__(256) k_ext_finalize(const float* __restrict__ tpart, int ntiles, int ld, int M,
+                                                      int r, void* __restrict__ a, int lda, int K, int ext_terms,
+                                                      bool bf16) {
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (i >= M * r) return;
   const int row = i / r, k = i % r;
   float t = 0.f;
-  for (int j = 0; j < ntiles; ++j) t += tpart[((size_t)j * ld + row) * r + k];
-  write_ext(a, (size_t)row * lda + K, k, t, ext_terms, bf16);
+  for (int j = lane; j < ntiles; j += 32) t += tpart[((size_t)j * ld + row) * r + k];
+  t = warp_sum(t);
+  if (lane == 0) write_ext(a, (size_t)row * lda + K, k, t, ext_terms, bf16);
 }
 
 void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
                          int ext_terms, bool bf16, cudaStream_t st) {
-  k_ext_finalize<<<(M * r + 255) / 256, 256, 0, st>>>(tpart, ntiles, ld, M, r, a, lda, K, ext_terms, bf16);
+  k_ext_finalize<<<(M * r + 7) / 8, 256, 0, st>>>(tpart, ntiles, ld, M, r, a, lda, K, ext_terms, bf16);
 }
 
 // ------------------------------------------------------------------ embed
@@ -121,11 +132,6 @@ void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const 
 }
 
 // ------------------------------------------------------------------ LN (+ extension), warp per row
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
 
 __device__ __forceinline__ void store4_16(void* out, size_t i, float a, float b, float c, float d, bool bf16) {
   uint2 w;
@@ -239,6 +245,95 @@ __global__ void __launch_bounds__(256) k_ln_ext_reg(const float* __restrict__ x3
     for (int k = 0; k < XR; ++k) write_ext(out, (size_t)row * ldo + d, k, t[k], ext_terms, bf16);
 }
 
+// CTA per row, 256 threads, NPT float4 per thread in registers: high occupancy,
+// one HBM read of x, block reductions through shared memory.
+template <int NPT, int XR>
+__global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, const float* __restrict__ g,
+                                                const float* __restrict__ bta, int d, void* __restrict__ out, int ldo,
+                                                bool bf16, const float* __restrict__ Pp, const float* __restrict__ Pm,
+                                                int rows_per_sign, int ext_terms) {
+  __shared__ float red[8 * (XR + 1)];
+  const int row = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const float4* x = reinterpret_cast<const float4*>(x32 + (size_t)row * d);
+  float4 v[NPT];
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) v[j] = x[tid + j * blockDim.x];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+  s = warp_sum(s);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < nw; ++w) tot += red[w];
+  const float mu = tot / (float)d;
+  s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const float a = v[j].x - mu, b = v[j].y - mu, c = v[j].z - mu, e = v[j].w - mu;
+    s += (a * a + b * b) + (c * c + e * e);
+  }
+  s = warp_sum(s);
+  __syncthreads();
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  tot = 0.f;
+  for (int w = 0; w < nw; ++w) tot += red[w];
+  const float rsd = 1.0f / sqrtf(tot / (float)d + 1e-5f);
+  const float* P = (row < rows_per_sign) ? Pp : Pm;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(bta);
+  float t[XR];
+#pragma unroll
+  for (int k = 0; k < XR; ++k) t[k] = 0.f;
+#pragma unroll
+  for (int j = 0; j < NPT; ++j) {
+    const int i = tid + j * blockDim.x;
+    const float4 gg = g4[i], bb = b4[i];
+    const float h[4] = {(v[j].x - mu) * rsd * gg.x + bb.x, (v[j].y - mu) * rsd * gg.y + bb.y,
+                        (v[j].z - mu) * rsd * gg.z + bb.z, (v[j].w - mu) * rsd * gg.w + bb.w};
+    store4_16(out, (size_t)row * ldo + 4 * i, h[0], h[1], h[2], h[3], bf16);
+    const float4* pr = reinterpret_cast<const float4*>(P + (size_t)(4 * i) * XR);
+    if constexpr (XR == 2) {
+      const float4 p01 = pr[0], p23 = pr[1];  // P[4i..4i+3][0..1]
+      t[0] += h[0] * p01.x + h[1] * p01.z + h[2] * p23.x + h[3] * p23.z;
+      t[1] += h[0] * p01.y + h[1] * p01.w + h[2] * p23.y + h[3] * p23.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int k = 0; k < XR; ++k) t[k] += h[e] * P[(size_t)(4 * i + e) * XR + k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < XR; ++k) t[k] = warp_sum(t[k]);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < XR; ++k) red[8 + warp * XR + k] = t[k];
+  __syncthreads();
+  if (tid < XR) {
+    float a = 0.f;
+    for (int w = 0; w < nw; ++w) a += red[8 + w * XR + tid];
+    write_ext(out, (size_t)row * ldo + d, tid, a, ext_terms, bf16);
+  }
+}
+
+template <int NPT>
+static bool ln_row_dispatch(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
+                            bool bf16, const float* Pp, const float* Pm, int r, int rps, int ext_terms,
+                            cudaStream_t st) {
+  const int threads = d / (4 * NPT);
+  if (threads * 4 * NPT != d || threads % 32 || threads > 256) return false;
+  switch (r) {
+    case 1: k_ln_row<NPT, 1><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
+    case 2: k_ln_row<NPT, 2><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
+    case 4: k_ln_row<NPT, 4><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
+    default: return false;
+  }
+}
+
 template <int NV>
 static bool ln_reg_dispatch(const float* x32, const float* gamma, const float* beta, int M, void* out, int ldo,
                             bool bf16, const float* Pp, const float* Pm, int r, int rps, int ext_terms,
@@ -257,7 +352,20 @@ void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int 
                    cudaStream_t st) {
   if (d % 4 || ldo % 4) throw Error(ZO_ERR_DIMENSION, "LN rows must be multiples of 4");
   bool done = false;
-  switch (d) {
+  // CTA-per-row kernel first (d multiple of 128 and <= 8192)
+  if (d % 1024 == 0) {
+    switch (d / 1024) {
+      case 1: done = ln_row_dispatch<1>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+      case 2: done = ln_row_dispatch<2>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+      case 4: done = ln_row_dispatch<4>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+      case 5: done = ln_row_dispatch<5>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+      case 8: done = ln_row_dispatch<8>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+      default: break;
+    }
+  } else if (d % 128 == 0 && d <= 1024) {
+    done = ln_row_dispatch<1>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st);
+  }
+  if (!done) switch (d) {
     case 768: done = ln_reg_dispatch<6>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
     case 1024: done = ln_reg_dispatch<8>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
     case 2048: done = ln_reg_dispatch<16>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
