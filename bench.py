@@ -186,6 +186,7 @@ def main():
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu/gemm microbench")
     args = ap.parse_args()
@@ -243,7 +244,10 @@ def main():
     def one_step(t):
         tp, gp = d_tok[t].data_ptr(), d_gold[t].data_ptr()
         if world == 1:
-            eng.step_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, Bl)
+            if args.graph:
+                eng.step_graph(zcfg.seed, t, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, Bl)
+            else:
+                eng.step_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, Bl)
         else:
             import torch.distributed as dist
             eng.step_score_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, tp, gp, Bl)

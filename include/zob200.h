@@ -126,6 +126,11 @@ int zo_step(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilo
 int zo_step_async(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon, double lr,
                   int32_t divide_by_r, const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B);
 int zo_fold_async(zo_ctx* ctx);
+/* zo_step_async with the step body (U sampling, probes, scoring, coefficient,
+ * update) replayed as one CUDA graph; captured on first use per
+ * (seed, B, epsilon, lr, divide_by_r). */
+int zo_step_graph(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon, double lr,
+                  int32_t divide_by_r, const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B);
 /* the two halves of zo_step_async; multi-GPU exact mode all-gathers the
  * per-example NLLs (zo_nll_io) between them, B_total = global batch */
 int zo_step_score_async(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon,

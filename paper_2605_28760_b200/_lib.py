@@ -65,6 +65,8 @@ SIGNATURES = [
     ("zo_step_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double,
                                  _c.c_int32, _P, _P, _c.c_int32]),
     ("zo_fold_async", _c.c_int, [_P]),
+    ("zo_step_graph", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double,
+                                 _c.c_int32, _P, _P, _c.c_int32]),
     ("zo_step_score_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _P, _P,
                                        _c.c_int32]),
     ("zo_step_apply_async", _c.c_int, [_P, _c.c_double, _c.c_double, _c.c_int32, _c.c_int32]),

@@ -127,7 +127,22 @@ struct zo_ctx {
   int64_t v_window = -1;  // window start whose V is loaded (-1: none)
   bool a_dirty = false;   // window A carries unfolded mass
 
+  // captured step graph (zo_step_graph)
+  cudaStream_t cap_st = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  struct GKey {
+    uint64_t seed;
+    int B, dbr;
+    double eps, lr;
+    bool operator==(const GKey& o) const {
+      return seed == o.seed && B == o.B && dbr == o.dbr && eps == o.eps && lr == o.lr;
+    }
+  } gkey{};
+  bool gkey_valid = false;
+
   ~zo_ctx() {
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (cap_st) cudaStreamDestroy(cap_st);
     if (h_tok) cudaFreeHost(h_tok);
     if (h_gold) cudaFreeHost(h_gold);
     if (h_out4) cudaFreeHost(h_out4);
@@ -931,6 +946,76 @@ extern "C" int zo_step_async(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu
   int rc = zo_step_score_async(c, seed, step, nu, eps, tokens_dev, gold_dev, B);
   if (rc) return rc;
   return zo_step_apply_async(c, eps, lr, divide_by_r, B);
+}
+
+// Directions (U), probes, paired scoring, coefficient and update for the step in
+// d_step: the part of a step that is identical every step (graph body).
+static void step_body(zo_ctx* c, uint64_t seed, double eps, double lr, int32_t divide_by_r, int32_t B) {
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  const double scale = lozo ? 1.0 : 1.0 / std::sqrt((double)c->r);
+  launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, eps, scale, c->Pp, c->Pm, c->st);
+  do_score(c, B, 2);
+  launch_coefficient(c->nll, B, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
+  if (lozo)
+    launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
+  else
+    launch_dense_update_dev(c, lr);
+}
+
+// zo_step_async as one CUDA-graph launch: the ~370 kernels of the step body are
+// captured once per (seed, B, eps, lr, divide_by_r) and replayed; the step index,
+// token staging and window work (V resampling / fold) stay eager in front of it.
+extern "C" int zo_step_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr,
+                             int32_t divide_by_r, const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
+  ZO_API_BEGIN
+  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  k_set_u64<<<1, 1, 0, c->st>>>(c->d_step, step);
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->tok, tokens_dev, (size_t)B * c->T * 4, cudaMemcpyDeviceToDevice, c->st));
+  const size_t ng = (size_t)B * c->d.opt_len * 4;
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->gold, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
+  ZO_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->gold) + ng, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
+  const int64_t wstart = lozo ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
+  if (!lozo || wstart != c->v_window) {
+    if (lozo && c->a_dirty) fold_all(c);
+    sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
+    write_vext_all(c);
+    c->v_window = wstart;
+  }
+  const zo_ctx::GKey key{seed, B, divide_by_r, eps, lr};
+  if (!c->gkey_valid || !(key == c->gkey)) {
+    // first use of this key: run eagerly (also warms attributes/plans), then capture
+    step_body(c, seed, eps, lr, divide_by_r, B);
+    if (!c->cap_st) ZO_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+    ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+    if (c->gexec) {
+      ZO_CUDA_TRY(cudaGraphExecDestroy(c->gexec));
+      c->gexec = nullptr;
+    }
+    cudaStream_t user = c->st;
+    c->st = c->cap_st;
+    cudaGraph_t graph = nullptr;
+    try {
+      ZO_CUDA_TRY(cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal));
+      step_body(c, seed, eps, lr, divide_by_r, B);
+      ZO_CUDA_TRY(cudaStreamEndCapture(c->cap_st, &graph));
+    } catch (...) {
+      c->st = user;
+      throw;
+    }
+    c->st = user;
+    ZO_CUDA_TRY(cudaGraphInstantiate(&c->gexec, graph, 0));
+    ZO_CUDA_TRY(cudaGraphDestroy(graph));
+    c->gkey = key;
+    c->gkey_valid = true;
+  } else {
+    ZO_CUDA_TRY(cudaGraphLaunch(c->gexec, c->st));
+  }
+  if (lozo) c->a_dirty = true;
+  return ZO_OK;
+  ZO_API_END
 }
 
 extern "C" int zo_fold_async(zo_ctx* c) {

@@ -208,6 +208,11 @@ class ZoEngine:
         check(lib().zo_step_async(self._h, seed, step, nu, float(epsilon), float(lr), int(divide_by_r),
                                   ctypes.c_void_p(tokens_dev), ctypes.c_void_p(gold_dev), B))
 
+    def step_graph(self, seed: int, step: int, nu: int, epsilon: float, lr: float, divide_by_r: bool,
+                   tokens_dev: int, gold_dev: int, B: int) -> None:
+        check(lib().zo_step_graph(self._h, seed, step, nu, float(epsilon), float(lr), int(divide_by_r),
+                                  ctypes.c_void_p(tokens_dev), ctypes.c_void_p(gold_dev), B))
+
     def step_score_async(self, seed: int, step: int, nu: int, epsilon: float, tokens_dev: int, gold_dev: int,
                          B: int) -> None:
         check(lib().zo_step_score_async(self._h, seed, step, nu, float(epsilon), ctypes.c_void_p(tokens_dev),

@@ -172,3 +172,37 @@ def test_forward_vs_oracle_streamk_shapes(precision):
     np.testing.assert_allclose(nll[0], ref[1], atol=NLL_TOL[precision], rtol=0)
     np.testing.assert_allclose(nll[1], ref[-1], atol=NLL_TOL[precision], rtol=0)
     assert abs(d_got - d_ref) <= max(DL_REL[precision] * abs(d_ref), 2e-4), (d_got, d_ref)
+
+
+def test_graph_step_bitwise_equals_eager():
+    """The CUDA-graph replay of the step body is bit-identical to eager launches
+    (losses, coefficient and the window A arena), across a window boundary."""
+    import torch
+    from paper_2605_28760_b200.engine import ZoEngine
+    cfg = R.ModelCfg(vocab=512, dim=128, n_layers=2, n_heads=2, prompt_len=63, init_seed=7, init_scale=0.02)
+    splits = R.generate_task(R.TaskCfg(seed=11, vocab=512, prompt_len=63, train_size=64, dev_size=4, val_size=4))
+    toks, golds = [], []
+    for t in range(7):
+        p, gl, _ = R.sample_minibatch(splits, "train", 42, t, 16)
+        g = np.array([[510], [511]])[gl]
+        toks.append(np.concatenate([p, g], axis=1))
+        golds.append(g)
+    d_tok = torch.from_numpy(np.stack(toks).astype(np.int32)).cuda()
+    d_gold = torch.from_numpy(np.stack(golds).astype(np.int32)).cuda()
+    outs = []
+    for graph in (False, True):
+        eng = ZoEngine(cfg.vocab, cfg.dim, cfg.n_layers, cfg.n_heads, cfg.prompt_len, max_batch=16, rank=2)
+        eng.init_params(cfg.init_seed, cfg.init_scale)
+        res = []
+        for t in range(7):
+            fn = eng.step_graph if graph else eng.step_async
+            fn(42, t, 3, 1e-3, 1e-3, False, d_tok[t].data_ptr(), d_gold[t].data_ptr(), 16)
+            res.append(eng.read_out4())
+            if (t + 1) % 3 == 0:
+                eng.fold_async()
+        res.append(eng.get_slot(2))
+        res.append(eng.download("blk0.qkv"))
+        outs.append(res)
+        eng.close()
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
