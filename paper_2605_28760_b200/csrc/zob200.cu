@@ -657,6 +657,8 @@ int zo_sample_u(zo_ctx* c, uint64_t seed, uint64_t step) {
 int zo_sample_v(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu) {
   ZO_API_BEGIN
   check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  // unfolded window mass must be folded before V changes (zo_engine.py:395-398)
+  if (c->d.estimator == ZO_EST_LOZO && c->a_dirty) fold_all(c);
   set_step(c, step);
   sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
   write_vext_all(c);

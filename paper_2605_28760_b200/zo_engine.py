@@ -266,10 +266,8 @@ def lozo_step(params, mcfg: ModelConfig, state: AdapterState, zcfg: ZoConfig, st
     else:
         window = (step // zcfg.nu) * zcfg.nu
         if getattr(state, "_window", None) != window:
-            if getattr(state, "_a_dirty", False):
-                eng.fold()
-                dp.invalidate()
-            eng.sample_v(zcfg.seed, step, zcfg.nu)
+            eng.sample_v(zcfg.seed, step, zcfg.nu)  # folds unfolded window mass first
+            dp.invalidate()
             state._window = window
         eng.sample_u(zcfg.seed, step)
         state._probe_on = True
@@ -281,7 +279,6 @@ def lozo_step(params, mcfg: ModelConfig, state: AdapterState, zcfg: ZoConfig, st
         beta = -(zcfg.learning_rate * c_used)
         eng.set_coefficient(np.array([lp, lm, c, beta]))
         eng.update_u()
-        state._a_dirty = True
     ud, vd = _digests(state, eng, zcfg, step, digests)
     return make_step_record(zcfg, step, lp, lm, beta, ud, vd, batch)
 

@@ -1,0 +1,145 @@
+"""The reference-shaped public API on the GPU, against the reference's golden
+trajectories (tests/golden/traj_*.jsonl).
+
+* With the reference's own coefficients injected through the `scorer=` seam,
+  the device update (K8) and folds (K9) must reproduce the reference's float64
+  parameters BIT-EXACTLY (final params_digest equal), and every step's U/V
+  digests must match.
+* run_serving_path end to end: digests exact, losses within the fp16 tolerance.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _traj(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        lines = [json.loads(l) for l in f if l.strip()]
+    return lines[0], [l for l in lines if l["record"] == "step"], lines[-1]
+
+
+def _setup(h):
+    from paper_2605_28760_b200 import model as M
+    from paper_2605_28760_b200.zo_engine import ZoConfig
+    mcfg = M.ModelConfig(**h["model"])
+    task = M.generate_task(M.TaskConfig(**h["task"]))
+    zcfg = ZoConfig(**h["zo"])
+    return M, mcfg, task, zcfg
+
+
+class _ReplayScorer:
+    """scorer(batch) returning the reference's recorded L+ then L- (zo_engine.py:318-326)."""
+
+    def __init__(self, recs):
+        self.recs, self.i, self.calls = recs, 0, 0
+
+    def __call__(self, batch):
+        r = self.recs[self.i]
+        v = r["loss_plus"] if self.calls % 2 == 0 else r["loss_minus"]
+        self.calls += 1
+        if self.calls % 2 == 0:
+            self.i += 1
+        return v
+
+
+@pytest.mark.parametrize("name", ["micro_lozo", "small_lozo"])
+def test_update_and_fold_bit_exact_with_reference_coefficients(golden_dir, name):
+    from paper_2605_28760_b200.adapter import AdapterState
+    from paper_2605_28760_b200.zo_engine import lozo_step
+    h, recs, fin = _traj(golden_dir, f"traj_{name}.jsonl")
+    M, mcfg, task, zcfg = _setup(h)
+    params = M.init_params(mcfg, max_batch=zcfg.batch_size)
+    assert M.params_digest(params) == h["model_digest"]
+    state = AdapterState(epsilon=zcfg.epsilon)
+    scorer = _ReplayScorer(recs)
+    for t, rec in enumerate(recs):
+        batch = M.sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
+        out = lozo_step(params, mcfg, state, zcfg, t, batch, scorer=scorer)
+        assert (out.u_digest, out.v_digest, out.minibatch_id) == (rec["u_digest"], rec["v_digest"],
+                                                                   rec["minibatch_id"])
+        assert out.beta == rec["beta"] and out.coefficient == rec["coefficient"]
+        if (t + 1) % zcfg.nu == 0:
+            params.engine.fold()
+            params.invalidate()
+    assert M.params_digest(params) == fin["pre_fold_params_digest"]
+    params.engine.fold()
+    params.invalidate()
+    assert M.params_digest(params) == fin["final_params_digest"]
+
+
+def test_factorized_dense_update_bit_exact(golden_dir):
+    from paper_2605_28760_b200.engine import U, V, ZoEngine
+    from paper_2605_28760_b200.numerics import canonical_mean, digest_hex
+    h, recs, fin = _traj(golden_dir, "traj_micro_fact.jsonl")
+    M, mcfg, task, zcfg = _setup(h)
+    eng = ZoEngine(mcfg.vocab, mcfg.dim, mcfg.n_layers, mcfg.n_heads, mcfg.prompt_len, max_batch=zcfg.batch_size,
+                   rank=zcfg.rank, estimator="factorized_sqrt_r")
+    eng.init_params(mcfg.init_seed, mcfg.init_scale)
+    dl = []
+    for t, rec in enumerate(recs):
+        batch = M.sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
+        eng.sample_v(zcfg.seed, t, 1)
+        eng.sample_u(zcfg.seed, t)
+        assert digest_hex(eng.digest(U)) == rec["u_digest"]
+        assert digest_hex(eng.digest(V)) == rec["v_digest"]
+        tokens, gold = batch.sequences()
+        eng.prepare_probe(zcfg.epsilon, 0)
+        nll = eng.score(tokens, np.stack([gold, gold]), nsign=2)
+        dl.append(max(abs(canonical_mean(nll[0]) - rec["loss_plus"]), abs(canonical_mean(nll[1]) - rec["loss_minus"])))
+        eng.set_coefficient(np.array([rec["loss_plus"], rec["loss_minus"], rec["coefficient"], rec["beta"]]))
+        eng.update_dense(zcfg.learning_rate)
+    assert max(dl) < 1.5e-2, dl
+    params = {lid: eng.download(lid) for lid in eng.lids}
+    params.update({k: v for k, v in M._vector_defaults(mcfg).items()})
+    assert M.params_digest(params) == fin["final_params_digest"]
+
+
+def test_run_serving_path_public_api(golden_dir):
+    from paper_2605_28760_b200.runtime import run_serving_path
+    h, recs, fin = _traj(golden_dir, "traj_micro_lozo.jsonl")
+    M, mcfg, task, zcfg = _setup(h)
+    run = run_serving_path(mcfg, task, zcfg, h["steps"], eval_every=10 ** 9)
+    assert run.model_digest == h["model_digest"] and run.task_digest == h["task_digest"]
+    assert run.steps_completed == len(recs) and not run.aborted
+    for a, b in zip(recs, run.trajectory):
+        assert (a["u_digest"], a["v_digest"], a["minibatch_id"]) == (b.u_digest, b.v_digest, b.minibatch_id)
+        assert abs(a["loss_plus"] - b.loss_plus) < 1.5e-2 and abs(a["loss_minus"] - b.loss_minus) < 1.5e-2
+    assert abs(run.eval_curve[-1].loss - fin["eval_loss"]) < 2e-2
+    # the reference's wire format round-trips
+    from paper_2605_28760_b200.zo_engine import read_trajectory, write_trajectory
+    write_trajectory("gpurun_out/parity_traj_micro_lozo_b200.jsonl", {"model_digest": run.model_digest},
+                     run.trajectory, {"eval_loss": run.eval_curve[-1].loss})
+    _, back, _ = read_trajectory("gpurun_out/parity_traj_micro_lozo_b200.jsonl")
+    assert [r.to_dict() for r in back] == [r.to_dict() for r in run.trajectory]
+
+
+def test_run_serving_path_abort_is_transactional(golden_dir):
+    from paper_2605_28760_b200.runtime import run_serving_path
+    h, recs, fin = _traj(golden_dir, "traj_micro_lozo.jsonl")
+    M, mcfg, task, zcfg = _setup(h)
+    run = run_serving_path(mcfg, task, zcfg, 8, eval_every=10 ** 9, abort_at=3)
+    assert run.aborted and run.steps_completed == 3 and len(run.trajectory) == 3
+
+
+def test_evaluate_split_vs_oracle():
+    from oracle import reference as R
+    from paper_2605_28760_b200 import model as M
+    mcfg = M.ModelConfig(vocab=512, dim=128, n_layers=2, n_heads=2, prompt_len=63, init_seed=7, init_scale=0.02)
+    task = M.generate_task(M.TaskConfig(seed=11, vocab=512, prompt_len=63, train_size=16, dev_size=40, val_size=4))
+    params = M.init_params(mcfg, max_batch=16)
+    loss, acc = M.evaluate_split(params, mcfg, task, "dev")
+    # oracle: base weights, gold-option NLL over the dev split (model.py:444-460)
+    cfg = R.ModelCfg(**{k: getattr(mcfg, k) for k in R.ModelCfg.__dataclass_fields__})
+    p = R.init_params(cfg)
+    prompts, golds = task.splits["dev"]
+    opts = np.array([[510], [511]])
+    per = [R.forward_nll(p, cfg, np.concatenate([prompts, np.tile(o, (len(prompts), 1))], axis=1),
+                         np.tile(o, (len(prompts), 1))) for o in opts]
+    ref_loss = R.canonical_mean(np.choose(golds, per))
+    ref_acc = float(np.mean(np.argmax(-np.stack(per, axis=1), axis=1) == golds))
+    assert abs(loss - ref_loss) < 1e-2
+    assert abs(acc - ref_acc) <= 1.0 / len(golds) + 1e-12
