@@ -16,9 +16,16 @@ value : steps/s over K device-timed steps (CUDA events on the engine stream,
         inputs resident in HBM, weights 25.7 GB >> 126 MB L2 so no flush).
 e2e   : the same through the public API (sample_minibatch + lozo_step with
         host batches: H2D tokens from pinned staging, D2H of L+/L-/c) -- wall clock.
-N > 1 : exact-trajectory mode -- the 16 examples are split over ranks (both
-        signs on every rank), the per-example NLLs are all-gathered over NCCL
-        (256 B/step) and every rank applies the identical update; "strong".
+N > 1 : --mode qdir (default; BASELINE config 3 "query directions sharded") --
+        rank g scores the direction and minibatch of reference step t*N+g on a
+        full B=16 batch at the shared state of macro-step t; the [L+,L-,c,beta]
+        of every rank are all-gathered over NCCL (32 B/rank) and every rank
+        regenerates the N counter-keyed U's and applies the N updates in rank
+        order (identical replicas, no weight traffic); value = reference steps/s
+        of the whole job, "weak".  nu is rounded down to a multiple of N.
+        --mode exact -- the 16 examples are split over ranks (both signs on every
+        rank), the per-example NLLs are all-gathered (256 B/step) and every rank
+        applies the identical update: the reference trajectory itself; "strong".
 """
 from __future__ import annotations
 
@@ -189,6 +196,9 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu/gemm microbench")
+    ap.add_argument("--mode", default="qdir", choices=["qdir", "exact"],
+                    help="N>1: qdir = query directions sharded (rank g scores reference step t*N+g on a full "
+                         "batch, weak scaling); exact = the 16 examples split over ranks (strong scaling)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     mdl = MODELS[args.model]
@@ -208,9 +218,15 @@ def main():
     from paper_2605_28760_b200.zo_engine import ZoConfig, lozo_step
 
     B, T = args.batch, args.seq
-    if B % world:
+    qdir = world > 1 and args.mode == "qdir"
+    if qdir and args.nu % world:
+        # the G directions of a macro-step must share one window (G | nu): round nu down
+        # to a multiple of G (50 -> 48 at 4 and 8 GPUs; the fold is ~1% of a step)
+        args.nu = max(world, args.nu // world * world)
+    if not qdir and B % world:
         raise SystemExit("global batch must divide over ranks")
-    Bl = B // world
+    Bl = B if qdir else B // world
+    G = world if qdir else 1  # reference steps (directions) per timed step
     prompt_len = T - 1
     mcfg = M.ModelConfig(vocab=mdl["vocab"], dim=mdl["dim"], n_layers=mdl["n_layers"], n_heads=mdl["n_heads"],
                          prompt_len=prompt_len, init_seed=7, init_scale=0.02)
@@ -232,6 +248,10 @@ def main():
     toks = np.zeros((nsteps, Bl, T), dtype=np.int32)
     golds = np.zeros((nsteps, Bl, 1), dtype=np.int32)
     for t in range(nsteps):
+        if qdir:  # this rank's direction: reference step t*G + rank, full batch
+            seq, gold = M.sample_minibatch(task, "train", zcfg.seed, t * G + rank, B).sequences()
+            toks[t], golds[t] = seq, gold
+            continue
         mb = M.sample_minibatch(task, "train", zcfg.seed, t, B)
         seq, gold = mb.sequences()
         toks[t] = seq[rank * Bl:(rank + 1) * Bl]
@@ -240,9 +260,20 @@ def main():
     d_gold = torch.from_numpy(golds).cuda()
     nll_local = torch.zeros(2 * Bl, dtype=torch.float64, device="cuda")
     nll_all = torch.zeros(world * 2 * Bl, dtype=torch.float64, device="cuda")
+    out4_local = torch.zeros(4, dtype=torch.float64, device="cuda")
+    out4_all = torch.zeros(world * 4, dtype=torch.float64, device="cuda")
 
     def one_step(t):
         tp, gp = d_tok[t].data_ptr(), d_gold[t].data_ptr()
+        if qdir:
+            import torch.distributed as dist
+            eng.qdir_score_async(zcfg.seed, t, G, rank, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, B)
+            eng.out4_io(out4_local.data_ptr(), False)
+            dist.all_gather_into_tensor(out4_all, out4_local)  # 32 B per rank
+            eng.qdir_apply_async(zcfg.seed, t, G, zcfg.learning_rate, out4_all.data_ptr())
+            if ((t + 1) * G) % zcfg.nu == 0:
+                eng.fold_async()
+            return
         if world == 1:
             if args.graph:
                 eng.step_graph(zcfg.seed, t, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, Bl)
@@ -287,19 +318,21 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
-    value = 1000.0 / ms_step
-    windows = sum(1 for t in range(args.warmup, nsteps) if t % zcfg.nu == 0)
-    launches = args.steps * launches_per_step(mcfg.n_layers, 4 * mcfg.n_layers + 1, False) + windows * (
+    value = 1000.0 * G / ms_step  # reference steps (ZO directions) per second, whole job
+    windows = sum(1 for t in range(args.warmup, nsteps) if (t * G) % zcfg.nu == 0)
+    launches = args.steps * (launches_per_step(mcfg.n_layers, 4 * mcfg.n_layers + 1, False)
+                             + (G - 1) * 6) + windows * (
         5 + 2 * (4 * mcfg.n_layers + 1))
 
     hbm_peak, tf_peak, peak_kind = peaks()
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": args.precision,
+            "scaling": "strong" if (world > 1 and not qdir) else "weak", "vs_baseline": None,
+            "dtype": args.precision,
             "data": "synthetic (marker task, random-init Role.INIT weights)",
             "config": {"workload": f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, "
                                    f"nu={args.nu}, fold amortised", "model": args.model, "global_batch": B,
-                       "seq_len": T, "parallelism": f"exact-dp{world}" if world > 1 else "single",
+                       "seq_len": T, "parallelism": (f"qdir{world}" if qdir else f"exact-dp{world}") if world > 1 else "single",
                        "l2": "inputs larger than L2 (25.7 GB 16-bit weights/step at 13B); no flush"},
             "scored_tokens_per_s": value * 2 * B * T, "option_tokens_per_s": value * 2 * B,
             "gpu_launches": launches, "clocks": clk.summary(), "init_s": t_init,

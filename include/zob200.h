@@ -137,6 +137,19 @@ int zo_step_score_async(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, d
                         const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B);
 int zo_step_apply_async(zo_ctx* ctx, double epsilon, double lr, int32_t divide_by_r, int32_t B_total);
 int zo_read_out4(zo_ctx* ctx, double* out4);
+/* q-direction mode (SURVEY.md §8(e) mode 2; no reference counterpart -- the
+ * reference has no multi-query estimator): rank g of G scores
+ * reference step s = macro_step*G + g (its U, V window and minibatch) at the
+ * shared state and leaves [L+, L-, c, beta] in the ctx (zo_out4_io moves it to /
+ * from the all-gather buffers).  zo_qdir_apply_async regenerates every U_s and
+ * applies the G updates in g order from the gathered [G, 4] device array.
+ * lozo needs G | nu.  G = 1 reproduces zo_step_async. */
+int zo_qdir_score_async(zo_ctx* ctx, uint64_t seed, uint64_t macro_step, int32_t G, int32_t g, int32_t nu,
+                        double epsilon, double lr, int32_t divide_by_r, const int32_t* tokens_dev,
+                        const int32_t* gold_dev, int32_t B);
+int zo_out4_io(zo_ctx* ctx, void* dev, int32_t to_ctx);
+int zo_qdir_apply_async(zo_ctx* ctx, uint64_t seed, uint64_t macro_step, int32_t G, double lr,
+                        const double* out4_all_dev);
 /* per-phase device time of the last zo_step (ms): [sample, score, update] */
 int zo_last_step_ms(zo_ctx* ctx, float ms[3]);
 

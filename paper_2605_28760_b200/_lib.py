@@ -71,6 +71,10 @@ SIGNATURES = [
                                        _c.c_int32]),
     ("zo_step_apply_async", _c.c_int, [_P, _c.c_double, _c.c_double, _c.c_int32, _c.c_int32]),
     ("zo_read_out4", _c.c_int, [_P, _P]),
+    ("zo_qdir_score_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_int32, _c.c_int32,
+                                       _c.c_double, _c.c_double, _c.c_int32, _P, _P, _c.c_int32]),
+    ("zo_out4_io", _c.c_int, [_P, _P, _c.c_int32]),
+    ("zo_qdir_apply_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _P]),
     ("zo_last_step_ms", _c.c_int, [_P, _c.POINTER(_c.c_float)]),
     ("zo_fnv1a64", _c.c_uint64, [_P, _c.c_uint64, _c.c_uint64]),
     ("zo_bench_gemm", _c.c_int, [_P, _c.c_int32, _c.c_int32, _c.c_int32, _c.POINTER(_c.c_float),

@@ -583,7 +583,8 @@ void launch_coefficient(const double* nll, int B, double eps, double lr, int div
 // ------------------------------------------------------------------ update (K8), probe prep
 __global__ void k_update(double* __restrict__ A, const double* __restrict__ U, int64_t n,
                          const double* __restrict__ out4, const unsigned* __restrict__ abort_flag) {
-  if (*abort_flag) return;
+  // abort_flag == nullptr: a gathered coefficient (q-direction mode) -- skip when its losses are non-finite
+  if (abort_flag ? *abort_flag != 0u : !(isfinite(out4[0]) && isfinite(out4[1]))) return;
   const double beta = out4[3];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
@@ -679,7 +680,7 @@ __global__ void k_fold_dev(double* __restrict__ W, int m, int n, const double* _
                            const double* __restrict__ Vv, int r, const double* __restrict__ out4, double lr,
                            double scale, const unsigned* __restrict__ abort_flag, void* __restrict__ W16, int ldw,
                            int transposed, bool bf16) {
-  if (*abort_flag) return;
+  if (abort_flag ? *abort_flag != 0u : !(isfinite(out4[0]) && isfinite(out4[1]))) return;
   const double alpha = __dmul_rn(-__dmul_rn(lr, out4[2]), scale);
   __shared__ float tile[32][33];
   const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;

@@ -897,9 +897,6 @@ uint64_t zo_digest_chain(const char* const* lids, const double* arena, const int
 // Stream-ordered step with device-resident inputs and no host synchronisation
 // (tokens_dev [B, T], gold_dev [B, opt_len] int32).  Results stay on the device
 // (zo_read_out4); a non-finite loss disarms the update on the device.
-// Stream-ordered step with device-resident inputs and no host synchronisation
-// (tokens_dev [B, T], gold_dev [B, opt_len] int32).  Results stay on the device
-// (zo_read_out4); a non-finite loss disarms the update on the device.
 // zo_step_score_async = directions + probes + paired scoring (per-example NLLs
 // in the ctx); zo_step_apply_async = canonical mean / c / update over B_total
 // examples.  Multi-GPU exact mode all-gathers the NLLs between the two.
@@ -1023,6 +1020,73 @@ extern "C" int zo_step_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu
 extern "C" int zo_fold_async(zo_ctx* c) {
   ZO_API_BEGIN
   if (c->d.estimator == ZO_EST_LOZO) fold_all(c);
+  return ZO_OK;
+  ZO_API_END
+}
+
+// ------------------------------------------------------------------ q-direction mode
+// SURVEY.md §8(e) mode 2: G ranks share the parameter state of macro-step t; rank
+// g scores the direction, window and minibatch of reference step s = t*G + g on a
+// full batch and computes its own [L+, L-, c, beta].  After the [G, 4] coefficients
+// are all-gathered (32 B per rank), every rank regenerates U_s for all g from the
+// counter-keyed stream and applies A += beta_g * U_g in g order (lozo), or the
+// dense factorized update per g -- identical replicas, no weight traffic.
+// G | nu keeps the G directions inside one window (they share V_win); G = 1 is
+// exactly zo_step_async.
+extern "C" int zo_qdir_score_async(zo_ctx* c, uint64_t seed, uint64_t macro_step, int32_t G, int32_t g, int32_t nu,
+                                   double eps, double lr, int32_t divide_by_r, const int32_t* tokens_dev,
+                                   const int32_t* gold_dev, int32_t B) {
+  ZO_API_BEGIN
+  check(G >= 1 && g >= 0 && g < G, ZO_ERR_CONFIG, "q-direction rank out of range");
+  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  check(!lozo || nu % G == 0, ZO_ERR_CONFIG, "q-direction mode needs the direction count to divide nu");
+  int rc = zo_step_score_async(c, seed, macro_step * (uint64_t)G + (uint64_t)g, lozo ? nu : 1, eps, tokens_dev,
+                               gold_dev, B);
+  if (rc) return rc;
+  launch_coefficient(c->nll, B, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
+  return ZO_OK;
+  ZO_API_END
+}
+
+// The ctx's [L+, L-, c, beta] <-> an external device buffer (the all-gather's send /
+// receive slots); stream-ordered.
+extern "C" int zo_out4_io(zo_ctx* c, void* dev, int32_t to_ctx) {
+  ZO_API_BEGIN
+  check(dev != nullptr, ZO_ERR_INPUT, "null buffer");
+  if (to_ctx)
+    ZO_CUDA_TRY(cudaMemcpyAsync(c->out4, dev, 32, cudaMemcpyDeviceToDevice, c->st));
+  else
+    ZO_CUDA_TRY(cudaMemcpyAsync(dev, c->out4, 32, cudaMemcpyDeviceToDevice, c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+extern "C" int zo_qdir_apply_async(zo_ctx* c, uint64_t seed, uint64_t macro_step, int32_t G, double lr,
+                                   const double* out4_all_dev) {
+  ZO_API_BEGIN
+  check(G >= 1 && out4_all_dev != nullptr, ZO_ERR_CONFIG, "bad q-direction gather");
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  for (int32_t g = 0; g < G; ++g) {
+    k_set_u64<<<1, 1, 0, c->st>>>(c->d_step, macro_step * (uint64_t)G + (uint64_t)g);
+    sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+    const double* o4 = out4_all_dev + 4 * (size_t)g;
+    if (lozo) {
+      launch_update(c->A, c->U, c->su, o4, nullptr, c->st);
+    } else {
+      // factorized: V is keyed by the step too (zo_engine.py:181-191)
+      sampler_launch(c->planV, seed, c->d_step, 1, c->V, c->st);
+      for (auto& m : c->mats)
+        launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, o4, lr,
+                        1.0 / std::sqrt((double)c->r), nullptr, m.W16, m.kind == K_EMBED ? (int)m.n : m.ldw,
+                        m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
+    }
+  }
+  if (lozo) c->a_dirty = true;
+  else c->v_window = -1;  // V holds the last direction's; the next score resamples it
+  // the ctx out4 mirrors the last direction (zo_read_out4)
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->out4, out4_all_dev + 4 * (size_t)(G - 1), 32, cudaMemcpyDeviceToDevice, c->st));
+  ZO_CUDA_TRY(cudaGetLastError());
   return ZO_OK;
   ZO_API_END
 }

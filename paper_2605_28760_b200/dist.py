@@ -39,3 +39,37 @@ def exchange_nll(nll_local, world: int, group=None):
     out = torch.empty(world * 2 * bl, dtype=nll_local.dtype, device=nll_local.device)
     dist.all_gather_into_tensor(out, nll_local.reshape(-1).contiguous(), group=group)
     return canonical_order(out, world, bl)
+
+
+# ---------------------------------------------------------------- q-direction mode
+# SURVEY.md §8(e) mode 2 (zob200.h zo_qdir_*): rank g of G scores reference step
+# s = t*G + g -- its own U, window V and minibatch -- on a FULL batch at the shared
+# state of macro-step t, so each GPU keeps M = 2*B*T rows (compute-bound) and the
+# job processes G reference directions per macro-step ("weak" scaling).  The only
+# exchange is the [L+, L-, c, beta] of every rank (32 B); each rank regenerates the
+# G counter-keyed U's and applies the G updates in g order -> identical replicas.
+
+
+def qdir_steps(t: int, world: int) -> list[int]:
+    """Reference step indices of macro-step t (rank order)."""
+    return [t * world + g for g in range(world)]
+
+
+def check_qdir(world: int, nu: int, estimator: str = "lozo_lazy") -> None:
+    if estimator == "lozo_lazy" and nu % world:
+        raise ValueError(f"q-direction mode needs the direction count {world} to divide nu={nu}")
+
+
+def exchange_out4(out4_local, world: int, group=None):
+    """All-gather every rank's [L+, L-, c, beta] -> [world, 4] in rank (= g) order."""
+    import torch
+    import torch.distributed as dist
+    out = torch.empty(world * 4, dtype=out4_local.dtype, device=out4_local.device)
+    dist.all_gather_into_tensor(out, out4_local.reshape(-1).contiguous(), group=group)
+    return out.view(world, 4)
+
+
+def fold_due(t: int, world: int, nu: int) -> bool:
+    """run_serving_path folds after reference step s when (s+1) % nu == 0
+    (runtime.py:327-330); the last step of macro-step t is s = t*world + world - 1."""
+    return ((t + 1) * world) % nu == 0

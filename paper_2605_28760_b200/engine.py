@@ -221,6 +221,19 @@ class ZoEngine:
     def step_apply_async(self, epsilon: float, lr: float, divide_by_r: bool, B_total: int) -> None:
         check(lib().zo_step_apply_async(self._h, float(epsilon), float(lr), int(divide_by_r), B_total))
 
+    def qdir_score_async(self, seed: int, macro_step: int, G: int, g: int, nu: int, epsilon: float, lr: float,
+                         divide_by_r: bool, tokens_dev: int, gold_dev: int, B: int) -> None:
+        """q-direction mode: score reference step macro_step*G + g (zob200.h)."""
+        check(lib().zo_qdir_score_async(self._h, seed, macro_step, G, g, nu, float(epsilon), float(lr),
+                                        int(divide_by_r), ctypes.c_void_p(tokens_dev), ctypes.c_void_p(gold_dev),
+                                        B))
+
+    def out4_io(self, dev_ptr: int, to_ctx: bool) -> None:
+        check(lib().zo_out4_io(self._h, ctypes.c_void_p(dev_ptr), int(to_ctx)))
+
+    def qdir_apply_async(self, seed: int, macro_step: int, G: int, lr: float, out4_all_dev: int) -> None:
+        check(lib().zo_qdir_apply_async(self._h, seed, macro_step, G, float(lr), ctypes.c_void_p(out4_all_dev)))
+
     def fold_async(self) -> None:
         check(lib().zo_fold_async(self._h))
 

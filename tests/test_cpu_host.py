@@ -170,3 +170,102 @@ def test_exact_mode_exchange_gloo_world2(tmp_path):
     outs = [p.communicate(timeout=240) for p in procs]
     res = [json.loads(o[0].strip().splitlines()[-1]) for o in outs]
     assert res[0]["c"] == res[1]["c"] == res[0]["ref"]  # bitwise: identical c on every rank
+
+
+_QDIR_WORKER = r"""
+import os, sys, json
+import numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, {repo!r})
+from oracle import reference as R
+from paper_2605_28760_b200.dist import exchange_out4, qdir_steps, fold_due, check_qdir
+dist.init_process_group("gloo", init_method="tcp://127.0.0.1:{port}", rank=int(sys.argv[1]), world_size=2)
+g, G, nu = dist.get_rank(), 2, 4
+check_qdir(G, nu)
+cfg = R.ModelCfg(vocab=64, dim=16, n_layers=1, n_heads=2, prompt_len=7, init_seed=7, init_scale=0.08)
+splits = R.generate_task(R.TaskCfg(seed=11, vocab=64, prompt_len=7, train_size=32, dev_size=4, val_size=4))
+z = R.ZoCfg(seed=42, epsilon=1e-3, learning_rate=1e-2, rank=2, nu=nu, batch_size=4)
+params = R.init_params(cfg)
+st = R.LozoState()
+def batch(s):
+    p, gl, idx = R.sample_minibatch(splits, "train", z.seed, s, z.batch_size)
+    gold = np.array([[cfg.vocab - 2], [cfg.vocab - 1]])[gl]
+    return np.concatenate([p, gold], axis=1), gold, idx
+for t in range(4):
+    s = qdir_steps(t, G)[g]
+    # this rank's direction only (the CPU stand-in for zo_qdir_score_async)
+    sg = R.LozoState({{k: v.copy() for k, v in st.A.items()}}, R.window_v(params, z, s) if st.A else {{}})
+    rec, _ = R.lozo_step(params, cfg, sg, z, s, *batch(s))
+    out4 = torch.tensor([rec.loss_plus, rec.loss_minus, rec.coefficient, rec.beta], dtype=torch.float64)
+    allc = exchange_out4(out4, G).numpy()
+    st.V = sg.V
+    for gg in range(G):  # zo_qdir_apply_async: every U regenerated, g order
+        dirs, _, _ = R.step_dirs({{k: v.shape for k, v in params.items() if v.ndim == 2}}, z, t * G + gg)
+        for lid, (u, _v) in dirs.items():
+            st.A.setdefault(lid, np.zeros((params[lid].shape[0], z.rank)))
+            st.A[lid] = st.A[lid] + allc[gg, 3] * u
+    if fold_due(t, G, nu):
+        R.fold_all(params, st)
+print(json.dumps({{"rank": g, "digest": R.params_digest(params),
+                  "a": float(sum(np.abs(a).sum() for a in st.A.values()))}}))
+dist.destroy_process_group()
+"""
+
+
+def test_qdir_mode_exchange_gloo_world2(tmp_path):
+    """Two ranks each score one direction per macro-step, exchange [L+,L-,c,beta] over
+    gloo and apply both updates: both replicas end bit-identical to the single-process
+    q-direction oracle (oracle.reference.qdir_macro_step)."""
+    import socket
+    sys.path.insert(0, REPO)
+    from oracle import reference as R
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    script = tmp_path / "q.py"
+    script.write_text(_QDIR_WORKER.format(repo=REPO, port=port))
+    procs = [subprocess.Popen([sys.executable, str(script), str(r)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                              text=True) for r in range(2)]
+    outs = [p.communicate(timeout=240) for p in procs]
+    res = [json.loads(o[0].strip().splitlines()[-1]) for o in outs]
+    assert res[0] == {**res[1], "rank": 0}
+    # single-process restatement
+    G, nu = 2, 4
+    cfg = R.ModelCfg(vocab=64, dim=16, n_layers=1, n_heads=2, prompt_len=7, init_seed=7, init_scale=0.08)
+    splits = R.generate_task(R.TaskCfg(seed=11, vocab=64, prompt_len=7, train_size=32, dev_size=4, val_size=4))
+    z = R.ZoCfg(seed=42, epsilon=1e-3, learning_rate=1e-2, rank=2, nu=nu, batch_size=4)
+    params = R.init_params(cfg)
+    st = R.LozoState()
+    for t in range(4):
+        bs = []
+        for s in range(t * G, t * G + G):
+            p, gl, idx = R.sample_minibatch(splits, "train", z.seed, s, z.batch_size)
+            gold = np.array([[cfg.vocab - 2], [cfg.vocab - 1]])[gl]
+            bs.append((np.concatenate([p, gold], axis=1), gold, idx))
+        R.qdir_macro_step(params, cfg, st, z, t, G, bs)
+        if ((t + 1) * G) % nu == 0:
+            R.fold_all(params, st)
+    assert res[0]["digest"] == R.params_digest(params)
+    assert res[0]["a"] == float(sum(np.abs(a).sum() for a in st.A.values()))
+
+
+def test_qdir_G1_oracle_is_lozo_step():
+    """qdir_macro_step with G = 1 reproduces the reference's lozo_step exactly."""
+    sys.path.insert(0, REPO)
+    from oracle import reference as R
+    cfg = R.ModelCfg(vocab=64, dim=16, n_layers=1, n_heads=2, prompt_len=7, init_seed=7, init_scale=0.08)
+    splits = R.generate_task(R.TaskCfg(seed=11, vocab=64, prompt_len=7, train_size=32, dev_size=4, val_size=4))
+    z = R.ZoCfg(seed=42, epsilon=1e-3, learning_rate=1e-2, rank=2, nu=2, batch_size=4)
+    pa, pb = R.init_params(cfg), R.init_params(cfg)
+    sa, sb = R.LozoState(), R.LozoState()
+    for t in range(4):
+        p, gl, idx = R.sample_minibatch(splits, "train", z.seed, t, z.batch_size)
+        gold = np.array([[cfg.vocab - 2], [cfg.vocab - 1]])[gl]
+        tok = np.concatenate([p, gold], axis=1)
+        ra, _ = R.lozo_step(pa, cfg, sa, z, t, tok, gold, idx)
+        (rb,) = R.qdir_macro_step(pb, cfg, sb, z, t, 1, [(tok, gold, idx)])
+        assert ra == rb
+        if (t + 1) % z.nu == 0:
+            R.fold_all(pa, sa)
+            R.fold_all(pb, sb)
+    assert R.params_digest(pa) == R.params_digest(pb)
