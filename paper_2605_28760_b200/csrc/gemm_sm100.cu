@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -191,23 +193,28 @@ struct GemmParams {
   const float* xPm;
   int xr, xrps, tpart_ld;
   float* tpart;
-  // stream-K (sk = 1): CTA c owns global k-iterations [c*sk_w, min((c+1)*sk_w, tiles*num_kb));
-  // a tile split between CTAs c-1 (k-start part, owns the epilogue) and c (k-end part,
-  // publishes an fp32 partial in sk_ws[c] + sk_flags[c]) is summed in that fixed order.
+  // stream-K tail (sk = 1): unit u (a CTA, or a CTA pair when CG = 2) owns the global
+  // k-iterations [sk_dp*num_kb + u*sk_w, +sk_w) of the tiles past the data-parallel
+  // waves.  A segment that starts after the tile's first k-block publishes its fp32
+  // partial (sk_ws / sk_flags slot of its CTA); the unit holding the first k-block owns
+  // the epilogue: its accumulator + the later units' partials in ascending k order --
+  // a fixed summation order, independent of timing.
   int sk, sk_w, sk_dp;
   float* sk_ws;
   unsigned* sk_flags;
 };
 
-// Work segments of one CTA: (tile, k-block range).  Data-parallel phase: whole
-// tiles blockIdx + i*grid below sk_dp (M-fastest order, so the CTAs resident at
-// once share weight tiles in L2); stream-K phase (sk = 1): the remaining tiles'
-// k-iterations split evenly, CTA c owning [sk_dp*kb + c*sk_w, +sk_w).
+// Work segments of one unit: (tile, k-block range).  Data-parallel phase: whole
+// tiles unit + i*units below sk_dp (M-fastest order, so the units resident at once
+// share weight tiles in L2); stream-K tail (sk = 1): the remaining (< one wave of)
+// tiles' k-iterations split evenly, unit u owning [sk_dp*kb + u*sk_w, +sk_w) -- the
+// units working on one tile read disjoint k-slices, so no operand is fetched twice.
 struct SegIter {
-  int cursor, hi, dp, step;
+  int cursor, hi, dp, step, unit;
   __device__ __forceinline__ void init(const GemmParams& p, int cg = 1) {
     dp = 1;
-    cursor = blockIdx.x / cg;  // CTA pairs share one tile when cg = 2
+    unit = blockIdx.x / cg;  // CTA pairs share one tile (and one stream-K range) when cg = 2
+    cursor = unit;
     step = gridDim.x / cg;
     hi = p.sk ? p.sk_dp : p.m_tiles * p.n_tiles;
   }
@@ -223,7 +230,7 @@ struct SegIter {
       if (!p.sk) return false;
       dp = 0;
       const int total = p.m_tiles * p.n_tiles * p.num_kb;
-      cursor = p.sk_dp * p.num_kb + blockIdx.x * p.sk_w;
+      cursor = p.sk_dp * p.num_kb + unit * p.sk_w;
       hi = min(total, cursor + p.sk_w);
     }
     if (cursor >= hi) return false;
@@ -385,30 +392,84 @@ __global__ void __launch_bounds__(192, 1)
       const int row = m0 + erow;
       const bool row_ok = row < p.M;
       if (k0 > 0) {
-        // k-end part of a split tile: publish the raw fp32 partial for CTA blockIdx-1
-        float* ws = p.sk_ws + ((size_t)blockIdx.x * C::BM + erow) * BN;
+        // not the tile's first k-block: publish the raw fp32 partial for the owner
+        // [BN/4][128 rows] float4 layout: the 32 lanes of a store write 512 contiguous bytes
+        float4* ws = reinterpret_cast<float4*>(p.sk_ws + (size_t)blockIdx.x * C::BM * BN) + erow;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           float v[32];
           tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            reinterpret_cast<float4*>(ws + c)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            ws[(size_t)(c / 4 + j) * C::BM] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty0 + 8 * acc);
+        if (lane == 0) {
+          if constexpr (CG == 2)
+            mbar_arrive_remote(tempty0 + 8 * acc, 0);
+          else
+            mbar_arrive(tempty0 + 8 * acc);
+        }
         __threadfence();
         named_bar_sync(1, 128);
         if (warp == 2 && lane == 0) st_release(p.sk_flags + blockIdx.x, 1u);
         continue;
       }
-      const bool split = k1 < p.num_kb;  // k-start part: add the partial of CTA blockIdx+1
-      const float* wsin = split ? p.sk_ws + ((size_t)(blockIdx.x + 1) * C::BM + erow) * BN : nullptr;
+      // owner (holds the tile's first k-block) of a tile whose later k-blocks were done
+      // by units si.unit+1 .. jend-1; their segments are their FIRST tail segments, so
+      // no unit's publication waits on another's (no dependency chains)
+      int jfirst = si.unit + 1, jend = si.unit + 1;
+      if (k1 < p.num_kb) jend = ((t + 1) * p.num_kb - 1 - p.sk_dp * p.num_kb) / p.sk_w + 1;
+      const bool split = jfirst < jend;
       if (split) {
-        for (uint32_t i = 0; ld_acquire(p.sk_flags + blockIdx.x + 1) == 0u; ++i)
-          if (i > (1u << 28)) __trap();
+        // one lane per warp polls (with backoff, so the spinning owners do not hammer the
+        // flags' L2 slice while the tail's TMA traffic is in flight); __syncwarp orders
+        // the acquire before the other lanes' partial loads
+        if (lane == 0)
+          for (int j = jfirst; j < jend; ++j)
+            for (uint32_t i = 0; ld_acquire(p.sk_flags + j * CG + (int)rank) == 0u; ++i) {
+              __nanosleep(128);
+              if (i > (1u << 24)) __trap();
+            }
+        __syncwarp();
       }
+      // own accumulator (the tile's first k-blocks) + the partials in ascending k order
+      auto add_partials = [&](float (&v)[32], int c) {
+        // two partials' chunks in flight per step (16 independent 16-byte loads per lane)
+        int j = jfirst;
+#pragma unroll 1
+        for (; j + 1 < jend; j += 2) {
+          const float4* wa =
+              reinterpret_cast<const float4*>(p.sk_ws + (size_t)(j * CG + (int)rank) * C::BM * BN) + erow;
+          const float4* wb = wa + (size_t)CG * C::BM * BN / 4;
+          float4 a[8], b[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            a[e] = wa[(size_t)(c / 4 + e) * C::BM];
+            b[e] = wb[(size_t)(c / 4 + e) * C::BM];
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            v[4 * e] = (v[4 * e] + a[e].x) + b[e].x;
+            v[4 * e + 1] = (v[4 * e + 1] + a[e].y) + b[e].y;
+            v[4 * e + 2] = (v[4 * e + 2] + a[e].z) + b[e].z;
+            v[4 * e + 3] = (v[4 * e + 3] + a[e].w) + b[e].w;
+          }
+        }
+        if (j < jend) {
+          const float4* wa =
+              reinterpret_cast<const float4*>(p.sk_ws + (size_t)(j * CG + (int)rank) * C::BM * BN) + erow;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float4 w = wa[(size_t)(c / 4 + e) * C::BM];
+            v[4 * e] += w.x;
+            v[4 * e + 1] += w.y;
+            v[4 * e + 2] += w.z;
+            v[4 * e + 3] += w.w;
+          }
+        }
+      };
       constexpr bool GELU = (EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT);
       constexpr bool OUT16 = (EPI == EPI_STORE16 || GELU);
       float tp[8];
@@ -434,16 +495,7 @@ __global__ void __launch_bounds__(192, 1)
             }
             float v[32];
             tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
-            if (split) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 w = reinterpret_cast<const float4*>(wsin + c)[j];
-                v[4 * j] += w.x;
-                v[4 * j + 1] += w.y;
-                v[4 * j + 2] += w.z;
-                v[4 * j + 3] += w.w;
-              }
-            }
+            if (split) add_partials(v, c);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               reinterpret_cast<float4*>(o + c)[j] =
@@ -459,16 +511,7 @@ __global__ void __launch_bounds__(192, 1)
       for (int c = 0; c < BN; c += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
-        if (split) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 w = reinterpret_cast<const float4*>(wsin + c)[j];
-            v[4 * j] += w.x;
-            v[4 * j + 1] += w.y;
-            v[4 * j + 2] += w.z;
-            v[4 * j + 3] += w.w;
-          }
-        }
+        if (split) add_partials(v, c);
         const int col0 = n0 + c;
         if (!row_ok || col0 >= p.N) continue;
         const size_t lin = (size_t)row * p.ldo + col0;
@@ -546,7 +589,8 @@ __global__ void __launch_bounds__(192, 1)
     tile_done:
       if (split) {
         named_bar_sync(1, 128);
-        if (warp == 2 && lane == 0) p.sk_flags[blockIdx.x + 1] = 0u;  // re-arm for the next launch
+        if (warp == 2 && lane < jend - jfirst)  // re-arm the consumed flags for the next launch
+          for (int j = jfirst + lane; j < jend; j += 32) p.sk_flags[j * CG + (int)rank] = 0u;
       }
       if constexpr (EPI == EPI_GELU16_EXT) {
         if (row_ok) {
@@ -636,7 +680,25 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
     return !e || std::atoi(e) != 0;
   }();
   g.cg = (cg2_on && bn >= 128 && M >= 512) ? 2 : 1;
-  if (g.cg == 2) g.bn = bn = 256;  // N=128 pair tiles measured 1.4-1.5x slower (A re-reads, fixed costs)
+  if (g.cg == 2) {
+    // N=128 pair tiles measured 1.4-1.5x slower (A re-reads, fixed costs).  Between 256
+    // and 192 pick the smaller ragged-wave cost: rounds * BN (the per-round tile time),
+    // with a 10% handicap on 192 for its extra A re-reads and per-MMA overheads.  At
+    // M=2048, N=5120 (attn_out, ff_down): 160 tiles = 2.16 waves of 74 pairs at 256,
+    // 216 tiles = 2.92 waves at 192.
+    const int mt2 = (M + 255) / 256, slots2 = num_sms / 2;
+    auto cost = [&](int b) {
+      const long tiles = (long)mt2 * ((N + b - 1) / b);
+      return (double)((tiles + slots2 - 1) / slots2) * b * (b == 256 ? 1.0 : 1.1);
+    };
+    static const bool bn192 = [] {
+      const char* e = std::getenv("ZO_BN192");
+      return e && std::atoi(e) != 0;
+    }();
+    // measured no faster than 256 (3 rounds of 192-wide tiles ~ 3 ragged rounds of 256:
+    // the narrower tile re-reads A 33% more); the stream-K tail fixes the ragged wave
+    g.bn = bn = (bn192 && cost(192) < cost(256)) ? 192 : 256;
+  }
   const int mt = (M + 128 * g.cg - 1) / (128 * g.cg);
   const int tiles = mt * ((N + bn - 1) / bn);
   const int slots = num_sms / g.cg;
@@ -670,7 +732,7 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.xrps = g.xrps;
   p.tpart_ld = g.tpart_ld;
   p.tpart = g.tpart;
-  p.sk = CG == 1 ? g.sk : 0;
+  p.sk = g.sk;
   p.sk_w = g.sk_w;
   p.sk_dp = g.sk_dp;
   p.sk_ws = g.sk_ws;
@@ -710,33 +772,73 @@ static void launch_e(const GemmDesc& g, cudaStream_t st) {
   }
 }
 
+// Co-resident 2-CTA clusters of the pair kernel (stream-K spins on peers, so every
+// unit must be resident at once; a GPC with an odd SM count leaves one SM unpaired).
+static int max_pair_units(int num_sms) {
+  static int units = -1;
+  if (units < 0) {
+    using C = GemmCfg<256, 2>;
+    auto* fn = k_gemm<256, EPI_STORE16, false, 0, 2>;
+    ZO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (num_sms / 2));
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    ZO_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, fn, &cfg));
+    units = n;
+    if (std::getenv("ZO_DEBUG")) fprintf(stderr, "[zob200] max co-resident CTA pairs: %d\n", n);
+  }
+  return units;
+}
+
 void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
-  const int m_tiles = (g.M + 127) / 128, n_tiles = (g.N + g.bn - 1) / g.bn;
+  // Data-parallel whole tiles for every full wave, then the last partial wave's tiles
+  // split k-wise over ALL persistent units (CTAs, or CTA pairs when cg = 2), so the
+  // ragged last wave disappears.  The units sharing a tail tile read disjoint k-slices
+  // of its operands (no re-reads); a full-waves-only (non-tail) stream-K split was
+  // measured slower -- units at scattered k offsets lose the L2 sharing of the
+  // lock-step data-parallel waves.
+  if (!ws || !flags) return;
+  const int cg = g.cg;
+  int units = g.grid / cg;
+  if (cg == 2) units = std::min(units, max_pair_units(num_sms));
+  const int m_tiles = (g.M + 128 * cg - 1) / (128 * cg), n_tiles = (g.N + g.bn - 1) / g.bn;
   const int tiles = m_tiles * n_tiles;
-  // worth it when the last wave is ragged; keep >= one full wave in the stream-K phase so
-  // every CTA owns >= one tile of k-iterations (<= 2 segments per split tile)
-  if (g.cg != 1 || tiles <= num_sms || tiles % num_sms == 0 || !ws || !flags) return;
-  const int dp_waves = tiles / num_sms - 1;
-  const int sk_tiles = tiles - dp_waves * num_sms;
-  const long sk_iters = (long)sk_tiles * g.num_kb;
-  const int w = (int)((sk_iters + num_sms - 1) / num_sms);
-  if (w < g.num_kb) return;
+  if (units < 2 || tiles <= units || tiles % units == 0) return;
+  const int dp_waves = tiles / units;
+  const int tail = tiles - dp_waves * units;
+  const long sk_iters = (long)tail * g.num_kb;
+  const int w = (int)((sk_iters + units - 1) / units);
+  // too fine: each owner would sum many partials; measured a loss at M=2048 attn_out
+  // (12 tail tiles x 81 k-blocks over 74 pairs -> 14 per unit), a gain for ff_down (53)
+  if (w < 32) return;
+  // only a mostly-empty last wave pays for the fixup (13B: ff_down's 12 of 74 pairs,
+  // 382 -> 350 us; qkv's 36/74 and ff_up's 48/74 measured neutral-to-worse)
+  if (3 * tail > units) return;
   g.sk = 1;
-  g.sk_dp = dp_waves * num_sms;
+  g.sk_dp = dp_waves * units;
   g.sk_w = w;
   g.sk_ws = ws;
   g.sk_flags = flags;
-  g.grid = num_sms;
+  g.grid = units * cg;
 }
 
 void gemm_launch(const GemmDesc& g, cudaStream_t st) {
   if (g.cg == 2) {
     if (g.bf16) {
       if (g.bn == 256) launch_e<256, true, 2>(g, st);
-      else launch_e<128, true, 2>(g, st);
+      else launch_e<192, true, 2>(g, st);
     } else {
       if (g.bn == 256) launch_e<256, false, 2>(g, st);
-      else launch_e<128, false, 2>(g, st);
+      else launch_e<192, false, 2>(g, st);
     }
     return;
   }

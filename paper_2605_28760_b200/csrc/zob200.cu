@@ -117,7 +117,7 @@ struct zo_ctx {
   float* tpart = nullptr;         // fused LoRA-extension partials [tiles][Mpad][r]
   float* sk_ws = nullptr;         // stream-K partial tiles
   unsigned* sk_flags = nullptr;
-  bool streamk = false;  // ZO_STREAMK=1 enables the DP + stream-K tail schedule
+  bool streamk = true;  // DP waves + stream-K tail where it pays (ZO_STREAMK=0 disables)
   int tpart_tiles = 0;
   bool fused_ext = true;
   // timing

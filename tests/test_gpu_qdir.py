@@ -107,6 +107,9 @@ def test_qdir_lozo_vs_oracle(G, nu):
             np.testing.assert_array_equal(got[lid], A[lid])
         # keep the oracle on the device's trajectory (coefficients differ within tolerance)
         st.A = {k: v.copy() for k, v in got.items()}
+        if ((t + 1) * G) % nu == 0:  # run_serving_path's fold after the window's last step
+            eng.fold()
+            R.fold_all(params, st)
     assert eng.sampler_flags()[0] == 0
     eng.close()
 
