@@ -81,21 +81,23 @@ __global__ void __launch_bounds__(TP * 2)
     const float* Pg = ((seq * T) < x.rps ? x.Pp : x.Pm) + (size_t)h * DH * x.r;
     for (int i = threadIdx.x; i < DH * x.r; i += blockDim.x) sP[i] = Pg[i];
   }
-  // stage Q, K, V (16-byte vectors; rows >= T zero)
+  // stage Q, K, V with asynchronous 16-byte copies (cp.async): every load of the CTA is
+  // in flight at once instead of one dependent load/store round trip per row block
+  // (the kernel is bound by this read of qkv); rows >= T are zero-filled
   constexpr int VPR = DH / 8;
   for (int idx = threadIdx.x; idx < TP * VPR; idx += blockDim.x) {
     const int t = idx / VPR, c = (idx % VPR) * 8;
-    uint4 q = make_uint4(0, 0, 0, 0), k = q, v = q;
-    if (t < T) {
-      const uint16_t* src = qkv + (size_t)(seq * T + t) * ldq + (size_t)h * DH + c;
-      q = *reinterpret_cast<const uint4*>(src);
-      k = *reinterpret_cast<const uint4*>(src + d);
-      v = *reinterpret_cast<const uint4*>(src + 2 * d);
-    }
-    *reinterpret_cast<uint4*>(sq + t * LD + c) = q;
-    *reinterpret_cast<uint4*>(sk + t * LD + c) = k;
-    *reinterpret_cast<uint4*>(sv + t * LD + c) = v;
+    const uint32_t dq = static_cast<uint32_t>(__cvta_generic_to_shared(sq + t * LD + c));
+    const uint32_t dk = static_cast<uint32_t>(__cvta_generic_to_shared(sk + t * LD + c));
+    const uint32_t dv = static_cast<uint32_t>(__cvta_generic_to_shared(sv + t * LD + c));
+    const uint16_t* src = qkv + (size_t)(seq * T + (t < T ? t : 0)) * ldq + (size_t)h * DH + c;
+    const int nbytes = t < T ? 16 : 0;  // src-size 0: the 16 bytes are zero-filled
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dq), "l"(src), "r"(nbytes) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dk), "l"(src + d), "r"(nbytes) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dv), "l"(src + 2 * d), "r"(nbytes)
+                 : "memory");
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = warp * 16;

@@ -150,9 +150,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 }
 
 __device__ __forceinline__ float gelu_tanh(float x) {
-  // model.py:145-146: 0.5*x*(1 + tanh(sqrt(2/pi)*(x + 0.044715*x^3)))
-  const float c = 0.7978845608028654f;
-  return 0.5f * x * (1.0f + tanhf(c * (x + 0.044715f * x * x * x)));
+  // model.py:145-146: 0.5*x*(1 + tanh(sqrt(2/pi)*(x + 0.044715*x^3))), evaluated as the
+  // identity 0.5*(1 + tanh(u)) = 1/(1 + e^(-2u)): one ex2 + one reciprocal on the SFU
+  // instead of tanhf's polynomial/branch sequence (abs. error of 0.5*(1+tanh) ~1e-7,
+  // far below the 16-bit rounding of the stored activation)
+  const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+  return __fdividef(x, 1.0f + __expf(-2.0f * u));
 }
 
 template <bool BF16>

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "zo_common.cuh"
 #include "zo_kernels.h"
@@ -352,7 +353,7 @@ void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int 
                    cudaStream_t st) {
   if (d % 4 || ldo % 4) throw Error(ZO_ERR_DIMENSION, "LN rows must be multiples of 4");
   bool done = false;
-  // CTA-per-row kernel first (d multiple of 128 and <= 8192)
+  // CTA-per-row kernel (d multiple of 128 and <= 8192)
   if (d % 1024 == 0) {
     switch (d / 1024) {
       case 1: done = ln_row_dispatch<1>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
