@@ -189,6 +189,9 @@ def main():
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--seq", type=int, default=64)
     ap.add_argument("--rank", type=int, default=2)
+    ap.add_argument("--estimator", default="lozo_lazy", choices=["lozo_lazy", "factorized_sqrt_r"],
+                    help="factorized_sqrt_r = BASELINE config 5 (MeZO-style high-rank, e.g. --rank 128): "
+                         "probe U V^T/sqrt(r), dense float64 update of every weight each step")
     ap.add_argument("--nu", type=int, default=50)
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -215,7 +218,7 @@ def main():
     from paper_2605_28760_b200 import model as M
     from paper_2605_28760_b200.adapter import AdapterState
     from paper_2605_28760_b200.engine import ZoEngine
-    from paper_2605_28760_b200.zo_engine import ZoConfig, lozo_step
+    from paper_2605_28760_b200.zo_engine import ZoConfig, factorized_step, lozo_step
 
     B, T = args.batch, args.seq
     qdir = world > 1 and args.mode == "qdir"
@@ -232,11 +235,15 @@ def main():
                          prompt_len=prompt_len, init_seed=7, init_scale=0.02)
     tcfg = M.TaskConfig(seed=11, vocab=mdl["vocab"], prompt_len=prompt_len, train_size=1000, dev_size=4,
                         val_size=4)
-    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=1e-7, rank=args.rank, nu=args.nu, batch_size=B)
+    fact = args.estimator == "factorized_sqrt_r"
+    if fact:
+        args.nu = 1
+    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=1e-7, rank=args.rank, nu=args.nu, batch_size=B,
+                    estimator=args.estimator)
     task = M.generate_task(tcfg)
     t_init = time.perf_counter()
     eng = ZoEngine(mcfg.vocab, mcfg.dim, mcfg.n_layers, mcfg.n_heads, prompt_len, opt_len=1, max_batch=Bl,
-                   rank=args.rank, precision=args.precision, device=local)
+                   rank=args.rank, estimator=args.estimator, precision=args.precision, device=local)
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     eng.init_params(mcfg.init_seed, mcfg.init_scale)
@@ -271,7 +278,7 @@ def main():
             eng.out4_io(out4_local.data_ptr(), False)
             dist.all_gather_into_tensor(out4_all, out4_local)  # 32 B per rank
             eng.qdir_apply_async(zcfg.seed, t, G, zcfg.learning_rate, out4_all.data_ptr())
-            if ((t + 1) * G) % zcfg.nu == 0:
+            if not fact and ((t + 1) * G) % zcfg.nu == 0:
                 eng.fold_async()
             return
         if world == 1:
@@ -288,7 +295,7 @@ def main():
             full = nll_all.view(world, 2, Bl).transpose(0, 1).contiguous()
             eng.nll_io(full.data_ptr(), 2 * B, True)
             eng.step_apply_async(zcfg.epsilon, zcfg.learning_rate, False, B)
-        if (t + 1) % zcfg.nu == 0:
+        if not fact and (t + 1) % zcfg.nu == 0:
             eng.fold_async()
 
     def barrier():
@@ -330,8 +337,10 @@ def main():
             "scaling": "strong" if (world > 1 and not qdir) else "weak", "vs_baseline": None,
             "dtype": args.precision,
             "data": "synthetic (marker task, random-init Role.INIT weights)",
-            "config": {"workload": f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, "
-                                   f"nu={args.nu}, fold amortised", "model": args.model, "global_batch": B,
+            "config": {"workload": (f"{args.model} factorized_sqrt_r (MeZO-style) r={args.rank} LoRA-only SST-2 "
+                                    f"shape, B={B} x T={T}, dense float64 update every step" if fact else
+                                    f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, "
+                                    f"nu={args.nu}, fold amortised"), "model": args.model, "global_batch": B,
                        "seq_len": T, "parallelism": (f"qdir{world}" if qdir else f"exact-dp{world}") if world > 1 else "single",
                        "l2": "inputs larger than L2 (25.7 GB 16-bit weights/step at 13B); no flush"},
             "scored_tokens_per_s": value * 2 * B * T, "option_tokens_per_s": value * 2 * B,
@@ -363,20 +372,21 @@ def main():
         params = M.DeviceParams(mcfg, precision=args.precision, max_batch=B)
         params._engine = eng  # reuse the initialised replica
         state = AdapterState(epsilon=zcfg.epsilon)
+        step_fn = factorized_step if fact else lozo_step
         for t in range(nsteps, nsteps + args.warmup):
-            lozo_step(params, mcfg, state, zcfg, t, M.sample_minibatch(task, "train", zcfg.seed, t, B),
-                      digests="off")
+            step_fn(params, mcfg, state, zcfg, t, M.sample_minibatch(task, "train", zcfg.seed, t, B),
+                    digests="off")
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for t in range(nsteps + args.warmup, nsteps + args.warmup + args.steps):
             mb = M.sample_minibatch(task, "train", zcfg.seed, t, B)
-            lozo_step(params, mcfg, state, zcfg, t, mb, digests="off")
-            if (t + 1) % zcfg.nu == 0:
+            step_fn(params, mcfg, state, zcfg, t, mb, digests="off")
+            if not fact and (t + 1) % zcfg.nu == 0:
                 eng.fold()
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / args.steps
         line["e2e"] = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * T * 4 + B * 4 + 8,
-                       "d2h_bytes_per_step": 32, "api": "model.sample_minibatch + zo_engine.lozo_step (host batch)",
+                       "d2h_bytes_per_step": 32, "api": f"model.sample_minibatch + zo_engine.{step_fn.__name__} (host batch)",
                        "phase_ms_last_step": dict(zip(["sample", "score", "update"], eng.last_step_ms()))}
 
     if rank == 0 and not args.no_cpu_baseline and not args.profile:

@@ -682,7 +682,7 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
     const char* e = std::getenv("ZO_CG2");
     return !e || std::atoi(e) != 0;
   }();
-  g.cg = (cg2_on && bn >= 128 && M >= 512) ? 2 : 1;
+  g.cg = (cg2_on && N > 128 && bn >= 128 && M >= 512) ? 2 : 1;
   if (g.cg == 2) {
     // N=128 pair tiles measured 1.4-1.5x slower (A re-reads, fixed costs).  Between 256
     // and 192 pick the smaller ragged-wave cost: rounds * BN (the per-round tile time),

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, c
   const float* P = (row < rows_per_sign) ? Pp : Pm;
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4* b4 = reinterpret_cast<const float4*>(bta);
-  float t[XR];
+  float t[XR > 0 ? XR : 1];
 #pragma unroll
   for (int k = 0; k < XR; ++k) t[k] = 0.f;
 #pragma unroll
@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, c
     const float h[4] = {(v[j].x - mu) * rsd * gg.x + bb.x, (v[j].y - mu) * rsd * gg.y + bb.y,
                         (v[j].z - mu) * rsd * gg.z + bb.z, (v[j].w - mu) * rsd * gg.w + bb.w};
     store4_16(out, (size_t)row * ldo + 4 * i, h[0], h[1], h[2], h[3], bf16);
+    if constexpr (XR == 0) continue;
     const float4* pr = reinterpret_cast<const float4*>(P + (size_t)(4 * i) * XR);
     if constexpr (XR == 2) {
       const float4 p01 = pr[0], p23 = pr[1];  // P[4i..4i+3][0..1]
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, c
         for (int k = 0; k < XR; ++k) t[k] += h[e] * P[(size_t)(4 * i + e) * XR + k];
     }
   }
+  if constexpr (XR == 0) return;
 #pragma unroll
   for (int k = 0; k < XR; ++k) t[k] = warp_sum(t[k]);
   __syncthreads();
@@ -328,6 +330,7 @@ static bool ln_row_dispatch(const float* x32, const float* gamma, const float* b
   const int threads = d / (4 * NPT);
   if (threads * 4 * NPT != d || threads % 32 || threads > 256) return false;
   switch (r) {
+    case 0: k_ln_row<NPT, 0><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
     case 1: k_ln_row<NPT, 1><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
     case 2: k_ln_row<NPT, 2><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
     case 4: k_ln_row<NPT, 4><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
@@ -547,10 +550,38 @@ __global__ void __launch_bounds__(1024) k_loss(const float* __restrict__ logits,
   if (threadIdx.x == 0) nll[ex] = (double)total;
 }
 
+// High-rank embedding delta (factorized r > 8): logits[row, v] += z[row] . P_s[v] with
+// one thread per vocabulary entry holding its P row in registers for every scored row
+// of its sign -- each P row is read once instead of once per scored row.
+__global__ void __launch_bounds__(256) k_embed_delta(float* __restrict__ logits, int ldl, int V,
+                                                     const float* __restrict__ z, int r,
+                                                     const float* __restrict__ P, int row0, int nrows) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const float* pv = P + (size_t)v * r;
+  for (int i = 0; i < nrows; ++i) {
+    const float* zr = z + (size_t)(row0 + i) * r;
+    float a = 0.f;
+    for (int k = 0; k < r; k += 4) {
+      const float4 p4 = *reinterpret_cast<const float4*>(pv + k);
+      const float4 z4 = *reinterpret_cast<const float4*>(zr + k);
+      a += p4.x * z4.x + p4.y * z4.y + p4.z * z4.z + p4.w * z4.w;
+    }
+    logits[(size_t)(row0 + i) * ldl + v] += a;
+  }
+}
+
 void launch_loss(const float* logits, int ldl, int V, const float* z, int r, const float* Pplus_e,
                  const float* Pminus_e, const int32_t* gold, int B, int Lopt, double* nll, cudaStream_t st) {
-  if (r > 64) throw Error(ZO_ERR_DIMENSION, "loss kernel supports rank <= 64 on the embedding");
   if (ldl % 4) throw Error(ZO_ERR_DIMENSION, "logits leading dimension must be a multiple of 4");
+  if (r > 8) {
+    // fold the embedding's rank-r delta into the logits first, then a plain log-softmax
+    if (r % 4) throw Error(ZO_ERR_DIMENSION, "high-rank embedding delta needs rank % 4 == 0");
+    const int rows = B * Lopt, grid = (V + 255) / 256;
+    k_embed_delta<<<grid, 256, 0, st>>>(const_cast<float*>(logits), ldl, V, z, r, Pplus_e, 0, rows);
+    k_embed_delta<<<grid, 256, 0, st>>>(const_cast<float*>(logits), ldl, V, z, r, Pminus_e, rows, rows);
+    r = 0;
+  }
   k_loss<<<2 * B, 1024, 0, st>>>(logits, ldl, V, z, r, Pplus_e, Pminus_e, gold, B, Lopt, nll);
 }
 
@@ -642,6 +673,29 @@ void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K
   k_vext<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(V, n, r, W16T, ldw, K, bf16, ext_terms, V32);
 }
 
+// ------------------------------------------------------------------ high-rank extension operand
+// P16T[k][i] = h16(P[i][k]) for one matrix's [m, r] probe block: the B operand
+// ([N = r, K = m], K-major) of the tensor-core extension GEMM t = a . P (r > 8).
+__global__ void k_p16t(const float* __restrict__ P, int m, int r, uint16_t* __restrict__ out, bool bf16) {
+  __shared__ float tile[32][33];
+  const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int i = i0 + yy, k = k0 + tx;
+    tile[yy][tx] = (i < m && k < r) ? P[(size_t)i * r + k] : 0.f;
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int k = k0 + yy, i = i0 + tx;
+    if (i < m && k < r) out[(size_t)k * m + i] = to16(tile[tx][yy], bf16);
+  }
+}
+
+void launch_p16t(const float* P, int m, int r, void* out, bool bf16, cudaStream_t st) {
+  dim3 grid((m + 31) / 32, (r + 31) / 32);
+  k_p16t<<<grid, dim3(32, 8), 0, st>>>(P, m, r, static_cast<uint16_t*>(out), bf16);
+}
+
 // ------------------------------------------------------------------ fold (K9) + 16-bit shadow refresh
 // 32x32 tile per block: W64 tile (+ sum_k alpha*(A_ik*V_jk), k ascending, each
 // term rounded as numpy does: numerics.py:211) -> W64, then the 16-bit shadow
@@ -707,18 +761,101 @@ __global__ void k_fold_dev(double* __restrict__ W, int m, int n, const double* _
   }
 }
 
+// High-rank variant (factorized r > 8, e.g. BASELINE config 5's r = 128 where this is
+// the dominant cost of a step: 3 float64 ops per weight per rank).  64x64 W tile per CTA,
+// each thread a 4x4 register micro-tile; the tile's A rows and V rows are staged
+// through shared memory 32 ranks at a time (V transposed).  Same per-element
+// arithmetic and order as k_fold_dev: w = w + alpha*(A_ik*V_jk), k ascending.
+__global__ void __launch_bounds__(256) k_fold_dev_tiled(double* __restrict__ W, int m, int n,
+                                                        const double* __restrict__ A, const double* __restrict__ Vv,
+                                                        int r, const double* __restrict__ out4, double lr,
+                                                        double scale, const unsigned* __restrict__ abort_flag,
+                                                        void* __restrict__ W16, int ldw, int transposed, bool bf16,
+                                                        double alpha_fixed) {
+  // out4 == nullptr: a host-side alpha (zo_update_dense / window fold); else alpha from the
+  // device coefficient, skipped when the step aborted
+  double alpha = alpha_fixed;
+  if (out4) {
+    if (abort_flag ? *abort_flag != 0u : !(isfinite(out4[0]) && isfinite(out4[1]))) return;
+    alpha = __dmul_rn(-__dmul_rn(lr, out4[2]), scale);
+  }
+  __shared__ double smem[64 * 33 + 32 * 65];
+  double* sA = smem;             // [64 rows i][33]: k within the chunk
+  double* sVt = smem + 64 * 33;  // [32 k][65]: column j
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16
+  double w[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      w[a][b] = (i < m && j < n) ? W[(size_t)i * n + j] : 0.0;
+    }
+  for (int k0 = 0; k0 < r; k0 += 32) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * 32; e += 256) {
+      const int rr = e >> 5, k = e & 31;
+      sA[rr * 33 + k] = (i0 + rr < m && k0 + k < r) ? A[(size_t)(i0 + rr) * r + k0 + k] : 0.0;
+      sVt[k * 65 + rr] = (j0 + rr < n && k0 + k < r) ? Vv[(size_t)(j0 + rr) * r + k0 + k] : 0.0;
+    }
+    __syncthreads();
+    const int kn = min(32, r - k0);
+    for (int k = 0; k < kn; ++k) {
+      double av[4], vv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sA[(ty + 16 * a) * 33 + k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) vv[b] = sVt[k * 65 + tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) w[a][b] = __dadd_rn(w[a][b], __dmul_rn(alpha, __dmul_rn(av[a], vv[b])));
+    }
+  }
+  __syncthreads();
+  float* tile = reinterpret_cast<float*>(smem);  // [64][65] fp32 image for the transposed shadow
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int yy = ty + 16 * a, xx = tx + 16 * b, i = i0 + yy, j = j0 + xx;
+      float f = 0.f;
+      if (i < m && j < n) {
+        W[(size_t)i * n + j] = w[a][b];
+        f = (float)w[a][b];
+        if (!transposed) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
+      }
+      tile[yy * 65 + xx] = f;
+    }
+  if (!transposed) return;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+    const int jj = e >> 6, ii = e & 63, j = j0 + jj, i = i0 + ii;
+    if (i < m && j < n) reinterpret_cast<uint16_t*>(W16)[(size_t)j * ldw + i] = to16(tile[ii * 65 + jj], bf16);
+  }
+}
+
 void launch_fold_dev(double* W64, int m, int n, const double* A, const double* V, int r, const double* out4,
                      double lr, double scale, const unsigned* abort_flag, void* W16, int ldw, int transposed,
                      bool bf16, cudaStream_t st) {
   dim3 grid((n + 31) / 32, (m + 31) / 32);
-  k_fold_dev<<<grid, dim3(32, 8), 0, st>>>(W64, m, n, A, V, r, out4, lr, scale, abort_flag, W16, ldw, transposed,
-                                           bf16);
+  if (r > 8)
+    k_fold_dev_tiled<<<dim3((n + 63) / 64, (m + 63) / 64), 256, 0, st>>>(W64, m, n, A, V, r, out4, lr, scale,
+                                                                          abort_flag, W16, ldw, transposed, bf16, 0.0);
+  else
+    k_fold_dev<<<grid, dim3(32, 8), 0, st>>>(W64, m, n, A, V, r, out4, lr, scale, abort_flag, W16, ldw,
+                                             transposed, bf16);
 }
 
 void launch_fold(double* W64, int m, int n, const double* A, const double* V, int r, double alpha, void* W16,
                  int ldw, int transposed, bool bf16, cudaStream_t st) {
   dim3 grid((n + 31) / 32, (m + 31) / 32);
-  k_fold_shadow<<<grid, dim3(32, 8), 0, st>>>(W64, m, n, A, V, r, alpha, W16, ldw, transposed, bf16);
+  if (r > 8)
+    k_fold_dev_tiled<<<dim3((n + 63) / 64, (m + 63) / 64), 256, 0, st>>>(W64, m, n, A, V, r, nullptr, 0.0, 0.0,
+                                                                          nullptr, W16, ldw, transposed, bf16, alpha);
+  else
+    k_fold_shadow<<<grid, dim3(32, 8), 0, st>>>(W64, m, n, A, V, r, alpha, W16, ldw, transposed, bf16);
 }
 
 void launch_shadow_T(const double* W64, int m, int n, void* W16T, int ldw, bool bf16, cudaStream_t st) {

@@ -52,6 +52,8 @@ void launch_update(double* A, const double* U, int64_t n, const double* out4, co
 // P+- = fp32(A +- eps*U)
 void launch_prep_probe(const double* A, const double* U, int64_t n, double eps, double probe_scale, float* Pp,
                        float* Pm, cudaStream_t st);
+// P16T[k][i] = h16(P[i][k]) for one [m, r] probe block (tensor-core extension B operand, r > 8)
+void launch_p16t(const float* P, int m, int r, void* out, bool bf16, cudaStream_t st);
 // V ext columns (hi, hi, lo) into W16T[:, K:K+3r] for one matrix; V32 copy
 void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K, bool bf16, int ext_terms,
                        float* V32, cudaStream_t st);

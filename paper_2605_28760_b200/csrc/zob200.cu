@@ -47,6 +47,9 @@ struct Matrix {
 
 struct LayerPlan {
   GemmDesc qkv, out, up, down;
+  // high-rank (r > 8) tensor-core extension t = a . P_s per GEMM input and probe sign:
+  // [qkv-in, out-in, up-in, down-in] x [sign]
+  std::vector<GemmDesc> ext;
 };
 struct RowPlan {
   std::vector<LayerPlan> layers;
@@ -115,6 +118,7 @@ struct zo_ctx {
   unsigned* flags = nullptr;
   std::map<int, RowPlan> plans;  // keyed by 2*M + (nsign == 1)
   float* tpart = nullptr;         // fused LoRA-extension partials [tiles][Mpad][r]
+  uint16_t* P16T = nullptr;       // high-rank extension B operands [2][su] (per matrix [r][m])
   float* sk_ws = nullptr;         // stream-K partial tiles
   unsigned* sk_flags = nullptr;
   bool streamk = true;  // DP waves + stream-K tail where it pays (ZO_STREAMK=0 disables)
@@ -233,6 +237,19 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
               c->num_sms);
     if (c->streamk)
       for (GemmDesc* g : {&lp.qkv, &lp.out, &lp.up, &lp.down}) gemm_enable_streamk(*g, c->sk_ws, c->sk_flags, c->num_sms);
+    if (!c->fused_ext) {
+      const int rps = M / nsign;
+      const Matrix* mm[4] = {&q, &o, &u, &w};
+      void* acts[4] = {c->hA, c->ctxA, c->hA, c->gA};
+      const int lds[4] = {ldh, ldh, ldh, ldg};
+      lp.ext.resize(8);
+      for (int i = 0; i < 4; ++i)
+        for (int sg = 0; sg < nsign; ++sg) {
+          uint16_t* a = static_cast<uint16_t*>(acts[i]) + (size_t)sg * rps * lds[i];
+          gemm_plan(lp.ext[2 * i + sg], a, rps, lds[i], c->P16T + (size_t)sg * c->su + mm[i]->u_off, c->r,
+                    (int)mm[i]->m, (int)mm[i]->m, EPI_STORE16, c->bf16, a + mm[i]->m, lds[i], c->num_sms);
+        }
+    }
     rp.layers.push_back(lp);
   }
   const Matrix& e = c->mats[c->i_embed];
@@ -262,14 +279,24 @@ void do_score(zo_ctx* c, int B, int nsign) {
   const int ldh = d + c->KE, ldg = 4 * d + c->KE;
   launch_embed(c->x32, c->tok, B, T, d, e.W64, e.W16, c->bf16, c->Pp + e.u_off, c->Pm + e.u_off, c->V32 + e.v_off,
                c->r, c->pe, M, c->st);
+  if (!c->fused_ext)  // high rank: 16-bit transposed probe operands of the extension GEMMs
+    for (const auto& m : c->mats) {
+      if (m.kind == K_EMBED) continue;
+      launch_p16t(c->Pp + m.u_off, (int)m.m, c->r, c->P16T + m.u_off, c->bf16, c->st);
+      if (nsign == 2) launch_p16t(c->Pm + m.u_off, (int)m.m, c->r, c->P16T + c->su + m.u_off, c->bf16, c->st);
+    }
+  auto ext_gemm = [&](const LayerPlan& lp, int i) {
+    for (int sg = 0; sg < nsign; ++sg) gemm_launch(lp.ext[2 * i + sg], c->st);
+  };
   for (int l = 0; l < c->d.n_layers; ++l) {
     const Matrix& q = c->mats[c->i_qkv[l]];
     const Matrix& o = c->mats[c->i_out[l]];
     const Matrix& u = c->mats[c->i_up[l]];
     const Matrix& w = c->mats[c->i_down[l]];
     const LayerPlan& lp = rp.layers[l];
-    launch_ln_ext(c->x32, c->ln1g[l], c->ln1b[l], M, d, c->hA, ldh, c->bf16, c->Pp + q.u_off, c->Pm + q.u_off, c->r,
-                  rps, c->ext_terms, c->st);
+    launch_ln_ext(c->x32, c->ln1g[l], c->ln1b[l], M, d, c->hA, ldh, c->bf16, c->Pp + q.u_off, c->Pm + q.u_off,
+                  c->fused_ext ? c->r : 0, rps, c->ext_terms, c->st);
+    if (!c->fused_ext) ext_gemm(lp, 0);
     gemm_launch(lp.qkv, c->st);
     AttnExt ax;
     if (c->fused_ext) {
@@ -284,16 +311,17 @@ void do_score(zo_ctx* c, int B, int nsign) {
     if (c->fused_ext)
       launch_ext_finalize(c->tpart, c->d.n_heads, c->Mpad, M, c->r, c->ctxA, ldh, d, c->ext_terms, c->bf16, c->st);
     else
-      launch_ext(c->ctxA, ldh, M, d, c->bf16, c->Pp + o.u_off, c->Pm + o.u_off, c->r, rps, c->ext_terms, c->st);
+      ext_gemm(lp, 1);
     gemm_launch(lp.out, c->st);
-    launch_ln_ext(c->x32, c->ln2g[l], c->ln2b[l], M, d, c->hA, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off, c->r,
-                  rps, c->ext_terms, c->st);
+    launch_ln_ext(c->x32, c->ln2g[l], c->ln2b[l], M, d, c->hA, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off,
+                  c->fused_ext ? c->r : 0, rps, c->ext_terms, c->st);
+    if (!c->fused_ext) ext_gemm(lp, 2);
     gemm_launch(lp.up, c->st);
     if (c->fused_ext)
       launch_ext_finalize(c->tpart, (4 * d + lp.up.bn - 1) / lp.up.bn, c->Mpad, M, c->r, c->gA, ldg, 4 * d,
                           c->ext_terms, c->bf16, c->st);
     else
-      launch_ext(c->gA, ldg, M, 4 * d, c->bf16, c->Pp + w.u_off, c->Pm + w.u_off, c->r, rps, c->ext_terms, c->st);
+      ext_gemm(lp, 3);
     gemm_launch(lp.down, c->st);
   }
   launch_final_ln(c->x32, c->lnfg, c->lnfb, B * nsign, T, d, c->d.prompt_len, c->d.opt_len, c->xs32, c->xs16,
@@ -367,7 +395,9 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->dh = d.dim / d.n_heads;
   c->r = d.rank;
   c->bf16 = d.precision == ZO_PREC_BF16;
-  c->ext_terms = (3 * d.rank <= 64) ? 3 : 1;
+  // rank <= 8: fused fp32 extension dots carried as (hi, lo, hi) 16-bit columns; above:
+  // one 16-bit column per rank from the tensor-core extension GEMM
+  c->ext_terms = d.rank <= 8 ? 3 : 1;
   c->ext_used = c->ext_terms * d.rank;
   c->KE = (int)ceil_div(c->ext_used, 64) * 64;
   for (auto& e : c->ev) ZO_CUDA_TRY(cudaEventCreate(&e));
@@ -476,6 +506,7 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->fused_ext = d.rank <= 8;
   c->tpart_tiles = std::max((int)ceil_div(4 * D, 64), d.n_heads);
   if (c->fused_ext) c->tpart = c->mem.get<float>((size_t)c->tpart_tiles * c->Mpad * d.rank);
+  else c->P16T = c->mem.get<uint16_t>((size_t)2 * c->su);
   // positional table: pos_encoding(T, d) (model.py:128-136), float64 -> float32
   {
     std::vector<float> pe((size_t)c->T * d.dim);

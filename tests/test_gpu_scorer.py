@@ -206,3 +206,38 @@ def test_graph_step_bitwise_equals_eager():
         eng.close()
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("rank", [16, 128])
+def test_factorized_high_rank_step_vs_oracle(rank):
+    """MeZO-style factorized step at high rank (BASELINE config 5 shape family): the
+    r > 8 paths (separate extension pass, 1-term 16-bit extension columns, embedding
+    delta folded into the logits) against the float64 oracle's factorized_step, and the
+    dense float64 update bit-exact given the device coefficient."""
+    import math
+    from paper_2605_28760_b200.engine import ZoEngine
+    cfg = R.ModelCfg(vocab=512, dim=128, n_layers=2, n_heads=2, prompt_len=63, init_seed=7, init_scale=0.02)
+    z = R.ZoCfg(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=rank, nu=1, batch_size=16,
+                estimator="factorized_sqrt_r")
+    splits = R.generate_task(R.TaskCfg(seed=11, vocab=512, prompt_len=63, train_size=64, dev_size=4, val_size=4))
+    eng = ZoEngine(cfg.vocab, cfg.dim, cfg.n_layers, cfg.n_heads, cfg.prompt_len, max_batch=16, rank=rank,
+                   estimator="factorized_sqrt_r")
+    eng.init_params(cfg.init_seed, cfg.init_scale)
+    params = R.init_params(cfg)
+    for t in range(2):
+        p, gl, idx = R.sample_minibatch(splits, "train", z.seed, t, z.batch_size)
+        gold = np.array([[cfg.vocab - 2], [cfg.vocab - 1]])[gl]
+        tokens = np.concatenate([p, gold], axis=1)
+        w_before = eng.download("blk1.ff_down")
+        out = eng.step(z.seed, t, 1, z.epsilon, z.learning_rate, False, tokens, gold)
+        ref_params = {k: v.copy() for k, v in params.items()}
+        rec = R.factorized_step(ref_params, cfg, z, t, tokens, gold, idx)
+        assert abs(out[0] - rec.loss_plus) <= LOSS_TOL["fp16"] and abs(out[1] - rec.loss_minus) <= LOSS_TOL["fp16"]
+        # dense update with the device's c: W += (-(lr c)/sqrt(r)) U V^T, k ascending
+        m, n = w_before.shape
+        u = R.gaussian(z.seed, t, "blk1.ff_down", R.ROLE_U, m, rank)
+        v = R.gaussian(z.seed, t, "blk1.ff_down", R.ROLE_V, n, rank)
+        R.axpy_outer_raw(w_before, -(z.learning_rate * float(out[2])) * (1.0 / math.sqrt(rank)), u, v)
+        np.testing.assert_array_equal(eng.download("blk1.ff_down"), w_before)
+        params = {lid: eng.download(lid) for lid in eng.lids} | {k: v for k, v in params.items() if v.ndim == 1}
+    eng.close()
