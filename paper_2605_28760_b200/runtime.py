@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import time
+
+import numpy as np
 from dataclasses import dataclass, field
 
 from .adapter import AdapterState
@@ -20,7 +22,7 @@ from .model import (EvalPoint, ModelConfig, TaskData, as_device_params, evaluate
 from .numerics import digest_hex
 from .zo_engine import ZoConfig, ZoStepRecord, factorized_step, lozo_step
 
-__all__ = ["CostMeter", "ServingRun", "ScoringAbort", "run_serving_path"]
+__all__ = ["CostMeter", "ServingRun", "ScoringAbort", "run_serving_path", "save_checkpoint", "load_checkpoint"]
 
 
 @dataclass
@@ -62,8 +64,15 @@ class ServingRun:
 
 def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: int, precision: str = "real64",
                      eval_every: int = 50, fold_on_eval: bool = False, abort_at: int | None = None,
-                     params=None, digests: bool = True, compute_param_digests: bool = True) -> ServingRun:
-    """ZO fine-tuning the serving way (runtime.py:253-359), device-resident."""
+                     params=None, digests: bool = True, compute_param_digests: bool = True,
+                     state: AdapterState | None = None, start_step: int = 0, final_fold: bool = True) -> ServingRun:
+    """ZO fine-tuning the serving way (runtime.py:253-359), device-resident.
+
+    Extensions over the reference signature (all defaulted to its behaviour):
+    ``state`` / ``start_step`` resume a run from ``load_checkpoint`` (steps
+    start_step .. start_step+steps-1, the counter-keyed streams make the
+    continuation bit-identical to an uninterrupted run), ``final_fold=False``
+    leaves the window unfolded so the run can be checkpointed mid-window."""
     if steps < 1:
         raise ConfigError("steps must be >= 1")
     if zcfg.estimator == "dense_mezo":
@@ -75,8 +84,9 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
     opt_len = len(task.config.options[0])
     eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, opt_len)
     model_digest = params_digest(dp) if compute_param_digests else ""
-    state = AdapterState(epsilon=zcfg.epsilon)
+    state = AdapterState(epsilon=zcfg.epsilon) if state is None else state
     state._bind(eng)
+    state._sync_to_engine(eng)
     meter = CostMeter()
     step_fn = lozo_step if zcfg.estimator == "lozo_lazy" else factorized_step
     pool = cf.ThreadPoolExecutor(max_workers=4) if digests else None
@@ -94,9 +104,9 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
         loss, acc = evaluate_split(dp, mcfg, task, "dev", state.view(), precision)
         evals.append(EvalPoint(at, wall * 1e3, loss, acc))
 
-    do_eval(0)
-    done = 0
-    for t in range(steps):
+    do_eval(start_step)
+    done = start_step
+    for t in range(start_step, start_step + steps):
         batch = sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
         t0 = time.perf_counter()
         try:
@@ -129,9 +139,9 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
             dt = time.perf_counter() - f0
             meter.time_fold_s += dt
             wall += dt
-        if (t + 1) % eval_every == 0 and (t + 1) != steps:
+        if (t + 1) % eval_every == 0 and (t + 1) != start_step + steps:
             do_eval(t + 1)
-    if not aborted and zcfg.estimator == "lozo_lazy":
+    if not aborted and final_fold and zcfg.estimator == "lozo_lazy":
         f0 = time.perf_counter()
         eng.fold()
         dp.invalidate()
@@ -149,3 +159,64 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
                       final_params_digest=params_digest(dp) if compute_param_digests else "", params=dp,
                       state=state, train_wall_s=wall, precision=precision, steps_completed=done,
                       model_digest=model_digest, task_digest=task.digest(), aborted=aborted)
+
+
+# ---------------------------------------------------------------- checkpoint / resume
+def save_checkpoint(path: str, params, state: AdapterState, next_step: int, mcfg: ModelConfig,
+                    zcfg: ZoConfig) -> dict:
+    """Checkpoint a (possibly mid-window) device run into directory ``path``:
+
+    * ``adapter.zoad`` (+ manifest) -- the window slots (A, V_win) in the
+      reference's ZOAD format (adapter.py:305-328);
+    * ``params/<layer id>.npy`` -- the float64 master weights with every fold
+      applied so far, and the LN vectors;
+    * ``meta.json`` -- next step, configs, digests.
+
+    Resuming needs nothing else: U, V and minibatches are counter-keyed by
+    (seed, step), so ``run_serving_path(..., state=, start_step=next_step)``
+    continues bit-identically."""
+    import json
+    import os
+    from dataclasses import asdict
+
+    from .adapter_io import save_adapter
+    os.makedirs(os.path.join(path, "params"), exist_ok=True)
+    dp = as_device_params(params, mcfg)
+    for k in dp:
+        np.save(os.path.join(path, "params", k + ".npy"), np.asarray(dp[k], dtype=np.float64))
+    man = save_adapter(state, os.path.join(path, "adapter.zoad"))
+    meta = {"format": "zob200-checkpoint-1", "next_step": int(next_step), "model": asdict(mcfg),
+            "zo": asdict(zcfg), "params_digest": params_digest(dp), "adapter_state_digest": man["state_digest"]}
+    with open(os.path.join(path, "meta.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+    return meta
+
+
+def load_checkpoint(path: str, precision: str = "fp16", max_batch: int = 16, device: int = 0):
+    """Inverse of ``save_checkpoint``: returns (params, state, next_step, meta) with
+    the params re-uploaded to a fresh device engine on first use and the digests
+    verified."""
+    import json
+    import os
+
+    from .adapter_io import load_adapter
+    from .errors import InputError
+    with open(os.path.join(path, "meta.json")) as f:
+        meta = json.load(f)
+    if meta.get("format") != "zob200-checkpoint-1":
+        raise InputError("not a zob200 checkpoint")
+    mcfg = ModelConfig(**meta["model"])
+    host = {}
+    for fn in sorted(os.listdir(os.path.join(path, "params"))):
+        if fn.endswith(".npy"):
+            host[fn[:-4]] = np.load(os.path.join(path, "params", fn))
+    if params_digest(host) != meta["params_digest"]:
+        raise InputError("checkpoint params digest mismatch")
+    from .model import DeviceParams
+    params = DeviceParams(mcfg, host=host, precision=precision if precision in ("fp16", "bf16") else "fp16",
+                          max_batch=max_batch, device=device)
+    state = load_adapter(os.path.join(path, "adapter.zoad"))
+    for e in state._host_entries.values():
+        e.perturb_slot = None  # probes are per-step and never carried across steps
+    state._probe_on = False
+    return params, state, int(meta["next_step"]), meta

@@ -16,6 +16,9 @@ Fixtures
   traj_*.jsonl      run_serving_path trajectories (runtime.py:253-359) with
                     header digests, per-step L+/L-/c/beta/u,v digests and the
                     final params digest, written by zoserve.write_trajectory
+  adapter_rich.zoad ZOAD adapter file (+ .manifest.json) written by the
+                    reference's save_adapter for a state with frozen, window
+                    and probe slots (adapter.py:279-415)
 """
 from __future__ import annotations
 
@@ -162,10 +165,35 @@ OPT125 = dict(vocab=50272, dim=768, n_layers=12, n_heads=12, prompt_len=63, init
 OPT125_TASK = dict(seed=11, vocab=50272, prompt_len=63, train_size=1000, dev_size=2, val_size=2)
 
 
+def adapter_fixture():
+    _ref()
+    from zoserve.adapter import AdapterState, LoraSlot, save_adapter
+
+    def slot(m, n, k, scale, seed):
+        g = np.random.default_rng(seed)
+        return LoraSlot(g.standard_normal((m, k)), g.standard_normal((n, k)), scale)
+
+    st = AdapterState(epsilon=2e-3, perturb_sign=0)
+    st.ensure_entry("blk0.qkv", 8, 24)
+    st.add_frozen_slot("blk0.qkv", slot(8, 24, 2, 0.5, 20))
+    st.entries["blk0.qkv"].window_slot = slot(8, 24, 2, 1.0, 21)
+    st.ensure_entry("blk1.ff_down", 32, 8)
+    st.entries["blk1.ff_down"].window_slot = slot(32, 8, 2, 1.0, 23)
+    st.entries["blk1.ff_down"].perturb_slot = slot(32, 8, 2, 1.0, 24)
+    st.ensure_entry("embed", 16, 8)
+    st.entries["embed"].perturb_slot = slot(16, 8, 1, 1.0, 22)
+    save_adapter(st, os.path.join(OUT, "adapter_rich.zoad"))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--opt125m", action="store_true")
+    ap.add_argument("--only", default=None, help="regenerate one fixture family (e.g. 'adapter')")
     a = ap.parse_args()
+    if a.only == "adapter":
+        adapter_fixture()
+        return
+    adapter_fixture()
     streams()
     fnv()
     forward_fixture("micro", MICRO, MICRO_TASK, B=8)

@@ -143,3 +143,24 @@ def test_evaluate_split_vs_oracle():
     ref_acc = float(np.mean(np.argmax(-np.stack(per, axis=1), axis=1) == golds))
     assert abs(loss - ref_loss) < 1e-2
     assert abs(acc - ref_acc) <= 1.0 / len(golds) + 1e-12
+
+
+def test_checkpoint_resume_bit_identical(golden_dir, tmp_path):
+    """Checkpoint mid-window (ZOAD adapter + float64 masters), resume on a fresh
+    engine: the continued trajectory and final parameters equal an uninterrupted
+    run bit for bit (counter-keyed streams)."""
+    from paper_2605_28760_b200.adapter_io import load_adapter
+    from paper_2605_28760_b200.runtime import load_checkpoint, run_serving_path, save_checkpoint
+    h, _, _ = _traj(golden_dir, "traj_micro_lozo.jsonl")
+    M, mcfg, task, zcfg = _setup(h)  # nu = 5
+    full = run_serving_path(mcfg, task, zcfg, 9, eval_every=10 ** 9)
+    part = run_serving_path(mcfg, task, zcfg, 7, eval_every=10 ** 9, final_fold=False)  # stops mid-window
+    meta = save_checkpoint(str(tmp_path / "ck"), part.params, part.state, 7, mcfg, zcfg)
+    assert load_adapter(str(tmp_path / "ck" / "adapter.zoad")).entries["blk0.qkv"].window_slot.rank == zcfg.rank
+    params, state, nxt, meta2 = load_checkpoint(str(tmp_path / "ck"))
+    assert nxt == 7 and meta2 == meta
+    rest = run_serving_path(mcfg, task, zcfg, 2, eval_every=10 ** 9, params=params, state=state, start_step=7)
+    for a, b in zip(full.trajectory[7:], rest.trajectory):
+        assert (a.step, a.loss_plus, a.loss_minus, a.beta, a.u_digest, a.v_digest) == \
+               (b.step, b.loss_plus, b.loss_minus, b.beta, b.u_digest, b.v_digest)
+    assert rest.final_params_digest == full.final_params_digest
