@@ -43,6 +43,12 @@ extern "C" {
 #define ZO_EST_LOZO 0       /* "lozo_lazy"          zo_engine.py:368 */
 #define ZO_EST_FACTORIZED 1 /* "factorized_sqrt_r"  zo_engine.py:420 */
 
+/* ZoConfig.scope (zo_engine.py:79, 256-260): "lora_only" perturbs the 2-D params
+ * through rank-r slots; "full" also probes every 1-D param (LN scale / shift)
+ * densely with Role.DENSE_Z directions (VectorProbe, zo_engine.py:269-295). */
+#define ZO_SCOPE_LORA_ONLY 0
+#define ZO_SCOPE_FULL 1
+
 typedef struct zo_ctx zo_ctx;
 
 /* ModelConfig (model.py:62-81) + ZoConfig shape fields (zo_engine.py:71-98). */
@@ -54,6 +60,7 @@ typedef struct {
   int32_t estimator; /* ZO_EST_* */
   int32_t precision; /* ZO_PREC_* */
   int32_t device;
+  int32_t scope;     /* ZO_SCOPE_* */
 } zo_model_desc;
 
 const char* zo_last_error(void);
@@ -76,6 +83,8 @@ int zo_upload_matrix(zo_ctx* ctx, const char* layer_id, const double* host, int6
 int zo_download_matrix(zo_ctx* ctx, const char* layer_id, double* host, int64_t rows, int64_t cols);
 /* 1-D params: blk{i}.ln{1,2}.{scale,shift}, ln_f.{scale,shift} (model.py:100-107) */
 int zo_upload_vector(zo_ctx* ctx, const char* layer_id, const double* host, int64_t n);
+/* the float64 master of a 1-D param (full scope updates it every step) */
+int zo_download_vector(zo_ctx* ctx, const char* layer_id, double* host, int64_t n);
 
 /* directions.  step_directions / lozo_direction / factorized_direction
  * (zo_engine.py:163-261): U keyed by step, V by window start (lozo) or step
@@ -86,7 +95,9 @@ int zo_sample_v(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu);
  * for an arbitrary stream; lid_hash = fnv1a64(utf8(layer_id)). */
 int zo_sample_stream(zo_ctx* ctx, uint64_t seed, uint64_t step, uint64_t lid_hash, int32_t role, int64_t n,
                      double* host_out);
-/* slot arenas in sorted-id order: which = 0 U (m x r), 1 V (n x r), 2 window A (m x r) */
+/* slot arenas in sorted-id order: which = 0 U (m x r), 1 V (n x r), 2 window A (m x r),
+ * 3 (full scope) the 1-D params' dense directions z (n_vec x dim, sorted vector ids,
+ * chained into u_digest after the matrices, zo_engine.py:256-260) */
 int zo_slot_count(const zo_ctx* ctx, int32_t which, int64_t* count);
 int zo_get_slot(zo_ctx* ctx, int32_t which, double* host, int64_t count);
 int zo_set_slot(zo_ctx* ctx, int32_t which, const double* host, int64_t count);
@@ -114,6 +125,9 @@ int zo_update_u(zo_ctx* ctx);
 int zo_fold(zo_ctx* ctx);
 /* factorized_step's dense update (zo_engine.py:449-450): W += (-(lr*c)/sqrt(r)) U V^T */
 int zo_update_dense(zo_ctx* ctx, double lr);
+/* full scope: every 1-D param p += (-(lr*c)) z with the installed c (VectorProbe.update,
+ * zo_engine.py:290-295, 412-416); no-op for lora_only.  zo_update_dense applies it too. */
+int zo_update_vectors(zo_ctx* ctx, double lr);
 
 /* one whole lozo_step / factorized_step on the device (zo_engine.py:368-453),
  * replayed as a CUDA graph: V at window starts, U, probes, paired scoring,

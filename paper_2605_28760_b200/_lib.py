@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(_HERE, "_build", "libzob200.so")
 ZO_OK, ZO_ERR_CONFIG, ZO_ERR_DIMENSION, ZO_ERR_INPUT, ZO_ERR_ABORT, ZO_ERR_CUDA, ZO_ERR_INTERNAL = range(7)
 PREC_FP16, PREC_BF16 = 0, 1
 EST_LOZO, EST_FACTORIZED = 0, 1
+SCOPE_LORA_ONLY, SCOPE_FULL = 0, 1
 
 _lib = None
 _lock = threading.Lock()
@@ -25,7 +26,7 @@ _lock = threading.Lock()
 class ZoModelDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "vocab", "dim", "n_layers", "n_heads", "prompt_len", "opt_len", "max_batch", "rank",
-        "estimator", "precision", "device")]
+        "estimator", "precision", "device", "scope")]
 
 
 # (name, restype, argtypes) for every symbol include/zob200.h declares
@@ -46,6 +47,7 @@ SIGNATURES = [
     ("zo_upload_matrix", _c.c_int, [_P, _c.c_char_p, _P, _c.c_int64, _c.c_int64]),
     ("zo_download_matrix", _c.c_int, [_P, _c.c_char_p, _P, _c.c_int64, _c.c_int64]),
     ("zo_upload_vector", _c.c_int, [_P, _c.c_char_p, _P, _c.c_int64]),
+    ("zo_download_vector", _c.c_int, [_P, _c.c_char_p, _P, _c.c_int64]),
     ("zo_sample_u", _c.c_int, [_P, _c.c_uint64, _c.c_uint64]),
     ("zo_sample_v", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32]),
     ("zo_sample_stream", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_int64, _P]),
@@ -60,6 +62,7 @@ SIGNATURES = [
     ("zo_update_u", _c.c_int, [_P]),
     ("zo_fold", _c.c_int, [_P]),
     ("zo_update_dense", _c.c_int, [_P, _c.c_double]),
+    ("zo_update_vectors", _c.c_int, [_P, _c.c_double]),
     ("zo_step", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double, _c.c_int32,
                            _P, _P, _c.c_int32, _P]),
     ("zo_step_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double,

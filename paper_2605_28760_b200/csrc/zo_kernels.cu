@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) k_ln_ext(const float* __restrict__ x32, c
                                                 const float* __restrict__ bta, int M, int d, void* __restrict__ out,
                                                 int ldo, bool bf16, const float* __restrict__ Pp,
                                                 const float* __restrict__ Pm, int r, int rows_per_sign,
-                                                int ext_terms) {
+                                                int ext_terms, long vstride) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -169,8 +169,10 @@ __global__ void __launch_bounds__(256) k_ln_ext(const float* __restrict__ x32, c
   }
   const float rsd = 1.0f / sqrtf(warp_sum(s) / (float)d + 1e-5f);
   const float* P = (row < rows_per_sign) ? Pp : Pm;
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  const float4* b4 = reinterpret_cast<const float4*>(bta);
+  // full scope: the -eps probe rows read the second (VectorProbe -1) copy of the LN params
+  const long voff = (row < rows_per_sign) ? 0 : vstride;
+  const float4* g4 = reinterpret_cast<const float4*>(g + voff);
+  const float4* b4 = reinterpret_cast<const float4*>(bta + voff);
   for (int k0 = 0; k0 < (r > 0 ? r : 1); k0 += 8) {
     float t[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     const int kn = min(8, r - k0);
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(256) k_ln_ext_reg(const float* __restrict__ x3
                                                     const float* __restrict__ bta, int M, void* __restrict__ out,
                                                     int ldo, bool bf16, const float* __restrict__ Pp,
                                                     const float* __restrict__ Pm, int rows_per_sign,
-                                                    int ext_terms) {
+                                                    int ext_terms, long vstride) {
   constexpr int d = NV * 128;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -223,8 +225,10 @@ __global__ void __launch_bounds__(256) k_ln_ext_reg(const float* __restrict__ x3
   }
   const float rsd = 1.0f / sqrtf(warp_sum(s) / (float)d + 1e-5f);
   const float* P = (row < rows_per_sign) ? Pp : Pm;
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  const float4* b4 = reinterpret_cast<const float4*>(bta);
+  // full scope: the -eps probe rows read the second (VectorProbe -1) copy of the LN params
+  const long voff = (row < rows_per_sign) ? 0 : vstride;
+  const float4* g4 = reinterpret_cast<const float4*>(g + voff);
+  const float4* b4 = reinterpret_cast<const float4*>(bta + voff);
   float t[XR > 0 ? XR : 1];
 #pragma unroll
   for (int k = 0; k < (XR > 0 ? XR : 1); ++k) t[k] = 0.f;
@@ -252,7 +256,7 @@ template <int NPT, int XR>
 __global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, const float* __restrict__ g,
                                                 const float* __restrict__ bta, int d, void* __restrict__ out, int ldo,
                                                 bool bf16, const float* __restrict__ Pp, const float* __restrict__ Pm,
-                                                int rows_per_sign, int ext_terms) {
+                                                int rows_per_sign, int ext_terms, long vstride) {
   __shared__ float red[8 * (XR + 1)];
   const int row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -283,8 +287,10 @@ __global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, c
   for (int w = 0; w < nw; ++w) tot += red[w];
   const float rsd = 1.0f / sqrtf(tot / (float)d + 1e-5f);
   const float* P = (row < rows_per_sign) ? Pp : Pm;
-  const float4* g4 = reinterpret_cast<const float4*>(g);
-  const float4* b4 = reinterpret_cast<const float4*>(bta);
+  // full scope: the -eps probe rows read the second (VectorProbe -1) copy of the LN params
+  const long voff = (row < rows_per_sign) ? 0 : vstride;
+  const float4* g4 = reinterpret_cast<const float4*>(g + voff);
+  const float4* b4 = reinterpret_cast<const float4*>(bta + voff);
   float t[XR > 0 ? XR : 1];
 #pragma unroll
   for (int k = 0; k < XR; ++k) t[k] = 0.f;
@@ -325,61 +331,62 @@ __global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, c
 
 template <int NPT>
 static bool ln_row_dispatch(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
-                            bool bf16, const float* Pp, const float* Pm, int r, int rps, int ext_terms,
+                            bool bf16, const float* Pp, const float* Pm, int r, int rps, int ext_terms, long vstride,
                             cudaStream_t st) {
   const int threads = d / (4 * NPT);
   if (threads * 4 * NPT != d || threads % 32 || threads > 256) return false;
   switch (r) {
-    case 0: k_ln_row<NPT, 0><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
-    case 1: k_ln_row<NPT, 1><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
-    case 2: k_ln_row<NPT, 2><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
-    case 4: k_ln_row<NPT, 4><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
+    case 0: k_ln_row<NPT, 0><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 1: k_ln_row<NPT, 1><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 2: k_ln_row<NPT, 2><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 4: k_ln_row<NPT, 4><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
     default: return false;
   }
 }
 
 template <int NV>
 static bool ln_reg_dispatch(const float* x32, const float* gamma, const float* beta, int M, void* out, int ldo,
-                            bool bf16, const float* Pp, const float* Pm, int r, int rps, int ext_terms,
+                            bool bf16, const float* Pp, const float* Pm, int r, int rps, int ext_terms, long vstride,
                             cudaStream_t st) {
   const int grid = (M + 7) / 8;
   switch (r) {
-    case 1: k_ln_ext_reg<NV, 1><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
-    case 2: k_ln_ext_reg<NV, 2><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
-    case 4: k_ln_ext_reg<NV, 4><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms); return true;
+    case 1: k_ln_ext_reg<NV, 1><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 2: k_ln_ext_reg<NV, 2><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 4: k_ln_ext_reg<NV, 4><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
     default: return false;
   }
 }
 
 void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
                    bool bf16, const float* Pplus, const float* Pminus, int r, int rows_per_sign, int ext_terms,
-                   cudaStream_t st) {
+                   long vstride, cudaStream_t st) {
   if (d % 4 || ldo % 4) throw Error(ZO_ERR_DIMENSION, "LN rows must be multiples of 4");
   bool done = false;
   // CTA-per-row kernel (d multiple of 128 and <= 8192)
   if (d % 1024 == 0) {
     switch (d / 1024) {
-      case 1: done = ln_row_dispatch<1>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
-      case 2: done = ln_row_dispatch<2>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
-      case 4: done = ln_row_dispatch<4>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
-      case 5: done = ln_row_dispatch<5>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
-      case 8: done = ln_row_dispatch<8>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+      case 1: done = ln_row_dispatch<1>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
+      case 2: done = ln_row_dispatch<2>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
+      case 4: done = ln_row_dispatch<4>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
+      case 5: done = ln_row_dispatch<5>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
+      case 8: done = ln_row_dispatch<8>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
       default: break;
     }
   } else if (d % 128 == 0 && d <= 1024) {
-    done = ln_row_dispatch<1>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st);
+    done = ln_row_dispatch<1>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms,
+                              vstride, st);
   }
   if (!done) switch (d) {
-    case 768: done = ln_reg_dispatch<6>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
-    case 1024: done = ln_reg_dispatch<8>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
-    case 2048: done = ln_reg_dispatch<16>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
-    case 4096: done = ln_reg_dispatch<32>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
-    case 5120: done = ln_reg_dispatch<40>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, st); break;
+    case 768: done = ln_reg_dispatch<6>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
+    case 1024: done = ln_reg_dispatch<8>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
+    case 2048: done = ln_reg_dispatch<16>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
+    case 4096: done = ln_reg_dispatch<32>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
+    case 5120: done = ln_reg_dispatch<40>(x32, gamma, beta, M, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign, ext_terms, vstride, st); break;
     default: break;
   }
   if (!done)
     k_ln_ext<<<(M + 7) / 8, 256, 0, st>>>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign,
-                                          ext_terms);
+                                          ext_terms, vstride);
 }
 
 // ------------------------------------------------------------------ extension of a 16-bit activation
@@ -426,7 +433,7 @@ void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, c
 __global__ void k_final_ln(const float* __restrict__ x32, const float* __restrict__ g, const float* __restrict__ bta,
                            int B, int T, int d, int prompt_len, int Lopt, float* __restrict__ xs32,
                            void* __restrict__ xs16, bool bf16, const float* __restrict__ Ve, int r,
-                           float* __restrict__ z) {
+                           float* __restrict__ z, int rows_per_sign, long vstride) {
   extern __shared__ float sh[];
   float* row = sh;
   float* red = sh + d;
@@ -434,6 +441,10 @@ __global__ void k_final_ln(const float* __restrict__ x32, const float* __restric
   const int s = srow / (B * Lopt), rem = srow % (B * Lopt), b = rem / Lopt, j = rem % Lopt;
   const int m = s * B * T + b * T + (prompt_len - 1 + j);
   const float* x = x32 + (size_t)m * d;
+  if (m >= rows_per_sign) {  // full scope: VectorProbe -1 copy of ln_f
+    g += vstride;
+    bta += vstride;
+  }
   float acc[1] = {0.f};
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     row[i] = x[i];
@@ -472,7 +483,7 @@ __global__ void k_final_ln(const float* __restrict__ x32, const float* __restric
 
 void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d, int prompt_len,
                      int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r, float* z,
-                     cudaStream_t st) {
+                     int rows_per_sign, long vstride, cudaStream_t st) {
   const size_t smem = (size_t)(d + 32 * 8) * sizeof(float);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
@@ -480,7 +491,7 @@ void launch_final_ln(const float* x32, const float* gamma, const float* beta, in
     configured = smem;
   }
   k_final_ln<<<B * Lopt, 256, smem, st>>>(x32, gamma, beta, B, T, d, prompt_len, Lopt, xs32, xs16, bf16, Ve32,
-                                              r, z);
+                                              r, z, rows_per_sign, vstride);
 }
 
 // ------------------------------------------------------------------ loss (K6b): log-softmax + gold gather
@@ -671,6 +682,55 @@ void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K
                        float* V32, cudaStream_t st) {
   const int64_t cnt = (int64_t)n * r;
   k_vext<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(V, n, r, W16T, ldw, K, bf16, ext_terms, V32);
+}
+
+// ------------------------------------------------------------------ full-scope 1-D params (VectorProbe)
+// zo_engine.py:269-295: sign +1 from 0 adds (1*eps)*z, sign -1 from +1 adds (-2*eps)*z
+// (axpy_dense: product rounded, then sum), float64; the fp32 copies are what the LN
+// kernels read -- [0] for the +eps rows, [1] for the -eps rows.  eps = 0 (no probe)
+// makes both copies fp32(p).
+__global__ void k_vec_probe(const double* __restrict__ p, const double* __restrict__ z, int64_t n, double eps,
+                            float* __restrict__ out32) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (eps == 0.0 || !z) {
+      out32[i] = out32[n + i] = (float)p[i];
+      continue;
+    }
+    const double plus = __dadd_rn(p[i], __dmul_rn(eps, z[i]));
+    const double minus = __dadd_rn(plus, __dmul_rn(-2.0 * eps, z[i]));
+    out32[i] = (float)plus;
+    out32[n + i] = (float)minus;
+  }
+}
+
+void launch_vec_probe(const double* p, const double* z, int64_t n, double eps, float* out32, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  k_vec_probe<<<grid > 0 ? grid : 1, 256, 0, st>>>(p, z, n, eps, out32);
+}
+
+// VectorProbe.update (zo_engine.py:290-295): p += (-(lr*c)) * z with the UNnormalised c
+// (out4[2]), skipped when the step aborted; refreshes both fp32 copies to fp32(p).
+__global__ void k_vec_update(double* __restrict__ p, const double* __restrict__ z, int64_t n,
+                             const double* __restrict__ out4, double lr, const unsigned* __restrict__ abort_flag,
+                             float* __restrict__ out32) {
+  const bool skip = abort_flag ? *abort_flag != 0u : !(isfinite(out4[0]) && isfinite(out4[1]));
+  const double alpha = -__dmul_rn(lr, out4[2]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v = p[i];
+    if (!skip) {
+      v = __dadd_rn(v, __dmul_rn(alpha, z[i]));
+      p[i] = v;
+    }
+    out32[i] = out32[n + i] = (float)v;
+  }
+}
+
+void launch_vec_update(double* p, const double* z, int64_t n, const double* out4, double lr,
+                       const unsigned* abort_flag, float* out32, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  k_vec_update<<<grid > 0 ? grid : 1, 256, 0, st>>>(p, z, n, out4, lr, abort_flag, out32);
 }
 
 // ------------------------------------------------------------------ high-rank extension operand

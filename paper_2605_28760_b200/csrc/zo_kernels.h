@@ -16,9 +16,11 @@ void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const 
                   const float* pe, int nrows, cudaStream_t st);
 // h = LN(x) (model.py:139-142) -> out[:, :d] (16-bit); ext columns [d, d+3r) = (t_hi, t_lo, t_hi)
 // per rank with t = h . P_s (fp32) -- the LoRA K-extension operand (A side).
+// vstride: offset (floats) of the -eps copy of gamma/beta read by rows >= rows_per_sign
+// (full scope, 0 otherwise)
 void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
                    bool bf16, const float* Pplus, const float* Pminus, int r, int rows_per_sign, int ext_terms,
-                   cudaStream_t st);
+                   long vstride, cudaStream_t st);
 // ext columns for a 16-bit activation a[:, :K] already in place (ctx -> attn_out, gelu -> ff_down).
 void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, const float* Pminus, int r,
                 int rows_per_sign, int ext_terms, cudaStream_t st);
@@ -39,7 +41,7 @@ void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, v
 // final LN at scored rows (prompt_len-1+j) of B sequences (both signs counted) -> xs32/xs16, z = xs . V_e
 void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d,
                      int prompt_len, int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r,
-                     float* z, cudaStream_t st);
+                     float* z, int rows_per_sign, long vstride, cudaStream_t st);
 // per scored row: logits + z.P_s,e^T -> log-softmax, gold gather -> nll[sign*B + b] (model.py:202-215)
 void launch_loss(const float* logits, int ldl, int V, const float* z, int r, const float* Pplus_e,
                  const float* Pminus_e, const int32_t* gold, int B, int Lopt, double* nll, cudaStream_t st);
@@ -52,6 +54,11 @@ void launch_update(double* A, const double* U, int64_t n, const double* out4, co
 // P+- = fp32(A +- eps*U)
 void launch_prep_probe(const double* A, const double* U, int64_t n, double eps, double probe_scale, float* Pp,
                        float* Pm, cudaStream_t st);
+// full scope (VectorProbe, zo_engine.py:269-295): out32[0] = fp32(p + eps*z), out32[1] =
+// fp32((p + eps*z) + (-2 eps)*z) (both fp32(p) when eps == 0); update p += (-(lr*c))*z
+void launch_vec_probe(const double* p, const double* z, int64_t n, double eps, float* out32, cudaStream_t st);
+void launch_vec_update(double* p, const double* z, int64_t n, const double* out4, double lr,
+                       const unsigned* abort_flag, float* out32, cudaStream_t st);
 // P16T[k][i] = h16(P[i][k]) for one [m, r] probe block (tensor-core extension B operand, r > 8)
 void launch_p16t(const float* P, int m, int r, void* out, bool bf16, cudaStream_t st);
 // V ext columns (hi, hi, lo) into W16T[:, K:K+3r] for one matrix; V32 copy

@@ -95,7 +95,17 @@ struct zo_ctx {
   int64_t su = 0, sv = 0;  // arena sizes
   double *U = nullptr, *V = nullptr, *A = nullptr;
   float *Pp = nullptr, *Pm = nullptr, *V32 = nullptr;
-  // LN params
+  // 1-D params (LN scale / shift) in sorted vector-id order (model.py:124-125):
+  // float64 masters, full-scope directions z, and the fp32 copies the LN kernels read
+  // ([0] +eps rows, [1] -eps rows; identical unless a full-scope probe is installed)
+  bool full_scope = false;
+  int nv = 0;
+  std::vector<std::string> vids;
+  double *VEC64 = nullptr, *VZ = nullptr;
+  float* VEC32 = nullptr;
+  long vstride = 0;  // offset of the -eps copy read by the LN kernels (0: lora_only)
+  SamplerPlan planZ;
+  std::vector<StreamDesc> streamsZ;
   std::vector<float*> ln1g, ln1b, ln2g, ln2b;
   float *lnfg = nullptr, *lnfb = nullptr;
   // activations
@@ -295,7 +305,7 @@ void do_score(zo_ctx* c, int B, int nsign) {
     const Matrix& w = c->mats[c->i_down[l]];
     const LayerPlan& lp = rp.layers[l];
     launch_ln_ext(c->x32, c->ln1g[l], c->ln1b[l], M, d, c->hA, ldh, c->bf16, c->Pp + q.u_off, c->Pm + q.u_off,
-                  c->fused_ext ? c->r : 0, rps, c->ext_terms, c->st);
+                  c->fused_ext ? c->r : 0, rps, c->ext_terms, c->vstride, c->st);
     if (!c->fused_ext) ext_gemm(lp, 0);
     gemm_launch(lp.qkv, c->st);
     AttnExt ax;
@@ -314,7 +324,7 @@ void do_score(zo_ctx* c, int B, int nsign) {
       ext_gemm(lp, 1);
     gemm_launch(lp.out, c->st);
     launch_ln_ext(c->x32, c->ln2g[l], c->ln2b[l], M, d, c->hA, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off,
-                  c->fused_ext ? c->r : 0, rps, c->ext_terms, c->st);
+                  c->fused_ext ? c->r : 0, rps, c->ext_terms, c->vstride, c->st);
     if (!c->fused_ext) ext_gemm(lp, 2);
     gemm_launch(lp.up, c->st);
     if (c->fused_ext)
@@ -325,7 +335,7 @@ void do_score(zo_ctx* c, int B, int nsign) {
     gemm_launch(lp.down, c->st);
   }
   launch_final_ln(c->x32, c->lnfg, c->lnfb, B * nsign, T, d, c->d.prompt_len, c->d.opt_len, c->xs32, c->xs16,
-                  c->bf16, c->V32 + e.v_off, c->r, c->z, c->st);
+                  c->bf16, c->V32 + e.v_off, c->r, c->z, rps, c->vstride, c->st);
   gemm_launch(rp.lm, c->st);
   launch_loss(c->logits, c->ldl, c->d.vocab, c->z, c->r, c->Pp + e.u_off, c->Pm + e.u_off, c->gold, B,
               c->d.opt_len, c->nll, c->st);
@@ -358,6 +368,19 @@ void launch_dense_update_dev(zo_ctx* c, double lr) {
     launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, c->out4, lr,
                     1.0 / std::sqrt((double)c->r), c->abort_flag, m.W16, m.kind == K_EMBED ? (int)m.n : m.ldw,
                     m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
+}
+
+// full scope: fp32 LN copies for the probe pair (eps) or the plain params (eps = 0)
+void vec_probe(zo_ctx* c, double eps) {
+  if (c->full_scope) launch_vec_probe(c->VEC64, c->VZ, (int64_t)c->nv * c->d.dim, eps, c->VEC32, c->st);
+}
+// full scope: VectorProbe.update with the coefficient in out4 (device)
+void vec_update(zo_ctx* c, const double* out4, double lr, const unsigned* abort_flag) {
+  if (c->full_scope)
+    launch_vec_update(c->VEC64, c->VZ, (int64_t)c->nv * c->d.dim, out4, lr, abort_flag, c->VEC32, c->st);
+}
+void sample_z(zo_ctx* c, uint64_t seed) {
+  if (c->full_scope) sampler_launch(c->planZ, seed, c->d_step, 1, c->VZ, c->st);
 }
 
 void fold_all(zo_ctx* c) {
@@ -395,6 +418,8 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->dh = d.dim / d.n_heads;
   c->r = d.rank;
   c->bf16 = d.precision == ZO_PREC_BF16;
+  check(d.scope == ZO_SCOPE_LORA_ONLY || d.scope == ZO_SCOPE_FULL, ZO_ERR_CONFIG, "unknown scope");
+  c->full_scope = d.scope == ZO_SCOPE_FULL;
   // rank <= 8: fused fp32 extension dots carried as (hi, lo, hi) 16-bit columns; above:
   // one 16-bit column per rank from the tensor-core extension GEMM
   c->ext_terms = d.rank <= 8 ? 3 : 1;
@@ -464,21 +489,43 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->Pp = c->mem.get<float>(c->su);
   c->Pm = c->mem.get<float>(c->su);
   c->V32 = c->mem.get<float>(c->sv);
-  // LN params (identity at init, model.py:100-107)
-  std::vector<float> ones(d.dim, 1.0f);
-  auto vec = [&](bool one) {
-    float* p = c->mem.get<float>(d.dim);
-    if (one) ZO_CUDA_TRY(cudaMemcpy(p, ones.data(), d.dim * 4, cudaMemcpyHostToDevice));
-    return p;
+  // 1-D params (identity at init, model.py:100-107), sorted ids
+  for (int l = 0; l < d.n_layers; ++l)
+    for (const char* w : {"ln1.scale", "ln1.shift", "ln2.scale", "ln2.shift"})
+      c->vids.push_back("blk" + std::to_string(l) + "." + w);
+  c->vids.push_back("ln_f.scale");
+  c->vids.push_back("ln_f.shift");
+  std::sort(c->vids.begin(), c->vids.end());
+  c->nv = (int)c->vids.size();
+  const size_t nvd = (size_t)c->nv * d.dim;
+  c->VEC64 = c->mem.get<double>(nvd);
+  c->VEC32 = c->mem.get<float>(2 * nvd);
+  {
+    std::vector<double> init(nvd, 0.0);
+    for (int v = 0; v < c->nv; ++v)
+      if (c->vids[v].size() >= 6 && c->vids[v].compare(c->vids[v].size() - 6, 6, ".scale") == 0)
+        std::fill(init.begin() + (size_t)v * d.dim, init.begin() + (size_t)(v + 1) * d.dim, 1.0);
+    ZO_CUDA_TRY(cudaMemcpy(c->VEC64, init.data(), nvd * 8, cudaMemcpyHostToDevice));
+    launch_vec_probe(c->VEC64, nullptr, (int64_t)nvd, 0.0, c->VEC32, nullptr);
+    ZO_CUDA_TRY(cudaDeviceSynchronize());
+  }
+  auto vptr = [&](const std::string& id) {
+    const int v = (int)(std::lower_bound(c->vids.begin(), c->vids.end(), id) - c->vids.begin());
+    return c->VEC32 + (size_t)v * d.dim;
   };
   for (int l = 0; l < d.n_layers; ++l) {
-    c->ln1g.push_back(vec(true));
-    c->ln1b.push_back(vec(false));
-    c->ln2g.push_back(vec(true));
-    c->ln2b.push_back(vec(false));
+    const std::string p = "blk" + std::to_string(l) + ".";
+    c->ln1g.push_back(vptr(p + "ln1.scale"));
+    c->ln1b.push_back(vptr(p + "ln1.shift"));
+    c->ln2g.push_back(vptr(p + "ln2.scale"));
+    c->ln2b.push_back(vptr(p + "ln2.shift"));
   }
-  c->lnfg = vec(true);
-  c->lnfb = vec(false);
+  c->lnfg = vptr("ln_f.scale");
+  c->lnfb = vptr("ln_f.shift");
+  if (c->full_scope) {
+    c->VZ = c->mem.get<double>(nvd);
+    c->vstride = (long)nvd;
+  }
   // activations
   c->Mmax = 2 * d.max_batch * c->T;
   c->Mpad = (int)ceil_div(c->Mmax, 128) * 128;
@@ -541,6 +588,20 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   }
   build_sampler_plan(c.get(), c->planU, c->streamsU);
   build_sampler_plan(c.get(), c->planV, c->streamsV);
+  if (c->full_scope) {
+    // dense_direction(seed, step, vid, (dim,)) = gaussian_vector (zo_engine.py:194-198)
+    for (int v = 0; v < c->nv; ++v) {
+      StreamDesc sz{};
+      sz.lid_hash = fnv(c->vids[v].data(), c->vids[v].size(), FNV0);
+      sz.role = 2;  // Role.DENSE_Z
+      sz.step_mode = STEP_CURRENT;
+      sz.n = (uint64_t)d.dim;
+      sz.out_off = (uint64_t)v * d.dim;
+      sz.scale = 1.0;
+      c->streamsZ.push_back(sz);
+    }
+    build_sampler_plan(c.get(), c->planZ, c->streamsZ);
+  }
   ZO_CUDA_TRY(cudaDeviceSynchronize());
   *out = c.release();
   return ZO_OK;
@@ -651,28 +712,32 @@ int zo_download_matrix(zo_ctx* c, const char* lid, double* host, int64_t rows, i
   ZO_API_END
 }
 
+static int vector_index(const zo_ctx* c, const char* lid) {
+  auto it = std::lower_bound(c->vids.begin(), c->vids.end(), std::string(lid));
+  check(it != c->vids.end() && *it == lid, ZO_ERR_INPUT, std::string("unknown vector id ") + lid);
+  return (int)(it - c->vids.begin());
+}
+
 int zo_upload_vector(zo_ctx* c, const char* lid, const double* host, int64_t n) {
   ZO_API_BEGIN
   check(n == c->d.dim, ZO_ERR_DIMENSION, "vector length must equal dim");
-  std::string s(lid);
-  float* dst = nullptr;
-  if (s == "ln_f.scale") dst = c->lnfg;
-  else if (s == "ln_f.shift") dst = c->lnfb;
-  else {
-    int l = -1;
-    char which[16] = {0};
-    if (std::sscanf(lid, "blk%d.%15s", &l, which) == 2 && l >= 0 && l < c->d.n_layers) {
-      std::string w(which);
-      if (w == "ln1.scale") dst = c->ln1g[l];
-      else if (w == "ln1.shift") dst = c->ln1b[l];
-      else if (w == "ln2.scale") dst = c->ln2g[l];
-      else if (w == "ln2.shift") dst = c->ln2b[l];
-    }
-  }
-  check(dst != nullptr, ZO_ERR_INPUT, "unknown vector id " + s);
+  const int v = vector_index(c, lid);
+  const size_t nvd = (size_t)c->nv * n;
+  ZO_CUDA_TRY(cudaMemcpy(c->VEC64 + (size_t)v * n, host, n * 8, cudaMemcpyHostToDevice));
   std::vector<float> f(n);
   for (int64_t i = 0; i < n; ++i) f[i] = (float)host[i];
-  ZO_CUDA_TRY(cudaMemcpy(dst, f.data(), n * 4, cudaMemcpyHostToDevice));
+  ZO_CUDA_TRY(cudaMemcpy(c->VEC32 + (size_t)v * n, f.data(), n * 4, cudaMemcpyHostToDevice));
+  ZO_CUDA_TRY(cudaMemcpy(c->VEC32 + nvd + (size_t)v * n, f.data(), n * 4, cudaMemcpyHostToDevice));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_download_vector(zo_ctx* c, const char* lid, double* host, int64_t n) {
+  ZO_API_BEGIN
+  check(n == c->d.dim, ZO_ERR_DIMENSION, "vector length must equal dim");
+  const int v = vector_index(c, lid);
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  ZO_CUDA_TRY(cudaMemcpy(host, c->VEC64 + (size_t)v * n, n * 8, cudaMemcpyDeviceToHost));
   return ZO_OK;
   ZO_API_END
 }
@@ -681,6 +746,7 @@ int zo_sample_u(zo_ctx* c, uint64_t seed, uint64_t step) {
   ZO_API_BEGIN
   set_step(c, step);
   sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  sample_z(c, seed);
   return ZO_OK;
   ZO_API_END
 }
@@ -738,17 +804,22 @@ int zo_sample_stream(zo_ctx* c, uint64_t seed, uint64_t step, uint64_t lid_hash,
 }
 
 int zo_slot_count(const zo_ctx* c, int32_t which, int64_t* count) {
-  if (which < 0 || which > 2) return ZO_ERR_INPUT;
-  *count = which == 1 ? c->sv : c->su;
+  if (which < 0 || which > 3 || (which == 3 && !c->full_scope)) return ZO_ERR_INPUT;
+  *count = which == 3 ? (int64_t)c->nv * c->d.dim : which == 1 ? c->sv : c->su;
   return ZO_OK;
 }
 
-static double* slot_ptr(zo_ctx* c, int which) { return which == 0 ? c->U : which == 1 ? c->V : c->A; }
+static double* slot_ptr(zo_ctx* c, int which) {
+  return which == 0 ? c->U : which == 1 ? c->V : which == 2 ? c->A : c->VZ;
+}
+static int64_t slot_size(const zo_ctx* c, int which) {
+  return which == 3 ? (int64_t)c->nv * c->d.dim : which == 1 ? c->sv : c->su;
+}
 
 int zo_get_slot(zo_ctx* c, int32_t which, double* host, int64_t count) {
   ZO_API_BEGIN
-  check(which >= 0 && which <= 2, ZO_ERR_INPUT, "bad slot id");
-  check(count == (which == 1 ? c->sv : c->su), ZO_ERR_DIMENSION, "slot arena size mismatch");
+  check(which >= 0 && which <= 3 && (which < 3 || c->full_scope), ZO_ERR_INPUT, "bad slot id");
+  check(count == slot_size(c, which), ZO_ERR_DIMENSION, "slot arena size mismatch");
   ZO_CUDA_TRY(cudaMemcpyAsync(host, slot_ptr(c, which), (size_t)count * 8, cudaMemcpyDeviceToHost, c->st));
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
   return ZO_OK;
@@ -784,6 +855,7 @@ int zo_prepare_probe(zo_ctx* c, double eps, int32_t sign_mode) {
   const double scale = c->d.estimator == ZO_EST_FACTORIZED ? 1.0 / std::sqrt((double)c->r) : 1.0;
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
   launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, sign_mode == 0 ? eps : 0.0, scale, c->Pp, c->Pm, c->st);
+  vec_probe(c, sign_mode == 0 ? eps : 0.0);
   c->probe_eps = eps;
   c->probe_scale = scale;
   return ZO_OK;
@@ -852,7 +924,17 @@ int zo_update_dense(zo_ctx* c, double lr) {
   for (auto& m : c->mats)
     launch_fold(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, alpha, m.W16,
                 m.kind == K_EMBED ? (int)m.n : m.ldw, m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
+  vec_update(c, c->out4, lr, c->abort_flag);
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+// full scope: VectorProbe.update with the installed coefficient (zo_engine.py:290-295,
+// 412-416) -- the custom-scorer path's complement of zo_update_u
+int zo_update_vectors(zo_ctx* c, double lr) {
+  ZO_API_BEGIN
+  vec_update(c, c->out4, lr, c->abort_flag);
   return ZO_OK;
   ZO_API_END
 }
@@ -876,8 +958,10 @@ int zo_step(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, dou
     c->v_window = wstart;
   }
   sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  sample_z(c, seed);
   const double scale = lozo ? 1.0 : 1.0 / std::sqrt((double)c->r);
   launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, eps, scale, c->Pp, c->Pm, c->st);
+  vec_probe(c, eps);
   ZO_CUDA_TRY(cudaEventRecord(c->ev[1], c->st));
   do_score(c, B, 2);
   launch_coefficient(c->nll, B, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
@@ -886,6 +970,7 @@ int zo_step(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, dou
     launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
     c->a_dirty = true;
   }
+  vec_update(c, c->out4, lr, c->abort_flag);
   ZO_CUDA_TRY(cudaMemcpyAsync(c->h_out4, c->out4, 32, cudaMemcpyDeviceToHost, c->st));
   ZO_CUDA_TRY(cudaEventRecord(c->ev[3], c->st));
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -950,8 +1035,10 @@ extern "C" int zo_step_score_async(zo_ctx* c, uint64_t seed, uint64_t step, int3
     c->v_window = wstart;
   }
   sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  sample_z(c, seed);
   const double scale = lozo ? 1.0 : 1.0 / std::sqrt((double)c->r);
   launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, eps, scale, c->Pp, c->Pm, c->st);
+  vec_probe(c, eps);
   do_score(c, B, 2);
   return ZO_OK;
   ZO_API_END
@@ -967,6 +1054,7 @@ extern "C" int zo_step_apply_async(zo_ctx* c, double eps, double lr, int32_t div
   } else {
     launch_dense_update_dev(c, lr);
   }
+  vec_update(c, c->out4, lr, c->abort_flag);
   return ZO_OK;
   ZO_API_END
 }
@@ -983,14 +1071,17 @@ extern "C" int zo_step_async(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu
 static void step_body(zo_ctx* c, uint64_t seed, double eps, double lr, int32_t divide_by_r, int32_t B) {
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
   sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  sample_z(c, seed);
   const double scale = lozo ? 1.0 : 1.0 / std::sqrt((double)c->r);
   launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, eps, scale, c->Pp, c->Pm, c->st);
+  vec_probe(c, eps);
   do_score(c, B, 2);
   launch_coefficient(c->nll, B, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
   if (lozo)
     launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
   else
     launch_dense_update_dev(c, lr);
+  vec_update(c, c->out4, lr, c->abort_flag);
 }
 
 // zo_step_async as one CUDA-graph launch: the ~370 kernels of the step body are
@@ -1072,6 +1163,7 @@ extern "C" int zo_qdir_score_async(zo_ctx* c, uint64_t seed, uint64_t macro_step
   check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
   check(!lozo || nu % G == 0, ZO_ERR_CONFIG, "q-direction mode needs the direction count to divide nu");
+  check(!c->full_scope || G == 1, ZO_ERR_CONFIG, "q-direction mode with G > 1 supports scope lora_only only");
   int rc = zo_step_score_async(c, seed, macro_step * (uint64_t)G + (uint64_t)g, lozo ? nu : 1, eps, tokens_dev,
                                gold_dev, B);
   if (rc) return rc;
@@ -1101,7 +1193,9 @@ extern "C" int zo_qdir_apply_async(zo_ctx* c, uint64_t seed, uint64_t macro_step
   for (int32_t g = 0; g < G; ++g) {
     k_set_u64<<<1, 1, 0, c->st>>>(c->d_step, macro_step * (uint64_t)G + (uint64_t)g);
     sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+    sample_z(c, seed);
     const double* o4 = out4_all_dev + 4 * (size_t)g;
+    vec_update(c, o4, lr, nullptr);
     if (lozo) {
       launch_update(c->A, c->U, c->su, o4, nullptr, c->st);
     } else {

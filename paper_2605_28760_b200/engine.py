@@ -19,8 +19,9 @@ PRECISIONS = {"fp16": _lib.PREC_FP16, "bf16": _lib.PREC_BF16}
 # the reference's precision strings run on the tensor-core path
 ALIASES = {"real64": "fp16", "real32": "fp16"}
 ESTIMATORS = {"lozo_lazy": _lib.EST_LOZO, "factorized_sqrt_r": _lib.EST_FACTORIZED}
+SCOPES = {"lora_only": _lib.SCOPE_LORA_ONLY, "full": _lib.SCOPE_FULL}
 
-U, V, A = 0, 1, 2
+U, V, A, Z = 0, 1, 2, 3  # slot arenas (Z: full-scope 1-D directions)
 
 
 def resolve_precision(precision: str) -> str:
@@ -33,9 +34,12 @@ def resolve_precision(precision: str) -> str:
 class ZoEngine:
     def __init__(self, vocab: int, dim: int, n_layers: int, n_heads: int, prompt_len: int, *,
                  opt_len: int = 1, max_batch: int = 16, rank: int = 2, estimator: str = "lozo_lazy",
-                 precision: str = "fp16", device: int = 0):
+                 precision: str = "fp16", device: int = 0, scope: str = "lora_only"):
         if estimator not in ESTIMATORS:
             raise ConfigError(f"estimator {estimator!r} has no device engine")
+        if scope not in SCOPES:
+            raise ConfigError(f"scope must be one of {tuple(SCOPES)}, got {scope!r}")
+        self.scope = scope
         self.precision = resolve_precision(precision)
         self.estimator = estimator
         self.rank = rank
@@ -43,7 +47,7 @@ class ZoEngine:
         self.prompt_len, self.opt_len, self.max_batch = prompt_len, opt_len, max_batch
         self.T = prompt_len + opt_len
         desc = _lib.ZoModelDesc(vocab, dim, n_layers, n_heads, prompt_len, opt_len, max_batch, rank,
-                                ESTIMATORS[estimator], PRECISIONS[self.precision], device)
+                                ESTIMATORS[estimator], PRECISIONS[self.precision], device, SCOPES[scope])
         h = ctypes.c_void_p()
         check(lib().zo_create(ctypes.byref(h), ctypes.byref(desc)))
         self._h = h
@@ -104,6 +108,20 @@ class ZoEngine:
             else:
                 check(lib().zo_upload_vector(self._h, lid.encode(), w.ctypes.data, w.shape[0]))
 
+    def download_vector(self, lid: str) -> np.ndarray:
+        out = np.empty(self.dim, dtype=np.float64)
+        check(lib().zo_download_vector(self._h, lid.encode(), out.ctypes.data, self.dim))
+        return out
+
+    @property
+    def vids(self) -> list[str]:
+        """1-D param ids in sorted order (model.py:124-125)."""
+        ids = [f"blk{i}.{ln}.{w}" for i in range(self.n_layers) for ln in ("ln1", "ln2") for w in ("scale", "shift")]
+        return sorted(ids + ["ln_f.scale", "ln_f.shift"])
+
+    def update_vectors(self, lr: float) -> None:
+        check(lib().zo_update_vectors(self._h, float(lr)))
+
     def download(self, lid: str) -> np.ndarray:
         m, n = self.shapes[lid]
         out = np.empty((m, n), dtype=np.float64)
@@ -118,7 +136,7 @@ class ZoEngine:
         check(lib().zo_sample_v(self._h, seed, step, nu))
 
     def get_slot(self, which: int) -> np.ndarray:
-        n = self.sv if which == V else self.su
+        n = self.sv if which == V else (len(self.vids) * self.dim if which == Z else self.su)
         out = np.empty(n, dtype=np.float64)
         check(lib().zo_get_slot(self._h, which, out.ctypes.data, n))
         return out
@@ -142,8 +160,10 @@ class ZoEngine:
     def join(self, which: int, mats: dict) -> np.ndarray:
         return np.concatenate([np.ascontiguousarray(mats[l], dtype=np.float64).reshape(-1) for l in self.lids])
 
-    def digest(self, which: int, arena: np.ndarray | None = None) -> int:
-        """Chained FNV over (lid, factor) in sorted id order (zo_engine.py:220-261)."""
+    def digest(self, which: int, arena: np.ndarray | None = None, z_arena: np.ndarray | None = None) -> int:
+        """Chained FNV over (lid, factor) in sorted id order (zo_engine.py:220-261); for the
+        U digest of a full-scope engine the 1-D directions (``z_arena``, default: the
+        current Z slot) chain after the matrices."""
         if arena is None:
             arena = self.get_slot(which)
         arena = np.ascontiguousarray(arena, dtype=np.float64)
@@ -151,8 +171,17 @@ class ZoEngine:
         rows = [(self.shapes[l][1] if which == V else self.shapes[l][0]) * self.rank for l in self.lids]
         off_c = (ctypes.c_int64 * len(self.lids))(*[offs[l] for l in self.lids])
         cnt_c = (ctypes.c_int64 * len(self.lids))(*rows)
-        return int(lib().zo_digest_chain(self._lid_c, arena.ctypes.data, off_c, cnt_c, len(self.lids),
-                                         0xCBF29CE484222325))
+        h = int(lib().zo_digest_chain(self._lid_c, arena.ctypes.data, off_c, cnt_c, len(self.lids),
+                                      0xCBF29CE484222325))
+        if which == U and self.scope == "full":
+            # full scope: the dense 1-D directions chain after the matrices (zo_engine.py:256-260)
+            z = np.ascontiguousarray(self.get_slot(Z) if z_arena is None else z_arena)
+            vids = self.vids
+            names = (ctypes.c_char_p * len(vids))(*[v.encode() for v in vids])
+            zo = (ctypes.c_int64 * len(vids))(*[i * self.dim for i in range(len(vids))])
+            zc = (ctypes.c_int64 * len(vids))(*[self.dim] * len(vids))
+            h = int(lib().zo_digest_chain(names, z.ctypes.data, zo, zc, len(vids), h))
+        return h
 
     def sampler_flags(self) -> tuple[int, int, int]:
         f = (ctypes.c_uint32 * 3)()

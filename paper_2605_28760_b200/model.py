@@ -102,6 +102,11 @@ class DeviceParams(Mapping):
     # Mapping protocol
     def __getitem__(self, lid: str) -> np.ndarray:
         if lid in self._vectors:
+            if self._engine is not None and self._engine.scope == "full":
+                # full scope: the device updates the 1-D params every step
+                if lid not in self._cache:
+                    self._cache[lid] = self._engine.download_vector(lid)
+                return self._cache[lid]
             return self._vectors[lid]
         if lid not in self._shapes:
             raise KeyError(lid)
@@ -132,9 +137,21 @@ class DeviceParams(Mapping):
         return self._engine
 
     def bind(self, rank: int = 2, estimator: str = "lozo_lazy", max_batch: int | None = None,
-             opt_len: int = 1) -> ZoEngine:
+             opt_len: int = 1, scope: str = "lora_only") -> ZoEngine:
         """Create (or check) the device engine for this parameter set."""
         mb = max(max_batch or 0, self.max_batch)
+        if self._engine is not None and self._engine.scope != scope:
+            # the scope is fixed per engine (full scope adds the 1-D probe arenas): move the
+            # current parameters into a fresh engine of the requested scope
+            old = self._engine
+            host = {lid: old.download(lid) for lid in old.lids}
+            if old.scope == "full":
+                for vid in old.vids:
+                    self._vectors[vid] = old.download_vector(vid)
+            old.close()
+            self._engine = None
+            self._cache.clear()
+            self._host = host
         if self._engine is not None:
             e = self._engine
             if (e.rank, e.estimator, e.opt_len) != (rank, estimator, opt_len) or e.max_batch < mb:
@@ -147,7 +164,7 @@ class DeviceParams(Mapping):
             return e
         c = self.cfg
         e = ZoEngine(c.vocab, c.dim, c.n_layers, c.n_heads, c.prompt_len, opt_len=opt_len, max_batch=mb,
-                     rank=rank, estimator=estimator, precision=self.precision, device=self.device)
+                     rank=rank, estimator=estimator, precision=self.precision, device=self.device, scope=scope)
         if self._host is None:
             e.init_params(c.init_seed, c.init_scale)
         else:

@@ -15,7 +15,7 @@ import numpy as np
 from dataclasses import dataclass, field
 
 from .adapter import AdapterState
-from .engine import U as SLOT_U, V as SLOT_V
+from .engine import U as SLOT_U, V as SLOT_V, Z as SLOT_Z
 from .errors import ConfigError, ScoringAbort
 from .model import (EvalPoint, ModelConfig, TaskData, as_device_params, evaluate_split, init_params,
                     params_digest, sample_minibatch)
@@ -82,7 +82,7 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
                          max_batch=max(16, zcfg.batch_size)) if params is None else params
     dp = as_device_params(params, mcfg)
     opt_len = len(task.config.options[0])
-    eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, opt_len)
+    eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, opt_len, zcfg.scope)
     model_digest = params_digest(dp) if compute_param_digests else ""
     state = AdapterState(epsilon=zcfg.epsilon) if state is None else state
     state._bind(eng)
@@ -125,7 +125,8 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
         meter.scoring_cost_units += 2 * zcfg.batch_size
         if pool is not None:
             u_arena = eng.get_slot(SLOT_U)
-            ufut = pool.submit(eng.digest, SLOT_U, u_arena)
+            z_arena = eng.get_slot(SLOT_Z) if zcfg.scope == "full" else None
+            ufut = pool.submit(eng.digest, SLOT_U, u_arena, z_arena)
             wkey = (t // zcfg.nu) * zcfg.nu if zcfg.estimator == "lozo_lazy" else t
             if vfut["key"] != wkey:
                 vfut["key"], vfut["fut"] = wkey, pool.submit(eng.digest, SLOT_V, eng.get_slot(SLOT_V))

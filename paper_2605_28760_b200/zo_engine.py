@@ -17,7 +17,7 @@ from dataclasses import asdict, dataclass
 import numpy as np
 
 from .adapter import AdapterState, LoraSlot
-from .engine import V as SLOT_V, U as SLOT_U
+from .engine import V as SLOT_V, U as SLOT_U, Z as SLOT_Z
 from .errors import ConfigError, InputError
 from .model import Minibatch, ModelConfig, as_device_params, matrix_ids
 from .numerics import FNV_OFFSET_BASIS, Role, StreamKey, digest_hex, digest_text, sample_gaussian
@@ -140,12 +140,10 @@ class StepDirections:
 
 
 def _engine_for(params, mcfg: ModelConfig, zcfg: ZoConfig, batch: Minibatch):
-    if zcfg.scope != "lora_only":
-        raise ConfigError("scope 'full' (dense 1-D vector probes) has no B200 engine path yet")
     if zcfg.estimator == "dense_mezo":
         raise ConfigError("dense_mezo has no B200 engine path (no compact update factor)")
     dp = as_device_params(params, mcfg)
-    eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, batch.option_array().shape[1])
+    eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, batch.option_array().shape[1], zcfg.scope)
     return dp, eng
 
 
@@ -153,13 +151,17 @@ def step_directions(params, zcfg: ZoConfig, step: int, mcfg: ModelConfig | None 
     """Every direction of one step plus chained digests (zo_engine.py:224-261).
     Device-sampled; the host copies are for inspection / digests."""
     dp = as_device_params(params, mcfg or params.cfg)
-    eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size)
+    eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, scope=zcfg.scope)
     eng.sample_v(zcfg.seed, step, zcfg.nu if zcfg.estimator == "lozo_lazy" else 1)
     eng.sample_u(zcfg.seed, step)
     u_ar, v_ar = eng.get_slot(SLOT_U), eng.get_slot(SLOT_V)
     U, Vd = eng.split(SLOT_U, u_ar), eng.split(SLOT_V, v_ar)
+    vectors = {}
+    if zcfg.scope == "full":
+        z = eng.get_slot(SLOT_Z)
+        vectors = {vid: z[i * eng.dim:(i + 1) * eng.dim].copy() for i, vid in enumerate(eng.vids)}
     scale = 1.0 if zcfg.estimator == "lozo_lazy" else 1.0 / math.sqrt(zcfg.rank)
-    return StepDirections({l: (U[l], Vd[l]) for l in eng.lids}, {}, digest_hex(eng.digest(SLOT_U, u_ar)),
+    return StepDirections({l: (U[l], Vd[l]) for l in eng.lids}, vectors, digest_hex(eng.digest(SLOT_U, u_ar)),
                           digest_hex(eng.digest(SLOT_V, v_ar)), scale)
 
 
@@ -263,6 +265,8 @@ def lozo_step(params, mcfg: ModelConfig, state: AdapterState, zcfg: ZoConfig, st
     if scorer is None:
         out = eng.step(zcfg.seed, step, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, zcfg.divide_by_r, tokens, gold)
         lp, lm, beta = float(out[0]), float(out[1]), float(out[3])
+        if zcfg.scope == "full":
+            dp.invalidate()
     else:
         window = (step // zcfg.nu) * zcfg.nu
         if getattr(state, "_window", None) != window:
@@ -279,6 +283,8 @@ def lozo_step(params, mcfg: ModelConfig, state: AdapterState, zcfg: ZoConfig, st
         beta = -(zcfg.learning_rate * c_used)
         eng.set_coefficient(np.array([lp, lm, c, beta]))
         eng.update_u()
+        eng.update_vectors(zcfg.learning_rate)  # full scope: VectorProbe.update (zo_engine.py:412-416)
+        dp.invalidate()
     ud, vd = _digests(state, eng, zcfg, step, digests)
     return make_step_record(zcfg, step, lp, lm, beta, ud, vd, batch)
 

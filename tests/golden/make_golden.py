@@ -185,6 +185,16 @@ def adapter_fixture():
     save_adapter(st, os.path.join(OUT, "adapter_rich.zoad"))
 
 
+def full_scope_trajectories():
+    """scope="full": every 1-D param (LN scale/shift) probed and updated densely with
+    Role.DENSE_Z directions (zo_engine.py:256-260, 269-295, 412-416, 439-452)."""
+    trajectory("micro_full", MICRO, MICRO_TASK,
+               dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=5, batch_size=8, scope="full"), 8)
+    trajectory("micro_fact_full", MICRO, MICRO_TASK,
+               dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=4, estimator="factorized_sqrt_r",
+                    batch_size=8, scope="full"), 4)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--opt125m", action="store_true")
@@ -192,6 +202,9 @@ def main():
     a = ap.parse_args()
     if a.only == "adapter":
         adapter_fixture()
+        return
+    if a.only == "full":
+        full_scope_trajectories()
         return
     adapter_fixture()
     streams()
@@ -205,6 +218,7 @@ def main():
                     estimator="factorized_sqrt_r", batch_size=8), 6)
     trajectory("small_lozo", SMALL, SMALL_TASK,
                dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=4, batch_size=16), 10)
+    full_scope_trajectories()
     if a.opt125m:
         forward_fixture("opt125m", OPT125, OPT125_TASK, B=16)
         trajectory("opt125m_lozo", OPT125, OPT125_TASK,

@@ -46,7 +46,7 @@ class _ReplayScorer:
         return v
 
 
-@pytest.mark.parametrize("name", ["micro_lozo", "small_lozo"])
+@pytest.mark.parametrize("name", ["micro_lozo", "small_lozo", "micro_full"])
 def test_update_and_fold_bit_exact_with_reference_coefficients(golden_dir, name):
     from paper_2605_28760_b200.adapter import AdapterState
     from paper_2605_28760_b200.zo_engine import lozo_step
@@ -71,13 +71,14 @@ def test_update_and_fold_bit_exact_with_reference_coefficients(golden_dir, name)
     assert M.params_digest(params) == fin["final_params_digest"]
 
 
-def test_factorized_dense_update_bit_exact(golden_dir):
+@pytest.mark.parametrize("name", ["micro_fact", "micro_fact_full"])
+def test_factorized_dense_update_bit_exact(golden_dir, name):
     from paper_2605_28760_b200.engine import U, V, ZoEngine
     from paper_2605_28760_b200.numerics import canonical_mean, digest_hex
-    h, recs, fin = _traj(golden_dir, "traj_micro_fact.jsonl")
+    h, recs, fin = _traj(golden_dir, f"traj_{name}.jsonl")
     M, mcfg, task, zcfg = _setup(h)
     eng = ZoEngine(mcfg.vocab, mcfg.dim, mcfg.n_layers, mcfg.n_heads, mcfg.prompt_len, max_batch=zcfg.batch_size,
-                   rank=zcfg.rank, estimator="factorized_sqrt_r")
+                   rank=zcfg.rank, estimator="factorized_sqrt_r", scope=zcfg.scope)
     eng.init_params(mcfg.init_seed, mcfg.init_scale)
     dl = []
     for t, rec in enumerate(recs):
@@ -94,13 +95,14 @@ def test_factorized_dense_update_bit_exact(golden_dir):
         eng.update_dense(zcfg.learning_rate)
     assert max(dl) < 1.5e-2, dl
     params = {lid: eng.download(lid) for lid in eng.lids}
-    params.update({k: v for k, v in M._vector_defaults(mcfg).items()})
+    params.update({k: eng.download_vector(k) for k in eng.vids})
     assert M.params_digest(params) == fin["final_params_digest"]
 
 
-def test_run_serving_path_public_api(golden_dir):
+@pytest.mark.parametrize("name", ["micro_lozo", "micro_full"])
+def test_run_serving_path_public_api(golden_dir, name):
     from paper_2605_28760_b200.runtime import run_serving_path
-    h, recs, fin = _traj(golden_dir, "traj_micro_lozo.jsonl")
+    h, recs, fin = _traj(golden_dir, f"traj_{name}.jsonl")
     M, mcfg, task, zcfg = _setup(h)
     run = run_serving_path(mcfg, task, zcfg, h["steps"], eval_every=10 ** 9)
     assert run.model_digest == h["model_digest"] and run.task_digest == h["task_digest"]
@@ -111,9 +113,10 @@ def test_run_serving_path_public_api(golden_dir):
     assert abs(run.eval_curve[-1].loss - fin["eval_loss"]) < 2e-2
     # the reference's wire format round-trips
     from paper_2605_28760_b200.zo_engine import read_trajectory, write_trajectory
-    write_trajectory("gpurun_out/parity_traj_micro_lozo_b200.jsonl", {"model_digest": run.model_digest},
-                     run.trajectory, {"eval_loss": run.eval_curve[-1].loss})
-    _, back, _ = read_trajectory("gpurun_out/parity_traj_micro_lozo_b200.jsonl")
+    os.makedirs("gpurun_out", exist_ok=True)
+    out = f"gpurun_out/parity_traj_{name}_b200.jsonl"
+    write_trajectory(out, {"model_digest": run.model_digest}, run.trajectory, {"eval_loss": run.eval_curve[-1].loss})
+    _, back, _ = read_trajectory(out)
     assert [r.to_dict() for r in back] == [r.to_dict() for r in run.trajectory]
 
 

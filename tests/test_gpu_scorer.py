@@ -24,12 +24,12 @@ def _load(golden_dir, name):
         return json.load(f)
 
 
-def _engine(g, precision="fp16", rank=None, estimator="lozo_lazy", max_batch=None):
+def _engine(g, precision="fp16", rank=None, estimator="lozo_lazy", max_batch=None, scope="lora_only"):
     from paper_2605_28760_b200.engine import ZoEngine
     m = g["model"]
     return ZoEngine(m["vocab"], m["dim"], m["n_layers"], m["n_heads"], m["prompt_len"], opt_len=1,
                     max_batch=max_batch or 16, rank=rank or g.get("rank", 2), estimator=estimator,
-                    precision=precision)
+                    precision=precision, scope=scope)
 
 
 def _params_digest(eng, cfg):
@@ -103,7 +103,7 @@ def _traj(golden_dir, name):
     return lines[0], [l for l in lines if l["record"] == "step"], lines[-1]
 
 
-@pytest.mark.parametrize("name", ["micro_lozo", "small_lozo"])
+@pytest.mark.parametrize("name", ["micro_lozo", "small_lozo", "micro_full"])
 def test_device_step_trajectory(golden_dir, name):
     """zo_step (fused device lozo_step) vs the reference's run_serving_path trajectory."""
     from paper_2605_28760_b200.engine import U as SU, V as SV
@@ -112,7 +112,7 @@ def test_device_step_trajectory(golden_dir, name):
     cfg = R.ModelCfg(**h["model"])
     z = R.ZoCfg(**h["zo"])
     splits = R.generate_task(R.TaskCfg(**h["task"]))
-    eng = _engine({"model": h["model"], "rank": z.rank}, max_batch=z.batch_size)
+    eng = _engine({"model": h["model"], "rank": z.rank}, max_batch=z.batch_size, scope=z.scope)
     eng.init_params(cfg.init_seed, cfg.init_scale)
     rows = []
     for t, rec in enumerate(recs):

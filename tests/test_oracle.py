@@ -69,7 +69,7 @@ def test_forward_nll_vs_reference(golden_dir, name):
         np.testing.assert_allclose(nll, ref, rtol=0, atol=tol)
 
 
-@pytest.mark.parametrize("name", ["micro_lozo", "micro_fact", "small_lozo"])
+@pytest.mark.parametrize("name", ["micro_lozo", "micro_fact", "small_lozo", "micro_full", "micro_fact_full"])
 def test_trajectory_vs_reference(golden_dir, name):
     h, recs, fin = _traj(golden_dir, f"traj_{name}.jsonl")
     cfg = R.ModelCfg(**h["model"])
