@@ -121,13 +121,14 @@ def ncu_traffic(model):
     """DRAM bytes (read + write) of one launch of each of the four layer GEMMs, from the
     committed `ncu --set full` capture (profiles/), or None when not captured for this model."""
     import csv
-    p = os.path.join(HERE, "profiles", "r01_ncu_full_gemm_opt13b_layer1.csv")
+    p = os.path.join(HERE, "profiles", "r01d_ncu_gemm_opt13b.csv")
     if model != "opt-13b" or not os.path.exists(p):
         return None
     tot = 0.0
     with open(p) as f:
-        for row in csv.DictReader(f):
-            tot += (float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])) * 1e6  # MB
+        rows = list(csv.DictReader(f))[:4]  # qkv, attn_out, ff_up, ff_down of layer 1
+        for row in rows:
+            tot += (float(row["dram__bytes_read.sum [Mbyte]"]) + float(row["dram__bytes_write.sum [Mbyte]"])) * 1e6
     return tot
 
 

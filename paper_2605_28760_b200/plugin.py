@@ -16,6 +16,12 @@
 
 The reference state is duck-typed: ``entries[lid].window_slot/.perturb_slot``
 with ``.A, .B, .scale`` and ``perturb_sign``, ``epsilon`` (adapter.py:53-197).
+
+scope="full": the reference's VectorProbe writes p + eps z (sign +1) and then
+p - eps z (sign -1) into the 1-D params in place before each scorer call
+(zo_engine.py:269-295, on_sign).  The scorer re-uploads the 1-D params whenever
+they changed since the last call and then serves only the half of the fused
+pair whose LN rows carry them (no L- cache across a vector change).
 """
 from __future__ import annotations
 
@@ -69,8 +75,21 @@ class ReferenceScorer:
     def __init__(self, params, mcfg, state, rank: int = 2, batch_size: int = 16, precision: str = "fp16",
                  engine: ZoEngine | None = None):
         self.state = state
+        self.params = params
         self.eng = engine or _engine_from_reference(params, mcfg, rank, batch_size, precision)
         self._cached = None
+        self._vecs = {k: np.array(v, dtype=np.float64) for k, v in params.items() if np.ndim(v) == 1}
+
+    def _sync_vectors(self) -> bool:
+        """Upload 1-D params the host changed (VectorProbe); True if any changed."""
+        changed = {}
+        for k, v in self.params.items():
+            if np.ndim(v) == 1 and not np.array_equal(v, self._vecs.get(k)):
+                changed[k] = np.array(v, dtype=np.float64)
+        if changed:
+            self.eng.upload(changed)
+            self._vecs.update(changed)
+        return bool(changed)
 
     def _tokens(self, batch):
         gold = batch.option_array()[batch.golds]
@@ -79,6 +98,8 @@ class ReferenceScorer:
     def __call__(self, batch) -> float:
         sign = self.state.perturb_sign
         key = batch.batch_id
+        if self._sync_vectors():
+            self._cached = None  # the -1 probe moved the 1-D params: score it afresh
         if sign == -1 and self._cached is not None and self._cached[0] == key:
             lm = self._cached[1]
             self._cached = None

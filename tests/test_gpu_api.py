@@ -118,6 +118,17 @@ def test_run_serving_path_public_api(golden_dir, name):
     write_trajectory(out, {"model_digest": run.model_digest}, run.trajectory, {"eval_loss": run.eval_curve[-1].loss})
     _, back, _ = read_trajectory(out)
     assert [r.to_dict() for r in back] == [r.to_dict() for r in run.trajectory]
+    # the reference's acceptance checks (verify.py): strict compare at the fp16 tolerance,
+    # sign agreement of L+ - L- on every high-signal step
+    from paper_2605_28760_b200.verify import record_deltas, sign_match, strict_compare
+    ref = read_trajectory(os.path.join(golden_dir, f"traj_{name}.jsonl"))
+    sc = strict_compare(ref, read_trajectory(out), loss_tol=1.5e-2)
+    sm = sign_match(record_deltas(ref[1]), record_deltas(back))
+    os.makedirs("gpurun_out/parity", exist_ok=True)
+    with open(f"gpurun_out/parity/verify_{name}.json", "w") as f:
+        json.dump({"strict_compare": sc.to_dict(), "sign_match": sm.to_dict()}, f, indent=1)
+    assert sc.accepted == sc.steps, sc.to_dict()
+    assert sm.high_signal_fraction == 1.0 and sm.overall_fraction >= 0.9, sm.to_dict()
 
 
 def test_run_serving_path_abort_is_transactional(golden_dir):
