@@ -150,6 +150,24 @@ def dense_flops(dim, L, B, T, V, r, opt_len=1):
 
 
 # --------------------------------------------------------------------------- CPU arms
+def workload_config(args, world: int) -> tuple[dict, str, bool]:
+    """The bench line's `config` (identical for both arms), `scaling`, and whether the
+    N>1 run is in q-direction mode."""
+    qdir = world > 1 and args.mode == "qdir"
+    fact = args.estimator == "factorized_sqrt_r"
+    B, T = args.batch, args.seq
+    nu = args.nu
+    if qdir and nu % world:
+        nu = max(world, nu // world * world)
+    workload = (f"{args.model} factorized_sqrt_r (MeZO-style) r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, "
+                f"dense float64 update every step" if fact else
+                f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, nu={nu}, fold amortised")
+    cfg = {"workload": workload, "model": args.model, "global_batch": B, "seq_len": T,
+           "parallelism": (f"qdir{world}" if qdir else f"exact-dp{world}") if world > 1 else "single",
+           "l2": "inputs larger than L2 (25.7 GB 16-bit weights/step at 13B); no flush"}
+    return cfg, ("strong" if (world > 1 and not qdir) else "weak"), qdir
+
+
 def run_reference(args, mdl):
     """--impl reference: the oracle port of the reference's path on host cores."""
     rank, world, _ = dist_env()
@@ -169,11 +187,10 @@ def run_reference(args, mdl):
     v = 1.0 / per_step
     sample = (f"oracle float64 port: per step 1 of {mdl['n_layers']} blocks, paired +-eps forward of 1 of {B} "
               f"sequences (T={T}, scaled x{B}) + the block's per-call composition; x{mdl['n_layers']} + LM-head rows")
+    cfg, scaling, _ = workload_config(args, world)
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.model} LoZO r=2 LoRA-only, B={B} x T={T}", "model": args.model,
-                       "global_batch": B, "seq_len": T},
+            "ms_per_step": per_step * 1e3, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "impl": "reference", "config": cfg,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": host_threads(), "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "scored_tokens_per_s": v * 2 * B * T}
@@ -333,17 +350,13 @@ def main():
         5 + 2 * (4 * mcfg.n_layers + 1))
 
     hbm_peak, tf_peak, peak_kind = peaks()
+    cfg, scaling, _ = workload_config(args, world)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "strong" if (world > 1 and not qdir) else "weak", "vs_baseline": None,
+            "scaling": scaling, "vs_baseline": None,
             "dtype": args.precision,
             "data": "synthetic (marker task, random-init Role.INIT weights)",
-            "config": {"workload": (f"{args.model} factorized_sqrt_r (MeZO-style) r={args.rank} LoRA-only SST-2 "
-                                    f"shape, B={B} x T={T}, dense float64 update every step" if fact else
-                                    f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, "
-                                    f"nu={args.nu}, fold amortised"), "model": args.model, "global_batch": B,
-                       "seq_len": T, "parallelism": (f"qdir{world}" if qdir else f"exact-dp{world}") if world > 1 else "single",
-                       "l2": "inputs larger than L2 (25.7 GB 16-bit weights/step at 13B); no flush"},
+            "config": cfg,
             "scored_tokens_per_s": value * 2 * B * T, "option_tokens_per_s": value * 2 * B,
             "gpu_launches": launches, "clocks": clk.summary(), "init_s": t_init,
             "last_losses": [float(out4[0]), float(out4[1]), float(out4[2])]}
