@@ -67,6 +67,8 @@ template <int DH, int TP, bool BF16>
 __global__ void __launch_bounds__(TP * 2)
     k_attn_mma(const uint16_t* __restrict__ qkv, int ldq, uint16_t* __restrict__ ctx, int ldc, int T, int H,
                AttnExt x) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int LD = DH + 8;  // padded row (halves): conflict-free ldmatrix
   constexpr int NT = TP / 8;  // key n-tiles
   constexpr int DT = DH / 8;  // output n-tiles
@@ -236,8 +238,8 @@ static void launch_t(const void* qkv, int ldq, void* ctx, int ldc, int nseq, int
                                      (int)smem));
     set = true;
   }
-  k_attn_mma<DH, TP, BF16><<<dim3(nseq, H), TP * 2, smem, st>>>(static_cast<const uint16_t*>(qkv), ldq,
-                                                                 static_cast<uint16_t*>(ctx), ldc, T, H, x);
+  launch_pdl(k_attn_mma<DH, TP, BF16>, dim3(nseq, H), dim3(TP * 2), smem, st, static_cast<const uint16_t*>(qkv),
+             ldq, static_cast<uint16_t*>(ctx), ldc, T, H, x);
 }
 
 template <int DH, bool BF16>

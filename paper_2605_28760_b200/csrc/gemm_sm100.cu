@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(192, 1)
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = smem_u32(bars + 2 * C::STAGES + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -305,6 +306,9 @@ __global__ void __launch_bounds__(192, 1)
   if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // prologue done (barriers, TMEM, descriptor prefetch): from here on the operands and
+  // the residual are read, so wait for the producing kernel (PDL, zo_common.cuh)
+  pdl_wait();
   const int num_tiles = p.m_tiles * p.n_tiles;
 
   if (warp == 0) {
@@ -741,20 +745,22 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.sk_ws = g.sk_ws;
   p.sk_flags = g.sk_flags;
   if constexpr (CG == 1) {
-    k_gemm<BN, EPI, BF16, XR, 1><<<g.grid, 192, C::SMEM, st>>>(g.tmA, g.tmB, p);
+    launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(192), C::SMEM, st, g.tmA, g.tmB, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.grid);
     cfg.blockDim = dim3(192);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     ZO_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm<BN, EPI, BF16, XR, 2>, g.tmA, g.tmB, p));
   }
 }

@@ -93,6 +93,8 @@ __device__ __forceinline__ void write_ext(void* out, size_t base, int k, float t
 __global__ void __launch_bounds__(256) k_ext_finalize(const float* __restrict__ tpart, int ntiles, int ld, int M,
                                                       int r, void* __restrict__ a, int lda, int K, int ext_terms,
                                                       bool bf16) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= M * r) return;
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(256) k_ext_finalize(const float* __restrict__ 
 
 void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
                          int ext_terms, bool bf16, cudaStream_t st) {
-  k_ext_finalize<<<(M * r + 7) / 8, 256, 0, st>>>(tpart, ntiles, ld, M, r, a, lda, K, ext_terms, bf16);
+  launch_pdl(k_ext_finalize, dim3((M * r + 7) / 8), dim3(256), 0, st, tpart, ntiles, ld, M, r, a, lda, K, ext_terms, bf16);
 }
 
 // ------------------------------------------------------------------ embed
@@ -148,6 +150,8 @@ __global__ void __launch_bounds__(256) k_ln_ext(const float* __restrict__ x32, c
                                                 int ldo, bool bf16, const float* __restrict__ Pp,
                                                 const float* __restrict__ Pm, int r, int rows_per_sign,
                                                 int ext_terms, long vstride) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -205,6 +209,8 @@ __global__ void __launch_bounds__(256) k_ln_ext_reg(const float* __restrict__ x3
                                                     int ldo, bool bf16, const float* __restrict__ Pp,
                                                     const float* __restrict__ Pm, int rows_per_sign,
                                                     int ext_terms, long vstride) {
+  pdl_launch_dependents();
+  pdl_wait();
   constexpr int d = NV * 128;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -257,6 +263,8 @@ __global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, c
                                                 const float* __restrict__ bta, int d, void* __restrict__ out, int ldo,
                                                 bool bf16, const float* __restrict__ Pp, const float* __restrict__ Pm,
                                                 int rows_per_sign, int ext_terms, long vstride) {
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ float red[8 * (XR + 1)];
   const int row = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -336,10 +344,10 @@ static bool ln_row_dispatch(const float* x32, const float* gamma, const float* b
   const int threads = d / (4 * NPT);
   if (threads * 4 * NPT != d || threads % 32 || threads > 256) return false;
   switch (r) {
-    case 0: k_ln_row<NPT, 0><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
-    case 1: k_ln_row<NPT, 1><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
-    case 2: k_ln_row<NPT, 2><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
-    case 4: k_ln_row<NPT, 4><<<M, threads, 0, st>>>(x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 0: launch_pdl(k_ln_row<NPT, 0>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 1: launch_pdl(k_ln_row<NPT, 1>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 2: launch_pdl(k_ln_row<NPT, 2>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 4: launch_pdl(k_ln_row<NPT, 4>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
     default: return false;
   }
 }
@@ -350,9 +358,9 @@ static bool ln_reg_dispatch(const float* x32, const float* gamma, const float* b
                             cudaStream_t st) {
   const int grid = (M + 7) / 8;
   switch (r) {
-    case 1: k_ln_ext_reg<NV, 1><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
-    case 2: k_ln_ext_reg<NV, 2><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
-    case 4: k_ln_ext_reg<NV, 4><<<grid, 256, 0, st>>>(x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 1: launch_pdl(k_ln_ext_reg<NV, 1>, dim3(grid), dim3(256), 0, st, x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 2: launch_pdl(k_ln_ext_reg<NV, 2>, dim3(grid), dim3(256), 0, st, x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    case 4: launch_pdl(k_ln_ext_reg<NV, 4>, dim3(grid), dim3(256), 0, st, x32, gamma, beta, M, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
     default: return false;
   }
 }
@@ -385,7 +393,7 @@ void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int 
     default: break;
   }
   if (!done)
-    k_ln_ext<<<(M + 7) / 8, 256, 0, st>>>(x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign,
+    launch_pdl(k_ln_ext, dim3((M + 7) / 8), dim3(256), 0, st, x32, gamma, beta, M, d, out, ldo, bf16, Pplus, Pminus, r, rows_per_sign,
                                           ext_terms, vstride);
 }
 

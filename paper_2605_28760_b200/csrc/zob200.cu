@@ -166,6 +166,16 @@ struct zo_ctx {
   }
 };
 
+namespace zo {
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("ZO_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+}  // namespace zo
+
 namespace {
 
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
