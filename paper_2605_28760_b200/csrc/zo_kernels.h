@@ -21,6 +21,19 @@ void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const 
 void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
                    bool bf16, const float* Pplus, const float* Pminus, int r, int rows_per_sign, int ext_terms,
                    long vstride, cudaStream_t st);
+// LN from the residual GEMM's statistics (EPI_RESID32_LN, see zo_kernels.cu): per LN job
+// and probe sign the row-independent G_k = sum gamma P_k, B_k = sum beta P_k
+struct LnConstJob {
+  const float* g;    // gamma (+ copy; the -eps copy is g + vstride)
+  const float* b;    // beta
+  const float* Pp;   // consumer GEMM's P+ / P- ([d, r])
+  const float* Pm;
+  float* out;        // [2 signs][G_0..G_{r-1}, B_0..B_{r-1}]
+};
+void launch_ln_consts(const LnConstJob* jobs_dev, int njobs, int d, int r, long vstride, cudaStream_t st);
+void launch_ln_apply(const float* x32, const float* stats, int ntiles, int ld, const float* gamma, const float* beta,
+                     long vstride, const float* consts, int M, int d, void* out, int ldo, bool bf16, int r,
+                     int rows_per_sign, int ext_terms, cudaStream_t st);
 // ext columns for a 16-bit activation a[:, :K] already in place (ctx -> attn_out, gelu -> ff_down).
 void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, const float* Pminus, int r,
                 int rows_per_sign, int ext_terms, cudaStream_t st);
@@ -38,6 +51,10 @@ void launch_attention(const void* qkv, int ldq, void* ctx, int ldc, int nseq, in
 // t_k = sum over tiles of tpart[tile][row][k] (fixed order) -> ext columns (hi, lo, hi) of a[:, K:]
 void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
                          int ext_terms, bool bf16, cudaStream_t st);
+// dst row i = src row of the i-th scored (sign, sequence, option token): the compact
+// rows the last layer's pruned tail runs on (row_bytes, strides in bytes)
+void launch_gather_scored(const void* src, size_t ld_src_bytes, void* dst, size_t ld_dst_bytes, int row_bytes,
+                          int nsign, int B, int T, int prompt_len, int Lopt, cudaStream_t st);
 // final LN at scored rows (prompt_len-1+j) of B sequences (both signs counted) -> xs32/xs16, z = xs . V_e
 void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d,
                      int prompt_len, int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r,

@@ -1,0 +1,61 @@
+"""BASELINE config 4: an OPT-13B-shaped LoZO run through the public API
+(run_serving_path: host minibatches, device step, folds every nu, async U/V digests,
+dev evals), writing the trajectory in the reference's JSON-lines format.
+
+    python scripts/long_run.py --model opt-13b --steps 20000 --eval-every 2000 --out gpurun_out/long
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, HERE)
+
+MODELS = {
+    "opt-125m": dict(vocab=50272, dim=768, n_layers=12, n_heads=12),
+    "opt-1.3b": dict(vocab=50272, dim=2048, n_layers=24, n_heads=32),
+    "opt-6.7b": dict(vocab=50272, dim=4096, n_layers=32, n_heads=32),
+    "opt-13b": dict(vocab=50272, dim=5120, n_layers=40, n_heads=40),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="opt-13b", choices=sorted(MODELS))
+    ap.add_argument("--steps", type=int, default=20000)
+    ap.add_argument("--eval-every", type=int, default=2000)
+    ap.add_argument("--dev-size", type=int, default=64)
+    ap.add_argument("--lr", type=float, default=1e-7)
+    ap.add_argument("--out", default="gpurun_out/long")
+    a = ap.parse_args()
+    from paper_2605_28760_b200 import model as M
+    from paper_2605_28760_b200.runtime import run_serving_path
+    from paper_2605_28760_b200.zo_engine import ZoConfig, write_trajectory
+    mdl = MODELS[a.model]
+    mcfg = M.ModelConfig(prompt_len=63, init_seed=7, init_scale=0.02, **mdl)
+    task = M.generate_task(M.TaskConfig(seed=11, vocab=mdl["vocab"], prompt_len=63, train_size=1000,
+                                        dev_size=a.dev_size, val_size=8))
+    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=a.lr, rank=2, nu=50, batch_size=16)
+    t0 = time.perf_counter()
+    run = run_serving_path(mcfg, task, zcfg, a.steps, precision="fp16", eval_every=a.eval_every,
+                           compute_param_digests=False)
+    wall = time.perf_counter() - t0
+    os.makedirs(a.out, exist_ok=True)
+    write_trajectory(os.path.join(a.out, f"traj_{a.model}_{a.steps}.jsonl"),
+                     {"model": mdl, "steps": a.steps, "zo_digest": zcfg.digest()}, run.trajectory,
+                     {"eval_loss": run.eval_curve[-1].loss, "eval_acc": run.eval_curve[-1].acc})
+    summary = {"model": a.model, "steps": run.steps_completed, "train_wall_s": run.train_wall_s,
+               "steps_per_s_train": run.steps_completed / run.train_wall_s, "total_wall_s": wall,
+               "meter": run.meter.to_dict(), "eval_curve": [p.to_dict() for p in run.eval_curve],
+               "last_record": run.trajectory[-1].to_dict()}
+    with open(os.path.join(a.out, f"summary_{a.model}_{a.steps}.json"), "w") as f:
+        json.dump(summary, f, indent=1)
+    print(json.dumps({k: summary[k] for k in ("model", "steps", "train_wall_s", "steps_per_s_train")}))
+
+
+if __name__ == "__main__":
+    main()
