@@ -196,10 +196,6 @@ struct GemmParams {
   const float* xPm;
   int xr, xrps, tpart_ld;
   float* tpart;
-  // EPI_RESID32_LN: the next LN's gamma (+ copy; the -eps rows read lng + lng_vstride);
-  // xPp/xPm/xr/xrps are the consumer GEMM's P+-, tpart/tpart_ld the statistics slabs
-  const float* lng;
-  long lng_vstride;
   // stream-K tail (sk = 1): unit u (a CTA, or a CTA pair when CG = 2) owns the global
   // k-iterations [sk_dp*num_kb + u*sk_w, +sk_w) of the tiles past the data-parallel
   // waves.  A segment that starts after the tile's first k-block publishes its fp32
@@ -487,30 +483,8 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
       for (int k = 0; k < 8; ++k) tp[k] = 0.f;
       const float* xP = nullptr;
-      if constexpr (EPI == EPI_GELU16_EXT || EPI == EPI_RESID32_LN) xP = (row < p.xrps) ? p.xPp : p.xPm;
-      constexpr bool RESID = (EPI == EPI_RESID32 || EPI == EPI_RESID32_LN);
-      // EPI_RESID32_LN: per-row statistics of the NEW residual over this tile's columns --
-      // sum x, sum x^2 and sum x * gamma * P_k -- from which k_ln_apply forms the next LN
-      // and its extension columns without a row reduction (zo_kernels.cu)
-      float ls1 = 0.f, ls2 = 0.f;
-      const float* lg = nullptr;
-      if constexpr (EPI == EPI_RESID32_LN) lg = p.lng + ((row < p.xrps) ? 0 : p.lng_vstride);
-      auto ln_acc = [&](float xn, int col) {
-        if constexpr (EPI == EPI_RESID32_LN) {
-          ls1 += xn;
-          ls2 += xn * xn;
-          const float gx = xn * lg[col];
-          if constexpr (XR > 0 && XR < 8) {
-#pragma unroll
-            for (int k = 0; k < XR; ++k) tp[k] += gx * xP[(size_t)col * XR + k];
-          } else if constexpr (XR == 8) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (k < p.xr) tp[k] += gx * xP[(size_t)col * p.xr + k];
-          }
-        }
-      };
-      if constexpr (RESID) {
+      if constexpr (EPI == EPI_GELU16_EXT) xP = (row < p.xrps) ? p.xPp : p.xPm;
+      if constexpr (EPI == EPI_RESID32) {
         // fast path: whole tile row in range -> residual loads for chunk c+1 are in
         // flight while chunk c is added and stored
         const size_t lin0 = (size_t)row * p.ldo + n0;
@@ -530,18 +504,10 @@ __global__ void __launch_bounds__(192, 1)
             tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
             if (split) add_partials(v, c);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 xn = make_float4(v[4 * j] + xa[j].x, v[4 * j + 1] + xa[j].y, v[4 * j + 2] + xa[j].z,
-                                            v[4 * j + 3] + xa[j].w);
-              reinterpret_cast<float4*>(o + c)[j] = xn;
-              if constexpr (EPI == EPI_RESID32_LN) {
-                const int cc = n0 + c + 4 * j;
-                ln_acc(xn.x, cc);
-                ln_acc(xn.y, cc + 1);
-                ln_acc(xn.z, cc + 2);
-                ln_acc(xn.w, cc + 3);
-              }
-            }
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4*>(o + c)[j] =
+                  make_float4(v[4 * j] + xa[j].x, v[4 * j + 1] + xa[j].y, v[4 * j + 2] + xa[j].z,
+                              v[4 * j + 3] + xa[j].w);
 #pragma unroll
             for (int j = 0; j < 8; ++j) xa[j] = xb[j];
           }
@@ -599,37 +565,29 @@ __global__ void __launch_bounds__(192, 1)
           float* o = reinterpret_cast<float*>(p.out) + lin;
           if (full) {
             float4 xr4[8];
-            if constexpr (RESID) {
+            if constexpr (EPI == EPI_RESID32) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) xr4[j] = reinterpret_cast<const float4*>(o)[j];
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               float4 w = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-              if constexpr (RESID) {
+              if constexpr (EPI == EPI_RESID32) {
                 w.x += xr4[j].x;
                 w.y += xr4[j].y;
                 w.z += xr4[j].z;
                 w.w += xr4[j].w;
               }
               reinterpret_cast<float4*>(o)[j] = w;
-              if constexpr (EPI == EPI_RESID32_LN) {
-                ln_acc(w.x, col0 + 4 * j);
-                ln_acc(w.y, col0 + 4 * j + 1);
-                ln_acc(w.z, col0 + 4 * j + 2);
-                ln_acc(w.w, col0 + 4 * j + 3);
-              }
             }
           } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) {
               if (col0 + i < p.N) {
-                if constexpr (RESID) {
+                if constexpr (EPI == EPI_RESID32)
                   o[i] += v[i];
-                  if constexpr (EPI == EPI_RESID32_LN) ln_acc(o[i], col0 + i);
-                } else {
+                else
                   o[i] = v[i];
-                }
               }
             }
           }
@@ -640,15 +598,6 @@ __global__ void __launch_bounds__(192, 1)
         named_bar_sync(1, 128);
         if (warp == 2 && lane < jend - jfirst)  // re-arm the consumed flags for the next launch
           for (int j = jfirst + lane; j < jend; j += 32) p.sk_flags[j * CG + (int)rank] = 0u;
-      }
-      if constexpr (EPI == EPI_RESID32_LN) {
-        if (row_ok) {
-          const int xs = 2 + p.xr;
-          float* dst = p.tpart + ((size_t)(n0 / BN) * p.tpart_ld + row) * xs;
-          dst[0] = ls1;
-          dst[1] = ls2;
-          for (int k = 0; k < p.xr && k < 8; ++k) dst[2 + k] = tp[k];
-        }
       }
       if constexpr (EPI == EPI_GELU16_EXT) {
         if (row_ok) {
@@ -790,8 +739,6 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.xrps = g.xrps;
   p.tpart_ld = g.tpart_ld;
   p.tpart = g.tpart;
-  p.lng = g.lng;
-  p.lng_vstride = g.lng_vstride;
   p.sk = g.sk;
   p.sk_w = g.sk_w;
   p.sk_dp = g.sk_dp;
@@ -830,13 +777,6 @@ static void launch_e(const GemmDesc& g, cudaStream_t st) {
       else launch_t<BN, EPI_GELU16_EXT, BF16, 8, CG>(g, st);
       break;
     case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16, 0, CG>(g, st); break;
-    case EPI_RESID32_LN:
-      if (g.xr == 0) launch_t<BN, EPI_RESID32_LN, BF16, 0, CG>(g, st);
-      else if (g.xr == 1) launch_t<BN, EPI_RESID32_LN, BF16, 1, CG>(g, st);
-      else if (g.xr == 2) launch_t<BN, EPI_RESID32_LN, BF16, 2, CG>(g, st);
-      else if (g.xr == 4) launch_t<BN, EPI_RESID32_LN, BF16, 4, CG>(g, st);
-      else launch_t<BN, EPI_RESID32_LN, BF16, 8, CG>(g, st);
-      break;
     default: launch_t<BN, EPI_STORE32, BF16, 0, CG>(g, st); break;
   }
 }

@@ -13,8 +13,6 @@ enum EpiKind : int {
   EPI_STORE32 = 3,  // out32[r, c] = acc                       (LM-head logits rows)
   EPI_GELU16_EXT = 4,  // EPI_GELU16 + per-tile partial t_k = sum_c a16[r,c] P[c,k] for the
                        // next GEMM's LoRA K-extension (tpart[n_tile][r][k], deterministic)
-  EPI_RESID32_LN = 5,  // EPI_RESID32 + per-tile statistics of the new residual for the next LN:
-                       // [sum x, sum x^2, sum_c x*gamma[c]*P[c,k]] -> tpart[n_tile][r][2 + xr]
 };
 
 // D[M, N] = A[M, Kp] * B[N, Kp]^T, both operands K-major 16-bit, fp32 accumulate.
@@ -36,9 +34,6 @@ struct GemmDesc {
   const float* xPm = nullptr;
   int xr = 0, xrps = 0, tpart_ld = 0;
   float* tpart = nullptr;
-  // EPI_RESID32_LN only (xPp/xPm/xr/xrps/tpart/tpart_ld as above)
-  const float* lng = nullptr;
-  long lng_vstride = 0;
   // stream-K split of the k-iteration space over the persistent CTAs (gemm_enable_streamk)
   int sk = 0, sk_w = 0, sk_dp = 0;
   float* sk_ws = nullptr;       // [grid][128][bn] fp32 partials of split tiles

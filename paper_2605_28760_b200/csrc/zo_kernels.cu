@@ -397,109 +397,6 @@ void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int 
                                           ext_terms, vstride);
 }
 
-// ------------------------------------------------------------------ LN from epilogue statistics
-// The residual GEMM before an LN (attn_out -> LN2, ff_down -> next LN1) leaves per
-// (n-tile, row) partials [sum x, sum x^2, sum x*gamma*P_k] (EPI_RESID32_LN); the LN
-// then needs no row reduction: mu = S1/d, var = S2/d - mu^2 (combined in float64),
-// h = (x - mu) * rsd * gamma + beta, and the extension dots
-// t_k = sum_i h_i P_ik = rsd * (Q_k - mu * G_k) + B_k with the row-independent
-// G_k = sum_i gamma_i P_ik, B_k = sum_i beta_i P_ik (k_ln_consts, per probe sign).
-
-// one CTA per (LN job, sign): G_k and B_k over d, fixed-order block reduction
-__global__ void __launch_bounds__(256) k_ln_consts(const LnConstJob* __restrict__ jobs, int d, int r, long vstride) {
-  pdl_launch_dependents();
-  pdl_wait();
-  __shared__ float red[32 * 16];
-  const LnConstJob jb = jobs[blockIdx.x];
-  const int sgn = blockIdx.y;
-  const float* g = jb.g + (sgn ? vstride : 0);
-  const float* b = jb.b + (sgn ? vstride : 0);
-  const float* P = sgn ? jb.Pm : jb.Pp;
-  float acc[16];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) acc[k] = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x)
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (k < r) {
-        acc[k] += g[i] * P[(size_t)i * r + k];
-        acc[8 + k] += b[i] * P[(size_t)i * r + k];
-      }
-  block_sum<16>(acc, red);
-  if (threadIdx.x < 2 * r) {
-    const int k = threadIdx.x % r, which = threadIdx.x / r;
-    jb.out[(size_t)sgn * 2 * r + threadIdx.x] = acc[which * 8 + k];
-  }
-}
-
-void launch_ln_consts(const LnConstJob* jobs, int njobs, int d, int r, long vstride, cudaStream_t st) {
-  if (r < 1 || r > 8 || njobs < 1) return;
-  launch_pdl(k_ln_consts, dim3(njobs, 2), dim3(256), 0, st, jobs, d, r, vstride);
-}
-
-template <int XR>
-__global__ void __launch_bounds__(256) k_ln_apply(const float* __restrict__ x32, const float* __restrict__ stats,
-                                                  int ntiles, int ld, const float* __restrict__ g,
-                                                  const float* __restrict__ bta, long vstride,
-                                                  const float* __restrict__ consts, int d, void* __restrict__ out,
-                                                  int ldo, bool bf16, int rows_per_sign, int ext_terms) {
-  pdl_launch_dependents();
-  pdl_wait();
-  __shared__ float sh[2 + 8];
-  const int row = blockIdx.x;
-  const int sgn = row < rows_per_sign ? 0 : 1;
-  constexpr int XS = 2 + XR;
-  if (threadIdx.x < 32) {
-    // lane j sums the tiles j, j+32, ... in double; then a fixed xor tree
-    double a[XS];
-#pragma unroll
-    for (int k = 0; k < XS; ++k) a[k] = 0.0;
-    for (int t = threadIdx.x; t < ntiles; t += 32) {
-      const float* st = stats + ((size_t)t * ld + row) * XS;
-#pragma unroll
-      for (int k = 0; k < XS; ++k) a[k] += (double)st[k];
-    }
-#pragma unroll
-    for (int k = 0; k < XS; ++k)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a[k] += __shfl_xor_sync(0xffffffffu, a[k], o);
-    if (threadIdx.x == 0) {
-      const double mu = a[0] / d;
-      const double var = fmax(a[1] / d - mu * mu, 0.0);
-      const float rsd = 1.0f / sqrtf((float)var + 1e-5f);
-      sh[0] = (float)mu;
-      sh[1] = rsd;
-      const float* cst = consts + (size_t)sgn * 2 * XR;  // [G_0..G_{r-1}, B_0..B_{r-1}]
-#pragma unroll
-      for (int k = 0; k < XR; ++k) sh[2 + k] = (float)((double)rsd * (a[2 + k] - mu * (double)cst[k]) + cst[XR + k]);
-    }
-  }
-  __syncthreads();
-  const float mu = sh[0], rsd = sh[1];
-  const float4* x = reinterpret_cast<const float4*>(x32 + (size_t)row * d);
-  const float4* g4 = reinterpret_cast<const float4*>(g + (sgn ? vstride : 0));
-  const float4* b4 = reinterpret_cast<const float4*>(bta + (sgn ? vstride : 0));
-  for (int i = threadIdx.x; i < (d >> 2); i += blockDim.x) {
-    const float4 v = x[i], gg = g4[i], bb = b4[i];
-    store4_16(out, (size_t)row * ldo + 4 * i, (v.x - mu) * rsd * gg.x + bb.x, (v.y - mu) * rsd * gg.y + bb.y,
-              (v.z - mu) * rsd * gg.z + bb.z, (v.w - mu) * rsd * gg.w + bb.w, bf16);
-  }
-  if (threadIdx.x < XR) write_ext(out, (size_t)row * ldo + d, threadIdx.x, sh[2 + threadIdx.x], ext_terms, bf16);
-}
-
-void launch_ln_apply(const float* x32, const float* stats, int ntiles, int ld, const float* gamma, const float* beta,
-                     long vstride, const float* consts, int M, int d, void* out, int ldo, bool bf16, int r,
-                     int rows_per_sign, int ext_terms, cudaStream_t st) {
-  if (d % 4 || ldo % 4) throw Error(ZO_ERR_DIMENSION, "LN rows must be multiples of 4");
-  switch (r) {
-#define ZO_LNA(R) \
-  case R: launch_pdl(k_ln_apply<R>, dim3(M), dim3(256), 0, st, x32, stats, ntiles, ld, gamma, beta, vstride, consts, d, out, ldo, bf16, rows_per_sign, ext_terms); return;
-    ZO_LNA(0) ZO_LNA(1) ZO_LNA(2) ZO_LNA(3) ZO_LNA(4) ZO_LNA(5) ZO_LNA(6) ZO_LNA(7) ZO_LNA(8)
-#undef ZO_LNA
-    default: throw Error(ZO_ERR_DIMENSION, "statistics LN supports rank <= 8");
-  }
-}
-
 // ------------------------------------------------------------------ extension of a 16-bit activation
 // t_k = a[row, :K] . P_s[:, k] -> ext columns, one warp per row, 16-byte loads.
 __global__ void __launch_bounds__(256) k_ext(void* __restrict__ a, int lda, int M, int K, bool bf16,

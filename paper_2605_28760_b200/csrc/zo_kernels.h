@@ -21,19 +21,6 @@ void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const 
 void launch_ln_ext(const float* x32, const float* gamma, const float* beta, int M, int d, void* out, int ldo,
                    bool bf16, const float* Pplus, const float* Pminus, int r, int rows_per_sign, int ext_terms,
                    long vstride, cudaStream_t st);
-// LN from the residual GEMM's statistics (EPI_RESID32_LN, see zo_kernels.cu): per LN job
-// and probe sign the row-independent G_k = sum gamma P_k, B_k = sum beta P_k
-struct LnConstJob {
-  const float* g;    // gamma (+ copy; the -eps copy is g + vstride)
-  const float* b;    // beta
-  const float* Pp;   // consumer GEMM's P+ / P- ([d, r])
-  const float* Pm;
-  float* out;        // [2 signs][G_0..G_{r-1}, B_0..B_{r-1}]
-};
-void launch_ln_consts(const LnConstJob* jobs_dev, int njobs, int d, int r, long vstride, cudaStream_t st);
-void launch_ln_apply(const float* x32, const float* stats, int ntiles, int ld, const float* gamma, const float* beta,
-                     long vstride, const float* consts, int M, int d, void* out, int ldo, bool bf16, int r,
-                     int rows_per_sign, int ext_terms, cudaStream_t st);
 // ext columns for a 16-bit activation a[:, :K] already in place (ctx -> attn_out, gelu -> ff_down).
 void launch_ext(void* a, int lda, int M, int K, bool bf16, const float* Pplus, const float* Pminus, int r,
                 int rows_per_sign, int ext_terms, cudaStream_t st);

@@ -135,11 +135,6 @@ struct zo_ctx {
   std::map<int, RowPlan> plans;  // keyed by 2*M + (nsign == 1)
   float* tpart = nullptr;         // fused LoRA-extension partials [tiles][Mpad][r]
   uint16_t* P16T = nullptr;       // high-rank extension B operands [2][su] (per matrix [r][m])
-  // LN from residual-GEMM statistics (EPI_RESID32_LN + k_ln_apply); ZO_LNSTATS=0 disables
-  bool ln_stats = true;
-  float* lnstats = nullptr;  // [n_tiles][Mpad][2 + r_ext]
-  float* lnconst = nullptr;  // [2L jobs][2 signs][2 r]
-  LnConstJob* d_lnjobs = nullptr;
   float* sk_ws = nullptr;         // stream-K partial tiles
   unsigned* sk_flags = nullptr;
   bool streamk = true;  // DP waves + stream-K tail where it pays (ZO_STREAMK=0 disables)
@@ -251,8 +246,8 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
     const Matrix& w = c->mats[c->i_down[l]];
     gemm_plan(lp.qkv, c->hA, M, ldh, q.W16, 3 * d, q.ldw, d + c->ext_used, EPI_STORE16, c->bf16, c->qkv, 3 * d,
               c->num_sms);
-    gemm_plan(lp.out, c->ctxA, M, ldh, o.W16, d, o.ldw, d + c->ext_used, c->ln_stats ? EPI_RESID32_LN : EPI_RESID32,
-              c->bf16, c->x32, d, c->num_sms);
+    gemm_plan(lp.out, c->ctxA, M, ldh, o.W16, d, o.ldw, d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
+              c->num_sms);
     gemm_plan(lp.up, c->hA, M, ldh, u.W16, 4 * d, u.ldw, d + c->ext_used,
               c->fused_ext ? EPI_GELU16_EXT : EPI_GELU16, c->bf16, c->gA, ldg, c->num_sms);
     if (c->fused_ext) {
@@ -264,23 +259,8 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
       lp.up.tpart = c->tpart;
       check((4 * d + lp.up.bn - 1) / lp.up.bn <= c->tpart_tiles, ZO_ERR_INTERNAL, "tpart too small");
     }
-    const bool down_stats = c->ln_stats && l + 1 < c->d.n_layers;
-    gemm_plan(lp.down, c->gA, M, ldg, w.W16, d, w.ldw, 4 * d + c->ext_used,
-              down_stats ? EPI_RESID32_LN : EPI_RESID32, c->bf16, c->x32, d, c->num_sms);
-    // statistics for the LN that consumes this residual: LN2 (ff_up's P) after attn_out,
-    // the next layer's LN1 (its qkv's P) after ff_down
-    auto stats_for = [&](GemmDesc& g, float* gamma, const Matrix& consumer) {
-      g.lng = gamma;
-      g.lng_vstride = c->vstride;
-      g.xPp = c->Pp + consumer.u_off;
-      g.xPm = c->Pm + consumer.u_off;
-      g.xr = c->fused_ext ? c->r : 0;
-      g.xrps = M / nsign;
-      g.tpart = c->lnstats;
-      g.tpart_ld = c->Mpad;
-    };
-    if (c->ln_stats) stats_for(lp.out, c->ln2g[l], u);
-    if (down_stats) stats_for(lp.down, c->ln1g[l + 1], c->mats[c->i_qkv[l + 1]]);
+    gemm_plan(lp.down, c->gA, M, ldg, w.W16, d, w.ldw, 4 * d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
+              c->num_sms);
     if (c->streamk)
       for (GemmDesc* g : {&lp.qkv, &lp.out, &lp.up, &lp.down}) gemm_enable_streamk(*g, c->sk_ws, c->sk_flags, c->num_sms);
     if (!c->fused_ext) {
@@ -357,24 +337,14 @@ void do_score(zo_ctx* c, int B, int nsign) {
   auto ext_gemm = [&](const LayerPlan& lp, int i) {
     for (int sg = 0; sg < nsign; ++sg) gemm_launch(lp.ext[2 * i + sg], c->st);
   };
-  const int rx = c->fused_ext ? c->r : 0;
-  if (c->ln_stats && rx > 0) launch_ln_consts(c->d_lnjobs, 2 * c->d.n_layers, d, rx, c->vstride, c->st);
-  auto ln_from_stats = [&](const GemmDesc& prod, int job, float* gamma, float* beta) {
-    launch_ln_apply(c->x32, c->lnstats, (d + prod.bn - 1) / prod.bn, c->Mpad, gamma, beta, c->vstride,
-                    c->lnconst + (size_t)job * 4 * std::max(rx, 1), M, d, c->hA, ldh, c->bf16, rx, rps,
-                    c->ext_terms, c->st);
-  };
   for (int l = 0; l < c->d.n_layers; ++l) {
     const Matrix& q = c->mats[c->i_qkv[l]];
     const Matrix& o = c->mats[c->i_out[l]];
     const Matrix& u = c->mats[c->i_up[l]];
     const Matrix& w = c->mats[c->i_down[l]];
     const LayerPlan& lp = rp.layers[l];
-    if (c->ln_stats && l > 0)
-      ln_from_stats(rp.layers[l - 1].down, 2 * l, c->ln1g[l], c->ln1b[l]);
-    else
-      launch_ln_ext(c->x32, c->ln1g[l], c->ln1b[l], M, d, c->hA, ldh, c->bf16, c->Pp + q.u_off, c->Pm + q.u_off,
-                    c->fused_ext ? c->r : 0, rps, c->ext_terms, c->vstride, c->st);
+    launch_ln_ext(c->x32, c->ln1g[l], c->ln1b[l], M, d, c->hA, ldh, c->bf16, c->Pp + q.u_off, c->Pm + q.u_off,
+                  c->fused_ext ? c->r : 0, rps, c->ext_terms, c->vstride, c->st);
     if (!c->fused_ext) ext_gemm(lp, 0);
     gemm_launch(lp.qkv, c->st);
     AttnExt ax;
@@ -410,11 +380,8 @@ void do_score(zo_ctx* c, int B, int nsign) {
     else
       ext_gemm(lp, 1);
     gemm_launch(lp.out, c->st);
-    if (c->ln_stats)
-      ln_from_stats(lp.out, 2 * l + 1, c->ln2g[l], c->ln2b[l]);
-    else
-      launch_ln_ext(c->x32, c->ln2g[l], c->ln2b[l], M, d, c->hA, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off,
-                    c->fused_ext ? c->r : 0, rps, c->ext_terms, c->vstride, c->st);
+    launch_ln_ext(c->x32, c->ln2g[l], c->ln2b[l], M, d, c->hA, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off,
+                  c->fused_ext ? c->r : 0, rps, c->ext_terms, c->vstride, c->st);
     if (!c->fused_ext) ext_gemm(lp, 2);
     gemm_launch(lp.up, c->st);
     if (c->fused_ext)
@@ -652,23 +619,6 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->tpart_tiles = std::max((int)ceil_div(4 * D, 64), d.n_heads);
   if (c->fused_ext) c->tpart = c->mem.get<float>((size_t)c->tpart_tiles * c->Mpad * d.rank);
   else c->P16T = c->mem.get<uint16_t>((size_t)2 * c->su);
-  if (const char* e = std::getenv("ZO_LNSTATS")) c->ln_stats = std::atoi(e) != 0;
-  {
-    const int rx = c->fused_ext ? d.rank : 0;
-    c->lnstats = c->mem.get<float>((size_t)(ceil_div(D, 64) + 1) * c->Mpad * (2 + rx));
-    c->lnconst = c->mem.get<float>((size_t)2 * d.n_layers * 4 * std::max(rx, 1));
-    std::vector<LnConstJob> jobs(2 * d.n_layers);
-    for (int l = 0; l < d.n_layers; ++l) {
-      const Matrix& q = c->mats[c->i_qkv[l]];
-      const Matrix& u = c->mats[c->i_up[l]];
-      jobs[2 * l] = {c->ln1g[l], c->ln1b[l], c->Pp + q.u_off, c->Pm + q.u_off,
-                     c->lnconst + (size_t)(2 * l) * 4 * std::max(rx, 1)};
-      jobs[2 * l + 1] = {c->ln2g[l], c->ln2b[l], c->Pp + u.u_off, c->Pm + u.u_off,
-                         c->lnconst + (size_t)(2 * l + 1) * 4 * std::max(rx, 1)};
-    }
-    c->d_lnjobs = c->mem.get<LnConstJob>(jobs.size());
-    ZO_CUDA_TRY(cudaMemcpy(c->d_lnjobs, jobs.data(), jobs.size() * sizeof(LnConstJob), cudaMemcpyHostToDevice));
-  }
   // positional table: pos_encoding(T, d) (model.py:128-136), float64 -> float32
   {
     std::vector<float> pe((size_t)c->T * d.dim);

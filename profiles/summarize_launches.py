@@ -12,4 +12,5 @@ def summarize(path, top=25):
     tot=sum(v[1] for v in agg.values())
     print('launches',len(data),'total us',tot/1e3)
     for k,(n,v) in sorted(agg.items(), key=lambda x:-x[1][1])[:top]: print(f"{k:60s} {n:5d} {v/1e3:10.1f} us  avg {v/1e3/n:8.1f} us {100*v/tot:5.1f}%")
-if __name__=='__main__': summarize(sys.argv[1])
+if __name__=="__main__":
+    import signal; signal.signal(signal.SIGPIPE, signal.SIG_DFL); summarize(sys.argv[1])
