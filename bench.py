@@ -133,8 +133,9 @@ def ncu_traffic(model):
 
 
 def launches_per_step(L: int, n_mats: int, window: bool) -> int:
-    # set_step + sampler(U) 5 + prep + embed + 9/layer + final LN + LM GEMM + loss + coefficient + update
-    n = 1 + 5 + 1 + 1 + 9 * L + 4 + 1
+    # set_step + sampler(U) 5 + prep + embed + 9/layer (+2 gathers of the pruned last layer)
+    # + final LN + LM GEMM + loss + coefficient + update
+    n = 1 + 5 + 1 + 1 + 9 * L + 2 + 4 + 1
     if window:
         n += 5 + n_mats + n_mats  # sampler(V) + V extension writes + fold kernels
     return n
@@ -345,9 +346,10 @@ def main():
     ms_step = ms / args.steps
     value = 1000.0 * G / ms_step  # reference steps (ZO directions) per second, whole job
     windows = sum(1 for t in range(args.warmup, nsteps) if (t * G) % zcfg.nu == 0)
-    launches = args.steps * (launches_per_step(mcfg.n_layers, 4 * mcfg.n_layers + 1, False)
-                             + (G - 1) * 6) + windows * (
-        5 + 2 * (4 * mcfg.n_layers + 1))
+    per_step, per_window = eng.graph_kernel_count()
+    if not (world == 1 and args.graph) or per_step <= 1:
+        per_step = launches_per_step(mcfg.n_layers, 4 * mcfg.n_layers + 1, False)  # eager paths: estimate
+    launches = args.steps * (per_step + (G - 1) * 6) + (0 if fact else windows * per_window)
 
     hbm_peak, tf_peak, peak_kind = peaks()
     cfg, scaling, _ = workload_config(args, world)

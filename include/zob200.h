@@ -151,6 +151,9 @@ int zo_step_score_async(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, d
                         const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B);
 int zo_step_apply_async(zo_ctx* ctx, double epsilon, double lr, int32_t divide_by_r, int32_t B_total);
 int zo_read_out4(zo_ctx* ctx, double* out4);
+/* kernels one zo_step_graph replay launches (+ the eager step-index write), and the
+ * window-start launches in front of it (V sampler, extension columns, fold) */
+int zo_graph_kernel_count(zo_ctx* ctx, int32_t* per_step, int32_t* per_window);
 /* q-direction mode (SURVEY.md §8(e) mode 2; no reference counterpart -- the
  * reference has no multi-query estimator): rank g of G scores
  * reference step s = macro_step*G + g (its U, V window and minibatch) at the

@@ -74,6 +74,7 @@ SIGNATURES = [
                                        _c.c_int32]),
     ("zo_step_apply_async", _c.c_int, [_P, _c.c_double, _c.c_double, _c.c_int32, _c.c_int32]),
     ("zo_read_out4", _c.c_int, [_P, _P]),
+    ("zo_graph_kernel_count", _c.c_int, [_P, _c.POINTER(_c.c_int32), _c.POINTER(_c.c_int32)]),
     ("zo_qdir_score_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_int32, _c.c_int32,
                                        _c.c_double, _c.c_double, _c.c_int32, _P, _P, _c.c_int32]),
     ("zo_out4_io", _c.c_int, [_P, _P, _c.c_int32]),

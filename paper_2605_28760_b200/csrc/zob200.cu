@@ -159,6 +159,7 @@ struct zo_ctx {
     }
   } gkey{};
   bool gkey_valid = false;
+  int graph_kernels = 0;  // kernel nodes of the captured step body
 
   ~zo_ctx() {
     if (gexec) cudaGraphExecDestroy(gexec);
@@ -1193,6 +1194,20 @@ extern "C" int zo_step_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu
     }
     c->st = user;
     ZO_CUDA_TRY(cudaGraphInstantiate(&c->gexec, graph, 0));
+    {
+      // kernels per replay (the bench's gpu_launches claim counts them from here)
+      size_t n = 0;
+      ZO_CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &n));
+      std::vector<cudaGraphNode_t> nodes(n);
+      ZO_CUDA_TRY(cudaGraphGetNodes(graph, nodes.data(), &n));
+      int k = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType ty;
+        ZO_CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
+        k += ty == cudaGraphNodeTypeKernel;
+      }
+      c->graph_kernels = k;
+    }
     ZO_CUDA_TRY(cudaGraphDestroy(graph));
     c->gkey = key;
     c->gkey_valid = true;
@@ -1200,6 +1215,16 @@ extern "C" int zo_step_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu
     ZO_CUDA_TRY(cudaGraphLaunch(c->gexec, c->st));
   }
   if (lozo) c->a_dirty = true;
+  return ZO_OK;
+  ZO_API_END
+}
+
+// kernels launched per zo_step_graph replay (0 before the first capture), and per
+// window start in front of it (V sampler + extension columns + fold)
+extern "C" int zo_graph_kernel_count(zo_ctx* c, int32_t* per_step, int32_t* per_window) {
+  ZO_API_BEGIN
+  *per_step = c->graph_kernels + 1;  // + the eager step-index write (k_set_u64)
+  *per_window = 5 + 2 * (int32_t)c->mats.size();
   return ZO_OK;
   ZO_API_END
 }

@@ -266,6 +266,12 @@ class ZoEngine:
     def fold_async(self) -> None:
         check(lib().zo_fold_async(self._h))
 
+    def graph_kernel_count(self) -> tuple[int, int]:
+        """(kernels per step_graph replay, kernels per window start)."""
+        a, b = ctypes.c_int32(), ctypes.c_int32()
+        check(lib().zo_graph_kernel_count(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
     def read_out4(self) -> np.ndarray:
         out = np.empty(4)
         check(lib().zo_read_out4(self._h, out.ctypes.data))
