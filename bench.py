@@ -230,10 +230,27 @@ def main():
 
     import torch
     rank, world, local = dist_env()
+    # ZO_BENCH_SAME_DEVICE=1 puts every rank on cuda:0 with gloo (a one-GPU functional test
+    # of the N>1 path; timing meaningless) -- the real runs use NCCL, one GPU per rank
+    same_dev = os.environ.get("ZO_BENCH_SAME_DEVICE") == "1"
+    if same_dev:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if same_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def all_gather(out, inp):
+        import torch.distributed as dist
+        if same_dev:  # gloo: exchange through host memory (a few bytes)
+            o = out.cpu()
+            dist.all_gather_into_tensor(o, inp.cpu())
+            out.copy_(o)
+        else:
+            dist.all_gather_into_tensor(out, inp)
     from paper_2605_28760_b200 import model as M
     from paper_2605_28760_b200.adapter import AdapterState
     from paper_2605_28760_b200.engine import ZoEngine
@@ -295,7 +312,7 @@ def main():
             import torch.distributed as dist
             eng.qdir_score_async(zcfg.seed, t, G, rank, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, B)
             eng.out4_io(out4_local.data_ptr(), False)
-            dist.all_gather_into_tensor(out4_all, out4_local)  # 32 B per rank
+            all_gather(out4_all, out4_local)  # 32 B per rank
             eng.qdir_apply_async(zcfg.seed, t, G, zcfg.learning_rate, out4_all.data_ptr())
             if not fact and ((t + 1) * G) % zcfg.nu == 0:
                 eng.fold_async()
@@ -309,7 +326,7 @@ def main():
             import torch.distributed as dist
             eng.step_score_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, tp, gp, Bl)
             eng.nll_io(nll_local.data_ptr(), 2 * Bl, False)
-            dist.all_gather_into_tensor(nll_all, nll_local)
+            all_gather(nll_all, nll_local)
             # [rank][sign][b] -> [sign][rank*Bl + b] (canonical example order)
             full = nll_all.view(world, 2, Bl).transpose(0, 1).contiguous()
             eng.nll_io(full.data_ptr(), 2 * B, True)
@@ -338,9 +355,19 @@ def main():
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     out4 = eng.read_out4()
+    replicas_identical = None
+    if world > 1:
+        # every replica must hold the identical window A after the run (no weight traffic)
+        import torch.distributed as dist
+        from paper_2605_28760_b200.engine import A as SLOT_A
+        dg = torch.tensor([eng.digest(SLOT_A) & ((1 << 62) - 1)], dtype=torch.int64,
+                          device="cpu" if same_dev else "cuda")
+        allg = [torch.zeros_like(dg) for _ in range(world)]
+        dist.all_gather(allg, dg)
+        replicas_identical = len({int(x.item()) for x in allg}) == 1
     if world > 1:
         import torch.distributed as dist
-        tt = torch.tensor([ms], device="cuda")
+        tt = torch.tensor([ms], device="cpu" if same_dev else "cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     ms_step = ms / args.steps
@@ -361,6 +388,7 @@ def main():
             "config": cfg,
             "scored_tokens_per_s": value * 2 * B * T, "option_tokens_per_s": value * 2 * B,
             "gpu_launches": launches, "clocks": clk.summary(), "init_s": t_init,
+            **({"replicas_identical": replicas_identical} if world > 1 else {}),
             "last_losses": [float(out4[0]), float(out4[1]), float(out4[2])]}
     dense, total = dense_flops(mcfg.dim, mcfg.n_layers, B, T, mcfg.vocab, args.rank)
     line["step_tflops"] = total / 1e12
