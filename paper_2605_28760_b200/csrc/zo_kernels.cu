@@ -256,84 +256,121 @@ __global__ void __launch_bounds__(256) k_ln_ext_reg(const float* __restrict__ x3
     for (int k = 0; k < XR; ++k) write_ext(out, (size_t)row * ldo + d, k, t[k], ext_terms, bf16);
 }
 
-// CTA per row, 256 threads, NPT float4 per thread in registers: high occupancy,
-// one HBM read of x, block reductions through shared memory.
-template <int NPT, int XR>
+// CTA per R rows (R = 2 when the rows pair up within one probe sign), 256 threads,
+// NPT float4 per thread and row in registers: one HBM read of x, and the LN
+// parameters / probe operand P (2 + r floats per column, the larger share of the
+// bytes a row touches) are loaded once for the R rows, which also share each
+// block-reduction round.
+template <int NPT, int XR, int R>
 __global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, const float* __restrict__ g,
                                                 const float* __restrict__ bta, int d, void* __restrict__ out, int ldo,
                                                 bool bf16, const float* __restrict__ Pp, const float* __restrict__ Pm,
                                                 int rows_per_sign, int ext_terms, long vstride) {
   pdl_launch_dependents();
   pdl_wait();
-  __shared__ float red[8 * (XR + 1)];
-  const int row = blockIdx.x;
+  __shared__ float red[8 * R * (XR + 1)];
+  const int row0 = blockIdx.x * R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const float4* x = reinterpret_cast<const float4*>(x32 + (size_t)row * d);
-  float4 v[NPT];
+  float4 v[R][NPT];
 #pragma unroll
-  for (int j = 0; j < NPT; ++j) v[j] = x[tid + j * blockDim.x];
-  float s = 0.f;
+  for (int rr = 0; rr < R; ++rr) {
+    const float4* x = reinterpret_cast<const float4*>(x32 + (size_t)(row0 + rr) * d);
 #pragma unroll
-  for (int j = 0; j < NPT; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
-  s = warp_sum(s);
-  if (lane == 0) red[warp] = s;
-  __syncthreads();
-  float tot = 0.f;
-  for (int w = 0; w < nw; ++w) tot += red[w];
-  const float mu = tot / (float)d;
-  s = 0.f;
-#pragma unroll
-  for (int j = 0; j < NPT; ++j) {
-    const float a = v[j].x - mu, b = v[j].y - mu, c = v[j].z - mu, e = v[j].w - mu;
-    s += (a * a + b * b) + (c * c + e * e);
+    for (int j = 0; j < NPT; ++j) v[rr][j] = x[tid + j * blockDim.x];
   }
-  s = warp_sum(s);
-  __syncthreads();
-  if (lane == 0) red[warp] = s;
-  __syncthreads();
-  tot = 0.f;
-  for (int w = 0; w < nw; ++w) tot += red[w];
-  const float rsd = 1.0f / sqrtf(tot / (float)d + 1e-5f);
-  const float* P = (row < rows_per_sign) ? Pp : Pm;
+  // block sums of R values per round, fixed order
+  auto bsum = [&](float (&a)[R]) {
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) a[rr] = warp_sum(a[rr]);
+    __syncthreads();  // the previous round's reads of red[] are done
+    if (lane == 0)
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) red[warp * R + rr] = a[rr];
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      float tot = 0.f;
+      for (int w = 0; w < nw; ++w) tot += red[w * R + rr];
+      a[rr] = tot;
+    }
+  };
+  float mu[R], rsd[R];
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) {
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) s += (v[rr][j].x + v[rr][j].y) + (v[rr][j].z + v[rr][j].w);
+    mu[rr] = s;
+  }
+  bsum(mu);
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) {
+    mu[rr] = mu[rr] / (float)d;
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+      const float a = v[rr][j].x - mu[rr], b = v[rr][j].y - mu[rr], c = v[rr][j].z - mu[rr], e = v[rr][j].w - mu[rr];
+      s += (a * a + b * b) + (c * c + e * e);
+    }
+    rsd[rr] = s;
+  }
+  bsum(rsd);
+#pragma unroll
+  for (int rr = 0; rr < R; ++rr) rsd[rr] = 1.0f / sqrtf(rsd[rr] / (float)d + 1e-5f);
+  const bool plus = row0 < rows_per_sign;  // the R rows share one probe sign
+  const float* P = plus ? Pp : Pm;
   // full scope: the -eps probe rows read the second (VectorProbe -1) copy of the LN params
-  const long voff = (row < rows_per_sign) ? 0 : vstride;
+  const long voff = plus ? 0 : vstride;
   const float4* g4 = reinterpret_cast<const float4*>(g + voff);
   const float4* b4 = reinterpret_cast<const float4*>(bta + voff);
-  float t[XR > 0 ? XR : 1];
+  float t[R][XR > 0 ? XR : 1];
 #pragma unroll
-  for (int k = 0; k < XR; ++k) t[k] = 0.f;
+  for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+    for (int k = 0; k < XR; ++k) t[rr][k] = 0.f;
 #pragma unroll
   for (int j = 0; j < NPT; ++j) {
     const int i = tid + j * blockDim.x;
     const float4 gg = g4[i], bb = b4[i];
-    const float h[4] = {(v[j].x - mu) * rsd * gg.x + bb.x, (v[j].y - mu) * rsd * gg.y + bb.y,
-                        (v[j].z - mu) * rsd * gg.z + bb.z, (v[j].w - mu) * rsd * gg.w + bb.w};
-    store4_16(out, (size_t)row * ldo + 4 * i, h[0], h[1], h[2], h[3], bf16);
-    if constexpr (XR == 0) continue;
-    const float4* pr = reinterpret_cast<const float4*>(P + (size_t)(4 * i) * XR);
+    float4 p01 = make_float4(0.f, 0.f, 0.f, 0.f), p23 = p01;
     if constexpr (XR == 2) {
-      const float4 p01 = pr[0], p23 = pr[1];  // P[4i..4i+3][0..1]
-      t[0] += h[0] * p01.x + h[1] * p01.z + h[2] * p23.x + h[3] * p23.z;
-      t[1] += h[0] * p01.y + h[1] * p01.w + h[2] * p23.y + h[3] * p23.w;
-    } else {
+      const float4* pr = reinterpret_cast<const float4*>(P + (size_t)(4 * i) * 2);
+      p01 = pr[0];  // P[4i..4i+1][0..1]
+      p23 = pr[1];  // P[4i+2..4i+3][0..1]
+    }
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
+    for (int rr = 0; rr < R; ++rr) {
+      const float h[4] = {(v[rr][j].x - mu[rr]) * rsd[rr] * gg.x + bb.x, (v[rr][j].y - mu[rr]) * rsd[rr] * gg.y + bb.y,
+                          (v[rr][j].z - mu[rr]) * rsd[rr] * gg.z + bb.z, (v[rr][j].w - mu[rr]) * rsd[rr] * gg.w + bb.w};
+      store4_16(out, (size_t)(row0 + rr) * ldo + 4 * i, h[0], h[1], h[2], h[3], bf16);
+      if constexpr (XR == 2) {
+        t[rr][0] += h[0] * p01.x + h[1] * p01.z + h[2] * p23.x + h[3] * p23.z;
+        t[rr][1] += h[0] * p01.y + h[1] * p01.w + h[2] * p23.y + h[3] * p23.w;
+      } else if constexpr (XR > 0) {
 #pragma unroll
-        for (int k = 0; k < XR; ++k) t[k] += h[e] * P[(size_t)(4 * i + e) * XR + k];
+        for (int e = 0; e < 4; ++e)
+#pragma unroll
+          for (int k = 0; k < XR; ++k) t[rr][k] += h[e] * P[(size_t)(4 * i + e) * XR + k];
+      }
     }
   }
   if constexpr (XR == 0) return;
 #pragma unroll
-  for (int k = 0; k < XR; ++k) t[k] = warp_sum(t[k]);
+  for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+    for (int k = 0; k < XR; ++k) t[rr][k] = warp_sum(t[rr][k]);
   __syncthreads();
   if (lane == 0)
 #pragma unroll
-    for (int k = 0; k < XR; ++k) red[8 + warp * XR + k] = t[k];
+    for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+      for (int k = 0; k < XR; ++k) red[8 * R + (warp * R + rr) * XR + k] = t[rr][k];
   __syncthreads();
-  if (tid < XR) {
+  if (tid < R * XR) {
+    const int rr = tid / XR, k = tid % XR;
     float a = 0.f;
-    for (int w = 0; w < nw; ++w) a += red[8 + w * XR + tid];
-    write_ext(out, (size_t)row * ldo + d, tid, a, ext_terms, bf16);
+    for (int w = 0; w < nw; ++w) a += red[8 * R + (w * R + rr) * XR + k];
+    write_ext(out, (size_t)(row0 + rr) * ldo + d, k, a, ext_terms, bf16);
   }
 }
 
@@ -343,13 +380,24 @@ static bool ln_row_dispatch(const float* x32, const float* gamma, const float* b
                             cudaStream_t st) {
   const int threads = d / (4 * NPT);
   if (threads * 4 * NPT != d || threads % 32 || threads > 256) return false;
+  const bool pair = (M % 2 == 0) && (rps % 2 == 0);  // row pairs never straddle the probe signs
+#define ZO_LNR(XR)                                                                                              \
+  case XR:                                                                                                      \
+    if (pair)                                                                                                   \
+      launch_pdl(k_ln_row<NPT, XR, 2>, dim3(M / 2), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, \
+                 Pp, Pm, rps, ext_terms, vstride);                                                              \
+    else                                                                                                        \
+      launch_pdl(k_ln_row<NPT, XR, 1>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, \
+                 Pm, rps, ext_terms, vstride);                                                                  \
+    return true;
   switch (r) {
-    case 0: launch_pdl(k_ln_row<NPT, 0>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
-    case 1: launch_pdl(k_ln_row<NPT, 1>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
-    case 2: launch_pdl(k_ln_row<NPT, 2>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
-    case 4: launch_pdl(k_ln_row<NPT, 4>, dim3(M), dim3(threads), 0, st, x32, gamma, beta, d, out, ldo, bf16, Pp, Pm, rps, ext_terms, vstride); return true;
+    ZO_LNR(0)
+    ZO_LNR(1)
+    ZO_LNR(2)
+    ZO_LNR(4)
     default: return false;
   }
+#undef ZO_LNR
 }
 
 template <int NV>
