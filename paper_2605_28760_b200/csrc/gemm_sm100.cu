@@ -687,25 +687,9 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
     return !e || std::atoi(e) != 0;
   }();
   g.cg = (cg2_on && N > 128 && bn >= 128 && M >= 512) ? 2 : 1;
-  if (g.cg == 2) {
-    // N=128 pair tiles measured 1.4-1.5x slower (A re-reads, fixed costs).  Between 256
-    // and 192 pick the smaller ragged-wave cost: rounds * BN (the per-round tile time),
-    // with a 10% handicap on 192 for its extra A re-reads and per-MMA overheads.  At
-    // M=2048, N=5120 (attn_out, ff_down): 160 tiles = 2.16 waves of 74 pairs at 256,
-    // 216 tiles = 2.92 waves at 192.
-    const int mt2 = (M + 255) / 256, slots2 = num_sms / 2;
-    auto cost = [&](int b) {
-      const long tiles = (long)mt2 * ((N + b - 1) / b);
-      return (double)((tiles + slots2 - 1) / slots2) * b * (b == 256 ? 1.0 : 1.1);
-    };
-    static const bool bn192 = [] {
-      const char* e = std::getenv("ZO_BN192");
-      return e && std::atoi(e) != 0;
-    }();
-    // measured no faster than 256 (3 rounds of 192-wide tiles ~ 3 ragged rounds of 256:
-    // the narrower tile re-reads A 33% more); the stream-K tail fixes the ragged wave
-    g.bn = bn = (bn192 && cost(192) < cost(256)) ? 192 : 256;
-  }
+  // N=128 pair tiles measured 1.4-1.5x slower (A re-reads, fixed costs), 192-wide no
+  // faster than 256 on the ragged 13B shapes (they re-read A 33% more)
+  if (g.cg == 2) g.bn = bn = 256;
   const int mt = (M + 128 * g.cg - 1) / (128 * g.cg);
   const int tiles = mt * ((N + bn - 1) / bn);
   const int slots = num_sms / g.cg;
@@ -842,13 +826,8 @@ void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
 
 void gemm_launch(const GemmDesc& g, cudaStream_t st) {
   if (g.cg == 2) {
-    if (g.bf16) {
-      if (g.bn == 256) launch_e<256, true, 2>(g, st);
-      else launch_e<192, true, 2>(g, st);
-    } else {
-      if (g.bn == 256) launch_e<256, false, 2>(g, st);
-      else launch_e<192, false, 2>(g, st);
-    }
+    if (g.bf16) launch_e<256, true, 2>(g, st);
+    else launch_e<256, false, 2>(g, st);
     return;
   }
   if (g.bf16) {
