@@ -217,6 +217,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="launch kernels eagerly (no CUDA graph)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-materialising", dest="materialising", action="store_false",
+                    help="skip the materialising training-loop comparand (baseline_loop.py) on the same GPU")
+    ap.add_argument("--materialising-steps", type=int, default=6)
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e/cpu/gemm microbench")
     ap.add_argument("--mode", default="qdir", choices=["qdir", "exact"],
                     help="N>1: qdir = query directions sharded (rank g scores reference step t*N+g on a full "
@@ -432,6 +435,35 @@ def main():
         line["e2e"] = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * T * 4 + B * 4 + 8,
                        "d2h_bytes_per_step": 32, "api": f"model.sample_minibatch + zo_engine.{step_fn.__name__} (host batch)",
                        "phase_ms_last_step": dict(zip(["sample", "score", "update"], eng.last_step_ms()))}
+
+    if args.materialising and not args.profile and world == 1:
+        # the conventional training loop (baseline_loop.py:122-239) on the same replica: probe
+        # written into the weights, one forward per sign, restore, update -- the paper's
+        # "official baseline" structure, timed the same way (CUDA events, device inputs)
+        eng.fold_async()  # the comparand starts from folded weights (no window mass)
+        nb = args.materialising_steps
+        bw = min(3, nb)
+        rc = False  # cached products: the reference's default mode
+        for t in range(bw):
+            eng.baseline_step_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, rc,
+                                    d_tok[t].data_ptr(), d_gold[t].data_ptr(), Bl)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for t in range(bw, bw + nb):
+            eng.baseline_step_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, rc,
+                                    d_tok[t % nsteps].data_ptr(), d_gold[t % nsteps].data_ptr(), Bl)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bms = e0.elapsed_time(e1) / nb
+        line["materialising_loop"] = {
+            "value": 1000.0 / bms, "unit": UNIT, "ms_per_step": bms, "steps": nb,
+            "speedup_of_serving_path": (1000.0 / ms_step) / (1000.0 / bms),
+            "mode": "cached products (restore = copy of the saved bits)",
+            "weight_writes_per_step": 4 * (sum(mcfg.dim * n for n in (3 * mcfg.dim, mcfg.dim, 4 * mcfg.dim))
+                                           * mcfg.n_layers + mcfg.vocab * mcfg.dim),
+            "what": "baseline_loop.py:122-239 on this GPU: W+=eps*P, score L+, W-=2eps*P, score L-, restore, "
+                    "W-=eta*c*P (zo_baseline_step_async, float64 master + 16-bit serving copy)"}
 
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         from oracle.cpu_bench import estimate_step, host_threads

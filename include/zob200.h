@@ -167,6 +167,22 @@ int zo_qdir_score_async(zo_ctx* ctx, uint64_t seed, uint64_t macro_step, int32_t
 int zo_out4_io(zo_ctx* ctx, void* dev, int32_t to_ctx);
 int zo_qdir_apply_async(zo_ctx* ctx, uint64_t seed, uint64_t macro_step, int32_t G, double lr,
                         const double* out4_all_dev);
+/* materialising training-loop comparand (baseline_loop.py:122-239, run_baseline;
+ * replaces the _Probe / VectorProbe writes of baseline_loop.py:68-119, 191-221):
+ * zo_baseline_directions samples the step's U (+ V at a window start / every
+ * factorized step) and zeroes the LoRA-extension operands (the forward reads the
+ * materialised weights); zo_baseline_pass writes the probe into the weights --
+ * pass 0: +eps P, 1: -2 eps P, 2: restore (recompute = 0: cached product, the
+ * restore copies the saved bits; 1: axpy_outer recompute, arithmetic restore) --
+ * with zo_score(nsign = 1) in between; zo_baseline_update applies
+ * W += (beta*scale) P with the ctx coefficient (zo_coefficient / zo_set_coefficient).
+ * zo_baseline_step_async: one whole step, device inputs, no host sync. */
+int zo_baseline_directions(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu);
+int zo_baseline_pass(zo_ctx* ctx, int32_t pass, double epsilon, int32_t recompute);
+int zo_baseline_update(zo_ctx* ctx, double lr, int32_t recompute);
+int zo_baseline_step_async(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon, double lr,
+                           int32_t divide_by_r, int32_t recompute, const int32_t* tokens_dev,
+                           const int32_t* gold_dev, int32_t B);
 /* per-phase device time of the last zo_step (ms): [sample, score, update] */
 int zo_last_step_ms(zo_ctx* ctx, float ms[3]);
 

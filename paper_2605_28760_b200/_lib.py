@@ -79,6 +79,11 @@ SIGNATURES = [
                                        _c.c_double, _c.c_double, _c.c_int32, _P, _P, _c.c_int32]),
     ("zo_out4_io", _c.c_int, [_P, _P, _c.c_int32]),
     ("zo_qdir_apply_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _P]),
+    ("zo_baseline_directions", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32]),
+    ("zo_baseline_pass", _c.c_int, [_P, _c.c_int32, _c.c_double, _c.c_int32]),
+    ("zo_baseline_update", _c.c_int, [_P, _c.c_double, _c.c_int32]),
+    ("zo_baseline_step_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double,
+                                          _c.c_int32, _c.c_int32, _P, _P, _c.c_int32]),
     ("zo_last_step_ms", _c.c_int, [_P, _c.POINTER(_c.c_float)]),
     ("zo_fnv1a64", _c.c_uint64, [_P, _c.c_uint64, _c.c_uint64]),
     ("zo_bench_gemm", _c.c_int, [_P, _c.c_int32, _c.c_int32, _c.c_int32, _c.POINTER(_c.c_float),

@@ -1025,4 +1025,135 @@ void launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t st) {
 
 void launch_zero(void* p, size_t bytes, cudaStream_t st) { ZO_CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st)); }
 
+// ------------------------------------------------------------------ materialising-loop comparand
+// baseline_loop.py:68-119 / 122-239: the conventional training loop writes every
+// perturbed matrix four times per step.  One 64x64 W tile per CTA, 4x4 per thread,
+// U/V rows staged through shared memory 32 ranks at a time.
+//   BL_PROBE   (cached _Probe.apply): P = dense_product(U, V) (numerics.py:256-267:
+//              0 + fl(u*v), k ascending), w = fl(w0 + fl(a1*P)) [then fl(w + fl(a2*P))]
+//              -> the 16-bit serving copy only.  The float64 master keeps w0, which is
+//              exactly the bits restore_matrix copies back (numerics.py:246-253).
+//   BL_UPDATE  (cached update): alpha = fl(beta*scale) from the device coefficient,
+//              w = fl(w0 + fl(alpha*P)) -> master + 16-bit copy.
+//   BL_OUTER   (recompute mode, axpy_outer in place, numerics.py:207-235): per k
+//              w = fl(w + fl(alpha*fl(u*v))) -> master + 16-bit copy; alpha = a1, or
+//              fl(beta*scale) when out4 is given.
+enum { BL_PROBE = 0, BL_UPDATE = 1, BL_OUTER = 2 };
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_materialise(double* __restrict__ W, int m, int n,
+                                                     const double* __restrict__ U, const double* __restrict__ Vv,
+                                                     int r, double a1, double a2, const double* __restrict__ out4,
+                                                     double scale, void* __restrict__ W16, int ldw, int transposed,
+                                                     bool bf16) {
+  double alpha = a1;
+  if (out4) alpha = __dmul_rn(out4[3], scale);
+  __shared__ double smem[64 * 33 + 32 * 65];
+  double* sU = smem;             // [64 rows i][33]
+  double* sVt = smem + 64 * 33;  // [32 k][65]
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double w[4][4], p[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + ty + 16 * a, j = j0 + tx + 16 * b;
+      w[a][b] = (i < m && j < n) ? W[(size_t)i * n + j] : 0.0;
+      p[a][b] = 0.0;
+    }
+  for (int k0 = 0; k0 < r; k0 += 32) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * 32; e += 256) {
+      const int rr = e >> 5, k = e & 31;
+      sU[rr * 33 + k] = (i0 + rr < m && k0 + k < r) ? U[(size_t)(i0 + rr) * r + k0 + k] : 0.0;
+      sVt[k * 65 + rr] = (j0 + rr < n && k0 + k < r) ? Vv[(size_t)(j0 + rr) * r + k0 + k] : 0.0;
+    }
+    __syncthreads();
+    const int kn = min(32, r - k0);
+    for (int k = 0; k < kn; ++k) {
+      double uv[4], vv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) uv[a] = sU[(ty + 16 * a) * 33 + k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) vv[b] = sVt[k * 65 + tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double t = __dmul_rn(uv[a], vv[b]);
+          if (MODE == BL_OUTER)
+            w[a][b] = __dadd_rn(w[a][b], __dmul_rn(alpha, t));
+          else
+            p[a][b] = __dadd_rn(p[a][b], t);
+        }
+    }
+  }
+  __syncthreads();
+  float* tile = reinterpret_cast<float*>(smem);  // [64][65] fp32 image for the transposed copy
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int yy = ty + 16 * a, xx = tx + 16 * b, i = i0 + yy, j = j0 + xx;
+      double v = w[a][b];
+      if (MODE == BL_PROBE) {
+        v = __dadd_rn(v, __dmul_rn(a1, p[a][b]));
+        if (a2 != 0.0) v = __dadd_rn(v, __dmul_rn(a2, p[a][b]));
+      } else if (MODE == BL_UPDATE) {
+        v = __dadd_rn(v, __dmul_rn(alpha, p[a][b]));
+      }
+      float f = 0.f;
+      if (i < m && j < n) {
+        if (MODE != BL_PROBE) W[(size_t)i * n + j] = v;
+        f = (float)v;
+        if (!transposed) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
+      }
+      tile[yy * 65 + xx] = f;
+    }
+  if (!transposed) return;
+  __syncthreads();
+  for (int e = threadIdx.x; e < 64 * 64; e += 256) {
+    const int jj = e >> 6, ii = e & 63, j = j0 + jj, i = i0 + ii;
+    if (i < m && j < n) reinterpret_cast<uint16_t*>(W16)[(size_t)j * ldw + i] = to16(tile[ii * 65 + jj], bf16);
+  }
+}
+
+void launch_materialise(int mode, double* W64, int m, int n, const double* U, const double* V, int r, double a1,
+                        double a2, const double* out4, double scale, void* W16, int ldw, int transposed, bool bf16,
+                        cudaStream_t st) {
+  const dim3 grid((n + 63) / 64, (m + 63) / 64);
+  switch (mode) {
+    case BL_PROBE:
+      k_materialise<BL_PROBE><<<grid, 256, 0, st>>>(W64, m, n, U, V, r, a1, a2, nullptr, scale, W16, ldw,
+                                                    transposed, bf16);
+      break;
+    case BL_UPDATE:
+      k_materialise<BL_UPDATE><<<grid, 256, 0, st>>>(W64, m, n, U, V, r, 0.0, 0.0, out4, scale, W16, ldw,
+                                                     transposed, bf16);
+      break;
+    default:
+      k_materialise<BL_OUTER><<<grid, 256, 0, st>>>(W64, m, n, U, V, r, a1, 0.0, out4, scale, W16, ldw,
+                                                    transposed, bf16);
+  }
+}
+
+// VectorProbe.set_sign for ONE scoring call (the loop scores each sign separately):
+// both fp32 copies = fp32(p + eps*z) (sign +1) or fp32((p + eps*z) + (-2 eps)*z) (sign -1)
+__global__ void k_vec_probe_sign(const double* __restrict__ p, const double* __restrict__ z, int64_t n, double eps,
+                                 int sign, float* __restrict__ out32) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double v = __dadd_rn(p[i], __dmul_rn(eps, z[i]));
+    if (sign < 0) v = __dadd_rn(v, __dmul_rn(-2.0 * eps, z[i]));
+    out32[i] = out32[n + i] = (float)v;
+  }
+}
+
+void launch_vec_probe_sign(const double* p, const double* z, int64_t n, double eps, int sign, float* out32,
+                           cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  k_vec_probe_sign<<<grid > 0 ? grid : 1, 256, 0, st>>>(p, z, n, eps, sign, out32);
+}
+
 }  // namespace zo

@@ -78,6 +78,15 @@ void launch_fold_dev(double* W64, int m, int n, const double* A, const double* V
 void launch_shadow_T(const double* W64, int m, int n, void* W16T, int ldw, bool bf16, cudaStream_t st);
 void launch_shadow(const double* W64, int64_t count, void* W16, bool bf16, cudaStream_t st);
 void launch_zero(void* p, size_t bytes, cudaStream_t st);
+// materialising-loop comparand (baseline_loop.py:68-239): mode 0 cached probe (16-bit copy
+// of fl(fl(w0 + a1*P) [+ a2*P]) only), 1 cached update (alpha = out4[3]*scale), 2 recompute
+// (axpy_outer in place, alpha = a1 or out4[3]*scale); modes 1/2 write master + 16-bit copy
+void launch_materialise(int mode, double* W64, int m, int n, const double* U, const double* V, int r, double a1,
+                        double a2, const double* out4, double scale, void* W16, int ldw, int transposed, bool bf16,
+                        cudaStream_t st);
+// VectorProbe at one sign for a single-sign scoring call (both fp32 copies)
+void launch_vec_probe_sign(const double* p, const double* z, int64_t n, double eps, int sign, float* out32,
+                           cudaStream_t st);
 void launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t st);
 
 }  // namespace zo

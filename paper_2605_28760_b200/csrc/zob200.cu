@@ -120,6 +120,7 @@ struct zo_ctx {
   void *hS = nullptr, *gS = nullptr;
   float* x32S = nullptr;
   double *nll = nullptr, *out4 = nullptr, *scratch = nullptr;
+  double* nll_bl = nullptr;  // materialising loop: the sign +1 NLLs while sign -1 is scored
   int64_t scratch_n = 0;
   unsigned* abort_flag = nullptr;
   int32_t *tok = nullptr, *gold = nullptr;
@@ -608,6 +609,7 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->z = c->mem.get<float>((size_t)c->Smax * d.rank);
   c->logits = c->mem.get<float>((size_t)c->Smax * c->ldl);
   c->nll = c->mem.get<double>(2 * std::max(d.max_batch, 4096));
+  c->nll_bl = c->mem.get<double>(d.max_batch);
   c->out4 = c->mem.get<double>(4);
   c->abort_flag = c->mem.get<unsigned>(1);
   c->tok = c->mem.get<int32_t>((size_t)d.max_batch * c->T);
@@ -1232,6 +1234,128 @@ extern "C" int zo_graph_kernel_count(zo_ctx* c, int32_t* per_step, int32_t* per_
 extern "C" int zo_fold_async(zo_ctx* c) {
   ZO_API_BEGIN
   if (c->d.estimator == ZO_EST_LOZO) fold_all(c);
+  return ZO_OK;
+  ZO_API_END
+}
+
+// ------------------------------------------------------------------ materialising-loop comparand
+// baseline_loop.py:122-239 (run_baseline) on the same replica: the conventional
+// training loop that writes the probe into the weights, scores each sign with its
+// own forward, restores, then writes the update -- four m*n weight writes per
+// matrix per step (here: three 16-bit serving-copy rewrites + one master+copy
+// update in cached mode; four master+copy rewrites in recompute mode).  It is the
+// cost comparand of the serving path (PAPER.md "official LoZO baseline") and keeps
+// the reference's float64 arithmetic, so its parameters are bit-exact given c.
+namespace {
+double probe_scale(const zo_ctx* c) {
+  return c->d.estimator == ZO_EST_FACTORIZED ? 1.0 / std::sqrt((double)c->r) : 1.0;
+}
+void baseline_pass(zo_ctx* c, int pass, double eps, bool recompute) {
+  const double s = probe_scale(c);
+  const double a_plus = eps * s, a_minus = (-2.0 * eps) * s;
+  for (auto& m : c->mats) {
+    const int ldw = m.kind == K_EMBED ? (int)m.n : m.ldw, tr = m.kind == K_EMBED ? 0 : 1;
+    double* Um = c->U + m.u_off;
+    double* Vm = c->V + m.v_off;
+    if (recompute) {  // _Probe.apply / restore(eps) arithmetic, in place (baseline_loop.py:94-104)
+      const double a = pass == 1 ? a_minus : a_plus;
+      launch_materialise(2, m.W64, (int)m.m, (int)m.n, Um, Vm, c->r, a, 0.0, nullptr, s, m.W16, ldw, tr, c->bf16,
+                         c->st);
+    } else if (pass == 2) {  // restore_matrix: the master was never modified
+      refresh_shadow(c, m);
+    } else {
+      launch_materialise(0, m.W64, (int)m.m, (int)m.n, Um, Vm, c->r, a_plus, pass == 1 ? a_minus : 0.0, nullptr,
+                         s, m.W16, ldw, tr, c->bf16, c->st);
+    }
+  }
+  if (c->full_scope) {  // VectorProbe.set_sign(+1 / -1 / 0) (zo_engine.py:278-286)
+    if (pass == 2)
+      launch_vec_probe(c->VEC64, c->VZ, (int64_t)c->nv * c->d.dim, 0.0, c->VEC32, c->st);
+    else
+      launch_vec_probe_sign(c->VEC64, c->VZ, (int64_t)c->nv * c->d.dim, eps, pass == 0 ? 1 : -1, c->VEC32, c->st);
+  }
+}
+void baseline_update(zo_ctx* c, double lr, bool recompute) {
+  const double s = probe_scale(c);
+  for (auto& m : c->mats) {
+    const int ldw = m.kind == K_EMBED ? (int)m.n : m.ldw, tr = m.kind == K_EMBED ? 0 : 1;
+    launch_materialise(recompute ? 2 : 1, m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, 0.0,
+                       0.0, c->out4, s, m.W16, ldw, tr, c->bf16, c->st);
+  }
+  vec_update(c, c->out4, lr, nullptr);  // VectorProbe.update with the unnormalised c
+}
+void baseline_directions(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu) {
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  const int64_t wstart = lozo ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
+  check(!c->a_dirty, ZO_ERR_CONFIG, "materialising loop on a replica with unfolded window mass");
+  if (!lozo || wstart != c->v_window) {
+    sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
+    write_vext_all(c);
+    c->v_window = wstart;
+  }
+  sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+  sample_z(c, seed);
+  // the forward reads the materialised weights: no LoRA extension (probe operands 0)
+  ZO_CUDA_TRY(cudaMemsetAsync(c->Pp, 0, (size_t)c->su * 4, c->st));
+  ZO_CUDA_TRY(cudaMemsetAsync(c->Pm, 0, (size_t)c->su * 4, c->st));
+}
+}  // namespace
+
+// pass 0: W + eps*P (probe +1), 1: then -2eps*P (probe -1), 2: restore.  U/V of the
+// step must be sampled (zo_sample_v / zo_sample_u) and the probe operands zeroed
+// (zo_baseline_directions); score with zo_score(nsign = 1) between passes.
+extern "C" int zo_baseline_pass(zo_ctx* c, int32_t pass, double eps, int32_t recompute) {
+  ZO_API_BEGIN
+  check(pass >= 0 && pass <= 2, ZO_ERR_INPUT, "baseline pass must be 0, 1 or 2");
+  baseline_pass(c, pass, eps, recompute != 0);
+  ZO_CUDA_TRY(cudaGetLastError());
+  return ZO_OK;
+  ZO_API_END
+}
+
+// W -= eta*c_used*P with the ctx coefficient (zo_coefficient / zo_set_coefficient)
+extern "C" int zo_baseline_update(zo_ctx* c, double lr, int32_t recompute) {
+  ZO_API_BEGIN
+  baseline_update(c, lr, recompute != 0);
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+// U (and V at a window start / every factorized step) for `step`, probe operands zeroed
+extern "C" int zo_baseline_directions(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu) {
+  ZO_API_BEGIN
+  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  set_step(c, step);
+  baseline_directions(c, seed, step, nu);
+  return ZO_OK;
+  ZO_API_END
+}
+
+// One whole materialising-loop step, stream-ordered, device-resident inputs (bench).
+extern "C" int zo_baseline_step_async(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr,
+                                      int32_t divide_by_r, int32_t recompute, const int32_t* tokens_dev,
+                                      const int32_t* gold_dev, int32_t B) {
+  ZO_API_BEGIN
+  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  k_set_u64<<<1, 1, 0, c->st>>>(c->d_step, step);
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->tok, tokens_dev, (size_t)B * c->T * 4, cudaMemcpyDeviceToDevice, c->st));
+  const size_t ng = (size_t)B * c->d.opt_len * 4;
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->gold, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
+  baseline_directions(c, seed, step, nu);
+  baseline_pass(c, 0, eps, recompute != 0);
+  do_score(c, B, 1);
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->nll_bl, c->nll, (size_t)B * 8, cudaMemcpyDeviceToDevice, c->st));
+  baseline_pass(c, 1, eps, recompute != 0);
+  do_score(c, B, 1);
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->nll + B, c->nll, (size_t)B * 8, cudaMemcpyDeviceToDevice, c->st));
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->nll, c->nll_bl, (size_t)B * 8, cudaMemcpyDeviceToDevice, c->st));
+  baseline_pass(c, 2, eps, recompute != 0);
+  launch_coefficient(c->nll, B, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
+  baseline_update(c, lr, recompute != 0);
+  ZO_CUDA_TRY(cudaGetLastError());
   return ZO_OK;
   ZO_API_END
 }

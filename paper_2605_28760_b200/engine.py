@@ -285,6 +285,22 @@ class ZoEngine:
     def nll_io(self, dev_ptr: int, count: int, to_ctx: bool) -> None:
         check(lib().zo_nll_io(self._h, ctypes.c_void_p(dev_ptr), count, int(to_ctx)))
 
+    # ---------------------------------------------------------------- materialising-loop comparand
+    def baseline_directions(self, seed: int, step: int, nu: int) -> None:
+        check(lib().zo_baseline_directions(self._h, seed, step, nu))
+
+    def baseline_pass(self, which: int, epsilon: float, recompute: bool) -> None:
+        check(lib().zo_baseline_pass(self._h, which, float(epsilon), int(recompute)))
+
+    def baseline_update(self, lr: float, recompute: bool) -> None:
+        check(lib().zo_baseline_update(self._h, float(lr), int(recompute)))
+
+    def baseline_step_async(self, seed: int, step: int, nu: int, epsilon: float, lr: float, divide_by_r: bool,
+                            recompute: bool, tokens_dev: int, gold_dev: int, B: int) -> None:
+        check(lib().zo_baseline_step_async(self._h, seed, step, nu, float(epsilon), float(lr), int(divide_by_r),
+                                           int(recompute), ctypes.c_void_p(tokens_dev), ctypes.c_void_p(gold_dev),
+                                           B))
+
     def last_step_ms(self) -> tuple[float, float, float]:
         f = (ctypes.c_float * 3)()
         check(lib().zo_last_step_ms(self._h, f))

@@ -16,6 +16,9 @@ Fixtures
   traj_*.jsonl      run_serving_path trajectories (runtime.py:253-359) with
                     header digests, per-step L+/L-/c/beta/u,v digests and the
                     final params digest, written by zoserve.write_trajectory
+  traj_*baseline*   run_baseline trajectories (baseline_loop.py:122-239), the
+                    materialising loop: cached and recompute products,
+                    factorized and full scope
   adapter_rich.zoad ZOAD adapter file (+ .manifest.json) written by the
                     reference's save_adapter for a state with frozen, window
                     and probe slots (adapter.py:279-415)
@@ -165,6 +168,37 @@ OPT125 = dict(vocab=50272, dim=768, n_layers=12, n_heads=12, prompt_len=63, init
 OPT125_TASK = dict(seed=11, vocab=50272, prompt_len=63, train_size=1000, dev_size=2, val_size=2)
 
 
+def baseline_trajectory(name, mcfg_kw, tcfg_kw, zcfg_kw, steps, recompute=False, precision="real64"):
+    """run_baseline (baseline_loop.py:122-239): the materialising training loop."""
+    _ref()
+    from zoserve.baseline_loop import run_baseline
+    from zoserve.model import ModelConfig, TaskConfig, generate_task
+    from zoserve.zo_engine import ZoConfig, write_trajectory
+
+    mcfg = ModelConfig(**mcfg_kw)
+    task = generate_task(TaskConfig(**tcfg_kw))
+    zcfg = ZoConfig(**zcfg_kw)
+    run = run_baseline(mcfg, task, zcfg, steps, precision=precision, eval_every=10**9,
+                       recompute_products=recompute)
+    header = {"model": mcfg_kw, "task": tcfg_kw, "zo": zcfg_kw, "steps": steps, "precision": precision,
+              "recompute_products": recompute, "model_digest": run.model_digest,
+              "task_digest": run.task_digest, "zo_digest": zcfg.digest()}
+    final = {"final_params_digest": run.final_params_digest, "weight_writes": run.weight_write_count,
+             "eval_loss": run.eval_curve[-1].loss, "eval_acc": run.eval_curve[-1].acc}
+    write_trajectory(os.path.join(OUT, f"traj_{name}.jsonl"), header, run.trajectory, final)
+
+
+def baseline_trajectories():
+    lozo = dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=5, batch_size=8)
+    baseline_trajectory("micro_baseline", MICRO, MICRO_TASK, lozo, 7)
+    baseline_trajectory("micro_baseline_recompute", MICRO, MICRO_TASK, dict(lozo, divide_by_r=True), 7,
+                        recompute=True)
+    baseline_trajectory("micro_baseline_fact", MICRO, MICRO_TASK,
+                        dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=8, estimator="factorized_sqrt_r",
+                             batch_size=8), 4)
+    baseline_trajectory("micro_baseline_full", MICRO, MICRO_TASK, dict(lozo, scope="full"), 4)
+
+
 def adapter_fixture():
     _ref()
     from zoserve.adapter import AdapterState, LoraSlot, save_adapter
@@ -206,6 +240,9 @@ def main():
     if a.only == "full":
         full_scope_trajectories()
         return
+    if a.only == "baseline":
+        baseline_trajectories()
+        return
     adapter_fixture()
     streams()
     fnv()
@@ -219,6 +256,7 @@ def main():
     trajectory("small_lozo", SMALL, SMALL_TASK,
                dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=4, batch_size=16), 10)
     full_scope_trajectories()
+    baseline_trajectories()
     if a.opt125m:
         forward_fixture("opt125m", OPT125, OPT125_TASK, B=16)
         trajectory("opt125m_lozo", OPT125, OPT125_TASK,

@@ -85,6 +85,25 @@ def test_trajectory_vs_reference(golden_dir, name):
         assert R.params_digest(params) == fin["final_params_digest"]
 
 
+@pytest.mark.parametrize("name", ["micro_baseline", "micro_baseline_recompute", "micro_baseline_fact",
+                                  "micro_baseline_full"])
+def test_baseline_loop_vs_reference(golden_dir, name):
+    """The materialising loop (baseline_loop.py:122-239): cached / recompute products,
+    factorized and full scope -- digests, losses and the final params bit-exact."""
+    h, recs, fin = _traj(golden_dir, f"traj_{name}.jsonl")
+    cfg = R.ModelCfg(**h["model"])
+    splits = R.generate_task(R.TaskCfg(**h["task"]))
+    z = R.ZoCfg(**h["zo"])
+    mine, params = R.run_baseline(cfg, splits, z, h["steps"], recompute=h["recompute_products"])
+    for a, b in zip(recs, mine):
+        assert (a["u_digest"], a["v_digest"], a["minibatch_id"]) == (b.u_digest, b.v_digest, b.minibatch_id)
+        assert abs(a["loss_plus"] - b.loss_plus) <= 1e-12
+        assert abs(a["loss_minus"] - b.loss_minus) <= 1e-12
+        assert abs(a["beta"] - b.beta) <= 1e-9 * max(1.0, abs(a["beta"]))
+    if all(a["loss_plus"] == b.loss_plus and a["loss_minus"] == b.loss_minus for a, b in zip(recs, mine)):
+        assert R.params_digest(params) == fin["final_params_digest"]
+
+
 def test_canonical_mean_pairwise_order():
     v = np.array([1e16, 1.0, -1e16, 1.0, 3.0])
     # ((1e16 + 1) + (-1e16 + (1 + 3))) / 5, evaluated pairwise
