@@ -836,75 +836,196 @@ void launch_p16t(const float* P, int m, int r, void* out, bool bf16, cudaStream_
 }
 
 // ------------------------------------------------------------------ fold (K9) + 16-bit shadow refresh
-// 32x32 tile per block: W64 tile (+ sum_k alpha*(A_ik*V_jk), k ascending, each
-// term rounded as numpy does: numerics.py:211) -> W64, then the 16-bit shadow
-// (transposed [n, ldw] for projections, straight [m, n] for the embedding).
-__global__ void k_fold_shadow(double* __restrict__ W, int m, int n, const double* __restrict__ A,
-                              const double* __restrict__ Vv, int r, double alpha, void* __restrict__ W16, int ldw,
-                              int transposed, bool bf16) {
-  __shared__ float tile[32][33];
-  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int i = i0 + yy, j = j0 + tx;
-    float f = 0.f;
-    if (i < m && j < n) {
-      double w = W[(size_t)i * n + j];
-      if (r > 0) {
-        for (int k = 0; k < r; ++k)
-          w = __dadd_rn(w, __dmul_rn(alpha, __dmul_rn(A[(size_t)i * r + k], Vv[(size_t)j * r + k])));
-        W[(size_t)i * n + j] = w;
-      }
-      f = (float)w;
-      if (!transposed && W16) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
-    }
-    tile[yy][tx] = f;
+// Low-rank (r <= 8) rewrite of a float64 master W[m, n] (reference (in, out) layout)
+// and its 16-bit tensor-core copy -- HBM-bound: 8 B read (+ 8 B written) per weight
+// plus the 2 B copy.  One 64 x 64 tile per CTA; warp w owns rows w, w+8, .., lane l
+// columns (2l, 2l+1), so every master access is a 512 B row segment per warp
+// (double2), and the transposed copy goes through a shared 16-bit tile and leaves as
+// 128 B row segments.  Per-element arithmetic is numpy's (no FMA contraction):
+//   LR_OUTER  axpy_outer in place (numerics.py:207-235): per k ascending
+//             w = fl(w + fl(alpha * fl(l_ik * r_jk)))           (fold, dense update)
+//   LR_PROBE  cached _Probe.apply (baseline_loop.py:94-98): p = dense_product (0 +
+//             fl(l*r), k ascending), copy <- fl(fl(w + fl(a1*p)) [+ fl(a2*p)]); the
+//             master keeps w (its bits are what restore_matrix copies back)
+//   LR_DENSE  cached update: w = fl(w + fl(alpha * p))
+//   LR_COPY   copy <- w (shadow refresh)
+// alpha: a1 (host), fl(beta*scale) with beta = out4[3] (materialising loop), or
+// fl(-fl(lr*c)*scale) with c = out4[2] (factorized update; no-op when aborted).
+enum { LR_OUTER = 0, LR_PROBE = 1, LR_DENSE = 2, LR_COPY = 3 };
+enum { ALPHA_HOST = 0, ALPHA_BETA = 1, ALPHA_LRC = 2 };
+struct LowRankArgs {
+  double* W;
+  int m, n;
+  const double* L;
+  const double* R;
+  int r;
+  double a1, a2;
+  const double* out4;
+  double lr, scale;
+  const unsigned* abort_flag;
+  void* W16;
+  int ldw, transposed;
+  bool bf16;
+  int alpha_src;
+};
+
+template <int MODE, int RK>
+__global__ void __launch_bounds__(256, 3) k_lowrank(LowRankArgs a) {
+  __shared__ double sL[64 * 9];
+  __shared__ uint16_t t16[64 * 66];  // [j][i] 16-bit transposed tile
+  double alpha = a.a1;
+  if (a.alpha_src == ALPHA_BETA) {
+    alpha = __dmul_rn(a.out4[3], a.scale);
+  } else if (a.alpha_src == ALPHA_LRC) {
+    if (a.abort_flag ? *a.abort_flag != 0u : !(isfinite(a.out4[0]) && isfinite(a.out4[1]))) return;
+    alpha = __dmul_rn(-__dmul_rn(a.lr, a.out4[2]), a.scale);
   }
-  if (!transposed || !W16) return;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = MODE == LR_COPY ? 0 : a.r;
+  const int jl = 2 * lane, j = j0 + jl;
+  for (int e = threadIdx.x; e < 64 * r; e += 256) {
+    const int rr = e / r, k = e - rr * r;
+    sL[rr * 9 + k] = (i0 + rr < a.m) ? a.L[(size_t)(i0 + rr) * r + k] : 0.0;
+  }
+  double rv[2][RK];  // this lane's two V rows (RK >= r; the ranks past r are never read)
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int k = 0; k < RK; ++k) rv[c][k] = (k < r && j + c < a.n) ? a.R[(size_t)(j + c) * r + k] : 0.0;
+  const bool vec = (a.n & 1) == 0;
+  double w[8][2];
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int i = i0 + warp + 8 * s;
+    w[s][0] = w[s][1] = 0.0;
+    if (i < a.m && j < a.n) {
+      const double* src = a.W + (size_t)i * a.n + j;
+      if (vec) {
+        const double2 v = __ldcs(reinterpret_cast<const double2*>(src));
+        w[s][0] = v.x;
+        w[s][1] = v.y;
+      } else {
+        w[s][0] = src[0];
+        if (j + 1 < a.n) w[s][1] = src[1];
+      }
+    }
+  }
   __syncthreads();
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int j = j0 + yy, i = i0 + tx;
-    if (i < m && j < n) reinterpret_cast<uint16_t*>(W16)[(size_t)j * ldw + i] = to16(tile[tx][yy], bf16);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int il = warp + 8 * s;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      double v = w[s][c];
+      if (MODE == LR_OUTER) {
+#pragma unroll
+        for (int k = 0; k < RK; ++k)
+          if (k < r) v = __dadd_rn(v, __dmul_rn(alpha, __dmul_rn(sL[il * 9 + k], rv[c][k])));
+      } else if (MODE != LR_COPY) {
+        double p = 0.0;
+#pragma unroll
+        for (int k = 0; k < RK; ++k)
+          if (k < r) p = __dadd_rn(p, __dmul_rn(sL[il * 9 + k], rv[c][k]));
+        if (MODE == LR_PROBE) {
+          v = __dadd_rn(v, __dmul_rn(a.a1, p));
+          if (a.a2 != 0.0) v = __dadd_rn(v, __dmul_rn(a.a2, p));
+        } else {
+          v = __dadd_rn(v, __dmul_rn(alpha, p));
+        }
+      }
+      w[s][c] = v;
+    }
+  }
+  uint16_t* W16 = static_cast<uint16_t*>(a.W16);
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const int il = warp + 8 * s, i = i0 + il;
+    if (i >= a.m || j >= a.n) continue;
+    const bool two = j + 1 < a.n;
+    if (MODE == LR_OUTER || MODE == LR_DENSE) {
+      double* dst = a.W + (size_t)i * a.n + j;
+      if (vec)
+        __stcs(reinterpret_cast<double2*>(dst), make_double2(w[s][0], w[s][1]));
+      else {
+        dst[0] = w[s][0];
+        if (two) dst[1] = w[s][1];
+      }
+    }
+    if (!W16) continue;
+    const uint16_t h0 = to16((float)w[s][0], a.bf16), h1 = to16((float)w[s][1], a.bf16);
+    if (a.transposed) {
+      t16[jl * 66 + il] = h0;
+      t16[(jl + 1) * 66 + il] = h1;
+    } else if (vec) {
+      *reinterpret_cast<uint32_t*>(W16 + (size_t)i * a.n + j) = (uint32_t)h0 | ((uint32_t)h1 << 16);
+    } else {
+      W16[(size_t)i * a.n + j] = h0;
+      if (two) W16[(size_t)i * a.n + j + 1] = h1;
+    }
+  }
+  if (!a.transposed || !W16) return;
+  __syncthreads();
+  const bool v32 = (a.ldw & 1) == 0;
+  const int ii = 2 * lane, io = i0 + ii;
+  for (int jj = warp; jj < 64; jj += 8) {
+    const int jo = j0 + jj;
+    if (jo >= a.n || io >= a.m) continue;
+    uint16_t* dst = W16 + (size_t)jo * a.ldw + io;
+    const uint16_t x0 = t16[jj * 66 + ii], x1 = t16[jj * 66 + ii + 1];
+    if (v32 && io + 1 < a.m)
+      *reinterpret_cast<uint32_t*>(dst) = (uint32_t)x0 | ((uint32_t)x1 << 16);
+    else {
+      dst[0] = x0;
+      if (io + 1 < a.m) dst[1] = x1;
+    }
   }
 }
 
-// factorized dense update with alpha = -(lr*c) * scale read from the device
-// coefficient (zo_engine.py:450); no-op when the step aborted.
-__global__ void k_fold_dev(double* __restrict__ W, int m, int n, const double* __restrict__ A,
-                           const double* __restrict__ Vv, int r, const double* __restrict__ out4, double lr,
-                           double scale, const unsigned* __restrict__ abort_flag, void* __restrict__ W16, int ldw,
-                           int transposed, bool bf16) {
-  if (abort_flag ? *abort_flag != 0u : !(isfinite(out4[0]) && isfinite(out4[1]))) return;
-  const double alpha = __dmul_rn(-__dmul_rn(lr, out4[2]), scale);
-  __shared__ float tile[32][33];
-  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int i = i0 + yy, j = j0 + tx;
-    float f = 0.f;
-    if (i < m && j < n) {
-      double w = W[(size_t)i * n + j];
-      for (int k = 0; k < r; ++k)
-        w = __dadd_rn(w, __dmul_rn(alpha, __dmul_rn(A[(size_t)i * r + k], Vv[(size_t)j * r + k])));
-      W[(size_t)i * n + j] = w;
-      f = (float)w;
-      if (!transposed) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
-    }
-    tile[yy][tx] = f;
+template <int RK>
+void launch_lowrank_rk(int mode, const LowRankArgs& a, const dim3& grid, cudaStream_t st) {
+  switch (mode) {
+    case LR_OUTER: k_lowrank<LR_OUTER, RK><<<grid, 256, 0, st>>>(a); break;
+    case LR_PROBE: k_lowrank<LR_PROBE, RK><<<grid, 256, 0, st>>>(a); break;
+    default: k_lowrank<LR_DENSE, RK><<<grid, 256, 0, st>>>(a);
   }
-  if (!transposed) return;
-  __syncthreads();
-  for (int yy = ty; yy < 32; yy += 8) {
-    const int j = j0 + yy, i = i0 + tx;
-    if (i < m && j < n) reinterpret_cast<uint16_t*>(W16)[(size_t)j * ldw + i] = to16(tile[tx][yy], bf16);
+}
+
+void launch_lowrank(int mode, const LowRankArgs& a, cudaStream_t st) {
+  const dim3 grid((a.n + 63) / 64, (a.m + 63) / 64);
+  if (mode == LR_COPY || a.r == 0) {
+    k_lowrank<LR_COPY, 1><<<grid, 256, 0, st>>>(a);
+    return;
   }
+  if (a.r <= 1) launch_lowrank_rk<1>(mode, a, grid, st);
+  else if (a.r <= 2) launch_lowrank_rk<2>(mode, a, grid, st);
+  else if (a.r <= 4) launch_lowrank_rk<4>(mode, a, grid, st);
+  else launch_lowrank_rk<8>(mode, a, grid, st);
+}
+
+LowRankArgs lowrank_args(double* W64, int m, int n, const double* L, const double* R, int r, void* W16, int ldw,
+                         int transposed, bool bf16) {
+  LowRankArgs a{};
+  a.W = W64;
+  a.m = m;
+  a.n = n;
+  a.L = L;
+  a.R = R;
+  a.r = r;
+  a.W16 = W16;
+  a.ldw = ldw;
+  a.transposed = transposed;
+  a.bf16 = bf16;
+  a.scale = 1.0;
+  a.alpha_src = ALPHA_HOST;
+  return a;
 }
 
 // High-rank variant (factorized r > 8, e.g. BASELINE config 5's r = 128 where this is
 // the dominant cost of a step: 3 float64 ops per weight per rank).  64x64 W tile per CTA,
 // each thread a 4x4 register micro-tile; the tile's A rows and V rows are staged
 // through shared memory 32 ranks at a time (V transposed).  Same per-element
-// arithmetic and order as k_fold_dev: w = w + alpha*(A_ik*V_jk), k ascending.
+// arithmetic and order as k_lowrank LR_OUTER: w = w + alpha*(A_ik*V_jk), k ascending.
 __global__ void __launch_bounds__(256) k_fold_dev_tiled(double* __restrict__ W, int m, int n,
                                                         const double* __restrict__ A, const double* __restrict__ Vv,
                                                         int r, const double* __restrict__ out4, double lr,
@@ -978,29 +1099,34 @@ __global__ void __launch_bounds__(256) k_fold_dev_tiled(double* __restrict__ W, 
 void launch_fold_dev(double* W64, int m, int n, const double* A, const double* V, int r, const double* out4,
                      double lr, double scale, const unsigned* abort_flag, void* W16, int ldw, int transposed,
                      bool bf16, cudaStream_t st) {
-  dim3 grid((n + 31) / 32, (m + 31) / 32);
-  if (r > 8)
+  if (r > 8) {
     k_fold_dev_tiled<<<dim3((n + 63) / 64, (m + 63) / 64), 256, 0, st>>>(W64, m, n, A, V, r, out4, lr, scale,
                                                                           abort_flag, W16, ldw, transposed, bf16, 0.0);
-  else
-    k_fold_dev<<<grid, dim3(32, 8), 0, st>>>(W64, m, n, A, V, r, out4, lr, scale, abort_flag, W16, ldw,
-                                             transposed, bf16);
+    return;
+  }
+  LowRankArgs a = lowrank_args(W64, m, n, A, V, r, W16, ldw, transposed, bf16);
+  a.out4 = out4;
+  a.lr = lr;
+  a.scale = scale;
+  a.abort_flag = abort_flag;
+  a.alpha_src = ALPHA_LRC;
+  launch_lowrank(LR_OUTER, a, st);
 }
 
 void launch_fold(double* W64, int m, int n, const double* A, const double* V, int r, double alpha, void* W16,
                  int ldw, int transposed, bool bf16, cudaStream_t st) {
-  dim3 grid((n + 31) / 32, (m + 31) / 32);
-  if (r > 8)
+  if (r > 8) {
     k_fold_dev_tiled<<<dim3((n + 63) / 64, (m + 63) / 64), 256, 0, st>>>(W64, m, n, A, V, r, nullptr, 0.0, 0.0,
                                                                           nullptr, W16, ldw, transposed, bf16, alpha);
-  else
-    k_fold_shadow<<<grid, dim3(32, 8), 0, st>>>(W64, m, n, A, V, r, alpha, W16, ldw, transposed, bf16);
+    return;
+  }
+  LowRankArgs a = lowrank_args(W64, m, n, A, V, r, W16, ldw, transposed, bf16);
+  a.a1 = alpha;
+  launch_lowrank(LR_OUTER, a, st);
 }
 
 void launch_shadow_T(const double* W64, int m, int n, void* W16T, int ldw, bool bf16, cudaStream_t st) {
-  dim3 grid((n + 31) / 32, (m + 31) / 32);
-  k_fold_shadow<<<grid, dim3(32, 8), 0, st>>>(const_cast<double*>(W64), m, n, nullptr, nullptr, 0, 1.0, W16T, ldw,
-                                                1, bf16);
+  launch_lowrank(LR_COPY, lowrank_args(const_cast<double*>(W64), m, n, nullptr, nullptr, 0, W16T, ldw, 1, bf16), st);
 }
 
 __global__ void k_shadow(const double* __restrict__ W, int64_t count, void* __restrict__ o, bool bf16) {
@@ -1122,6 +1248,16 @@ __global__ void __launch_bounds__(256) k_materialise(double* __restrict__ W, int
 void launch_materialise(int mode, double* W64, int m, int n, const double* U, const double* V, int r, double a1,
                         double a2, const double* out4, double scale, void* W16, int ldw, int transposed, bool bf16,
                         cudaStream_t st) {
+  if (r <= 8) {  // HBM-bound: the row-segment kernel
+    LowRankArgs a = lowrank_args(W64, m, n, U, V, r, W16, ldw, transposed, bf16);
+    a.a1 = a1;
+    a.a2 = a2;
+    a.out4 = out4;
+    a.scale = scale;
+    a.alpha_src = out4 ? ALPHA_BETA : ALPHA_HOST;
+    launch_lowrank(mode == BL_PROBE ? LR_PROBE : mode == BL_UPDATE ? LR_DENSE : LR_OUTER, a, st);
+    return;
+  }
   const dim3 grid((n + 63) / 64, (m + 63) / 64);
   switch (mode) {
     case BL_PROBE:
