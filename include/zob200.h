@@ -49,6 +49,14 @@ extern "C" {
 #define ZO_SCOPE_LORA_ONLY 0
 #define ZO_SCOPE_FULL 1
 
+/* decoder architecture.  ZOSERVE: the reference's model (model.py:170-199: GELU-tanh
+ * FFN, sinusoidal positions, no biases).  OPT: the OPT family's decoder (ReLU FFN,
+ * learned positions at offset 2, biases on qkv / attn_out / ff_up / ff_down,
+ * pre-LN) -- the §8(f) f4 variant that real OPT checkpoints load into; its extra
+ * params are the 2-D "pos_embed" [max_pos + 2, dim] and the 1-D "<blk>.<proj>.bias". */
+#define ZO_ARCH_ZOSERVE 0
+#define ZO_ARCH_OPT 1
+
 typedef struct zo_ctx zo_ctx;
 
 /* ModelConfig (model.py:62-81) + ZoConfig shape fields (zo_engine.py:71-98). */
@@ -61,6 +69,8 @@ typedef struct {
   int32_t precision; /* ZO_PREC_* */
   int32_t device;
   int32_t scope;     /* ZO_SCOPE_* */
+  int32_t arch;      /* ZO_ARCH_* */
+  int32_t max_pos;   /* ZO_ARCH_OPT: max_position_embeddings (table rows = max_pos + 2) */
 } zo_model_desc;
 
 const char* zo_last_error(void);

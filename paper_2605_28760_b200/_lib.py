@@ -18,6 +18,7 @@ ZO_OK, ZO_ERR_CONFIG, ZO_ERR_DIMENSION, ZO_ERR_INPUT, ZO_ERR_ABORT, ZO_ERR_CUDA,
 PREC_FP16, PREC_BF16 = 0, 1
 EST_LOZO, EST_FACTORIZED = 0, 1
 SCOPE_LORA_ONLY, SCOPE_FULL = 0, 1
+ARCH_ZOSERVE, ARCH_OPT = 0, 1
 
 _lib = None
 _lock = threading.Lock()
@@ -26,7 +27,7 @@ _lock = threading.Lock()
 class ZoModelDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "vocab", "dim", "n_layers", "n_heads", "prompt_len", "opt_len", "max_batch", "rank",
-        "estimator", "precision", "device", "scope")]
+        "estimator", "precision", "device", "scope", "arch", "max_pos")]
 
 
 # (name, restype, argtypes) for every symbol include/zob200.h declares

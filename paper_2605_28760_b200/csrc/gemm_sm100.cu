@@ -205,6 +205,11 @@ struct GemmParams {
   int sk, sk_w, sk_dp;
   float* sk_ws;
   unsigned* sk_flags;
+  // per-column bias (OPT arch; see zo_gemm.h) and the ReLU activation of EPI_GELU16*
+  const float* bias;
+  int bias_rps;
+  long bias_vstride;
+  int relu;
 };
 
 // Work segments of one unit: (tile, k-block range).  Data-parallel phase: whole
@@ -484,6 +489,18 @@ __global__ void __launch_bounds__(192, 1)
       for (int k = 0; k < 8; ++k) tp[k] = 0.f;
       const float* xP = nullptr;
       if constexpr (EPI == EPI_GELU16_EXT) xP = (row < p.xrps) ? p.xPp : p.xPm;
+      const float* bb = p.bias ? p.bias + ((row < p.bias_rps) ? 0 : p.bias_vstride) + n0 : nullptr;
+      auto add_bias = [&](float (&v)[32], int c) {
+        const float4* b4 = reinterpret_cast<const float4*>(bb + c);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 w = __ldg(b4 + j);
+          v[4 * j] += w.x;
+          v[4 * j + 1] += w.y;
+          v[4 * j + 2] += w.z;
+          v[4 * j + 3] += w.w;
+        }
+      };
       if constexpr (EPI == EPI_RESID32) {
         // fast path: whole tile row in range -> residual loads for chunk c+1 are in
         // flight while chunk c is added and stored
@@ -503,6 +520,7 @@ __global__ void __launch_bounds__(192, 1)
             float v[32];
             tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
             if (split) add_partials(v, c);
+            if (bb) add_bias(v, c);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               reinterpret_cast<float4*>(o + c)[j] =
@@ -524,10 +542,22 @@ __global__ void __launch_bounds__(192, 1)
         const size_t lin = (size_t)row * p.ldo + col0;
         constexpr int VEC = OUT16 ? 8 : 4;
         const bool full = col0 + 32 <= p.N && (lin % VEC) == 0;
+        if (bb) {
+          if (col0 + 32 <= p.N)
+            add_bias(v, c);
+          else
+            for (int i = 0; i < 32; ++i)
+              if (col0 + i < p.N) v[i] += bb[c + i];
+        }
         if constexpr (OUT16) {
           if constexpr (GELU) {
+            if (p.relu) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+              for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+            }
           }
           uint32_t pk[16];
 #pragma unroll
@@ -728,6 +758,10 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.sk_dp = g.sk_dp;
   p.sk_ws = g.sk_ws;
   p.sk_flags = g.sk_flags;
+  p.bias = g.bias;
+  p.bias_rps = g.bias_rps;
+  p.bias_vstride = g.bias_vstride;
+  p.relu = g.relu;
   if constexpr (CG == 1) {
     launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(192), C::SMEM, st, g.tmA, g.tmB, p);
   } else {

@@ -34,6 +34,12 @@ struct GemmDesc {
   const float* xPm = nullptr;
   int xr = 0, xrps = 0, tpart_ld = 0;
   float* tpart = nullptr;
+  // per-column bias added to the accumulator before the activation / residual (OPT
+  // arch); rows >= bias_rps read bias + bias_vstride (the -eps copy under full scope)
+  const float* bias = nullptr;
+  int bias_rps = 0;
+  long bias_vstride = 0;
+  int relu = 0;  // EPI_GELU16*: ReLU instead of GELU-tanh (OPT arch)
   // stream-K split of the k-iteration space over the persistent CTAs (gemm_enable_streamk)
   int sk = 0, sk_w = 0, sk_dp = 0;
   float* sk_ws = nullptr;       // [grid][128][bn] fp32 partials of split tiles

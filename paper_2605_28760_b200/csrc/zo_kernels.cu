@@ -114,24 +114,34 @@ void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, v
 __global__ void k_embed(float* __restrict__ x32, const int32_t* __restrict__ tokens, int B, int T, int d,
                         const double* __restrict__ E64, const void* __restrict__ E16, bool bf16,
                         const float* __restrict__ Pp, const float* __restrict__ Pm, const float* __restrict__ Ve,
-                        int r, const float* __restrict__ pe) {
+                        int r, const float* __restrict__ pe, PosEmbed pos) {
   const int row = blockIdx.x;
   const int per_sign = B * T;
   const int s = row / per_sign, rem = row % per_sign, b = rem / T, t = rem % T;
   const int tok = tokens[b * T + t];
   const float* P = (s == 0 ? Pp : Pm) + (size_t)tok * r;
+  const size_t prow = (size_t)(t + pos.offset);
+  const float* PP = pos.W64 ? (s == 0 ? pos.Pp : pos.Pm) + prow * r : nullptr;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     float e = E64 ? (float)E64[(size_t)tok * d + i] : ld16(E16, (size_t)tok * d + i, bf16);
     float delta = 0.f;
     for (int k = 0; k < r; ++k) delta += P[k] * Ve[(size_t)i * r + k];
-    x32[(size_t)row * d + i] = (e + delta) + pe[(size_t)t * d + i];
+    float pv;
+    if (PP) {  // OPT: inputs_embeds + embed_positions(t + 2), each with its LoRA delta
+      float pd = 0.f;
+      for (int k = 0; k < r; ++k) pd += PP[k] * pos.V32[(size_t)i * r + k];
+      pv = (float)pos.W64[prow * d + i] + pd;
+    } else {
+      pv = pe[(size_t)t * d + i];
+    }
+    x32[(size_t)row * d + i] = (e + delta) + pv;
   }
 }
 
 void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const double* E64, const void* E16,
                   bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r, const float* pe,
-                  int nrows, cudaStream_t st) {
-  k_embed<<<nrows, 256, 0, st>>>(x32, tokens, B, T, d, E64, E16, bf16, Pplus, Pminus, Ve32, r, pe);
+                  const PosEmbed& pos, int nrows, cudaStream_t st) {
+  k_embed<<<nrows, 256, 0, st>>>(x32, tokens, B, T, d, E64, E16, bf16, Pplus, Pminus, Ve32, r, pe, pos);
 }
 
 // ------------------------------------------------------------------ LN (+ extension), warp per row
@@ -1084,11 +1094,11 @@ __global__ void __launch_bounds__(256) k_fold_dev_tiled(double* __restrict__ W, 
       if (i < m && j < n) {
         W[(size_t)i * n + j] = w[a][b];
         f = (float)w[a][b];
-        if (!transposed) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
+        if (!transposed && W16) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
       }
       tile[yy * 65 + xx] = f;
     }
-  if (!transposed) return;
+  if (!transposed || !W16) return;
   __syncthreads();
   for (int e = threadIdx.x; e < 64 * 64; e += 256) {
     const int jj = e >> 6, ii = e & 63, j = j0 + jj, i = i0 + ii;
@@ -1233,11 +1243,11 @@ __global__ void __launch_bounds__(256) k_materialise(double* __restrict__ W, int
       if (i < m && j < n) {
         if (MODE != BL_PROBE) W[(size_t)i * n + j] = v;
         f = (float)v;
-        if (!transposed) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
+        if (!transposed && W16) reinterpret_cast<uint16_t*>(W16)[(size_t)i * n + j] = to16(f, bf16);
       }
       tile[yy * 65 + xx] = f;
     }
-  if (!transposed) return;
+  if (!transposed || !W16) return;
   __syncthreads();
   for (int e = threadIdx.x; e < 64 * 64; e += 256) {
     const int jj = e >> 6, ii = e & 63, j = j0 + jj, i = i0 + ii;

@@ -32,7 +32,7 @@ namespace {
 
 thread_local std::string g_last_error;
 
-enum Kind { K_EMBED = 0, K_QKV = 1, K_OUT = 2, K_UP = 3, K_DOWN = 4 };
+enum Kind { K_EMBED = 0, K_QKV = 1, K_OUT = 2, K_UP = 3, K_DOWN = 4, K_POS = 5 };
 
 struct Matrix {
   std::string lid;
@@ -104,6 +104,11 @@ struct zo_ctx {
   bool full_scope = false;
   int nv = 0;
   std::vector<std::string> vids;
+  std::vector<int64_t> voff, vlen;  // per 1-D param: offset / length in the vector arenas
+  int64_t nvt = 0;                  // total 1-D elements
+  bool opt = false;                 // ZO_ARCH_OPT
+  int i_pos = -1;                   // OPT: learned positions (offset 2)
+  std::vector<float*> bqkv, bout, bup, bdown;  // OPT: fp32 bias copies per layer ([0] +eps rows)
   double *VEC64 = nullptr, *VZ = nullptr;
   float* VEC32 = nullptr;
   long vstride = 0;  // offset of the -eps copy read by the LN kernels (0: lora_only)
@@ -232,6 +237,14 @@ void build_sampler_plan(zo_ctx* c, SamplerPlan& P, std::vector<StreamDesc>& sd) 
   ZO_CUDA_TRY(cudaMemcpy(P.d_chunk_stream, chunk_stream.data(), chunk_stream.size() * 4, cudaMemcpyHostToDevice));
 }
 
+// OPT biases in a GEMM epilogue; rows of the -eps probe read the second fp32 copy
+// (the VectorProbe -1 values under full scope, identical otherwise)
+void set_bias(const zo_ctx* c, GemmDesc& g, const float* bias, int rows_per_sign) {
+  g.bias = bias;
+  g.bias_rps = rows_per_sign;
+  g.bias_vstride = c->vstride;
+}
+
 RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
   const int key = 2 * M + (nsign == 1 ? 1 : 0);
   auto it = c->plans.find(key);
@@ -263,6 +276,11 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
     }
     gemm_plan(lp.down, c->gA, M, ldg, w.W16, d, w.ldw, 4 * d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
               c->num_sms);
+    set_bias(c, lp.qkv, c->bqkv[l], M / nsign);
+    set_bias(c, lp.out, c->bout[l], M / nsign);
+    set_bias(c, lp.up, c->bup[l], M / nsign);
+    set_bias(c, lp.down, c->bdown[l], M / nsign);
+    lp.up.relu = c->opt ? 1 : 0;
     if (c->streamk)
       for (GemmDesc* g : {&lp.qkv, &lp.out, &lp.up, &lp.down}) gemm_enable_streamk(*g, c->sk_ws, c->sk_flags, c->num_sms);
     if (!c->fused_ext) {
@@ -303,12 +321,17 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
     rp.last_up.tpart = c->tpart;
     gemm_plan(rp.last_down, c->gS, S, ldg, w.W16, d, w.ldw, 4 * d + c->ext_used, EPI_RESID32, c->bf16, c->x32S, d,
               c->num_sms);
+    set_bias(c, rp.last_out, c->bout[L], S / nsign);
+    set_bias(c, rp.last_up, c->bup[L], S / nsign);
+    set_bias(c, rp.last_down, c->bdown[L], S / nsign);
+    rp.last_up.relu = c->opt ? 1 : 0;
     rp.pruned = true;
   }
   return c->plans.emplace(key, std::move(rp)).first->second;
 }
 
 void refresh_shadow(zo_ctx* c, const Matrix& m) {
+  if (m.kind == K_POS) return;
   if (m.kind == K_EMBED)
     launch_shadow(m.W64, m.m * m.n, m.W16, c->bf16, c->st);
   else
@@ -328,11 +351,20 @@ void do_score(zo_ctx* c, int B, int nsign) {
   const Matrix& e = c->mats[c->i_embed];
   const int rps = B * T;
   const int ldh = d + c->KE, ldg = 4 * d + c->KE;
+  PosEmbed pos;
+  if (c->opt) {  // learned positions at offset 2 (+ their LoRA delta)
+    const Matrix& pm = c->mats[c->i_pos];
+    pos.W64 = pm.W64;
+    pos.Pp = c->Pp + pm.u_off;
+    pos.Pm = c->Pm + pm.u_off;
+    pos.V32 = c->V32 + pm.v_off;
+    pos.offset = 2;
+  }
   launch_embed(c->x32, c->tok, B, T, d, e.W64, e.W16, c->bf16, c->Pp + e.u_off, c->Pm + e.u_off, c->V32 + e.v_off,
-               c->r, c->pe, M, c->st);
+               c->r, c->pe, pos, M, c->st);
   if (!c->fused_ext)  // high rank: 16-bit transposed probe operands of the extension GEMMs
     for (const auto& m : c->mats) {
-      if (m.kind == K_EMBED) continue;
+      if (m.kind == K_EMBED || m.kind == K_POS) continue;
       launch_p16t(c->Pp + m.u_off, (int)m.m, c->r, c->P16T + m.u_off, c->bf16, c->st);
       if (nsign == 2) launch_p16t(c->Pm + m.u_off, (int)m.m, c->r, c->P16T + c->su + m.u_off, c->bf16, c->st);
     }
@@ -435,12 +467,12 @@ void launch_dense_update_dev(zo_ctx* c, double lr) {
 
 // full scope: fp32 LN copies for the probe pair (eps) or the plain params (eps = 0)
 void vec_probe(zo_ctx* c, double eps) {
-  if (c->full_scope) launch_vec_probe(c->VEC64, c->VZ, (int64_t)c->nv * c->d.dim, eps, c->VEC32, c->st);
+  if (c->full_scope) launch_vec_probe(c->VEC64, c->VZ, c->nvt, eps, c->VEC32, c->st);
 }
 // full scope: VectorProbe.update with the coefficient in out4 (device)
 void vec_update(zo_ctx* c, const double* out4, double lr, const unsigned* abort_flag) {
   if (c->full_scope)
-    launch_vec_update(c->VEC64, c->VZ, (int64_t)c->nv * c->d.dim, out4, lr, abort_flag, c->VEC32, c->st);
+    launch_vec_update(c->VEC64, c->VZ, c->nvt, out4, lr, abort_flag, c->VEC32, c->st);
 }
 void sample_z(zo_ctx* c, uint64_t seed) {
   if (c->full_scope) sampler_launch(c->planZ, seed, c->d_step, 1, c->VZ, c->st);
@@ -483,6 +515,9 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->bf16 = d.precision == ZO_PREC_BF16;
   check(d.scope == ZO_SCOPE_LORA_ONLY || d.scope == ZO_SCOPE_FULL, ZO_ERR_CONFIG, "unknown scope");
   c->full_scope = d.scope == ZO_SCOPE_FULL;
+  check(d.arch == ZO_ARCH_ZOSERVE || d.arch == ZO_ARCH_OPT, ZO_ERR_CONFIG, "unknown architecture");
+  c->opt = d.arch == ZO_ARCH_OPT;
+  if (c->opt) check(d.max_pos >= c->T, ZO_ERR_DIMENSION, "max_pos shorter than the sequence");
   // rank <= 8: fused fp32 extension dots carried as (hi, lo, hi) 16-bit columns; above:
   // one 16-bit column per rank from the tensor-core extension GEMM
   c->ext_terms = d.rank <= 8 ? 3 : 1;
@@ -505,6 +540,7 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
     ms.push_back(x);
   };
   add("embed", K_EMBED, -1, d.vocab, D);
+  if (c->opt) add("pos_embed", K_POS, -1, (int64_t)d.max_pos + 2, D);
   for (int l = 0; l < d.n_layers; ++l) {
     const std::string p = "blk" + std::to_string(l) + ".";
     add(p + "qkv", K_QKV, l, D, 3 * D);
@@ -529,6 +565,7 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   for (size_t i = 0; i < c->mats.size(); ++i) {
     Matrix& m = c->mats[i];
     if (m.kind == K_EMBED) c->i_embed = (int)i;
+    if (m.kind == K_POS) c->i_pos = (int)i;
     if (m.kind == K_QKV) c->i_qkv[m.layer] = (int)i;
     if (m.kind == K_OUT) c->i_out[m.layer] = (int)i;
     if (m.kind == K_UP) c->i_up[m.layer] = (int)i;
@@ -540,6 +577,9 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
     if (m.kind == K_EMBED) {
       m.ldw = (int)m.n;
       m.W16 = c->mem.get<uint16_t>((size_t)(m.m * m.n));
+    } else if (m.kind == K_POS) {  // read as float64 by the embedding gather: no 16-bit copy
+      m.ldw = (int)m.n;
+      m.W16 = nullptr;
     } else {
       m.ldw = (int)(m.m + c->KE);
       m.W16 = c->mem.get<uint16_t>((size_t)(m.n * m.ldw));
@@ -552,29 +592,45 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->Pp = c->mem.get<float>(c->su);
   c->Pm = c->mem.get<float>(c->su);
   c->V32 = c->mem.get<float>(c->sv);
-  // 1-D params (identity at init, model.py:100-107), sorted ids
-  for (int l = 0; l < d.n_layers; ++l)
-    for (const char* w : {"ln1.scale", "ln1.shift", "ln2.scale", "ln2.shift"})
-      c->vids.push_back("blk" + std::to_string(l) + "." + w);
-  c->vids.push_back("ln_f.scale");
-  c->vids.push_back("ln_f.shift");
-  std::sort(c->vids.begin(), c->vids.end());
+  // 1-D params (identity at init, model.py:100-107; OPT biases zero), sorted ids
+  {
+    std::vector<std::pair<std::string, int64_t>> vs;
+    for (int l = 0; l < d.n_layers; ++l) {
+      const std::string p = "blk" + std::to_string(l) + ".";
+      for (const char* w : {"ln1.scale", "ln1.shift", "ln2.scale", "ln2.shift"}) vs.push_back({p + w, D});
+      if (c->opt) {
+        vs.push_back({p + "qkv.bias", 3 * D});
+        vs.push_back({p + "attn_out.bias", D});
+        vs.push_back({p + "ff_up.bias", 4 * D});
+        vs.push_back({p + "ff_down.bias", D});
+      }
+    }
+    vs.push_back({"ln_f.scale", D});
+    vs.push_back({"ln_f.shift", D});
+    std::sort(vs.begin(), vs.end());
+    for (auto& v : vs) {
+      c->vids.push_back(v.first);
+      c->voff.push_back(c->nvt);
+      c->vlen.push_back(v.second);
+      c->nvt += v.second;
+    }
+  }
   c->nv = (int)c->vids.size();
-  const size_t nvd = (size_t)c->nv * d.dim;
+  const size_t nvd = (size_t)c->nvt;
   c->VEC64 = c->mem.get<double>(nvd);
   c->VEC32 = c->mem.get<float>(2 * nvd);
   {
     std::vector<double> init(nvd, 0.0);
     for (int v = 0; v < c->nv; ++v)
       if (c->vids[v].size() >= 6 && c->vids[v].compare(c->vids[v].size() - 6, 6, ".scale") == 0)
-        std::fill(init.begin() + (size_t)v * d.dim, init.begin() + (size_t)(v + 1) * d.dim, 1.0);
+        std::fill(init.begin() + c->voff[v], init.begin() + c->voff[v] + c->vlen[v], 1.0);
     ZO_CUDA_TRY(cudaMemcpy(c->VEC64, init.data(), nvd * 8, cudaMemcpyHostToDevice));
     launch_vec_probe(c->VEC64, nullptr, (int64_t)nvd, 0.0, c->VEC32, nullptr);
     ZO_CUDA_TRY(cudaDeviceSynchronize());
   }
   auto vptr = [&](const std::string& id) {
     const int v = (int)(std::lower_bound(c->vids.begin(), c->vids.end(), id) - c->vids.begin());
-    return c->VEC32 + (size_t)v * d.dim;
+    return c->VEC32 + c->voff[v];
   };
   for (int l = 0; l < d.n_layers; ++l) {
     const std::string p = "blk" + std::to_string(l) + ".";
@@ -582,6 +638,10 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
     c->ln1b.push_back(vptr(p + "ln1.shift"));
     c->ln2g.push_back(vptr(p + "ln2.scale"));
     c->ln2b.push_back(vptr(p + "ln2.shift"));
+    c->bqkv.push_back(c->opt ? vptr(p + "qkv.bias") : nullptr);
+    c->bout.push_back(c->opt ? vptr(p + "attn_out.bias") : nullptr);
+    c->bup.push_back(c->opt ? vptr(p + "ff_up.bias") : nullptr);
+    c->bdown.push_back(c->opt ? vptr(p + "ff_down.bias") : nullptr);
   }
   c->lnfg = vptr("ln_f.scale");
   c->lnfb = vptr("ln_f.shift");
@@ -663,8 +723,8 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
       sz.lid_hash = fnv(c->vids[v].data(), c->vids[v].size(), FNV0);
       sz.role = 2;  // Role.DENSE_Z
       sz.step_mode = STEP_CURRENT;
-      sz.n = (uint64_t)d.dim;
-      sz.out_off = (uint64_t)v * d.dim;
+      sz.n = (uint64_t)c->vlen[v];
+      sz.out_off = (uint64_t)c->voff[v];
       sz.scale = 1.0;
       c->streamsZ.push_back(sz);
     }
@@ -788,24 +848,25 @@ static int vector_index(const zo_ctx* c, const char* lid) {
 
 int zo_upload_vector(zo_ctx* c, const char* lid, const double* host, int64_t n) {
   ZO_API_BEGIN
-  check(n == c->d.dim, ZO_ERR_DIMENSION, "vector length must equal dim");
   const int v = vector_index(c, lid);
-  const size_t nvd = (size_t)c->nv * n;
-  ZO_CUDA_TRY(cudaMemcpy(c->VEC64 + (size_t)v * n, host, n * 8, cudaMemcpyHostToDevice));
+  check(n == c->vlen[v], ZO_ERR_DIMENSION, std::string("vector length mismatch for ") + lid);
+  const size_t nvd = (size_t)c->nvt, o = (size_t)c->voff[v];
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  ZO_CUDA_TRY(cudaMemcpy(c->VEC64 + o, host, n * 8, cudaMemcpyHostToDevice));
   std::vector<float> f(n);
   for (int64_t i = 0; i < n; ++i) f[i] = (float)host[i];
-  ZO_CUDA_TRY(cudaMemcpy(c->VEC32 + (size_t)v * n, f.data(), n * 4, cudaMemcpyHostToDevice));
-  ZO_CUDA_TRY(cudaMemcpy(c->VEC32 + nvd + (size_t)v * n, f.data(), n * 4, cudaMemcpyHostToDevice));
+  ZO_CUDA_TRY(cudaMemcpy(c->VEC32 + o, f.data(), n * 4, cudaMemcpyHostToDevice));
+  ZO_CUDA_TRY(cudaMemcpy(c->VEC32 + nvd + o, f.data(), n * 4, cudaMemcpyHostToDevice));
   return ZO_OK;
   ZO_API_END
 }
 
 int zo_download_vector(zo_ctx* c, const char* lid, double* host, int64_t n) {
   ZO_API_BEGIN
-  check(n == c->d.dim, ZO_ERR_DIMENSION, "vector length must equal dim");
   const int v = vector_index(c, lid);
+  check(n == c->vlen[v], ZO_ERR_DIMENSION, std::string("vector length mismatch for ") + lid);
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
-  ZO_CUDA_TRY(cudaMemcpy(host, c->VEC64 + (size_t)v * n, n * 8, cudaMemcpyDeviceToHost));
+  ZO_CUDA_TRY(cudaMemcpy(host, c->VEC64 + c->voff[v], n * 8, cudaMemcpyDeviceToHost));
   return ZO_OK;
   ZO_API_END
 }
@@ -873,7 +934,7 @@ int zo_sample_stream(zo_ctx* c, uint64_t seed, uint64_t step, uint64_t lid_hash,
 
 int zo_slot_count(const zo_ctx* c, int32_t which, int64_t* count) {
   if (which < 0 || which > 3 || (which == 3 && !c->full_scope)) return ZO_ERR_INPUT;
-  *count = which == 3 ? (int64_t)c->nv * c->d.dim : which == 1 ? c->sv : c->su;
+  *count = which == 3 ? c->nvt : which == 1 ? c->sv : c->su;
   return ZO_OK;
 }
 
@@ -881,7 +942,7 @@ static double* slot_ptr(zo_ctx* c, int which) {
   return which == 0 ? c->U : which == 1 ? c->V : which == 2 ? c->A : c->VZ;
 }
 static int64_t slot_size(const zo_ctx* c, int which) {
-  return which == 3 ? (int64_t)c->nv * c->d.dim : which == 1 ? c->sv : c->su;
+  return which == 3 ? c->nvt : which == 1 ? c->sv : c->su;
 }
 
 int zo_get_slot(zo_ctx* c, int32_t which, double* host, int64_t count) {
@@ -1270,9 +1331,9 @@ void baseline_pass(zo_ctx* c, int pass, double eps, bool recompute) {
   }
   if (c->full_scope) {  // VectorProbe.set_sign(+1 / -1 / 0) (zo_engine.py:278-286)
     if (pass == 2)
-      launch_vec_probe(c->VEC64, c->VZ, (int64_t)c->nv * c->d.dim, 0.0, c->VEC32, c->st);
+      launch_vec_probe(c->VEC64, c->VZ, c->nvt, 0.0, c->VEC32, c->st);
     else
-      launch_vec_probe_sign(c->VEC64, c->VZ, (int64_t)c->nv * c->d.dim, eps, pass == 0 ? 1 : -1, c->VEC32, c->st);
+      launch_vec_probe_sign(c->VEC64, c->VZ, c->nvt, eps, pass == 0 ? 1 : -1, c->VEC32, c->st);
   }
 }
 void baseline_update(zo_ctx* c, double lr, bool recompute) {

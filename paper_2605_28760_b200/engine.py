@@ -20,6 +20,24 @@ PRECISIONS = {"fp16": _lib.PREC_FP16, "bf16": _lib.PREC_BF16}
 ALIASES = {"real64": "fp16", "real32": "fp16"}
 ESTIMATORS = {"lozo_lazy": _lib.EST_LOZO, "factorized_sqrt_r": _lib.EST_FACTORIZED}
 SCOPES = {"lora_only": _lib.SCOPE_LORA_ONLY, "full": _lib.SCOPE_FULL}
+ARCHS = {"zoserve": _lib.ARCH_ZOSERVE, "opt": _lib.ARCH_OPT}
+
+
+def vector_shapes(n_layers: int, dim: int, arch: str = "zoserve") -> dict[str, int]:
+    """1-D params and their lengths (model.py:100-107; OPT adds the projection biases)."""
+    out = {}
+    for i in range(n_layers):
+        for ln in ("ln1", "ln2"):
+            out[f"blk{i}.{ln}.scale"] = dim
+            out[f"blk{i}.{ln}.shift"] = dim
+        if arch == "opt":
+            out[f"blk{i}.qkv.bias"] = 3 * dim
+            out[f"blk{i}.attn_out.bias"] = dim
+            out[f"blk{i}.ff_up.bias"] = 4 * dim
+            out[f"blk{i}.ff_down.bias"] = dim
+    out["ln_f.scale"] = dim
+    out["ln_f.shift"] = dim
+    return out
 
 U, V, A, Z = 0, 1, 2, 3  # slot arenas (Z: full-scope 1-D directions)
 
@@ -34,12 +52,17 @@ def resolve_precision(precision: str) -> str:
 class ZoEngine:
     def __init__(self, vocab: int, dim: int, n_layers: int, n_heads: int, prompt_len: int, *,
                  opt_len: int = 1, max_batch: int = 16, rank: int = 2, estimator: str = "lozo_lazy",
-                 precision: str = "fp16", device: int = 0, scope: str = "lora_only"):
+                 precision: str = "fp16", device: int = 0, scope: str = "lora_only", arch: str = "zoserve",
+                 max_pos: int = 2048):
         if estimator not in ESTIMATORS:
             raise ConfigError(f"estimator {estimator!r} has no device engine")
         if scope not in SCOPES:
             raise ConfigError(f"scope must be one of {tuple(SCOPES)}, got {scope!r}")
+        if arch not in ARCHS:
+            raise ConfigError(f"arch must be one of {tuple(ARCHS)}, got {arch!r}")
         self.scope = scope
+        self.arch = arch
+        self.vlens = vector_shapes(n_layers, dim, arch)
         self.precision = resolve_precision(precision)
         self.estimator = estimator
         self.rank = rank
@@ -47,7 +70,8 @@ class ZoEngine:
         self.prompt_len, self.opt_len, self.max_batch = prompt_len, opt_len, max_batch
         self.T = prompt_len + opt_len
         desc = _lib.ZoModelDesc(vocab, dim, n_layers, n_heads, prompt_len, opt_len, max_batch, rank,
-                                ESTIMATORS[estimator], PRECISIONS[self.precision], device, SCOPES[scope])
+                                ESTIMATORS[estimator], PRECISIONS[self.precision], device, SCOPES[scope],
+                                ARCHS[arch], max_pos)
         h = ctypes.c_void_p()
         check(lib().zo_create(ctypes.byref(h), ctypes.byref(desc)))
         self._h = h
@@ -109,15 +133,15 @@ class ZoEngine:
                 check(lib().zo_upload_vector(self._h, lid.encode(), w.ctypes.data, w.shape[0]))
 
     def download_vector(self, lid: str) -> np.ndarray:
-        out = np.empty(self.dim, dtype=np.float64)
-        check(lib().zo_download_vector(self._h, lid.encode(), out.ctypes.data, self.dim))
+        n = self.vlens.get(lid, self.dim)
+        out = np.empty(n, dtype=np.float64)
+        check(lib().zo_download_vector(self._h, lid.encode(), out.ctypes.data, n))
         return out
 
     @property
     def vids(self) -> list[str]:
         """1-D param ids in sorted order (model.py:124-125)."""
-        ids = [f"blk{i}.{ln}.{w}" for i in range(self.n_layers) for ln in ("ln1", "ln2") for w in ("scale", "shift")]
-        return sorted(ids + ["ln_f.scale", "ln_f.shift"])
+        return sorted(self.vlens)
 
     def update_vectors(self, lr: float) -> None:
         check(lib().zo_update_vectors(self._h, float(lr)))
@@ -136,7 +160,7 @@ class ZoEngine:
         check(lib().zo_sample_v(self._h, seed, step, nu))
 
     def get_slot(self, which: int) -> np.ndarray:
-        n = self.sv if which == V else (len(self.vids) * self.dim if which == Z else self.su)
+        n = self.sv if which == V else (sum(self.vlens.values()) if which == Z else self.su)
         out = np.empty(n, dtype=np.float64)
         check(lib().zo_get_slot(self._h, which, out.ctypes.data, n))
         return out
@@ -178,8 +202,9 @@ class ZoEngine:
             z = np.ascontiguousarray(self.get_slot(Z) if z_arena is None else z_arena)
             vids = self.vids
             names = (ctypes.c_char_p * len(vids))(*[v.encode() for v in vids])
-            zo = (ctypes.c_int64 * len(vids))(*[i * self.dim for i in range(len(vids))])
-            zc = (ctypes.c_int64 * len(vids))(*[self.dim] * len(vids))
+            lens = [self.vlens[v] for v in vids]
+            zo = (ctypes.c_int64 * len(vids))(*[sum(lens[:i]) for i in range(len(vids))])
+            zc = (ctypes.c_int64 * len(vids))(*lens)
             h = int(lib().zo_digest_chain(names, z.ctypes.data, zo, zc, len(vids), h))
         return h
 

@@ -15,7 +15,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .engine import ZoEngine, resolve_precision
+from .engine import ZoEngine, resolve_precision, vector_shapes
 from .errors import ConfigError, DimensionError, InputError
 from .numerics import (Role, StreamKey, canonical_mean, digest_array, digest_bytes, digest_hex, digest_text,
                        sample_indices)
@@ -30,7 +30,14 @@ __all__ = [
 @dataclass(frozen=True)
 class ModelConfig:
     """Decoder shape (model.py:62-81): pre-LN, packed qkv, GELU-tanh FFN (4d),
-    sinusoidal positions, no biases, tied head."""
+    sinusoidal positions, no biases, tied head.
+
+    ``arch="opt"`` (no reference counterpart) is the OPT
+    family's decoder that real checkpoints load into (opt_io.py): ReLU FFN,
+    learned positions ``pos_embed`` [max_positions + 2, dim] read at offset 2,
+    biases on qkv / attn_out / ff_up / ff_down, pre-LN, tied head.  Its extra 2-D
+    param joins the LoRA scope like every other matrix (matrix_ids rule,
+    model.py:120-121); the biases are 1-D (full scope)."""
     vocab: int = 64
     dim: int = 32
     n_layers: int = 2
@@ -38,8 +45,14 @@ class ModelConfig:
     prompt_len: int = 16
     init_seed: int = 7
     init_scale: float = 0.08
+    arch: str = "zoserve"
+    max_positions: int = 2048
 
     def __post_init__(self) -> None:
+        if self.arch not in ("zoserve", "opt"):
+            raise ConfigError(f"arch must be 'zoserve' or 'opt', got {self.arch!r}")
+        if self.arch == "opt" and self.max_positions <= self.prompt_len:
+            raise ConfigError("max_positions must exceed prompt_len")
         if self.dim % self.n_heads != 0:
             raise ConfigError(f"dim {self.dim} not divisible by n_heads {self.n_heads}")
         if self.vocab < 8:
@@ -48,12 +61,18 @@ class ModelConfig:
             raise ConfigError("model dimensions must be positive")
 
     def digest(self) -> str:
-        return digest_hex(digest_text(json.dumps(self.__dict__, sort_keys=True)))
+        d = dict(self.__dict__)
+        if d["arch"] == "zoserve":  # the reference's ModelConfig fields only (model.py:62-81)
+            d.pop("arch")
+            d.pop("max_positions")
+        return digest_hex(digest_text(json.dumps(d, sort_keys=True)))
 
 
 def matrix_shapes(cfg: ModelConfig) -> dict[str, tuple[int, int]]:
     d = cfg.dim
     out = {"embed": (cfg.vocab, d)}
+    if cfg.arch == "opt":
+        out["pos_embed"] = (cfg.max_positions + 2, d)
     for i in range(cfg.n_layers):
         out[f"blk{i}.qkv"] = (d, 3 * d)
         out[f"blk{i}.attn_out"] = (d, d)
@@ -63,14 +82,9 @@ def matrix_shapes(cfg: ModelConfig) -> dict[str, tuple[int, int]]:
 
 
 def _vector_defaults(cfg: ModelConfig) -> dict[str, np.ndarray]:
-    out = {}
-    for i in range(cfg.n_layers):
-        for ln in ("ln1", "ln2"):
-            out[f"blk{i}.{ln}.scale"] = np.ones(cfg.dim)
-            out[f"blk{i}.{ln}.shift"] = np.zeros(cfg.dim)
-    out["ln_f.scale"] = np.ones(cfg.dim)
-    out["ln_f.shift"] = np.zeros(cfg.dim)
-    return out
+    """LN scale 1 / shift 0 (model.py:100-107); OPT biases 0."""
+    return {k: (np.ones(n) if k.endswith(".scale") else np.zeros(n))
+            for k, n in vector_shapes(cfg.n_layers, cfg.dim, cfg.arch).items()}
 
 
 class DeviceParams(Mapping):
@@ -164,7 +178,8 @@ class DeviceParams(Mapping):
             return e
         c = self.cfg
         e = ZoEngine(c.vocab, c.dim, c.n_layers, c.n_heads, c.prompt_len, opt_len=opt_len, max_batch=mb,
-                     rank=rank, estimator=estimator, precision=self.precision, device=self.device, scope=scope)
+                     rank=rank, estimator=estimator, precision=self.precision, device=self.device, scope=scope,
+                     arch=c.arch, max_pos=c.max_positions)
         if self._host is None:
             e.init_params(c.init_seed, c.init_scale)
         else:

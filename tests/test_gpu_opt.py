@@ -1,0 +1,148 @@
+"""OPT-architecture variant on the GPU: learned positions at
+offset 2 (+ their LoRA delta), projection biases in the tcgen05 GEMM epilogues, ReLU
+FFN.  Parity: per-example NLLs against Hugging Face transformers' OPTForCausalLM
+(tests/golden/forward_opt_micro.json, float64), and LoZO / full-scope trajectories
+against the oracle -- U/V/z digests and the float64 update + fold bit-exact given the
+oracle's coefficients, losses within the 16-bit tolerance."""
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from oracle import reference as R
+
+pytestmark = pytest.mark.gpu
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+from make_opt_golden import MICRO_OPT, MICRO_TASK, opt_params  # noqa: E402
+
+NLL_TOL = {"fp16": 2e-2, "bf16": 8e-2}
+
+
+def _load(golden_dir):
+    with open(os.path.join(golden_dir, "forward_opt_micro.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("precision", ["fp16", "bf16"])
+def test_opt_forward_vs_hf(golden_dir, precision):
+    from paper_2605_28760_b200.engine import ZoEngine
+    g = _load(golden_dir)
+    cfg = R.ModelCfg(**g["model"])
+    eng = ZoEngine(cfg.vocab, cfg.dim, cfg.n_layers, cfg.n_heads, cfg.prompt_len, max_batch=g["batch"],
+                   rank=g["rank"], precision=precision, arch="opt", max_pos=cfg.max_positions)
+    assert "pos_embed" in eng.lids
+    params = opt_params(R, cfg, g["vec_seed"], g["vec_scale"])
+    eng.upload(params)
+    step, r = g["step"], g["rank"]
+    eng.sample_v(g["zseed"], step, 50)
+    eng.sample_u(g["zseed"], step)
+    A = {lid: g["a_scale"] * R.gaussian(g["a_seed"], step, lid, R.ROLE_U, eng.shapes[lid][0], r) for lid in eng.lids}
+    eng.set_slot(2, eng.join(2, A))
+    tokens = np.asarray(g["tokens"])
+    gold = tokens[:, cfg.prompt_len:]
+    eng.prepare_probe(g["epsilon"], 0)
+    nll = eng.score(tokens, np.stack([gold, gold]), nsign=2)
+    eng.prepare_probe(g["epsilon"], 1)
+    nll0 = eng.score(tokens, gold, nsign=1)[0]
+    ref = {s: np.array(g["nll"][str(s)]) for s in (-1, 0, 1)}
+    tol = NLL_TOL[precision]
+    np.testing.assert_allclose(nll[0], ref[1], atol=tol, rtol=0)
+    np.testing.assert_allclose(nll[1], ref[-1], atol=tol, rtol=0)
+    np.testing.assert_allclose(nll0, ref[0], atol=tol, rtol=0)
+    d_ref = R.canonical_mean(ref[1]) - R.canonical_mean(ref[-1])
+    d_got = R.canonical_mean(nll[0]) - R.canonical_mean(nll[1])
+    os.makedirs("gpurun_out/parity", exist_ok=True)
+    with open(f"gpurun_out/parity/forward_opt_micro_{precision}.json", "w") as f:
+        json.dump({"max_abs_nll": float(max(np.abs(nll[0] - ref[1]).max(), np.abs(nll[1] - ref[-1]).max(),
+                                            np.abs(nll0 - ref[0]).max())),
+                   "dL_ref": d_ref, "dL_got": d_got}, f, indent=1)
+    assert abs(d_got - d_ref) <= max(0.1 * abs(d_ref), 5e-4), (d_got, d_ref)
+    eng.close()
+
+
+class _Replay:
+    def __init__(self, recs):
+        self.recs, self.calls = recs, 0
+
+    def __call__(self, batch):
+        r = self.recs[self.calls // 2]
+        v = r.loss_plus if self.calls % 2 == 0 else r.loss_minus
+        self.calls += 1
+        return v
+
+
+@pytest.mark.parametrize("scope", ["lora_only", "full"])
+def test_opt_lozo_bit_exact_with_oracle_coefficients(scope):
+    from paper_2605_28760_b200 import model as M
+    from paper_2605_28760_b200.adapter import AdapterState
+    from paper_2605_28760_b200.zo_engine import ZoConfig, lozo_step
+    rc = R.ModelCfg(**MICRO_OPT)
+    splits = R.generate_task(R.TaskCfg(**MICRO_TASK))
+    z = R.ZoCfg(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=3, batch_size=8, scope=scope)
+    steps = 5
+    host = opt_params(R, rc)
+    recs, final, _ = R.run_serving(rc, splits, z, steps, params={k: v.copy() for k, v in host.items()})
+    mcfg = M.ModelConfig(**MICRO_OPT)
+    task = M.generate_task(M.TaskConfig(**MICRO_TASK))
+    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=3, batch_size=8, scope=scope)
+    params = M.DeviceParams(mcfg, host={k: v.copy() for k, v in host.items()}, max_batch=8)
+    assert M.params_digest(params) == R.params_digest(host)
+    state = AdapterState(epsilon=zcfg.epsilon)
+    scorer = _Replay(recs)
+    for t, rec in enumerate(recs):
+        batch = M.sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
+        out = lozo_step(params, mcfg, state, zcfg, t, batch, scorer=scorer)
+        assert (out.u_digest, out.v_digest, out.minibatch_id) == (rec.u_digest, rec.v_digest, rec.minibatch_id)
+        assert out.beta == rec.beta
+        if (t + 1) % zcfg.nu == 0:
+            params.engine.fold()
+            params.invalidate()
+    params.engine.fold()
+    params.invalidate()
+    assert M.params_digest(params) == R.params_digest(final)
+
+
+def test_opt_serving_path_vs_oracle():
+    from paper_2605_28760_b200 import model as M
+    from paper_2605_28760_b200.runtime import run_serving_path
+    from paper_2605_28760_b200.zo_engine import ZoConfig
+    rc = R.ModelCfg(**MICRO_OPT)
+    splits = R.generate_task(R.TaskCfg(**MICRO_TASK))
+    z = R.ZoCfg(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=3, batch_size=8)
+    host = opt_params(R, rc)
+    recs, _, _ = R.run_serving(rc, splits, z, 6, params={k: v.copy() for k, v in host.items()})
+    mcfg = M.ModelConfig(**MICRO_OPT)
+    task = M.generate_task(M.TaskConfig(**MICRO_TASK))
+    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=3, batch_size=8)
+    run = run_serving_path(mcfg, task, zcfg, 6, eval_every=10**9,
+                           params=M.DeviceParams(mcfg, host={k: v.copy() for k, v in host.items()}, max_batch=8))
+    for a, b in zip(recs, run.trajectory):
+        assert (a.u_digest, a.v_digest, a.minibatch_id) == (b.u_digest, b.v_digest, b.minibatch_id)
+        assert abs(a.loss_plus - b.loss_plus) < 1.5e-2 and abs(a.loss_minus - b.loss_minus) < 1.5e-2
+
+
+def test_opt_materialising_loop_bit_exact_given_coefficients():
+    from paper_2605_28760_b200 import model as M
+    rc = R.ModelCfg(**MICRO_OPT)
+    splits = R.generate_task(R.TaskCfg(**MICRO_TASK))
+    z = R.ZoCfg(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=3, batch_size=8)
+    host = opt_params(R, rc)
+    recs, final = R.run_baseline(rc, splits, z, 4, params={k: v.copy() for k, v in host.items()})
+    mcfg = M.ModelConfig(**MICRO_OPT)
+    task = M.generate_task(M.TaskConfig(**MICRO_TASK))
+    params = M.DeviceParams(mcfg, host={k: v.copy() for k, v in host.items()}, max_batch=8)
+    eng = params.bind(2, "lozo_lazy", 8, 1, "lora_only")
+    for t, rec in enumerate(recs):
+        tokens, gold = M.sample_minibatch(task, "train", 42, t, 8).sequences()
+        eng.baseline_directions(42, t, 3)
+        for p in (0, 1):
+            eng.baseline_pass(p, 1e-3, False)
+            got = R.canonical_mean(eng.score(tokens, gold, nsign=1)[0])
+            assert abs(got - (rec.loss_plus if p == 0 else rec.loss_minus)) < 1.5e-2
+        eng.baseline_pass(2, 1e-3, False)
+        eng.set_coefficient([rec.loss_plus, rec.loss_minus, rec.coefficient, rec.beta])
+        eng.baseline_update(1e-3, False)
+    params.invalidate()
+    assert M.params_digest(params) == R.params_digest(final)
