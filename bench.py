@@ -163,6 +163,8 @@ def workload_config(args, world: int) -> tuple[dict, str, bool]:
     workload = (f"{args.model} factorized_sqrt_r (MeZO-style) r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, "
                 f"dense float64 update every step" if fact else
                 f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, nu={nu}, fold amortised")
+    if args.arch == "opt":
+        workload += ", OPT decoder (ReLU FFN, learned positions, projection biases)"
     cfg = {"workload": workload, "model": args.model, "global_batch": B, "seq_len": T,
            "parallelism": (f"qdir{world}" if qdir else f"exact-dp{world}") if world > 1 else "single",
            "l2": "inputs larger than L2 (25.7 GB 16-bit weights/step at 13B); no flush"}
@@ -213,6 +215,9 @@ def main():
                          "probe U V^T/sqrt(r), dense float64 update of every weight each step")
     ap.add_argument("--nu", type=int, default=50)
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
+    ap.add_argument("--arch", default="zoserve", choices=["zoserve", "opt"],
+                    help="decoder: the reference's (default, parity-backed) or the OPT family's "
+                         "(ReLU, learned positions, biases; real checkpoints load into it)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false", help="launch kernels eagerly (no CUDA graph)")
@@ -270,7 +275,8 @@ def main():
     Bl = B if qdir else B // world
     G = world if qdir else 1  # reference steps (directions) per timed step
     prompt_len = T - 1
-    mcfg = M.ModelConfig(vocab=mdl["vocab"], dim=mdl["dim"], n_layers=mdl["n_layers"], n_heads=mdl["n_heads"],
+    mcfg = M.ModelConfig(arch=args.arch, vocab=mdl["vocab"], dim=mdl["dim"], n_layers=mdl["n_layers"],
+                         n_heads=mdl["n_heads"],
                          prompt_len=prompt_len, init_seed=7, init_scale=0.02)
     tcfg = M.TaskConfig(seed=11, vocab=mdl["vocab"], prompt_len=prompt_len, train_size=1000, dev_size=4,
                         val_size=4)
@@ -282,7 +288,8 @@ def main():
     task = M.generate_task(tcfg)
     t_init = time.perf_counter()
     eng = ZoEngine(mcfg.vocab, mcfg.dim, mcfg.n_layers, mcfg.n_heads, prompt_len, opt_len=1, max_batch=Bl,
-                   rank=args.rank, estimator=args.estimator, precision=args.precision, device=local)
+                   rank=args.rank, estimator=args.estimator, precision=args.precision, device=local,
+                   arch=args.arch, max_pos=mcfg.max_positions)
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     eng.init_params(mcfg.init_seed, mcfg.init_scale)
