@@ -146,3 +146,33 @@ def test_opt_materialising_loop_bit_exact_given_coefficients():
         eng.baseline_update(1e-3, False)
     params.invalidate()
     assert M.params_digest(params) == R.params_digest(final)
+
+
+def test_load_hf_model_and_score_matches_transformers():
+    """A transformers OPTForCausalLM (random init, tiny config) loaded through opt_io:
+    the device NLLs at the loaded weights equal transformers' own float64 forward."""
+    torch = pytest.importorskip("torch")
+    tr = pytest.importorskip("transformers")
+    from paper_2605_28760_b200 import model as M
+    from paper_2605_28760_b200.opt_io import load_hf_opt
+    torch.manual_seed(0)
+    hc = tr.OPTConfig(vocab_size=96, hidden_size=64, num_hidden_layers=2, ffn_dim=256, num_attention_heads=4,
+                      max_position_embeddings=64, word_embed_proj_dim=64, do_layer_norm_before=True,
+                      activation_function="relu", dropout=0.0, attention_dropout=0.0, tie_word_embeddings=True)
+    hf = tr.OPTForCausalLM(hc).eval()
+    with torch.no_grad():  # non-trivial biases / LN params
+        for n, p in hf.named_parameters():
+            if p.ndim == 1:
+                p.add_(0.05 * torch.randn_like(p))
+    mcfg, params = load_hf_opt(hf, prompt_len=20, max_batch=8)
+    assert mcfg.arch == "opt" and mcfg.max_positions == 64
+    task = M.generate_task(M.TaskConfig(seed=3, vocab=96, prompt_len=20, train_size=32, dev_size=8, val_size=8))
+    batch = M.sample_minibatch(task, "train", 42, 0, 8)
+    tokens, gold = batch.sequences()
+    got = M.forward_nll(params, mcfg, batch.prompts, gold)
+    with torch.no_grad():
+        logits = hf.double()(input_ids=torch.from_numpy(np.asarray(tokens))).logits.numpy()
+    row = logits[:, mcfg.prompt_len - 1, :]
+    m = row.max(axis=-1)
+    ref = m + np.log(np.exp(row - m[:, None]).sum(axis=-1)) - row[np.arange(8), gold[:, 0]]
+    np.testing.assert_allclose(got, ref, atol=2e-2, rtol=0)
