@@ -111,14 +111,14 @@ void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, v
 }
 
 // ------------------------------------------------------------------ embed
-__global__ void k_embed(float* __restrict__ x32, const int32_t* __restrict__ tokens, int B, int T, int d,
+__global__ void k_embed(float* __restrict__ x32, const int32_t* __restrict__ tokens, int tok_ld, int B, int T, int d,
                         const double* __restrict__ E64, const void* __restrict__ E16, bool bf16,
                         const float* __restrict__ Pp, const float* __restrict__ Pm, const float* __restrict__ Ve,
                         int r, const float* __restrict__ pe, PosEmbed pos) {
   const int row = blockIdx.x;
   const int per_sign = B * T;
   const int s = row / per_sign, rem = row % per_sign, b = rem / T, t = rem % T;
-  const int tok = tokens[b * T + t];
+  const int tok = tokens[b * tok_ld + t];
   const float* P = (s == 0 ? Pp : Pm) + (size_t)tok * r;
   const size_t prow = (size_t)(t + pos.offset);
   const float* PP = pos.W64 ? (s == 0 ? pos.Pp : pos.Pm) + prow * r : nullptr;
@@ -138,10 +138,10 @@ __global__ void k_embed(float* __restrict__ x32, const int32_t* __restrict__ tok
   }
 }
 
-void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const double* E64, const void* E16,
-                  bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r, const float* pe,
-                  const PosEmbed& pos, int nrows, cudaStream_t st) {
-  k_embed<<<nrows, 256, 0, st>>>(x32, tokens, B, T, d, E64, E16, bf16, Pplus, Pminus, Ve32, r, pe, pos);
+void launch_embed(float* x32, const int32_t* tokens, int tok_ld, int B, int T, int d, const double* E64,
+                  const void* E16, bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r,
+                  const float* pe, const PosEmbed& pos, int nrows, cudaStream_t st) {
+  k_embed<<<nrows, 256, 0, st>>>(x32, tokens, tok_ld, B, T, d, E64, E16, bf16, Pplus, Pminus, Ve32, r, pe, pos);
 }
 
 // ------------------------------------------------------------------ LN (+ extension), warp per row

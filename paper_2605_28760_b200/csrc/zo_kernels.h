@@ -20,8 +20,9 @@ struct PosEmbed {
   int offset = 0;
 };
 // x32[M,d] = E[tok] + sum_k P_s[tok,k] V_e[:,k] + PE[t]   (model.py:180, adapter.py:200-234)
-void launch_embed(float* x32, const int32_t* tokens, int B, int T, int d, const double* E64, const void* E16,
-                  bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r,
+// for positions t < T of token rows tokens[b * tok_ld + t]
+void launch_embed(float* x32, const int32_t* tokens, int tok_ld, int B, int T, int d, const double* E64,
+                  const void* E16, bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r,
                   const float* pe, const PosEmbed& pos, int nrows, cudaStream_t st);
 // h = LN(x) (model.py:139-142) -> out[:, :d] (16-bit); ext columns [d, d+3r) = (t_hi, t_lo, t_hi)
 // per rank with t = h . P_s (fp32) -- the LoRA K-extension operand (A side).

@@ -88,7 +88,7 @@ struct DevAlloc {
 
 struct zo_ctx {
   zo_model_desc d{};
-  int T = 0, dh = 0, r = 0, ext_terms = 3, KE = 64, ext_used = 0, num_sms = 148;
+  int T = 0, Tf = 0, dh = 0, r = 0, ext_terms = 3, KE = 64, ext_used = 0, num_sms = 148;
   bool bf16 = false;
   cudaStream_t st = nullptr;
   DevAlloc mem;
@@ -252,7 +252,7 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
   RowPlan rp;
   const int d = c->d.dim;
   const int ldh = d + c->KE, ldg = 4 * d + c->KE;
-  const int S = M / c->T * c->d.opt_len;
+  const int S = M / c->Tf * c->d.opt_len;
   for (int l = 0; l < c->d.n_layers; ++l) {
     LayerPlan lp;
     const Matrix& q = c->mats[c->i_qkv[l]];
@@ -345,7 +345,7 @@ void write_vext_all(zo_ctx* c) {
 }
 
 void do_score(zo_ctx* c, int B, int nsign) {
-  const int d = c->d.dim, T = c->T, M = nsign * B * T;
+  const int d = c->d.dim, T = c->Tf, M = nsign * B * T;
   check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
   RowPlan& rp = row_plan(c, M, nsign);
   const Matrix& e = c->mats[c->i_embed];
@@ -360,7 +360,7 @@ void do_score(zo_ctx* c, int B, int nsign) {
     pos.V32 = c->V32 + pm.v_off;
     pos.offset = 2;
   }
-  launch_embed(c->x32, c->tok, B, T, d, e.W64, e.W16, c->bf16, c->Pp + e.u_off, c->Pm + e.u_off, c->V32 + e.v_off,
+  launch_embed(c->x32, c->tok, c->T, B, T, d, e.W64, e.W16, c->bf16, c->Pp + e.u_off, c->Pm + e.u_off, c->V32 + e.v_off,
                c->r, c->pe, pos, M, c->st);
   if (!c->fused_ext)  // high rank: 16-bit transposed probe operands of the extension GEMMs
     for (const auto& m : c->mats) {
@@ -510,6 +510,9 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   check(prop.major == 10, ZO_ERR_CUDA, std::string("libzob200 targets sm_100a (B200); found ") + prop.name);
   c->num_sms = prop.multiProcessorCount;
   c->T = d.prompt_len + d.opt_len;
+  // the forward runs positions [0, T-1): the last token is never attended by a scored row
+  // (rows prompt_len-1+j, j < opt_len, are causal), so its rows are not computed at all
+  c->Tf = c->T - 1;
   c->dh = d.dim / d.n_heads;
   c->r = d.rank;
   c->bf16 = d.precision == ZO_PREC_BF16;
@@ -1509,7 +1512,7 @@ extern "C" int zo_read_out4(zo_ctx* c, double* out4) {
 extern "C" int zo_bench_gemm(zo_ctx* c, int32_t which, int32_t B, int32_t reps, float* avg_ms, double* flops) {
   ZO_API_BEGIN
   check(which >= 0 && which <= 4 && reps >= 1, ZO_ERR_INPUT, "bad gemm id / reps");
-  const int M = 2 * B * c->T;
+  const int M = 2 * B * c->Tf;
   RowPlan& rp = row_plan(c, M);
   const GemmDesc& g = which == 0 ? rp.layers[0].qkv : which == 1 ? rp.layers[0].out
                     : which == 2 ? rp.layers[0].up : which == 3 ? rp.layers[0].down : rp.lm;
