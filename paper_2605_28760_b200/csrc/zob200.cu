@@ -488,6 +488,8 @@ void fold_all(zo_ctx* c) {
 
 }  // namespace
 
+static void graph_body(zo_ctx* c, uint64_t seed, double eps, double lr, int32_t divide_by_r, int32_t B);
+
 extern "C" {
 
 const char* zo_last_error(void) { return g_last_error.c_str(); }
@@ -1089,20 +1091,13 @@ int zo_step(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, dou
     write_vext_all(c);
     c->v_window = wstart;
   }
-  sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
-  sample_z(c, seed);
-  const double scale = lozo ? 1.0 : 1.0 / std::sqrt((double)c->r);
-  launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, eps, scale, c->Pp, c->Pm, c->st);
-  vec_probe(c, eps);
   ZO_CUDA_TRY(cudaEventRecord(c->ev[1], c->st));
-  do_score(c, B, 2);
-  launch_coefficient(c->nll, B, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
+  // U, probes, paired scoring, coefficient and update: the captured step body (bit-identical
+  // to eager launches, tests/test_gpu_scorer.py), one graph launch instead of ~370 kernel
+  // launches from the host
+  graph_body(c, seed, eps, lr, lozo ? divide_by_r : 0, B);
+  if (lozo) c->a_dirty = true;
   ZO_CUDA_TRY(cudaEventRecord(c->ev[2], c->st));
-  if (lozo) {
-    launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
-    c->a_dirty = true;
-  }
-  vec_update(c, c->out4, lr, c->abort_flag);
   ZO_CUDA_TRY(cudaMemcpyAsync(c->h_out4, c->out4, 32, cudaMemcpyDeviceToHost, c->st));
   ZO_CUDA_TRY(cudaEventRecord(c->ev[3], c->st));
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -1113,13 +1108,6 @@ int zo_step(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, dou
   if (out4) std::memcpy(out4, c->h_out4, 32);
   if (!std::isfinite(c->h_out4[0]) || !std::isfinite(c->h_out4[1]))
     throw Error(ZO_ERR_ABORT, "non-finite paired loss; step not applied");
-  if (!lozo) {
-    const double cc = c->h_out4[2];
-    const double alpha = (-(lr * cc)) * (1.0 / std::sqrt((double)c->r));
-    for (auto& m : c->mats)
-      launch_fold(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, alpha, m.W16,
-                  m.kind == K_EMBED ? (int)m.n : m.ldw, m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
-  }
   return ZO_OK;
   ZO_API_END
 }
@@ -1216,27 +1204,10 @@ static void step_body(zo_ctx* c, uint64_t seed, double eps, double lr, int32_t d
   vec_update(c, c->out4, lr, c->abort_flag);
 }
 
-// zo_step_async as one CUDA-graph launch: the ~370 kernels of the step body are
-// captured once per (seed, B, eps, lr, divide_by_r) and replayed; the step index,
-// token staging and window work (V resampling / fold) stay eager in front of it.
-extern "C" int zo_step_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr,
-                             int32_t divide_by_r, const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
-  ZO_API_BEGIN
-  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
-  check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
-  const bool lozo = c->d.estimator == ZO_EST_LOZO;
-  k_set_u64<<<1, 1, 0, c->st>>>(c->d_step, step);
-  ZO_CUDA_TRY(cudaMemcpyAsync(c->tok, tokens_dev, (size_t)B * c->T * 4, cudaMemcpyDeviceToDevice, c->st));
-  const size_t ng = (size_t)B * c->d.opt_len * 4;
-  ZO_CUDA_TRY(cudaMemcpyAsync(c->gold, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
-  ZO_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->gold) + ng, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
-  const int64_t wstart = lozo ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
-  if (!lozo || wstart != c->v_window) {
-    if (lozo && c->a_dirty) fold_all(c);
-    sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
-    write_vext_all(c);
-    c->v_window = wstart;
-  }
+// The step body as one CUDA-graph launch: captured once per (seed, B, eps, lr,
+// divide_by_r) -- the first use of a key runs eagerly (warming plans / attributes),
+// then captures -- and replayed afterwards.
+static void graph_body(zo_ctx* c, uint64_t seed, double eps, double lr, int32_t divide_by_r, int32_t B) {
   const zo_ctx::GKey key{seed, B, divide_by_r, eps, lr};
   if (!c->gkey_valid || !(key == c->gkey)) {
     // first use of this key: run eagerly (also warms attributes/plans), then capture
@@ -1280,6 +1251,30 @@ extern "C" int zo_step_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu
   } else {
     ZO_CUDA_TRY(cudaGraphLaunch(c->gexec, c->st));
   }
+}
+
+// zo_step_async as one CUDA-graph launch: the ~370 kernels of the step body are
+// captured once per (seed, B, eps, lr, divide_by_r) and replayed; the step index,
+// token staging and window work (V resampling / fold) stay eager in front of it.
+extern "C" int zo_step_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr,
+                             int32_t divide_by_r, const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
+  ZO_API_BEGIN
+  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
+  check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  k_set_u64<<<1, 1, 0, c->st>>>(c->d_step, step);
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->tok, tokens_dev, (size_t)B * c->T * 4, cudaMemcpyDeviceToDevice, c->st));
+  const size_t ng = (size_t)B * c->d.opt_len * 4;
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->gold, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
+  ZO_CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(c->gold) + ng, gold_dev, ng, cudaMemcpyDeviceToDevice, c->st));
+  const int64_t wstart = lozo ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
+  if (!lozo || wstart != c->v_window) {
+    if (lozo && c->a_dirty) fold_all(c);
+    sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
+    write_vext_all(c);
+    c->v_window = wstart;
+  }
+  graph_body(c, seed, eps, lr, divide_by_r, B);
   if (lozo) c->a_dirty = true;
   return ZO_OK;
   ZO_API_END
