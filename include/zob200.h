@@ -206,6 +206,12 @@ uint64_t zo_digest_chain(const char* const* lids, const double* arena, const int
 /* measurement: average ms of one launch of a layer GEMM at batch B
  * (which: 0 qkv, 1 attn_out, 2 ff_up, 3 ff_down, 4 LM head) and its FLOPs */
 int zo_bench_gemm(zo_ctx* ctx, int32_t which, int32_t B, int32_t reps, float* avg_ms, double* flops);
+/* one eager zo_step_async (device inputs, divide_by_r = 0) with a CUDA event in front of every
+ * scorer kernel group; ms[10] = device ms per family summed over the layers: embed, LN, qkv GEMM,
+ * attention, extension finalize, attn_out GEMM, ff_up GEMM, ff_down GEMM, last-layer tail + LM
+ * head + loss, other (sampler, probes, coefficient, update).  The bench's in-step roofline. */
+int zo_profile_step(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon, double lr,
+                    const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B, float* ms);
 /* copy per-example NLLs between the ctx and an external device buffer
  * (to_ctx = 1: dev -> ctx) -- the multi-GPU exact-mode exchange point */
 int zo_nll_io(zo_ctx* ctx, void* dev, int32_t count, int32_t to_ctx);

@@ -148,6 +148,12 @@ struct zo_ctx {
   bool fused_ext = true;
   // timing
   cudaEvent_t ev[4];
+  // in-step kernel-family profile (zo_profile_step): an event before each launch group,
+  // the interval up to the next mark is charged to the group's family
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<int> prof_kind;
+  size_t prof_n = 0;
   float last_ms[3] = {0, 0, 0};
   double probe_eps = 0.0, probe_scale = 1.0;
   int64_t v_window = -1;  // window start whose V is loaded (-1: none)
@@ -176,6 +182,7 @@ struct zo_ctx {
     if (h_step) cudaFreeHost(h_step);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    for (auto& e : prof_ev) cudaEventDestroy(e);
   }
 };
 
@@ -344,6 +351,19 @@ void write_vext_all(zo_ctx* c) {
                       c->bf16, c->ext_terms, c->V32 + m.v_off, c->st);
 }
 
+enum ProfKind { PK_EMBED = 0, PK_LN, PK_QKV, PK_ATTN, PK_EXT, PK_OUT, PK_UP, PK_DOWN, PK_TAIL, PK_OTHER, PK_N };
+void prof_mark(zo_ctx* c, int kind) {
+  if (!c->prof_on) return;
+  if (c->prof_n == c->prof_ev.size()) {
+    cudaEvent_t e;
+    ZO_CUDA_TRY(cudaEventCreate(&e));
+    c->prof_ev.push_back(e);
+    c->prof_kind.push_back(0);
+  }
+  ZO_CUDA_TRY(cudaEventRecord(c->prof_ev[c->prof_n], c->st));
+  c->prof_kind[c->prof_n++] = kind;
+}
+
 void do_score(zo_ctx* c, int B, int nsign) {
   const int d = c->d.dim, T = c->Tf, M = nsign * B * T;
   check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
@@ -360,6 +380,7 @@ void do_score(zo_ctx* c, int B, int nsign) {
     pos.V32 = c->V32 + pm.v_off;
     pos.offset = 2;
   }
+  prof_mark(c, PK_EMBED);
   launch_embed(c->x32, c->tok, c->T, B, T, d, e.W64, e.W16, c->bf16, c->Pp + e.u_off, c->Pm + e.u_off, c->V32 + e.v_off,
                c->r, c->pe, pos, M, c->st);
   if (!c->fused_ext)  // high rank: 16-bit transposed probe operands of the extension GEMMs
@@ -377,9 +398,11 @@ void do_score(zo_ctx* c, int B, int nsign) {
     const Matrix& u = c->mats[c->i_up[l]];
     const Matrix& w = c->mats[c->i_down[l]];
     const LayerPlan& lp = rp.layers[l];
+    prof_mark(c, PK_LN);
     launch_ln_ext(c->x32, c->ln1g[l], c->ln1b[l], M, d, c->hA, ldh, c->bf16, c->Pp + q.u_off, c->Pm + q.u_off,
                   c->fused_ext ? c->r : 0, rps, c->ext_terms, c->vstride, c->st);
     if (!c->fused_ext) ext_gemm(lp, 0);
+    prof_mark(c, PK_QKV);
     gemm_launch(lp.qkv, c->st);
     AttnExt ax;
     if (c->fused_ext) {
@@ -390,11 +413,13 @@ void do_score(zo_ctx* c, int B, int nsign) {
       ax.ld = c->Mpad;
       ax.tpart = c->tpart;
     }
+    prof_mark(c, PK_ATTN);
     launch_attention(c->qkv, 3 * d, c->ctxA, ldh, nsign * B, T, c->d.n_heads, c->dh, c->bf16, ax, c->st);
     if (rp.pruned && l == c->d.n_layers - 1) {
       // scored rows only from here (RowPlan::pruned): compact ctx (+ extension columns)
       // and residual rows, then attn_out / LN2 / FFN on S rows
       const int S = nsign * B * c->d.opt_len;
+      prof_mark(c, PK_TAIL);
       launch_ext_finalize(c->tpart, c->d.n_heads, c->Mpad, M, c->r, c->ctxA, ldh, d, c->ext_terms, c->bf16, c->st);
       launch_gather_scored(c->ctxA, (size_t)ldh * 2, c->hS, (size_t)ldh * 2, ldh * 2, nsign, B, T, c->d.prompt_len,
                            c->d.opt_len, c->st);
@@ -409,22 +434,29 @@ void do_score(zo_ctx* c, int B, int nsign) {
       gemm_launch(rp.last_down, c->st);
       break;
     }
+    prof_mark(c, PK_EXT);
     if (c->fused_ext)
       launch_ext_finalize(c->tpart, c->d.n_heads, c->Mpad, M, c->r, c->ctxA, ldh, d, c->ext_terms, c->bf16, c->st);
     else
       ext_gemm(lp, 1);
+    prof_mark(c, PK_OUT);
     gemm_launch(lp.out, c->st);
+    prof_mark(c, PK_LN);
     launch_ln_ext(c->x32, c->ln2g[l], c->ln2b[l], M, d, c->hA, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off,
                   c->fused_ext ? c->r : 0, rps, c->ext_terms, c->vstride, c->st);
     if (!c->fused_ext) ext_gemm(lp, 2);
+    prof_mark(c, PK_UP);
     gemm_launch(lp.up, c->st);
+    prof_mark(c, PK_EXT);
     if (c->fused_ext)
       launch_ext_finalize(c->tpart, (4 * d + lp.up.bn - 1) / lp.up.bn, c->Mpad, M, c->r, c->gA, ldg, 4 * d,
                           c->ext_terms, c->bf16, c->st);
     else
       ext_gemm(lp, 3);
+    prof_mark(c, PK_DOWN);
     gemm_launch(lp.down, c->st);
   }
+  prof_mark(c, PK_TAIL);
   if (rp.pruned)  // x32S rows are already the scored rows, in [sign][b][j] order
     launch_final_ln(c->x32S, c->lnfg, c->lnfb, B * nsign, c->d.opt_len, d, 1, c->d.opt_len, c->xs32, c->xs16,
                     c->bf16, c->V32 + e.v_off, c->r, c->z, B * c->d.opt_len, c->vstride, c->st);
@@ -1500,6 +1532,37 @@ extern "C" int zo_read_out4(zo_ctx* c, double* out4) {
 }
 
 // ------------------------------------------------------------------ measurement hooks
+// One eager step (zo_step_async semantics, device inputs) with a CUDA event in front of
+// every kernel group of the scorer; ms[k] = device time charged to family k
+// (0 embed, 1 LN, 2 qkv GEMM, 3 attention, 4 extension finalize, 5 attn_out GEMM,
+// 6 ff_up GEMM, 7 ff_down GEMM, 8 last-layer tail + final LN + LM head + loss,
+// 9 everything else: sampler, probes, coefficient, update), summed over the layers.
+// The events between kernels cost little (PDL on/off moves the step by ~0.5%).
+extern "C" int zo_profile_step(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr,
+                               const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B, float* ms) {
+  ZO_API_BEGIN
+  c->prof_on = true;
+  c->prof_n = 0;
+  prof_mark(c, PK_OTHER);
+  int rc = zo_step_score_async(c, seed, step, nu, eps, tokens_dev, gold_dev, B);
+  if (rc == ZO_OK) {
+    prof_mark(c, PK_OTHER);
+    rc = zo_step_apply_async(c, eps, lr, 0, B);
+  }
+  prof_mark(c, PK_OTHER);
+  c->prof_on = false;
+  if (rc != ZO_OK) return rc;
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  for (int k = 0; k < PK_N; ++k) ms[k] = 0.f;
+  for (size_t i = 0; i + 1 < c->prof_n; ++i) {
+    float t = 0.f;
+    ZO_CUDA_TRY(cudaEventElapsedTime(&t, c->prof_ev[i], c->prof_ev[i + 1]));
+    ms[c->prof_kind[i]] += t;
+  }
+  return ZO_OK;
+  ZO_API_END
+}
+
 // Average device time (ms) of one launch of a layer-0 GEMM of the scorer at
 // batch B (both signs): which = 0 qkv, 1 attn_out, 2 ff_up, 3 ff_down, 4 LM head.
 // CUDA events bracket `reps` back-to-back launches on the ctx stream; the

@@ -307,6 +307,17 @@ class ZoEngine:
         check(lib().zo_bench_gemm(self._h, which, B, reps, ctypes.byref(ms), ctypes.byref(fl)))
         return float(ms.value), float(fl.value)
 
+    PROFILE_FAMILIES = ("embed", "ln", "qkv", "attention", "ext_finalize", "attn_out", "ff_up", "ff_down", "tail",
+                        "other")
+
+    def profile_step(self, seed: int, step: int, nu: int, epsilon: float, lr: float, tokens_dev: int,
+                     gold_dev: int, B: int) -> dict:
+        """Device ms per kernel family of one eager step (zob200.h zo_profile_step)."""
+        f = (ctypes.c_float * 10)()
+        check(lib().zo_profile_step(self._h, seed, step, nu, float(epsilon), float(lr), ctypes.c_void_p(tokens_dev),
+                                    ctypes.c_void_p(gold_dev), B, f))
+        return {k: float(f[i]) for i, k in enumerate(self.PROFILE_FAMILIES)}
+
     def nll_io(self, dev_ptr: int, count: int, to_ctx: bool) -> None:
         check(lib().zo_nll_io(self._h, ctypes.c_void_p(dev_ptr), count, int(to_ctx)))
 
