@@ -130,3 +130,33 @@ def test_baseline_rejects_unfolded_window():
               M.sample_minibatch(task, "train", zcfg.seed, 0, 4))
     with pytest.raises(ConfigError):
         params.engine.baseline_directions(zcfg.seed, 1, zcfg.nu)
+
+
+@pytest.mark.parametrize("recompute", [False, True])
+def test_high_rank_materialising_writes_bit_exact(recompute):
+    """r > 8 (the factorized MeZO-style comparand, config 5's estimator) runs the tiled
+    float64 kernel; params bit-exact vs the oracle's run_baseline given its coefficients."""
+    from oracle import reference as R
+    from paper_2605_28760_b200 import model as M
+    mk = dict(vocab=64, dim=32, n_layers=2, n_heads=2, prompt_len=16, init_seed=7, init_scale=0.08)
+    tk = dict(seed=11, vocab=64, prompt_len=16, train_size=64, dev_size=8, val_size=8)
+    rc = R.ModelCfg(**mk)
+    splits = R.generate_task(R.TaskCfg(**tk))
+    z = R.ZoCfg(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=16, batch_size=8, estimator="factorized_sqrt_r")
+    recs, final = R.run_baseline(rc, splits, z, 3, recompute=recompute)
+    mcfg = M.ModelConfig(**mk)
+    task = M.generate_task(M.TaskConfig(**tk))
+    params = M.init_params(mcfg, max_batch=8)
+    eng = params.bind(16, "factorized_sqrt_r", 8, 1, "lora_only")
+    for t, rec in enumerate(recs):
+        tokens, gold = M.sample_minibatch(task, "train", 42, t, 8).sequences()
+        eng.baseline_directions(42, t, 1)
+        for p in (0, 1):
+            eng.baseline_pass(p, 1e-3, recompute)
+            got = R.canonical_mean(eng.score(tokens, gold, nsign=1)[0])
+            assert abs(got - (rec.loss_plus if p == 0 else rec.loss_minus)) < 2e-2
+        eng.baseline_pass(2, 1e-3, recompute)
+        eng.set_coefficient([rec.loss_plus, rec.loss_minus, rec.coefficient, rec.beta])
+        eng.baseline_update(1e-3, recompute)
+    params.invalidate()
+    assert M.params_digest(params) == R.params_digest(final)
