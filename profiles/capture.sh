@@ -28,4 +28,17 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -s 2500 -c 1500 --csv \
   --log-file gpurun_out/${TAG}_fact_launches.csv python bench.py --model $MODEL --estimator factorized_sqrt_r \
   --rank 128 --profile --no-graph --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_fact.log 2>&1
+# summaries on the box (the .ncu-rep files are large; gpurun brings back <= 64 MiB)
+python profiles/extract_ncu.py gpurun_out/${TAG}_gemm.ncu-rep gpurun_out/${TAG}_ncu_gemm.csv
+python profiles/extract_ncu.py gpurun_out/${TAG}_aux.ncu-rep gpurun_out/${TAG}_ncu_aux.csv
+ncu -i gpurun_out/${TAG}_gemm.ncu-rep --page source --csv --print-source sass -k regex:k_gemm --launch-count 1 \
+  > gpurun_out/${TAG}_gemm_qkv_source.csv 2>/dev/null
+ncu -i gpurun_out/${TAG}_aux.ncu-rep --page source --csv --print-source sass -k regex:k_attn --launch-count 1 \
+  > gpurun_out/${TAG}_attn_source.csv 2>/dev/null
+gzip -9 -f gpurun_out/${TAG}_gemm.ncu-rep gpurun_out/${TAG}_aux.ncu-rep
+# keep the bundle under gpurun's 64 MiB: drop the aux report first, then the GEMM report
+for f in gpurun_out/${TAG}_aux.ncu-rep.gz gpurun_out/${TAG}_gemm.ncu-rep.gz; do
+  [ "$(du -sm gpurun_out | cut -f1)" -gt 58 ] && rm -f "$f"
+done
+du -sh gpurun_out
 echo done
