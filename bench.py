@@ -136,7 +136,7 @@ def ncu_traffic(model):
     """DRAM bytes (read + write) of one launch of each of the four layer GEMMs, from the
     committed `ncu --set full` capture (profiles/), or None when not captured for this model."""
     import csv
-    p = os.path.join(HERE, "profiles", "r01d_ncu_gemm_opt13b.csv")
+    p = os.path.join(HERE, "profiles", "r01f_ncu_gemm_opt13b.csv")
     if model != "opt-13b" or not os.path.exists(p):
         return None
     tot = 0.0
@@ -450,6 +450,11 @@ def main():
                             "peak_kind": f"{peak_kind} bf16 sustained (MEASURED_PEAKS.json): GEMMs timed inside "
                                          f"an eager step right after the timed region",
                             "share_of_step": (gemm_ms / prof_total) if fam is not None else None}
+        # DRAM bytes of one launch each of the four layer GEMMs (ncu, layer 1) beside their
+        # algorithmic bytes: weights once, A operands once, outputs (RMW for the residual ones)
+        line["roofline"]["traffic_scope"] = "one launch each of qkv, attn_out, ff_up, ff_down (ncu --set full)"
+        line["roofline"]["algorithmic_bytes"] = (2.0 * 12 * d * d + 2.0 * Mr * 7 * d
+                                                 + Mr * d * (2 * 3 + 8 + 2 * 4 + 8))
         if fam is not None:
             line["roofline"]["in_step_ms"] = {k: round(v, 4) for k, v in fam.items()}
             line["roofline"]["in_step_total_ms"] = prof_total
