@@ -241,3 +241,36 @@ def test_factorized_high_rank_step_vs_oracle(rank):
         np.testing.assert_array_equal(eng.download("blk1.ff_down"), w_before)
         params = {lid: eng.download(lid) for lid in eng.lids} | {k: v for k, v in params.items() if v.ndim == 1}
     eng.close()
+
+
+@pytest.mark.parametrize("opt_len", [2, 3])
+def test_multi_token_options_vs_oracle(opt_len):
+    """Options of L > 1 tokens (model.py:202-215 sums the NLL of rows prompt_len-1+j, j < L):
+    the forward runs positions [0, T-1) only (the last token is never attended by a scored
+    row), the L scored rows per sequence go through the pruned last layer, the LM head and
+    the loss; paired probes against the float64 oracle."""
+    from paper_2605_28760_b200.engine import ZoEngine
+    cfg = R.ModelCfg(vocab=256, dim=64, n_layers=2, n_heads=2, prompt_len=20, init_seed=7, init_scale=0.05)
+    B, r, step, eps = 8, 2, 3, 1e-3
+    rng = np.random.default_rng(0)
+    prompts = rng.integers(4, cfg.vocab, size=(B, cfg.prompt_len))
+    gold = rng.integers(4, cfg.vocab, size=(B, opt_len))
+    tokens = np.concatenate([prompts, gold], axis=1)
+    eng = ZoEngine(cfg.vocab, cfg.dim, cfg.n_layers, cfg.n_heads, cfg.prompt_len, opt_len=opt_len, max_batch=B,
+                   rank=r)
+    eng.init_params(cfg.init_seed, cfg.init_scale)
+    eng.sample_v(42, step, 50)
+    eng.sample_u(42, step)
+    params = R.init_params(cfg)
+    A = {lid: 1e-3 * R.gaussian(43, step, lid, R.ROLE_U, eng.shapes[lid][0], r) for lid in eng.lids}
+    eng.set_slot(2, eng.join(2, A))
+    Uh, Vh = eng.split(0, eng.get_slot(0)), eng.split(1, eng.get_slot(1))
+    eng.prepare_probe(eps, 0)
+    nll = eng.score(tokens, np.stack([gold, gold]), nsign=2)
+    for si, sign in enumerate((1, -1)):
+        eff = dict(params)
+        for lid in eng.lids:
+            eff[lid] = R.compose(params[lid], A[lid], Vh[lid], Uh[lid], sign, eps)
+        ref = R.forward_nll(eff, cfg, tokens, gold)
+        np.testing.assert_allclose(nll[si], ref, atol=2e-2 * opt_len, rtol=0)
+    eng.close()
