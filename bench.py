@@ -331,8 +331,9 @@ def main():
     out4_local = torch.zeros(4, dtype=torch.float64, device="cuda")
     out4_all = torch.zeros(world * 4, dtype=torch.float64, device="cuda")
 
-    def one_step(t):
-        tp, gp = d_tok[t].data_ptr(), d_gold[t].data_ptr()
+    def one_step(t, tp=None, gp=None):
+        if tp is None:
+            tp, gp = d_tok[t].data_ptr(), d_gold[t].data_ptr()
         if qdir:
             import torch.distributed as dist
             eng.qdir_score_async(zcfg.seed, t, G, rank, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, B)
@@ -488,6 +489,48 @@ def main():
         line["e2e"] = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * T * 4 + B * 4 + 8,
                        "d2h_bytes_per_step": 32, "api": f"model.sample_minibatch + zo_engine.{step_fn.__name__} (host batch)",
                        "phase_ms_last_step": dict(zip(["sample", "score", "update"], eng.last_step_ms()))}
+
+    if not args.no_e2e and not args.profile and world > 1:
+        # end to end at N GPUs: every step each rank draws its minibatch on the host (its own
+        # direction's in q-direction mode, its slice in exact mode), copies it from pinned
+        # memory, runs score -> all-gather -> apply, and reads the gathered coefficients back
+        # (the losses the public API returns); wall clock, max over ranks
+        import torch.distributed as dist
+        h_tok = torch.empty((Bl, T), dtype=torch.int32).pin_memory()
+        h_gold = torch.empty((Bl, 1), dtype=torch.int32).pin_memory()
+        e_tok = torch.empty((Bl, T), dtype=torch.int32, device="cuda")
+        e_gold = torch.empty((Bl, 1), dtype=torch.int32, device="cuda")
+
+        def e2e_step(t):
+            if qdir:
+                seq, gold = M.sample_minibatch(task, "train", zcfg.seed, t * G + rank, B).sequences()
+            else:
+                seq, gold = M.sample_minibatch(task, "train", zcfg.seed, t, B).sequences()
+                seq, gold = seq[rank * Bl:(rank + 1) * Bl], gold[rank * Bl:(rank + 1) * Bl]
+            h_tok.copy_(torch.from_numpy(np.ascontiguousarray(seq, dtype=np.int32)))
+            h_gold.copy_(torch.from_numpy(np.ascontiguousarray(gold, dtype=np.int32)))
+            e_tok.copy_(h_tok, non_blocking=True)
+            e_gold.copy_(h_gold, non_blocking=True)
+            one_step(t, e_tok.data_ptr(), e_gold.data_ptr())
+            return out4_all.cpu() if qdir else torch.from_numpy(eng.read_out4())
+
+        t_e0 = nsteps + 2
+        for t in range(t_e0, t_e0 + args.warmup):
+            e2e_step(t)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for t in range(t_e0 + args.warmup, t_e0 + args.warmup + args.steps):
+            e2e_step(t)
+        torch.cuda.synchronize()
+        el = torch.tensor([time.perf_counter() - t0], device="cpu" if same_dev else "cuda")
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        e2e_s = float(el.item()) / args.steps
+        line["e2e"] = {"value": G / e2e_s, "unit": UNIT, "h2d_bytes_per_step": Bl * T * 4 + Bl * 4,
+                       "d2h_bytes_per_step": (G * 32) if qdir else 32,
+                       "api": ("model.sample_minibatch + zo_qdir_score_async / all-gather / zo_qdir_apply_async"
+                               if qdir else "model.sample_minibatch + zo_step_score_async / all-gather of NLLs / "
+                                            "zo_step_apply_async") + " (host batch per rank, wall clock, max over ranks)"}
 
     if args.materialising and not args.profile and world == 1:
         # the conventional training loop (baseline_loop.py:122-239) on the same replica: probe
