@@ -197,6 +197,9 @@ def baseline_trajectories():
                         dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=8, estimator="factorized_sqrt_r",
                              batch_size=8), 4)
     baseline_trajectory("micro_baseline_full", MICRO, MICRO_TASK, dict(lozo, scope="full"), 4)
+    dense = dict(seed=42, epsilon=1e-3, learning_rate=1e-3, estimator="dense_mezo", batch_size=8)
+    baseline_trajectory("micro_baseline_dense", MICRO, MICRO_TASK, dense, 4)
+    baseline_trajectory("micro_baseline_dense_recompute", MICRO, MICRO_TASK, dense, 4, recompute=True)
 
 
 def adapter_fixture():

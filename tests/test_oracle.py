@@ -86,7 +86,7 @@ def test_trajectory_vs_reference(golden_dir, name):
 
 
 @pytest.mark.parametrize("name", ["micro_baseline", "micro_baseline_recompute", "micro_baseline_fact",
-                                  "micro_baseline_full"])
+                                  "micro_baseline_full", "micro_baseline_dense", "micro_baseline_dense_recompute"])
 def test_baseline_loop_vs_reference(golden_dir, name):
     """The materialising loop (baseline_loop.py:122-239): cached / recompute products,
     factorized and full scope -- digests, losses and the final params bit-exact."""
