@@ -42,6 +42,7 @@ extern "C" {
 
 #define ZO_EST_LOZO 0       /* "lozo_lazy"          zo_engine.py:368 */
 #define ZO_EST_FACTORIZED 1 /* "factorized_sqrt_r"  zo_engine.py:420 */
+#define ZO_EST_DENSE 2      /* "dense_mezo"         zo_engine.py:476 -- materialising loop only */
 
 /* ZoConfig.scope (zo_engine.py:79, 256-260): "lora_only" perturbs the 2-D params
  * through rank-r slots; "full" also probes every 1-D param (LN scale / shift)

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "_build", "libzob200.so")
 
 ZO_OK, ZO_ERR_CONFIG, ZO_ERR_DIMENSION, ZO_ERR_INPUT, ZO_ERR_ABORT, ZO_ERR_CUDA, ZO_ERR_INTERNAL = range(7)
 PREC_FP16, PREC_BF16 = 0, 1
-EST_LOZO, EST_FACTORIZED = 0, 1
+EST_LOZO, EST_FACTORIZED, EST_DENSE = 0, 1, 2
 SCOPE_LORA_ONLY, SCOPE_FULL = 0, 1
 ARCH_ZOSERVE, ARCH_OPT = 0, 1
 

@@ -8,7 +8,8 @@ its own forward over the materialised weights (no LoRA extension, two
 launches of every GEMM instead of one).  ``recompute_products`` selects the
 reference's two _Probe modes (baseline_loop.py:68-104): cached (dense product
 applied with axpy_dense, bit-exact restore) or recompute (axpy_outer per term,
-arithmetic restore).  The float64 arithmetic is the reference's, so the
+arithmetic restore), and all three estimators run (dense_mezo: a dense z per weight,
+regenerated every step, _DenseProbe).  The float64 arithmetic is the reference's, so the
 parameters are bit-exact given the coefficients (tests/test_gpu_baseline.py);
 the scoring runs on the 16-bit tensor-core path like the serving scorer.
 """
@@ -58,9 +59,6 @@ def run_baseline(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: int, 
     host-side fingerprints off for long timing runs."""
     if steps < 1:
         raise ConfigError("steps must be >= 1")
-    if zcfg.estimator == "dense_mezo":
-        raise ConfigError("dense_mezo has no device engine (a dense direction per weight does not fit "
-                          "beside the float64 master at the BASELINE shapes)")
     params = init_params(mcfg, precision=precision if precision in ("fp16", "bf16") else "fp16",
                          max_batch=max(16, zcfg.batch_size)) if params is None else params
     dp = as_device_params(params, mcfg)
@@ -72,8 +70,8 @@ def run_baseline(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: int, 
     rec_mode = bool(recompute_products)
     # 4 counted writes per perturbed element per step (baseline_loop.py:131-135)
     per_step = sum(m * n for m, n in eng.shapes.values())
-    if zcfg.scope == "full":
-        per_step += len(eng.vids) * eng.dim
+    if zcfg.scope == "full" or zcfg.estimator == "dense_mezo":
+        per_step += sum(eng.vlens.values())
     trajectory: list[ZoStepRecord] = []
     evals: list[EvalPoint] = []
     wall = 0.0

@@ -877,9 +877,10 @@ struct LowRankArgs {
   int ldw, transposed;
   bool bf16;
   int alpha_src;
+  const double* Z;  // dense direction z[m, n] (dense_mezo): p = z instead of the rank-r product
 };
 
-template <int MODE, int RK>
+template <int MODE, int RK, bool DZ = false>
 __global__ void __launch_bounds__(256, 3) k_lowrank(LowRankArgs a) {
   __shared__ double sL[64 * 9];
   __shared__ uint16_t t16[64 * 66];  // [j][i] 16-bit transposed tile
@@ -904,11 +905,12 @@ __global__ void __launch_bounds__(256, 3) k_lowrank(LowRankArgs a) {
 #pragma unroll
     for (int k = 0; k < RK; ++k) rv[c][k] = (k < r && j + c < a.n) ? a.R[(size_t)(j + c) * r + k] : 0.0;
   const bool vec = (a.n & 1) == 0;
-  double w[8][2];
+  double w[8][2], zd[8][2];
 #pragma unroll
   for (int s = 0; s < 8; ++s) {
     const int i = i0 + warp + 8 * s;
     w[s][0] = w[s][1] = 0.0;
+    zd[s][0] = zd[s][1] = 0.0;
     if (i < a.m && j < a.n) {
       const double* src = a.W + (size_t)i * a.n + j;
       if (vec) {
@@ -919,6 +921,17 @@ __global__ void __launch_bounds__(256, 3) k_lowrank(LowRankArgs a) {
         w[s][0] = src[0];
         if (j + 1 < a.n) w[s][1] = src[1];
       }
+      if (DZ) {
+        const double* zs = a.Z + (size_t)i * a.n + j;
+        if (vec) {
+          const double2 v = __ldcs(reinterpret_cast<const double2*>(zs));
+          zd[s][0] = v.x;
+          zd[s][1] = v.y;
+        } else {
+          zd[s][0] = zs[0];
+          if (j + 1 < a.n) zd[s][1] = zs[1];
+        }
+      }
     }
   }
   __syncthreads();
@@ -928,7 +941,15 @@ __global__ void __launch_bounds__(256, 3) k_lowrank(LowRankArgs a) {
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       double v = w[s][c];
-      if (MODE == LR_OUTER) {
+      if (DZ && MODE != LR_COPY) {
+        // dense direction (_DenseProbe, baseline_loop.py:107-119): axpy_dense with z itself
+        if (MODE == LR_PROBE) {
+          v = __dadd_rn(v, __dmul_rn(a.a1, zd[s][c]));
+          if (a.a2 != 0.0) v = __dadd_rn(v, __dmul_rn(a.a2, zd[s][c]));
+        } else {
+          v = __dadd_rn(v, __dmul_rn(alpha, zd[s][c]));
+        }
+      } else if (MODE == LR_OUTER) {
 #pragma unroll
         for (int k = 0; k < RK; ++k)
           if (k < r) v = __dadd_rn(v, __dmul_rn(alpha, __dmul_rn(sL[il * 9 + k], rv[c][k])));
@@ -1003,6 +1024,14 @@ void launch_lowrank_rk(int mode, const LowRankArgs& a, const dim3& grid, cudaStr
 
 void launch_lowrank(int mode, const LowRankArgs& a, cudaStream_t st) {
   const dim3 grid((a.n + 63) / 64, (a.m + 63) / 64);
+  if (a.Z && mode != LR_COPY) {
+    switch (mode) {
+      case LR_OUTER: k_lowrank<LR_OUTER, 1, true><<<grid, 256, 0, st>>>(a); break;
+      case LR_PROBE: k_lowrank<LR_PROBE, 1, true><<<grid, 256, 0, st>>>(a); break;
+      default: k_lowrank<LR_DENSE, 1, true><<<grid, 256, 0, st>>>(a);
+    }
+    return;
+  }
   if (mode == LR_COPY || a.r == 0) {
     k_lowrank<LR_COPY, 1><<<grid, 256, 0, st>>>(a);
     return;
@@ -1282,6 +1311,36 @@ void launch_materialise(int mode, double* W64, int m, int n, const double* U, co
       k_materialise<BL_OUTER><<<grid, 256, 0, st>>>(W64, m, n, U, V, r, a1, 0.0, out4, scale, W16, ldw,
                                                     transposed, bf16);
   }
+}
+
+void launch_dense_rw(int mode, double* W64, int m, int n, const double* Z, double a1, double a2, const double* out4,
+                     void* W16, int ldw, int transposed, bool bf16, cudaStream_t st) {
+  LowRankArgs a = lowrank_args(W64, m, n, nullptr, nullptr, 0, W16, ldw, transposed, bf16);
+  a.Z = Z;
+  a.a1 = a1;
+  a.a2 = a2;
+  a.out4 = out4;
+  a.alpha_src = out4 ? ALPHA_BETA : ALPHA_HOST;
+  launch_lowrank(mode == BL_PROBE ? LR_PROBE : mode == BL_UPDATE ? LR_DENSE : mode == 3 ? LR_COPY : LR_OUTER, a, st);
+}
+
+// _DenseProbe on 1-D params in recompute mode (in place): p = fl(p + fl(alpha*z)),
+// alpha = a1 or beta from the device coefficient; both fp32 copies refreshed
+__global__ void k_vec_inplace(double* __restrict__ p, const double* __restrict__ z, int64_t n, double a1,
+                              const double* __restrict__ out4, float* __restrict__ out32) {
+  const double alpha = out4 ? out4[3] : a1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = __dadd_rn(p[i], __dmul_rn(alpha, z[i]));
+    p[i] = v;
+    out32[i] = out32[n + i] = (float)v;
+  }
+}
+
+void launch_vec_inplace(double* p, const double* z, int64_t n, double a1, const double* out4, float* out32,
+                        cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+  k_vec_inplace<<<grid > 0 ? grid : 1, 256, 0, st>>>(p, z, n, a1, out4, out32);
 }
 
 // VectorProbe.set_sign for ONE scoring call (the loop scores each sign separately):

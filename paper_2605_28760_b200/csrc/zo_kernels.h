@@ -94,6 +94,13 @@ void launch_zero(void* p, size_t bytes, cudaStream_t st);
 void launch_materialise(int mode, double* W64, int m, int n, const double* U, const double* V, int r, double a1,
                         double a2, const double* out4, double scale, void* W16, int ldw, int transposed, bool bf16,
                         cudaStream_t st);
+// dense_mezo materialising loop (_DenseProbe, baseline_loop.py:107-119): the same modes with
+// the dense direction Z[m, n] in place of the rank-r product (mode 3 = shadow copy)
+void launch_dense_rw(int mode, double* W64, int m, int n, const double* Z, double a1, double a2, const double* out4,
+                     void* W16, int ldw, int transposed, bool bf16, cudaStream_t st);
+// 1-D params in place (recompute-mode _DenseProbe): p += alpha*z, alpha = a1 or out4[3]
+void launch_vec_inplace(double* p, const double* z, int64_t n, double a1, const double* out4, float* out32,
+                        cudaStream_t st);
 // VectorProbe at one sign for a single-sign scoring call (both fp32 copies)
 void launch_vec_probe_sign(const double* p, const double* z, int64_t n, double eps, int sign, float* out32,
                            cudaStream_t st);

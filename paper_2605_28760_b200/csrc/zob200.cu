@@ -40,6 +40,7 @@ struct Matrix {
   int64_t m = 0, n = 0;  // reference layout: (in, out)
   uint64_t lid_hash = 0;
   int64_t u_off = 0, v_off = 0;
+  int64_t z_off = 0;  // dense_mezo: offset of this matrix's z[m, n] in the dense arena
   double* W64 = nullptr;
   void* W16 = nullptr;
   int ldw = 0;
@@ -107,6 +108,11 @@ struct zo_ctx {
   std::vector<int64_t> voff, vlen;  // per 1-D param: offset / length in the vector arenas
   int64_t nvt = 0;                  // total 1-D elements
   bool opt = false;                 // ZO_ARCH_OPT
+  bool dense = false;               // ZO_EST_DENSE: dense z per weight (materialising loop only)
+  double* ZM = nullptr;             // dense directions of every matrix, sorted lid order
+  int64_t szm = 0;
+  SamplerPlan planZM;
+  std::vector<StreamDesc> streamsZM;
   int i_pos = -1;                   // OPT: learned positions (offset 2)
   std::vector<float*> bqkv, bout, bup, bdown;  // OPT: fp32 bias copies per layer ([0] +eps rows)
   double *VEC64 = nullptr, *VZ = nullptr;
@@ -551,7 +557,12 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->r = d.rank;
   c->bf16 = d.precision == ZO_PREC_BF16;
   check(d.scope == ZO_SCOPE_LORA_ONLY || d.scope == ZO_SCOPE_FULL, ZO_ERR_CONFIG, "unknown scope");
-  c->full_scope = d.scope == ZO_SCOPE_FULL;
+  check(d.estimator == ZO_EST_LOZO || d.estimator == ZO_EST_FACTORIZED || d.estimator == ZO_EST_DENSE, ZO_ERR_CONFIG,
+        "unknown estimator");
+  c->dense = d.estimator == ZO_EST_DENSE;
+  // dense_mezo perturbs every parameter (scope ignored, zo_engine.py:486-488): the 1-D params
+  // take the full-scope direction machinery
+  c->full_scope = d.scope == ZO_SCOPE_FULL || c->dense;
   check(d.arch == ZO_ARCH_ZOSERVE || d.arch == ZO_ARCH_OPT, ZO_ERR_CONFIG, "unknown architecture");
   c->opt = d.arch == ZO_ARCH_OPT;
   if (c->opt) check(d.max_pos >= c->T, ZO_ERR_DIMENSION, "max_pos shorter than the sequence");
@@ -587,7 +598,7 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   }
   std::sort(ms.begin(), ms.end(), [](const Matrix& a, const Matrix& b) { return a.lid < b.lid; });
   for (auto& m : ms) {
-    check(d.estimator == ZO_EST_FACTORIZED || d.rank <= std::min(m.m, m.n), ZO_ERR_CONFIG,
+    check(d.estimator != ZO_EST_LOZO || d.rank <= std::min(m.m, m.n), ZO_ERR_CONFIG,
           "rank " + std::to_string(d.rank) + " exceeds min dim of " + m.lid);
     m.u_off = c->su;
     m.v_off = c->sv;
@@ -629,6 +640,18 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->Pp = c->mem.get<float>(c->su);
   c->Pm = c->mem.get<float>(c->su);
   c->V32 = c->mem.get<float>(c->sv);
+  if (c->dense) {
+    for (auto& m : c->mats) {
+      m.z_off = c->szm;
+      c->szm += m.m * m.n;
+    }
+    size_t free_b = 0, total_b = 0;
+    ZO_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    check((double)c->szm * 8.0 + 4e9 < (double)free_b, ZO_ERR_CONFIG,
+          "dense_mezo: the dense direction arena (" + std::to_string(c->szm * 8 / 1000000000) +
+              " GB) does not fit beside the float64 master");
+    c->ZM = c->mem.get<double>(c->szm);
+  }
   // 1-D params (identity at init, model.py:100-107; OPT biases zero), sorted ids
   {
     std::vector<std::pair<std::string, int64_t>> vs;
@@ -753,6 +776,20 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   }
   build_sampler_plan(c.get(), c->planU, c->streamsU);
   build_sampler_plan(c.get(), c->planV, c->streamsV);
+  if (c->dense) {
+    // dense_direction(seed, step, lid, (m, n)) = sample_gaussian(key DENSE_Z, m, n) row-major
+    for (auto& m : c->mats) {
+      StreamDesc sz{};
+      sz.lid_hash = m.lid_hash;
+      sz.role = 2;  // Role.DENSE_Z
+      sz.step_mode = STEP_CURRENT;
+      sz.n = (uint64_t)(m.m * m.n);
+      sz.out_off = (uint64_t)m.z_off;
+      sz.scale = 1.0;
+      c->streamsZM.push_back(sz);
+    }
+    build_sampler_plan(c.get(), c->planZM, c->streamsZM);
+  }
   if (c->full_scope) {
     // dense_direction(seed, step, vid, (dim,)) = gaussian_vector (zo_engine.py:194-198)
     for (int v = 0; v < c->nv; ++v) {
@@ -970,21 +1007,22 @@ int zo_sample_stream(zo_ctx* c, uint64_t seed, uint64_t step, uint64_t lid_hash,
 }
 
 int zo_slot_count(const zo_ctx* c, int32_t which, int64_t* count) {
-  if (which < 0 || which > 3 || (which == 3 && !c->full_scope)) return ZO_ERR_INPUT;
-  *count = which == 3 ? c->nvt : which == 1 ? c->sv : c->su;
+  if (which < 0 || which > 4 || (which == 3 && !c->full_scope) || (which == 4 && !c->dense)) return ZO_ERR_INPUT;
+  *count = which == 4 ? c->szm : which == 3 ? c->nvt : which == 1 ? c->sv : c->su;
   return ZO_OK;
 }
 
 static double* slot_ptr(zo_ctx* c, int which) {
-  return which == 0 ? c->U : which == 1 ? c->V : which == 2 ? c->A : c->VZ;
+  return which == 0 ? c->U : which == 1 ? c->V : which == 2 ? c->A : which == 3 ? c->VZ : c->ZM;
 }
 static int64_t slot_size(const zo_ctx* c, int which) {
-  return which == 3 ? c->nvt : which == 1 ? c->sv : c->su;
+  return which == 4 ? c->szm : which == 3 ? c->nvt : which == 1 ? c->sv : c->su;
 }
 
 int zo_get_slot(zo_ctx* c, int32_t which, double* host, int64_t count) {
   ZO_API_BEGIN
-  check(which >= 0 && which <= 3 && (which < 3 || c->full_scope), ZO_ERR_INPUT, "bad slot id");
+  check(which >= 0 && which <= 4 && (which != 3 || c->full_scope) && (which != 4 || c->dense), ZO_ERR_INPUT,
+        "bad slot id");
   check(count == slot_size(c, which), ZO_ERR_DIMENSION, "slot arena size mismatch");
   ZO_CUDA_TRY(cudaMemcpyAsync(host, slot_ptr(c, which), (size_t)count * 8, cudaMemcpyDeviceToHost, c->st));
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -1108,6 +1146,7 @@ int zo_update_vectors(zo_ctx* c, double lr) {
 int zo_step(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr, int32_t divide_by_r,
             const int32_t* tokens, const int32_t* gold, int32_t B, double* out4) {
   ZO_API_BEGIN
+  check(!c->dense, ZO_ERR_CONFIG, "dense_mezo has no serving-path form (runtime.py:275-279): use the materialising loop");
   check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
   check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
@@ -1171,6 +1210,7 @@ uint64_t zo_digest_chain(const char* const* lids, const double* arena, const int
 extern "C" int zo_step_score_async(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps,
                                    const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
   ZO_API_BEGIN
+  check(!c->dense, ZO_ERR_CONFIG, "dense_mezo has no serving-path form (runtime.py:275-279): use the materialising loop");
   check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
   check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
@@ -1291,6 +1331,7 @@ static void graph_body(zo_ctx* c, uint64_t seed, double eps, double lr, int32_t 
 extern "C" int zo_step_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps, double lr,
                              int32_t divide_by_r, const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
   ZO_API_BEGIN
+  check(!c->dense, ZO_ERR_CONFIG, "dense_mezo has no serving-path form (runtime.py:275-279): use the materialising loop");
   check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
   check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
@@ -1344,6 +1385,27 @@ double probe_scale(const zo_ctx* c) {
 void baseline_pass(zo_ctx* c, int pass, double eps, bool recompute) {
   const double s = probe_scale(c);
   const double a_plus = eps * s, a_minus = (-2.0 * eps) * s;
+  if (c->dense) {  // _DenseProbe on every parameter (baseline_loop.py:107-119, 172-174)
+    for (auto& m : c->mats) {
+      const int ldw = m.kind == K_EMBED ? (int)m.n : m.ldw, tr = m.kind == K_EMBED ? 0 : 1;
+      const double* Zm = c->ZM + m.z_off;
+      if (recompute)
+        launch_dense_rw(2, m.W64, (int)m.m, (int)m.n, Zm, pass == 1 ? a_minus : a_plus, 0.0, nullptr, m.W16, ldw,
+                        tr, c->bf16, c->st);
+      else if (pass == 2)
+        refresh_shadow(c, m);
+      else
+        launch_dense_rw(0, m.W64, (int)m.m, (int)m.n, Zm, a_plus, pass == 1 ? a_minus : 0.0, nullptr, m.W16, ldw, tr,
+                        c->bf16, c->st);
+    }
+    if (recompute)
+      launch_vec_inplace(c->VEC64, c->VZ, c->nvt, pass == 1 ? a_minus : a_plus, nullptr, c->VEC32, c->st);
+    else if (pass == 2)
+      launch_vec_probe(c->VEC64, c->VZ, c->nvt, 0.0, c->VEC32, c->st);
+    else
+      launch_vec_probe_sign(c->VEC64, c->VZ, c->nvt, eps, pass == 0 ? 1 : -1, c->VEC32, c->st);
+    return;
+  }
   for (auto& m : c->mats) {
     const int ldw = m.kind == K_EMBED ? (int)m.n : m.ldw, tr = m.kind == K_EMBED ? 0 : 1;
     double* Um = c->U + m.u_off;
@@ -1368,6 +1430,15 @@ void baseline_pass(zo_ctx* c, int pass, double eps, bool recompute) {
 }
 void baseline_update(zo_ctx* c, double lr, bool recompute) {
   const double s = probe_scale(c);
+  if (c->dense) {  // p += (-(eta*c)) z for every parameter, beta from the device coefficient
+    for (auto& m : c->mats) {
+      const int ldw = m.kind == K_EMBED ? (int)m.n : m.ldw, tr = m.kind == K_EMBED ? 0 : 1;
+      launch_dense_rw(recompute ? 2 : 1, m.W64, (int)m.m, (int)m.n, c->ZM + m.z_off, 0.0, 0.0, c->out4, m.W16, ldw,
+                      tr, c->bf16, c->st);
+    }
+    launch_vec_inplace(c->VEC64, c->VZ, c->nvt, 0.0, c->out4, c->VEC32, c->st);
+    return;
+  }
   for (auto& m : c->mats) {
     const int ldw = m.kind == K_EMBED ? (int)m.n : m.ldw, tr = m.kind == K_EMBED ? 0 : 1;
     launch_materialise(recompute ? 2 : 1, m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, 0.0,
@@ -1379,6 +1450,13 @@ void baseline_directions(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu) {
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
   const int64_t wstart = lozo ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
   check(!c->a_dirty, ZO_ERR_CONFIG, "materialising loop on a replica with unfolded window mass");
+  if (c->dense) {
+    sampler_launch(c->planZM, seed, c->d_step, 1, c->ZM, c->st);
+    sample_z(c, seed);
+    ZO_CUDA_TRY(cudaMemsetAsync(c->Pp, 0, (size_t)c->su * 4, c->st));
+    ZO_CUDA_TRY(cudaMemsetAsync(c->Pm, 0, (size_t)c->su * 4, c->st));
+    return;
+  }
   if (!lozo || wstart != c->v_window) {
     sampler_launch(c->planV, seed, c->d_step, (uint32_t)nu, c->V, c->st);
     write_vext_all(c);
@@ -1464,6 +1542,7 @@ extern "C" int zo_qdir_score_async(zo_ctx* c, uint64_t seed, uint64_t macro_step
                                    double eps, double lr, int32_t divide_by_r, const int32_t* tokens_dev,
                                    const int32_t* gold_dev, int32_t B) {
   ZO_API_BEGIN
+  check(!c->dense, ZO_ERR_CONFIG, "dense_mezo has no serving-path form (runtime.py:275-279): use the materialising loop");
   check(G >= 1 && g >= 0 && g < G, ZO_ERR_CONFIG, "q-direction rank out of range");
   check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
   const bool lozo = c->d.estimator == ZO_EST_LOZO;

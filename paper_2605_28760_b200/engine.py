@@ -18,7 +18,8 @@ from .errors import ConfigError, DimensionError
 PRECISIONS = {"fp16": _lib.PREC_FP16, "bf16": _lib.PREC_BF16}
 # the reference's precision strings run on the tensor-core path
 ALIASES = {"real64": "fp16", "real32": "fp16"}
-ESTIMATORS = {"lozo_lazy": _lib.EST_LOZO, "factorized_sqrt_r": _lib.EST_FACTORIZED}
+ESTIMATORS = {"lozo_lazy": _lib.EST_LOZO, "factorized_sqrt_r": _lib.EST_FACTORIZED,
+              "dense_mezo": _lib.EST_DENSE}  # dense_mezo: the materialising loop only
 SCOPES = {"lora_only": _lib.SCOPE_LORA_ONLY, "full": _lib.SCOPE_FULL}
 ARCHS = {"zoserve": _lib.ARCH_ZOSERVE, "opt": _lib.ARCH_OPT}
 
@@ -39,7 +40,7 @@ def vector_shapes(n_layers: int, dim: int, arch: str = "zoserve") -> dict[str, i
     out["ln_f.shift"] = dim
     return out
 
-U, V, A, Z = 0, 1, 2, 3  # slot arenas (Z: full-scope 1-D directions)
+U, V, A, Z, ZM = 0, 1, 2, 3, 4  # slot arenas (Z: 1-D directions; ZM: dense_mezo matrix directions)
 
 
 def resolve_precision(precision: str) -> str:
@@ -93,6 +94,11 @@ class ZoEngine:
             su += m * rank
             sv += nn * rank
         self.su, self.sv = su, sv
+        self.zm_off, zm = {}, 0
+        for lid in self.lids:
+            self.zm_off[lid] = zm
+            zm += self.shapes[lid][0] * self.shapes[lid][1]
+        self.szm = zm if estimator == "dense_mezo" else 0
         self._lid_c = (ctypes.c_char_p * n)(*[l.encode() for l in self.lids])
         self.last_out4 = np.zeros(4)
 
@@ -160,7 +166,8 @@ class ZoEngine:
         check(lib().zo_sample_v(self._h, seed, step, nu))
 
     def get_slot(self, which: int) -> np.ndarray:
-        n = self.sv if which == V else (sum(self.vlens.values()) if which == Z else self.su)
+        n = (self.sv if which == V else sum(self.vlens.values()) if which == Z else self.szm if which == ZM
+             else self.su)
         out = np.empty(n, dtype=np.float64)
         check(lib().zo_get_slot(self._h, which, out.ctypes.data, n))
         return out
@@ -188,16 +195,24 @@ class ZoEngine:
         """Chained FNV over (lid, factor) in sorted id order (zo_engine.py:220-261); for the
         U digest of a full-scope engine the 1-D directions (``z_arena``, default: the
         current Z slot) chain after the matrices."""
+        if self.estimator == "dense_mezo":
+            if which == V:
+                return 0xCBF29CE484222325  # no V part: the empty chain (zo_engine.py:235-246)
+            which = ZM
         if arena is None:
             arena = self.get_slot(which)
         arena = np.ascontiguousarray(arena, dtype=np.float64)
-        offs = self.v_off if which == V else self.u_off
-        rows = [(self.shapes[l][1] if which == V else self.shapes[l][0]) * self.rank for l in self.lids]
+        if which == ZM:
+            offs = self.zm_off
+            rows = [self.shapes[l][0] * self.shapes[l][1] for l in self.lids]
+        else:
+            offs = self.v_off if which == V else self.u_off
+            rows = [(self.shapes[l][1] if which == V else self.shapes[l][0]) * self.rank for l in self.lids]
         off_c = (ctypes.c_int64 * len(self.lids))(*[offs[l] for l in self.lids])
         cnt_c = (ctypes.c_int64 * len(self.lids))(*rows)
         h = int(lib().zo_digest_chain(self._lid_c, arena.ctypes.data, off_c, cnt_c, len(self.lids),
                                       0xCBF29CE484222325))
-        if which == U and self.scope == "full":
+        if which in (U, ZM) and (self.scope == "full" or self.estimator == "dense_mezo"):
             # full scope: the dense 1-D directions chain after the matrices (zo_engine.py:256-260)
             z = np.ascontiguousarray(self.get_slot(Z) if z_arena is None else z_arena)
             vids = self.vids

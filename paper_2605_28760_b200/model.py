@@ -116,7 +116,8 @@ class DeviceParams(Mapping):
     # Mapping protocol
     def __getitem__(self, lid: str) -> np.ndarray:
         if lid in self._vectors:
-            if self._engine is not None and self._engine.scope == "full":
+            if self._engine is not None and (self._engine.scope == "full"
+                                             or self._engine.estimator == "dense_mezo"):
                 # full scope: the device updates the 1-D params every step
                 if lid not in self._cache:
                     self._cache[lid] = self._engine.download_vector(lid)
@@ -159,7 +160,7 @@ class DeviceParams(Mapping):
             # current parameters into a fresh engine of the requested scope
             old = self._engine
             host = {lid: old.download(lid) for lid in old.lids}
-            if old.scope == "full":
+            if old.scope == "full" or old.estimator == "dense_mezo":
                 for vid in old.vids:
                     self._vectors[vid] = old.download_vector(vid)
             old.close()

@@ -8,6 +8,8 @@ against the reference's own run_baseline trajectories (tests/golden/traj_*baseli
 * run_baseline end to end: digests exact, losses within the fp16 tolerance.
 * The fused device step (zo_baseline_step_async, the bench path) equals the
   host-driven loop bit for bit.
+* All three estimators of run_baseline: lozo_lazy, factorized_sqrt_r and dense_mezo (a dense
+  Role.DENSE_Z direction per weight, _DenseProbe).
 """
 import json
 import os
@@ -17,7 +19,8 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-NAMES = ["micro_baseline", "micro_baseline_recompute", "micro_baseline_fact", "micro_baseline_full"]
+NAMES = ["micro_baseline", "micro_baseline_recompute", "micro_baseline_fact", "micro_baseline_full",
+         "micro_baseline_dense", "micro_baseline_dense_recompute"]
 
 
 def _traj(golden_dir, name):
