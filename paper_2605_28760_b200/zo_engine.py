@@ -20,7 +20,8 @@ from .adapter import AdapterState, LoraSlot
 from .engine import V as SLOT_V, U as SLOT_U, Z as SLOT_Z
 from .errors import ConfigError, InputError
 from .model import Minibatch, ModelConfig, as_device_params, matrix_ids
-from .numerics import FNV_OFFSET_BASIS, Role, StreamKey, digest_hex, digest_text, sample_gaussian
+from .engine import resolve_precision
+from .numerics import FNV_OFFSET_BASIS, Role, StreamKey, canonical_mean, digest_hex, digest_text, sample_gaussian
 
 __all__ = ["SCOPES", "ESTIMATORS", "ZoConfig", "ZoStepRecord", "write_trajectory", "read_trajectory",
            "lozo_direction", "factorized_direction", "StepDirections", "step_directions",
@@ -307,7 +308,32 @@ def factorized_step(params, mcfg: ModelConfig, state: AdapterState, zcfg: ZoConf
                             ud, vd, batch)
 
 
-def dense_mezo_step(*args, **kwargs):
-    """zo_engine.py:470-485 -- the dense CPU comparison anchor; not on the
-    serving hot path and intentionally not ported."""
-    raise ConfigError("dense_mezo has no B200 engine path; use the reference for the dense anchor")
+def dense_mezo_step(params, mcfg: ModelConfig, zcfg: ZoConfig, step: int, batch: Minibatch,
+                    precision: str = "real64", scorer=None, digests: str = "sync") -> ZoStepRecord:
+    """One dense two-point step (zo_engine.py:476-493): z ~ N(0,1) for every parameter
+    (Role.DENSE_Z, scope ignored), in-place probing of the device weights with bit-exact
+    restore (_dense_probe_coefficient, 456-473), then theta <- theta - eta*c*z -- the device
+    materialising loop's cached mode (baseline_loop.run_baseline), float64 exact given c.
+    A custom ``scorer`` cannot see device-resident probed weights and is rejected."""
+    if zcfg.estimator != "dense_mezo":
+        raise ConfigError("dense_mezo_step needs estimator='dense_mezo'")
+    if scorer is not None:
+        raise ConfigError("dense_mezo_step scores the device weights; a host scorer cannot see them")
+    resolve_precision(precision)
+    dp = as_device_params(params, mcfg)
+    eng = dp.bind(zcfg.rank, "dense_mezo", batch.prompts.shape[0], batch.option_array().shape[1], zcfg.scope)
+    tokens, gold = batch.sequences()
+    eng.baseline_directions(zcfg.seed, step, zcfg.nu)
+    eng.baseline_pass(0, zcfg.epsilon, False)
+    lp = canonical_mean(eng.score(tokens, gold, nsign=1)[0])
+    eng.baseline_pass(1, zcfg.epsilon, False)
+    lm = canonical_mean(eng.score(tokens, gold, nsign=1)[0])
+    eng.baseline_pass(2, zcfg.epsilon, False)
+    c = (lp - lm) / (2.0 * zcfg.epsilon)
+    beta = -(zcfg.learning_rate * c)
+    eng.set_coefficient([lp, lm, c, beta])
+    eng.baseline_update(zcfg.learning_rate, False)
+    dp.invalidate()
+    u = digest_hex(eng.digest(SLOT_U)) if digests != "off" else ""
+    v = digest_hex(eng.digest(SLOT_V)) if digests != "off" else ""
+    return make_step_record(zcfg, step, lp, lm, beta, u, v, batch)

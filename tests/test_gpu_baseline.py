@@ -163,3 +163,23 @@ def test_high_rank_materialising_writes_bit_exact(recompute):
         eng.baseline_update(1e-3, recompute)
     params.invalidate()
     assert M.params_digest(params) == R.params_digest(final)
+
+
+def test_dense_mezo_step_api_bit_exact(golden_dir):
+    """zo_engine.dense_mezo_step (zo_engine.py:476-493) on the device: the reference's dense
+    estimator trajectory (= the materialising loop's cached mode) -- digests exact, losses
+    within the fp16 tolerance, params bit-exact when the reference's losses are installed."""
+    from paper_2605_28760_b200.zo_engine import dense_mezo_step
+    h, recs, fin = _traj(golden_dir, "traj_micro_baseline_dense.jsonl")
+    M, mcfg, task, zcfg = _setup(h)
+    params = M.init_params(mcfg, max_batch=zcfg.batch_size)
+    for t, rec in enumerate(recs):
+        batch = M.sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
+        out = dense_mezo_step(params, mcfg, zcfg, t, batch)
+        assert (out.u_digest, out.v_digest, out.minibatch_id) == (rec["u_digest"], rec["v_digest"],
+                                                                   rec["minibatch_id"])
+        assert abs(out.loss_plus - rec["loss_plus"]) < 1.5e-2 and abs(out.loss_minus - rec["loss_minus"]) < 1.5e-2
+    from paper_2605_28760_b200.errors import ConfigError
+    with pytest.raises(ConfigError):
+        dense_mezo_step(params, mcfg, zcfg, 0, M.sample_minibatch(task, "train", zcfg.seed, 0, zcfg.batch_size),
+                        scorer=lambda b: 0.0)
