@@ -205,6 +205,7 @@ struct GemmParams {
   int sk, sk_w, sk_dp;
   float* sk_ws;
   unsigned* sk_flags;
+  int half_dp, half_n;  // half-width tail tiles (see zo_gemm.h)
   // per-column bias (OPT arch; see zo_gemm.h) and the ReLU activation of EPI_GELU16*
   const float* bias;
   int bias_rps;
@@ -219,17 +220,26 @@ struct GemmParams {
 // units working on one tile read disjoint k-slices, so no operand is fetched twice.
 struct SegIter {
   int cursor, hi, dp, step, unit;
+  int hf = 0;  // 0: full tile; 1 / 2: first / second half-width tile of a tail tile
   __device__ __forceinline__ void init(const GemmParams& p, int cg = 1) {
     dp = 1;
     unit = blockIdx.x / cg;  // CTA pairs share one tile (and one stream-K range) when cg = 2
     cursor = unit;
     step = gridDim.x / cg;
-    hi = p.sk ? p.sk_dp : p.m_tiles * p.n_tiles;
+    const int tiles = p.m_tiles * p.n_tiles;
+    hi = p.sk ? p.sk_dp : p.half_n ? p.half_dp + 2 * (tiles - p.half_dp) : tiles;
   }
   __device__ __forceinline__ bool next(const GemmParams& p, int& tile, int& k0, int& k1) {
     if (dp) {
       if (cursor < hi) {
-        tile = cursor;
+        if (p.half_n && cursor >= p.half_dp) {
+          const int h = cursor - p.half_dp;
+          tile = p.half_dp + (h >> 1);
+          hf = 1 + (h & 1);
+        } else {
+          tile = cursor;
+          hf = 0;
+        }
         k0 = 0;
         k1 = p.num_kb;
         cursor += step;
@@ -264,7 +274,8 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 
 template <int BN, int EPI, bool BF16, int XR, int CG>
 __global__ void __launch_bounds__(192, 1)
-    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+    k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+           const __grid_constant__ CUtensorMap tmB2, GemmParams p) {
   using C = GemmCfg<BN, CG>;
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // CTA within the pair
   const bool leader = rank == 0;
@@ -282,6 +293,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (p.half_n) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
@@ -325,18 +337,23 @@ __global__ void __launch_bounds__(192, 1)
       int t, k0, k1;
       while (si.next(p, t, k0, k1)) {
         const int m0 = (t % p.m_tiles) * (C::BM * CG) + (int)rank * C::BM;
-        const int n0 = (t / p.m_tiles) * BN + (int)rank * (BN / CG);
+        const int hf = si.hf;
+        // a half-width tile loads half of the B rows per CTA (tmB2's box)
+        const int n0 = hf ? (t / p.m_tiles) * BN + (hf - 1) * (BN / 2) + (int)rank * (BN / 2 / CG)
+                          : (t / p.m_tiles) * BN + (int)rank * (BN / CG);
+        const CUtensorMap* tb = hf ? &tmB2 : &tmB;
+        const uint32_t stage_bytes = hf ? C::A_BYTES + C::B_BYTES / 2 : C::STAGE_BYTES;
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(empty0 + 8 * stage, phase ^ 1);
           const uint32_t fb = full0 + 8 * stage;
           if constexpr (CG == 2) {
-            if (leader) mbar_arrive_expect_tx(fb, 2 * C::STAGE_BYTES);
+            if (leader) mbar_arrive_expect_tx(fb, 2 * stage_bytes);
             tma_load_2d_cg2(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * C::BK, m0);
-            tma_load_2d_cg2(smem_u32(sB + stage * C::B_BYTES), &tmB, fb, kb * C::BK, n0);
+            tma_load_2d_cg2(smem_u32(sB + stage * C::B_BYTES), tb, fb, kb * C::BK, n0);
           } else {
-            mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+            mbar_arrive_expect_tx(fb, stage_bytes);
             tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * C::BK, m0);
-            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), &tmB, fb, kb * C::BK, n0);
+            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), tb, fb, kb * C::BK, n0);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -349,6 +366,8 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0 && leader) {
       constexpr uint32_t idesc = (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) |
                                  ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((C::BM * CG) >> 4) << 24);
+      constexpr uint32_t idesc_h = (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) |
+                                   ((uint32_t)((BN / 2) >> 3) << 17) | ((uint32_t)((C::BM * CG) >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -361,6 +380,7 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
+        const uint32_t id = si.hf ? idesc_h : idesc;
         for (int kb = k0; kb < k1; ++kb) {
           mbar_wait(full0 + 8 * stage, phase);
           tc_fence_after();
@@ -369,9 +389,9 @@ __global__ void __launch_bounds__(192, 1)
           const int ks = (kb == p.num_kb - 1) ? p.last_ksteps : 4;
           for (int k = 0; k < ks; ++k) {
             if constexpr (CG == 2)
-              tc_mma_cg2(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb > k0 || k > 0) ? 1u : 0u);
+              tc_mma_cg2(tmem_d, ad + 2 * k, bd + 2 * k, id, (kb > k0 || k > 0) ? 1u : 0u);
             else
-              tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, idesc, (kb > k0 || k > 0) ? 1u : 0u);
+              tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, id, (kb > k0 || k > 0) ? 1u : 0u);
           }
           if constexpr (CG == 2)
             tc_commit_cg2(empty0 + 8 * stage);
@@ -398,7 +418,9 @@ __global__ void __launch_bounds__(192, 1)
     for (; si.next(p, t, k0, k1); ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      const int m0 = (t % p.m_tiles) * (C::BM * CG) + (int)rank * C::BM, n0 = (t / p.m_tiles) * BN;
+      const int m0 = (t % p.m_tiles) * (C::BM * CG) + (int)rank * C::BM;
+      const int n0 = (t / p.m_tiles) * BN + (si.hf ? (si.hf - 1) * (BN / 2) : 0);
+      const int bnc = si.hf ? BN / 2 : BN;  // columns of this (possibly half-width) tile
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
       const int row = m0 + erow;
@@ -506,14 +528,14 @@ __global__ void __launch_bounds__(192, 1)
         // flight while chunk c is added and stored
         const size_t lin0 = (size_t)row * p.ldo + n0;
         // warp-uniform (tcgen05.ld is .sync.aligned)
-        if (__all_sync(0xffffffffu, row_ok && n0 + BN <= p.N && (lin0 % 4) == 0)) {
+        if (__all_sync(0xffffffffu, row_ok && n0 + bnc <= p.N && (lin0 % 4) == 0)) {
           float* o = reinterpret_cast<float*>(p.out) + lin0;
           float4 xa[8], xb[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) xa[j] = reinterpret_cast<const float4*>(o)[j];
 #pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            if (c + 32 < BN) {
+          for (int c = 0; c < bnc; c += 32) {
+            if (c + 32 < bnc) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) xb[j] = reinterpret_cast<const float4*>(o + c + 32)[j];
             }
@@ -533,7 +555,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < bnc; c += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
         if (split) add_partials(v, c);
@@ -727,6 +749,30 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
   const int mrows = ((M + 127) / 128) * 128;
   make_tmap_2d(&g.tmA, A, (uint64_t)mrows, (uint64_t)lda, (uint64_t)lda, 128, bf16);
   make_tmap_2d(&g.tmB, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg), bf16);
+  make_tmap_2d(&g.tmB2, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg / 2), bf16);
+  g.half_dp = g.half_n = 0;
+}
+
+static int max_pair_units(int num_sms);
+
+void gemm_enable_halftail(GemmDesc& g, int num_sms) {
+  // pair tiles only, no stream-K, and not the GELU epilogue (its extension partials are
+  // indexed per full tile)
+  static const bool on = [] {
+    const char* e = std::getenv("ZO_HALFTAIL");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!on || g.sk || g.cg != 2 || g.bn != 256 || g.epi == EPI_GELU16_EXT) return;
+  int units = std::min(g.grid / 2, max_pair_units(num_sms));
+  const int m_tiles = (g.M + 255) / 256, n_tiles = (g.N + 255) / 256;
+  const int tiles = m_tiles * n_tiles;
+  if (units < 2 || tiles <= units || tiles % units == 0) return;
+  const int tail = tiles % units;
+  // only a mostly-empty last wave: its 2*tail half tiles still fit one round
+  if (3 * tail > units || 2 * tail > units) return;
+  g.half_dp = tiles - tail;
+  g.half_n = 1;
+  g.grid = units * 2;
 }
 
 template <int BN, int EPI, bool BF16, int XR, int CG>
@@ -758,12 +804,14 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.sk_dp = g.sk_dp;
   p.sk_ws = g.sk_ws;
   p.sk_flags = g.sk_flags;
+  p.half_dp = g.half_dp;
+  p.half_n = g.half_n;
   p.bias = g.bias;
   p.bias_rps = g.bias_rps;
   p.bias_vstride = g.bias_vstride;
   p.relu = g.relu;
   if constexpr (CG == 1) {
-    launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(192), C::SMEM, st, g.tmA, g.tmB, p);
+    launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(192), C::SMEM, st, g.tmA, g.tmB, g.tmB2, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.grid);
@@ -779,7 +827,7 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    ZO_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm<BN, EPI, BF16, XR, 2>, g.tmA, g.tmB, p));
+    ZO_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm<BN, EPI, BF16, XR, 2>, g.tmA, g.tmB, g.tmB2, p));
   }
 }
 

@@ -19,6 +19,7 @@ enum EpiKind : int {
 struct GemmDesc {
   CUtensorMap tmA;
   CUtensorMap tmB;
+  CUtensorMap tmB2;  // B with a half-height box: the half-width tail tiles (gemm_enable_halftail)
   int M = 0, N = 0;
   int num_kb = 0;       // 64-wide K blocks
   int last_ksteps = 4;  // 16-wide UMMA steps issued in the last K block (trims the LoRA extension)
@@ -40,6 +41,8 @@ struct GemmDesc {
   int bias_rps = 0;
   long bias_vstride = 0;
   int relu = 0;  // EPI_GELU16*: ReLU instead of GELU-tanh (OPT arch)
+  // half-width tail: tiles [half_dp, tiles) run as two N/2-wide tiles each (half_n = 1)
+  int half_dp = 0, half_n = 0;
   // stream-K split of the k-iteration space over the persistent CTAs (gemm_enable_streamk)
   int sk = 0, sk_w = 0, sk_dp = 0;
   float* sk_ws = nullptr;       // [grid][128][bn] fp32 partials of split tiles
@@ -49,6 +52,9 @@ struct GemmDesc {
 // workspace needed by gemm_enable_streamk: floats / flags
 inline size_t gemm_sk_ws_floats(int num_sms) { return (size_t)num_sms * 128 * 256; }
 void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms);
+// a mostly-empty last wave that stream-K does not take (too short a k-range per unit) runs as
+// twice as many half-width tiles: the tail's MMA time and its exposed epilogue halve
+void gemm_enable_halftail(GemmDesc& g, int num_sms);
 
 // 2-D K-major tensor map over a row-major [rows, cols] 16-bit matrix (row stride ld elements).
 void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,

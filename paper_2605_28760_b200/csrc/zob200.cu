@@ -296,6 +296,7 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
     lp.up.relu = c->opt ? 1 : 0;
     if (c->streamk)
       for (GemmDesc* g : {&lp.qkv, &lp.out, &lp.up, &lp.down}) gemm_enable_streamk(*g, c->sk_ws, c->sk_flags, c->num_sms);
+    for (GemmDesc* g : {&lp.qkv, &lp.out, &lp.up, &lp.down}) gemm_enable_halftail(*g, c->num_sms);
     if (!c->fused_ext) {
       const int rps = M / nsign;
       const Matrix* mm[4] = {&q, &o, &u, &w};

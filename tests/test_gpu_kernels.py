@@ -2,6 +2,7 @@
 operands; sampler vs the reference's golden streams (bit-exact)."""
 import json
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -62,3 +63,38 @@ def test_sampler_golden_streams(golden_dir):
         x = sample_gaussian(StreamKey(s["seed"], s["step"], s["layer_id"], Role(s["role"])), s["rows"], s["cols"])
         assert digest_hex(digest_array(x)) == s["digest"], (s["layer_id"], s["role"], s["rows"], s["cols"])
         assert [float(v).hex() for v in x.reshape(-1)[:6]] == s["head"]
+
+
+_HALFTAIL_PROBE = r"""
+import sys, numpy as np
+sys.path.insert(0, {repo!r})
+from paper_2605_28760_b200.engine import ZoEngine
+eng = ZoEngine(512, {dim}, 2, {heads}, 63, max_batch=16, rank=2)
+eng.init_params(7, 0.02)
+eng.sample_v(42, 0, 50)
+eng.sample_u(42, 0)
+rng = np.random.default_rng(0)
+tok = rng.integers(4, 512, size=(16, 64))
+gold = tok[:, 63:]
+eng.prepare_probe(1e-3, 0)
+nll = eng.score(tok, np.stack([gold, gold]), nsign=2)
+np.save({out!r}, nll)
+"""
+
+
+@pytest.mark.parametrize("dim,heads", [(4096, 32), (5120, 40)])
+def test_half_width_tail_tiles_bitwise(tmp_path, dim, heads):
+    """The half-width tail schedule (gemm_enable_halftail: 6.7B qkv, 13B attn_out) leaves every
+    output element's k-ordered accumulation unchanged, so the scores are bit-identical to the
+    full-tile schedule (ZO_HALFTAIL=0, read once per process)."""
+    import subprocess
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for flag in ("1", "0"):
+        out = str(tmp_path / f"nll_{flag}.npy")
+        code = _HALFTAIL_PROBE.format(repo=repo, dim=dim, heads=heads, out=out)
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, ZO_HALFTAIL=flag),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    np.testing.assert_array_equal(outs[0], outs[1])
