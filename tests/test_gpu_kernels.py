@@ -82,18 +82,18 @@ np.save({out!r}, nll)
 """
 
 
-@pytest.mark.parametrize("dim,heads", [(4096, 32), (5120, 40)])
-def test_half_width_tail_tiles_bitwise(tmp_path, dim, heads):
-    """The half-width tail schedule (gemm_enable_halftail: 6.7B qkv, 13B attn_out) leaves every
-    output element's k-ordered accumulation unchanged, so the scores are bit-identical to the
-    full-tile schedule (ZO_HALFTAIL=0, read once per process)."""
+@pytest.mark.parametrize("env,dim,heads", [("ZO_HALFTAIL", 4096, 32), ("ZO_HALFTAIL", 5120, 40)])
+def test_schedule_variants_bitwise(tmp_path, env, dim, heads):
+    """Schedule variants that leave every output element's k-ordered accumulation unchanged
+    give bit-identical scores (env switch read once per process, so one subprocess each):
+    half-width tail tiles (gemm_enable_halftail: 6.7B qkv, 13B attn_out)."""
     import subprocess
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for flag in ("1", "0"):
         out = str(tmp_path / f"nll_{flag}.npy")
         code = _HALFTAIL_PROBE.format(repo=repo, dim=dim, heads=heads, out=out)
-        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, ZO_HALFTAIL=flag),
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **{env: flag}),
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(out))
