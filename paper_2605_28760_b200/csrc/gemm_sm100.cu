@@ -891,13 +891,16 @@ void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
   const int dp_waves = tiles / units;
   const int tail = tiles - dp_waves * units;
   const long sk_iters = (long)tail * g.num_kb;
-  const int w = (int)((sk_iters + units - 1) / units);
+  int w = (int)((sk_iters + units - 1) / units);
   // too fine: each owner would sum many partials; measured a loss at M=2048 attn_out
   // (12 tail tiles x 81 k-blocks over 74 pairs -> 14 per unit), a gain for ff_down (53)
   if (w < 32) return;
   // only a mostly-empty last wave pays for the fixup (13B: ff_down's 12 of 74 pairs,
   // 382 -> 350 us; qkv's 36/74 and ff_up's 48/74 measured neutral-to-worse)
   if (3 * tail > units) return;
+  // at most 4 units per tail tile: the owner then sums <= 3 partials (13B ff_down: 6 -> 4
+  // participants, 271 -> 265 us); the other units idle through the tail
+  if (4 * tail <= units) w = std::max(w, (g.num_kb + 3) / 4);
   g.sk = 1;
   g.sk_dp = dp_waves * units;
   g.sk_w = w;
