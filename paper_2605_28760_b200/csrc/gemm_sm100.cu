@@ -768,8 +768,8 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms) {
   const int tiles = m_tiles * n_tiles;
   if (units < 2 || tiles <= units || tiles % units == 0) return;
   const int tail = tiles % units;
-  // only a mostly-empty last wave: its 2*tail half tiles still fit one round
-  if (3 * tail > units || 2 * tail > units) return;
+  // the last wave's 2*tail half tiles must still fit one round
+  if (2 * tail > units) return;
   g.half_dp = tiles - tail;
   g.half_n = 1;
   g.grid = units * 2;
