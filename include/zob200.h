@@ -211,6 +211,10 @@ int zo_bench_gemm(zo_ctx* ctx, int32_t which, int32_t B, int32_t reps, float* av
  * scorer kernel group; ms[10] = device ms per family summed over the layers: embed, LN, qkv GEMM,
  * attention, extension finalize, attn_out GEMM, ff_up GEMM, ff_down GEMM, last-layer tail + LM
  * head + loss, other (sampler, probes, coefficient, update).  The bench's in-step roofline. */
+/* diagnostic timeline of one launch of a layer GEMM (which as zo_bench_gemm): per CTA 64
+ * globaltimer stamps -- [0] start, [1] end, [2+2i, 3+2i] MMA window and [32+2i, 33+2i]
+ * epilogue window of the CTA's i-th tile segment (i < 15); *grid = the launch's CTA count */
+int zo_trace_gemm(zo_ctx* ctx, int32_t which, int32_t B, uint64_t* host, int32_t cap, int32_t* grid);
 int zo_profile_step(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon, double lr,
                     const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B, float* ms);
 /* copy per-example NLLs between the ctx and an external device buffer

@@ -90,6 +90,7 @@ SIGNATURES = [
     ("zo_bench_gemm", _c.c_int, [_P, _c.c_int32, _c.c_int32, _c.c_int32, _c.POINTER(_c.c_float),
                                  _c.POINTER(_c.c_double)]),
     ("zo_nll_io", _c.c_int, [_P, _P, _c.c_int32, _c.c_int32]),
+    ("zo_trace_gemm", _c.c_int, [_P, _c.c_int32, _c.c_int32, _P, _c.c_int32, _c.POINTER(_c.c_int32)]),
     ("zo_profile_step", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double, _P, _P,
                                    _c.c_int32, _c.POINTER(_c.c_float)]),
     ("zo_test_gemm", _c.c_int, [_c.c_int32] * 6 + [_P, _P, _P]),

@@ -67,6 +67,11 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -206,6 +211,7 @@ struct GemmParams {
   float* sk_ws;
   unsigned* sk_flags;
   int half_dp, half_n;  // half-width tail tiles (see zo_gemm.h)
+  unsigned long long* trace;  // diagnostic timeline (see zo_gemm.h), nullptr in production
   // per-column bias (OPT arch; see zo_gemm.h) and the ReLU activation of EPI_GELU16*
   const float* bias;
   int bias_rps;
@@ -326,6 +332,8 @@ __global__ void __launch_bounds__(192, 1)
   // prologue done (barriers, TMEM, descriptor prefetch): from here on the operands and
   // the residual are read, so wait for the producing kernel (PDL, zo_common.cuh)
   pdl_wait();
+  unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * 64 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   const int num_tiles = p.m_tiles * p.n_tiles;
 
   if (warp == 0) {
@@ -379,6 +387,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(tempty0 + 8 * acc, acc_phase ^ 1);
         tc_fence_after();
+        if (tr && it < 15) tr[2 + 2 * it] = globaltimer();
         const uint32_t tmem_d = tmem_base + acc * BN;
         const uint32_t id = si.hf ? idesc_h : idesc;
         for (int kb = k0; kb < k1; ++kb) {
@@ -406,6 +415,7 @@ __global__ void __launch_bounds__(192, 1)
           tc_commit_cg2(tfull0 + 8 * acc);
         else
           tc_commit(tfull0 + 8 * acc);
+        if (tr && it < 15) tr[3 + 2 * it] = globaltimer();
       }
     }
   } else {
@@ -423,6 +433,7 @@ __global__ void __launch_bounds__(192, 1)
       const int bnc = si.hf ? BN / 2 : BN;  // columns of this (possibly half-width) tile
       mbar_wait(tfull0 + 8 * acc, acc_phase);
       tc_fence_after();
+      if (tr && warp == 2 && lane == 0 && it < 15) tr[32 + 2 * it] = globaltimer();
       const int row = m0 + erow;
       const bool row_ok = row < p.M;
       if (k0 > 0) {
@@ -646,6 +657,7 @@ __global__ void __launch_bounds__(192, 1)
         }
       }
     tile_done:
+      if (tr && warp == 2 && lane == 0 && it < 15) tr[33 + 2 * it] = globaltimer();
       if (split) {
         named_bar_sync(1, 128);
         if (warp == 2 && lane < jend - jfirst)  // re-arm the consumed flags for the next launch
@@ -668,6 +680,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
   __syncthreads();
+  if (tr && threadIdx.x == 0) tr[1] = globaltimer();
   if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/epilogues are done before TMEM is freed
   if (warp == 1) {
     tc_fence_after();
@@ -805,6 +818,7 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.sk_ws = g.sk_ws;
   p.sk_flags = g.sk_flags;
   p.half_dp = g.half_dp;
+  p.trace = g.trace;
   p.half_n = g.half_n;
   p.bias = g.bias;
   p.bias_rps = g.bias_rps;

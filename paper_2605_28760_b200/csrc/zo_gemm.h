@@ -41,6 +41,9 @@ struct GemmDesc {
   int bias_rps = 0;
   long bias_vstride = 0;
   int relu = 0;  // EPI_GELU16*: ReLU instead of GELU-tanh (OPT arch)
+  // diagnostic timeline (zo_trace_gemm): per CTA 64 globaltimer stamps -- [0] start, [1] end,
+  // [2+2i, 3+2i] MMA window of segment i (i < 15), [32+2i, 33+2i] its epilogue window
+  unsigned long long* trace = nullptr;
   // half-width tail: tiles [half_dp, tiles) run as two N/2-wide tiles each (half_n = 1)
   int half_dp = 0, half_n = 0;
   // stream-K split of the k-iteration space over the persistent CTAs (gemm_enable_streamk)

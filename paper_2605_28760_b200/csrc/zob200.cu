@@ -1672,6 +1672,31 @@ extern "C" int zo_bench_gemm(zo_ctx* c, int32_t which, int32_t B, int32_t reps, 
   ZO_API_END
 }
 
+// Diagnostic timeline of one launch of a layer GEMM (which as zo_bench_gemm): per CTA 64
+// globaltimer stamps (zo_gemm.h GemmDesc::trace) into host[grid * 64] and the grid size.
+extern "C" int zo_trace_gemm(zo_ctx* c, int32_t which, int32_t B, uint64_t* host, int32_t cap, int32_t* grid) {
+  ZO_API_BEGIN
+  check(which >= 0 && which <= 4, ZO_ERR_INPUT, "bad gemm id");
+  const int M = 2 * B * c->Tf;
+  RowPlan& rp = row_plan(c, M);
+  GemmDesc g = which == 0 ? rp.layers[0].qkv : which == 1 ? rp.layers[0].out
+             : which == 2 ? rp.layers[0].up : which == 3 ? rp.layers[0].down : rp.lm;
+  const int l = c->d.n_layers > 1 ? 1 : 0;
+  const GemmDesc& g2 = which == 0 ? rp.layers[l].qkv : which == 1 ? rp.layers[l].out
+                     : which == 2 ? rp.layers[l].up : which == 3 ? rp.layers[l].down : rp.lm;
+  check(cap >= g.grid * 64, ZO_ERR_DIMENSION, "trace buffer too small");
+  DevAlloc tmp;
+  unsigned long long* d = tmp.get<unsigned long long>((size_t)g.grid * 64);
+  for (int i = 0; i < 6; ++i) gemm_launch((i & 1) ? g2 : g, c->st);  // warm, alternating weights
+  g.trace = d;
+  gemm_launch(g, c->st);
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  ZO_CUDA_TRY(cudaMemcpy(host, d, (size_t)g.grid * 64 * 8, cudaMemcpyDeviceToHost));
+  *grid = g.grid;
+  return ZO_OK;
+  ZO_API_END
+}
+
 // External device buffer <-> ctx per-example NLLs [2, B] (multi-GPU exact mode
 // exchanges them between the scoring and the coefficient phases).
 extern "C" int zo_nll_io(zo_ctx* c, void* dev, int32_t count, int32_t to_ctx) {

@@ -322,6 +322,14 @@ class ZoEngine:
         check(lib().zo_bench_gemm(self._h, which, B, reps, ctypes.byref(ms), ctypes.byref(fl)))
         return float(ms.value), float(fl.value)
 
+    def trace_gemm(self, which: int, B: int) -> np.ndarray:
+        """Per-CTA timeline of one launch of layer GEMM `which` (zob200.h zo_trace_gemm):
+        [grid, 64] globaltimer ns -- start, end, MMA and epilogue windows per tile segment."""
+        buf = np.zeros(256 * 64, dtype=np.uint64)
+        g = ctypes.c_int32()
+        check(lib().zo_trace_gemm(self._h, which, B, buf.ctypes.data, buf.size, ctypes.byref(g)))
+        return buf[: g.value * 64].reshape(g.value, 64)
+
     PROFILE_FAMILIES = ("embed", "ln", "qkv", "attention", "ext_finalize", "attn_out", "ff_up", "ff_down", "tail",
                         "other")
 
