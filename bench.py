@@ -136,7 +136,7 @@ def ncu_traffic(model):
     """DRAM bytes (read + write) of one launch of each of the four layer GEMMs, from the
     committed `ncu --set full` capture (profiles/), or None when not captured for this model."""
     import csv
-    p = os.path.join(HERE, "profiles", "r01f_ncu_gemm_opt13b.csv")
+    p = os.path.join(HERE, "profiles", "r01g_ncu_gemm_opt13b.csv")
     if model != "opt-13b" or not os.path.exists(p):
         return None
     tot = 0.0
