@@ -31,6 +31,12 @@ def main():
     ap.add_argument("--dev-size", type=int, default=64)
     ap.add_argument("--lr", type=float, default=1e-7)
     ap.add_argument("--out", default="gpurun_out/long")
+    ap.add_argument("--estimator", default="lozo_lazy", choices=["lozo_lazy", "factorized_sqrt_r"],
+                    help="factorized_sqrt_r with --rank 128 = BASELINE config 5 (1000 steps)")
+    ap.add_argument("--rank", type=int, default=2)
+    ap.add_argument("--digests", choices=["auto", "on", "off"], default="auto",
+                    help="per-step U/V digests on the host pool; auto = off above rank 8 (r = 128 means "
+                         "3.4 GB of directions per step, SURVEY.md §0 fact 7)")
     a = ap.parse_args()
     from paper_2605_28760_b200 import model as M
     from paper_2605_28760_b200.runtime import run_serving_path
@@ -39,20 +45,23 @@ def main():
     mcfg = M.ModelConfig(prompt_len=63, init_seed=7, init_scale=0.02, **mdl)
     task = M.generate_task(M.TaskConfig(seed=11, vocab=mdl["vocab"], prompt_len=63, train_size=1000,
                                         dev_size=a.dev_size, val_size=8))
-    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=a.lr, rank=2, nu=50, batch_size=16)
+    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=a.lr, rank=a.rank, nu=50, batch_size=16,
+                    estimator=a.estimator)
     t0 = time.perf_counter()
+    digests = a.digests == "on" or (a.digests == "auto" and a.rank <= 8)
     run = run_serving_path(mcfg, task, zcfg, a.steps, precision="fp16", eval_every=a.eval_every,
-                           compute_param_digests=False)
+                           compute_param_digests=False, digests=digests)
     wall = time.perf_counter() - t0
     os.makedirs(a.out, exist_ok=True)
-    write_trajectory(os.path.join(a.out, f"traj_{a.model}_{a.steps}.jsonl"),
+    tag = f"{a.model}_{a.steps}" + ("" if a.estimator == "lozo_lazy" else f"_fact_r{a.rank}")
+    write_trajectory(os.path.join(a.out, f"traj_{tag}.jsonl"),
                      {"model": mdl, "steps": a.steps, "zo_digest": zcfg.digest()}, run.trajectory,
                      {"eval_loss": run.eval_curve[-1].loss, "eval_acc": run.eval_curve[-1].acc})
-    summary = {"model": a.model, "steps": run.steps_completed, "train_wall_s": run.train_wall_s,
+    summary = {"model": a.model, "estimator": a.estimator, "rank": a.rank, "steps": run.steps_completed, "train_wall_s": run.train_wall_s,
                "steps_per_s_train": run.steps_completed / run.train_wall_s, "total_wall_s": wall,
                "meter": run.meter.to_dict(), "eval_curve": [p.to_dict() for p in run.eval_curve],
                "last_record": run.trajectory[-1].to_dict()}
-    with open(os.path.join(a.out, f"summary_{a.model}_{a.steps}.json"), "w") as f:
+    with open(os.path.join(a.out, f"summary_{tag}.json"), "w") as f:
         json.dump(summary, f, indent=1)
     print(json.dumps({k: summary[k] for k in ("model", "steps", "train_wall_s", "steps_per_s_train")}))
 
