@@ -17,7 +17,7 @@ from dataclasses import asdict, dataclass
 import numpy as np
 
 from .adapter import AdapterState, LoraSlot
-from .engine import V as SLOT_V, U as SLOT_U, Z as SLOT_Z
+from .engine import V as SLOT_V, U as SLOT_U, Z as SLOT_Z, ZM as SLOT_ZM
 from .errors import ConfigError, InputError
 from .model import Minibatch, ModelConfig, as_device_params, matrix_ids
 from .engine import resolve_precision
@@ -153,14 +153,27 @@ def step_directions(params, zcfg: ZoConfig, step: int, mcfg: ModelConfig | None 
     Device-sampled; the host copies are for inspection / digests."""
     dp = as_device_params(params, mcfg or params.cfg)
     eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, scope=zcfg.scope)
+
+    def vector_dirs():
+        z, out, off = eng.get_slot(SLOT_Z), {}, 0
+        for vid in eng.vids:  # sorted ids, per-id lengths (OPT biases are 3d / 4d long)
+            n = eng.vlens[vid]
+            out[vid] = z[off:off + n].copy()
+            off += n
+        return out
+
+    if zcfg.estimator == "dense_mezo":  # dense z for every parameter (zo_engine.py:235-246)
+        eng.baseline_directions(zcfg.seed, step, zcfg.nu)
+        zm = eng.get_slot(SLOT_ZM)
+        mats = {l: zm[eng.zm_off[l]: eng.zm_off[l] + eng.shapes[l][0] * eng.shapes[l][1]].reshape(eng.shapes[l])
+                for l in eng.lids}
+        return StepDirections(mats, vector_dirs(), digest_hex(eng.digest(SLOT_U)), digest_hex(FNV_OFFSET_BASIS),
+                              1.0)
     eng.sample_v(zcfg.seed, step, zcfg.nu if zcfg.estimator == "lozo_lazy" else 1)
     eng.sample_u(zcfg.seed, step)
     u_ar, v_ar = eng.get_slot(SLOT_U), eng.get_slot(SLOT_V)
     U, Vd = eng.split(SLOT_U, u_ar), eng.split(SLOT_V, v_ar)
-    vectors = {}
-    if zcfg.scope == "full":
-        z = eng.get_slot(SLOT_Z)
-        vectors = {vid: z[i * eng.dim:(i + 1) * eng.dim].copy() for i, vid in enumerate(eng.vids)}
+    vectors = vector_dirs() if zcfg.scope == "full" else {}
     scale = 1.0 if zcfg.estimator == "lozo_lazy" else 1.0 / math.sqrt(zcfg.rank)
     return StepDirections({l: (U[l], Vd[l]) for l in eng.lids}, vectors, digest_hex(eng.digest(SLOT_U, u_ar)),
                           digest_hex(eng.digest(SLOT_V, v_ar)), scale)

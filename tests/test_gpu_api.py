@@ -178,3 +178,25 @@ def test_checkpoint_resume_bit_identical(golden_dir, tmp_path):
         assert (a.step, a.loss_plus, a.loss_minus, a.beta, a.u_digest, a.v_digest) == \
                (b.step, b.loss_plus, b.loss_minus, b.beta, b.u_digest, b.v_digest)
     assert rest.final_params_digest == full.final_params_digest
+
+
+@pytest.mark.parametrize("name", ["micro_lozo", "micro_full", "micro_fact", "micro_baseline_dense"])
+def test_step_directions_match_reference(golden_dir, name):
+    """zo_engine.step_directions (zo_engine.py:224-261) on the device: the chained U/V digests of
+    the reference's records, matrices / vectors of the right shapes (dense_mezo: a dense z per
+    weight, no V part)."""
+    from oracle import reference as R
+    from paper_2605_28760_b200.zo_engine import step_directions
+    h, recs, _ = _traj(golden_dir, f"traj_{name}.jsonl")
+    M, mcfg, task, zcfg = _setup(h)
+    params = M.init_params(mcfg, max_batch=zcfg.batch_size)
+    for t in (0, 1):
+        d = step_directions(params, zcfg, t, mcfg)
+        assert (d.u_digest, d.v_digest) == (recs[t]["u_digest"], recs[t]["v_digest"])
+    if zcfg.estimator == "dense_mezo":
+        lid = "blk1.ff_up"
+        np.testing.assert_array_equal(d.matrices[lid], R.gaussian(zcfg.seed, 1, lid, R.ROLE_DENSE_Z,
+                                                                  *d.matrices[lid].shape))
+        assert set(d.vectors) == set(params.engine.vids)
+    elif zcfg.scope == "full":
+        assert all(v.shape == (mcfg.dim,) for v in d.vectors.values())
