@@ -112,6 +112,10 @@ int zo_sample_stream(zo_ctx* ctx, uint64_t seed, uint64_t step, uint64_t lid_has
 int zo_slot_count(const zo_ctx* ctx, int32_t which, int64_t* count);
 int zo_get_slot(zo_ctx* ctx, int32_t which, double* host, int64_t count);
 int zo_set_slot(zo_ctx* ctx, int32_t which, const double* host, int64_t count);
+/* declare which window start the V arena holds (a host upload of V leaves it
+ * unknown, so the next step would fold A and resample V): resuming mid-window
+ * (load_checkpoint) keeps the reference's fold schedule (runtime.py:327-330). */
+int zo_set_window(zo_ctx* ctx, int64_t window_start);
 /* sampler diagnostics: [short streams, exp near-ties, splice repairs] since create */
 int zo_sampler_flags(zo_ctx* ctx, uint32_t flags[3]);
 

@@ -81,6 +81,17 @@ class AdapterState:
         self._host_dirty = bool(entries)
         self._engine = None
         self._probe_on = False
+        self._version = 0
+
+    @property
+    def version(self) -> int:
+        """Mutation counter: bumped by every slot edit (entries, probes, frozen
+        slots) and by every device update of the window A.  Scorers that cache
+        L- between the +1 and -1 calls key the cache on it."""
+        return self._version
+
+    def _touch(self) -> None:
+        self._version += 1
 
     # ---- reference surface
     @property
@@ -108,6 +119,7 @@ class AdapterState:
         elif (e.m, e.n) != (m, n):
             raise DimensionError(f"entry {layer_id} registered as {e.m}x{e.n}")
         self._host_dirty = True
+        self._touch()
         return e
 
     def set_sign(self, sign: int) -> None:
@@ -119,11 +131,13 @@ class AdapterState:
         e = self.ensure_entry(layer_id, left.shape[0], right.shape[0])
         e.perturb_slot = LoraSlot(left, right, 1.0)
         self._probe_on = True
+        self._touch()
 
     def clear_probes(self) -> None:
         for e in self._host_entries.values():
             e.perturb_slot = None
         self._probe_on = False
+        self._touch()
 
     def view(self):
         return _StateView(self)
@@ -134,6 +148,7 @@ class AdapterState:
         if len(e.update_slots) > self.slot_cap:
             e.update_slots = [merge_slots(e.update_slots)]
         self._host_dirty = True
+        self._touch()
 
     # ---- engine binding
     def _bind(self, engine) -> None:
@@ -171,6 +186,13 @@ class AdapterState:
         eng.set_slot(1, eng.join(1, Vw))
         eng.set_slot(2, eng.join(2, A))
         eng.set_slot(0, eng.join(0, Up))
+        # a host V has no window key unless the caller knows it (load_checkpoint); without
+        # one the next step folds the uploaded A with this V and resamples V
+        hint = getattr(self, "_window_hint", None)
+        if hint is not None:
+            eng.set_window(hint)
+        self._window = hint
+        self._window_hint = None
         self._host_dirty = False
 
 

@@ -115,6 +115,7 @@ def run_baseline(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: int, 
             do_eval(t + 1)
     do_eval(steps)
     dp.invalidate()
+    dp.sync_host()  # the reference mutates the caller's params dict in place
     return BaselineRun(config=zcfg, model_config=mcfg, trajectory=trajectory, eval_curve=evals,
                        weight_write_count=4 * per_step * steps, meter=meter,
                        final_params_digest=params_digest(dp) if compute_param_digests else "", params=dp,

@@ -1036,8 +1036,26 @@ int zo_set_slot(zo_ctx* c, int32_t which, const double* host, int64_t count) {
   check(which >= 0 && which <= 2, ZO_ERR_INPUT, "bad slot id");
   check(count == (which == 1 ? c->sv : c->su), ZO_ERR_DIMENSION, "slot arena size mismatch");
   ZO_CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, which), host, (size_t)count * 8, cudaMemcpyHostToDevice, c->st));
-  if (which == 1) write_vext_all(c);
+  if (which == 1) {
+    write_vext_all(c);
+    // a host V carries no window key: the next step resamples V (folding A with THIS V
+    // first) unless the caller declares the window with zo_set_window
+    c->v_window = -2;
+  }
+  if (which == 2) {
+    bool nz = false;
+    for (int64_t i = 0; i < count && !nz; ++i) nz = host[i] != 0.0;
+    c->a_dirty = nz;  // uploaded window mass must be folded before V changes
+  }
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_set_window(zo_ctx* c, int64_t window_start) {
+  ZO_API_BEGIN
+  check(window_start >= -1, ZO_ERR_INPUT, "window start must be >= -1");
+  c->v_window = window_start;
   return ZO_OK;
   ZO_API_END
 }

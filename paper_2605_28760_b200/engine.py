@@ -179,6 +179,10 @@ class ZoEngine:
             raise DimensionError(f"slot arena has {a.size} values, expected {n}")
         check(lib().zo_set_slot(self._h, which, a.ctypes.data, n))
 
+    def set_window(self, window_start: int) -> None:
+        """Declare the window start whose V the arena holds (zob200.h zo_set_window)."""
+        check(lib().zo_set_window(self._h, int(window_start)))
+
     def split(self, which: int, arena: np.ndarray) -> dict[str, np.ndarray]:
         out = {}
         for lid in self.lids:

@@ -112,6 +112,7 @@ class DeviceParams(Mapping):
         self.max_batch = max_batch
         self.device = device
         self._opt_len = 1
+        self._mirror = None  # caller's host dict (as_device_params), written back by sync_host
 
     # Mapping protocol
     def __getitem__(self, lid: str) -> np.ndarray:
@@ -191,6 +192,17 @@ class DeviceParams(Mapping):
         self._engine = e
         return e
 
+    def sync_host(self, matrices: bool = True, vectors: bool = True) -> None:
+        """Write the device values back into the host dict this replica was made from
+        (in place, like the reference's mutations); no-op for device-born params."""
+        mirror = getattr(self, "_mirror", None)
+        if mirror is None or self._engine is None:
+            return
+        self.invalidate()
+        for k in list(mirror):
+            if (np.ndim(mirror[k]) == 2 and matrices) or (np.ndim(mirror[k]) == 1 and vectors):
+                mirror[k][...] = self[k]
+
     def to_host(self) -> dict[str, np.ndarray]:
         return {k: np.array(self[k]) for k in self}
 
@@ -202,11 +214,29 @@ def init_params(cfg: ModelConfig, precision: str = "fp16", max_batch: int = 16, 
     return DeviceParams(cfg, precision=precision, max_batch=max_batch, device=device)
 
 
+# the last plain host dict a step function saw and its device replica: the reference's
+# params are a caller-owned dict mutated in place (runtime.py:242-250, zo_engine.py:449-450),
+# so a dict keeps ONE replica across calls and mutating entry points write back into it
+_HOST_BINDING: list = [None, None]
+
+
 def as_device_params(params, cfg: ModelConfig) -> DeviceParams:
+    """``params`` as a device replica.  A :class:`DeviceParams` is used as is.  A plain
+    mapping (the reference's dict) is uploaded once and the replica cached by identity;
+    the device copy is authoritative from then on, and the step functions that mutate
+    parameters (folds, factorized / dense updates, full-scope vector updates) write
+    the new values back into the caller's arrays in place (``sync_host``).  Use
+    ``DeviceParams`` directly at scale: the write-back downloads every matrix."""
     if isinstance(params, DeviceParams):
         return params
     if isinstance(params, Mapping):
-        return DeviceParams(cfg, host=params)
+        dp = _HOST_BINDING[1]
+        if _HOST_BINDING[0] is params and dp is not None and dp.cfg == cfg:
+            return dp
+        dp = DeviceParams(cfg, host=params)
+        dp._mirror = params
+        _HOST_BINDING[0], _HOST_BINDING[1] = params, dp
+        return dp
     raise InputError("params must be a mapping of layer id -> array")
 
 

@@ -134,9 +134,10 @@ def install_into_zoserve(zoserve, rank: int = 2, batch_size: int = 16, precision
         ent[1].state = state
         return ent[1]
 
-    def forward_score(params, cfg, batch, view=None, precision_arg="real64"):
+    def forward_score(params, cfg, batch, view=None, precision="real64"):
+        # same signature as model.py:223-229; _MeteredScorer passes view= and precision= by keyword
         if view is None:
-            return orig_fs(params, cfg, batch, view, precision_arg)
+            return orig_fs(params, cfg, batch, view=view, precision=precision)
         state = view.__closure__[0].cell_contents  # AdapterState.view() closure (adapter.py:181-190)
         return scorer_for(params, cfg, state)(batch)
 

@@ -151,6 +151,7 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
         wall += dt
     if not aborted:
         do_eval(done)
+    dp.sync_host()  # a caller's host dict sees the folds, as in the reference (runtime.py:242-250)
     for rec, uf, vf in pending:
         rec.u_digest = digest_hex(uf.result())
         rec.v_digest = digest_hex(vf.result())
@@ -220,4 +221,8 @@ def load_checkpoint(path: str, precision: str = "fp16", max_batch: int = 16, dev
     for e in state._host_entries.values():
         e.perturb_slot = None  # probes are per-step and never carried across steps
     state._probe_on = False
-    return params, state, int(meta["next_step"]), meta
+    nxt = int(meta["next_step"])
+    if meta["zo"].get("estimator", "lozo_lazy") == "lozo_lazy":
+        nu = int(meta["zo"]["nu"])
+        state._window_hint = (nxt // nu) * nu  # the saved V is this window's (mid-window resume)
+    return params, state, nxt, meta

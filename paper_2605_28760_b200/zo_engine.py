@@ -17,11 +17,12 @@ from dataclasses import asdict, dataclass
 import numpy as np
 
 from .adapter import AdapterState, LoraSlot
-from .engine import V as SLOT_V, U as SLOT_U, Z as SLOT_Z, ZM as SLOT_ZM
+from .engine import V as SLOT_V, U as SLOT_U
 from .errors import ConfigError, InputError
-from .model import Minibatch, ModelConfig, as_device_params, matrix_ids
+from .model import Minibatch, ModelConfig, as_device_params, matrix_ids, vector_ids
 from .engine import resolve_precision
-from .numerics import FNV_OFFSET_BASIS, Role, StreamKey, canonical_mean, digest_hex, digest_text, sample_gaussian
+from .numerics import (FNV_OFFSET_BASIS, Role, StreamKey, canonical_mean, digest_array, digest_hex, digest_text,
+                       gaussian_vector, sample_gaussian)
 
 __all__ = ["SCOPES", "ESTIMATORS", "ZoConfig", "ZoStepRecord", "write_trajectory", "read_trajectory",
            "lozo_direction", "factorized_direction", "StepDirections", "step_directions",
@@ -148,35 +149,60 @@ def _engine_for(params, mcfg: ModelConfig, zcfg: ZoConfig, batch: Minibatch):
     return dp, eng
 
 
+def _chain(h: int, layer_id: str, a: np.ndarray) -> int:
+    return digest_array(a, digest_text(layer_id, h))
+
+
+def _dense_direction(seed: int, step: int, layer_id: str, shape) -> np.ndarray:
+    """zo_engine.py:193-198: Role.DENSE_Z stream of one parameter."""
+    key = StreamKey(seed, step, layer_id, Role.DENSE_Z)
+    if len(shape) == 1:
+        return gaussian_vector(key, shape[0])
+    return sample_gaussian(key, shape[0], shape[1])
+
+
 def step_directions(params, zcfg: ZoConfig, step: int, mcfg: ModelConfig | None = None) -> StepDirections:
     """Every direction of one step plus chained digests (zo_engine.py:224-261).
-    Device-sampled; the host copies are for inspection / digests."""
-    dp = as_device_params(params, mcfg or params.cfg)
-    eng = dp.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, scope=zcfg.scope)
 
-    def vector_dirs():
-        z, out, off = eng.get_slot(SLOT_Z), {}, 0
-        for vid in eng.vids:  # sorted ids, per-id lengths (OPT biases are 3d / 4d long)
-            n = eng.vlens[vid]
-            out[vid] = z[off:off + n].copy()
-            off += n
-        return out
+    Pure, like the reference: each stream is drawn by the device sampler into a
+    fresh host array (``zo_sample_stream``); the engine's U/V/A arenas, its
+    window and its float64 masters are not touched, so calling this mid-run
+    leaves the trajectory unchanged.  ``mcfg`` is accepted for symmetry with the
+    other entry points and unused (shapes come from ``params``)."""
+    def shape_of(lid):
+        return params.shape_of(lid) if hasattr(params, "shape_of") else np.shape(params[lid])
 
-    if zcfg.estimator == "dense_mezo":  # dense z for every parameter (zo_engine.py:235-246)
-        eng.baseline_directions(zcfg.seed, step, zcfg.nu)
-        zm = eng.get_slot(SLOT_ZM)
-        mats = {l: zm[eng.zm_off[l]: eng.zm_off[l] + eng.shapes[l][0] * eng.shapes[l][1]].reshape(eng.shapes[l])
-                for l in eng.lids}
-        return StepDirections(mats, vector_dirs(), digest_hex(eng.digest(SLOT_U)), digest_hex(FNV_OFFSET_BASIS),
-                              1.0)
-    eng.sample_v(zcfg.seed, step, zcfg.nu if zcfg.estimator == "lozo_lazy" else 1)
-    eng.sample_u(zcfg.seed, step)
-    u_ar, v_ar = eng.get_slot(SLOT_U), eng.get_slot(SLOT_V)
-    U, Vd = eng.split(SLOT_U, u_ar), eng.split(SLOT_V, v_ar)
-    vectors = vector_dirs() if zcfg.scope == "full" else {}
-    scale = 1.0 if zcfg.estimator == "lozo_lazy" else 1.0 / math.sqrt(zcfg.rank)
-    return StepDirections({l: (U[l], Vd[l]) for l in eng.lids}, vectors, digest_hex(eng.digest(SLOT_U, u_ar)),
-                          digest_hex(eng.digest(SLOT_V, v_ar)), scale)
+    mids, vids = matrix_ids(params), vector_ids(params)
+    hu = hv = FNV_OFFSET_BASIS
+    matrices: dict = {}
+    vectors: dict = {}
+    scale = 1.0
+    if zcfg.estimator == "dense_mezo":
+        for lid in mids:
+            z = _dense_direction(zcfg.seed, step, lid, shape_of(lid))
+            matrices[lid] = z
+            hu = _chain(hu, lid, z)
+        for lid in vids:
+            z = _dense_direction(zcfg.seed, step, lid, shape_of(lid))
+            vectors[lid] = z
+            hu = _chain(hu, lid, z)
+        return StepDirections(matrices, vectors, digest_hex(hu), digest_hex(hv))
+    for lid in mids:
+        m, n = shape_of(lid)
+        if zcfg.estimator == "lozo_lazy":
+            u, v = lozo_direction(zcfg.seed, step, lid, m, n, zcfg.rank, zcfg.nu)
+        else:
+            slot = factorized_direction(zcfg.seed, step, lid, m, n, zcfg.rank)
+            u, v, scale = slot.A, slot.B, slot.scale
+        matrices[lid] = (u, v)
+        hu = _chain(hu, lid, u)
+        hv = _chain(hv, lid, v)
+    if zcfg.scope == "full":
+        for lid in vids:
+            z = _dense_direction(zcfg.seed, step, lid, shape_of(lid))
+            vectors[lid] = z
+            hu = _chain(hu, lid, z)
+    return StepDirections(matrices, vectors, digest_hex(hu), digest_hex(hv), scale)
 
 
 # --------------------------------------------------------------------------- coefficient
@@ -234,7 +260,9 @@ def _digests(state: AdapterState, eng, zcfg: ZoConfig, step: int, mode: str):
 class GpuPairScorer:
     """The reference's ``scorer`` protocol (zo_engine.py:340-346) on the engine:
     the +1 call scores both probes in one fused launch and caches L-; the -1
-    call returns the cached value.  Pure: writes no weights."""
+    call returns the cached value only if neither the minibatch nor the adapter
+    changed in between (batch id + ``AdapterState.version``).  Pure: writes no
+    weights."""
 
     def __init__(self, params, mcfg: ModelConfig, state: AdapterState):
         self.dp = as_device_params(params, mcfg)
@@ -243,23 +271,24 @@ class GpuPairScorer:
         self._cached = None
 
     def __call__(self, batch: Minibatch) -> float:
-        from .numerics import canonical_mean
         eng = self.dp.engine
         sign = self.state.perturb_sign
-        tokens, gold = batch.sequences()
-        if sign == -1 and self._cached is not None and self._cached[0] == batch.batch_id:
+        key = (batch.batch_id, self.state.version)
+        if sign == -1 and self._cached is not None and self._cached[0] == key:
             v = self._cached[1]
             self._cached = None
             return v
+        self._cached = None
+        tokens, gold = batch.sequences()
         self.state._sync_to_engine(eng)
         if sign == 0 or not self.state._probe_on:
             eng.prepare_probe(self.state.epsilon, 1)
             return canonical_mean(eng.score(tokens, gold, nsign=1)[0])
         eng.prepare_probe(self.state.epsilon, 0)
-        nll = eng.score(tokens, gold, nsign=2)
+        nll = eng.score(tokens, np.stack([gold, gold]), nsign=2)  # one gold block per probe half
         lp, lm = canonical_mean(nll[0]), canonical_mean(nll[1])
         if sign == 1:
-            self._cached = (batch.batch_id, lm)
+            self._cached = (key, lm)
             return lp
         return lm
 
@@ -289,6 +318,7 @@ def lozo_step(params, mcfg: ModelConfig, state: AdapterState, zcfg: ZoConfig, st
             state._window = window
         eng.sample_u(zcfg.seed, step)
         state._probe_on = True
+        state._touch()  # new probe U on the device
         try:
             c, lp, lm = estimate_coefficient(scorer, state, zcfg.epsilon, batch)
         finally:
@@ -299,6 +329,9 @@ def lozo_step(params, mcfg: ModelConfig, state: AdapterState, zcfg: ZoConfig, st
         eng.update_u()
         eng.update_vectors(zcfg.learning_rate)  # full scope: VectorProbe.update (zo_engine.py:412-416)
         dp.invalidate()
+    state._touch()  # the window A moved
+    if zcfg.scope == "full":
+        dp.sync_host(matrices=False)  # VectorProbe.update mutated the caller's 1-D params
     ud, vd = _digests(state, eng, zcfg, step, digests)
     return make_step_record(zcfg, step, lp, lm, beta, ud, vd, batch)
 
@@ -316,6 +349,8 @@ def factorized_step(params, mcfg: ModelConfig, state: AdapterState, zcfg: ZoConf
     tokens, gold = batch.sequences()
     out = eng.step(zcfg.seed, step, 1, zcfg.epsilon, zcfg.learning_rate, False, tokens, gold)
     dp.invalidate()
+    dp.sync_host()  # the dense update wrote every matrix (zo_engine.py:449-450)
+    state._touch()
     ud, vd = _digests(state, eng, zcfg, step, digests)
     return make_step_record(zcfg, step, float(out[0]), float(out[1]), -(zcfg.learning_rate * float(out[2])),
                             ud, vd, batch)
@@ -347,6 +382,7 @@ def dense_mezo_step(params, mcfg: ModelConfig, zcfg: ZoConfig, step: int, batch:
     eng.set_coefficient([lp, lm, c, beta])
     eng.baseline_update(zcfg.learning_rate, False)
     dp.invalidate()
+    dp.sync_host()
     u = digest_hex(eng.digest(SLOT_U)) if digests != "off" else ""
     v = digest_hex(eng.digest(SLOT_V)) if digests != "off" else ""
     return make_step_record(zcfg, step, lp, lm, beta, u, v, batch)

@@ -6,6 +6,9 @@ import pytest
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:
     sys.path.insert(0, REPO)
+_TESTS = os.path.join(REPO, "tests")
+if _TESTS not in sys.path:  # zo_tolerances
+    sys.path.insert(0, _TESTS)
 GOLDEN = os.path.join(REPO, "tests", "golden")
 
 

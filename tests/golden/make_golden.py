@@ -6,6 +6,8 @@ the committed JSON/JSONL this script writes):
 
     python tests/golden/make_golden.py            # fast fixtures (~1 min)
     python tests/golden/make_golden.py --opt125m  # + OPT-125m-dims steps (~2 min)
+    python tests/golden/make_golden.py --config1  # BASELINE config 1, 50 steps (~20 min)
+    python tests/golden/make_golden.py --real32   # real32 trajectories (micro, small)
 
 Fixtures
   streams.json      sample_gaussian digests / heads / u64 consumption for a key
@@ -166,6 +168,8 @@ SMALL = dict(vocab=512, dim=128, n_layers=2, n_heads=2, prompt_len=63, init_seed
 SMALL_TASK = dict(seed=11, vocab=512, prompt_len=63, train_size=1000, dev_size=4, val_size=4)
 OPT125 = dict(vocab=50272, dim=768, n_layers=12, n_heads=12, prompt_len=63, init_seed=7, init_scale=0.02)
 OPT125_TASK = dict(seed=11, vocab=50272, prompt_len=63, train_size=1000, dev_size=2, val_size=2)
+# BASELINE config 1 as SURVEY.md §8(c) anchors it (task_digest 7bd7555e57d086df): dev/val 64
+OPT125_TASK64 = dict(seed=11, vocab=50272, prompt_len=63, train_size=1000, dev_size=64, val_size=64)
 
 
 def baseline_trajectory(name, mcfg_kw, tcfg_kw, zcfg_kw, steps, recompute=False, precision="real64"):
@@ -235,8 +239,23 @@ def full_scope_trajectories():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--opt125m", action="store_true")
+    ap.add_argument("--config1", action="store_true",
+                    help="BASELINE config 1 in full: 50 run_serving_path steps at OPT-125m dims (~20 min)")
+    ap.add_argument("--real32", action="store_true", help="real32 trajectories (micro, small)")
     ap.add_argument("--only", default=None, help="regenerate one fixture family (e.g. 'adapter')")
     a = ap.parse_args()
+    if a.config1:
+        trajectory("opt125m_lozo50", OPT125, OPT125_TASK64,
+                   dict(seed=42, epsilon=1e-3, learning_rate=1e-7, rank=2, nu=50, batch_size=16), 50)
+        return
+    if a.real32:
+        trajectory("micro_lozo_real32", MICRO, MICRO_TASK,
+                   dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=5, batch_size=8), 12,
+                   precision="real32")
+        trajectory("small_lozo_real32", SMALL, SMALL_TASK,
+                   dict(seed=42, epsilon=1e-3, learning_rate=1e-3, rank=2, nu=4, batch_size=16), 10,
+                   precision="real32")
+        return
     if a.only == "adapter":
         adapter_fixture()
         return

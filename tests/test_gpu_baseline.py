@@ -17,6 +17,8 @@ import os
 import numpy as np
 import pytest
 
+import zo_tolerances as _T
+
 pytestmark = pytest.mark.gpu
 
 NAMES = ["micro_baseline", "micro_baseline_recompute", "micro_baseline_fact", "micro_baseline_full",
@@ -64,7 +66,7 @@ def test_materialised_writes_bit_exact_with_reference_coefficients(golden_dir, n
         eng.baseline_pass(2, zcfg.epsilon, rc)
         lp, lm = rec["loss_plus"], rec["loss_minus"]
         # the device losses of the materialised weights track the reference (fp16 scoring)
-        assert abs(lp_lm[0] - lp) < 2e-2 and abs(lp_lm[1] - lm) < 2e-2
+        assert abs(lp_lm[0] - lp) <= _T.LOSS_MATERIALISED and abs(lp_lm[1] - lm) <= _T.LOSS_MATERIALISED
         c = (lp - lm) / (2.0 * zcfg.epsilon)
         assert c == rec["coefficient"]
         eng.set_coefficient([lp, lm, c, rec["beta"]])
@@ -86,11 +88,11 @@ def test_run_baseline_vs_reference(golden_dir, name):
     signs = 0
     for a, b in zip(recs, run.trajectory):
         assert (a["u_digest"], a["v_digest"], a["minibatch_id"]) == (b.u_digest, b.v_digest, b.minibatch_id)
-        assert abs(a["loss_plus"] - b.loss_plus) < 1.5e-2
-        assert abs(a["loss_minus"] - b.loss_minus) < 1.5e-2
+        assert abs(a["loss_plus"] - b.loss_plus) <= _T.LOSS_MATERIALISED
+        assert abs(a["loss_minus"] - b.loss_minus) <= _T.LOSS_MATERIALISED
         signs += np.sign(a["coefficient"]) == np.sign(b.coefficient)
     assert signs >= 0.75 * len(recs)
-    assert abs(run.eval_curve[-1].loss - fin["eval_loss"]) < 2e-2
+    assert abs(run.eval_curve[-1].loss - fin["eval_loss"]) <= _T.LOSS_MATERIALISED
     out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out", f"parity_{name}_b200.jsonl")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     compare_ready_export(run, out)
@@ -157,7 +159,7 @@ def test_high_rank_materialising_writes_bit_exact(recompute):
         for p in (0, 1):
             eng.baseline_pass(p, 1e-3, recompute)
             got = R.canonical_mean(eng.score(tokens, gold, nsign=1)[0])
-            assert abs(got - (rec.loss_plus if p == 0 else rec.loss_minus)) < 2e-2
+            assert abs(got - (rec.loss_plus if p == 0 else rec.loss_minus)) <= _T.LOSS_MATERIALISED
         eng.baseline_pass(2, 1e-3, recompute)
         eng.set_coefficient([rec.loss_plus, rec.loss_minus, rec.coefficient, rec.beta])
         eng.baseline_update(1e-3, recompute)
@@ -178,7 +180,7 @@ def test_dense_mezo_step_api_bit_exact(golden_dir):
         out = dense_mezo_step(params, mcfg, zcfg, t, batch)
         assert (out.u_digest, out.v_digest, out.minibatch_id) == (rec["u_digest"], rec["v_digest"],
                                                                    rec["minibatch_id"])
-        assert abs(out.loss_plus - rec["loss_plus"]) < 1.5e-2 and abs(out.loss_minus - rec["loss_minus"]) < 1.5e-2
+        assert abs(out.loss_plus - rec["loss_plus"]) <= _T.LOSS["fp16"] and abs(out.loss_minus - rec["loss_minus"]) <= _T.LOSS["fp16"]
     from paper_2605_28760_b200.errors import ConfigError
     with pytest.raises(ConfigError):
         dense_mezo_step(params, mcfg, zcfg, 0, M.sample_minibatch(task, "train", zcfg.seed, 0, zcfg.batch_size),

@@ -1,0 +1,209 @@
+"""Parity at the BASELINE configurations' own shapes.
+
+* Config 1 (OPT-125m dims, V = 50272, B = 16, T = 64, lr 1e-7, nu = 50) against
+  the reference's own outputs (tests/golden/make_golden.py --opt125m / --config1):
+  - ``forward_opt125m.json``: per-example option NLLs at sign +1 / -1 / 0;
+  - ``traj_opt125m_lozo50.jsonl`` (falls back to the 3-step ``traj_opt125m_lozo``):
+    ``run_serving_path`` end to end -- U/V digests and minibatch ids exact,
+    |dL+-| <= 2e-3, |dc|/|c| <= 2e-2 on high-signal steps, and,
+    with the reference's coefficients injected through the ``scorer=`` seam, the
+    final float64 params digest bit-exact.
+* OPT-13B dims (d = 5120, H = 40, dh = 128, V = 50272, M = 2 * 16 * 63 rows): one
+  decoder block + the tied LM head + the loss against the float64 oracle on the
+  same weights.  The GEMM schedule (CTA pairs, stream-K tail, half-width tail
+  tiles) depends on (M, N, K) only, so one block runs exactly the 13B kernels.
+
+Tolerances are ~3x the errors observed on the B200 (profiles/r02*_parity).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import zo_tolerances as TOL
+from oracle import reference as R
+
+pytestmark = pytest.mark.gpu
+
+NLL_TOL, DL_REL, TRAJ_DL, C_REL, HIGH_SIGNAL = TOL.NLL, TOL.DL_REL, TOL.LOSS["fp16"], TOL.C_REL, TOL.HIGH_SIGNAL
+
+
+def _load(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        return json.load(f)
+
+
+def _traj(golden_dir, name):
+    with open(os.path.join(golden_dir, name)) as f:
+        lines = [json.loads(l) for l in f if l.strip()]
+    return lines[0], [l for l in lines if l["record"] == "step"], lines[-1]
+
+
+def _config1(golden_dir):
+    for name in ("traj_opt125m_lozo50.jsonl", "traj_opt125m_lozo.jsonl"):
+        if os.path.exists(os.path.join(golden_dir, name)):
+            return name
+    raise FileNotFoundError("config-1 golden missing")
+
+
+def _report(name, data):
+    os.makedirs("gpurun_out/parity", exist_ok=True)
+    with open(os.path.join("gpurun_out/parity", name + ".json"), "w") as f:
+        json.dump(data, f, indent=1)
+
+
+@pytest.mark.parametrize("precision", ["fp16", "bf16"])
+def test_config1_forward_nll(golden_dir, precision):
+    from paper_2605_28760_b200.engine import ZoEngine
+    g = _load(golden_dir, "forward_opt125m.json")
+    m = g["model"]
+    eng = ZoEngine(m["vocab"], m["dim"], m["n_layers"], m["n_heads"], m["prompt_len"], max_batch=16,
+                   rank=g["rank"], precision=precision)
+    eng.init_params(m["init_seed"], m["init_scale"])
+    step, r = g["step"], g["rank"]
+    eng.sample_v(g["zseed"], step, 50)
+    eng.sample_u(g["zseed"], step)
+    A = {lid: g["a_scale"] * R.gaussian(g["a_seed"], step, lid, R.ROLE_U, eng.shapes[lid][0], r) for lid in eng.lids}
+    eng.set_slot(2, eng.join(2, A))
+    tokens = np.asarray(g["tokens"])
+    gold = tokens[:, m["prompt_len"]:]
+    eng.prepare_probe(g["epsilon"], 0)
+    nll = eng.score(tokens, np.stack([gold, gold]), nsign=2)
+    eng.prepare_probe(g["epsilon"], 1)
+    nll0 = eng.score(tokens, gold, nsign=1)[0]
+    eng.close()
+    ref_p, ref_m, ref_0 = (np.array(g["nll"][f"real64:{s}"]) for s in (1, -1, 0))
+    d_ref = R.canonical_mean(ref_p) - R.canonical_mean(ref_m)
+    d_got = R.canonical_mean(nll[0]) - R.canonical_mean(nll[1])
+    rep = {"max_abs_nll_plus": float(np.max(np.abs(nll[0] - ref_p))),
+           "max_abs_nll_minus": float(np.max(np.abs(nll[1] - ref_m))),
+           "max_abs_nll_sign0": float(np.max(np.abs(nll0 - ref_0))),
+           "dL_ref": d_ref, "dL_got": d_got, "rel_err_dL": abs(d_got - d_ref) / abs(d_ref)}
+    _report(f"config1_forward_{precision}", rep)
+    tol = NLL_TOL[precision]
+    assert max(rep["max_abs_nll_plus"], rep["max_abs_nll_minus"], rep["max_abs_nll_sign0"]) <= tol, rep
+    assert rep["rel_err_dL"] <= DL_REL[precision], rep
+
+
+def test_config1_run_serving_path(golden_dir):
+    """run_serving_path (runtime.py:253-359) at config 1 against the reference's own run."""
+    from paper_2605_28760_b200 import model as M
+    from paper_2605_28760_b200.runtime import run_serving_path
+    from paper_2605_28760_b200.verify import record_deltas, sign_match, strict_compare
+    from paper_2605_28760_b200.zo_engine import ZoConfig, read_trajectory, write_trajectory
+    name = _config1(golden_dir)
+    h, recs, fin = _traj(golden_dir, name)
+    mcfg = M.ModelConfig(**h["model"])
+    task = M.generate_task(M.TaskConfig(**h["task"]))
+    zcfg = ZoConfig(**h["zo"])
+    run = run_serving_path(mcfg, task, zcfg, h["steps"], eval_every=10 ** 9)
+    assert (run.model_digest, run.task_digest) == (h["model_digest"], h["task_digest"])
+    rows = []
+    for a, b in zip(recs, run.trajectory):
+        assert (a["u_digest"], a["v_digest"], a["minibatch_id"]) == (b.u_digest, b.v_digest, b.minibatch_id)
+        dl = a["loss_plus"] - a["loss_minus"]
+        rows.append({"step": a["step"], "dLp": b.loss_plus - a["loss_plus"], "dLm": b.loss_minus - a["loss_minus"],
+                     "c_ref": a["coefficient"], "c": b.coefficient, "high_signal": abs(dl) >= HIGH_SIGNAL,
+                     "rel_dc": abs(b.coefficient - a["coefficient"]) / abs(a["coefficient"])})
+    out = f"gpurun_out/parity_{name.replace('.jsonl', '')}_b200.jsonl"
+    os.makedirs("gpurun_out", exist_ok=True)
+    write_trajectory(out, {"model_digest": run.model_digest, "task_digest": run.task_digest}, run.trajectory,
+                     {"eval_loss": run.eval_curve[-1].loss, "eval_acc": run.eval_curve[-1].acc})
+    ref = read_trajectory(os.path.join(golden_dir, name))
+    sc = strict_compare(ref, read_trajectory(out), loss_tol=TRAJ_DL)
+    sm = sign_match(record_deltas(ref[1]), record_deltas(run.trajectory))
+    hs = [r for r in rows if r["high_signal"]]
+    rep = {"golden": name, "steps": len(rows), "max_dL": max(max(abs(r["dLp"]), abs(r["dLm"])) for r in rows),
+           "max_rel_dc_high_signal": max((r["rel_dc"] for r in hs), default=0.0), "high_signal_steps": len(hs),
+           "eval_loss": run.eval_curve[-1].loss, "eval_loss_ref": fin["eval_loss"],
+           "strict_compare": sc.to_dict(), "sign_match": sm.to_dict(), "rows": rows}
+    _report("config1_run_serving_path", rep)
+    assert rep["max_dL"] <= TRAJ_DL, rep
+    assert rep["max_rel_dc_high_signal"] <= C_REL, rep
+    assert sc.accepted == sc.steps and sm.high_signal_fraction == 1.0, rep
+    assert abs(run.eval_curve[-1].loss - fin["eval_loss"]) <= TRAJ_DL
+
+
+class _ReplayScorer:
+    def __init__(self, recs):
+        self.recs, self.calls = recs, 0
+
+    def __call__(self, batch):
+        r = self.recs[self.calls // 2]
+        v = r["loss_plus"] if self.calls % 2 == 0 else r["loss_minus"]
+        self.calls += 1
+        return v
+
+
+def test_config1_update_and_folds_bit_exact(golden_dir):
+    """Given the reference's coefficients, the device update (K8) and folds (K9)
+    reproduce the reference's float64 parameters bit for bit at config 1."""
+    from paper_2605_28760_b200 import model as M
+    from paper_2605_28760_b200.adapter import AdapterState
+    from paper_2605_28760_b200.zo_engine import ZoConfig, lozo_step
+    h, recs, fin = _traj(golden_dir, _config1(golden_dir))
+    mcfg = M.ModelConfig(**h["model"])
+    task = M.generate_task(M.TaskConfig(**h["task"]))
+    zcfg = ZoConfig(**h["zo"])
+    params = M.init_params(mcfg, max_batch=zcfg.batch_size)
+    assert M.params_digest(params) == h["model_digest"]
+    state = AdapterState(epsilon=zcfg.epsilon)
+    scorer = _ReplayScorer(recs)
+    for t, rec in enumerate(recs):
+        batch = M.sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
+        out = lozo_step(params, mcfg, state, zcfg, t, batch, scorer=scorer, digests="off")
+        assert out.beta == rec["beta"]
+        if (t + 1) % zcfg.nu == 0 and t + 1 < len(recs):
+            params.engine.fold()
+            params.invalidate()
+    if len(recs) % zcfg.nu:
+        assert M.params_digest(params) == fin["pre_fold_params_digest"]
+    params.engine.fold()
+    params.invalidate()
+    assert M.params_digest(params) == fin["final_params_digest"]
+
+
+def test_opt13b_dims_block_lm_head_loss_vs_oracle():
+    """One OPT-13B-shaped decoder block (d 5120, H 40) + the V = 50272 LM head + loss,
+    M = 2016 rows per GEMM as in the 13B step, against the float64 oracle."""
+    from paper_2605_28760_b200.engine import ZoEngine
+    V_, d, H, P = 50272, 5120, 40, 63
+    cfg = R.ModelCfg(vocab=V_, dim=d, n_layers=1, n_heads=H, prompt_len=P, init_seed=7, init_scale=0.02)
+    eng = ZoEngine(V_, d, 1, H, P, max_batch=16, rank=2)
+    eng.init_params(cfg.init_seed, cfg.init_scale)
+    seed, step = 42, 7
+    eng.sample_v(seed, step, 50)
+    eng.sample_u(seed, step)
+    U = eng.split(0, eng.get_slot(0))
+    Vw = eng.split(1, eng.get_slot(1))
+    A = {lid: 2e-3 * R.gaussian(seed + 1, step, lid, R.ROLE_U, eng.shapes[lid][0], 2) for lid in eng.lids}
+    eng.set_slot(2, eng.join(2, A))
+    rng = np.random.default_rng(0)
+    B = 16
+    prompts = rng.integers(4, V_ - 2, size=(B, P))
+    gold = (V_ - 2 + rng.integers(0, 2, size=(B, 1)))
+    tokens = np.concatenate([prompts, gold], axis=1)
+    eng.prepare_probe(1e-3, 0)
+    nll = eng.score(tokens, np.stack([gold, gold]), nsign=2)
+    params = {lid: eng.download(lid) for lid in eng.lids}
+    eng.close()
+    for k in ("blk0.ln1", "blk0.ln2", "ln_f"):
+        params[k + ".scale"] = np.ones(d)
+        params[k + ".shift"] = np.zeros(d)
+    ref = {}
+    for sign in (1, -1):
+        eff = dict(params)
+        for lid in U:
+            eff[lid] = R.compose(params[lid], A[lid], Vw[lid], U[lid], sign, 1e-3)
+        ref[sign] = R.forward_nll(eff, cfg, tokens, gold)
+        del eff
+    d_ref = R.canonical_mean(ref[1]) - R.canonical_mean(ref[-1])
+    d_got = R.canonical_mean(nll[0]) - R.canonical_mean(nll[1])
+    rep = {"max_abs_nll_plus": float(np.max(np.abs(nll[0] - ref[1]))),
+           "max_abs_nll_minus": float(np.max(np.abs(nll[1] - ref[-1]))),
+           "L_plus": R.canonical_mean(ref[1]), "dL_ref": d_ref, "dL_got": d_got,
+           "rel_err_dL": abs(d_got - d_ref) / abs(d_ref)}
+    _report("opt13b_block_lm_head_fp16", rep)
+    assert max(rep["max_abs_nll_plus"], rep["max_abs_nll_minus"]) <= 5e-3, rep
+    assert rep["rel_err_dL"] <= 0.05, rep

@@ -17,7 +17,9 @@ pytestmark = pytest.mark.gpu
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
 from make_opt_golden import MICRO_OPT, MICRO_TASK, opt_params  # noqa: E402
 
-NLL_TOL = {"fp16": 2e-2, "bf16": 8e-2}
+import zo_tolerances as _T
+
+NLL_TOL = {"fp16": _T.NLL["fp16"], "bf16": 2.5e-2}  # bf16 observed 8.1e-3 on the OPT micro decoder
 
 
 def _load(golden_dir):
@@ -120,7 +122,7 @@ def test_opt_serving_path_vs_oracle():
                            params=M.DeviceParams(mcfg, host={k: v.copy() for k, v in host.items()}, max_batch=8))
     for a, b in zip(recs, run.trajectory):
         assert (a.u_digest, a.v_digest, a.minibatch_id) == (b.u_digest, b.v_digest, b.minibatch_id)
-        assert abs(a.loss_plus - b.loss_plus) < 1.5e-2 and abs(a.loss_minus - b.loss_minus) < 1.5e-2
+        assert abs(a.loss_plus - b.loss_plus) <= _T.LOSS["fp16"] and abs(a.loss_minus - b.loss_minus) <= _T.LOSS["fp16"]
 
 
 def test_opt_materialising_loop_bit_exact_given_coefficients():
@@ -140,7 +142,7 @@ def test_opt_materialising_loop_bit_exact_given_coefficients():
         for p in (0, 1):
             eng.baseline_pass(p, 1e-3, False)
             got = R.canonical_mean(eng.score(tokens, gold, nsign=1)[0])
-            assert abs(got - (rec.loss_plus if p == 0 else rec.loss_minus)) < 1.5e-2
+            assert abs(got - (rec.loss_plus if p == 0 else rec.loss_minus)) <= _T.LOSS["fp16"]
         eng.baseline_pass(2, 1e-3, False)
         eng.set_coefficient([rec.loss_plus, rec.loss_minus, rec.coefficient, rec.beta])
         eng.baseline_update(1e-3, False)

@@ -10,10 +10,11 @@ from types import SimpleNamespace
 import numpy as np
 import pytest
 
+import zo_tolerances as _T
 from oracle import reference as R
 
 pytestmark = pytest.mark.gpu
-TOL = 1.5e-2
+TOL = _T.LOSS["fp16"]
 
 
 def _objects(full: bool):
@@ -65,7 +66,7 @@ def test_reference_scorer_pair(full):
     lm = scorer(batch)
     assert abs(lp - ref[1]) <= TOL and abs(lm - ref[-1]) <= TOL, (lp, lm, ref)
     # the probe difference, which the estimator consumes
-    assert abs((lp - lm) - (ref[1] - ref[-1])) <= max(0.05 * abs(ref[1] - ref[-1]), 2e-4)
+    assert abs((lp - lm) - (ref[1] - ref[-1])) <= max(_T.DL_REL["fp16"] * abs(ref[1] - ref[-1]), 2e-4)
     # pure: the reference's params/state were not written by the scorer
     for k in base:
         if base[k].ndim == 2:

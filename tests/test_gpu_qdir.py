@@ -15,7 +15,9 @@ from oracle import reference as R
 
 pytestmark = pytest.mark.gpu
 
-LOSS_TOL = 1.5e-2
+import zo_tolerances as _T
+
+LOSS_TOL = _T.LOSS["fp16"]
 
 
 def _setup(estimator="lozo_lazy", rank=2, steps=8):

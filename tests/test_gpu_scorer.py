@@ -1,8 +1,7 @@
 """Scorer / step parity on the GPU against the reference's golden fixtures.
 
-Tolerances (fp16 tensor-core operands, fp32 accumulate):
-per-example NLL |d| <= 2e-2, paired mean losses |dL+-| <= 1e-2; U/V digests and
-the float64 init are bit-exact.
+Tolerances: tests/tolerances.py (fp16 / bf16 tensor-core operands, fp32 accumulate;
+~3x the observed error); U/V digests and the float64 init are bit-exact.
 """
 import json
 import os
@@ -14,9 +13,11 @@ from oracle import reference as R
 
 pytestmark = pytest.mark.gpu
 
-NLL_TOL = {"fp16": 2e-2, "bf16": 8e-2}
-LOSS_TOL = {"fp16": 1e-2, "bf16": 4e-2}
-DL_REL = {"fp16": 0.05, "bf16": 0.1}  # |d(L+ - L-)| relative, SURVEY.md §8(c)
+import zo_tolerances as TOL
+
+NLL_TOL = TOL.NLL
+LOSS_TOL = TOL.LOSS
+DL_REL = TOL.DL_REL  # |d(L+ - L-)| relative
 
 
 def _load(golden_dir, name):
@@ -129,7 +130,10 @@ def test_device_step_trajectory(golden_dir, name):
             eng.fold()
     _report(f"traj_{name}", {"rows": rows, "max_dL": max(max(abs(r["dLp"]), abs(r["dLm"])) for r in rows)})
     assert all(r["u_ok"] and r["v_ok"] for r in rows)
-    assert max(max(abs(r["dLp"]), abs(r["dLm"])) for r in rows) <= LOSS_TOL["fp16"] * 1.5, rows
+    assert max(max(abs(r["dLp"]), abs(r["dLm"])) for r in rows) <= LOSS_TOL["fp16"], rows
+    for r in rows:  # the coefficient the update consumes, on high-signal steps
+        if abs(r["c_ref"]) * 2e-3 >= TOL.HIGH_SIGNAL:
+            assert abs(r["c"] - r["c_ref"]) <= TOL.C_REL * abs(r["c_ref"]), r
     assert sum(r["sign_ok"] for r in rows) >= 0.9 * len(rows)
     assert eng.sampler_flags()[0] == 0
 
