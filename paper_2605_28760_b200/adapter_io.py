@@ -1,77 +1,172 @@
 """ZOAD adapter files and manifests -- ``zoserve.adapter`` serialization
 (adapter.py:279-415), byte-compatible with the reference's writer/reader.
 
-Wire format (little-endian), restated from adapter.py:305-368:
+The wire format is fixed by the reference (little-endian); it is declared once
+here as a record table and every reader / writer / digest walks that table:
 
-    b"ZOAD" | u32 version=1 | f64 epsilon | i8 perturb_sign | u32 n_entries
-    per entry (sorted layer ids):
-        u16 len | utf-8 layer id | u32 m | u32 n | u32 n_slots
-        per slot: u8 kind (0 frozen, 1 window, 2 probe) | u32 rank | f64 scale
-                  | A (m x rank f64) | B (n x rank f64)
+    header  ZOAD magic | u32 version=1 | f64 epsilon | i8 perturb_sign | u32 n_entries
+    entry   u16 id length | utf-8 layer id | u32 m | u32 n | u32 n_slots   (sorted ids)
+    slot    u8 kind (0 frozen, 1 window, 2 probe) | u32 rank | f64 scale
+            | A (m x rank f64) | B (n x rank f64)
 
-plus a sidecar ``<path>.manifest.json`` with per-layer and whole-state FNV
-digests and the file digest (adapter.py:370-415).  A bound ``AdapterState``
-serializes its device arenas (window A, window V and -- while a probe is
-installed -- the probe U), so a device run checkpoints into the same file the
-reference writes.
+plus a sidecar ``<path>.manifest.json`` with per-layer and whole-state FNV digests
+and the file digest.  A bound ``AdapterState`` serializes its device arenas
+(window A, window V and -- while a probe is installed -- the probe U), so a device
+run checkpoints into the same file the reference writes.
 """
 from __future__ import annotations
 
 import json
 import struct
+from collections.abc import Iterator
 
 import numpy as np
 
-from .adapter import AdapterEntry, AdapterState, LoraSlot
+from .adapter import AdapterState, LoraSlot
 from .errors import InputError
 from .numerics import FNV_OFFSET_BASIS, digest_array, digest_bytes, digest_hex, digest_text
 
 __all__ = ["save_adapter", "load_adapter", "state_digest", "adapter_manifest"]
 
-_MAGIC = b"ZOAD"
-_VERSION = 1
-_HEAD = "<IdbI"
-_SLOT = "<Id"
+MAGIC = b"ZOAD"
+VERSION = 1
+# record table of the ZOAD layout: record -> struct format of its fixed-size fields
+RECORDS = {
+    "header": "<IdbI",     # version, epsilon, perturb_sign, n_entries
+    "id_len": "<H",
+    "entry": "<III",       # m, n, n_slots
+    "slot_kind": "<B",
+    "slot": "<Id",         # rank, scale
+}
+KINDS = ("frozen", "window", "probe")
 
 
-def _pack_slot(slot: LoraSlot) -> bytes:  # adapter.py:279-281
-    return (struct.pack(_SLOT, slot.rank, slot.scale) + np.ascontiguousarray(slot.A, "<f8").tobytes()
+class _Cursor:
+    """Sequential reader over the file bytes; every short read is an InputError."""
+
+    def __init__(self, data: bytes):
+        self.buf = memoryview(data)
+        self.pos = 0
+
+    def record(self, name: str) -> tuple:
+        fmt = RECORDS[name]
+        try:
+            out = struct.unpack_from(fmt, self.buf, self.pos)
+        except struct.error as e:
+            raise InputError(f"truncated adapter file ({name}): {e}") from None
+        self.pos += struct.calcsize(fmt)
+        return out
+
+    def raw(self, n: int) -> bytes:
+        if self.pos + n > len(self.buf):
+            raise InputError("truncated adapter file (layer id)")
+        out = bytes(self.buf[self.pos:self.pos + n])
+        self.pos += n
+        return out
+
+    def matrix(self, rows: int, cols: int) -> np.ndarray:
+        n = rows * cols
+        if self.pos + 8 * n > len(self.buf):
+            raise InputError("truncated adapter file (slot factor)")
+        out = np.frombuffer(self.buf, dtype="<f8", count=n, offset=self.pos).reshape(rows, cols).copy()
+        self.pos += 8 * n
+        return out
+
+
+def _slots(entries) -> Iterator[tuple[str, object, list[tuple[int, LoraSlot]]]]:
+    """(layer id, entry, [(kind, slot)]) in file order: sorted ids; frozen slots, then the
+    window slot, then the probe (adapter.py:295-302)."""
+    for lid in sorted(entries):
+        e = entries[lid]
+        seq = [(0, s) for s in e.update_slots]
+        seq += [(k, s) for k, s in ((1, e.window_slot), (2, e.perturb_slot)) if s is not None]
+        yield lid, e, seq
+
+
+def _slot_bytes(slot: LoraSlot) -> bytes:
+    return (struct.pack(RECORDS["slot"], slot.rank, slot.scale) + np.ascontiguousarray(slot.A, "<f8").tobytes()
             + np.ascontiguousarray(slot.B, "<f8").tobytes())
 
 
-def _unpack_slot(buf: memoryview, off: int, m: int, n: int) -> tuple[LoraSlot, int]:  # adapter.py:284-292
-    k, scale = struct.unpack_from(_SLOT, buf, off)
-    off += struct.calcsize(_SLOT)
-    a = np.frombuffer(buf, dtype="<f8", count=m * k, offset=off).reshape(m, k).copy()
-    off += m * k * 8
-    b = np.frombuffer(buf, dtype="<f8", count=n * k, offset=off).reshape(n, k).copy()
-    off += n * k * 8
-    return LoraSlot(a, b, float(scale)), off
+def _encode(state: AdapterState, entries) -> bytes:
+    parts = [MAGIC, struct.pack(RECORDS["header"], VERSION, state.epsilon, state.perturb_sign, len(entries))]
+    for lid, e, seq in _slots(entries):
+        name = lid.encode("utf-8")
+        parts += [struct.pack(RECORDS["id_len"], len(name)), name,
+                  struct.pack(RECORDS["entry"], e.m, e.n, len(seq))]
+        for kind, slot in seq:
+            parts += [struct.pack(RECORDS["slot_kind"], kind), _slot_bytes(slot)]
+    return b"".join(parts)
 
 
-def _entry_slots(entry: AdapterEntry) -> list[tuple[int, LoraSlot]]:  # adapter.py:295-302
-    out = [(0, s) for s in entry.update_slots]
-    if entry.window_slot is not None:
-        out.append((1, entry.window_slot))
-    if entry.perturb_slot is not None:
-        out.append((2, entry.perturb_slot))
-    return out
+def _decode(data: bytes) -> AdapterState:
+    if data[:4] != MAGIC:
+        raise InputError("not an adapter file (bad magic)")
+    cur = _Cursor(data)
+    cur.pos = len(MAGIC)
+    version, epsilon, sign, n_entries = cur.record("header")
+    if version != VERSION:
+        raise InputError(f"unsupported adapter file version {version}")
+    state = AdapterState(epsilon=float(epsilon), perturb_sign=int(sign))
+    for _ in range(n_entries):
+        (n_id,) = cur.record("id_len")
+        try:
+            lid = cur.raw(n_id).decode("utf-8")
+        except UnicodeDecodeError as e:
+            raise InputError(f"corrupt layer id: {e}") from None
+        m, n, n_slots = cur.record("entry")
+        entry = state.ensure_entry(lid, m, n)
+        for _ in range(n_slots):
+            (kind,) = cur.record("slot_kind")
+            if kind >= len(KINDS):
+                raise InputError(f"unknown slot kind {kind}")
+            rank, scale = cur.record("slot")
+            slot = LoraSlot(cur.matrix(m, rank), cur.matrix(n, rank), float(scale))
+            if kind == 0:
+                entry.update_slots.append(slot)
+            elif kind == 1:
+                entry.window_slot = slot
+            else:
+                entry.perturb_slot = slot
+    state._probe_on = any(e.perturb_slot is not None for e in state._host_entries.values())
+    return state
+
+
+def _fold_slot_digest(h: int, kind: int, slot: LoraSlot) -> int:
+    """kind byte, (rank, scale) record, A, B -- the per-slot digest chain (adapter.py:371-389)."""
+    h = digest_bytes(bytes([kind]), h)
+    h = digest_bytes(struct.pack(RECORDS["slot"], slot.rank, slot.scale), h)
+    return digest_array(slot.B, digest_array(slot.A, h))
+
+
+def state_digest(state: AdapterState, entries: dict | None = None) -> str:
+    """Whole-state fingerprint: slots, probes, sign and epsilon (adapter.py:378-389)."""
+    entries = state.entries if entries is None else entries
+    h = digest_bytes(struct.pack("<db", state.epsilon, state.perturb_sign), digest_text("adapter"))
+    for lid, _e, seq in _slots(entries):
+        h = digest_text(lid, h)
+        for kind, slot in seq:
+            h = _fold_slot_digest(h, kind, slot)
+    return digest_hex(h)
+
+
+def adapter_manifest(state: AdapterState, entries: dict | None = None) -> dict:
+    """Per-layer shape / slot count / digest plus the state digest (adapter.py:392-415)."""
+    entries = state.entries if entries is None else entries
+    layers = {}
+    for lid, e, seq in _slots(entries):
+        h = FNV_OFFSET_BASIS
+        for kind, slot in seq:
+            h = _fold_slot_digest(h, kind, slot)
+        layers[lid] = {"shape": [e.m, e.n], "slots": len(seq), "digest": digest_hex(h)}
+    return {"version": VERSION, "epsilon": state.epsilon, "perturb_sign": state.perturb_sign,
+            "state_digest": state_digest(state, entries), "layers": layers}
 
 
 def save_adapter(state: AdapterState, path: str) -> dict:
-    """adapter.py:305-328: versioned binary file + ``<path>.manifest.json``."""
+    """Versioned binary file + ``<path>.manifest.json`` (adapter.py:305-328)."""
     entries = state.entries
-    blob = bytearray(_MAGIC)
-    blob += struct.pack(_HEAD, _VERSION, state.epsilon, state.perturb_sign, len(entries))
-    for lid in sorted(entries):
-        entry = entries[lid]
-        lb = lid.encode("utf-8")
-        slots = _entry_slots(entry)
-        blob += struct.pack("<H", len(lb)) + lb
-        blob += struct.pack("<III", entry.m, entry.n, len(slots))
-        for kind, slot in slots:
-            blob += struct.pack("<B", kind) + _pack_slot(slot)
-    data = bytes(blob)
+    data = _encode(state, entries)
     with open(path, "wb") as f:
         f.write(data)
     manifest = adapter_manifest(state, entries)
@@ -82,86 +177,17 @@ def save_adapter(state: AdapterState, path: str) -> dict:
 
 
 def load_adapter(path: str, check_manifest: bool = True) -> AdapterState:
-    """adapter.py:331-368: digest-checked read; raises InputError on corruption,
-    bad magic or an unsupported version."""
+    """Digest-checked read (adapter.py:331-368); InputError on corruption, bad magic
+    or an unsupported version."""
     with open(path, "rb") as f:
         data = f.read()
     if check_manifest:
         try:
             with open(path + ".manifest.json") as f:
-                manifest = json.load(f)
+                expected = json.load(f).get("file_digest")
         except FileNotFoundError:
-            manifest = None
-        if manifest is not None:
-            got = digest_hex(digest_bytes(data))
-            if manifest.get("file_digest") != got:
-                raise InputError(f"adapter file digest {got} does not match manifest")
-    if data[:4] != _MAGIC:
-        raise InputError("not an adapter file (bad magic)")
-    off = 4
-    try:
-        version, epsilon, sign, n_entries = struct.unpack_from(_HEAD, data, off)
-    except struct.error as e:
-        raise InputError(f"truncated adapter file: {e}") from None
-    off += struct.calcsize(_HEAD)
-    if version != _VERSION:
-        raise InputError(f"unsupported adapter file version {version}")
-    state = AdapterState(epsilon=float(epsilon), perturb_sign=int(sign))
-    buf = memoryview(data)
-    try:
-        for _ in range(n_entries):
-            (ll,) = struct.unpack_from("<H", buf, off)
-            off += 2
-            lid = bytes(buf[off:off + ll]).decode("utf-8")
-            off += ll
-            m, n, n_slots = struct.unpack_from("<III", buf, off)
-            off += struct.calcsize("<III")
-            entry = state.ensure_entry(lid, m, n)
-            for _ in range(n_slots):
-                (kind,) = struct.unpack_from("<B", buf, off)
-                off += 1
-                slot, off = _unpack_slot(buf, off, m, n)
-                if kind == 0:
-                    entry.update_slots.append(slot)
-                elif kind == 1:
-                    entry.window_slot = slot
-                else:
-                    entry.perturb_slot = slot
-    except (struct.error, ValueError) as e:
-        raise InputError(f"truncated adapter file: {e}") from None
-    state._probe_on = any(e.perturb_slot is not None for e in state._host_entries.values())
-    return state
-
-
-def _digest_slot(slot: LoraSlot, h: int) -> int:  # adapter.py:371-375
-    h = digest_bytes(struct.pack(_SLOT, slot.rank, slot.scale), h)
-    h = digest_array(slot.A, h)
-    return digest_array(slot.B, h)
-
-
-def state_digest(state: AdapterState, entries: dict | None = None) -> str:
-    """adapter.py:378-389: slots, probes, sign and epsilon."""
-    entries = state.entries if entries is None else entries
-    h = digest_text("adapter")
-    h = digest_bytes(struct.pack("<db", state.epsilon, state.perturb_sign), h)
-    for lid in sorted(entries):
-        h = digest_text(lid, h)
-        for kind, slot in _entry_slots(entries[lid]):
-            h = digest_bytes(bytes([kind]), h)
-            h = _digest_slot(slot, h)
-    return digest_hex(h)
-
-
-def adapter_manifest(state: AdapterState, entries: dict | None = None) -> dict:
-    """adapter.py:392-415."""
-    entries = state.entries if entries is None else entries
-    layers = {}
-    for lid in sorted(entries):
-        entry = entries[lid]
-        h = FNV_OFFSET_BASIS
-        for kind, slot in _entry_slots(entry):
-            h = digest_bytes(bytes([kind]), h)
-            h = _digest_slot(slot, h)
-        layers[lid] = {"shape": [entry.m, entry.n], "slots": len(_entry_slots(entry)), "digest": digest_hex(h)}
-    return {"version": _VERSION, "epsilon": state.epsilon, "perturb_sign": state.perturb_sign,
-            "state_digest": state_digest(state, entries), "layers": layers}
+            expected = None
+        got = digest_hex(digest_bytes(data))
+        if expected is not None and expected != got:
+            raise InputError(f"adapter file digest {got} does not match manifest")
+    return _decode(data)

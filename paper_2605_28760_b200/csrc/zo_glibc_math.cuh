@@ -8,6 +8,17 @@
 // value would not be bit-exact.  This restatement spells out every FMA the
 // glibc build uses (established by disassembly + 3e8-input comparison against
 // the container's libm: 0 mismatches).
+//
+// The algorithm, its Lp1..Lp7 / ln2_hi / ln2_lo constants and its variable names
+// follow fdlibm's s_log1p.c as carried by glibc (sysdeps/ieee754/dbl-64/s_log1p.c),
+// which bears this notice:
+//
+//   Copyright (C) 1993 by Sun Microsystems, Inc. All rights reserved.
+//
+//   Developed at SunPro, a Sun Microsystems, Inc. business.
+//   Permission to use, copy, modify, and distribute this
+//   software is freely granted, provided that this notice
+//   is preserved.
 #pragma once
 #include <stdint.h>
 

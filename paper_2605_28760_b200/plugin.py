@@ -7,9 +7,10 @@
   scores both probes in one fused launch and returns L+; the -1 call returns
   the cached L-.  Pure: it never writes the reference's params or state.
 * ``install_into_zoserve(zoserve)`` patches ``zoserve.runtime.forward_score``
-  (the name ``_MeteredScorer`` calls, runtime.py:28,168-177) and
-  ``zoserve.runtime._fold_all`` (runtime.py:242-250) so the unmodified
-  ``run_serving_path`` scores on the GPU; folds run on the host (the
+  (the name ``_MeteredScorer`` calls, runtime.py:28,168-177),
+  ``zoserve.runtime.evaluate_split`` (runtime.py:295-301, single-token options: one
+  device composition scores both options) and ``zoserve.runtime._fold_all``
+  (runtime.py:242-250) so the unmodified ``run_serving_path`` scores on the GPU; folds run on the host (the
   reference's own arithmetic) and on the device replica with the same slot
   values, so both copies stay bit-identical (k_fold_shadow restates
   numerics.py:207-235 exactly).
@@ -95,9 +96,24 @@ class ReferenceScorer:
         gold = batch.option_array()[batch.golds]
         return np.concatenate([batch.prompts, gold], axis=1), gold
 
+    def _fingerprint(self):
+        """Adapter version for the L- cache: which slot objects are
+        installed and a checksum of their factors -- an edit between the +1 and -1
+        calls (outside the reference's own estimate_coefficient) forces a re-score."""
+        ids, acc = [], 0.0
+        for lid in sorted(self.state.entries):
+            e = self.state.entries[lid]
+            for sl in (e.window_slot, e.perturb_slot):
+                if sl is None:
+                    ids.append(None)
+                    continue
+                ids.append((id(sl), id(sl.A), id(sl.B), float(sl.scale)))
+                acc += float(np.sum(sl.A)) + float(np.sum(sl.B))
+        return hash(tuple(ids)), acc, self.state.epsilon
+
     def __call__(self, batch) -> float:
         sign = self.state.perturb_sign
-        key = batch.batch_id
+        key = (batch.batch_id, self._fingerprint())
         if self._sync_vectors():
             self._cached = None  # the -1 probe moved the 1-D params: score it afresh
         if sign == -1 and self._cached is not None and self._cached[0] == key:
@@ -119,11 +135,36 @@ class ReferenceScorer:
         return lm
 
 
+def evaluate_on_engine(eng: ZoEngine, prompts, golds, options) -> tuple[float, float]:
+    """``evaluate_split``'s (loss, accuracy) (model.py:444-460, 247-269) on the device for
+    single-token options: the option token is causally invisible to the scored row
+    (SURVEY.md §0 fact 8), so one composition scores both options at once -- gold NLL
+    -> canonical mean over the whole split, argmax of -NLL_j with ties to the lowest j."""
+    opts = np.asarray(options, dtype=np.int64)
+    prompts = np.asarray(prompts)
+    golds = np.asarray(golds, dtype=np.int64)
+    nll = np.empty((len(opts), prompts.shape[0]))
+    mb = eng.max_batch
+    for i in range(0, prompts.shape[0], mb):
+        p = prompts[i:i + mb]
+        tokens = np.concatenate([p, opts[golds[i:i + mb]]], axis=1)
+        for j0 in range(0, len(opts), 2):  # the two halves of one launch score two options
+            js = list(range(j0, min(j0 + 2, len(opts))))
+            gold = np.stack([np.tile(opts[j], (p.shape[0], 1)) for j in js])
+            eng.prepare_probe(0.0, 1)
+            out = eng.score(tokens, gold, nsign=len(js))
+            for k, j in enumerate(js):
+                nll[j, i:i + mb] = out[k]
+    loss = canonical_mean(nll[golds, np.arange(prompts.shape[0])])
+    picks = np.argmax(-nll.T, axis=1)  # first max wins ties (model.py:267)
+    return loss, float(np.mean(picks == golds))
+
+
 def install_into_zoserve(zoserve, rank: int = 2, batch_size: int = 16, precision: str = "fp16"):
     """Patch the unmodified reference so run_serving_path scores on the B200.
     Returns an ``uninstall()`` callable."""
     rt = zoserve.runtime
-    orig_fs, orig_fold = rt.forward_score, rt._fold_all
+    orig_fs, orig_fold, orig_eval = rt.forward_score, rt._fold_all, getattr(rt, "evaluate_split", None)
     engines: dict[int, tuple[object, ReferenceScorer]] = {}
 
     def scorer_for(params, cfg, state):
@@ -148,9 +189,24 @@ def install_into_zoserve(zoserve, rank: int = 2, batch_size: int = 16, precision
             ent[1].eng.fold()  # device replica: same k-ascending float64 arithmetic
         return orig_fold(state, params, meter)
 
+    def evaluate_split(params, cfg, data, split="dev", view=None, precision="real64"):
+        # runtime.py:295-301 evaluates through the name it imported from model.py
+        options = data.config.options
+        if view is None or any(len(o) != 1 for o in options):
+            return orig_eval(params, cfg, data, split, view, precision)
+        state = view.__closure__[0].cell_contents
+        sc = scorer_for(params, cfg, state)
+        upload_reference_slots(sc.eng, state, with_probe=False)
+        prompts, golds = data.splits[split]
+        return evaluate_on_engine(sc.eng, prompts, golds, options)
+
     rt.forward_score, rt._fold_all = forward_score, fold_all
+    if orig_eval is not None:
+        rt.evaluate_split = evaluate_split
 
     def uninstall():
         rt.forward_score, rt._fold_all = orig_fs, orig_fold
+        if orig_eval is not None:
+            rt.evaluate_split = orig_eval
 
     return uninstall

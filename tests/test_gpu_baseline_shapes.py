@@ -205,5 +205,6 @@ def test_opt13b_dims_block_lm_head_loss_vs_oracle():
            "L_plus": R.canonical_mean(ref[1]), "dL_ref": d_ref, "dL_got": d_got,
            "rel_err_dL": abs(d_got - d_ref) / abs(d_ref)}
     _report("opt13b_block_lm_head_fp16", rep)
-    assert max(rep["max_abs_nll_plus"], rep["max_abs_nll_minus"]) <= 5e-3, rep
-    assert rep["rel_err_dL"] <= 0.05, rep
+    # observed on the B200: 1.2e-3 / 1.6e-5 (profiles/r02b_parity)
+    assert max(rep["max_abs_nll_plus"], rep["max_abs_nll_minus"]) <= 4e-3, rep
+    assert rep["rel_err_dL"] <= 5e-3, rep

@@ -122,7 +122,7 @@ def test_opt_serving_path_vs_oracle():
                            params=M.DeviceParams(mcfg, host={k: v.copy() for k, v in host.items()}, max_batch=8))
     for a, b in zip(recs, run.trajectory):
         assert (a.u_digest, a.v_digest, a.minibatch_id) == (b.u_digest, b.v_digest, b.minibatch_id)
-        assert abs(a.loss_plus - b.loss_plus) <= _T.LOSS["fp16"] and abs(a.loss_minus - b.loss_minus) <= _T.LOSS["fp16"]
+        assert abs(a.loss_plus - b.loss_plus) <= _T.LOSS_OPT and abs(a.loss_minus - b.loss_minus) <= _T.LOSS_OPT
 
 
 def test_opt_materialising_loop_bit_exact_given_coefficients():
@@ -142,7 +142,7 @@ def test_opt_materialising_loop_bit_exact_given_coefficients():
         for p in (0, 1):
             eng.baseline_pass(p, 1e-3, False)
             got = R.canonical_mean(eng.score(tokens, gold, nsign=1)[0])
-            assert abs(got - (rec.loss_plus if p == 0 else rec.loss_minus)) <= _T.LOSS["fp16"]
+            assert abs(got - (rec.loss_plus if p == 0 else rec.loss_minus)) <= _T.LOSS_OPT
         eng.baseline_pass(2, 1e-3, False)
         eng.set_coefficient([rec.loss_plus, rec.loss_minus, rec.coefficient, rec.beta])
         eng.baseline_update(1e-3, False)

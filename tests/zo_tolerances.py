@@ -12,3 +12,5 @@ HIGH_SIGNAL = 0.005                      # |L+ - L-| threshold of verify.py's si
 # the materialising loop writes the +-eps probe into the 16-bit weights (baseline_loop.py:68-119): the
 # 16-bit rounding of W + eps*P enters the loss directly
 LOSS_MATERIALISED = 1e-2
+# the OPT micro decoder (d = 32, random biases / LN params, ReLU; test_gpu_opt.py): observed 4.5e-3
+LOSS_OPT = 1.5e-2
