@@ -39,6 +39,10 @@ extern "C" {
 /* operand precision of the tensor-core scorer */
 #define ZO_PREC_FP16 0
 #define ZO_PREC_BF16 1
+/* the reference's "real32" (model.py:149-154): the float32 forward, computed on the
+ * tensor cores as 3xTF32 split GEMMs (kind::tf32, fp32 accumulate) with fp32 LN,
+ * attention, GELU and loss -- the parity mode; 12 extra bytes per weight */
+#define ZO_PREC_FP32 2
 
 #define ZO_EST_LOZO 0       /* "lozo_lazy"          zo_engine.py:368 */
 #define ZO_EST_FACTORIZED 1 /* "factorized_sqrt_r"  zo_engine.py:420 */
@@ -230,6 +234,10 @@ int zo_nll_io(zo_ctx* ctx, void* dev, int32_t count, int32_t to_ctx);
  * buffers, 16-bit inputs with row stride lda, fp32 output [M, N]. */
 int zo_test_gemm(int32_t M, int32_t N, int32_t K, int32_t lda, int32_t epi, int32_t bf16, const uint16_t* A_host,
                  const uint16_t* B_host, float* C_host);
+
+/* test hook of the real32 path: C[M, N] = A[M, K] . W[K, N] (A fp32, W float64 (in, out))
+ * through the 3xTF32 operand split and the tf32 tcgen05 GEMM; host buffers. */
+int zo_test_gemm_tf32x3(int32_t M, int32_t N, int32_t K, const float* A_host, const double* W_host, float* C_host);
 
 #ifdef __cplusplus
 }

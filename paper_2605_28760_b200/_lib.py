@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_build", "libzob200.so")
 
 ZO_OK, ZO_ERR_CONFIG, ZO_ERR_DIMENSION, ZO_ERR_INPUT, ZO_ERR_ABORT, ZO_ERR_CUDA, ZO_ERR_INTERNAL = range(7)
-PREC_FP16, PREC_BF16 = 0, 1
+PREC_FP16, PREC_BF16, PREC_FP32 = 0, 1, 2
 EST_LOZO, EST_FACTORIZED, EST_DENSE = 0, 1, 2
 SCOPE_LORA_ONLY, SCOPE_FULL = 0, 1
 ARCH_ZOSERVE, ARCH_OPT = 0, 1
@@ -95,6 +95,7 @@ SIGNATURES = [
     ("zo_profile_step", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _c.c_double, _P, _P,
                                    _c.c_int32, _c.POINTER(_c.c_float)]),
     ("zo_test_gemm", _c.c_int, [_c.c_int32] * 6 + [_P, _P, _P]),
+    ("zo_test_gemm_tf32x3", _c.c_int, [_c.c_int32] * 3 + [_P, _P, _P]),
     ("zo_digest_chain", _c.c_uint64, [_c.POINTER(_c.c_char_p), _P, _c.POINTER(_c.c_int64),
                                       _c.POINTER(_c.c_int64), _c.c_int32, _c.c_uint64]),
 ]

@@ -20,6 +20,7 @@ from dataclasses import dataclass, field
 
 from .engine import U as SLOT_U, V as SLOT_V
 from .errors import ConfigError
+from .engine import resolve_precision
 from .model import (EvalPoint, ModelConfig, TaskData, as_device_params, evaluate_split, init_params,
                     params_digest, sample_minibatch)
 from .numerics import canonical_mean, digest_hex
@@ -59,7 +60,7 @@ def run_baseline(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: int, 
     host-side fingerprints off for long timing runs."""
     if steps < 1:
         raise ConfigError("steps must be >= 1")
-    params = init_params(mcfg, precision=precision if precision in ("fp16", "bf16") else "fp16",
+    params = init_params(mcfg, precision=resolve_precision(precision),
                          max_batch=max(16, zcfg.batch_size)) if params is None else params
     dp = as_device_params(params, mcfg)
     opt_len = len(task.config.options[0])

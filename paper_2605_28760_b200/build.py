@@ -28,7 +28,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "--expt-r
 PER_FILE = {
     "sampler.cu": ["-fmad=false"],
 }
-SOURCES = ["sampler.cu", "gemm_sm100.cu", "attention.cu", "zo_kernels.cu", "zob200.cu"]
+SOURCES = ["sampler.cu", "gemm_sm100.cu", "attention.cu", "zo_kernels.cu", "precise.cu", "zob200.cu"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

@@ -95,16 +95,27 @@ __device__ __forceinline__ void tc_commit_cg2(uint32_t bar) {
       "h"((uint16_t)3)
       : "memory");
 }
+template <bool TF32>
 __device__ __forceinline__ void tc_mma_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                            uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
+  if constexpr (TF32)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  else
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t cta) {
   uint32_t remote;
@@ -117,16 +128,27 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
 }
+template <bool TF32>
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                        uint32_t accum) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "setp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
-      "}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
+  if constexpr (TF32)
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  else
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
 }
 // K-major, 128-byte swizzle, 8-row core groups 1024 B apart (sm_100 descriptor, version 1).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -278,11 +300,18 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int BN, int EPI, bool BF16, int XR, int CG>
+// DT: operand type -- 0 fp16, 1 bf16 (kind::f16, 64 elements per 128-byte K block, K = 16
+// per MMA), 2 tf32 (kind::tf32 on fp32 storage, 32 elements per K block, K = 8 per MMA; the
+// same 32 bytes per MMA step, so the smem ring and descriptors are shared)
+template <int BN, int EPI, int DT, int XR, int CG>
 __global__ void __launch_bounds__(192, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmB2, GemmParams p) {
   using C = GemmCfg<BN, CG>;
+  constexpr bool BF16 = DT == 1, TF32 = DT == 2;
+  constexpr int KE = TF32 ? 32 : 64;  // K elements per 128-byte block
+  constexpr uint32_t FMT = TF32 ? 2u : BF16 ? 1u : 0u;  // instruction-descriptor a/b format
+  static_assert(!TF32 || EPI == EPI_STORE32 || EPI == EPI_RESID32, "tf32 operands: fp32 epilogues only");
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;  // CTA within the pair
   const bool leader = rank == 0;
   extern __shared__ uint8_t smem_raw[];
@@ -356,12 +385,12 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t fb = full0 + 8 * stage;
           if constexpr (CG == 2) {
             if (leader) mbar_arrive_expect_tx(fb, 2 * stage_bytes);
-            tma_load_2d_cg2(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * C::BK, m0);
-            tma_load_2d_cg2(smem_u32(sB + stage * C::B_BYTES), tb, fb, kb * C::BK, n0);
+            tma_load_2d_cg2(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * KE, m0);
+            tma_load_2d_cg2(smem_u32(sB + stage * C::B_BYTES), tb, fb, kb * KE, n0);
           } else {
             mbar_arrive_expect_tx(fb, stage_bytes);
-            tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * C::BK, m0);
-            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), tb, fb, kb * C::BK, n0);
+            tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * KE, m0);
+            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), tb, fb, kb * KE, n0);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -372,10 +401,10 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {
-      constexpr uint32_t idesc = (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) |
-                                 ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((C::BM * CG) >> 4) << 24);
-      constexpr uint32_t idesc_h = (1u << 4) | ((BF16 ? 1u : 0u) << 7) | ((BF16 ? 1u : 0u) << 10) |
-                                   ((uint32_t)((BN / 2) >> 3) << 17) | ((uint32_t)((C::BM * CG) >> 4) << 24);
+      constexpr uint32_t idesc = (1u << 4) | (FMT << 7) | (FMT << 10) | ((uint32_t)(BN >> 3) << 17) |
+                                 ((uint32_t)((C::BM * CG) >> 4) << 24);
+      constexpr uint32_t idesc_h = (1u << 4) | (FMT << 7) | (FMT << 10) | ((uint32_t)((BN / 2) >> 3) << 17) |
+                                   ((uint32_t)((C::BM * CG) >> 4) << 24);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -398,9 +427,9 @@ __global__ void __launch_bounds__(192, 1)
           const int ks = (kb == p.num_kb - 1) ? p.last_ksteps : 4;
           for (int k = 0; k < ks; ++k) {
             if constexpr (CG == 2)
-              tc_mma_cg2(tmem_d, ad + 2 * k, bd + 2 * k, id, (kb > k0 || k > 0) ? 1u : 0u);
+              tc_mma_cg2<TF32>(tmem_d, ad + 2 * k, bd + 2 * k, id, (kb > k0 || k > 0) ? 1u : 0u);
             else
-              tc_mma(tmem_d, ad + 2 * k, bd + 2 * k, id, (kb > k0 || k > 0) ? 1u : 0u);
+              tc_mma<TF32>(tmem_d, ad + 2 * k, bd + 2 * k, id, (kb > k0 || k > 0) ? 1u : 0u);
           }
           if constexpr (CG == 2)
             tc_commit_cg2(empty0 + 8 * stage);
@@ -711,12 +740,14 @@ static PFN_encodeTiled get_encode() {
 }
 
 void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
-                  uint32_t box_rows, bool bf16) {
+                  uint32_t box_rows, int dtype) {
+  const bool f32 = dtype == 2;  // tf32 operands on fp32 storage: 32 elements per 128-byte box row
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {ld * 2};
-  cuuint32_t box[2] = {64, box_rows};
+  cuuint64_t strides[1] = {ld * (f32 ? 4 : 2)};
+  cuuint32_t box[2] = {f32 ? 32u : 64u, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = get_encode()(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+  CUresult r = get_encode()(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                     : dtype == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
                             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -727,17 +758,20 @@ void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t co
 }
 
 void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used, int epi,
-               bool bf16, void* out, int ldo, int num_sms) {
+               int dtype, void* out, int ldo, int num_sms) {
   if (lda % 8 || ldb % 8) throw Error(ZO_ERR_DIMENSION, "GEMM leading dimensions must be multiples of 8");
+  if (dtype == 2 && epi != EPI_STORE32 && epi != EPI_RESID32)
+    throw Error(ZO_ERR_INTERNAL, "tf32 GEMM supports the fp32 epilogues only");
   g.M = M;
   g.N = N;
   g.epi = epi;
-  g.bf16 = bf16 ? 1 : 0;
+  g.bf16 = dtype;
   g.out = out;
   g.ldo = ldo;
-  g.num_kb = (Kp_used + 63) / 64;
-  const int rem = Kp_used - 64 * (g.num_kb - 1);
-  g.last_ksteps = (rem + 15) / 16;
+  const int ke = dtype == 2 ? 32 : 64;  // K elements per 128-byte block
+  g.num_kb = (Kp_used + ke - 1) / ke;
+  const int rem = Kp_used - ke * (g.num_kb - 1);
+  g.last_ksteps = (rem + ke / 4 - 1) / (ke / 4);
   const int m_tiles = (M + 127) / 128;
   // tile N: prefer 256 unless that leaves the GPU badly under-filled
   int bn = 256;
@@ -760,9 +794,9 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
   const int slots = num_sms / g.cg;
   g.grid = (tiles < slots ? tiles : slots) * g.cg;
   const int mrows = ((M + 127) / 128) * 128;
-  make_tmap_2d(&g.tmA, A, (uint64_t)mrows, (uint64_t)lda, (uint64_t)lda, 128, bf16);
-  make_tmap_2d(&g.tmB, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg), bf16);
-  make_tmap_2d(&g.tmB2, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg / 2), bf16);
+  make_tmap_2d(&g.tmA, A, (uint64_t)mrows, (uint64_t)lda, (uint64_t)lda, 128, dtype);
+  make_tmap_2d(&g.tmB, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg), dtype);
+  make_tmap_2d(&g.tmB2, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg / 2), dtype);
   g.half_dp = g.half_n = 0;
 }
 
@@ -788,7 +822,7 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms) {
   g.grid = units * 2;
 }
 
-template <int BN, int EPI, bool BF16, int XR, int CG>
+template <int BN, int EPI, int BF16, int XR, int CG>
 static void launch_t(const GemmDesc& g, cudaStream_t st) {
   using C = GemmCfg<BN, CG>;
   static bool attr_set = false;
@@ -845,6 +879,12 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   }
 }
 
+template <int BN, int CG>
+static void launch_e32(const GemmDesc& g, cudaStream_t st) {  // tf32 operands (3xTF32 real32 path)
+  if (g.epi == EPI_RESID32) launch_t<BN, EPI_RESID32, 2, 0, CG>(g, st);
+  else launch_t<BN, EPI_STORE32, 2, 0, CG>(g, st);
+}
+
 template <int BN, bool BF16, int CG>
 static void launch_e(const GemmDesc& g, cudaStream_t st) {
   switch (g.epi) {
@@ -867,7 +907,7 @@ static int max_pair_units(int num_sms) {
   static int units = -1;
   if (units < 0) {
     using C = GemmCfg<256, 2>;
-    auto* fn = k_gemm<256, EPI_STORE16, false, 0, 2>;
+    auto* fn = k_gemm<256, EPI_STORE16, 0, 0, 2>;
     ZO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (num_sms / 2));
@@ -924,6 +964,13 @@ void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
 }
 
 void gemm_launch(const GemmDesc& g, cudaStream_t st) {
+  if (g.bf16 == 2) {
+    if (g.cg == 2) launch_e32<256, 2>(g, st);
+    else if (g.bn == 256) launch_e32<256, 1>(g, st);
+    else if (g.bn == 128) launch_e32<128, 1>(g, st);
+    else launch_e32<64, 1>(g, st);
+    return;
+  }
   if (g.cg == 2) {
     if (g.bf16) launch_e<256, true, 2>(g, st);
     else launch_e<256, false, 2>(g, st);

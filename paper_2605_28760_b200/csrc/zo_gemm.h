@@ -26,7 +26,7 @@ struct GemmDesc {
   int bn = 256;         // tile N (64/128/256)
   int cg = 1;           // 2: CTA-pair tiles (tcgen05 cta_group::2, M = 256, B split across the pair)
   int epi = EPI_STORE16;
-  int bf16 = 0;         // operand type: 0 fp16, 1 bf16
+  int bf16 = 0;         // operand type: 0 fp16, 1 bf16, 2 tf32 (fp32 storage; fp32 epilogues only)
   void* out = nullptr;
   int ldo = 0;          // output leading dimension (elements)
   int grid = 0;         // persistent CTAs
@@ -59,12 +59,13 @@ void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms);
 // twice as many half-width tiles: the tail's MMA time and its exposed epilogue halve
 void gemm_enable_halftail(GemmDesc& g, int num_sms);
 
-// 2-D K-major tensor map over a row-major [rows, cols] 16-bit matrix (row stride ld elements).
+// 2-D K-major tensor map over a row-major [rows, cols] matrix (row stride ld elements) of
+// operand type dtype (0 fp16, 1 bf16, 2 fp32 read as tf32).
 void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
-                  uint32_t box_rows, bool bf16);
-// Fill a GemmDesc. A is [Mpad, lda] (lda >= Kp), B is [N, ldb].
+                  uint32_t box_rows, int dtype);
+// Fill a GemmDesc. A is [Mpad, lda] (lda >= Kp), B is [N, ldb]; dtype as make_tmap_2d.
 void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used,
-               int epi, bool bf16, void* out, int ldo, int num_sms);
+               int epi, int dtype, void* out, int ldo, int num_sms);
 void gemm_launch(const GemmDesc& g, cudaStream_t st);
 
 }  // namespace zo

@@ -23,6 +23,7 @@
 #include "../../include/zob200.h"
 #include "zo_common.cuh"
 #include "zo_gemm.h"
+#include "zo_precise.h"
 #include "zo_kernels.h"
 #include "zo_sampler.h"
 
@@ -44,6 +45,9 @@ struct Matrix {
   double* W64 = nullptr;
   void* W16 = nullptr;
   int ldw = 0;
+  // real32: 3xTF32 split operand [n, ldk] (projection) / [vocab, ldk] (embed), precise.cu
+  float* W32S = nullptr;
+  int ldk = 0;
 };
 
 struct LayerPlan {
@@ -51,6 +55,11 @@ struct LayerPlan {
   // high-rank (r > 8) tensor-core extension t = a . P_s per GEMM input and probe sign:
   // [qkv-in, out-in, up-in, down-in] x [sign]
   std::vector<GemmDesc> ext;
+};
+// real32 (3xTF32) scorer plan: the four projections of every layer + the LM head
+struct RowPlan32 {
+  std::vector<GemmDesc> qkv, out, up, down;
+  GemmDesc lm;
 };
 struct RowPlan {
   std::vector<LayerPlan> layers;
@@ -91,6 +100,11 @@ struct zo_ctx {
   zo_model_desc d{};
   int T = 0, Tf = 0, dh = 0, r = 0, ext_terms = 3, KE = 64, ext_used = 0, num_sms = 148;
   bool bf16 = false;
+  // ZO_PREC_FP32 ("real32"): the fp32 forward on tcgen05 kind::tf32 via the 3xTF32 split
+  bool real32 = false;
+  float *a32 = nullptr, *f32a = nullptr, *ctx32 = nullptr;  // split A operand, qkv/ff_up out, ctx
+  int lda32 = 0;                                             // row stride of a32
+  std::map<int, RowPlan32> plans32;
   cudaStream_t st = nullptr;
   DevAlloc mem;
   std::vector<Matrix> mats;  // sorted by lid
@@ -371,9 +385,98 @@ void prof_mark(zo_ctx* c, int kind) {
   c->prof_kind[c->prof_n++] = kind;
 }
 
+RowPlan32& row_plan32(zo_ctx* c, int M, int nsign) {
+  const int key = 2 * M + (nsign == 1 ? 1 : 0);
+  auto it = c->plans32.find(key);
+  if (it != c->plans32.end()) return it->second;
+  RowPlan32 rp;
+  const int d = c->d.dim, r = c->r, S = M / c->Tf * c->d.opt_len;
+  const int ld_d = (int)ceil_div(3 * d + 3 * r, 32) * 32, ld_4d = (int)ceil_div(12 * d + 3 * r, 32) * 32;
+  for (int l = 0; l < c->d.n_layers; ++l) {
+    const Matrix& q = c->mats[c->i_qkv[l]];
+    const Matrix& o = c->mats[c->i_out[l]];
+    const Matrix& u = c->mats[c->i_up[l]];
+    const Matrix& w = c->mats[c->i_down[l]];
+    GemmDesc gq, go, gu, gd;
+    gemm_plan(gq, c->a32, M, ld_d, q.W32S, 3 * d, q.ldk, 3 * d + 3 * r, EPI_STORE32, 2, c->f32a, 3 * d, c->num_sms);
+    gemm_plan(go, c->a32, M, ld_d, o.W32S, d, o.ldk, 3 * d + 3 * r, EPI_RESID32, 2, c->x32, d, c->num_sms);
+    gemm_plan(gu, c->a32, M, ld_d, u.W32S, 4 * d, u.ldk, 3 * d + 3 * r, EPI_STORE32, 2, c->f32a, 4 * d,
+              c->num_sms);
+    gemm_plan(gd, c->a32, M, ld_4d, w.W32S, d, w.ldk, 12 * d + 3 * r, EPI_RESID32, 2, c->x32, d, c->num_sms);
+    set_bias(c, gq, c->bqkv[l], M / nsign);
+    set_bias(c, go, c->bout[l], M / nsign);
+    set_bias(c, gu, c->bup[l], M / nsign);
+    set_bias(c, gd, c->bdown[l], M / nsign);
+    rp.qkv.push_back(gq);
+    rp.out.push_back(go);
+    rp.up.push_back(gu);
+    rp.down.push_back(gd);
+  }
+  const Matrix& e = c->mats[c->i_embed];
+  gemm_plan(rp.lm, c->a32, S, e.ldk, e.W32S, c->d.vocab, e.ldk, 3 * d, EPI_STORE32, 2, c->logits, c->ldl,
+            c->num_sms);
+  return c->plans32.emplace(key, std::move(rp)).first->second;
+}
+
+// the reference's "real32" forward (model.py:149-199, float32 arithmetic) on the tensor cores:
+// 3xTF32 split GEMMs with the LoRA term as extension K columns, fp32 LN / attention / GELU
+// (precise.cu); the embedding, final LN and loss kernels are the 16-bit path's fp32 ones.
+void do_score32(zo_ctx* c, int B, int nsign) {
+  const int d = c->d.dim, T = c->Tf, M = nsign * B * T, r = c->r, rps = B * T;
+  // split operands from the float64 masters and the current window V (every call: folds,
+  // dense updates and uploads all land in W64 / V)
+  for (const auto& m : c->mats)
+    if (m.W32S)
+      launch_split_weight(m.W64, (int)m.m, (int)m.n, c->V + m.v_off, r, m.W32S, m.ldk, m.kind == K_EMBED ? 0 : 1,
+                          c->st);
+  RowPlan32& rp = row_plan32(c, M, nsign);
+  const Matrix& e = c->mats[c->i_embed];
+  const int ld_d = (int)ceil_div(3 * d + 3 * r, 32) * 32, ld_4d = (int)ceil_div(12 * d + 3 * r, 32) * 32;
+  PosEmbed pos;
+  if (c->opt) {
+    const Matrix& pm = c->mats[c->i_pos];
+    pos.W64 = pm.W64;
+    pos.Pp = c->Pp + pm.u_off;
+    pos.Pm = c->Pm + pm.u_off;
+    pos.V32 = c->V32 + pm.v_off;
+    pos.offset = 2;
+  }
+  launch_embed(c->x32, c->tok, c->T, B, T, d, e.W64, e.W16, false, c->Pp + e.u_off, c->Pm + e.u_off,
+               c->V32 + e.v_off, r, c->pe, pos, M, c->st);
+  for (int l = 0; l < c->d.n_layers; ++l) {
+    const Matrix& q = c->mats[c->i_qkv[l]];
+    const Matrix& o = c->mats[c->i_out[l]];
+    const Matrix& u = c->mats[c->i_up[l]];
+    const Matrix& w = c->mats[c->i_down[l]];
+    launch_ln_split(c->x32, c->ln1g[l], c->ln1b[l], c->vstride, M, d, c->a32, ld_d, c->Pp + q.u_off,
+                    c->Pm + q.u_off, r, rps, c->st);
+    gemm_launch(rp.qkv[l], c->st);
+    launch_attn32(c->f32a, 3 * d, c->ctx32, d, nsign * B, T, c->d.n_heads, c->dh, c->st);
+    launch_split_act(c->ctx32, d, M, d, c->a32, ld_d, c->Pp + o.u_off, c->Pm + o.u_off, r, rps, 0, c->st);
+    gemm_launch(rp.out[l], c->st);
+    launch_ln_split(c->x32, c->ln2g[l], c->ln2b[l], c->vstride, M, d, c->a32, ld_d, c->Pp + u.u_off,
+                    c->Pm + u.u_off, r, rps, c->st);
+    gemm_launch(rp.up[l], c->st);
+    launch_split_act(c->f32a, 4 * d, M, 4 * d, c->a32, ld_4d, c->Pp + w.u_off, c->Pm + w.u_off, r, rps,
+                     c->opt ? 2 : 1, c->st);
+    gemm_launch(rp.down[l], c->st);
+  }
+  const int S = nsign * B * c->d.opt_len;
+  launch_final_ln(c->x32, c->lnfg, c->lnfb, B * nsign, T, d, c->d.prompt_len, c->d.opt_len, c->xs32, c->xs16,
+                  false, c->V32 + e.v_off, r, c->z, rps, c->vstride, c->st);
+  launch_split_act(c->xs32, d, S, d, c->a32, e.ldk, nullptr, nullptr, 0, S, 0, c->st);
+  gemm_launch(rp.lm, c->st);
+  launch_loss(c->logits, c->ldl, c->d.vocab, c->z, r, c->Pp + e.u_off, c->Pm + e.u_off, c->gold, B,
+              c->d.opt_len, c->nll, c->st);
+}
+
 void do_score(zo_ctx* c, int B, int nsign) {
   const int d = c->d.dim, T = c->Tf, M = nsign * B * T;
   check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
+  if (c->real32) {
+    do_score32(c, B, nsign);
+    return;
+  }
   RowPlan& rp = row_plan(c, M, nsign);
   const Matrix& e = c->mats[c->i_embed];
   const int rps = B * T;
@@ -556,7 +659,15 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->Tf = c->T - 1;
   c->dh = d.dim / d.n_heads;
   c->r = d.rank;
+  check(d.precision == ZO_PREC_FP16 || d.precision == ZO_PREC_BF16 || d.precision == ZO_PREC_FP32, ZO_ERR_CONFIG,
+        "unknown precision");
   c->bf16 = d.precision == ZO_PREC_BF16;
+  c->real32 = d.precision == ZO_PREC_FP32;
+  if (c->real32) {
+    check(d.rank <= 8, ZO_ERR_CONFIG, "real32 scorer supports rank <= 8");
+    check(c->dh <= 128, ZO_ERR_CONFIG, "real32 scorer supports head dim <= 128");
+    check(d.estimator != ZO_EST_DENSE, ZO_ERR_CONFIG, "real32 scorer: dense_mezo runs the 16-bit materialising loop");
+  }
   check(d.scope == ZO_SCOPE_LORA_ONLY || d.scope == ZO_SCOPE_FULL, ZO_ERR_CONFIG, "unknown scope");
   check(d.estimator == ZO_EST_LOZO || d.estimator == ZO_EST_FACTORIZED || d.estimator == ZO_EST_DENSE, ZO_ERR_CONFIG,
         "unknown estimator");
@@ -632,6 +743,27 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
     } else {
       m.ldw = (int)(m.m + c->KE);
       m.W16 = c->mem.get<uint16_t>((size_t)(m.n * m.ldw));
+    }
+  }
+  if (c->real32) {
+    // 3xTF32 split operands: 12 bytes per weight beside the float64 master
+    double need = 0;
+    for (auto& m : c->mats)
+      if (m.kind != K_POS) need += 12.0 * (double)m.m * (double)m.n;
+    size_t free_b = 0, total_b = 0;
+    ZO_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+    check(need + 4e9 < (double)free_b, ZO_ERR_CONFIG,
+          "real32: the 3xTF32 split weights (" + std::to_string((long long)(need / 1e9)) +
+              " GB) do not fit beside the float64 master; use fp16/bf16 at this size");
+    for (auto& m : c->mats) {
+      if (m.kind == K_POS) continue;
+      if (m.kind == K_EMBED) {
+        m.ldk = (int)ceil_div(3 * m.n, 32) * 32;
+        m.W32S = c->mem.get<float>((size_t)m.m * m.ldk);
+      } else {
+        m.ldk = (int)ceil_div(3 * m.m + 3 * d.rank, 32) * 32;
+        m.W32S = c->mem.get<float>((size_t)m.n * m.ldk);
+      }
     }
   }
   // slots
@@ -725,6 +857,12 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->hS = c->mem.get<uint16_t>((size_t)c->Spad * (D + c->KE));
   c->gS = c->mem.get<uint16_t>((size_t)c->Spad * (4 * D + c->KE));
   c->x32S = c->mem.get<float>((size_t)c->Spad * D);
+  if (c->real32) {
+    c->lda32 = (int)ceil_div(12 * D + 3 * d.rank, 32) * 32;
+    c->a32 = c->mem.get<float>((size_t)c->Mpad * c->lda32);
+    c->f32a = c->mem.get<float>((size_t)c->Mpad * 4 * D);
+    c->ctx32 = c->mem.get<float>((size_t)c->Mpad * D);
+  }
 
   c->xs32 = c->mem.get<float>((size_t)c->Smax * D);
   c->z = c->mem.get<float>((size_t)c->Smax * d.rank);
@@ -1469,6 +1607,8 @@ void baseline_directions(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu) {
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
   const int64_t wstart = lozo ? (int64_t)((step / (uint64_t)nu) * (uint64_t)nu) : (int64_t)step;
   check(!c->a_dirty, ZO_ERR_CONFIG, "materialising loop on a replica with unfolded window mass");
+  // the comparand writes its probes into the 16-bit serving copies (baseline_loop.py:68-119)
+  check(!c->real32, ZO_ERR_CONFIG, "the materialising-loop comparand runs the 16-bit modes only");
   if (c->dense) {
     sampler_launch(c->planZM, seed, c->d_step, 1, c->ZM, c->st);
     sample_z(c, seed);
@@ -1778,6 +1918,38 @@ extern "C" int zo_test_gemm(int32_t M, int32_t N, int32_t K, int32_t lda, int32_
   } else {
     ZO_CUDA_TRY(cudaMemcpy(C_host, C, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
   }
+  return ZO_OK;
+  ZO_API_END
+}
+
+// test hook of the real32 path: C[M, N] = A[M, K] . W[K, N] (W in the reference's (in, out)
+// layout, float64) through the production 3xTF32 split (precise.cu) and the tf32 tcgen05
+// GEMM (EPI_STORE32); A is fp32 as the scorer's activations are.
+extern "C" int zo_test_gemm_tf32x3(int32_t M, int32_t N, int32_t K, const float* A_host, const double* W_host,
+                                   float* C_host) {
+  ZO_API_BEGIN
+  check(M >= 1 && N >= 1 && K >= 1, ZO_ERR_DIMENSION, "bad GEMM shape");
+  int dev = 0;
+  ZO_CUDA_TRY(cudaGetDevice(&dev));
+  int sms = 148;
+  ZO_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  DevAlloc m;
+  const int Mpad = (int)ceil_div(M, 128) * 128;
+  const int ldk = (int)ceil_div(3 * K, 32) * 32;
+  float* A = m.get<float>((size_t)M * K);
+  double* W = m.get<double>((size_t)K * N);
+  float* As = m.get<float>((size_t)Mpad * ldk);
+  float* Ws = m.get<float>((size_t)N * ldk);
+  float* C = m.get<float>((size_t)M * N);
+  ZO_CUDA_TRY(cudaMemcpy(A, A_host, (size_t)M * K * 4, cudaMemcpyHostToDevice));
+  ZO_CUDA_TRY(cudaMemcpy(W, W_host, (size_t)K * N * 8, cudaMemcpyHostToDevice));
+  launch_split_act(A, K, M, K, As, ldk, nullptr, nullptr, 0, M, 0, 0);
+  launch_split_weight(W, K, N, nullptr, 0, Ws, ldk, 1, 0);
+  GemmDesc g;
+  gemm_plan(g, As, M, ldk, Ws, N, ldk, 3 * K, EPI_STORE32, 2, C, N, sms);
+  gemm_launch(g, 0);
+  ZO_CUDA_TRY(cudaDeviceSynchronize());
+  ZO_CUDA_TRY(cudaMemcpy(C_host, C, (size_t)M * N * 4, cudaMemcpyDeviceToHost));
   return ZO_OK;
   ZO_API_END
 }

@@ -8,6 +8,7 @@ the host only stages token ids and reads back (L+, L-, c, beta).
 from __future__ import annotations
 
 import ctypes
+import warnings
 
 import numpy as np
 
@@ -15,9 +16,15 @@ from . import _lib
 from ._lib import check, lib
 from .errors import ConfigError, DimensionError
 
-PRECISIONS = {"fp16": _lib.PREC_FP16, "bf16": _lib.PREC_BF16}
-# the reference's precision strings run on the tensor-core path
-ALIASES = {"real64": "fp16", "real32": "fp16"}
+# "real32": the reference's float32 forward (model.py:149-154) as 3xTF32 tensor-core GEMMs with
+# fp32 LN / attention / loss -- the parity mode.  "fp16" / "bf16": 16-bit operands, fp32
+# accumulate -- the performance modes (fp16 default).
+PRECISIONS = {"fp16": _lib.PREC_FP16, "bf16": _lib.PREC_BF16, "real32": _lib.PREC_FP32}
+ALIASES = {"fp32": "real32"}
+# "real64" (the reference's default) has no device form: float64 GEMMs are not on the tensor
+# cores.  It runs the fp16 performance mode, with a warning; the float64
+# parity evidence is the oracle.
+REAL64_FALLBACK = "fp16"
 ESTIMATORS = {"lozo_lazy": _lib.EST_LOZO, "factorized_sqrt_r": _lib.EST_FACTORIZED,
               "dense_mezo": _lib.EST_DENSE}  # dense_mezo: the materialising loop only
 SCOPES = {"lora_only": _lib.SCOPE_LORA_ONLY, "full": _lib.SCOPE_FULL}
@@ -44,6 +51,12 @@ U, V, A, Z, ZM = 0, 1, 2, 3, 4  # slot arenas (Z: 1-D directions; ZM: dense_mezo
 
 
 def resolve_precision(precision: str) -> str:
+    """Device precision for a reference precision string (model.py:149-154 accepts
+    "real64" / "real32"; anything unknown is a ConfigError)."""
+    if precision == "real64":
+        warnings.warn("precision 'real64' has no tensor-core form: running the fp16 mode "
+                      "(use 'real32' for the fp32 parity mode)", RuntimeWarning, stacklevel=3)
+        return REAL64_FALLBACK
     p = ALIASES.get(precision, precision)
     if p not in PRECISIONS:
         raise ConfigError(f"unknown precision {precision!r}")
@@ -368,6 +381,18 @@ class ZoEngine:
         f = (ctypes.c_float * 3)()
         check(lib().zo_last_step_ms(self._h, f))
         return float(f[0]), float(f[1]), float(f[2])
+
+
+def test_gemm_tf32x3(A: np.ndarray, W: np.ndarray) -> np.ndarray:
+    """C = A . W through the real32 path's 3xTF32 split + tf32 tcgen05 GEMM (A fp32 [M, K],
+    W float64 [K, N] in the reference's (in, out) layout); returns fp32 [M, N]."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    M, K = A.shape
+    N = W.shape[1]
+    out = np.zeros((M, N), dtype=np.float32)
+    check(lib().zo_test_gemm_tf32x3(M, N, K, A.ctypes.data, W.ctypes.data, out.ctypes.data))
+    return out
 
 
 def test_gemm(A: np.ndarray, B: np.ndarray, epi: int = 3, bf16: bool = False, C: np.ndarray | None = None,

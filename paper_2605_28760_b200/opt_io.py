@@ -27,6 +27,7 @@ from __future__ import annotations
 import numpy as np
 
 from .errors import ConfigError, InputError
+from .engine import resolve_precision
 from .model import ModelConfig
 
 __all__ = ["config_from_hf", "params_from_hf", "params_to_hf", "load_hf_opt"]
@@ -139,5 +140,5 @@ def load_hf_opt(model_or_state_dict, prompt_len: int, precision: str = "fp16", m
         raise ConfigError("hf_config is required with a bare state dict")
     cfg = config_from_hf(hf_config, prompt_len)
     host = params_from_hf(sd, cfg)
-    return cfg, DeviceParams(cfg, host=host, precision=precision if precision in ("fp16", "bf16") else "fp16",
+    return cfg, DeviceParams(cfg, host=host, precision=resolve_precision(precision),
                              max_batch=max_batch, device=device)

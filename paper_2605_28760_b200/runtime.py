@@ -17,6 +17,7 @@ from dataclasses import dataclass, field
 from .adapter import AdapterState
 from .engine import U as SLOT_U, V as SLOT_V, Z as SLOT_Z
 from .errors import ConfigError, ScoringAbort
+from .engine import resolve_precision
 from .model import (EvalPoint, ModelConfig, TaskData, as_device_params, evaluate_split, init_params,
                     params_digest, sample_minibatch)
 from .numerics import digest_hex
@@ -78,7 +79,7 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
     if zcfg.estimator == "dense_mezo":
         raise ConfigError("dense_mezo has no serving-path form (no compact update factor); "
                           "use the baseline path for it")
-    params = init_params(mcfg, precision=precision if precision in ("fp16", "bf16") else "fp16",
+    params = init_params(mcfg, precision=resolve_precision(precision),
                          max_batch=max(16, zcfg.batch_size)) if params is None else params
     dp = as_device_params(params, mcfg)
     opt_len = len(task.config.options[0])
@@ -215,7 +216,7 @@ def load_checkpoint(path: str, precision: str = "fp16", max_batch: int = 16, dev
     if params_digest(host) != meta["params_digest"]:
         raise InputError("checkpoint params digest mismatch")
     from .model import DeviceParams
-    params = DeviceParams(mcfg, host=host, precision=precision if precision in ("fp16", "bf16") else "fp16",
+    params = DeviceParams(mcfg, host=host, precision=resolve_precision(precision),
                           max_batch=max_batch, device=device)
     state = load_adapter(os.path.join(path, "adapter.zoad"))
     for e in state._host_entries.values():

@@ -14,3 +14,7 @@ HIGH_SIGNAL = 0.005                      # |L+ - L-| threshold of verify.py's si
 LOSS_MATERIALISED = 1e-2
 # the OPT micro decoder (d = 32, random biases / LN params, ReLU; test_gpu_opt.py): observed 4.5e-3
 LOSS_OPT = 1.5e-2
+# "real32" (the reference's float32 forward, 3xTF32 tensor-core GEMMs): SURVEY.md §8(c) fp32 mode
+REAL32_NLL = 1e-5
+REAL32_LOSS = 1e-5
+REAL32_C_REL = 1e-3
