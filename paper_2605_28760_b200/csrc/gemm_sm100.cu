@@ -216,6 +216,7 @@ struct GemmCfg {
 
 struct GemmParams {
   int M, N, num_kb, last_ksteps, m_tiles, n_tiles, ldo;
+  int kb0;  // first K block of this launch (the tf32 path's K-chunked launches; 0 otherwise)
   void* out;
   // EPI_GELU16_EXT: per-tile partial LoRA-extension dots of the stored 16-bit
   // activation with the NEXT matrix's P+- (see zo_gemm.h)
@@ -385,12 +386,12 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t fb = full0 + 8 * stage;
           if constexpr (CG == 2) {
             if (leader) mbar_arrive_expect_tx(fb, 2 * stage_bytes);
-            tma_load_2d_cg2(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * KE, m0);
-            tma_load_2d_cg2(smem_u32(sB + stage * C::B_BYTES), tb, fb, kb * KE, n0);
+            tma_load_2d_cg2(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, (p.kb0 + kb) * KE, m0);
+            tma_load_2d_cg2(smem_u32(sB + stage * C::B_BYTES), tb, fb, (p.kb0 + kb) * KE, n0);
           } else {
             mbar_arrive_expect_tx(fb, stage_bytes);
-            tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, kb * KE, m0);
-            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), tb, fb, kb * KE, n0);
+            tma_load_2d(smem_u32(sA + stage * C::A_BYTES), &tmA, fb, (p.kb0 + kb) * KE, m0);
+            tma_load_2d(smem_u32(sB + stage * C::B_BYTES), tb, fb, (p.kb0 + kb) * KE, n0);
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -823,7 +824,7 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms) {
 }
 
 template <int BN, int EPI, int BF16, int XR, int CG>
-static void launch_t(const GemmDesc& g, cudaStream_t st) {
+static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = -1, int last_ksteps = -1) {
   using C = GemmCfg<BN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -834,8 +835,9 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   GemmParams p;
   p.M = g.M;
   p.N = g.N;
-  p.num_kb = g.num_kb;
-  p.last_ksteps = g.last_ksteps;
+  p.kb0 = kb0;
+  p.num_kb = nkb < 0 ? g.num_kb : nkb;
+  p.last_ksteps = last_ksteps < 0 ? g.last_ksteps : last_ksteps;
   p.m_tiles = (g.M + 128 * CG - 1) / (128 * CG);
   p.n_tiles = (g.N + BN - 1) / BN;
   p.ldo = g.ldo;
@@ -854,7 +856,7 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   p.half_dp = g.half_dp;
   p.trace = g.trace;
   p.half_n = g.half_n;
-  p.bias = g.bias;
+  p.bias = kb0 == 0 ? g.bias : nullptr;  // a K-chunked launch adds the bias once
   p.bias_rps = g.bias_rps;
   p.bias_vstride = g.bias_vstride;
   p.relu = g.relu;
@@ -879,10 +881,30 @@ static void launch_t(const GemmDesc& g, cudaStream_t st) {
   }
 }
 
+// tf32 operands (the real32 path's 3xTF32 GEMMs).  The tensor core's fp32 accumulation
+// truncates on every MMA, an error growing linearly with the number of accumulations
+// (measured: ~1e-8 x K relative, scripts/diag_tf32.py), so K is cut into chunks of
+// ZO_TF32_KCHUNK 32-wide blocks (default 4 = 16 MMAs; K = 4096: 4e-5 unchunked, 2.9e-6 at 8,
+// 1.9e-6 at 4 -- fp32-GEMM class): the first chunk stores (or adds
+// into the residual), every later chunk adds its fp32 partial with a round-to-nearest
+// add in the epilogue (EPI_RESID32).
+static int tf32_kchunk() {
+  static const int kc = [] {
+    const char* e = std::getenv("ZO_TF32_KCHUNK");
+    const int v = e ? std::atoi(e) : 4;
+    return v > 0 ? v : 4;
+  }();
+  return kc;
+}
 template <int BN, int CG>
-static void launch_e32(const GemmDesc& g, cudaStream_t st) {  // tf32 operands (3xTF32 real32 path)
-  if (g.epi == EPI_RESID32) launch_t<BN, EPI_RESID32, 2, 0, CG>(g, st);
-  else launch_t<BN, EPI_STORE32, 2, 0, CG>(g, st);
+static void launch_e32(const GemmDesc& g, cudaStream_t st) {
+  const int kc = tf32_kchunk();
+  for (int kb0 = 0; kb0 < g.num_kb; kb0 += kc) {
+    const int n = std::min(kc, g.num_kb - kb0);
+    const int ls = (kb0 + n == g.num_kb) ? g.last_ksteps : 4;
+    if (g.epi == EPI_RESID32 || kb0 > 0) launch_t<BN, EPI_RESID32, 2, 0, CG>(g, st, kb0, n, ls);
+    else launch_t<BN, EPI_STORE32, 2, 0, CG>(g, st, kb0, n, ls);
+  }
 }
 
 template <int BN, bool BF16, int CG>
