@@ -215,6 +215,48 @@ def run_reference(args, mdl):
     print(json.dumps(line), flush=True)
 
 
+def config1_gpu(args, M, ZoEngine, torch, stream, steps: int = 50, warmup: int = 5) -> dict:
+    """BASELINE config 1 (OPT-125m dims, B = 16, T = 64, r = 2, nu = 50) on this GPU: the fused
+    step graph over device-resident batches, CUDA events, the window boundary inside."""
+    mdl = MODELS["opt-125m"]
+    mcfg = M.ModelConfig(vocab=mdl["vocab"], dim=mdl["dim"], n_layers=mdl["n_layers"], n_heads=mdl["n_heads"],
+                         prompt_len=63, init_seed=7, init_scale=0.02)
+    task = M.generate_task(M.TaskConfig(seed=11, vocab=mdl["vocab"], prompt_len=63, train_size=1000, dev_size=4,
+                                        val_size=4))
+    eng = ZoEngine(mcfg.vocab, mcfg.dim, mcfg.n_layers, mcfg.n_heads, 63, max_batch=16, rank=2,
+                   precision=args.precision)
+    eng.set_stream(stream.cuda_stream)
+    eng.init_params(mcfg.init_seed, mcfg.init_scale)
+    t0 = 50 - steps // 2 - warmup
+    toks, golds = [], []
+    for t in range(t0, t0 + warmup + steps):
+        seq, gold = M.sample_minibatch(task, "train", 42, t, 16).sequences()
+        toks.append(seq)
+        golds.append(gold)
+    d_tok = torch.from_numpy(np.asarray(toks, dtype=np.int32)).cuda()
+    d_gold = torch.from_numpy(np.asarray(golds, dtype=np.int32)).cuda()
+
+    def step(i):
+        t = t0 + i
+        eng.step_graph(42, t, 50, 1e-3, 1e-7, False, d_tok[i].data_ptr(), d_gold[i].data_ptr(), 16)
+        if (t + 1) % 50 == 0:
+            eng.fold_async()
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(warmup, warmup + steps):
+        step(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    eng.close()
+    return {"value": 1000.0 / ms, "unit": UNIT, "ms_per_step": ms, "steps": steps,
+            "workload": "opt-125m LoZO r=2 LoRA-only SST-2 shape, B=16 x T=64, nu=50 (BASELINE config 1), "
+                        f"timed steps {t0 + warmup}..{t0 + warmup + steps - 1} incl. the window boundary"}
+
+
 # --------------------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -311,19 +353,25 @@ def main():
     torch.cuda.synchronize()
     t_init = time.perf_counter() - t_init
 
-    # device-resident batches for every step of the run (the contract's `value`)
+    # step schedule: the timed span is centred on a window boundary, so it contains the fold
+    # of one window and the V resample of the next (runtime.py:327-330 / zo_engine.py:389-400)
+    # -- with K < nu the boundary is over-represented (conservative for `value`)
+    nu_m = max(1, zcfg.nu // G)  # macro-steps per window
+    t_first = nu_m * -(-(args.warmup + args.steps // 2) // nu_m) - args.steps // 2
+    t0_run = t_first - args.warmup
     nsteps = args.warmup + args.steps
     toks = np.zeros((nsteps, Bl, T), dtype=np.int32)
     golds = np.zeros((nsteps, Bl, 1), dtype=np.int32)
-    for t in range(nsteps):
+    for i in range(nsteps):
+        t = t0_run + i
         if qdir:  # this rank's direction: reference step t*G + rank, full batch
             seq, gold = M.sample_minibatch(task, "train", zcfg.seed, t * G + rank, B).sequences()
-            toks[t], golds[t] = seq, gold
+            toks[i], golds[i] = seq, gold
             continue
         mb = M.sample_minibatch(task, "train", zcfg.seed, t, B)
         seq, gold = mb.sequences()
-        toks[t] = seq[rank * Bl:(rank + 1) * Bl]
-        golds[t] = gold[rank * Bl:(rank + 1) * Bl]
+        toks[i] = seq[rank * Bl:(rank + 1) * Bl]
+        golds[i] = gold[rank * Bl:(rank + 1) * Bl]
     d_tok = torch.from_numpy(toks).cuda()
     d_gold = torch.from_numpy(golds).cuda()
     nll_local = torch.zeros(2 * Bl, dtype=torch.float64, device="cuda")
@@ -333,7 +381,7 @@ def main():
 
     def one_step(t, tp=None, gp=None):
         if tp is None:
-            tp, gp = d_tok[t].data_ptr(), d_gold[t].data_ptr()
+            tp, gp = d_tok[t - t0_run].data_ptr(), d_gold[t - t0_run].data_ptr()
         if qdir:
             import torch.distributed as dist
             eng.qdir_score_async(zcfg.seed, t, G, rank, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, B)
@@ -366,7 +414,7 @@ def main():
             dist.barrier()
 
     cold = layer_gemms(eng, Bl) if (rank == 0 and not args.profile) else None
-    for t in range(args.warmup):
+    for t in range(t0_run, t_first):
         one_step(t)
     torch.cuda.synchronize()
     barrier()
@@ -374,7 +422,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
-        for t in range(args.warmup, nsteps):
+        for t in range(t_first, t_first + args.steps):
             one_step(t)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -399,7 +447,7 @@ def main():
         ms = float(tt.item())
     ms_step = ms / args.steps
     value = 1000.0 * G / ms_step  # reference steps (ZO directions) per second, whole job
-    windows = sum(1 for t in range(args.warmup, nsteps) if (t * G) % zcfg.nu == 0)
+    windows = sum(1 for t in range(t_first, t_first + args.steps) if (t * G) % zcfg.nu == 0)
     per_step, per_window = eng.graph_kernel_count()
     if not (world == 1 and args.graph) or per_step <= 1:
         per_step = launches_per_step(mcfg.n_layers, 4 * mcfg.n_layers + 1, False)  # eager paths: estimate
@@ -407,6 +455,8 @@ def main():
 
     hbm_peak, tf_peak, tf_sust, peak_kind = peaks()
     cfg, scaling, _ = workload_config(args, world)
+    cfg["timed_steps"] = [t_first, t_first + args.steps - 1]
+    cfg["window_boundaries_timed"] = windows
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None,
@@ -428,11 +478,11 @@ def main():
         # a CUDA event in front of every kernel group on the engine stream; the GEMMs' device
         # time over their algorithmic FLOPs, against the SUSTAINED measured bf16 peak
         if not qdir and world == 1:
-            t_prof = nsteps % len(d_tok)
-            eng.profile_step(zcfg.seed, nsteps, zcfg.nu, zcfg.epsilon, zcfg.learning_rate,
-                             d_tok[t_prof].data_ptr(), d_gold[t_prof].data_ptr(), Bl)  # plans warm
-            fam = eng.profile_step(zcfg.seed, nsteps + 1, zcfg.nu, zcfg.epsilon, zcfg.learning_rate,
-                                   d_tok[t_prof].data_ptr(), d_gold[t_prof].data_ptr(), Bl)
+            t_prof = t_first + args.steps
+            eng.profile_step(zcfg.seed, t_prof, zcfg.nu, zcfg.epsilon, zcfg.learning_rate,
+                             d_tok[0].data_ptr(), d_gold[0].data_ptr(), Bl)  # plans warm
+            fam = eng.profile_step(zcfg.seed, t_prof + 1, zcfg.nu, zcfg.epsilon, zcfg.learning_rate,
+                                   d_tok[0].data_ptr(), d_gold[0].data_ptr(), Bl)
         else:
             fam = None
         d, Lr, Mr = mcfg.dim, mcfg.n_layers, 2 * Bl * (T - 1)  # rows the forward computes
@@ -469,25 +519,33 @@ def main():
                 "when": "same isolated launches on the cold GPU before the warm-up (burst clocks)"}
 
     if not args.no_e2e and not args.profile and world == 1:
-        # public API: sample_minibatch + lozo_step on host batches (+ fold at boundaries)
+        # the public API end to end: run_serving_path (runtime.py:253-359, row a1) on host
+        # minibatches -- per step sample_minibatch, the H2D copy of tokens/golds from pinned
+        # staging, one fused lozo_step, the D2H read of [L+, L-, c, beta], the U arena copied
+        # back for the U/V digests the reference's records carry (FNV on a host thread pool)
+        # and the fold at the window boundary.  Timed by wall clock over the step loop plus
+        # the final digest wait, evals excluded (train_wall_s semantics).
+        from paper_2605_28760_b200.runtime import run_serving_path
         params = M.DeviceParams(mcfg, precision=args.precision, max_batch=B)
         params._engine = eng  # reuse the initialised replica
         state = AdapterState(epsilon=zcfg.epsilon)
-        step_fn = factorized_step if fact else lozo_step
-        for t in range(nsteps, nsteps + args.warmup):
-            step_fn(params, mcfg, state, zcfg, t, M.sample_minibatch(task, "train", zcfg.seed, t, B),
-                    digests="off")
+        base = t_first + args.steps + 2
+        e_first = nu_m * -(-(base + args.warmup + args.steps // 2) // nu_m) - args.steps // 2
+        kw = dict(eval_every=10 ** 9, params=params, state=state, compute_param_digests=False, final_fold=False,
+                  digests=True)
+        run_serving_path(mcfg, task, zcfg, args.warmup, start_step=e_first - args.warmup, **kw)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for t in range(nsteps + args.warmup, nsteps + args.warmup + args.steps):
-            mb = M.sample_minibatch(task, "train", zcfg.seed, t, B)
-            step_fn(params, mcfg, state, zcfg, t, mb, digests="off")
-            if not fact and (t + 1) % zcfg.nu == 0:
-                eng.fold()
+        run = run_serving_path(mcfg, task, zcfg, args.steps, start_step=e_first, **kw)
         torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / args.steps
-        line["e2e"] = {"value": 1.0 / e2e_s, "unit": UNIT, "h2d_bytes_per_step": B * T * 4 + B * 4 + 8,
-                       "d2h_bytes_per_step": 32, "api": f"model.sample_minibatch + zo_engine.{step_fn.__name__} (host batch)",
+        e2e_s = (run.extra["loop_wall_s"] + run.extra["digest_wait_s"]) / args.steps
+        assert all(r.u_digest and r.v_digest for r in run.trajectory)
+        line["e2e"] = {"value": 1.0 / e2e_s, "unit": UNIT,
+                       "h2d_bytes_per_step": B * T * 4 + 2 * B * 4 + 8,
+                       "d2h_bytes_per_step": 32 + 8 * eng.su,
+                       "api": "runtime.run_serving_path (host minibatches, fused lozo_step, U/V digests on the "
+                              "host pool, folds at window boundaries)",
+                       "timed_steps": [e_first, e_first + args.steps - 1],
+                       "digest_wait_s": run.extra["digest_wait_s"],
                        "phase_ms_last_step": dict(zip(["sample", "score", "update"], eng.last_step_ms()))}
 
     if not args.no_e2e and not args.profile and world > 1:
@@ -562,11 +620,23 @@ def main():
                     "W-=eta*c*P (zo_baseline_step_async, float64 master + 16-bit serving copy)"}
 
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
-        from oracle.cpu_bench import estimate_step, host_threads
+        from oracle.cpu_bench import estimate_step, host_threads, reference_config1
         step_s, desc, _ = estimate_step(mcfg.dim, mcfg.n_layers, mcfg.n_heads, mcfg.vocab, B, T,
                                         n_examples=4 if mcfg.dim >= 4096 else B)
         line["cpu_baseline"] = {"value": 1.0 / step_s, "unit": UNIT, "cores": host_threads(), "kind": "port",
-                                "sample": desc}
+                                "sample": desc + " (extrapolated: the 13B step does not fit a bounded CPU run)"}
+        if world == 1:
+            # BASELINE config 1 measured in whole steps on both sides, no extrapolation: the
+            # reference's own lozo_step on the host cores and the same step on this B200
+            ref1 = reference_config1(steps=2, warmup=0)
+            g1 = config1_gpu(args, M, ZoEngine, torch, stream)
+            if ref1 is not None:
+                line["cpu_baseline"]["config1_reference"] = {
+                    "value": ref1[0], "unit": UNIT, "cores": host_threads(), "kind": "reference",
+                    "sample": ref1[1]}
+            line["config1_b200"] = g1
+            if ref1 is not None:
+                line["config1_b200"]["speedup_vs_reference"] = g1["value"] / ref1[0]
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -113,3 +113,38 @@ def host_threads() -> int:
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+def reference_config1(steps: int = 2, warmup: int = 1):
+    """The UNMODIFIED reference (oracle/_ref/zoserve, staged by oracle/stage_ref.sh) timed on
+    BASELINE config 1 -- OPT-125m dims, V = 50272, B = 16, T = 64, r = 2, nu = 50, lr 1e-7,
+    real64: whole ``zoserve.zo_engine.lozo_step`` calls (directions, both composed float64
+    forwards, coefficient, update), the state carried across steps exactly as
+    run_serving_path does (runtime.py:303-330).  Returns (steps/s, description) or None when
+    the reference was not staged."""
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref")
+    if not os.path.isfile(os.path.join(ref, "zoserve", "zo_engine.py")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from zoserve.adapter import AdapterState
+    from zoserve.model import ModelConfig, TaskConfig, generate_task, init_params, sample_minibatch
+    from zoserve.zo_engine import ZoConfig, lozo_step
+    mcfg = ModelConfig(vocab=50272, dim=768, n_layers=12, n_heads=12, prompt_len=63, init_seed=7, init_scale=0.02)
+    task = generate_task(TaskConfig(seed=11, vocab=50272, prompt_len=63, train_size=1000, dev_size=64, val_size=64))
+    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=1e-7, rank=2, nu=50, batch_size=16)
+    params = init_params(mcfg)
+    state = AdapterState(epsilon=zcfg.epsilon)
+    times = []
+    for t in range(warmup + steps):
+        batch = sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
+        t0 = time.perf_counter()
+        rec = lozo_step(params, mcfg, state, zcfg, t, batch, "real64")
+        if t >= warmup:
+            times.append(time.perf_counter() - t0)
+    s = float(np.mean(times))
+    desc = (f"the reference itself (zoserve.zo_engine.lozo_step, real64, oracle/_ref) at BASELINE config 1 "
+            f"(OPT-125m dims, B=16, T=64): {steps} whole steps timed after {warmup} warm-up, "
+            f"{s:.2f} s/step; last step L+ = {rec.loss_plus:.6f}")
+    return 1.0 / s, desc

@@ -107,6 +107,8 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
 
     do_eval(start_step)
     done = start_step
+    loop_t0 = time.perf_counter()
+    eval_in_loop = 0.0
     for t in range(start_step, start_step + steps):
         batch = sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
         t0 = time.perf_counter()
@@ -142,7 +144,10 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
             meter.time_fold_s += dt
             wall += dt
         if (t + 1) % eval_every == 0 and (t + 1) != start_step + steps:
+            e0 = time.perf_counter()
             do_eval(t + 1)
+            eval_in_loop += time.perf_counter() - e0
+    loop_wall = time.perf_counter() - loop_t0 - eval_in_loop
     if not aborted and final_fold and zcfg.estimator == "lozo_lazy":
         f0 = time.perf_counter()
         eng.fold()
@@ -153,15 +158,18 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
     if not aborted:
         do_eval(done)
     dp.sync_host()  # a caller's host dict sees the folds, as in the reference (runtime.py:242-250)
+    d0 = time.perf_counter()
     for rec, uf, vf in pending:
         rec.u_digest = digest_hex(uf.result())
         rec.v_digest = digest_hex(vf.result())
     if pool is not None:
         pool.shutdown()
+    digest_wait = time.perf_counter() - d0
     return ServingRun(config=zcfg, model_config=mcfg, trajectory=trajectory, eval_curve=evals, meter=meter,
                       final_params_digest=params_digest(dp) if compute_param_digests else "", params=dp,
                       state=state, train_wall_s=wall, precision=precision, steps_completed=done,
-                      model_digest=model_digest, task_digest=task.digest(), aborted=aborted)
+                      model_digest=model_digest, task_digest=task.digest(), aborted=aborted,
+                      extra={"loop_wall_s": loop_wall, "digest_wait_s": digest_wait})
 
 
 # ---------------------------------------------------------------- checkpoint / resume
