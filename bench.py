@@ -175,9 +175,12 @@ def workload_config(args, world: int) -> tuple[dict, str, bool]:
     nu = args.nu
     if qdir and nu % world:
         nu = max(world, nu // world * world)
+    upd = ("float64 dense update every step (bit-exact)" if args.dense_update == "exact" else
+           "dense update every step as tcgen05 U V^T fused into the float64-master / 16-bit-shadow RMW")
     workload = (f"{args.model} factorized_sqrt_r (MeZO-style) r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, "
-                f"dense float64 update every step" if fact else
-                f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, nu={nu}, fold amortised")
+                f"{upd}" if fact else
+                f"{args.model} LoZO r={args.rank} LoRA-only SST-2 shape, B={B} x T={T}, nu={nu}, "
+                f"timed span centred on a window boundary (fold + V resample inside)")
     if args.arch == "opt":
         workload += ", OPT decoder (ReLU FFN, learned positions, projection biases)"
     cfg = {"workload": workload, "model": args.model, "global_batch": B, "seq_len": T,
@@ -271,6 +274,9 @@ def main():
                     help="factorized_sqrt_r = BASELINE config 5 (MeZO-style high-rank, e.g. --rank 128): "
                          "probe U V^T/sqrt(r), dense float64 update of every weight each step")
     ap.add_argument("--nu", type=int, default=50)
+    ap.add_argument("--dense-update", default="exact", choices=["exact", "tensor"],
+                    help="factorized_sqrt_r dense update: float64 bit-exact (default) or the tcgen05 U V^T "
+                         "fused into the master/shadow update (HBM-bound, ~1e-3 of each step's update)")
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16"])
     ap.add_argument("--arch", default="zoserve", choices=["zoserve", "opt"],
                     help="decoder: the reference's (default, parity-backed) or the OPT family's "
@@ -350,6 +356,8 @@ def main():
     stream = torch.cuda.current_stream()
     eng.set_stream(stream.cuda_stream)
     eng.init_params(mcfg.init_seed, mcfg.init_scale)
+    if fact and args.dense_update == "tensor":
+        eng.set_update_mode("tensor")
     torch.cuda.synchronize()
     t_init = time.perf_counter() - t_init
 

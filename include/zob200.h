@@ -144,6 +144,11 @@ int zo_update_u(zo_ctx* ctx);
 int zo_fold(zo_ctx* ctx);
 /* factorized_step's dense update (zo_engine.py:449-450): W += (-(lr*c)/sqrt(r)) U V^T */
 int zo_update_dense(zo_ctx* ctx, double lr);
+/* factorized dense update mode: 0 = float64, bit-exact with the reference's axpy_outer
+ * (default); 1 = tensor cores -- U V^T on tcgen05 (16-bit operands, fp32 accumulate) fused
+ * into the float64-master / 16-bit-shadow read-modify-write, HBM-bound; parameters then agree
+ * with the reference to ~1e-3 of each step's update, not bit for bit.  rank >= 16, % 16 == 0. */
+int zo_set_update_mode(zo_ctx* ctx, int32_t mode);
 /* full scope: every 1-D param p += (-(lr*c)) z with the installed c (VectorProbe.update,
  * zo_engine.py:290-295, 412-416); no-op for lora_only.  zo_update_dense applies it too. */
 int zo_update_vectors(zo_ctx* ctx, double lr);

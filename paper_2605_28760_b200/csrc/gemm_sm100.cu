@@ -240,6 +240,13 @@ struct GemmParams {
   int bias_rps;
   long bias_vstride;
   int relu;
+  // EPI_UPDATE64 (see zo_gemm.h)
+  double* upd_w64;
+  void* upd_w16;
+  int upd_ld64, upd_ld16, upd_transposed;
+  const double* upd_out4;
+  double upd_lr, upd_scale;
+  const unsigned* upd_abort;
 };
 
 // Work segments of one unit: (tile, k-block range).  Data-parallel phase: whole
@@ -564,6 +571,62 @@ __global__ void __launch_bounds__(192, 1)
           v[4 * j + 3] += w.w;
         }
       };
+      if constexpr (EPI == EPI_UPDATE64) {
+        // W64 += alpha * D with the 16-bit shadow rewritten from the new value.  Every lane
+        // runs the TMEM loads (.sync.aligned); memory ops are guarded per row / column.
+        const bool skip = p.upd_abort ? (*p.upd_abort != 0u)
+                                      : !(isfinite(p.upd_out4[0]) && isfinite(p.upd_out4[1]));
+        const double alpha = -(p.upd_lr * p.upd_out4[2]) * p.upd_scale;
+#pragma unroll 1
+        for (int c = 0; c < bnc; c += 32) {
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+          const int col0 = n0 + c;
+          if (skip || !row_ok || col0 >= p.N) continue;
+          const int nc = min(32, p.N - col0);
+          double w[32];
+          if (p.upd_transposed) {
+            // row = output index j, columns = input indices i: W64[i][j] -- one 256-byte
+            // row segment per column across the warp's 32 consecutive rows
+            const double* src = p.upd_w64 + (size_t)col0 * p.upd_ld64 + row;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nc) w[i] = src[(size_t)i * p.upd_ld64];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nc) {
+                w[i] = fma(alpha, (double)v[i], w[i]);
+                p.upd_w64[(size_t)(col0 + i) * p.upd_ld64 + row] = w[i];
+              }
+          } else {
+            double* src = p.upd_w64 + (size_t)row * p.upd_ld64 + col0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nc) w[i] = src[i];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nc) {
+                w[i] = fma(alpha, (double)v[i], w[i]);
+                src[i] = w[i];
+              }
+          }
+          uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)row * p.upd_ld16 + col0;
+          if (nc == 32 && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pk[j] = pack2<BF16>((float)w[2 * j], (float)w[2 * j + 1]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              reinterpret_cast<uint4*>(o)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          } else {
+            for (int i = 0; i < nc; ++i) {
+              const uint32_t pk = pack2<BF16>((float)w[i], 0.f);
+              o[i] = (uint16_t)(pk & 0xffffu);
+            }
+          }
+        }
+        goto tile_done;
+      }
       if constexpr (EPI == EPI_RESID32) {
         // fast path: whole tile row in range -> residual loads for chunk c+1 are in
         // flight while chunk c is added and stored
@@ -860,6 +923,15 @@ static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = 
   p.bias_rps = g.bias_rps;
   p.bias_vstride = g.bias_vstride;
   p.relu = g.relu;
+  p.upd_w64 = g.upd_w64;
+  p.upd_w16 = g.upd_w16;
+  p.upd_ld64 = g.upd_ld64;
+  p.upd_ld16 = g.upd_ld16;
+  p.upd_transposed = g.upd_transposed;
+  p.upd_out4 = g.upd_out4;
+  p.upd_lr = g.upd_lr;
+  p.upd_scale = g.upd_scale;
+  p.upd_abort = g.upd_abort;
   if constexpr (CG == 1) {
     launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(192), C::SMEM, st, g.tmA, g.tmB, g.tmB2, p);
   } else {
@@ -919,6 +991,7 @@ static void launch_e(const GemmDesc& g, cudaStream_t st) {
       else launch_t<BN, EPI_GELU16_EXT, BF16, 8, CG>(g, st);
       break;
     case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16, 0, CG>(g, st); break;
+    case EPI_UPDATE64: launch_t<BN, EPI_UPDATE64, BF16, 0, CG>(g, st); break;
     default: launch_t<BN, EPI_STORE32, BF16, 0, CG>(g, st); break;
   }
 }

@@ -13,6 +13,9 @@ enum EpiKind : int {
   EPI_STORE32 = 3,  // out32[r, c] = acc                       (LM-head logits rows)
   EPI_GELU16_EXT = 4,  // EPI_GELU16 + per-tile partial t_k = sum_c a16[r,c] P[c,k] for the
                        // next GEMM's LoRA K-extension (tpart[n_tile][r][k], deterministic)
+  EPI_UPDATE64 = 5,    // factorized dense update on the tensor cores (zo_engine.py:449-450):
+                       // W64 += alpha * acc (alpha = -(lr*c)*scale from the device coefficient,
+                       // skipped when the step aborted), 16-bit shadow rewritten in the same pass
 };
 
 // D[M, N] = A[M, Kp] * B[N, Kp]^T, both operands K-major 16-bit, fp32 accumulate.
@@ -41,6 +44,15 @@ struct GemmDesc {
   int bias_rps = 0;
   long bias_vstride = 0;
   int relu = 0;  // EPI_GELU16*: ReLU instead of GELU-tanh (OPT arch)
+  // EPI_UPDATE64: the float64 master (row stride upd_ld64) and its 16-bit shadow (row stride
+  // upd_ld16); upd_transposed = 1: D = V U^T, D[j, i] updates W64[i, j] and W16T[j, i]
+  // (projections); 0: D = U V^T, D[i, j] updates W64[i, j] and W16[i, j] (embedding)
+  double* upd_w64 = nullptr;
+  void* upd_w16 = nullptr;
+  int upd_ld64 = 0, upd_ld16 = 0, upd_transposed = 0;
+  const double* upd_out4 = nullptr;
+  double upd_lr = 0.0, upd_scale = 1.0;
+  const unsigned* upd_abort = nullptr;
   // diagnostic timeline (zo_trace_gemm): per CTA 64 globaltimer stamps -- [0] start, [1] end,
   // [2+2i, 3+2i] MMA window of segment i (i < 15), [32+2i, 33+2i] its epilogue window
   unsigned long long* trace = nullptr;

@@ -102,6 +102,12 @@ struct zo_ctx {
   bool bf16 = false;
   // ZO_PREC_FP32 ("real32"): the fp32 forward on tcgen05 kind::tf32 via the 3xTF32 split
   bool real32 = false;
+  // factorized dense update mode (zo_set_update_mode): false = float64 SIMT, bit-exact with the
+  // reference (k_fold_dev_tiled); true = tensor-core UV^T fused into the master/shadow RMW
+  // (EPI_UPDATE64, r >= 16, r % 16 == 0) -- HBM-bound, not bit-exact
+  bool fast_update = false;
+  uint16_t *U16 = nullptr, *V16 = nullptr;  // 16-bit U / V operands of the fast update
+  std::vector<GemmDesc> upd_plans;           // per matrix (empty entry: exact path)
   float *a32 = nullptr, *f32a = nullptr, *ctx32 = nullptr;  // split A operand, qkv/ff_up out, ctx
   int lda32 = 0;                                             // row stride of a32
   std::map<int, RowPlan32> plans32;
@@ -601,6 +607,46 @@ void set_step(zo_ctx* c, uint64_t step) {
 }
 
 void launch_dense_update_dev(zo_ctx* c, double lr) {
+  if (c->fast_update) {
+    // 16-bit operands of this step's directions, then one fused GEMM + RMW per matrix
+    launch_shadow(c->U, c->su, c->U16, c->bf16, c->st);
+    launch_shadow(c->V, c->sv, c->V16, c->bf16, c->st);
+    if (c->upd_plans.empty()) {
+      c->upd_plans.resize(c->mats.size());
+      for (size_t i = 0; i < c->mats.size(); ++i) {
+        const Matrix& m = c->mats[i];
+        if (m.kind == K_POS) continue;  // no 16-bit shadow: the exact path below
+        GemmDesc& g = c->upd_plans[i];
+        const bool tr = m.kind != K_EMBED;
+        if (tr)  // D[j, i] = sum_k V[j, k] U[i, k]: rows = outputs (W16T rows)
+          gemm_plan(g, c->V16 + m.v_off, (int)m.n, c->r, c->U16 + m.u_off, (int)m.m, c->r, c->r, EPI_UPDATE64,
+                    c->bf16, nullptr, 0, c->num_sms);
+        else
+          gemm_plan(g, c->U16 + m.u_off, (int)m.m, c->r, c->V16 + m.v_off, (int)m.n, c->r, c->r, EPI_UPDATE64,
+                    c->bf16, nullptr, 0, c->num_sms);
+        g.upd_w64 = m.W64;
+        g.upd_w16 = m.W16;
+        g.upd_ld64 = (int)m.n;
+        g.upd_ld16 = m.ldw;
+        g.upd_transposed = tr ? 1 : 0;
+        g.upd_out4 = c->out4;
+        g.upd_lr = lr;
+        g.upd_scale = 1.0 / std::sqrt((double)c->r);
+        g.upd_abort = c->abort_flag;
+      }
+    }
+    for (size_t i = 0; i < c->mats.size(); ++i) {
+      const Matrix& m = c->mats[i];
+      if (m.kind == K_POS) {
+        launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, c->out4, lr,
+                        1.0 / std::sqrt((double)c->r), c->abort_flag, m.W16, (int)m.n, 0, c->bf16, c->st);
+        continue;
+      }
+      c->upd_plans[i].upd_lr = lr;
+      gemm_launch(c->upd_plans[i], c->st);
+    }
+    return;
+  }
   for (auto& m : c->mats)
     launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, c->out4, lr,
                     1.0 / std::sqrt((double)c->r), c->abort_flag, m.W16, m.kind == K_EMBED ? (int)m.n : m.ldw,
@@ -1186,6 +1232,25 @@ int zo_set_slot(zo_ctx* c, int32_t which, const double* host, int64_t count) {
     c->a_dirty = nz;  // uploaded window mass must be folded before V changes
   }
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_set_update_mode(zo_ctx* c, int32_t mode) {
+  ZO_API_BEGIN
+  check(mode == 0 || mode == 1, ZO_ERR_CONFIG, "update mode must be 0 (exact) or 1 (tensor)");
+  if (mode == 1) {
+    check(c->d.estimator == ZO_EST_FACTORIZED, ZO_ERR_CONFIG, "the tensor-core dense update serves factorized_sqrt_r");
+    check(c->r >= 16 && c->r % 16 == 0, ZO_ERR_CONFIG, "the tensor-core dense update needs rank >= 16, multiple of 16");
+    check(!c->real32, ZO_ERR_CONFIG, "real32 keeps the exact float64 update");
+    if (!c->U16) {
+      c->U16 = c->mem.get<uint16_t>((size_t)c->su);
+      c->V16 = c->mem.get<uint16_t>((size_t)c->sv);
+    }
+  }
+  c->fast_update = mode == 1;
+  c->upd_plans.clear();
+  c->gkey_valid = false;  // the captured step graph holds the old update
   return ZO_OK;
   ZO_API_END
 }

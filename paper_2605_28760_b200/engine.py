@@ -278,6 +278,14 @@ class ZoEngine:
     def fold(self) -> None:
         check(lib().zo_fold(self._h))
 
+    def set_update_mode(self, mode: str) -> None:
+        """Factorized dense update: "exact" (float64, bit-exact, default) or "tensor"
+        (tcgen05 U V^T fused into the master/shadow update, HBM-bound; zob200.h)."""
+        if mode not in ("exact", "tensor"):
+            raise ConfigError(f"update mode must be 'exact' or 'tensor', got {mode!r}")
+        check(lib().zo_set_update_mode(self._h, 0 if mode == "exact" else 1))
+        self.update_mode = mode
+
     def update_dense(self, lr: float) -> None:
         check(lib().zo_update_dense(self._h, float(lr)))
 
