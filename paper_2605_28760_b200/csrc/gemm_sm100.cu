@@ -203,15 +203,19 @@ __device__ __forceinline__ float unpack16(uint32_t w, int hi) {
   else return __half2float(__ushort_as_half(h));
 }
 
-template <int BN, int CG = 1>
+template <int BN, int CG = 1, bool UPD = false>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;  // rows per CTA; a CTA pair (CG = 2) covers 256
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
+  // EPI_UPDATE64: a short operand ring (K = rank) and a ring of float64 master blocks
+  // [32 rows][128 cols] streamed in and out by TMA (W_SLOTS x 32 KB)
+  static constexpr int W_SLOTS = UPD ? 3 : 0;
+  static constexpr int W_BYTES = 32 * BM * 8;
+  static constexpr int STAGES = UPD ? 3 : ((196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + W_SLOTS * W_BYTES + 512;
 };
 
 struct GemmParams {
@@ -315,7 +319,7 @@ template <int BN, int EPI, int DT, int XR, int CG>
 __global__ void __launch_bounds__(192, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmB2, GemmParams p) {
-  using C = GemmCfg<BN, CG>;
+  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE64>;
   constexpr bool BF16 = DT == 1, TF32 = DT == 2;
   constexpr int KE = TF32 ? 32 : 64;  // K elements per 128-byte block
   constexpr uint32_t FMT = TF32 ? 2u : BF16 ? 1u : 0u;  // instruction-descriptor a/b format
@@ -326,8 +330,12 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4);
+  uint8_t* sW = smem + C::STAGES * C::STAGE_BYTES;  // EPI_UPDATE64 master-block ring
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW + C::W_SLOTS * C::W_BYTES);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4 + 2 * C::W_SLOTS);
+  // TMA-streamed master update (EPI_UPDATE64 on a projection): W64 blocks in/out through sW
+  const bool wtma = (EPI == EPI_UPDATE64) && p.upd_transposed;
+  const uint32_t wfull0 = smem_u32(bars + 2 * C::STAGES + 4), wempty0 = wfull0 + 8 * C::W_SLOTS;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = smem_u32(bars + 2 * C::STAGES + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -336,7 +344,7 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    if (p.half_n) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
+    if (p.half_n || wtma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
@@ -344,6 +352,10 @@ __global__ void __launch_bounds__(192, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, 4 * CG);  // every epilogue warp of the pair arrives at the leader
+    }
+    for (int w = 0; w < C::W_SLOTS; ++w) {
+      mbar_init(wfull0 + 8 * w, 1);
+      mbar_init(wempty0 + 8 * w, 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -377,6 +389,7 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      int wround = 0;  // EPI_UPDATE64: master blocks issued so far
       SegIter si;
       si.init(p, CG);
       int t, k0, k1;
@@ -403,6 +416,20 @@ __global__ void __launch_bounds__(192, 1)
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
+          }
+        }
+        if constexpr (EPI == EPI_UPDATE64) {
+          // this CTA's master block rows = D columns (input index i), block cols = its 128
+          // D rows (output index j); tmB2 is the float64 map over W64 [m, n]
+          if (wtma) {
+            const int j0 = (t % p.m_tiles) * (C::BM * CG) + (int)rank * C::BM;
+            const int i0 = (t / p.m_tiles) * BN;
+            for (int r = 0; r < BN / 32; ++r, ++wround) {
+              const int ws = wround % C::W_SLOTS;
+              mbar_wait(wempty0 + 8 * ws, ((wround / C::W_SLOTS) & 1) ^ 1);
+              mbar_arrive_expect_tx(wfull0 + 8 * ws, C::W_BYTES);
+              tma_load_2d(smem_u32(sW + ws * C::W_BYTES), &tmB2, wfull0 + 8 * ws, j0, i0 + 32 * r);
+            }
           }
         }
       }
@@ -457,6 +484,7 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int wround_e = 0;        // EPI_UPDATE64: master blocks consumed so far
     const int erow = q * 32 + lane;  // row within the 128-row tile
     int it = 0;
     SegIter si;
@@ -572,57 +600,116 @@ __global__ void __launch_bounds__(192, 1)
         }
       };
       if constexpr (EPI == EPI_UPDATE64) {
-        // W64 += alpha * D with the 16-bit shadow rewritten from the new value.  Every lane
-        // runs the TMEM loads (.sync.aligned); memory ops are guarded per row / column.
+        if (wtma) {
+          // projection: the master block of round r ([32 input rows i][128 output cols j],
+          // this warp's 32 j columns) arrives by TMA; lane j updates its column in place in
+          // shared memory, writes its 32 shadow values W16T[j][i..i+31] (64 contiguous bytes),
+          // and one thread streams the block back with a TMA store.  A block's slot is
+          // returned to the producer once the store of the NEXT round has been issued and
+          // this one's shared-memory reads are complete (cp.async.bulk.wait_group.read 1).
+          const bool skip = p.upd_abort ? (*p.upd_abort != 0u)
+                                        : !(isfinite(p.upd_out4[0]) && isfinite(p.upd_out4[1]));
+          const double alpha = -(p.upd_lr * p.upd_out4[2]) * p.upd_scale;
+#pragma unroll 1
+          for (int r = 0; r < BN / 32; ++r, ++wround_e) {
+            const int ws = wround_e % C::W_SLOTS;
+            float v[32];
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + 32 * r, v);
+            mbar_wait(wfull0 + 8 * ws, (wround_e / C::W_SLOTS) & 1);
+            double* blk = reinterpret_cast<double*>(sW + ws * C::W_BYTES) + erow;  // column erow
+            const int col0 = n0 + 32 * r;
+            if (!skip) {
+              double w[32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) w[i] = blk[i * C::BM];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                w[i] = fma(alpha, (double)v[i], w[i]);
+                blk[i * C::BM] = w[i];
+              }
+              if (row_ok && col0 < p.N) {
+                uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)row * p.upd_ld16 + col0;
+                if (col0 + 32 <= p.N && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    uint4 u;
+                    u.x = pack2<BF16>((float)w[8 * j], (float)w[8 * j + 1]);
+                    u.y = pack2<BF16>((float)w[8 * j + 2], (float)w[8 * j + 3]);
+                    u.z = pack2<BF16>((float)w[8 * j + 4], (float)w[8 * j + 5]);
+                    u.w = pack2<BF16>((float)w[8 * j + 6], (float)w[8 * j + 7]);
+                    __stcs(reinterpret_cast<uint4*>(o) + j, u);
+                  }
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i)
+                    if (col0 + i < p.N) o[i] = (uint16_t)(pack2<BF16>((float)w[i], 0.f) & 0xffffu);
+                }
+              }
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            named_bar_sync(2, 128);
+            if (warp == 2 && lane == 0) {
+              if (!skip) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                        reinterpret_cast<uint64_t>(&tmB2)),
+                    "r"(m0), "r"(col0), "r"(smem_u32(sW + ws * C::W_BYTES))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+              // the previous round's store has finished reading its slot: hand it back
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              if (wround_e > 0) mbar_arrive(wempty0 + 8 * ((wround_e - 1) % C::W_SLOTS));
+            }
+          }
+          goto tile_done;
+        }
+        // W64 += alpha * D with the 16-bit shadow rewritten from the new value, 64 columns per
+        // round: the 64 master loads of a round are all in flight before the first is used
+        // (the kernel is HBM-latency-bound: 18 B per weight against 256 MMA FLOPs).  Every
+        // lane runs the TMEM loads (.sync.aligned); memory ops are guarded per row / column.
         const bool skip = p.upd_abort ? (*p.upd_abort != 0u)
                                       : !(isfinite(p.upd_out4[0]) && isfinite(p.upd_out4[1]));
         const double alpha = -(p.upd_lr * p.upd_out4[2]) * p.upd_scale;
+        const bool live = !skip && row_ok;
 #pragma unroll 1
-        for (int c = 0; c < bnc; c += 32) {
-          float v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+        for (int c = 0; c < bnc; c += 64) {
           const int col0 = n0 + c;
-          if (skip || !row_ok || col0 >= p.N) continue;
-          const int nc = min(32, p.N - col0);
-          double w[32];
-          if (p.upd_transposed) {
-            // row = output index j, columns = input indices i: W64[i][j] -- one 256-byte
-            // row segment per column across the warp's 32 consecutive rows
-            const double* src = p.upd_w64 + (size_t)col0 * p.upd_ld64 + row;
+          const int nc = live ? max(0, min(64, p.N - col0)) : 0;
+          double w[64];
+          const size_t base = p.upd_transposed ? (size_t)col0 * p.upd_ld64 + row : (size_t)row * p.upd_ld64 + col0;
+          const size_t step = p.upd_transposed ? (size_t)p.upd_ld64 : 1;
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i < nc) w[i] = __ldcs(p.upd_w64 + base + (size_t)i * step);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float v[32];
+            if (c + 32 * h < bnc)
+              tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c + 32 * h, v);
 #pragma unroll
             for (int i = 0; i < 32; ++i)
-              if (i < nc) w[i] = src[(size_t)i * p.upd_ld64];
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < nc) {
-                w[i] = fma(alpha, (double)v[i], w[i]);
-                p.upd_w64[(size_t)(col0 + i) * p.upd_ld64 + row] = w[i];
-              }
-          } else {
-            double* src = p.upd_w64 + (size_t)row * p.upd_ld64 + col0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < nc) w[i] = src[i];
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < nc) {
-                w[i] = fma(alpha, (double)v[i], w[i]);
-                src[i] = w[i];
+              if (32 * h + i < nc) {
+                w[32 * h + i] = fma(alpha, (double)v[i], w[32 * h + i]);
+                __stcs(p.upd_w64 + base + (size_t)(32 * h + i) * step, w[32 * h + i]);
               }
           }
+          if (nc == 0) continue;
           uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)row * p.upd_ld16 + col0;
-          if (nc == 32 && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
-            uint32_t pk[16];
+          if (nc == 64 && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) pk[j] = pack2<BF16>((float)w[2 * j], (float)w[2 * j + 1]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-              reinterpret_cast<uint4*>(o)[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
-          } else {
-            for (int i = 0; i < nc; ++i) {
-              const uint32_t pk = pack2<BF16>((float)w[i], 0.f);
-              o[i] = (uint16_t)(pk & 0xffffu);
+            for (int j = 0; j < 8; ++j) {
+              uint4 u;
+              u.x = pack2<BF16>((float)w[8 * j], (float)w[8 * j + 1]);
+              u.y = pack2<BF16>((float)w[8 * j + 2], (float)w[8 * j + 3]);
+              u.z = pack2<BF16>((float)w[8 * j + 4], (float)w[8 * j + 5]);
+              u.w = pack2<BF16>((float)w[8 * j + 6], (float)w[8 * j + 7]);
+              __stcs(reinterpret_cast<uint4*>(o) + j, u);
             }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 64; ++i)
+              if (i < nc) o[i] = (uint16_t)(pack2<BF16>((float)w[i], 0.f) & 0xffffu);
           }
         }
         goto tile_done;
@@ -772,6 +859,8 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   }
+  if constexpr (EPI == EPI_UPDATE64)
+    if (wtma && warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();
   if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/epilogues are done before TMEM is freed
@@ -819,6 +908,23 @@ void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t co
     throw Error(ZO_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ") rows=" +
                                  std::to_string(rows) + " cols=" + std::to_string(cols) + " ld=" +
                                  std::to_string(ld));
+}
+
+void gemm_set_update_master(GemmDesc& g) {
+  // EPI_UPDATE64 on a projection: a float64 map over the master W64 [N (inputs), M (outputs)]
+  // (row stride upd_ld64), 32 x 128 boxes, no swizzle -- streamed through the kernel's
+  // master-block ring in place of the half-tile B map
+  if (g.epi != EPI_UPDATE64 || !g.upd_transposed) return;
+  if (g.cg != 1 && g.cg != 2) throw Error(ZO_ERR_INTERNAL, "bad CTA group");
+  if (g.bn % 32 || g.half_n || g.sk) throw Error(ZO_ERR_INTERNAL, "update GEMM: plain tiles only");
+  cuuint64_t dims[2] = {(cuuint64_t)g.M, (cuuint64_t)g.N};
+  cuuint64_t strides[1] = {(cuuint64_t)g.upd_ld64 * 8};
+  cuuint32_t box[2] = {128, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode()(&g.tmB2, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, g.upd_w64, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(ZO_ERR_CUDA, "cuTensorMapEncodeTiled (float64 master) failed");
 }
 
 void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used, int epi,
@@ -888,7 +994,7 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms) {
 
 template <int BN, int EPI, int BF16, int XR, int CG>
 static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = -1, int last_ksteps = -1) {
-  using C = GemmCfg<BN, CG>;
+  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE64>;
   static bool attr_set = false;
   if (!attr_set) {
     ZO_CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI, BF16, XR, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,

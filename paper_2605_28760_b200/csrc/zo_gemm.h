@@ -79,5 +79,8 @@ void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t co
 void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used,
                int epi, int dtype, void* out, int ldo, int num_sms);
 void gemm_launch(const GemmDesc& g, cudaStream_t st);
+// EPI_UPDATE64 on a projection (upd_transposed): after gemm_plan and the upd_* fields, build the
+// float64 master map the kernel streams W64 blocks through (TMA load -> update -> TMA store)
+void gemm_set_update_master(GemmDesc& g);
 
 }  // namespace zo

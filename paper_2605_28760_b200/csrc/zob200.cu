@@ -633,6 +633,7 @@ void launch_dense_update_dev(zo_ctx* c, double lr) {
         g.upd_lr = lr;
         g.upd_scale = 1.0 / std::sqrt((double)c->r);
         g.upd_abort = c->abort_flag;
+        gemm_set_update_master(g);
       }
     }
     for (size_t i = 0; i < c->mats.size(); ++i) {
