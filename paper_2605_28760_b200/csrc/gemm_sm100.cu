@@ -238,6 +238,10 @@ struct GemmParams {
   float* sk_ws;
   unsigned* sk_flags;
   int half_dp, half_n;  // half-width tail tiles (see zo_gemm.h)
+  // split-K (gemm_enable_splitk): CTA u computes k-blocks [s*kchunk, +kchunk) of tile u % tiles,
+  // s = u / tiles, and stores its fp32 partial at out + s * split_stride (EPI_STORE32)
+  int ksplit, kchunk;
+  long split_stride;
   unsigned long long* trace;  // diagnostic timeline (see zo_gemm.h), nullptr in production
   // per-column bias (OPT arch; see zo_gemm.h) and the ReLU activation of EPI_GELU16*
   const float* bias;
@@ -268,8 +272,19 @@ struct SegIter {
     step = gridDim.x / cg;
     const int tiles = p.m_tiles * p.n_tiles;
     hi = p.sk ? p.sk_dp : p.half_n ? p.half_dp + 2 * (tiles - p.half_dp) : tiles;
+    if (p.ksplit) hi = 1;  // one (tile, k-chunk) segment per CTA
   }
   __device__ __forceinline__ bool next(const GemmParams& p, int& tile, int& k0, int& k1) {
+    if (p.ksplit) {
+      if (cursor >= hi) return false;
+      const int tiles = p.m_tiles * p.n_tiles;
+      tile = unit % tiles;
+      k0 = (unit / tiles) * p.kchunk;
+      k1 = min(p.num_kb, k0 + p.kchunk);
+      hf = 0;
+      cursor = hi;
+      return true;
+    }
     if (dp) {
       if (cursor < hi) {
         if (p.half_n && cursor >= p.half_dp) {
@@ -501,7 +516,7 @@ __global__ void __launch_bounds__(192, 1)
       if (tr && warp == 2 && lane == 0 && it < 15) tr[32 + 2 * it] = globaltimer();
       const int row = m0 + erow;
       const bool row_ok = row < p.M;
-      if (k0 > 0) {
+      if (k0 > 0 && !p.ksplit) {
         // not the tile's first k-block: publish the raw fp32 partial for the owner
         // [BN/4][128 rows] float4 layout: the 32 lanes of a store write 512 contiguous bytes
         float4* ws = reinterpret_cast<float4*>(p.sk_ws + (size_t)blockIdx.x * C::BM * BN) + erow;
@@ -530,7 +545,7 @@ __global__ void __launch_bounds__(192, 1)
       // by units si.unit+1 .. jend-1; their segments are their FIRST tail segments, so
       // no unit's publication waits on another's (no dependency chains)
       int jfirst = si.unit + 1, jend = si.unit + 1;
-      if (k1 < p.num_kb) jend = ((t + 1) * p.num_kb - 1 - p.sk_dp * p.num_kb) / p.sk_w + 1;
+      if (k1 < p.num_kb && !p.ksplit) jend = ((t + 1) * p.num_kb - 1 - p.sk_dp * p.num_kb) / p.sk_w + 1;
       const bool split = jfirst < jend;
       if (split) {
         // one lane per warp polls (with backoff, so the spinning owners do not hammer the
@@ -805,7 +820,8 @@ __global__ void __launch_bounds__(192, 1)
               if (col0 + i < p.N) o[i] = (uint16_t)(pk[i >> 1] >> (16 * (i & 1)));
           }
         } else {
-          float* o = reinterpret_cast<float*>(p.out) + lin;
+          float* o = reinterpret_cast<float*>(p.out) + lin +
+                     (p.ksplit ? (size_t)(k0 / p.kchunk) * (size_t)p.split_stride : (size_t)0);
           if (full) {
             float4 xr4[8];
             if constexpr (EPI == EPI_RESID32) {
@@ -1029,6 +1045,9 @@ static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = 
   p.bias_rps = g.bias_rps;
   p.bias_vstride = g.bias_vstride;
   p.relu = g.relu;
+  p.ksplit = g.ksplit;
+  p.kchunk = g.kchunk;
+  p.split_stride = g.split_stride;
   p.upd_w64 = g.upd_w64;
   p.upd_w16 = g.upd_w16;
   p.upd_ld64 = g.upd_ld64;
@@ -1162,6 +1181,20 @@ void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
   g.sk_ws = ws;
   g.sk_flags = flags;
   g.grid = units * cg;
+}
+
+int gemm_enable_splitk(GemmDesc& g, int splits, long split_stride) {
+  if (g.cg != 1 || g.epi != EPI_STORE32 || g.bf16 == 2) throw Error(ZO_ERR_INTERNAL, "split-K: fp32 single-CTA tiles only");
+  const int kc = std::max(1, (g.num_kb + splits - 1) / splits);
+  const int s = (g.num_kb + kc - 1) / kc;
+  const int tiles = ((g.M + 127) / 128) * ((g.N + g.bn - 1) / g.bn);
+  g.ksplit = s;
+  g.kchunk = kc;
+  g.split_stride = split_stride;
+  g.grid = tiles * s;
+  g.sk = 0;
+  g.half_n = 0;
+  return s;
 }
 
 void gemm_launch(const GemmDesc& g, cudaStream_t st) {

@@ -58,6 +58,9 @@ struct GemmDesc {
   unsigned long long* trace = nullptr;
   // half-width tail: tiles [half_dp, tiles) run as two N/2-wide tiles each (half_n = 1)
   int half_dp = 0, half_n = 0;
+  // split-K (gemm_enable_splitk): non-persistent, one (tile, k-chunk) per CTA, fp32 partials
+  int ksplit = 0, kchunk = 0;
+  long split_stride = 0;
   // stream-K split of the k-iteration space over the persistent CTAs (gemm_enable_streamk)
   int sk = 0, sk_w = 0, sk_dp = 0;
   float* sk_ws = nullptr;       // [grid][128][bn] fp32 partials of split tiles
@@ -79,6 +82,10 @@ void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t co
 void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used,
                int epi, int dtype, void* out, int ldo, int num_sms);
 void gemm_launch(const GemmDesc& g, cudaStream_t st);
+// skinny GEMMs (few output tiles, long K -- the high-rank LoRA-extension t = a . P): split K over
+// `splits` CTAs per tile; partial s lands at out + s * split_stride (EPI_STORE32), summed by the
+// caller in a fixed order.  Returns the number of splits used.
+int gemm_enable_splitk(GemmDesc& g, int splits, long split_stride);
 // EPI_UPDATE64 on a projection (upd_transposed): after gemm_plan and the upd_* fields, build the
 // float64 master map the kernel streams W64 blocks through (TMA load -> update -> TMA store)
 void gemm_set_update_master(GemmDesc& g);

@@ -53,8 +53,11 @@ struct Matrix {
 struct LayerPlan {
   GemmDesc qkv, out, up, down;
   // high-rank (r > 8) tensor-core extension t = a . P_s per GEMM input and probe sign:
-  // [qkv-in, out-in, up-in, down-in] x [sign]
+  // [qkv-in, out-in, up-in, down-in] x [sign]; split-K GEMMs into the fp32 workspace xws,
+  // reduced in a fixed order into the activation's extension columns (ext_a / ext_ld / ext_K)
   std::vector<GemmDesc> ext;
+  std::vector<void*> ext_a;
+  std::vector<int> ext_ld, ext_K, ext_M;
 };
 // real32 (3xTF32) scorer plan: the four projections of every layer + the LM head
 struct RowPlan32 {
@@ -167,6 +170,7 @@ struct zo_ctx {
   std::map<int, RowPlan> plans;  // keyed by 2*M + (nsign == 1)
   float* tpart = nullptr;         // fused LoRA-extension partials [tiles][Mpad][r]
   uint16_t* P16T = nullptr;       // high-rank extension B operands [2][su] (per matrix [r][m])
+  float* xws = nullptr;           // high-rank extension split-K partials [num_sms][Mpad][r]
   float* sk_ws = nullptr;         // stream-K partial tiles
   unsigned* sk_flags = nullptr;
   bool streamk = true;  // DP waves + stream-K tail where it pays (ZO_STREAMK=0 disables)
@@ -323,11 +327,23 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
       void* acts[4] = {c->hA, c->ctxA, c->hA, c->gA};
       const int lds[4] = {ldh, ldh, ldh, ldg};
       lp.ext.resize(8);
+      lp.ext_a.resize(8);
+      lp.ext_ld.resize(8);
+      lp.ext_K.resize(8);
+      lp.ext_M.resize(8);
       for (int i = 0; i < 4; ++i)
         for (int sg = 0; sg < nsign; ++sg) {
           uint16_t* a = static_cast<uint16_t*>(acts[i]) + (size_t)sg * rps * lds[i];
-          gemm_plan(lp.ext[2 * i + sg], a, rps, lds[i], c->P16T + (size_t)sg * c->su + mm[i]->u_off, c->r,
-                    (int)mm[i]->m, (int)mm[i]->m, EPI_STORE16, c->bf16, a + mm[i]->m, lds[i], c->num_sms);
+          GemmDesc& g = lp.ext[2 * i + sg];
+          // t = a . P_s: a few output tiles over K = 5120 .. 20480 -- split K so every SM works
+          gemm_plan(g, a, rps, lds[i], c->P16T + (size_t)sg * c->su + mm[i]->u_off, c->r, (int)mm[i]->m,
+                    (int)mm[i]->m, EPI_STORE32, c->bf16, c->xws, c->r, c->num_sms);
+          const int tiles = ((rps + 127) / 128) * ((c->r + g.bn - 1) / g.bn);
+          gemm_enable_splitk(g, std::max(1, c->num_sms / tiles), (long)c->Mpad * c->r);
+          lp.ext_a[2 * i + sg] = a;
+          lp.ext_ld[2 * i + sg] = lds[i];
+          lp.ext_K[2 * i + sg] = (int)mm[i]->m;
+          lp.ext_M[2 * i + sg] = rps;
         }
     }
     rp.layers.push_back(lp);
@@ -506,7 +522,12 @@ void do_score(zo_ctx* c, int B, int nsign) {
       if (nsign == 2) launch_p16t(c->Pm + m.u_off, (int)m.m, c->r, c->P16T + c->su + m.u_off, c->bf16, c->st);
     }
   auto ext_gemm = [&](const LayerPlan& lp, int i) {
-    for (int sg = 0; sg < nsign; ++sg) gemm_launch(lp.ext[2 * i + sg], c->st);
+    for (int sg = 0; sg < nsign; ++sg) {
+      const int j = 2 * i + sg;
+      gemm_launch(lp.ext[j], c->st);
+      launch_ext_finalize(c->xws, lp.ext[j].ksplit, c->Mpad, lp.ext_M[j], c->r, lp.ext_a[j], lp.ext_ld[j],
+                          lp.ext_K[j], 1, c->bf16, c->st);
+    }
   };
   for (int l = 0; l < c->d.n_layers; ++l) {
     const Matrix& q = c->mats[c->i_qkv[l]];
@@ -927,7 +948,10 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->fused_ext = d.rank <= 8;
   c->tpart_tiles = std::max((int)ceil_div(4 * D, 64), d.n_heads);
   if (c->fused_ext) c->tpart = c->mem.get<float>((size_t)c->tpart_tiles * c->Mpad * d.rank);
-  else c->P16T = c->mem.get<uint16_t>((size_t)2 * c->su);
+  else {
+    c->P16T = c->mem.get<uint16_t>((size_t)2 * c->su);
+    c->xws = c->mem.get<float>((size_t)c->num_sms * c->Mpad * d.rank);
+  }
   // positional table: pos_encoding(T, d) (model.py:128-136), float64 -> float32
   {
     std::vector<float> pe((size_t)c->T * d.dim);
