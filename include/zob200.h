@@ -149,6 +149,13 @@ int zo_update_dense(zo_ctx* ctx, double lr);
  * into the float64-master / 16-bit-shadow read-modify-write, HBM-bound; parameters then agree
  * with the reference to ~1e-3 of each step's update, not bit for bit.  rank >= 16, % 16 == 0. */
 int zo_set_update_mode(zo_ctx* ctx, int32_t mode);
+/* GEMM schedule: 0 = fastest (data-parallel waves + a stream-K tail where it pays; the
+ * tail's fp32 partial sums make a row's rounding depend on the per-GPU row count M);
+ * 1 = row-invariant (no stream-K: every output element is one in-order tcgen05 K
+ * accumulation whatever M, tile width or CTA pairing) -- the per-example NLLs of a
+ * sequence are then bitwise independent of how the batch is sliced over GPUs
+ * (multi-GPU exact mode sets it on every rank). */
+int zo_set_schedule(zo_ctx* ctx, int32_t row_invariant);
 /* full scope: every 1-D param p += (-(lr*c)) z with the installed c (VectorProbe.update,
  * zo_engine.py:290-295, 412-416); no-op for lora_only.  zo_update_dense applies it too. */
 int zo_update_vectors(zo_ctx* ctx, double lr);

@@ -210,10 +210,12 @@ struct GemmCfg {
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // EPI_UPDATE64: a short operand ring (K = rank) and a ring of float64 master blocks
-  // [32 rows][128 cols] streamed in and out by TMA (W_SLOTS x 32 KB)
-  static constexpr int W_SLOTS = UPD ? 3 : 0;
+  // [32 rows][128 cols] streamed in and out by TMA: W_SLOTS x 32 KB for a float64 master, or
+  // 2 W_SLOTS x 16 KB for an fp32 master (the ring is latency-bound: twice the blocks in flight)
+  static constexpr int W_SLOTS = UPD ? 4 : 0;
+  static constexpr int W_NBAR = 2 * W_SLOTS;  // barrier pairs (the fp32 ring's slot count)
   static constexpr int W_BYTES = 32 * BM * 8;
-  static constexpr int STAGES = UPD ? 3 : ((196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES);
+  static constexpr int STAGES = UPD ? 2 : ((196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + W_SLOTS * W_BYTES + 512;
 };
@@ -252,6 +254,7 @@ struct GemmParams {
   double* upd_w64;
   void* upd_w16;
   int upd_ld64, upd_ld16, upd_transposed;
+  int upd_m32;  // the master holds fp32 values (zo_set_update_mode 1): half the master bytes
   const double* upd_out4;
   double upd_lr, upd_scale;
   const unsigned* upd_abort;
@@ -347,10 +350,13 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sW = smem + C::STAGES * C::STAGE_BYTES;  // EPI_UPDATE64 master-block ring
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + C::W_SLOTS * C::W_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4 + 2 * C::W_SLOTS);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4 + 2 * C::W_NBAR);
   // TMA-streamed master update (EPI_UPDATE64 on a projection): W64 blocks in/out through sW
   const bool wtma = (EPI == EPI_UPDATE64) && p.upd_transposed;
-  const uint32_t wfull0 = smem_u32(bars + 2 * C::STAGES + 4), wempty0 = wfull0 + 8 * C::W_SLOTS;
+  const uint32_t wfull0 = smem_u32(bars + 2 * C::STAGES + 4), wempty0 = wfull0 + 8 * C::W_NBAR;
+  // master-block ring geometry: fp32 masters use twice the slots at half the size
+  const int wslots = (EPI == EPI_UPDATE64 && p.upd_m32) ? C::W_NBAR : C::W_SLOTS;
+  const uint32_t wbytes = (EPI == EPI_UPDATE64 && p.upd_m32) ? C::W_BYTES / 2 : C::W_BYTES;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = smem_u32(bars + 2 * C::STAGES + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -368,7 +374,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, 4 * CG);  // every epilogue warp of the pair arrives at the leader
     }
-    for (int w = 0; w < C::W_SLOTS; ++w) {
+    for (int w = 0; w < C::W_NBAR; ++w) {
       mbar_init(wfull0 + 8 * w, 1);
       mbar_init(wempty0 + 8 * w, 1);
     }
@@ -440,10 +446,10 @@ __global__ void __launch_bounds__(192, 1)
             const int j0 = (t % p.m_tiles) * (C::BM * CG) + (int)rank * C::BM;
             const int i0 = (t / p.m_tiles) * BN;
             for (int r = 0; r < BN / 32; ++r, ++wround) {
-              const int ws = wround % C::W_SLOTS;
-              mbar_wait(wempty0 + 8 * ws, ((wround / C::W_SLOTS) & 1) ^ 1);
-              mbar_arrive_expect_tx(wfull0 + 8 * ws, C::W_BYTES);
-              tma_load_2d(smem_u32(sW + ws * C::W_BYTES), &tmB2, wfull0 + 8 * ws, j0, i0 + 32 * r);
+              const int ws = wround % wslots;
+              mbar_wait(wempty0 + 8 * ws, ((wround / wslots) & 1) ^ 1);
+              mbar_arrive_expect_tx(wfull0 + 8 * ws, wbytes);
+              tma_load_2d(smem_u32(sW + ws * wbytes), &tmB2, wfull0 + 8 * ws, j0, i0 + 32 * r);
             }
           }
         }
@@ -627,20 +633,31 @@ __global__ void __launch_bounds__(192, 1)
           const double alpha = -(p.upd_lr * p.upd_out4[2]) * p.upd_scale;
 #pragma unroll 1
           for (int r = 0; r < BN / 32; ++r, ++wround_e) {
-            const int ws = wround_e % C::W_SLOTS;
+            const int ws = wround_e % wslots;
             float v[32];
             tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + 32 * r, v);
-            mbar_wait(wfull0 + 8 * ws, (wround_e / C::W_SLOTS) & 1);
-            double* blk = reinterpret_cast<double*>(sW + ws * C::W_BYTES) + erow;  // column erow
+            mbar_wait(wfull0 + 8 * ws, (wround_e / wslots) & 1);
+            double* blk = reinterpret_cast<double*>(sW + ws * wbytes) + erow;  // column erow
+            float* blk32 = reinterpret_cast<float*>(sW + ws * wbytes) + erow;  // fp32 master
             const int col0 = n0 + 32 * r;
             if (!skip) {
               double w[32];
+              if (p.upd_m32) {
 #pragma unroll
-              for (int i = 0; i < 32; ++i) w[i] = blk[i * C::BM];
+                for (int i = 0; i < 32; ++i) w[i] = (double)blk32[i * C::BM];
 #pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                w[i] = fma(alpha, (double)v[i], w[i]);
-                blk[i * C::BM] = w[i];
+                for (int i = 0; i < 32; ++i) {
+                  w[i] = (double)(float)fma(alpha, (double)v[i], w[i]);
+                  blk32[i * C::BM] = (float)w[i];
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) w[i] = blk[i * C::BM];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                  w[i] = fma(alpha, (double)v[i], w[i]);
+                  blk[i * C::BM] = w[i];
+                }
               }
               if (row_ok && col0 < p.N) {
                 uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)row * p.upd_ld16 + col0;
@@ -668,13 +685,13 @@ __global__ void __launch_bounds__(192, 1)
                 asm volatile(
                     "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                         reinterpret_cast<uint64_t>(&tmB2)),
-                    "r"(m0), "r"(col0), "r"(smem_u32(sW + ws * C::W_BYTES))
+                    "r"(m0), "r"(col0), "r"(smem_u32(sW + ws * wbytes))
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
               }
               // the previous round's store has finished reading its slot: hand it back
               asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-              if (wround_e > 0) mbar_arrive(wempty0 + 8 * ((wround_e - 1) % C::W_SLOTS));
+              if (wround_e > 0) mbar_arrive(wempty0 + 8 * ((wround_e - 1) % wslots));
             }
           }
           goto tile_done;
@@ -694,9 +711,11 @@ __global__ void __launch_bounds__(192, 1)
           double w[64];
           const size_t base = p.upd_transposed ? (size_t)col0 * p.upd_ld64 + row : (size_t)row * p.upd_ld64 + col0;
           const size_t step = p.upd_transposed ? (size_t)p.upd_ld64 : 1;
+          float* w32p = reinterpret_cast<float*>(p.upd_w64);
 #pragma unroll
           for (int i = 0; i < 64; ++i)
-            if (i < nc) w[i] = __ldcs(p.upd_w64 + base + (size_t)i * step);
+            if (i < nc)
+              w[i] = p.upd_m32 ? (double)__ldcs(w32p + base + (size_t)i * step) : __ldcs(p.upd_w64 + base + (size_t)i * step);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             float v[32];
@@ -706,7 +725,12 @@ __global__ void __launch_bounds__(192, 1)
             for (int i = 0; i < 32; ++i)
               if (32 * h + i < nc) {
                 w[32 * h + i] = fma(alpha, (double)v[i], w[32 * h + i]);
-                __stcs(p.upd_w64 + base + (size_t)(32 * h + i) * step, w[32 * h + i]);
+                if (p.upd_m32) {
+                  w[32 * h + i] = (double)(float)w[32 * h + i];
+                  __stcs(w32p + base + (size_t)(32 * h + i) * step, (float)w[32 * h + i]);
+                } else {
+                  __stcs(p.upd_w64 + base + (size_t)(32 * h + i) * step, w[32 * h + i]);
+                }
               }
           }
           if (nc == 0) continue;
@@ -934,10 +958,11 @@ void gemm_set_update_master(GemmDesc& g) {
   if (g.cg != 1 && g.cg != 2) throw Error(ZO_ERR_INTERNAL, "bad CTA group");
   if (g.bn % 32 || g.half_n || g.sk) throw Error(ZO_ERR_INTERNAL, "update GEMM: plain tiles only");
   cuuint64_t dims[2] = {(cuuint64_t)g.M, (cuuint64_t)g.N};
-  cuuint64_t strides[1] = {(cuuint64_t)g.upd_ld64 * 8};
+  cuuint64_t strides[1] = {(cuuint64_t)g.upd_ld64 * (g.upd_m32 ? 4 : 8)};
   cuuint32_t box[2] = {128, 32};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = get_encode()(&g.tmB2, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, g.upd_w64, dims, strides, box, estr,
+  CUresult r = get_encode()(&g.tmB2, g.upd_m32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                            g.upd_w64, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(ZO_ERR_CUDA, "cuTensorMapEncodeTiled (float64 master) failed");
@@ -1053,6 +1078,7 @@ static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = 
   p.upd_ld64 = g.upd_ld64;
   p.upd_ld16 = g.upd_ld16;
   p.upd_transposed = g.upd_transposed;
+  p.upd_m32 = g.upd_m32;
   p.upd_out4 = g.upd_out4;
   p.upd_lr = g.upd_lr;
   p.upd_scale = g.upd_scale;

@@ -11,16 +11,19 @@
 // chunk splice:
 //   k_spec : every chunk of CH u64 positions is parsed as if an attempt started
 //            at its first position -> speculative exit (first attempt start at
-//            or past the chunk end).
-//   k_true : chunk c re-parses from the speculative exit of chunk c-1 (its
-//            candidate true entry) -> sample count and exit.  Attempt chains
-//            started at different positions merge within a few attempts
-//            (SURVEY.md App. A.7), so this exit equals the speculative one
-//            except with vanishing probability.
-//   k_scan : one CTA per stream verifies the splice (exit[c-1] == spec[c-1]),
-//            repairs any broken link serially, and scans counts -> offsets.
+//            or past the chunk end), sample count, and which of the chunk's
+//            first 8 positions start an attempt / yield a sample.
+//   k_scan : one CTA per stream.  Chunk c's true entry is chunk c-1's exit
+//            (a few positions into c at most).  When that entry is one of the
+//            speculative attempt starts the two parses are the same chain from
+//            there on: the true count is the speculative
+//            count minus the samples of the skipped attempts, the exit is the
+//            speculative exit -- no second Philox pass.  Otherwise (~2e-4 of
+//            chunks) the chunk is re-parsed from its entry; a re-parse whose exit
+//            differs breaks the splice and the rest of the stream is repaired
+//            serially (never observed; counted).  Then counts -> offsets.
 //   k_emit : re-parse from the verified entry and write samples in place.
-// Every step is exact; the repair path keeps it exact even when a merge fails.
+// Philox runs twice per sample (spec + emit); every step is exact.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -214,7 +217,8 @@ __global__ void k_keys(const StreamDesc* __restrict__ streams, int S, uint64_t s
 __global__ void __launch_bounds__(256) k_spec(const StreamDesc* __restrict__ streams,
                                               const uint32_t* __restrict__ chunk_stream, int64_t C,
                                               const uint64_t* __restrict__ keys,
-                                              uint64_t* __restrict__ spec_exit, unsigned* flags) {
+                                              uint64_t* __restrict__ spec_exit, uint32_t* __restrict__ count,
+                                              unsigned* flags) {
   __shared__ uint64_t ki[256];
   __shared__ double wi[256], fi[256];
   Zig z;
@@ -226,35 +230,19 @@ __global__ void __launch_bounds__(256) k_spec(const StreamDesc* __restrict__ str
   uint64_t beg = local * CH, end = beg + CH;
   Parser p;
   p.init(keys[2 * s], keys[2 * s + 1], beg);
-  unsigned amb = 0;
+  unsigned amb = 0, n = 0, starts = 0, yields = 0;
   double x;
-  while (p.pos < end) p.attempt(z, &x, &amb);
+  while (p.pos < end) {
+    const uint64_t at = p.pos - beg;
+    const bool y = p.attempt(z, &x, &amb);
+    n += y ? 1u : 0u;
+    if (at < 8) {
+      starts |= 1u << at;
+      yields |= (y ? 1u : 0u) << at;
+    }
+  }
   spec_exit[c] = p.pos;
-}
-
-__global__ void __launch_bounds__(256) k_true(const StreamDesc* __restrict__ streams,
-                                              const uint32_t* __restrict__ chunk_stream, int64_t C,
-                                              const uint64_t* __restrict__ keys,
-                                              const uint64_t* __restrict__ spec_exit,
-                                              uint64_t* __restrict__ exit_pos, uint32_t* __restrict__ count,
-                                              unsigned* flags) {
-  __shared__ uint64_t ki[256];
-  __shared__ double wi[256], fi[256];
-  Zig z;
-  load_tables(z, ki, wi, fi);
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  uint32_t s = chunk_stream[c];
-  uint64_t local = (uint64_t)(c - (int64_t)streams[s].chunk_begin);
-  uint64_t end = (local + 1) * CH;
-  uint64_t entry = local == 0 ? 0 : spec_exit[c - 1];
-  Parser p;
-  p.init(keys[2 * s], keys[2 * s + 1], entry);
-  unsigned amb = 0, n = 0;
-  double x;
-  while (p.pos < end) n += p.attempt(z, &x, &amb) ? 1u : 0u;
-  exit_pos[c] = p.pos;
-  count[c] = n;
+  count[c] = n | (starts << 16) | (yields << 24);
 }
 
 // One CTA per stream: verify/repair the splice, exclusive-scan the counts.
@@ -274,9 +262,32 @@ __global__ void __launch_bounds__(1024) k_scan(const StreamDesc* __restrict__ st
   const int64_t cb = (int64_t)d.chunk_begin, nc = (int64_t)d.n_chunks;
   if (threadIdx.x == 0) first_bad = nc;
   __syncthreads();
-  // chunk c (local >= 1) used entry spec_exit[c-1]; valid iff exit_pos[c-1] matches.
-  for (int64_t i = 1 + threadIdx.x; i < nc; i += blockDim.x)
-    if (exit_pos[cb + i - 1] != spec_exit[cb + i - 1]) atomicMin((unsigned long long*)&first_bad, (unsigned long long)i);
+  // true entry of chunk i = exit of chunk i-1 (= its speculative exit unless a re-parse
+  // below changed it, which breaks the splice at i+1 and sends the rest to the repair)
+  for (int64_t i = threadIdx.x; i < nc; i += blockDim.x) {
+    const uint32_t raw = count[cb + i];
+    uint32_t n = raw & 0xffffu;
+    uint64_t ex = spec_exit[cb + i];
+    if (i > 0) {
+      const uint64_t off = spec_exit[cb + i - 1] - (uint64_t)i * CH;
+      const uint32_t starts = (raw >> 16) & 0xffu, yields = raw >> 24;
+      if (off < 8 && ((starts >> off) & 1u)) {
+        n -= (uint32_t)__popc(yields & ((1u << off) - 1u));
+      } else {  // the entry falls inside a speculative attempt: re-parse this chunk
+        Parser p;
+        p.init(keys[2 * blockIdx.x], keys[2 * blockIdx.x + 1], spec_exit[cb + i - 1]);
+        const uint64_t end = (uint64_t)(i + 1) * CH;
+        unsigned amb = 0;
+        double x;
+        n = 0;
+        while (p.pos < end) n += p.attempt(z, &x, &amb) ? 1u : 0u;
+        if (p.pos != ex) atomicMin((unsigned long long*)&first_bad, (unsigned long long)(i + 1));
+        ex = p.pos;
+      }
+    }
+    count[cb + i] = n;
+    exit_pos[cb + i] = ex;
+  }
   __syncthreads();
   if (first_bad < nc && threadIdx.x == 0) {
     // serial repair (vanishingly rare): re-parse every chunk after the break
@@ -371,9 +382,7 @@ void sampler_launch(const SamplerPlan& P, uint64_t seed, const uint64_t* d_step,
   if (P.S == 0) return;
   k_keys<<<(P.S + 127) / 128, 128, 0, st>>>(P.d_streams, P.S, seed, d_step, nu, P.d_keys);
   unsigned grid = (unsigned)((P.C + 255) / 256);
-  k_spec<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_spec, P.d_flags);
-  k_true<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_spec, P.d_exit, P.d_count,
-                               P.d_flags);
+  k_spec<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_spec, P.d_count, P.d_flags);
   k_scan<<<P.S, 1024, 0, st>>>(P.d_streams, P.d_keys, P.d_spec, P.d_exit, P.d_count, P.d_offset, P.d_flags);
   k_emit<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_exit, P.d_offset, out,
                                P.d_flags);

@@ -88,32 +88,56 @@ __device__ __forceinline__ void write_ext(void* out, size_t base, int k, float t
 }
 
 // ------------------------------------------------------------------ fused-extension finalize
-// one warp per (row, k): lanes stride over the tiles, then a fixed xor-shuffle tree
-// (deterministic; independent of scheduling)
+// t[row, k] = sum over tiles j of tpart[j][row][k].  A CTA of 256 threads owns PAIRS
+// consecutive (row, k) pairs x GROUPS tile groups: group g sums tiles g, g+GROUPS, ... in
+// ascending order (for a fixed tile the pairs are contiguous: coalesced), then the group
+// sums are added in group order.  GROUPS is chosen from the tile count alone (8 up to 16
+// tiles -- the high-rank split-K partials --, 32 above -- the fused GELU-epilogue / attention
+// partials), so the summation order depends on neither M nor the launch shape.
+template <int GROUPS>
 __global__ void __launch_bounds__(256) k_ext_finalize(const float* __restrict__ tpart, int ntiles, int ld, int M,
                                                       int r, void* __restrict__ a, int lda, int K, int ext_terms,
                                                       bool bf16) {
+  constexpr int PAIRS = 256 / GROUPS;
   pdl_launch_dependents();
   pdl_wait();
-  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (i >= M * r) return;
-  const int row = i / r, k = i % r;
+  __shared__ float part[GROUPS][PAIRS];
+  const int p = threadIdx.x % PAIRS, g = threadIdx.x / PAIRS;
+  const int64_t i = (int64_t)blockIdx.x * PAIRS + p;  // = row * r + k
+  const bool ok = i < (int64_t)M * r;
   float t = 0.f;
-  for (int j = lane; j < ntiles; j += 32) t += tpart[((size_t)j * ld + row) * r + k];
-  t = warp_sum(t);
-  if (lane == 0) write_ext(a, (size_t)row * lda + K, k, t, ext_terms, bf16);
+  if (ok) {
+    const float* src = tpart + i;
+    const size_t stride = (size_t)ld * r;
+#pragma unroll 4
+    for (int j = g; j < ntiles; j += GROUPS) t += src[(size_t)j * stride];
+  }
+  part[g][p] = t;
+  __syncthreads();
+  if (g == 0 && ok) {
+    float s = part[0][p];
+#pragma unroll
+    for (int q = 1; q < GROUPS; ++q) s += part[q][p];
+    const int row = (int)(i / r), k = (int)(i % r);
+    write_ext(a, (size_t)row * lda + K, k, s, ext_terms, bf16);
+  }
 }
 
 void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
                          int ext_terms, bool bf16, cudaStream_t st) {
-  launch_pdl(k_ext_finalize, dim3((M * r + 7) / 8), dim3(256), 0, st, tpart, ntiles, ld, M, r, a, lda, K, ext_terms, bf16);
+  const int64_t pairs = (int64_t)M * r;
+  if (ntiles <= 16)
+    launch_pdl(k_ext_finalize<8>, dim3((unsigned)((pairs + 31) / 32)), dim3(256), 0, st, tpart, ntiles, ld, M, r, a,
+               lda, K, ext_terms, bf16);
+  else
+    launch_pdl(k_ext_finalize<32>, dim3((unsigned)((pairs + 7) / 8)), dim3(256), 0, st, tpart, ntiles, ld, M, r, a,
+               lda, K, ext_terms, bf16);
 }
 
 // ------------------------------------------------------------------ embed
 __global__ void k_embed(float* __restrict__ x32, const int32_t* __restrict__ tokens, int tok_ld, int B, int T, int d,
-                        const double* __restrict__ E64, const void* __restrict__ E16, bool bf16,
-                        const float* __restrict__ Pp, const float* __restrict__ Pm, const float* __restrict__ Ve,
+                        const double* __restrict__ E64, const float* __restrict__ E32,
+                        const void* __restrict__ E16, bool bf16, const float* __restrict__ Pp, const float* __restrict__ Pm, const float* __restrict__ Ve,
                         int r, const float* __restrict__ pe, PosEmbed pos) {
   const int row = blockIdx.x;
   const int per_sign = B * T;
@@ -123,7 +147,7 @@ __global__ void k_embed(float* __restrict__ x32, const int32_t* __restrict__ tok
   const size_t prow = (size_t)(t + pos.offset);
   const float* PP = pos.W64 ? (s == 0 ? pos.Pp : pos.Pm) + prow * r : nullptr;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float e = E64 ? (float)E64[(size_t)tok * d + i] : ld16(E16, (size_t)tok * d + i, bf16);
+    float e = E64 ? (float)E64[(size_t)tok * d + i] : E32 ? E32[(size_t)tok * d + i] : ld16(E16, (size_t)tok * d + i, bf16);
     float delta = 0.f;
     for (int k = 0; k < r; ++k) delta += P[k] * Ve[(size_t)i * r + k];
     float pv;
@@ -138,10 +162,77 @@ __global__ void k_embed(float* __restrict__ x32, const int32_t* __restrict__ tok
   }
 }
 
+// High rank (r % 32 == 0): the delta P_s[tok] . V_e^T is a [rows x r] x [r x d] product --
+// a CTA computes 32 rows x 128 columns with 32-wide rank slices of P and V staged in
+// shared memory (V transposed, padded against bank conflicts), k ascending per element as
+// in k_embed.  The learned-position (OPT) form keeps k_embed.
+constexpr int EHR_ROWS = 32, EHR_COLS = 128, EHR_K = 32;
+__global__ void __launch_bounds__(EHR_COLS) k_embed_hr(float* __restrict__ x32, const int32_t* __restrict__ tokens,
+                                                       int tok_ld, int B, int T, int d,
+                                                       const double* __restrict__ E64, const float* __restrict__ E32,
+                                                       const void* __restrict__ E16, bool bf16,
+                                                       const float* __restrict__ Pp,
+                                                       const float* __restrict__ Pm, const float* __restrict__ Ve,
+                                                       int r, const float* __restrict__ pe, int nrows) {
+  __shared__ float Ps[EHR_ROWS][EHR_K];
+  __shared__ float Vs[EHR_K][EHR_COLS + 1];
+  __shared__ int toks[EHR_ROWS];
+  const int i = blockIdx.x * EHR_COLS + threadIdx.x;
+  const int row0 = blockIdx.y * EHR_ROWS;
+  const int per_sign = B * T;
+  if (threadIdx.x < EHR_ROWS) {
+    const int row = row0 + threadIdx.x;
+    int tk = 0;
+    if (row < nrows) {
+      const int rem = row % per_sign;
+      tk = tokens[(rem / T) * tok_ld + rem % T];
+    }
+    toks[threadIdx.x] = tk;
+  }
+  float acc[EHR_ROWS];
+#pragma unroll
+  for (int q = 0; q < EHR_ROWS; ++q) acc[q] = 0.f;
+  __syncthreads();
+  for (int k0 = 0; k0 < r; k0 += EHR_K) {
+    for (int e = threadIdx.x; e < EHR_ROWS * EHR_K; e += EHR_COLS) {
+      const int rr = e / EHR_K, kk = e % EHR_K, row = row0 + rr;
+      const float* P = (row < per_sign) ? Pp : Pm;
+      Ps[rr][kk] = row < nrows ? P[(size_t)toks[rr] * r + k0 + kk] : 0.f;
+    }
+    for (int e = threadIdx.x; e < EHR_COLS * EHR_K; e += EHR_COLS) {
+      const int c = e / EHR_K, kk = e % EHR_K, col = blockIdx.x * EHR_COLS + c;
+      Vs[kk][c] = col < d ? Ve[(size_t)col * r + k0 + kk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < EHR_K; ++kk) {
+      const float v = Vs[kk][threadIdx.x];
+#pragma unroll
+      for (int q = 0; q < EHR_ROWS; ++q) acc[q] += Ps[q][kk] * v;
+    }
+    __syncthreads();
+  }
+  if (i >= d) return;
+#pragma unroll
+  for (int q = 0; q < EHR_ROWS; ++q) {
+    const int row = row0 + q;
+    if (row >= nrows) break;
+    const int t = (row % per_sign) % T, tk = toks[q];
+    const float e = E64 ? (float)E64[(size_t)tk * d + i] : E32 ? E32[(size_t)tk * d + i] : ld16(E16, (size_t)tk * d + i, bf16);
+    x32[(size_t)row * d + i] = (e + acc[q]) + pe[(size_t)t * d + i];
+  }
+}
+
 void launch_embed(float* x32, const int32_t* tokens, int tok_ld, int B, int T, int d, const double* E64,
-                  const void* E16, bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r,
+                  const float* E32, const void* E16, bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r,
                   const float* pe, const PosEmbed& pos, int nrows, cudaStream_t st) {
-  k_embed<<<nrows, 256, 0, st>>>(x32, tokens, tok_ld, B, T, d, E64, E16, bf16, Pplus, Pminus, Ve32, r, pe, pos);
+  if (r > 8 && r % EHR_K == 0 && !pos.W64) {
+    const dim3 grid((unsigned)ceil_div(d, EHR_COLS), (unsigned)ceil_div(nrows, EHR_ROWS));
+    k_embed_hr<<<grid, EHR_COLS, 0, st>>>(x32, tokens, tok_ld, B, T, d, E64, E32, E16, bf16, Pplus, Pminus, Ve32, r, pe,
+                                          nrows);
+    return;
+  }
+  k_embed<<<nrows, 256, 0, st>>>(x32, tokens, tok_ld, B, T, d, E64, E32, E16, bf16, Pplus, Pminus, Ve32, r, pe, pos);
 }
 
 // ------------------------------------------------------------------ LN (+ extension), warp per row
@@ -519,135 +610,224 @@ void launch_gather_scored(const void* src, size_t ld_src_bytes, void* dst, size_
 }
 
 // ------------------------------------------------------------------ final LN at scored rows
-__global__ void k_final_ln(const float* __restrict__ x32, const float* __restrict__ g, const float* __restrict__ bta,
-                           int B, int T, int d, int prompt_len, int Lopt, float* __restrict__ xs32,
-                           void* __restrict__ xs16, bool bf16, const float* __restrict__ Ve, int r,
-                           float* __restrict__ z, int rows_per_sign, long vstride) {
+// One CTA (1024 threads) per scored row: float4 loads of the row into shared memory, the
+// two block reductions, xs32/xs16, then z = xs . V_e -- for r <= 8 every thread keeps r
+// partial dots over its columns; above that thread (k, group) sums column k over the rows
+// i = group mod G, G = 1024 / r (coalesced V_e reads), and the G group sums are added in
+// group order.
+constexpr int FLN_THREADS = 1024;
+__global__ void __launch_bounds__(FLN_THREADS) k_final_ln(const float* __restrict__ x32, const float* __restrict__ g,
+                                                         const float* __restrict__ bta, int B, int T, int d,
+                                                         int prompt_len, int Lopt, float* __restrict__ xs32,
+                                                         void* __restrict__ xs16, bool bf16,
+                                                         const float* __restrict__ Ve, int r, float* __restrict__ z,
+                                                         int rows_per_sign, long vstride) {
   extern __shared__ float sh[];
   float* row = sh;
-  float* red = sh + d;
+  float* red = sh + d;  // 32 * 8 floats, then (high rank) FLN_THREADS partial dots
   const int srow = blockIdx.x;
   const int s = srow / (B * Lopt), rem = srow % (B * Lopt), b = rem / Lopt, j = rem % Lopt;
   const int m = s * B * T + b * T + (prompt_len - 1 + j);
-  const float* x = x32 + (size_t)m * d;
   if (m >= rows_per_sign) {  // full scope: VectorProbe -1 copy of ln_f
     g += vstride;
     bta += vstride;
   }
+  const int n4 = d >> 2;
+  const float4* x4 = reinterpret_cast<const float4*>(x32 + (size_t)m * d);
+  float4* row4 = reinterpret_cast<float4*>(row);
   float acc[1] = {0.f};
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    row[i] = x[i];
-    acc[0] += row[i];
+#pragma unroll 4
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    const float4 v = x4[i];
+    row4[i] = v;
+    acc[0] += (v.x + v.y) + (v.z + v.w);
   }
   block_sum<1>(acc, red);
   const float mu = acc[0] / (float)d;
   acc[0] = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float c = row[i] - mu;
-    acc[0] += c * c;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    const float4 v = row4[i];
+    const float a = v.x - mu, c = v.y - mu, e = v.z - mu, f = v.w - mu;
+    acc[0] += (a * a + c * c) + (e * e + f * f);
   }
   block_sum<1>(acc, red);
   const float sd = sqrtf(acc[0] / (float)d + 1e-5f);
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float h = (row[i] - mu) / sd * g[i] + bta[i];
-    row[i] = h;
-    xs32[(size_t)srow * d + i] = h;
-    st16(xs16, (size_t)srow * d + i, h, bf16);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(bta);
+  float4* o32 = reinterpret_cast<float4*>(xs32 + (size_t)srow * d);
+#pragma unroll 4
+  for (int i = threadIdx.x; i < n4; i += blockDim.x) {
+    const float4 v = row4[i], gg = g4[i], bb = b4[i];
+    float4 h;
+    h.x = (v.x - mu) / sd * gg.x + bb.x;
+    h.y = (v.y - mu) / sd * gg.y + bb.y;
+    h.z = (v.z - mu) / sd * gg.z + bb.z;
+    h.w = (v.w - mu) / sd * gg.w + bb.w;
+    row4[i] = h;
+    o32[i] = h;
+    store4_16(xs16, (size_t)srow * d + 4 * i, h.x, h.y, h.z, h.w, bf16);
   }
   __syncthreads();
-  for (int k0 = 0; k0 < r; k0 += 8) {
-    float a8[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) a8[q] = 0.f;
-    const int kn = min(8, r - k0);
-    for (int i = threadIdx.x; i < d; i += blockDim.x)
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < kn) a8[q] += row[i] * Ve[(size_t)i * r + k0 + q];
-    block_sum<8>(a8, red);
-    if (threadIdx.x == 0)
-      for (int q = 0; q < kn; ++q) z[(size_t)srow * r + k0 + q] = a8[q];
+  if (r > 8) {
+    float* part = red + 32 * 8;
+    const int G = blockDim.x / r, k = threadIdx.x % r, grp = threadIdx.x / r;
+    float a = 0.f;
+    if (threadIdx.x < G * r) {
+#pragma unroll 8
+      for (int i = grp; i < d; i += G) a += row[i] * Ve[(size_t)i * r + k];
+    }
+    part[threadIdx.x] = a;
+    __syncthreads();
+    if (threadIdx.x < r) {
+      float t = part[threadIdx.x];
+      for (int q = 1; q < G; ++q) t += part[q * r + threadIdx.x];
+      z[(size_t)srow * r + threadIdx.x] = t;
+    }
+    return;
   }
+  float a8[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) a8[q] = 0.f;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < d; i += blockDim.x)
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < r) a8[q] += row[i] * Ve[(size_t)i * r + q];
+  block_sum<8>(a8, red);
+  if (threadIdx.x == 0)
+    for (int q = 0; q < r; ++q) z[(size_t)srow * r + q] = a8[q];
 }
 
 void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d, int prompt_len,
                      int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r, float* z,
                      int rows_per_sign, long vstride, cudaStream_t st) {
-  const size_t smem = (size_t)(d + 32 * 8) * sizeof(float);
+  if (d % 4) throw Error(ZO_ERR_DIMENSION, "final LN needs dim % 4 == 0");
+  if (r > FLN_THREADS) throw Error(ZO_ERR_DIMENSION, "final LN: rank above 1024");
+  const size_t smem = (size_t)(d + 32 * 8 + FLN_THREADS) * sizeof(float);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     ZO_CUDA_TRY(cudaFuncSetAttribute(k_final_ln, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  k_final_ln<<<B * Lopt, 256, smem, st>>>(x32, gamma, beta, B, T, d, prompt_len, Lopt, xs32, xs16, bf16, Ve32,
-                                              r, z, rows_per_sign, vstride);
+  k_final_ln<<<B * Lopt, FLN_THREADS, smem, st>>>(x32, gamma, beta, B, T, d, prompt_len, Lopt, xs32, xs16, bf16,
+                                                    Ve32, r, z, rows_per_sign, vstride);
 }
 
 // ------------------------------------------------------------------ loss (K6b): log-softmax + gold gather
-// One CTA per example (sign, b); streams its Lopt logits rows from HBM with
-// float4 loads, adds the embedding LoRA term z . P_s,e[v]^T on the fly and
-// never materialises probabilities.
-__global__ void __launch_bounds__(1024) k_loss(const float* __restrict__ logits, int ldl, int V,
-                                               const float* __restrict__ z, int r, const float* __restrict__ Pp,
-                                               const float* __restrict__ Pm, const int32_t* __restrict__ gold,
-                                               int B, int Lopt, double* __restrict__ nll) {
-  __shared__ float red[32];
-  __shared__ float zs[64];
-  const int ex = blockIdx.x;  // s*B + b
-  const int s = ex / B, b = ex % B;
-  const float* P = s == 0 ? Pp : Pm;
-  float total = 0.f;
-  for (int j = 0; j < Lopt; ++j) {
-    const int srow = ex * Lopt + j;
-    const float* lr = logits + (size_t)srow * ldl;
-    if (threadIdx.x < r && threadIdx.x < 64) zs[threadIdx.x] = z[(size_t)srow * r + threadIdx.x];
-    __syncthreads();
-    float mx = -CUDART_INF_F;
-    const int V4 = V >> 2;
-    for (int i = threadIdx.x; i < V4; i += blockDim.x) {
-      const float4 l4 = reinterpret_cast<const float4*>(lr)[i];
-      float l[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float add = 0.f;
-        for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)(4 * i + e) * r + k];
-        mx = fmaxf(mx, l[e] + add);
-      }
-    }
-    for (int v = 4 * V4 + threadIdx.x; v < V; v += blockDim.x) {
-      float add = 0.f;
-      for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)v * r + k];
-      mx = fmaxf(mx, lr[v] + add);
-    }
-    mx = block_max(mx, red);
-    float sum = 0.f;
-    for (int i = threadIdx.x; i < V4; i += blockDim.x) {
-      const float4 l4 = reinterpret_cast<const float4*>(lr)[i];
-      float l[4] = {l4.x, l4.y, l4.z, l4.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float add = 0.f;
-        for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)(4 * i + e) * r + k];
-        sum += expf(l[e] + add - mx);
-      }
-    }
-    for (int v = 4 * V4 + threadIdx.x; v < V; v += blockDim.x) {
-      float add = 0.f;
-      for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)v * r + k];
-      sum += expf(lr[v] + add - mx);
-    }
-    float acc[1] = {sum};
-    block_sum<1>(acc, red);
-    if (threadIdx.x == 0) {
-      const int gv = gold[(size_t)ex * Lopt + j];
-      float add = 0.f;
-      for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)gv * r + k];
-      const float lse = mx + logf(acc[0]);
-      total = total + (lse - (lr[gv] + add));
-    }
-    __syncthreads();
+// Split-vocabulary, single pass (model.py:202-215).  Grid = (LOSS_SPLITS, scored rows):
+// CTA (j, row) loads its <= LOSS_CHUNK logits of the row once into registers (float4,
+// coalesced), adds the embedding LoRA term z . P_s,e[v]^T (P read once), and reduces
+// them to a partial (max, sum exp(x - max)); the gold logit is captured by the CTA whose
+// slice holds it.  The last CTA of a row (arrival counter) combines the partials in split
+// order -- deterministic whichever CTA arrives last -- and the last row of an example sums
+// its Lopt option-token NLLs in token order into nll[sign*B + b].  Counters reset
+// themselves, so the launch replays inside a CUDA graph.  Probabilities are never stored.
+constexpr int LOSS_THREADS = 256, LOSS_VEC = 4;  // float4 per thread per slice
+constexpr int LOSS_CHUNK = LOSS_THREADS * LOSS_VEC * 4;
+
+template <int R>
+__device__ __forceinline__ float embed_term(const float* __restrict__ P, int v, const float* zs, int r) {
+  float add = 0.f;
+  if constexpr (R == 2) {
+    const float2 p = *reinterpret_cast<const float2*>(P + (size_t)v * 2);
+    add = zs[0] * p.x + zs[1] * p.y;
+  } else {
+    for (int k = 0; k < r; ++k) add += zs[k] * P[(size_t)v * r + k];
   }
-  if (threadIdx.x == 0) nll[ex] = (double)total;
+  return add;
+}
+
+template <int R>
+__global__ void __launch_bounds__(LOSS_THREADS) k_loss(const float* __restrict__ logits, int ldl, int V,
+                                                       const float* __restrict__ z, int r,
+                                                       const float* __restrict__ Pp, const float* __restrict__ Pm,
+                                                       const int32_t* __restrict__ gold, int B, int Lopt,
+                                                       float* __restrict__ part, unsigned* __restrict__ counters,
+                                                       double* __restrict__ nll) {
+  __shared__ float red[32];
+  __shared__ float zs[8];
+  __shared__ unsigned last;
+  const int nsplit = gridDim.x, split = blockIdx.x, srow = blockIdx.y;
+  const int ex = srow / Lopt;  // s*B + b
+  const float* P = ex / B == 0 ? Pp : Pm;
+  const float* lr = logits + (size_t)srow * ldl;
+  const int chunk = (int)(((int64_t)V + nsplit - 1) / nsplit + 3) & ~3;
+  const int v0 = split * chunk, v1 = min(V, v0 + chunk);
+  const int gv = gold[srow];
+  if (threadIdx.x < r) zs[threadIdx.x] = z[(size_t)srow * r + threadIdx.x];
+  __syncthreads();
+  float x[LOSS_VEC * 4];
+  float mx = -CUDART_INF_F;
+#pragma unroll
+  for (int q = 0; q < LOSS_VEC; ++q) {
+    const int v = v0 + 4 * (q * LOSS_THREADS + threadIdx.x);
+    if (v + 3 < v1) {
+      const float4 l4 = *reinterpret_cast<const float4*>(lr + v);
+      x[4 * q] = l4.x, x[4 * q + 1] = l4.y, x[4 * q + 2] = l4.z, x[4 * q + 3] = l4.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[4 * q + e] = v + e < v1 ? lr[v + e] : -CUDART_INF_F;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (R > 0 && v + e < v1) x[4 * q + e] += embed_term<R>(P, v + e, zs, r);
+      mx = fmaxf(mx, x[4 * q + e]);
+      if (v + e == gv) red[31] = x[4 * q + e];  // read after the block reductions' barriers
+    }
+  }
+  mx = block_max(mx, red);
+  float acc[1] = {0.f};
+#pragma unroll
+  for (int q = 0; q < LOSS_VEC * 4; ++q) acc[0] += expf(x[q] - mx);
+  // red[31] (the gold logit) survives: block_sum<1> writes red[warp] for 8 warps only
+  const bool has_gold = gv >= v0 && gv < v1;
+  const float gx = has_gold ? red[31] : 0.f;
+  block_sum<1>(acc, red);
+  if (threadIdx.x == 0) {
+    float* pr = part + ((size_t)srow * nsplit + split) * 2;
+    pr[0] = mx;
+    pr[1] = acc[0];
+    if (has_gold) part[((size_t)gridDim.y * nsplit) * 2 + srow] = gx;
+    __threadfence();
+    last = atomicAdd(&counters[srow], 1u) == (unsigned)nsplit - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  // the row's last CTA: every slice partial is visible (fence + counter); load them in
+  // parallel, combine in slice order on one thread
+  __shared__ float pm[64], ps[64];
+  __threadfence();
+  const size_t rows_off = ((size_t)gridDim.y * nsplit) * 2 + gridDim.y;
+  if (threadIdx.x < nsplit) {
+    const volatile float* pv = part + ((size_t)srow * nsplit + threadIdx.x) * 2;
+    pm[threadIdx.x] = pv[0];
+    ps[threadIdx.x] = pv[1];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = -CUDART_INF_F;
+    for (int j = 0; j < nsplit; ++j) m = fmaxf(m, pm[j]);
+    float sum = 0.f;
+    for (int j = 0; j < nsplit; ++j) sum += ps[j] * expf(pm[j] - m);
+    const float g = ((const volatile float*)part)[((size_t)gridDim.y * nsplit) * 2 + srow];
+    const float row_nll = (m + logf(sum)) - g;
+    counters[srow] = 0u;
+    if (Lopt == 1) {
+      nll[ex] = (double)row_nll;
+      return;
+    }
+    ((volatile float*)part)[rows_off + srow] = row_nll;
+    __threadfence();
+    unsigned* exc = counters + gridDim.y;
+    if (atomicAdd(&exc[ex], 1u) == (unsigned)Lopt - 1) {
+      __threadfence();
+      float total = 0.f;
+      for (int j = 0; j < Lopt; ++j) total = total + ((const volatile float*)part)[rows_off + ex * Lopt + j];
+      nll[ex] = (double)total;
+      exc[ex] = 0u;
+    }
+  }
 }
 
 // High-rank embedding delta (factorized r > 8): logits[row, v] += z[row] . P_s[v] with
@@ -671,8 +851,12 @@ __global__ void __launch_bounds__(256) k_embed_delta(float* __restrict__ logits,
   }
 }
 
+size_t loss_ws_floats(int rows, int V) { return (size_t)rows * (2 * loss_splits(V) + 2); }
+int loss_splits(int V) { return (int)ceil_div(V, LOSS_CHUNK); }
+
 void launch_loss(const float* logits, int ldl, int V, const float* z, int r, const float* Pplus_e,
-                 const float* Pminus_e, const int32_t* gold, int B, int Lopt, double* nll, cudaStream_t st) {
+                 const float* Pminus_e, const int32_t* gold, int B, int Lopt, float* ws, unsigned* counters,
+                 double* nll, cudaStream_t st) {
   if (ldl % 4) throw Error(ZO_ERR_DIMENSION, "logits leading dimension must be a multiple of 4");
   if (r > 8) {
     // fold the embedding's rank-r delta into the logits first, then a plain log-softmax
@@ -682,7 +866,14 @@ void launch_loss(const float* logits, int ldl, int V, const float* z, int r, con
     k_embed_delta<<<grid, 256, 0, st>>>(const_cast<float*>(logits), ldl, V, z, r, Pminus_e, rows, rows);
     r = 0;
   }
-  k_loss<<<2 * B, 1024, 0, st>>>(logits, ldl, V, z, r, Pplus_e, Pminus_e, gold, B, Lopt, nll);
+  const dim3 grid(loss_splits(V), 2 * B * Lopt);
+  if (grid.x > 64) throw Error(ZO_ERR_DIMENSION, "vocabulary too large for the loss kernel's slice table");
+  if (r == 0)
+    k_loss<0><<<grid, LOSS_THREADS, 0, st>>>(logits, ldl, V, z, r, Pplus_e, Pminus_e, gold, B, Lopt, ws, counters, nll);
+  else if (r == 2)
+    k_loss<2><<<grid, LOSS_THREADS, 0, st>>>(logits, ldl, V, z, r, Pplus_e, Pminus_e, gold, B, Lopt, ws, counters, nll);
+  else
+    k_loss<1><<<grid, LOSS_THREADS, 0, st>>>(logits, ldl, V, z, r, Pplus_e, Pminus_e, gold, B, Lopt, ws, counters, nll);
 }
 
 // ------------------------------------------------------------------ coefficient (K7)
@@ -843,6 +1034,49 @@ __global__ void k_p16t(const float* __restrict__ P, int m, int r, uint16_t* __re
 void launch_p16t(const float* P, int m, int r, void* out, bool bf16, cudaStream_t st) {
   dim3 grid((m + 31) / 32, (r + 31) / 32);
   k_p16t<<<grid, dim3(32, 8), 0, st>>>(P, m, r, static_cast<uint16_t*>(out), bf16);
+}
+
+// Every extension matrix's P_s -> 16-bit [r][m] in one launch: blockIdx.x enumerates the
+// 32-row tiles of all matrices (tab: per matrix {first tile, u_off, m}, ascending), y the
+// 32-rank slices, z the probe sign (P+ / P- -> out / out + su).
+__global__ void k_p16t_all(const float* __restrict__ Pp, const float* __restrict__ Pm, int64_t su,
+                           const int64_t* __restrict__ tab, int ntab, int r, uint16_t* __restrict__ out,
+                           bool bf16) {
+  __shared__ float tile[32][33];
+  __shared__ int64_t mat[3];
+  if (threadIdx.x == 0 && threadIdx.y == 0) {
+    int lo = 0, hi = ntab - 1;  // last entry with first tile <= blockIdx.x
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) / 2;
+      if (tab[3 * mid] <= (int64_t)blockIdx.x) lo = mid;
+      else hi = mid - 1;
+    }
+    mat[0] = tab[3 * lo];
+    mat[1] = tab[3 * lo + 1];
+    mat[2] = tab[3 * lo + 2];
+  }
+  __syncthreads();
+  const int m = (int)mat[2];
+  const float* P = (blockIdx.z == 0 ? Pp : Pm) + mat[1];
+  uint16_t* o = out + (size_t)blockIdx.z * su + mat[1];
+  const int i0 = (int)((int64_t)blockIdx.x - mat[0]) * 32, k0 = blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int i = i0 + yy, k = k0 + tx;
+    tile[yy][tx] = (i < m && k < r) ? P[(size_t)i * r + k] : 0.f;
+  }
+  __syncthreads();
+  for (int yy = ty; yy < 32; yy += 8) {
+    const int k = k0 + yy, i = i0 + tx;
+    if (i < m && k < r) o[(size_t)k * m + i] = to16(tile[tx][yy], bf16);
+  }
+}
+
+void launch_p16t_all(const float* Pp, const float* Pm, int64_t su, const int64_t* tab, int ntab, int tiles, int r,
+                     int nsign, void* out, bool bf16, cudaStream_t st) {
+  if (ntab == 0) return;
+  dim3 grid((unsigned)tiles, (unsigned)((r + 31) / 32), (unsigned)nsign);
+  k_p16t_all<<<grid, dim3(32, 8), 0, st>>>(Pp, Pm, su, tab, ntab, r, static_cast<uint16_t*>(out), bf16);
 }
 
 // ------------------------------------------------------------------ fold (K9) + 16-bit shadow refresh
@@ -1186,6 +1420,15 @@ __global__ void k_f64_to_f32(const double* __restrict__ a, float* __restrict__ b
 void launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t st) {
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   k_f64_to_f32<<<grid > 0 ? grid : 1, 256, 0, st>>>(a, b, n);
+}
+
+__global__ void k_f32_to_f64(const float* __restrict__ a, double* __restrict__ b, int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) b[i] = (double)a[i];
+}
+void launch_f32_to_f64(const float* a, double* b, int64_t n, cudaStream_t st) {
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_f32_to_f64<<<grid > 0 ? grid : 1, 256, 0, st>>>(a, b, n);
 }
 
 void launch_zero(void* p, size_t bytes, cudaStream_t st) { ZO_CUDA_TRY(cudaMemsetAsync(p, 0, bytes, st)); }

@@ -21,8 +21,9 @@ struct PosEmbed {
 };
 // x32[M,d] = E[tok] + sum_k P_s[tok,k] V_e[:,k] + PE[t]   (model.py:180, adapter.py:200-234)
 // for positions t < T of token rows tokens[b * tok_ld + t]
+// token rows from E64 (float64 master), else E32 (fp32 master), else E16 (16-bit shadow)
 void launch_embed(float* x32, const int32_t* tokens, int tok_ld, int B, int T, int d, const double* E64,
-                  const void* E16, bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r,
+                  const float* E32, const void* E16, bool bf16, const float* Pplus, const float* Pminus, const float* Ve32, int r,
                   const float* pe, const PosEmbed& pos, int nrows, cudaStream_t st);
 // h = LN(x) (model.py:139-142) -> out[:, :d] (16-bit); ext columns [d, d+3r) = (t_hi, t_lo, t_hi)
 // per rank with t = h . P_s (fp32) -- the LoRA K-extension operand (A side).
@@ -56,9 +57,13 @@ void launch_gather_scored(const void* src, size_t ld_src_bytes, void* dst, size_
 void launch_final_ln(const float* x32, const float* gamma, const float* beta, int B, int T, int d,
                      int prompt_len, int Lopt, float* xs32, void* xs16, bool bf16, const float* Ve32, int r,
                      float* z, int rows_per_sign, long vstride, cudaStream_t st);
-// per scored row: logits + z.P_s,e^T -> log-softmax, gold gather -> nll[sign*B + b] (model.py:202-215)
+// per scored row: logits + z.P_s,e^T -> log-softmax, gold gather -> nll[sign*B + b] (model.py:202-215);
+// ws: loss_ws_floats(2*B*Lopt, V) floats, counters: 2*B*Lopt + 2*B zeroed (self-resetting)
+int loss_splits(int V);
+size_t loss_ws_floats(int rows, int V);
 void launch_loss(const float* logits, int ldl, int V, const float* z, int r, const float* Pplus_e,
-                 const float* Pminus_e, const int32_t* gold, int B, int Lopt, double* nll, cudaStream_t st);
+                 const float* Pminus_e, const int32_t* gold, int B, int Lopt, float* ws, unsigned* counters,
+                 double* nll, cudaStream_t st);
 // canonical_mean per sign, c, c_used, beta (numerics.py:271-284, zo_engine.py:331,411)
 void launch_coefficient(const double* nll, int B, double eps, double lr, int divide_by_r, int rank,
                         double* out4, unsigned* abort_flag, cudaStream_t st);
@@ -75,6 +80,9 @@ void launch_vec_update(double* p, const double* z, int64_t n, const double* out4
                        const unsigned* abort_flag, float* out32, cudaStream_t st);
 // P16T[k][i] = h16(P[i][k]) for one [m, r] probe block (tensor-core extension B operand, r > 8)
 void launch_p16t(const float* P, int m, int r, void* out, bool bf16, cudaStream_t st);
+// launch_p16t for every matrix of tab ({first 32-row tile, u_off, m} per matrix) and both signs
+void launch_p16t_all(const float* Pp, const float* Pm, int64_t su, const int64_t* tab, int ntab, int tiles, int r,
+                     int nsign, void* out, bool bf16, cudaStream_t st);
 // V ext columns (hi, hi, lo) into W16T[:, K:K+3r] for one matrix; V32 copy
 void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K, bool bf16, int ext_terms,
                        float* V32, cudaStream_t st);
@@ -105,5 +113,6 @@ void launch_vec_inplace(double* p, const double* z, int64_t n, double a1, const 
 void launch_vec_probe_sign(const double* p, const double* z, int64_t n, double eps, int sign, float* out32,
                            cudaStream_t st);
 void launch_f64_to_f32(const double* a, float* b, int64_t n, cudaStream_t st);
+void launch_f32_to_f64(const float* a, double* b, int64_t n, cudaStream_t st);
 
 }  // namespace zo

@@ -79,6 +79,11 @@ uint64_t fnv(const void* p, size_t n, uint64_t h) {
 }
 const uint64_t FNV0 = 0xCBF29CE484222325ULL;
 
+bool env_streamk_off() {
+  const char* e = std::getenv("ZO_STREAMK");
+  return e && std::atoi(e) == 0;
+}
+
 struct DevAlloc {
   std::vector<void*> ptrs;
   uint64_t bytes = 0;
@@ -109,6 +114,10 @@ struct zo_ctx {
   // reference (k_fold_dev_tiled); true = tensor-core UV^T fused into the master/shadow RMW
   // (EPI_UPDATE64, r >= 16, r % 16 == 0) -- HBM-bound, not bit-exact
   bool fast_update = false;
+  // fast update mode keeps the projection / embedding masters as fp32 (in the first half of
+  // each W64 allocation): 10 instead of 18 bytes per weight per update.  K_POS stays float64.
+  bool master32 = false;
+  float* conv_tmp = nullptr;  // CONV_CHUNK floats: in-place float64 <-> fp32 master conversion
   uint16_t *U16 = nullptr, *V16 = nullptr;  // 16-bit U / V operands of the fast update
   std::vector<GemmDesc> upd_plans;           // per matrix (empty entry: exact path)
   float *a32 = nullptr, *f32a = nullptr, *ctx32 = nullptr;  // split A operand, qkv/ff_up out, ctx
@@ -170,8 +179,12 @@ struct zo_ctx {
   std::map<int, RowPlan> plans;  // keyed by 2*M + (nsign == 1)
   float* tpart = nullptr;         // fused LoRA-extension partials [tiles][Mpad][r]
   uint16_t* P16T = nullptr;       // high-rank extension B operands [2][su] (per matrix [r][m])
+  int64_t* p16t_tab = nullptr;    // launch_p16t_all's matrix table; p16t_n entries, p16t_tiles tiles
+  int p16t_n = 0, p16t_tiles = 0;
   float* xws = nullptr;           // high-rank extension split-K partials [num_sms][Mpad][r]
   float* sk_ws = nullptr;         // stream-K partial tiles
+  float* loss_ws = nullptr;       // k_loss per-slice partials (loss_ws_floats)
+  unsigned* loss_cnt = nullptr;   // k_loss arrival counters (self-resetting)
   unsigned* sk_flags = nullptr;
   bool streamk = true;  // DP waves + stream-K tail where it pays (ZO_STREAMK=0 disables)
   int tpart_tiles = 0;
@@ -388,6 +401,38 @@ void refresh_shadow(zo_ctx* c, const Matrix& m) {
     launch_shadow_T(m.W64, (int)m.m, (int)m.n, m.W16, m.ldw, c->bf16, c->st);
 }
 
+// In-place master conversion, chunk by chunk through conv_tmp (stream-ordered): narrowing
+// walks up (chunk k's fp32 bytes [4kC, 4kC+4C) only overwrite float64 chunks < k, already
+// read), widening walks down (chunk k's float64 bytes only overwrite fp32 chunks >= k).
+constexpr int64_t CONV_CHUNK = 1 << 24;
+bool has_master32(const Matrix& m) { return m.kind != K_POS; }
+void narrow_master(zo_ctx* c, Matrix& m) {
+  const int64_t n = m.m * m.n;
+  float* dst = reinterpret_cast<float*>(m.W64);
+  for (int64_t o = 0; o < n; o += CONV_CHUNK) {
+    const int64_t k = std::min(CONV_CHUNK, n - o);
+    launch_f64_to_f32(m.W64 + o, c->conv_tmp, k, c->st);
+    ZO_CUDA_TRY(cudaMemcpyAsync(dst + o, c->conv_tmp, (size_t)k * 4, cudaMemcpyDeviceToDevice, c->st));
+  }
+}
+void widen_master(zo_ctx* c, Matrix& m) {
+  const int64_t n = m.m * m.n;
+  const float* src = reinterpret_cast<const float*>(m.W64);
+  for (int64_t o = ((n - 1) / CONV_CHUNK) * CONV_CHUNK; o >= 0; o -= CONV_CHUNK) {
+    const int64_t k = std::min(CONV_CHUNK, n - o);
+    ZO_CUDA_TRY(cudaMemcpyAsync(c->conv_tmp, src + o, (size_t)k * 4, cudaMemcpyDeviceToDevice, c->st));
+    launch_f32_to_f64(c->conv_tmp, m.W64 + o, k, c->st);
+  }
+}
+// run f on a float64 view of m's master (widen -> f -> narrow when the master is fp32)
+template <class F>
+void with_master64(zo_ctx* c, Matrix& m, F&& f) {
+  const bool conv = c->master32 && has_master32(m);
+  if (conv) widen_master(c, m);
+  f();
+  if (conv) narrow_master(c, m);
+}
+
 void write_vext_all(zo_ctx* c) {
   for (auto& m : c->mats)
     launch_write_vext(c->V + m.v_off, (int)m.n, c->r, m.kind == K_EMBED ? nullptr : m.W16, m.ldw, (int)m.m,
@@ -463,7 +508,7 @@ void do_score32(zo_ctx* c, int B, int nsign) {
     pos.V32 = c->V32 + pm.v_off;
     pos.offset = 2;
   }
-  launch_embed(c->x32, c->tok, c->T, B, T, d, e.W64, e.W16, false, c->Pp + e.u_off, c->Pm + e.u_off,
+  launch_embed(c->x32, c->tok, c->T, B, T, d, e.W64, nullptr, e.W16, false, c->Pp + e.u_off, c->Pm + e.u_off,
                c->V32 + e.v_off, r, c->pe, pos, M, c->st);
   for (int l = 0; l < c->d.n_layers; ++l) {
     const Matrix& q = c->mats[c->i_qkv[l]];
@@ -489,7 +534,7 @@ void do_score32(zo_ctx* c, int B, int nsign) {
   launch_split_act(c->xs32, d, S, d, c->a32, e.ldk, nullptr, nullptr, 0, S, 0, c->st);
   gemm_launch(rp.lm, c->st);
   launch_loss(c->logits, c->ldl, c->d.vocab, c->z, r, c->Pp + e.u_off, c->Pm + e.u_off, c->gold, B,
-              c->d.opt_len, c->nll, c->st);
+              c->d.opt_len, c->loss_ws, c->loss_cnt, c->nll, c->st);
 }
 
 void do_score(zo_ctx* c, int B, int nsign) {
@@ -513,14 +558,13 @@ void do_score(zo_ctx* c, int B, int nsign) {
     pos.offset = 2;
   }
   prof_mark(c, PK_EMBED);
-  launch_embed(c->x32, c->tok, c->T, B, T, d, e.W64, e.W16, c->bf16, c->Pp + e.u_off, c->Pm + e.u_off, c->V32 + e.v_off,
+  launch_embed(c->x32, c->tok, c->T, B, T, d, c->master32 ? nullptr : e.W64,
+               c->master32 ? reinterpret_cast<const float*>(e.W64) : nullptr, e.W16, c->bf16, c->Pp + e.u_off,
+               c->Pm + e.u_off, c->V32 + e.v_off,
                c->r, c->pe, pos, M, c->st);
   if (!c->fused_ext)  // high rank: 16-bit transposed probe operands of the extension GEMMs
-    for (const auto& m : c->mats) {
-      if (m.kind == K_EMBED || m.kind == K_POS) continue;
-      launch_p16t(c->Pp + m.u_off, (int)m.m, c->r, c->P16T + m.u_off, c->bf16, c->st);
-      if (nsign == 2) launch_p16t(c->Pm + m.u_off, (int)m.m, c->r, c->P16T + c->su + m.u_off, c->bf16, c->st);
-    }
+    launch_p16t_all(c->Pp, c->Pm, c->su, c->p16t_tab, c->p16t_n, c->p16t_tiles, c->r, nsign, c->P16T, c->bf16,
+                    c->st);
   auto ext_gemm = [&](const LayerPlan& lp, int i) {
     for (int sg = 0; sg < nsign; ++sg) {
       const int j = 2 * i + sg;
@@ -602,7 +646,7 @@ void do_score(zo_ctx* c, int B, int nsign) {
                     c->bf16, c->V32 + e.v_off, c->r, c->z, rps, c->vstride, c->st);
   gemm_launch(rp.lm, c->st);
   launch_loss(c->logits, c->ldl, c->d.vocab, c->z, c->r, c->Pp + e.u_off, c->Pm + e.u_off, c->gold, B,
-              c->d.opt_len, c->nll, c->st);
+              c->d.opt_len, c->loss_ws, c->loss_cnt, c->nll, c->st);
 }
 
 // gold: [gold_signs, B, opt_len]; with gold_signs == 1 both probe halves share it
@@ -627,7 +671,7 @@ void set_step(zo_ctx* c, uint64_t step) {
   ZO_CUDA_TRY(cudaMemcpyAsync(c->d_step, c->h_step, 8, cudaMemcpyHostToDevice, c->st));
 }
 
-void launch_dense_update_dev(zo_ctx* c, double lr) {
+void launch_dense_update_dev(zo_ctx* c, double lr, const double* out4, const unsigned* abort_flag) {
   if (c->fast_update) {
     // 16-bit operands of this step's directions, then one fused GEMM + RMW per matrix
     launch_shadow(c->U, c->su, c->U16, c->bf16, c->st);
@@ -646,32 +690,33 @@ void launch_dense_update_dev(zo_ctx* c, double lr) {
           gemm_plan(g, c->U16 + m.u_off, (int)m.m, c->r, c->V16 + m.v_off, (int)m.n, c->r, c->r, EPI_UPDATE64,
                     c->bf16, nullptr, 0, c->num_sms);
         g.upd_w64 = m.W64;
+        g.upd_m32 = c->master32 ? 1 : 0;
         g.upd_w16 = m.W16;
         g.upd_ld64 = (int)m.n;
         g.upd_ld16 = m.ldw;
         g.upd_transposed = tr ? 1 : 0;
-        g.upd_out4 = c->out4;
         g.upd_lr = lr;
         g.upd_scale = 1.0 / std::sqrt((double)c->r);
-        g.upd_abort = c->abort_flag;
         gemm_set_update_master(g);
       }
     }
     for (size_t i = 0; i < c->mats.size(); ++i) {
       const Matrix& m = c->mats[i];
       if (m.kind == K_POS) {
-        launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, c->out4, lr,
-                        1.0 / std::sqrt((double)c->r), c->abort_flag, m.W16, (int)m.n, 0, c->bf16, c->st);
+        launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, out4, lr,
+                        1.0 / std::sqrt((double)c->r), abort_flag, m.W16, (int)m.n, 0, c->bf16, c->st);
         continue;
       }
       c->upd_plans[i].upd_lr = lr;
+      c->upd_plans[i].upd_out4 = out4;
+      c->upd_plans[i].upd_abort = abort_flag;
       gemm_launch(c->upd_plans[i], c->st);
     }
     return;
   }
   for (auto& m : c->mats)
-    launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, c->out4, lr,
-                    1.0 / std::sqrt((double)c->r), c->abort_flag, m.W16, m.kind == K_EMBED ? (int)m.n : m.ldw,
+    launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, out4, lr,
+                    1.0 / std::sqrt((double)c->r), abort_flag, m.W16, m.kind == K_EMBED ? (int)m.n : m.ldw,
                     m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
 }
 
@@ -935,6 +980,8 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->xs32 = c->mem.get<float>((size_t)c->Smax * D);
   c->z = c->mem.get<float>((size_t)c->Smax * d.rank);
   c->logits = c->mem.get<float>((size_t)c->Smax * c->ldl);
+  c->loss_ws = c->mem.get<float>(loss_ws_floats(c->Smax, d.vocab));
+  c->loss_cnt = c->mem.get<unsigned>(2 * (size_t)c->Smax);
   c->nll = c->mem.get<double>(2 * std::max(d.max_batch, 4096));
   c->nll_bl = c->mem.get<double>(d.max_batch);
   c->out4 = c->mem.get<double>(4);
@@ -944,12 +991,22 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->d_step = c->mem.get<uint64_t>(1);
   c->sk_ws = c->mem.get<float>(gemm_sk_ws_floats(c->num_sms));
   c->sk_flags = c->mem.get<unsigned>(c->num_sms + 1);
-  if (const char* e = std::getenv("ZO_STREAMK")) c->streamk = std::atoi(e) != 0;
+  if (env_streamk_off()) c->streamk = false;
   c->fused_ext = d.rank <= 8;
   c->tpart_tiles = std::max((int)ceil_div(4 * D, 64), d.n_heads);
   if (c->fused_ext) c->tpart = c->mem.get<float>((size_t)c->tpart_tiles * c->Mpad * d.rank);
   else {
     c->P16T = c->mem.get<uint16_t>((size_t)2 * c->su);
+    std::vector<int64_t> tab;
+    for (const auto& m : c->mats) {
+      if (m.kind == K_EMBED || m.kind == K_POS) continue;
+      tab.insert(tab.end(), {(int64_t)c->p16t_tiles, m.u_off, m.m});
+      c->p16t_tiles += (int)ceil_div(m.m, 32);
+    }
+    c->p16t_n = (int)(tab.size() / 3);
+    c->p16t_tab = c->mem.get<int64_t>(tab.size() + 1);
+    if (!tab.empty())
+      ZO_CUDA_TRY(cudaMemcpy(c->p16t_tab, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice));
     c->xws = c->mem.get<float>((size_t)c->num_sms * c->Mpad * d.rank);
   }
   // positional table: pos_encoding(T, d) (model.py:128-136), float64 -> float32
@@ -1096,6 +1153,7 @@ int zo_init_params(zo_ctx* c, uint64_t init_seed, double init_scale) {
     ZO_CUDA_TRY(cudaMemcpyAsync(P.d_streams, sd.data(), sizeof(StreamDesc), cudaMemcpyHostToDevice, c->st));
     sampler_launch(P, init_seed, c->d_step, 1, m.W64, c->st);
     refresh_shadow(c, m);
+    if (c->master32 && has_master32(m)) narrow_master(c, m);
     ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
   }
   ZO_CUDA_TRY(cudaGetLastError());
@@ -1109,6 +1167,7 @@ int zo_upload_matrix(zo_ctx* c, const char* lid, const double* host, int64_t row
   check(rows == m.m && cols == m.n, ZO_ERR_DIMENSION, "matrix shape mismatch for " + m.lid);
   ZO_CUDA_TRY(cudaMemcpyAsync(m.W64, host, (size_t)(rows * cols) * 8, cudaMemcpyHostToDevice, c->st));
   refresh_shadow(c, m);
+  if (c->master32 && has_master32(m)) narrow_master(c, m);
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
   return ZO_OK;
   ZO_API_END
@@ -1118,7 +1177,9 @@ int zo_download_matrix(zo_ctx* c, const char* lid, double* host, int64_t rows, i
   ZO_API_BEGIN
   Matrix& m = find(c, lid);
   check(rows == m.m && cols == m.n, ZO_ERR_DIMENSION, "matrix shape mismatch for " + m.lid);
-  ZO_CUDA_TRY(cudaMemcpyAsync(host, m.W64, (size_t)(rows * cols) * 8, cudaMemcpyDeviceToHost, c->st));
+  with_master64(c, m, [&] {
+    ZO_CUDA_TRY(cudaMemcpyAsync(host, m.W64, (size_t)(rows * cols) * 8, cudaMemcpyDeviceToHost, c->st));
+  });
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
   return ZO_OK;
   ZO_API_END
@@ -1273,9 +1334,33 @@ int zo_set_update_mode(zo_ctx* c, int32_t mode) {
       c->V16 = c->mem.get<uint16_t>((size_t)c->sv);
     }
   }
+  if ((mode == 1) != c->master32) {
+    if (!c->conv_tmp) c->conv_tmp = c->mem.get<float>(CONV_CHUNK);
+    for (auto& m : c->mats) {
+      if (!has_master32(m)) continue;
+      if (mode == 1) narrow_master(c, m);
+      else widen_master(c, m);
+    }
+    c->master32 = mode == 1;
+    ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  }
   c->fast_update = mode == 1;
   c->upd_plans.clear();
   c->gkey_valid = false;  // the captured step graph holds the old update
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_set_schedule(zo_ctx* c, int32_t row_invariant) {
+  ZO_API_BEGIN
+  check(row_invariant == 0 || row_invariant == 1, ZO_ERR_CONFIG, "schedule must be 0 (fastest) or 1 (row-invariant)");
+  const bool sk = row_invariant == 0 && !env_streamk_off();
+  if (sk != c->streamk) {
+    ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+    c->streamk = sk;
+    c->plans.clear();        // GEMM plans carry the stream-K split
+    c->gkey_valid = false;   // the captured step graph holds the old plans
+  }
   return ZO_OK;
   ZO_API_END
 }
@@ -1361,6 +1446,7 @@ int zo_update_u(zo_ctx* c) {
 
 int zo_fold(zo_ctx* c) {
   ZO_API_BEGIN
+  check(!c->master32, ZO_ERR_CONFIG, "fold needs the float64 masters: set update mode 0 first");
   fold_all(c);
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
   return ZO_OK;
@@ -1369,6 +1455,14 @@ int zo_fold(zo_ctx* c) {
 
 int zo_update_dense(zo_ctx* c, double lr) {
   ZO_API_BEGIN
+  if (c->fast_update) {
+    // tensor mode: the installed coefficient (zo_set_coefficient's device copy) drives the
+    // fused tcgen05 update, as in a fused step
+    launch_dense_update_dev(c, lr, c->out4, nullptr);
+    vec_update(c, c->out4, lr, c->abort_flag);
+    ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+    return ZO_OK;
+  }
   // alpha = -(lr*c) * (1/sqrt(r)) as zo_engine.py:450 computes it (host copy of c)
   const double cc = c->h_out4[2];
   const double alpha = (-(lr * cc)) * (1.0 / std::sqrt((double)c->r));
@@ -1491,7 +1585,7 @@ extern "C" int zo_step_apply_async(zo_ctx* c, double eps, double lr, int32_t div
     launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
     c->a_dirty = true;
   } else {
-    launch_dense_update_dev(c, lr);
+    launch_dense_update_dev(c, lr, c->out4, c->abort_flag);
   }
   vec_update(c, c->out4, lr, c->abort_flag);
   return ZO_OK;
@@ -1519,7 +1613,7 @@ static void step_body(zo_ctx* c, uint64_t seed, double eps, double lr, int32_t d
   if (lozo)
     launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
   else
-    launch_dense_update_dev(c, lr);
+    launch_dense_update_dev(c, lr, c->out4, c->abort_flag);
   vec_update(c, c->out4, lr, c->abort_flag);
 }
 
@@ -1724,6 +1818,7 @@ void baseline_directions(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu) {
 // (zo_baseline_directions); score with zo_score(nsign = 1) between passes.
 extern "C" int zo_baseline_pass(zo_ctx* c, int32_t pass, double eps, int32_t recompute) {
   ZO_API_BEGIN
+  check(!c->master32, ZO_ERR_CONFIG, "the materialising loop keeps float64 masters: set update mode 0 first");
   check(pass >= 0 && pass <= 2, ZO_ERR_INPUT, "baseline pass must be 0, 1 or 2");
   baseline_pass(c, pass, eps, recompute != 0);
   ZO_CUDA_TRY(cudaGetLastError());
@@ -1734,6 +1829,7 @@ extern "C" int zo_baseline_pass(zo_ctx* c, int32_t pass, double eps, int32_t rec
 // W -= eta*c_used*P with the ctx coefficient (zo_coefficient / zo_set_coefficient)
 extern "C" int zo_baseline_update(zo_ctx* c, double lr, int32_t recompute) {
   ZO_API_BEGIN
+  check(!c->master32, ZO_ERR_CONFIG, "the materialising loop keeps float64 masters: set update mode 0 first");
   baseline_update(c, lr, recompute != 0);
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
   return ZO_OK;
@@ -1834,10 +1930,7 @@ extern "C" int zo_qdir_apply_async(zo_ctx* c, uint64_t seed, uint64_t macro_step
     } else {
       // factorized: V is keyed by the step too (zo_engine.py:181-191)
       sampler_launch(c->planV, seed, c->d_step, 1, c->V, c->st);
-      for (auto& m : c->mats)
-        launch_fold_dev(m.W64, (int)m.m, (int)m.n, c->U + m.u_off, c->V + m.v_off, c->r, o4, lr,
-                        1.0 / std::sqrt((double)c->r), nullptr, m.W16, m.kind == K_EMBED ? (int)m.n : m.ldw,
-                        m.kind == K_EMBED ? 0 : 1, c->bf16, c->st);
+      launch_dense_update_dev(c, lr, o4, nullptr);
     }
   }
   if (lozo) c->a_dirty = true;

@@ -286,6 +286,15 @@ class ZoEngine:
         check(lib().zo_set_update_mode(self._h, 0 if mode == "exact" else 1))
         self.update_mode = mode
 
+    def set_schedule(self, schedule: str) -> None:
+        """GEMM schedule: "fast" (stream-K tail where it pays, default) or "row_invariant"
+        (no stream-K: per-example NLLs bitwise independent of the batch slicing over
+        GPUs; zob200.h zo_set_schedule)."""
+        if schedule not in ("fast", "row_invariant"):
+            raise ConfigError(f"schedule must be 'fast' or 'row_invariant', got {schedule!r}")
+        check(lib().zo_set_schedule(self._h, 0 if schedule == "fast" else 1))
+        self.schedule = schedule
+
     def update_dense(self, lr: float) -> None:
         check(lib().zo_update_dense(self._h, float(lr)))
 

@@ -1,6 +1,8 @@
 """The tensor-core factorized dense update (zo_set_update_mode 1; BASELINE config 5):
 W += (-(lr*c)/sqrt(r)) U V^T (zo_engine.py:449-450) with U V^T on tcgen05 (16-bit operands,
-fp32 accumulate) fused into the float64-master / 16-bit-shadow read-modify-write.
+fp32 accumulate) fused into the master / 16-bit-shadow read-modify-write.  In this mode the
+projection and embedding masters are held as fp32 (10 instead of 18 bytes per weight per
+update); switching modes converts them in place.
 
 Stated tolerance: each step's update agrees with the reference's float64 axpy_outer to
 1e-2 of its own magnitude (16-bit rounding of the N(0,1) directions, ~3e-3 RMS); the exact
@@ -64,3 +66,33 @@ def test_tensor_update_trajectory_close_to_exact():
         assert np.max(np.abs(dt - de)) <= 2 * UPDATE_REL * np.max(np.abs(de)), lid
     for e in engs.values():
         e.close()
+
+
+def test_fp32_master_mode_switch():
+    """Entering the tensor mode narrows the masters to fp32 in place (downloads read them back
+    widened), the scorer's embedding gather then reads the fp32 master -- the same fp32 values
+    the float64 path rounds to, so the NLLs are bitwise unchanged -- and leaving the mode widens
+    them again exactly."""
+    from paper_2605_28760_b200.engine import ZoEngine
+    eng = ZoEngine(256, 64, 2, 2, 15, max_batch=8, rank=32, estimator="factorized_sqrt_r")
+    eng.init_params(7, 0.08)
+    before = {lid: eng.download(lid) for lid in eng.lids}
+    rng = np.random.default_rng(0)
+    tok = rng.integers(0, 256, size=(8, 16)).astype(np.int32)
+    gold = tok[:, -1:].copy()
+    eng.prepare_probe(1e-3, 1)
+    nll64 = eng.score(tok, gold, nsign=1)
+    eng.set_update_mode("tensor")
+    for lid in eng.lids:
+        assert np.array_equal(eng.download(lid), before[lid].astype(np.float32).astype(np.float64)), lid
+    eng.prepare_probe(1e-3, 1)
+    assert np.array_equal(eng.score(tok, gold, nsign=1), nll64)
+    # an upload in fp32-master mode lands rounded to fp32
+    w = before["blk0.qkv"] * 1.5
+    eng.upload({"blk0.qkv": w})
+    assert np.array_equal(eng.download("blk0.qkv"), w.astype(np.float32).astype(np.float64))
+    eng.set_update_mode("exact")
+    for lid in eng.lids:
+        want = (w if lid == "blk0.qkv" else before[lid]).astype(np.float32).astype(np.float64)
+        assert np.array_equal(eng.download(lid), want), lid
+    eng.close()
