@@ -358,6 +358,10 @@ def main():
     eng.init_params(mcfg.init_seed, mcfg.init_scale)
     if fact and args.dense_update == "tensor":
         eng.set_update_mode("tensor")
+    if args.mode == "exact":
+        # exact-trajectory mode: row-invariant GEMM schedule, so every slicing of the batch over
+        # the ranks gives the N = 1 NLLs bit for bit (tests/test_gpu_cross_n.py)
+        eng.set_schedule("row_invariant")
     torch.cuda.synchronize()
     t_init = time.perf_counter() - t_init
 
@@ -384,6 +388,7 @@ def main():
     d_gold = torch.from_numpy(golds).cuda()
     nll_local = torch.zeros(2 * Bl, dtype=torch.float64, device="cuda")
     nll_all = torch.zeros(world * 2 * Bl, dtype=torch.float64, device="cuda")
+    nll_full = torch.zeros(2 * B, dtype=torch.float64, device="cuda")  # canonical [sign][example]
     out4_local = torch.zeros(4, dtype=torch.float64, device="cuda")
     out4_all = torch.zeros(world * 4, dtype=torch.float64, device="cuda")
 
@@ -391,11 +396,14 @@ def main():
         if tp is None:
             tp, gp = d_tok[t - t0_run].data_ptr(), d_gold[t - t0_run].data_ptr()
         if qdir:
-            import torch.distributed as dist
-            eng.qdir_score_async(zcfg.seed, t, G, rank, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, B)
+            # score half and apply half as captured CUDA graphs (args.graph), the 32 B
+            # all-gather between them
+            score = eng.qdir_score_graph if args.graph else eng.qdir_score_async
+            apply = eng.qdir_apply_graph if args.graph else eng.qdir_apply_async
+            score(zcfg.seed, t, G, rank, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, B)
             eng.out4_io(out4_local.data_ptr(), False)
             all_gather(out4_all, out4_local)  # 32 B per rank
-            eng.qdir_apply_async(zcfg.seed, t, G, zcfg.learning_rate, out4_all.data_ptr())
+            apply(zcfg.seed, t, G, zcfg.learning_rate, out4_all.data_ptr())
             if not fact and ((t + 1) * G) % zcfg.nu == 0:
                 eng.fold_async()
             return
@@ -405,14 +413,15 @@ def main():
             else:
                 eng.step_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, zcfg.learning_rate, False, tp, gp, Bl)
         else:
-            import torch.distributed as dist
-            eng.step_score_async(zcfg.seed, t, zcfg.nu, zcfg.epsilon, tp, gp, Bl)
+            score = eng.step_score_graph if args.graph else eng.step_score_async
+            apply = eng.step_apply_graph if args.graph else eng.step_apply_async
+            score(zcfg.seed, t, zcfg.nu, zcfg.epsilon, tp, gp, Bl)
             eng.nll_io(nll_local.data_ptr(), 2 * Bl, False)
             all_gather(nll_all, nll_local)
             # [rank][sign][b] -> [sign][rank*Bl + b] (canonical example order)
-            full = nll_all.view(world, 2, Bl).transpose(0, 1).contiguous()
-            eng.nll_io(full.data_ptr(), 2 * B, True)
-            eng.step_apply_async(zcfg.epsilon, zcfg.learning_rate, False, B)
+            nll_full.view(2, world, Bl).copy_(nll_all.view(world, 2, Bl).transpose(0, 1))
+            eng.nll_io(nll_full.data_ptr(), 2 * B, True)
+            apply(zcfg.epsilon, zcfg.learning_rate, False, B)
         if not fact and (t + 1) % zcfg.nu == 0:
             eng.fold_async()
 
@@ -457,9 +466,16 @@ def main():
     value = 1000.0 * G / ms_step  # reference steps (ZO directions) per second, whole job
     windows = sum(1 for t in range(t_first, t_first + args.steps) if (t * G) % zcfg.nu == 0)
     per_step, per_window = eng.graph_kernel_count()
-    if not (world == 1 and args.graph) or per_step <= 1:
-        per_step = launches_per_step(mcfg.n_layers, 4 * mcfg.n_layers + 1, False)  # eager paths: estimate
-    launches = args.steps * (per_step + (G - 1) * 6) + (0 if fact else windows * per_window)
+    split = eng.split_graph_kernels()  # [score, apply, qdir score, qdir apply] graph kernels
+    if world > 1 and args.graph:
+        # + the eager step-index write in front of the score graph (+ the macro-step base)
+        per_step = (split[2] + split[3] + 2) if qdir else (split[0] + split[1] + 1)
+        G_extra = 0
+    else:
+        G_extra = G - 1
+        if not (world == 1 and args.graph) or per_step <= 1:
+            per_step = launches_per_step(mcfg.n_layers, 4 * mcfg.n_layers + 1, False)  # eager paths: estimate
+    launches = args.steps * (per_step + G_extra * 6) + (0 if fact else windows * per_window)
 
     hbm_peak, tf_peak, tf_sust, peak_kind = peaks()
     cfg, scaling, _ = workload_config(args, world)

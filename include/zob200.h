@@ -132,6 +132,13 @@ int zo_sampler_flags(zo_ctx* ctx, uint32_t flags[3]);
  * per-example option NLL, float64 (model.py:202-215). */
 int zo_prepare_probe(zo_ctx* ctx, double epsilon, int32_t sign_mode);
 int zo_score(zo_ctx* ctx, const int32_t* tokens, const int32_t* gold, int32_t B, int32_t nsign, double* nll_out);
+/* every single-token option of the task from ONE sign-0 forward (evaluate_split /
+ * eval_accuracy, model.py:247-269, 444-460): the scored row prompt_len-1 never sees the
+ * option token, so its logits serve all options -- per option only the loss kernel runs.
+ * tokens: [B, T] (the option column is ignored), options: [n_opt] token ids, nll_out:
+ * [n_opt, B].  opt_len 1 and rank <= 8 only (ZO_ERR_CONFIG otherwise: score per option). */
+int zo_score_options(zo_ctx* ctx, const int32_t* tokens, const int32_t* options, int32_t n_opt, int32_t B,
+                     double* nll_out);
 /* canonical_mean per sign, c = (L+ - L-)/(2 eps), c_used, beta = -(lr*c_used)
  * (numerics.py:271-284, zo_engine.py:331,411,417): out4 = [L+, L-, c, beta].
  * Returns ZO_ERR_ABORT (no update armed) when a loss is not finite. */
@@ -198,6 +205,22 @@ int zo_qdir_score_async(zo_ctx* ctx, uint64_t seed, uint64_t macro_step, int32_t
 int zo_out4_io(zo_ctx* ctx, void* dev, int32_t to_ctx);
 int zo_qdir_apply_async(zo_ctx* ctx, uint64_t seed, uint64_t macro_step, int32_t G, double lr,
                         const double* out4_all_dev);
+/* the split steps with their bodies replayed as captured CUDA graphs (one graph launch per
+ * half instead of ~370 kernel launches; the collective runs between the two launches).
+ * Staging (step index, tokens, window fold / V resample) stays eager in front of the score
+ * graph.  Graphs are captured on first use per (seed, B, epsilon[, lr, divide_by_r]) /
+ * (B_total, epsilon, lr, divide_by_r) / (seed, G, lr, gather buffer) and dropped by
+ * zo_set_update_mode / zo_set_schedule.  Results are identical to the _async forms. */
+int zo_step_score_graph(zo_ctx* ctx, uint64_t seed, uint64_t step, int32_t nu, double epsilon,
+                        const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B);
+int zo_step_apply_graph(zo_ctx* ctx, double epsilon, double lr, int32_t divide_by_r, int32_t B_total);
+int zo_qdir_score_graph(zo_ctx* ctx, uint64_t seed, uint64_t macro_step, int32_t G, int32_t g, int32_t nu,
+                        double epsilon, double lr, int32_t divide_by_r, const int32_t* tokens_dev,
+                        const int32_t* gold_dev, int32_t B);
+int zo_qdir_apply_graph(zo_ctx* ctx, uint64_t seed, uint64_t macro_step, int32_t G, double lr,
+                        const double* out4_all_dev);
+/* kernels per launch of [score, apply, qdir score, qdir apply] graphs (0 before capture) */
+int zo_split_graph_kernels(zo_ctx* ctx, int32_t out[4]);
 /* materialising training-loop comparand (baseline_loop.py:122-239, run_baseline;
  * replaces the _Probe / VectorProbe writes of baseline_loop.py:68-119, 191-221):
  * zo_baseline_directions samples the step's U (+ V at a window start / every

@@ -61,6 +61,7 @@ SIGNATURES = [
     ("zo_sampler_flags", _c.c_int, [_P, _c.POINTER(_c.c_uint32)]),
     ("zo_prepare_probe", _c.c_int, [_P, _c.c_double, _c.c_int32]),
     ("zo_score", _c.c_int, [_P, _P, _P, _c.c_int32, _c.c_int32, _P]),
+    ("zo_score_options", _c.c_int, [_P, _P, _P, _c.c_int32, _c.c_int32, _P]),
     ("zo_coefficient", _c.c_int, [_P, _c.c_int32, _c.c_double, _c.c_double, _c.c_int32, _P]),
     ("zo_set_coefficient", _c.c_int, [_P, _P]),
     ("zo_update_u", _c.c_int, [_P]),
@@ -83,6 +84,13 @@ SIGNATURES = [
                                        _c.c_double, _c.c_double, _c.c_int32, _P, _P, _c.c_int32]),
     ("zo_out4_io", _c.c_int, [_P, _P, _c.c_int32]),
     ("zo_qdir_apply_async", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _P]),
+    ("zo_step_score_graph", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _P, _P,
+                                       _c.c_int32]),
+    ("zo_step_apply_graph", _c.c_int, [_P, _c.c_double, _c.c_double, _c.c_int32, _c.c_int32]),
+    ("zo_qdir_score_graph", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_int32, _c.c_int32,
+                                       _c.c_double, _c.c_double, _c.c_int32, _P, _P, _c.c_int32]),
+    ("zo_qdir_apply_graph", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32, _c.c_double, _P]),
+    ("zo_split_graph_kernels", _c.c_int, [_P, _P]),
     ("zo_baseline_directions", _c.c_int, [_P, _c.c_uint64, _c.c_uint64, _c.c_int32]),
     ("zo_baseline_pass", _c.c_int, [_P, _c.c_int32, _c.c_double, _c.c_int32]),
     ("zo_baseline_update", _c.c_int, [_P, _c.c_double, _c.c_int32]),

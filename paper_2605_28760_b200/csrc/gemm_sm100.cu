@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -334,10 +335,16 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // per MMA), 2 tf32 (kind::tf32 on fp32 storage, 32 elements per K block, K = 8 per MMA; the
 // same 32 bytes per MMA step, so the smem ring and descriptors are shared)
 template <int BN, int EPI, int DT, int XR, int CG>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ? 320 : 192, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmB2, GemmParams p) {
-  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE64>;
+  // EPI_UPDATE32: EPI_UPDATE64 over an fp32 master (fp32 arithmetic, its own register budget)
+  constexpr bool UPD = EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32, M32 = EPI == EPI_UPDATE32;
+  // epilogue warp groups: the update variants run two groups of 4 warps (320 threads) -- their
+  // epilogue is the whole kernel (a read-modify-write of every master block), latency-bound
+  // at one warp per scheduler; group g takes the master-block rounds / column chunks = g mod 2
+  constexpr int EGRP = UPD ? 2 : 1;
+  using C = GemmCfg<BN, CG, UPD>;
   constexpr bool BF16 = DT == 1, TF32 = DT == 2;
   constexpr int KE = TF32 ? 32 : 64;  // K elements per 128-byte block
   constexpr uint32_t FMT = TF32 ? 2u : BF16 ? 1u : 0u;  // instruction-descriptor a/b format
@@ -352,11 +359,11 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + C::W_SLOTS * C::W_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4 + 2 * C::W_NBAR);
   // TMA-streamed master update (EPI_UPDATE64 on a projection): W64 blocks in/out through sW
-  const bool wtma = (EPI == EPI_UPDATE64) && p.upd_transposed;
+  const bool wtma = UPD && p.upd_transposed;
   const uint32_t wfull0 = smem_u32(bars + 2 * C::STAGES + 4), wempty0 = wfull0 + 8 * C::W_NBAR;
   // master-block ring geometry: fp32 masters use twice the slots at half the size
-  const int wslots = (EPI == EPI_UPDATE64 && p.upd_m32) ? C::W_NBAR : C::W_SLOTS;
-  const uint32_t wbytes = (EPI == EPI_UPDATE64 && p.upd_m32) ? C::W_BYTES / 2 : C::W_BYTES;
+  constexpr int wslots = M32 ? C::W_NBAR : C::W_SLOTS;
+  constexpr uint32_t wbytes = M32 ? C::W_BYTES / 2 : C::W_BYTES;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = smem_u32(bars + 2 * C::STAGES + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -372,7 +379,7 @@ __global__ void __launch_bounds__(192, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8 * a, 1);
-      mbar_init(tempty0 + 8 * a, 4 * CG);  // every epilogue warp of the pair arrives at the leader
+      mbar_init(tempty0 + 8 * a, 4 * EGRP * CG);  // every epilogue warp of the pair arrives at the leader
     }
     for (int w = 0; w < C::W_NBAR; ++w) {
       mbar_init(wfull0 + 8 * w, 1);
@@ -439,7 +446,7 @@ __global__ void __launch_bounds__(192, 1)
             phase ^= 1;
           }
         }
-        if constexpr (EPI == EPI_UPDATE64) {
+        if constexpr (UPD) {
           // this CTA's master block rows = D columns (input index i), block cols = its 128
           // D rows (output index j); tmB2 is the float64 map over W64 [m, n]
           if (wtma) {
@@ -505,7 +512,10 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
-    int wround_e = 0;        // EPI_UPDATE64: master blocks consumed so far
+    const int grp = (warp - 2) >> 2;  // epilogue warp group (0 unless UPD)
+    const bool storer = ((warp - 2) & 3) == 0 && lane == 0;  // UPD: the group's TMA-store thread
+    int wround_e = 0;        // EPI_UPDATE64: master blocks consumed so far (all groups, global order)
+    int wprev = -1;          // EPI_UPDATE64: this group's previous round (its slot is released next)
     const int erow = q * 32 + lane;  // row within the 128-row tile
     int it = 0;
     SegIter si;
@@ -620,7 +630,7 @@ __global__ void __launch_bounds__(192, 1)
           v[4 * j + 3] += w.w;
         }
       };
-      if constexpr (EPI == EPI_UPDATE64) {
+      if constexpr (UPD) {
         if (wtma) {
           // projection: the master block of round r ([32 input rows i][128 output cols j],
           // this warp's 32 j columns) arrives by TMA; lane j updates its column in place in
@@ -631,24 +641,28 @@ __global__ void __launch_bounds__(192, 1)
           const bool skip = p.upd_abort ? (*p.upd_abort != 0u)
                                         : !(isfinite(p.upd_out4[0]) && isfinite(p.upd_out4[1]));
           const double alpha = -(p.upd_lr * p.upd_out4[2]) * p.upd_scale;
+          const int rbase = wround_e;  // global index of this tile's first round (producer order)
 #pragma unroll 1
-          for (int r = 0; r < BN / 32; ++r, ++wround_e) {
-            const int ws = wround_e % wslots;
+          for (int r = grp; r < BN / 32; r += EGRP) {
+            const int gi = rbase + r;
+            const int ws = gi % wslots;
             float v[32];
             tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + 32 * r, v);
-            mbar_wait(wfull0 + 8 * ws, (wround_e / wslots) & 1);
+            mbar_wait(wfull0 + 8 * ws, (gi / wslots) & 1);
             double* blk = reinterpret_cast<double*>(sW + ws * wbytes) + erow;  // column erow
             float* blk32 = reinterpret_cast<float*>(sW + ws * wbytes) + erow;  // fp32 master
             const int col0 = n0 + 32 * r;
             if (!skip) {
-              double w[32];
-              if (p.upd_m32) {
+              using WT = std::conditional_t<M32, float, double>;
+              WT w[32];
+              if constexpr (M32) {  // fp32 master: one fp32 FMA per weight, rounded once
+                const float alpha32 = (float)alpha;
 #pragma unroll
-                for (int i = 0; i < 32; ++i) w[i] = (double)blk32[i * C::BM];
+                for (int i = 0; i < 32; ++i) w[i] = blk32[i * C::BM];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                  w[i] = (double)(float)fma(alpha, (double)v[i], w[i]);
-                  blk32[i * C::BM] = (float)w[i];
+                  w[i] = fmaf(alpha32, v[i], w[i]);
+                  blk32[i * C::BM] = w[i];
                 }
               } else {
 #pragma unroll
@@ -679,8 +693,8 @@ __global__ void __launch_bounds__(192, 1)
               }
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
-            named_bar_sync(2, 128);
-            if (warp == 2 && lane == 0) {
+            named_bar_sync(2 + grp, 128);
+            if (storer) {
               if (!skip) {
                 asm volatile(
                     "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
@@ -689,55 +703,52 @@ __global__ void __launch_bounds__(192, 1)
                     : "memory");
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
               }
-              // the previous round's store has finished reading its slot: hand it back
+              // this group's previous round's store has finished reading its slot: hand it back
+              // (with an even slot count a slot always serves the same group)
               asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-              if (wround_e > 0) mbar_arrive(wempty0 + 8 * ((wround_e - 1) % wslots));
+              if (wprev >= 0) mbar_arrive(wempty0 + 8 * (wprev % wslots));
             }
+            wprev = gi;
           }
+          wround_e = rbase + BN / 32;
           goto tile_done;
         }
-        // W64 += alpha * D with the 16-bit shadow rewritten from the new value, 64 columns per
-        // round: the 64 master loads of a round are all in flight before the first is used
-        // (the kernel is HBM-latency-bound: 18 B per weight against 256 MMA FLOPs).  Every
-        // lane runs the TMEM loads (.sync.aligned); memory ops are guarded per row / column.
+        // W64 += alpha * D with the 16-bit shadow rewritten from the new value (the embedding's
+        // untransposed master; the kernel is HBM-latency-bound: 18 B per weight against 256
+        // MMA FLOPs).  Every lane runs the TMEM loads (.sync.aligned); memory ops are guarded
+        // per row / column.
         const bool skip = p.upd_abort ? (*p.upd_abort != 0u)
                                       : !(isfinite(p.upd_out4[0]) && isfinite(p.upd_out4[1]));
         const double alpha = -(p.upd_lr * p.upd_out4[2]) * p.upd_scale;
         const bool live = !skip && row_ok;
 #pragma unroll 1
-        for (int c = 0; c < bnc; c += 64) {
+        for (int c = 32 * grp; c < bnc; c += 32 * EGRP) {
+          // 32 columns per round (the two warp groups alternate): the 32 master loads are in
+          // flight before the first is used
           const int col0 = n0 + c;
-          const int nc = live ? max(0, min(64, p.N - col0)) : 0;
-          double w[64];
+          const int nc = live ? max(0, min(32, p.N - col0)) : 0;
+          using WT = std::conditional_t<M32, float, double>;
+          WT w[32];
           const size_t base = p.upd_transposed ? (size_t)col0 * p.upd_ld64 + row : (size_t)row * p.upd_ld64 + col0;
           const size_t step = p.upd_transposed ? (size_t)p.upd_ld64 : 1;
-          float* w32p = reinterpret_cast<float*>(p.upd_w64);
+          WT* wp = reinterpret_cast<WT*>(p.upd_w64) + base;
 #pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (i < nc)
-              w[i] = p.upd_m32 ? (double)__ldcs(w32p + base + (size_t)i * step) : __ldcs(p.upd_w64 + base + (size_t)i * step);
+          for (int i = 0; i < 32; ++i)
+            if (i < nc) w[i] = __ldcs(wp + (size_t)i * step);
+          float v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float v[32];
-            if (c + 32 * h < bnc)
-              tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c + 32 * h, v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (32 * h + i < nc) {
-                w[32 * h + i] = fma(alpha, (double)v[i], w[32 * h + i]);
-                if (p.upd_m32) {
-                  w[32 * h + i] = (double)(float)w[32 * h + i];
-                  __stcs(w32p + base + (size_t)(32 * h + i) * step, (float)w[32 * h + i]);
-                } else {
-                  __stcs(p.upd_w64 + base + (size_t)(32 * h + i) * step, w[32 * h + i]);
-                }
-              }
-          }
+          for (int i = 0; i < 32; ++i)
+            if (i < nc) {
+              if constexpr (M32) w[i] = fmaf((float)alpha, v[i], w[i]);
+              else w[i] = fma(alpha, (double)v[i], w[i]);
+              __stcs(wp + (size_t)i * step, w[i]);
+            }
           if (nc == 0) continue;
           uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)row * p.upd_ld16 + col0;
-          if (nc == 64 && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
+          if (nc == 32 && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
               uint4 u;
               u.x = pack2<BF16>((float)w[8 * j], (float)w[8 * j + 1]);
               u.y = pack2<BF16>((float)w[8 * j + 2], (float)w[8 * j + 3]);
@@ -747,7 +758,7 @@ __global__ void __launch_bounds__(192, 1)
             }
           } else {
 #pragma unroll
-            for (int i = 0; i < 64; ++i)
+            for (int i = 0; i < 32; ++i)
               if (i < nc) o[i] = (uint16_t)(pack2<BF16>((float)w[i], 0.f) & 0xffffu);
           }
         }
@@ -899,8 +910,8 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
   }
-  if constexpr (EPI == EPI_UPDATE64)
-    if (wtma && warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if constexpr (UPD)
+    if (wtma && warp >= 2 && ((warp - 2) & 3) == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();
   if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/epilogues are done before TMEM is freed
@@ -1035,7 +1046,8 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms) {
 
 template <int BN, int EPI, int BF16, int XR, int CG>
 static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = -1, int last_ksteps = -1) {
-  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE64>;
+  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32>;
+  constexpr int NT = (EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ? 320 : 192;  // k_gemm's launch bounds
   static bool attr_set = false;
   if (!attr_set) {
     ZO_CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI, BF16, XR, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1084,11 +1096,11 @@ static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = 
   p.upd_scale = g.upd_scale;
   p.upd_abort = g.upd_abort;
   if constexpr (CG == 1) {
-    launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(192), C::SMEM, st, g.tmA, g.tmB, g.tmB2, p);
+    launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(NT), C::SMEM, st, g.tmA, g.tmB, g.tmB2, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.grid);
-    cfg.blockDim = dim3(192);
+    cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
@@ -1142,7 +1154,10 @@ static void launch_e(const GemmDesc& g, cudaStream_t st) {
       else launch_t<BN, EPI_GELU16_EXT, BF16, 8, CG>(g, st);
       break;
     case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16, 0, CG>(g, st); break;
-    case EPI_UPDATE64: launch_t<BN, EPI_UPDATE64, BF16, 0, CG>(g, st); break;
+    case EPI_UPDATE64:
+      if (g.upd_m32) launch_t<BN, EPI_UPDATE32, BF16, 0, CG>(g, st);
+      else launch_t<BN, EPI_UPDATE64, BF16, 0, CG>(g, st);
+      break;
     default: launch_t<BN, EPI_STORE32, BF16, 0, CG>(g, st); break;
   }
 }

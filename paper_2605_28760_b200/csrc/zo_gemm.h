@@ -16,6 +16,8 @@ enum EpiKind : int {
   EPI_UPDATE64 = 5,    // factorized dense update on the tensor cores (zo_engine.py:449-450):
                        // W64 += alpha * acc (alpha = -(lr*c)*scale from the device coefficient,
                        // skipped when the step aborted), 16-bit shadow rewritten in the same pass
+  EPI_UPDATE32 = 6,    // EPI_UPDATE64 on an fp32 master (kernel variant; plans say EPI_UPDATE64 +
+                       // upd_m32 = 1)
 };
 
 // D[M, N] = A[M, Kp] * B[N, Kp]^T, both operands K-major 16-bit, fp32 accumulate.

@@ -97,7 +97,7 @@ __device__ __forceinline__ void write_ext(void* out, size_t base, int k, float t
 template <int GROUPS>
 __global__ void __launch_bounds__(256) k_ext_finalize(const float* __restrict__ tpart, int ntiles, int ld, int M,
                                                       int r, void* __restrict__ a, int lda, int K, int ext_terms,
-                                                      bool bf16) {
+                                                      bool bf16, int neg_from) {
   constexpr int PAIRS = 256 / GROUPS;
   pdl_launch_dependents();
   pdl_wait();
@@ -119,19 +119,20 @@ __global__ void __launch_bounds__(256) k_ext_finalize(const float* __restrict__ 
 #pragma unroll
     for (int q = 1; q < GROUPS; ++q) s += part[q][p];
     const int row = (int)(i / r), k = (int)(i % r);
+    if (neg_from >= 0 && row >= neg_from) s = -s;
     write_ext(a, (size_t)row * lda + K, k, s, ext_terms, bf16);
   }
 }
 
 void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
-                         int ext_terms, bool bf16, cudaStream_t st) {
+                         int ext_terms, bool bf16, cudaStream_t st, int neg_from) {
   const int64_t pairs = (int64_t)M * r;
   if (ntiles <= 16)
     launch_pdl(k_ext_finalize<8>, dim3((unsigned)((pairs + 31) / 32)), dim3(256), 0, st, tpart, ntiles, ld, M, r, a,
-               lda, K, ext_terms, bf16);
+               lda, K, ext_terms, bf16, neg_from);
   else
     launch_pdl(k_ext_finalize<32>, dim3((unsigned)((pairs + 7) / 8)), dim3(256), 0, st, tpart, ntiles, ld, M, r, a,
-               lda, K, ext_terms, bf16);
+               lda, K, ext_terms, bf16, neg_from);
 }
 
 // ------------------------------------------------------------------ embed

@@ -48,7 +48,7 @@ void launch_attention(const void* qkv, int ldq, void* ctx, int ldc, int nseq, in
                       const AttnExt& x, cudaStream_t st);
 // t_k = sum over tiles of tpart[tile][row][k] (fixed order) -> ext columns (hi, lo, hi) of a[:, K:]
 void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
-                         int ext_terms, bool bf16, cudaStream_t st);
+                         int ext_terms, bool bf16, cudaStream_t st, int neg_from = -1);
 // dst row i = src row of the i-th scored (sign, sequence, option token): the compact
 // rows the last layer's pruned tail runs on (row_bytes, strides in bytes)
 void launch_gather_scored(const void* src, size_t ld_src_bytes, void* dst, size_t ld_dst_bytes, int row_bytes,

@@ -57,7 +57,11 @@ struct LayerPlan {
   // reduced in a fixed order into the activation's extension columns (ext_a / ext_ld / ext_K)
   std::vector<GemmDesc> ext;
   std::vector<void*> ext_a;
-  std::vector<int> ext_ld, ext_K, ext_M;
+  std::vector<int> ext_ld, ext_K, ext_M, ext_neg;
+  // factorized estimator: P- = -P+ exactly (A = 0), so one GEMM over both probe halves with
+  // P+ and a negated finalize of the -eps rows (ext_neg = first negated row) -- 1 launch per
+  // matrix instead of 2, bitwise the same t
+  int ext_signs = 0;
 };
 // real32 (3xTF32) scorer plan: the four projections of every layer + the LM head
 struct RowPlan32 {
@@ -215,9 +219,25 @@ struct zo_ctx {
   } gkey{};
   bool gkey_valid = false;
   int graph_kernels = 0;  // kernel nodes of the captured step body
+  // captured halves of the multi-GPU step (zo_step_score_graph / zo_step_apply_graph,
+  // zo_qdir_*_graph): the collective runs between two graph launches
+  struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<uint64_t> key;
+    bool valid = false;
+    int kernels = 0;
+  };
+  GraphSlot gs_score, gs_apply, gs_qscore, gs_qapply;
+  uint64_t* d_base = nullptr;  // q-direction macro-step base step (t * G), set before the apply graph
+  void drop_graphs() {
+    gkey_valid = false;
+    for (GraphSlot* g : {&gs_score, &gs_apply, &gs_qscore, &gs_qapply}) g->valid = false;
+  }
 
   ~zo_ctx() {
     if (gexec) cudaGraphExecDestroy(gexec);
+    for (GraphSlot* g : {&gs_score, &gs_apply, &gs_qscore, &gs_qapply})
+      if (g->exec) cudaGraphExecDestroy(g->exec);
     if (cap_st) cudaStreamDestroy(cap_st);
     if (h_tok) cudaFreeHost(h_tok);
     if (h_gold) cudaFreeHost(h_gold);
@@ -242,6 +262,7 @@ bool pdl_enabled() {
 namespace {
 
 __global__ void k_set_u64(uint64_t* p, uint64_t v) { *p = v; }
+__global__ void k_step_from_base(uint64_t* step, const uint64_t* base, uint64_t g) { *step = *base + g; }
 
 int fail(const Error& e) {
   g_last_error = e.msg;
@@ -295,6 +316,11 @@ void set_bias(const zo_ctx* c, GemmDesc& g, const float* bias, int rows_per_sign
   g.bias_vstride = c->vstride;
 }
 
+// high-rank extension of a factorized probe pair: one GEMM for both signs (LayerPlan::ext_signs)
+bool ext_merged(const zo_ctx* c, int nsign) {
+  return !c->fused_ext && nsign == 2 && c->d.estimator == ZO_EST_FACTORIZED && !c->full_scope;
+}
+
 RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
   const int key = 2 * M + (nsign == 1 ? 1 : 0);
   auto it = c->plans.find(key);
@@ -344,19 +370,24 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
       lp.ext_ld.resize(8);
       lp.ext_K.resize(8);
       lp.ext_M.resize(8);
+      lp.ext_neg.resize(8);
+      const bool merged = ext_merged(c, nsign);
+      lp.ext_signs = merged ? 1 : nsign;
+      const int mext = merged ? 2 * rps : rps;
       for (int i = 0; i < 4; ++i)
-        for (int sg = 0; sg < nsign; ++sg) {
+        for (int sg = 0; sg < lp.ext_signs; ++sg) {
           uint16_t* a = static_cast<uint16_t*>(acts[i]) + (size_t)sg * rps * lds[i];
           GemmDesc& g = lp.ext[2 * i + sg];
           // t = a . P_s: a few output tiles over K = 5120 .. 20480 -- split K so every SM works
-          gemm_plan(g, a, rps, lds[i], c->P16T + (size_t)sg * c->su + mm[i]->u_off, c->r, (int)mm[i]->m,
+          gemm_plan(g, a, mext, lds[i], c->P16T + (size_t)sg * c->su + mm[i]->u_off, c->r, (int)mm[i]->m,
                     (int)mm[i]->m, EPI_STORE32, c->bf16, c->xws, c->r, c->num_sms);
-          const int tiles = ((rps + 127) / 128) * ((c->r + g.bn - 1) / g.bn);
+          const int tiles = ((mext + 127) / 128) * ((c->r + g.bn - 1) / g.bn);
           gemm_enable_splitk(g, std::max(1, c->num_sms / tiles), (long)c->Mpad * c->r);
           lp.ext_a[2 * i + sg] = a;
           lp.ext_ld[2 * i + sg] = lds[i];
           lp.ext_K[2 * i + sg] = (int)mm[i]->m;
-          lp.ext_M[2 * i + sg] = rps;
+          lp.ext_M[2 * i + sg] = mext;
+          lp.ext_neg[2 * i + sg] = merged ? rps : -1;
         }
     }
     rp.layers.push_back(lp);
@@ -563,14 +594,14 @@ void do_score(zo_ctx* c, int B, int nsign) {
                c->Pm + e.u_off, c->V32 + e.v_off,
                c->r, c->pe, pos, M, c->st);
   if (!c->fused_ext)  // high rank: 16-bit transposed probe operands of the extension GEMMs
-    launch_p16t_all(c->Pp, c->Pm, c->su, c->p16t_tab, c->p16t_n, c->p16t_tiles, c->r, nsign, c->P16T, c->bf16,
-                    c->st);
+    launch_p16t_all(c->Pp, c->Pm, c->su, c->p16t_tab, c->p16t_n, c->p16t_tiles, c->r, ext_merged(c, nsign) ? 1 : nsign,
+                    c->P16T, c->bf16, c->st);
   auto ext_gemm = [&](const LayerPlan& lp, int i) {
-    for (int sg = 0; sg < nsign; ++sg) {
+    for (int sg = 0; sg < lp.ext_signs; ++sg) {
       const int j = 2 * i + sg;
       gemm_launch(lp.ext[j], c->st);
       launch_ext_finalize(c->xws, lp.ext[j].ksplit, c->Mpad, lp.ext_M[j], c->r, lp.ext_a[j], lp.ext_ld[j],
-                          lp.ext_K[j], 1, c->bf16, c->st);
+                          lp.ext_K[j], 1, c->bf16, c->st, lp.ext_neg[j]);
     }
   };
   for (int l = 0; l < c->d.n_layers; ++l) {
@@ -989,6 +1020,7 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
   c->tok = c->mem.get<int32_t>((size_t)d.max_batch * c->T);
   c->gold = c->mem.get<int32_t>((size_t)2 * d.max_batch * d.opt_len);
   c->d_step = c->mem.get<uint64_t>(1);
+  c->d_base = c->mem.get<uint64_t>(1);
   c->sk_ws = c->mem.get<float>(gemm_sk_ws_floats(c->num_sms));
   c->sk_flags = c->mem.get<unsigned>(c->num_sms + 1);
   if (env_streamk_off()) c->streamk = false;
@@ -1346,7 +1378,7 @@ int zo_set_update_mode(zo_ctx* c, int32_t mode) {
   }
   c->fast_update = mode == 1;
   c->upd_plans.clear();
-  c->gkey_valid = false;  // the captured step graph holds the old update
+  c->drop_graphs();  // the captured step graphs hold the old update
   return ZO_OK;
   ZO_API_END
 }
@@ -1359,7 +1391,7 @@ int zo_set_schedule(zo_ctx* c, int32_t row_invariant) {
     ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
     c->streamk = sk;
     c->plans.clear();        // GEMM plans carry the stream-K split
-    c->gkey_valid = false;   // the captured step graph holds the old plans
+    c->drop_graphs();        // the captured step graphs hold the old plans
   }
   return ZO_OK;
   ZO_API_END
@@ -1408,6 +1440,37 @@ int zo_score(zo_ctx* c, const int32_t* tokens, const int32_t* gold, int32_t B, i
     ZO_CUDA_TRY(cudaMemcpyAsync(nll_out, c->nll, (size_t)nsign * B * 8, cudaMemcpyDeviceToHost, c->st));
     ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
   }
+  ZO_CUDA_TRY(cudaGetLastError());
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_score_options(zo_ctx* c, const int32_t* tokens, const int32_t* options, int32_t n_opt, int32_t B,
+                     double* nll_out) {
+  ZO_API_BEGIN
+  check(c->d.opt_len == 1, ZO_ERR_CONFIG, "one-forward option scoring needs single-token options");
+  check(c->fused_ext && !c->real32, ZO_ERR_CONFIG, "one-forward option scoring: rank <= 8, 16-bit modes");
+  check(n_opt >= 1 && B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "bad option count / batch size");
+  std::vector<int32_t> gold((size_t)B);
+  for (int32_t j = 0; j < n_opt; ++j) {
+    std::fill(gold.begin(), gold.end(), options[j]);
+    if (j == 0) {
+      stage_batch(c, tokens, gold.data(), B, 1);
+      do_score(c, B, 1);  // logits of the scored rows stay in c->logits
+    } else {
+      for (int32_t b = 0; b < B; ++b)
+        check(options[j] >= 0 && options[j] < c->d.vocab, ZO_ERR_INPUT, "gold token id out of range");
+      ZO_CUDA_TRY(cudaStreamSynchronize(c->st));  // the pinned gold staging is reused
+      std::memcpy(c->h_gold, gold.data(), (size_t)B * 4);
+      std::memcpy(c->h_gold + B, gold.data(), (size_t)B * 4);
+      ZO_CUDA_TRY(cudaMemcpyAsync(c->gold, c->h_gold, (size_t)2 * B * 4, cudaMemcpyHostToDevice, c->st));
+      const Matrix& e = c->mats[c->i_embed];
+      launch_loss(c->logits, c->ldl, c->d.vocab, c->z, c->r, c->Pp + e.u_off, c->Pm + e.u_off, c->gold, B, 1,
+                  c->loss_ws, c->loss_cnt, c->nll, c->st);
+    }
+    ZO_CUDA_TRY(cudaMemcpyAsync(nll_out + (size_t)j * B, c->nll, (size_t)B * 8, cudaMemcpyDeviceToHost, c->st));
+  }
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
   ZO_CUDA_TRY(cudaGetLastError());
   return ZO_OK;
   ZO_API_END
@@ -1548,9 +1611,11 @@ uint64_t zo_digest_chain(const char* const* lids, const double* arena, const int
 // zo_step_score_async = directions + probes + paired scoring (per-example NLLs
 // in the ctx); zo_step_apply_async = canonical mean / c / update over B_total
 // examples.  Multi-GPU exact mode all-gathers the NLLs between the two.
-extern "C" int zo_step_score_async(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps,
-                                   const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
-  ZO_API_BEGIN
+namespace {
+// Step index, device-resident tokens/gold into the ctx, and the window work (fold of the
+// unfolded window mass + V resample at a window start): the eager head of every step.
+void stage_dev(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, const int32_t* tokens_dev,
+               const int32_t* gold_dev, int32_t B) {
   check(!c->dense, ZO_ERR_CONFIG, "dense_mezo has no serving-path form (runtime.py:275-279): use the materialising loop");
   check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
   check(B >= 1 && B <= c->d.max_batch, ZO_ERR_DIMENSION, "batch size out of range");
@@ -1567,27 +1632,138 @@ extern "C" int zo_step_score_async(zo_ctx* c, uint64_t seed, uint64_t step, int3
     write_vext_all(c);
     c->v_window = wstart;
   }
+}
+
+// directions (U, z), probes and paired scoring of the staged step: per-example NLLs in the ctx
+void score_body(zo_ctx* c, uint64_t seed, double eps, int32_t B) {
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
   sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
   sample_z(c, seed);
   const double scale = lozo ? 1.0 : 1.0 / std::sqrt((double)c->r);
   launch_prep_probe(lozo ? c->A : nullptr, c->U, c->su, eps, scale, c->Pp, c->Pm, c->st);
   vec_probe(c, eps);
   do_score(c, B, 2);
+}
+
+// canonical mean / c / update over B_total gathered NLLs
+void apply_body(zo_ctx* c, double eps, double lr, int32_t divide_by_r, int32_t B_total) {
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  launch_coefficient(c->nll, B_total, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
+  if (lozo)
+    launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
+  else
+    launch_dense_update_dev(c, lr, c->out4, c->abort_flag);
+  vec_update(c, c->out4, lr, c->abort_flag);
+}
+
+// q-direction apply: regenerate the G counter-keyed U's (steps d_base + g) and apply the G
+// gathered coefficients in g order
+void qdir_apply_body(zo_ctx* c, uint64_t seed, int32_t G, double lr, const double* out4_all_dev) {
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  for (int32_t g = 0; g < G; ++g) {
+    k_step_from_base<<<1, 1, 0, c->st>>>(c->d_step, c->d_base, (uint64_t)g);
+    sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
+    sample_z(c, seed);
+    const double* o4 = out4_all_dev + 4 * (size_t)g;
+    vec_update(c, o4, lr, nullptr);
+    if (lozo) {
+      launch_update(c->A, c->U, c->su, o4, nullptr, c->st);
+    } else {
+      // factorized: V is keyed by the step too (zo_engine.py:181-191)
+      sampler_launch(c->planV, seed, c->d_step, 1, c->V, c->st);
+      launch_dense_update_dev(c, lr, o4, nullptr);
+    }
+  }
+  // the ctx out4 mirrors the last direction (zo_read_out4)
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->out4, out4_all_dev + 4 * (size_t)(G - 1), 32, cudaMemcpyDeviceToDevice, c->st));
+}
+
+// Launch `body` as a captured CUDA graph: the first use of a key runs it eagerly (warming
+// plans / attributes) and captures it; later uses with the same key replay the graph.
+template <class F>
+void run_graph(zo_ctx* c, zo_ctx::GraphSlot& gs, const std::vector<uint64_t>& key, F&& body) {
+  if (gs.valid && gs.key == key) {
+    ZO_CUDA_TRY(cudaGraphLaunch(gs.exec, c->st));
+    return;
+  }
+  body();
+  if (!c->cap_st) ZO_CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_st, cudaStreamNonBlocking));
+  ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  if (gs.exec) {
+    ZO_CUDA_TRY(cudaGraphExecDestroy(gs.exec));
+    gs.exec = nullptr;
+  }
+  gs.valid = false;
+  cudaStream_t user = c->st;
+  c->st = c->cap_st;
+  cudaGraph_t graph = nullptr;
+  try {
+    ZO_CUDA_TRY(cudaStreamBeginCapture(c->cap_st, cudaStreamCaptureModeThreadLocal));
+    body();
+    ZO_CUDA_TRY(cudaStreamEndCapture(c->cap_st, &graph));
+  } catch (...) {
+    c->st = user;
+    throw;
+  }
+  c->st = user;
+  ZO_CUDA_TRY(cudaGraphInstantiate(&gs.exec, graph, 0));
+  size_t n = 0;
+  ZO_CUDA_TRY(cudaGraphGetNodes(graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  ZO_CUDA_TRY(cudaGraphGetNodes(graph, nodes.data(), &n));
+  int k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    ZO_CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
+    k += ty == cudaGraphNodeTypeKernel;
+  }
+  gs.kernels = k;
+  ZO_CUDA_TRY(cudaGraphDestroy(graph));
+  gs.key = key;
+  gs.valid = true;
+}
+
+uint64_t dbits(double v) {
+  uint64_t u;
+  std::memcpy(&u, &v, 8);
+  return u;
+}
+}  // namespace
+
+extern "C" int zo_step_score_async(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps,
+                                   const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
+  ZO_API_BEGIN
+  stage_dev(c, seed, step, nu, tokens_dev, gold_dev, B);
+  score_body(c, seed, eps, B);
   return ZO_OK;
   ZO_API_END
 }
 
 extern "C" int zo_step_apply_async(zo_ctx* c, double eps, double lr, int32_t divide_by_r, int32_t B_total) {
   ZO_API_BEGIN
-  const bool lozo = c->d.estimator == ZO_EST_LOZO;
-  launch_coefficient(c->nll, B_total, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
-  if (lozo) {
-    launch_update(c->A, c->U, c->su, c->out4, c->abort_flag, c->st);
-    c->a_dirty = true;
-  } else {
-    launch_dense_update_dev(c, lr, c->out4, c->abort_flag);
-  }
-  vec_update(c, c->out4, lr, c->abort_flag);
+  apply_body(c, eps, lr, divide_by_r, B_total);
+  if (c->d.estimator == ZO_EST_LOZO) c->a_dirty = true;
+  return ZO_OK;
+  ZO_API_END
+}
+
+// The two halves of the multi-GPU exact-mode step as captured graphs (one graph launch each
+// instead of ~370 kernel launches); staging and window work stay eager in front of the score
+// graph, the NLL all-gather runs between the two.
+extern "C" int zo_step_score_graph(zo_ctx* c, uint64_t seed, uint64_t step, int32_t nu, double eps,
+                                   const int32_t* tokens_dev, const int32_t* gold_dev, int32_t B) {
+  ZO_API_BEGIN
+  stage_dev(c, seed, step, nu, tokens_dev, gold_dev, B);
+  run_graph(c, c->gs_score, {seed, (uint64_t)B, dbits(eps)}, [&] { score_body(c, seed, eps, B); });
+  return ZO_OK;
+  ZO_API_END
+}
+
+extern "C" int zo_step_apply_graph(zo_ctx* c, double eps, double lr, int32_t divide_by_r, int32_t B_total) {
+  ZO_API_BEGIN
+  run_graph(c, c->gs_apply, {(uint64_t)B_total, dbits(eps), dbits(lr), (uint64_t)divide_by_r},
+            [&] { apply_body(c, eps, lr, divide_by_r, B_total); });
+  if (c->d.estimator == ZO_EST_LOZO) c->a_dirty = true;
   return ZO_OK;
   ZO_API_END
 }
@@ -1887,16 +2063,31 @@ extern "C" int zo_qdir_score_async(zo_ctx* c, uint64_t seed, uint64_t macro_step
                                    double eps, double lr, int32_t divide_by_r, const int32_t* tokens_dev,
                                    const int32_t* gold_dev, int32_t B) {
   ZO_API_BEGIN
-  check(!c->dense, ZO_ERR_CONFIG, "dense_mezo has no serving-path form (runtime.py:275-279): use the materialising loop");
   check(G >= 1 && g >= 0 && g < G, ZO_ERR_CONFIG, "q-direction rank out of range");
-  check(nu >= 1, ZO_ERR_CONFIG, "nu must be >= 1");
   const bool lozo = c->d.estimator == ZO_EST_LOZO;
   check(!lozo || nu % G == 0, ZO_ERR_CONFIG, "q-direction mode needs the direction count to divide nu");
   check(!c->full_scope || G == 1, ZO_ERR_CONFIG, "q-direction mode with G > 1 supports scope lora_only only");
-  int rc = zo_step_score_async(c, seed, macro_step * (uint64_t)G + (uint64_t)g, lozo ? nu : 1, eps, tokens_dev,
-                               gold_dev, B);
-  if (rc) return rc;
+  stage_dev(c, seed, macro_step * (uint64_t)G + (uint64_t)g, lozo ? nu : 1, tokens_dev, gold_dev, B);
+  score_body(c, seed, eps, B);
   launch_coefficient(c->nll, B, eps, lr, lozo ? divide_by_r : 0, c->r, c->out4, c->abort_flag, c->st);
+  return ZO_OK;
+  ZO_API_END
+}
+
+extern "C" int zo_qdir_score_graph(zo_ctx* c, uint64_t seed, uint64_t macro_step, int32_t G, int32_t g, int32_t nu,
+                                   double eps, double lr, int32_t divide_by_r, const int32_t* tokens_dev,
+                                   const int32_t* gold_dev, int32_t B) {
+  ZO_API_BEGIN
+  check(G >= 1 && g >= 0 && g < G, ZO_ERR_CONFIG, "q-direction rank out of range");
+  const bool lozo = c->d.estimator == ZO_EST_LOZO;
+  check(!lozo || nu % G == 0, ZO_ERR_CONFIG, "q-direction mode needs the direction count to divide nu");
+  check(!c->full_scope || G == 1, ZO_ERR_CONFIG, "q-direction mode with G > 1 supports scope lora_only only");
+  stage_dev(c, seed, macro_step * (uint64_t)G + (uint64_t)g, lozo ? nu : 1, tokens_dev, gold_dev, B);
+  const int32_t dbr = lozo ? divide_by_r : 0;
+  run_graph(c, c->gs_qscore, {seed, (uint64_t)B, dbits(eps), dbits(lr), (uint64_t)dbr}, [&] {
+    score_body(c, seed, eps, B);
+    launch_coefficient(c->nll, B, eps, lr, dbr, c->r, c->out4, c->abort_flag, c->st);
+  });
   return ZO_OK;
   ZO_API_END
 }
@@ -1918,26 +2109,38 @@ extern "C" int zo_qdir_apply_async(zo_ctx* c, uint64_t seed, uint64_t macro_step
                                    const double* out4_all_dev) {
   ZO_API_BEGIN
   check(G >= 1 && out4_all_dev != nullptr, ZO_ERR_CONFIG, "bad q-direction gather");
-  const bool lozo = c->d.estimator == ZO_EST_LOZO;
-  for (int32_t g = 0; g < G; ++g) {
-    k_set_u64<<<1, 1, 0, c->st>>>(c->d_step, macro_step * (uint64_t)G + (uint64_t)g);
-    sampler_launch(c->planU, seed, c->d_step, 1, c->U, c->st);
-    sample_z(c, seed);
-    const double* o4 = out4_all_dev + 4 * (size_t)g;
-    vec_update(c, o4, lr, nullptr);
-    if (lozo) {
-      launch_update(c->A, c->U, c->su, o4, nullptr, c->st);
-    } else {
-      // factorized: V is keyed by the step too (zo_engine.py:181-191)
-      sampler_launch(c->planV, seed, c->d_step, 1, c->V, c->st);
-      launch_dense_update_dev(c, lr, o4, nullptr);
-    }
-  }
-  if (lozo) c->a_dirty = true;
+  k_set_u64<<<1, 1, 0, c->st>>>(c->d_base, macro_step * (uint64_t)G);
+  qdir_apply_body(c, seed, G, lr, out4_all_dev);
+  if (c->d.estimator == ZO_EST_LOZO) c->a_dirty = true;
   else c->v_window = -1;  // V holds the last direction's; the next score resamples it
-  // the ctx out4 mirrors the last direction (zo_read_out4)
-  ZO_CUDA_TRY(cudaMemcpyAsync(c->out4, out4_all_dev + 4 * (size_t)(G - 1), 32, cudaMemcpyDeviceToDevice, c->st));
   ZO_CUDA_TRY(cudaGetLastError());
+  return ZO_OK;
+  ZO_API_END
+}
+
+// zo_qdir_apply_async as a captured graph (replayed while seed, G, lr and the gather buffer
+// stay the same); the macro-step base is written eagerly in front of it
+extern "C" int zo_qdir_apply_graph(zo_ctx* c, uint64_t seed, uint64_t macro_step, int32_t G, double lr,
+                                   const double* out4_all_dev) {
+  ZO_API_BEGIN
+  check(G >= 1 && out4_all_dev != nullptr, ZO_ERR_CONFIG, "bad q-direction gather");
+  k_set_u64<<<1, 1, 0, c->st>>>(c->d_base, macro_step * (uint64_t)G);
+  run_graph(c, c->gs_qapply, {seed, (uint64_t)G, dbits(lr), (uint64_t)(uintptr_t)out4_all_dev},
+            [&] { qdir_apply_body(c, seed, G, lr, out4_all_dev); });
+  if (c->d.estimator == ZO_EST_LOZO) c->a_dirty = true;
+  else c->v_window = -1;
+  return ZO_OK;
+  ZO_API_END
+}
+
+// kernels per launch of the split-step graphs (0 before their first capture):
+// [score, apply, qdir score, qdir apply]
+extern "C" int zo_split_graph_kernels(zo_ctx* c, int32_t out[4]) {
+  ZO_API_BEGIN
+  out[0] = c->gs_score.valid ? c->gs_score.kernels : 0;
+  out[1] = c->gs_apply.valid ? c->gs_apply.kernels : 0;
+  out[2] = c->gs_qscore.valid ? c->gs_qscore.kernels : 0;
+  out[3] = c->gs_qapply.valid ? c->gs_qapply.kernels : 0;
   return ZO_OK;
   ZO_API_END
 }

@@ -263,6 +263,18 @@ class ZoEngine:
         check(lib().zo_score(self._h, tok.ctypes.data, g.ctypes.data, B, nsign, out.ctypes.data))
         return out.reshape(nsign, B)
 
+    def score_options(self, tokens, options) -> np.ndarray:
+        """NLL of every single-token option [n_opt, B] from one sign-0 forward (zob200.h
+        zo_score_options; the caller has prepared the sign-0 probe)."""
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        if tok.ndim != 2 or tok.shape[1] != self.T:
+            raise DimensionError(f"tokens must be [B, {self.T}], got {tok.shape}")
+        opts = np.ascontiguousarray(options, dtype=np.int32).reshape(-1)
+        out = np.empty((opts.size, tok.shape[0]), dtype=np.float64)
+        check(lib().zo_score_options(self._h, tok.ctypes.data, opts.ctypes.data, opts.size, tok.shape[0],
+                                     out.ctypes.data))
+        return out
+
     def coefficient(self, B: int, epsilon: float, lr: float, divide_by_r: bool) -> np.ndarray:
         out = np.empty(4)
         check(lib().zo_coefficient(self._h, B, float(epsilon), float(lr), int(divide_by_r), out.ctypes.data))
@@ -324,6 +336,15 @@ class ZoEngine:
     def step_apply_async(self, epsilon: float, lr: float, divide_by_r: bool, B_total: int) -> None:
         check(lib().zo_step_apply_async(self._h, float(epsilon), float(lr), int(divide_by_r), B_total))
 
+    def step_score_graph(self, seed: int, step: int, nu: int, epsilon: float, tokens_dev: int, gold_dev: int,
+                         B: int) -> None:
+        """step_score_async with the body replayed as a captured CUDA graph (zob200.h)."""
+        check(lib().zo_step_score_graph(self._h, seed, step, nu, float(epsilon), ctypes.c_void_p(tokens_dev),
+                                        ctypes.c_void_p(gold_dev), B))
+
+    def step_apply_graph(self, epsilon: float, lr: float, divide_by_r: bool, B_total: int) -> None:
+        check(lib().zo_step_apply_graph(self._h, float(epsilon), float(lr), int(divide_by_r), B_total))
+
     def qdir_score_async(self, seed: int, macro_step: int, G: int, g: int, nu: int, epsilon: float, lr: float,
                          divide_by_r: bool, tokens_dev: int, gold_dev: int, B: int) -> None:
         """q-direction mode: score reference step macro_step*G + g (zob200.h)."""
@@ -336,6 +357,21 @@ class ZoEngine:
 
     def qdir_apply_async(self, seed: int, macro_step: int, G: int, lr: float, out4_all_dev: int) -> None:
         check(lib().zo_qdir_apply_async(self._h, seed, macro_step, G, float(lr), ctypes.c_void_p(out4_all_dev)))
+
+    def qdir_score_graph(self, seed: int, macro_step: int, G: int, g: int, nu: int, epsilon: float, lr: float,
+                         divide_by_r: bool, tokens_dev: int, gold_dev: int, B: int) -> None:
+        check(lib().zo_qdir_score_graph(self._h, seed, macro_step, G, g, nu, float(epsilon), float(lr),
+                                        int(divide_by_r), ctypes.c_void_p(tokens_dev), ctypes.c_void_p(gold_dev),
+                                        B))
+
+    def qdir_apply_graph(self, seed: int, macro_step: int, G: int, lr: float, out4_all_dev: int) -> None:
+        check(lib().zo_qdir_apply_graph(self._h, seed, macro_step, G, float(lr), ctypes.c_void_p(out4_all_dev)))
+
+    def split_graph_kernels(self) -> list[int]:
+        """Kernels per launch of the [score, apply, qdir score, qdir apply] graphs."""
+        out = (ctypes.c_int32 * 4)()
+        check(lib().zo_split_graph_kernels(self._h, out))
+        return list(out)
 
     def fold_async(self) -> None:
         check(lib().zo_fold_async(self._h))

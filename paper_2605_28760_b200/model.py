@@ -456,13 +456,41 @@ def eval_accuracy(params, cfg: ModelConfig, prompts: np.ndarray, golds: np.ndarr
     return float(np.mean(np.argmax(scores, axis=1) == np.asarray(golds)))
 
 
+def _one_forward_options(params, cfg: ModelConfig, prompts: np.ndarray, opts: np.ndarray, view):
+    """Every single-token option's NLL [n_opt, B] from ONE sign-0 forward per batch chunk
+    (zob200.h zo_score_options): the scored row never sees the option token, so its
+    logits serve all options.  None when the configuration needs a forward per option
+    (multi-token options, a +-eps probe view, high rank, real32)."""
+    if opts.shape[1] != 1:
+        return None
+    dp = as_device_params(params, cfg)
+    eng = dp.engine if dp.bound else dp.bind(opt_len=1)
+    st = _view_state(view)
+    if (st is not None and st.perturb_sign != 0 and st._probe_on) or eng.rank > 8 or eng.precision == "real32":
+        return None
+    if st is not None:
+        st._sync_to_engine(eng)
+    eng.prepare_probe(st.epsilon if st is not None else 0.0, 1)
+    seq = np.concatenate([prompts, np.tile(opts[0], (prompts.shape[0], 1))], axis=1)
+    _check_tokens(seq, cfg.vocab)
+    out = np.empty((opts.shape[0], seq.shape[0]))
+    for s in range(0, seq.shape[0], eng.max_batch):
+        tk = seq[s: s + eng.max_batch]
+        out[:, s: s + len(tk)] = eng.score_options(tk, opts[:, 0])
+    return out
+
+
 def evaluate_split(params, cfg: ModelConfig, data: TaskData, split: str = "dev", view=None,
                    precision: str = "real64") -> tuple[float, float]:
-    """(loss, accuracy) over a whole split (model.py:444-460)."""
+    """(loss, accuracy) over a whole split (model.py:444-460).  Single-token options
+    (the SST-2 shape) are all scored from one forward (_one_forward_options); otherwise
+    one forward per option, as the reference does."""
     prompts, golds = data.splits[split]
     opts = np.asarray(data.config.options, dtype=np.int64)
-    per_opt = [forward_nll(params, cfg, prompts, np.tile(opts[j], (prompts.shape[0], 1)), view, precision)
-               for j in range(len(opts))]
+    one = _one_forward_options(params, cfg, prompts, opts, view)
+    per_opt = list(one) if one is not None else [
+        forward_nll(params, cfg, prompts, np.tile(opts[j], (prompts.shape[0], 1)), view, precision)
+        for j in range(len(opts))]
     nll_gold = np.choose(golds, per_opt)
     loss = canonical_mean(nll_gold)
     scores = -np.stack(per_opt, axis=1)

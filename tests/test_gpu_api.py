@@ -164,6 +164,22 @@ def test_evaluate_split_vs_oracle():
     assert abs(acc - ref_acc) <= 1.0 / len(golds) + 1e-12
 
 
+def test_score_options_one_forward_equals_per_option():
+    """zo_score_options: every single-token option from one forward is bitwise the
+    per-option forward (the scored row never attends the option token)."""
+    from paper_2605_28760_b200.engine import ZoEngine
+    eng = ZoEngine(512, 128, 2, 2, 63, max_batch=16, rank=2)
+    eng.init_params(7, 0.02)
+    rng = np.random.default_rng(4)
+    prompts = rng.integers(0, 510, size=(16, 63))
+    eng.prepare_probe(0.0, 1)
+    both = eng.score_options(np.concatenate([prompts, np.full((16, 1), 510)], axis=1), [510, 511, 7])
+    for j, o in enumerate((510, 511, 7)):
+        tok = np.concatenate([prompts, np.full((16, 1), o)], axis=1)
+        np.testing.assert_array_equal(both[j], eng.score(tok, np.full((16, 1), o), nsign=1)[0])
+    eng.close()
+
+
 def test_checkpoint_resume_bit_identical(golden_dir, tmp_path):
     """Checkpoint mid-window (ZOAD adapter + float64 masters), resume on a fresh
     engine: the continued trajectory and final parameters equal an uninterrupted
