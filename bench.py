@@ -490,6 +490,8 @@ def main():
             "scored_tokens_per_s": value * 2 * B * T, "option_tokens_per_s": value * 2 * B,
             "gpu_launches": launches, "clocks": clk.summary(), "init_s": t_init,
             **({"replicas_identical": replicas_identical} if world > 1 else {}),
+            **({"split_graphs": {"score_kernels": split[2] if qdir else split[0],
+                                 "apply_kernels": split[3] if qdir else split[1]}} if world > 1 and args.graph else {}),
             "last_losses": [float(out4[0]), float(out4[1]), float(out4[2])]}
     dense, total = dense_flops(mcfg.dim, mcfg.n_layers, B, T, mcfg.vocab, args.rank)
     line["step_tflops"] = total / 1e12
@@ -555,19 +557,25 @@ def main():
         state = AdapterState(epsilon=zcfg.epsilon)
         base = t_first + args.steps + 2
         e_first = nu_m * -(-(base + args.warmup + args.steps // 2) // nu_m) - args.steps // 2
+        # rank > 8 (config 5): audit the U/V digests of every 50th step -- the full arenas are
+        # 3.4 GB per step there and FNV-1a is byte-serial (runtime.run_serving_path digest_every)
+        dig_every = 1 if args.rank <= 8 else 50
         kw = dict(eval_every=10 ** 9, params=params, state=state, compute_param_digests=False, final_fold=False,
-                  digests=True)
+                  digests=True, digest_every=dig_every)
         run_serving_path(mcfg, task, zcfg, args.warmup, start_step=e_first - args.warmup, **kw)
         torch.cuda.synchronize()
         run = run_serving_path(mcfg, task, zcfg, args.steps, start_step=e_first, **kw)
         torch.cuda.synchronize()
         e2e_s = (run.extra["loop_wall_s"] + run.extra["digest_wait_s"]) / args.steps
-        assert all(r.u_digest and r.v_digest for r in run.trajectory)
+        assert all(r.u_digest and r.v_digest for i, r in enumerate(run.trajectory) if i % dig_every == 0)
+        v_reads = (1.0 / dig_every) if fact else (1.0 / zcfg.nu)  # V arena copies per step
         line["e2e"] = {"value": 1.0 / e2e_s, "unit": UNIT,
                        "h2d_bytes_per_step": B * T * 4 + 2 * B * 4 + 8,
-                       "d2h_bytes_per_step": 32 + 8 * eng.su,
+                       "d2h_bytes_per_step": 32 + 8 * eng.su / dig_every + 8 * eng.sv * v_reads,
+                       "digest_every": dig_every,
                        "api": "runtime.run_serving_path (host minibatches, fused lozo_step, U/V digests on the "
-                              "host pool, folds at window boundaries)",
+                              "host pool" + (f", audited every {dig_every} steps" if dig_every > 1 else "")
+                              + ", folds at window boundaries)",
                        "timed_steps": [e_first, e_first + args.steps - 1],
                        "digest_wait_s": run.extra["digest_wait_s"],
                        "phase_ms_last_step": dict(zip(["sample", "score", "update"], eng.last_step_ms()))}

@@ -123,6 +123,18 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t cta) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(cta));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
+// relaxed arrives: the barrier orders only what the waiting side needs (TMEM reads fenced by
+// tcgen05.fence::before_thread_sync, shared-memory reads whose values are already in
+// registers), not the arriving warp's outstanding global stores -- a release arrive waits
+// for those to be acknowledged (ERRBAR), once per tile per warp
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(cta));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_relaxed(uint32_t bar) {
+  asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_commit(uint32_t bar) {
@@ -216,7 +228,7 @@ struct GemmCfg {
   static constexpr int W_SLOTS = UPD ? 4 : 0;
   static constexpr int W_NBAR = 2 * W_SLOTS;  // barrier pairs (the fp32 ring's slot count)
   static constexpr int W_BYTES = 32 * BM * 8;
-  static constexpr int STAGES = UPD ? 2 : ((196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES);
+  static constexpr int STAGES = UPD ? 3 : ((196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES);
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + W_SLOTS * W_BYTES + 512;
 };
@@ -256,6 +268,7 @@ struct GemmParams {
   void* upd_w16;
   int upd_ld64, upd_ld16, upd_transposed;
   int upd_m32;  // the master holds fp32 values (zo_set_update_mode 1): half the master bytes
+  int upd_shadow_rm;  // transposed update whose 16-bit shadow is row-major [i][j] (the embedding)
   const double* upd_out4;
   double upd_lr, upd_scale;
   const unsigned* upd_abort;
@@ -383,7 +396,7 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
     }
     for (int w = 0; w < C::W_NBAR; ++w) {
       mbar_init(wfull0 + 8 * w, 1);
-      mbar_init(wempty0 + 8 * w, 1);
+      mbar_init(wempty0 + 8 * w, M32 ? 4 : 1);  // fp32: the group's 4 warps release; fp64: the storer
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -630,8 +643,76 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
           v[4 * j + 3] += w.w;
         }
       };
-      if constexpr (UPD) {
+      if constexpr (M32) {
         if (wtma) {
+          // projection, fp32 master W32[i][j] (row i = input, contiguous in the output j):
+          // the master block of round r ([32 i][128 j]) arrives by TMA (the ring keeps up to
+          // 8 blocks = 128 KB per SM in flight); lane = tile row = output j reads its column,
+          // updates it with D[j][i0..i0+31] from its TMEM row and writes it straight back --
+          // for a fixed i the 32 lanes store one 128-byte line -- together with its 16-bit
+          // shadow row segment W16T[j][i0..i0+31] (64 B).  The slot returns to the producer
+          // as soon as the group's 4 warps have read it: no staging of the stores, no
+          // barriers between warps.
+          const bool skip = p.upd_abort ? (*p.upd_abort != 0u)
+                                        : !(isfinite(p.upd_out4[0]) && isfinite(p.upd_out4[1]));
+          const float alpha32 = (float)(-(p.upd_lr * p.upd_out4[2]) * p.upd_scale);
+          float* W32 = reinterpret_cast<float*>(p.upd_w64);
+          const size_t ld = (size_t)p.upd_ld64;
+          const int rbase = wround_e;
+#pragma unroll 1
+          for (int r = grp; r < BN / 32; r += EGRP) {
+            const int gi = rbase + r;
+            const int ws = gi % wslots;
+            float v[32];
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + 32 * r, v);
+            mbar_wait(wfull0 + 8 * ws, (gi / wslots) & 1);
+            const float* blk32 = reinterpret_cast<const float*>(sW + ws * wbytes) + erow;
+            const int col0 = n0 + 32 * r;
+            float w[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w[i] = blk32[i * C::BM];
+            __syncwarp();
+            if (lane == 0) mbar_arrive_relaxed(wempty0 + 8 * ws);  // this warp is done with the slot
+            if (!skip && row_ok) {
+              float* dst = W32 + (size_t)col0 * ld + row;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                w[i] = fmaf(alpha32, v[i], w[i]);
+                if (col0 + i < p.N) __stcs(dst + (size_t)i * ld, w[i]);
+              }
+              {
+              if (p.upd_shadow_rm) {  // E16[i][j]: for a fixed i the lanes write 64 contiguous bytes
+                uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)col0 * p.upd_ld16 + row;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < p.N) o[(size_t)i * p.upd_ld16] = (uint16_t)(pack2<BF16>(w[i], 0.f) & 0xffffu);
+              } else {
+              uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)row * p.upd_ld16 + col0;
+              if (col0 + 32 <= p.N && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  uint4 u;
+                  u.x = pack2<BF16>(w[8 * j], w[8 * j + 1]);
+                  u.y = pack2<BF16>(w[8 * j + 2], w[8 * j + 3]);
+                  u.z = pack2<BF16>(w[8 * j + 4], w[8 * j + 5]);
+                  u.w = pack2<BF16>(w[8 * j + 6], w[8 * j + 7]);
+                  __stcs(reinterpret_cast<uint4*>(o) + j, u);
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < p.N) o[i] = (uint16_t)(pack2<BF16>(w[i], 0.f) & 0xffffu);
+              }
+              }
+              }
+            }
+          }
+          wround_e = rbase + BN / 32;
+          goto tile_done;
+        }
+      }
+      if constexpr (UPD) {
+        if (!M32 && wtma) {
           // projection: the master block of round r ([32 input rows i][128 output cols j],
           // this warp's 32 j columns) arrives by TMA; lane j updates its column in place in
           // shared memory, writes its 32 shadow values W16T[j][i..i+31] (64 contiguous bytes),
@@ -903,10 +984,16 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2)
+        if constexpr (M32) {  // the update's global stores need no ordering against the MMA
+          if constexpr (CG == 2)
+            mbar_arrive_remote_relaxed(tempty0 + 8 * acc, 0);
+          else
+            mbar_arrive_relaxed(tempty0 + 8 * acc);
+        } else if constexpr (CG == 2) {
           mbar_arrive_remote(tempty0 + 8 * acc, 0);
-        else
+        } else {
           mbar_arrive(tempty0 + 8 * acc);
+        }
       }
     }
   }
@@ -1091,6 +1178,7 @@ static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = 
   p.upd_ld16 = g.upd_ld16;
   p.upd_transposed = g.upd_transposed;
   p.upd_m32 = g.upd_m32;
+  p.upd_shadow_rm = g.upd_shadow_rm;
   p.upd_out4 = g.upd_out4;
   p.upd_lr = g.upd_lr;
   p.upd_scale = g.upd_scale;

@@ -53,6 +53,7 @@ struct GemmDesc {
   void* upd_w16 = nullptr;
   int upd_ld64 = 0, upd_ld16 = 0, upd_transposed = 0;
   int upd_m32 = 0;  // upd_w64 actually holds fp32 values (the fast update mode's fp32 master)
+  int upd_shadow_rm = 0;  // upd_transposed with a row-major shadow W16[i][j] (the embedding, fp32 master)
   const double* upd_out4 = nullptr;
   double upd_lr = 0.0, upd_scale = 1.0;
   const unsigned* upd_abort = nullptr;

@@ -965,6 +965,41 @@ void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K
   k_vext<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(V, n, r, W16T, ldw, K, bf16, ext_terms, V32);
 }
 
+// launch_write_vext for every matrix in one launch: the V arena is contiguous in matrix order,
+// so element i belongs to the last matrix whose v_off <= i (binary search over tab)
+__global__ void k_vext_all(const double* __restrict__ V, int64_t sv, const VextMat* __restrict__ tab, int ntab,
+                           int r, bool bf16, int ext_terms, float* __restrict__ V32) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sv) return;
+  int lo = 0, hi = ntab - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) / 2;
+    if (tab[mid].v_off <= i) lo = mid;
+    else hi = mid - 1;
+  }
+  const VextMat m = tab[lo];
+  const int64_t loc = i - m.v_off;
+  const int j = (int)(loc / r), k = (int)(loc % r);
+  const float vf = (float)V[i];
+  V32[i] = vf;
+  if (!m.W) return;
+  uint16_t* o = reinterpret_cast<uint16_t*>(m.W) + (size_t)j * m.ldw + m.K;
+  if (ext_terms == 3) {
+    const uint16_t hi16 = to16(vf, bf16);
+    o[3 * k] = hi16;
+    o[3 * k + 1] = hi16;
+    o[3 * k + 2] = to16(vf - from16(hi16, bf16), bf16);
+  } else {
+    o[k] = to16(vf, bf16);
+  }
+}
+
+void launch_write_vext_all(const double* V, int64_t sv, const VextMat* tab, int ntab, int r, bool bf16,
+                           int ext_terms, float* V32, cudaStream_t st) {
+  if (sv == 0) return;
+  k_vext_all<<<(unsigned)((sv + 255) / 256), 256, 0, st>>>(V, sv, tab, ntab, r, bf16, ext_terms, V32);
+}
+
 // ------------------------------------------------------------------ full-scope 1-D params (VectorProbe)
 // zo_engine.py:269-295: sign +1 from 0 adds (1*eps)*z, sign -1 from +1 adds (-2*eps)*z
 // (axpy_dense: product rounded, then sum), float64; the fp32 copies are what the LN

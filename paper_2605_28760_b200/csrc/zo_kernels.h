@@ -86,6 +86,14 @@ void launch_p16t_all(const float* Pp, const float* Pm, int64_t su, const int64_t
 // V ext columns (hi, hi, lo) into W16T[:, K:K+3r] for one matrix; V32 copy
 void launch_write_vext(const double* V, int n, int r, void* W16T, int ldw, int K, bool bf16, int ext_terms,
                        float* V32, cudaStream_t st);
+// every matrix's V -> V32 (+ its W16T extension columns) in one launch; tab sorted by v_off
+struct VextMat {
+  int64_t v_off;
+  void* W;  // W16T (nullptr: V32 only -- the embedding)
+  int ldw, K;
+};
+void launch_write_vext_all(const double* V, int64_t sv, const VextMat* tab, int ntab, int r, bool bf16,
+                           int ext_terms, float* V32, cudaStream_t st);
 // W64[m,n] += sum_k A[:,k] V[:,k]^T (k ascending, numerics.py:207-235) then A = 0
 void launch_fold(double* W64, int m, int n, const double* A, const double* V, int r, double alpha, void* W16,
                  int ldw, int transposed, bool bf16, cudaStream_t st);

@@ -185,6 +185,7 @@ struct zo_ctx {
   uint16_t* P16T = nullptr;       // high-rank extension B operands [2][su] (per matrix [r][m])
   int64_t* p16t_tab = nullptr;    // launch_p16t_all's matrix table; p16t_n entries, p16t_tiles tiles
   int p16t_n = 0, p16t_tiles = 0;
+  VextMat* vext_tab = nullptr;    // write_vext_all's matrix table
   float* xws = nullptr;           // high-rank extension split-K partials [num_sms][Mpad][r]
   float* sk_ws = nullptr;         // stream-K partial tiles
   float* loss_ws = nullptr;       // k_loss per-slice partials (loss_ws_floats)
@@ -465,9 +466,13 @@ void with_master64(zo_ctx* c, Matrix& m, F&& f) {
 }
 
 void write_vext_all(zo_ctx* c) {
-  for (auto& m : c->mats)
-    launch_write_vext(c->V + m.v_off, (int)m.n, c->r, m.kind == K_EMBED ? nullptr : m.W16, m.ldw, (int)m.m,
-                      c->bf16, c->ext_terms, c->V32 + m.v_off, c->st);
+  if (!c->vext_tab) {  // one table for the batched launch (matrix order = V arena order)
+    std::vector<VextMat> tab;
+    for (auto& m : c->mats) tab.push_back({m.v_off, m.kind == K_EMBED ? nullptr : m.W16, m.ldw, (int)m.m});
+    c->vext_tab = c->mem.get<VextMat>(tab.size());
+    ZO_CUDA_TRY(cudaMemcpy(c->vext_tab, tab.data(), tab.size() * sizeof(VextMat), cudaMemcpyHostToDevice));
+  }
+  launch_write_vext_all(c->V, c->sv, c->vext_tab, (int)c->mats.size(), c->r, c->bf16, c->ext_terms, c->V32, c->st);
 }
 
 enum ProfKind { PK_EMBED = 0, PK_LN, PK_QKV, PK_ATTN, PK_EXT, PK_OUT, PK_UP, PK_DOWN, PK_TAIL, PK_OTHER, PK_N };
@@ -713,7 +718,10 @@ void launch_dense_update_dev(zo_ctx* c, double lr, const double* out4, const uns
         const Matrix& m = c->mats[i];
         if (m.kind == K_POS) continue;  // no 16-bit shadow: the exact path below
         GemmDesc& g = c->upd_plans[i];
-        const bool tr = m.kind != K_EMBED;
+        // D = V U^T (rows = outputs j): the master W[i][j] is then read / written with the lanes
+        // along j (coalesced) -- projections, and the embedding too when its master is fp32
+        // (its shadow E16[i][j] is row-major: upd_shadow_rm)
+        const bool tr = m.kind != K_EMBED || c->master32;
         if (tr)  // D[j, i] = sum_k V[j, k] U[i, k]: rows = outputs (W16T rows)
           gemm_plan(g, c->V16 + m.v_off, (int)m.n, c->r, c->U16 + m.u_off, (int)m.m, c->r, c->r, EPI_UPDATE64,
                     c->bf16, nullptr, 0, c->num_sms);
@@ -724,8 +732,9 @@ void launch_dense_update_dev(zo_ctx* c, double lr, const double* out4, const uns
         g.upd_m32 = c->master32 ? 1 : 0;
         g.upd_w16 = m.W16;
         g.upd_ld64 = (int)m.n;
-        g.upd_ld16 = m.ldw;
+        g.upd_ld16 = m.kind == K_EMBED ? (int)m.n : m.ldw;
         g.upd_transposed = tr ? 1 : 0;
+        g.upd_shadow_rm = (tr && m.kind == K_EMBED) ? 1 : 0;
         g.upd_lr = lr;
         g.upd_scale = 1.0 / std::sqrt((double)c->r);
         gemm_set_update_master(g);

@@ -101,6 +101,7 @@ class StrictCompareReport:
     seed_mismatch_steps: list = field(default_factory=list)
     digest_mismatch_steps: list = field(default_factory=list)
     loss_mismatch_steps: list = field(default_factory=list)
+    digests_audited: int = -1  # steps whose U/V digests were compared (-1: not counted)
 
     @property
     def rejected(self) -> int:
@@ -121,6 +122,7 @@ def strict_compare(traj_a, traj_b, loss_tol: float = 1e-12) -> StrictCompareRepo
     if len(ra) != len(rb):
         raise InputError(f"step count mismatch: {len(ra)} vs {len(rb)}")
     seed_bad, dig_bad, loss_bad = [], [], []
+    n_audited = 0
     accepted, max_dp, max_dm = 0, 0.0, 0.0
     for x, y in zip(ra, rb):
         if x.step != y.step:
@@ -129,7 +131,10 @@ def strict_compare(traj_a, traj_b, loss_tol: float = 1e-12) -> StrictCompareRepo
         if x.seed != y.seed:
             seed_bad.append(x.step)
             ok = False
-        if x.u_digest != y.u_digest or x.v_digest != y.v_digest:
+        # an empty digest is an unaudited step (runtime.run_serving_path digest_every > 1)
+        audited = all((x.u_digest, y.u_digest, x.v_digest, y.v_digest))
+        n_audited += audited
+        if audited and (x.u_digest != y.u_digest or x.v_digest != y.v_digest):
             dig_bad.append(x.step)
             ok = False
         dp, dm = abs(x.loss_plus - y.loss_plus), abs(x.loss_minus - y.loss_minus)
@@ -142,7 +147,7 @@ def strict_compare(traj_a, traj_b, loss_tol: float = 1e-12) -> StrictCompareRepo
     if fa is not None and fb is not None and "eval_loss" in fa and "eval_loss" in fb:
         final = abs(fa["eval_loss"] - fb["eval_loss"])
     return StrictCompareReport(len(ra), accepted, len(seed_bad), len(dig_bad), max_dp, max_dm, loss_tol, final,
-                               seed_bad, dig_bad, loss_bad)
+                               seed_bad, dig_bad, loss_bad, n_audited)
 
 
 def rank_check(delta_w, r: int) -> float:

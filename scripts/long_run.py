@@ -35,8 +35,12 @@ def main():
                     help="factorized_sqrt_r with --rank 128 = BASELINE config 5 (1000 steps)")
     ap.add_argument("--rank", type=int, default=2)
     ap.add_argument("--digests", choices=["auto", "on", "off"], default="auto",
-                    help="per-step U/V digests on the host pool; auto = off above rank 8 (r = 128 means "
-                         "3.4 GB of directions per step, SURVEY.md §0 fact 7)")
+                    help="U/V digests on the host pool; auto = every step up to rank 8, an audit of every "
+                         "--digest-every-th step above (r = 128 means 3.4 GB of directions per step, "
+                         "SURVEY.md §0 fact 7)")
+    ap.add_argument("--digest-every", type=int, default=50, help="audit period above rank 8 (--digests auto)")
+    ap.add_argument("--dense-update", default="exact", choices=["exact", "tensor"],
+                    help="factorized dense update: float64 bit-exact, or tcgen05 over fp32 masters (zob200.h)")
     a = ap.parse_args()
     from paper_2605_28760_b200 import model as M
     from paper_2605_28760_b200.runtime import run_serving_path
@@ -48,16 +52,22 @@ def main():
     zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=a.lr, rank=a.rank, nu=50, batch_size=16,
                     estimator=a.estimator)
     t0 = time.perf_counter()
-    digests = a.digests == "on" or (a.digests == "auto" and a.rank <= 8)
+    digests = a.digests != "off"
+    every = a.digest_every if (a.digests == "auto" and a.rank > 8) else 1
+    params = M.init_params(mcfg, precision="fp16", max_batch=16)
+    eng = params.bind(zcfg.rank, zcfg.estimator, zcfg.batch_size, 1, zcfg.scope)
+    if a.estimator == "factorized_sqrt_r":
+        eng.set_update_mode(a.dense_update)
     run = run_serving_path(mcfg, task, zcfg, a.steps, precision="fp16", eval_every=a.eval_every,
-                           compute_param_digests=False, digests=digests)
+                           compute_param_digests=False, digests=digests, digest_every=every, params=params)
     wall = time.perf_counter() - t0
     os.makedirs(a.out, exist_ok=True)
     tag = f"{a.model}_{a.steps}" + ("" if a.estimator == "lozo_lazy" else f"_fact_r{a.rank}")
     write_trajectory(os.path.join(a.out, f"traj_{tag}.jsonl"),
                      {"model": mdl, "steps": a.steps, "zo_digest": zcfg.digest()}, run.trajectory,
                      {"eval_loss": run.eval_curve[-1].loss, "eval_acc": run.eval_curve[-1].acc})
-    summary = {"model": a.model, "estimator": a.estimator, "rank": a.rank, "steps": run.steps_completed, "train_wall_s": run.train_wall_s,
+    summary = {"model": a.model, "estimator": a.estimator, "rank": a.rank, "dense_update": a.dense_update,
+               "digest_every": every, "steps": run.steps_completed, "train_wall_s": run.train_wall_s,
                "steps_per_s_train": run.steps_completed / run.train_wall_s, "total_wall_s": wall,
                "meter": run.meter.to_dict(), "eval_curve": [p.to_dict() for p in run.eval_curve],
                "last_record": run.trajectory[-1].to_dict()}

@@ -7,7 +7,9 @@ device time of
   "dense_mezo": a dense Role.DENSE_Z direction per weight regenerated every step, probe /
   restore / update written into the weights, one forward per sign), and
 * the factorized estimator on the serving path (zo_step_async: rank-r directions, both
-  probes in one fused forward, the float64 dense update U V^T / sqrt(r) into the base).
+  probes in one fused forward, the dense update U V^T / sqrt(r) into the base) -- with
+  the bit-exact float64 update ("exact") and the tensor-core update over fp32 masters
+  ("tensor", zo_set_update_mode 1).
 
     python scripts/phase6.py [--model opt-1.3b] [--steps 10]
 """
@@ -45,6 +47,7 @@ def main():
     ap.add_argument("--model", default="opt-1.3b", choices=sorted(MODELS))
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--ranks", default="128,256,512")
+    ap.add_argument("--modes", default="exact,tensor", help="factorized dense update modes to time")
     a = ap.parse_args()
     mdl = MODELS[a.model]
     B, T = 16, 64
@@ -67,15 +70,18 @@ def main():
                                           d_gold[t].data_ptr(), B), a.steps)
     eng.close()
     for r in [int(x) for x in a.ranks.split(",")]:
-        eng = ZoEngine(mdl["vocab"], mdl["dim"], mdl["n_layers"], mdl["n_heads"], T - 1, max_batch=B, rank=r,
-                       estimator="factorized_sqrt_r")
-        eng.init_params(7, 0.02)
-        ms = timed(lambda t: eng.step_async(42, t, 1, 1e-3, 1e-7, False, d_tok[t].data_ptr(), d_gold[t].data_ptr(),
-                                            B), a.steps)
-        out[f"factorized_r{r}_serving_ms"] = ms
-        out[f"speedup_r{r}"] = out["dense_mezo_materialising_ms"] / ms
-        eng.close()
-        print(json.dumps(out), flush=True)
+        for mode in a.modes.split(","):
+            eng = ZoEngine(mdl["vocab"], mdl["dim"], mdl["n_layers"], mdl["n_heads"], T - 1, max_batch=B, rank=r,
+                           estimator="factorized_sqrt_r")
+            eng.init_params(7, 0.02)
+            eng.set_update_mode(mode)
+            ms = timed(lambda t: eng.step_async(42, t, 1, 1e-3, 1e-7, False, d_tok[t].data_ptr(),
+                                                d_gold[t].data_ptr(), B), a.steps)
+            sfx = "" if mode == "exact" else "_tensor"
+            out[f"factorized_r{r}{sfx}_serving_ms"] = ms
+            out[f"speedup_r{r}{sfx}"] = out["dense_mezo_materialising_ms"] / ms
+            eng.close()
+            print(json.dumps(out), flush=True)
     os.makedirs(os.path.join(HERE, "gpurun_out"), exist_ok=True)
     with open(os.path.join(HERE, "gpurun_out", "phase6.json"), "w") as f:
         json.dump(out, f, indent=1)
