@@ -190,12 +190,28 @@ def workload_config(args, world: int) -> tuple[dict, str, bool]:
 
 
 def run_reference(args, mdl):
-    """--impl reference: the oracle port of the reference's path on host cores."""
+    """--impl reference: the reference's own path on host cores -- the unmodified zoserve
+    staged in oracle/_ref (whole lozo_step calls at the model's dims with 1 and 2 blocks,
+    depth-extrapolated), else the oracle port."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle.cpu_bench import BlockSample, host_threads
+    from oracle.cpu_bench import BlockSample, host_threads, reference_layers
     B, T = args.batch, args.seq
+    got = reference_layers(mdl["dim"], mdl["n_layers"], mdl["n_heads"], mdl["vocab"], B, T) \
+        if args.estimator == "lozo_lazy" and args.rank == 2 else None
+    if got is not None:
+        v, sample = got
+        cfg, scaling, _ = workload_config(args, world)
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": scaling,
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference", "config": cfg,
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": host_threads(), "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "scored_tokens_per_s": v * 2 * B * T}
+        print(json.dumps(line), flush=True)
+        return
     n_ex = 1
     bs = BlockSample(mdl["dim"], mdl["n_heads"], mdl["vocab"], T, n_ex)
     t_head = bs.run_head() * B

@@ -148,3 +148,47 @@ def reference_config1(steps: int = 2, warmup: int = 1):
             f"(OPT-125m dims, B=16, T=64): {steps} whole steps timed after {warmup} warm-up, "
             f"{s:.2f} s/step; last step L+ = {rec.loss_plus:.6f}")
     return 1.0 / s, desc
+
+
+def reference_layers(dim: int, n_layers: int, n_heads: int, vocab: int, B: int = 16, T: int = 64,
+                     layer_counts=(1, 2)):
+    """The UNMODIFIED reference (oracle/_ref/zoserve) at a large model's own dims, bounded by
+    depth: one whole ``lozo_step`` (real64: directions, both composed float64 forwards,
+    coefficient, update) of the same model with 1 and with 2 decoder blocks; the block cost is
+    the difference, the rest (embedding, LM head, loss, sampling) the remainder, and the full
+    model's step = remainder + n_layers x block (every block has the same shape).  Returns
+    (steps/s, description) or None when the reference was not staged."""
+    import sys
+    ref = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref")
+    if not os.path.isfile(os.path.join(ref, "zoserve", "zo_engine.py")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from zoserve.adapter import AdapterState
+    from zoserve.model import ModelConfig, TaskConfig, generate_task, init_params, sample_minibatch
+    from zoserve.zo_engine import ZoConfig, lozo_step
+    task = generate_task(TaskConfig(seed=11, vocab=vocab, prompt_len=T - 1, train_size=64, dev_size=2, val_size=2))
+    zcfg = ZoConfig(seed=42, epsilon=1e-3, learning_rate=1e-7, rank=2, nu=50, batch_size=B)
+    secs = {}
+    for L in layer_counts:
+        mcfg = ModelConfig(vocab=vocab, dim=dim, n_layers=L, n_heads=n_heads, prompt_len=T - 1, init_seed=7,
+                           init_scale=0.02)
+        params = init_params(mcfg)
+        state = AdapterState(epsilon=zcfg.epsilon)
+        batch = sample_minibatch(task, "train", zcfg.seed, 0, B)
+        t0 = time.perf_counter()
+        lozo_step(params, mcfg, state, zcfg, 0, batch, "real64")
+        secs[L] = time.perf_counter() - t0
+        del params
+    l1, l2 = layer_counts[0], layer_counts[-1]
+    block = (secs[l2] - secs[l1]) / (l2 - l1)
+    if block <= 0:  # timing noise on a tiny model: split the deeper step evenly
+        block = secs[l2] / (l2 + 1)
+    rest = max(secs[l1] - l1 * block, 0.0)
+    step = rest + n_layers * block
+    desc = (f"the reference itself (zoserve.zo_engine.lozo_step, real64, oracle/_ref) at the model's own dims "
+            f"(d={dim}, H={n_heads}, V={vocab}, B={B}, T={T}) with {l1} and {l2} decoder blocks: "
+            f"{secs[l1]:.1f} s / {secs[l2]:.1f} s per whole step -> {block:.1f} s per block + {rest:.1f} s "
+            f"embedding/LM head/loss/sampling; {n_layers} blocks -> {step:.0f} s per step "
+            f"(depth-extrapolated: the full model's step does not fit a bounded CPU run)")
+    return 1.0 / step, desc

@@ -22,10 +22,19 @@
 //            chunks) the chunk is re-parsed from its entry; a re-parse whose exit
 //            differs breaks the splice and the rest of the stream is repaired
 //            serially (never observed; counted).  Then counts -> offsets.
-//   k_emit : re-parse from the verified entry and write samples in place.
-// Philox runs twice per sample (spec + emit); every step is exact.
+//   k_emit : re-parse from the verified entry and write samples in place -- or, with a
+//            scratch (SamplerPlan::d_scratch, the direction plans), k_emit_copy: k_spec
+//            kept each chunk's speculative samples, and a warp per chunk copies them
+//            (minus the d_skip leading ones) to their offsets, coalesced, writing the
+//            optional 16-bit / fp32 copies in the same pass; only chunks whose entry fell
+//            inside a speculative attempt are re-parsed.
+// Philox runs twice per sample without a scratch, once with; every step is exact.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <algorithm>
 
 #include "zo_common.cuh"
 #include "zo_glibc_math.cuh"
@@ -218,7 +227,7 @@ __global__ void __launch_bounds__(256) k_spec(const StreamDesc* __restrict__ str
                                               const uint32_t* __restrict__ chunk_stream, int64_t C,
                                               const uint64_t* __restrict__ keys,
                                               uint64_t* __restrict__ spec_exit, uint32_t* __restrict__ count,
-                                              unsigned* flags) {
+                                              double* __restrict__ scratch, unsigned* flags) {
   __shared__ uint64_t ki[256];
   __shared__ double wi[256], fi[256];
   Zig z;
@@ -232,9 +241,11 @@ __global__ void __launch_bounds__(256) k_spec(const StreamDesc* __restrict__ str
   p.init(keys[2 * s], keys[2 * s + 1], beg);
   unsigned amb = 0, n = 0, starts = 0, yields = 0;
   double x;
+  double* sc = scratch ? scratch + (size_t)c * CH : nullptr;
   while (p.pos < end) {
     const uint64_t at = p.pos - beg;
     const bool y = p.attempt(z, &x, &amb);
+    if (y && sc) sc[n] = x;  // raw (unscaled) speculative sample n of the chunk
     n += y ? 1u : 0u;
     if (at < 8) {
       starts |= 1u << at;
@@ -250,7 +261,8 @@ __global__ void __launch_bounds__(1024) k_scan(const StreamDesc* __restrict__ st
                                                const uint64_t* __restrict__ keys,
                                                const uint64_t* __restrict__ spec_exit,
                                                uint64_t* __restrict__ exit_pos, uint32_t* __restrict__ count,
-                                               uint64_t* __restrict__ offset, unsigned* flags) {
+                                               uint64_t* __restrict__ offset, uint32_t* __restrict__ skip,
+                                               unsigned* flags) {
   __shared__ uint64_t ki[256];
   __shared__ double wi[256], fi[256];
   __shared__ int64_t first_bad;
@@ -268,12 +280,15 @@ __global__ void __launch_bounds__(1024) k_scan(const StreamDesc* __restrict__ st
     const uint32_t raw = count[cb + i];
     uint32_t n = raw & 0xffffu;
     uint64_t ex = spec_exit[cb + i];
+    uint32_t sk = 0;  // leading speculative samples the true parse drops (~0u: re-parse in emit)
     if (i > 0) {
       const uint64_t off = spec_exit[cb + i - 1] - (uint64_t)i * CH;
       const uint32_t starts = (raw >> 16) & 0xffu, yields = raw >> 24;
       if (off < 8 && ((starts >> off) & 1u)) {
-        n -= (uint32_t)__popc(yields & ((1u << off) - 1u));
+        sk = (uint32_t)__popc(yields & ((1u << off) - 1u));
+        n -= sk;
       } else {  // the entry falls inside a speculative attempt: re-parse this chunk
+        sk = ~0u;
         Parser p;
         p.init(keys[2 * blockIdx.x], keys[2 * blockIdx.x + 1], spec_exit[cb + i - 1]);
         const uint64_t end = (uint64_t)(i + 1) * CH;
@@ -287,6 +302,7 @@ __global__ void __launch_bounds__(1024) k_scan(const StreamDesc* __restrict__ st
     }
     count[cb + i] = n;
     exit_pos[cb + i] = ex;
+    if (skip) skip[cb + i] = sk;
   }
   __syncthreads();
   if (first_bad < nc && threadIdx.x == 0) {
@@ -302,6 +318,7 @@ __global__ void __launch_bounds__(1024) k_scan(const StreamDesc* __restrict__ st
       while (p.pos < end) n += p.attempt(z, &x, &amb) ? 1u : 0u;
       exit_pos[cb + i] = p.pos;
       count[cb + i] = n;
+      if (skip) skip[cb + i] = ~0u;
     }
   }
   __syncthreads();
@@ -371,6 +388,71 @@ __global__ void __launch_bounds__(256) k_emit(const StreamDesc* __restrict__ str
   if (amb) atomicAdd(&flags[1], amb);
 }
 
+// store one emitted sample (scaled if the stream asks) and its optional 16-bit / fp32 copies
+__device__ __forceinline__ void put_sample(double* dst, uint16_t* d16, bool bf16, float* d32, uint64_t o, double v) {
+  dst[o] = v;
+  if (d16) {
+    const float f = (float)v;
+    d16[o] = bf16 ? __bfloat16_as_ushort(__float2bfloat16_rn(f)) : __half_as_ushort(__float2half_rn(f));
+  }
+  if (d32) d32[o] = (float)v;
+}
+
+// warp per chunk (grid-stride): copy the chunk's speculative samples [skip, skip + count) to
+// their offsets (lanes along the samples: coalesced), or re-parse it on lane 0 when
+// skip == ~0u -- with the ziggurat tables read from global memory (the rare path; staging
+// them in shared memory per CTA would cost more than the copy itself)
+__global__ void __launch_bounds__(256) k_emit_copy(const StreamDesc* __restrict__ streams,
+                                                   const uint32_t* __restrict__ chunk_stream, int64_t C,
+                                                   const uint64_t* __restrict__ keys,
+                                                   const uint64_t* __restrict__ exit_pos,
+                                                   const uint64_t* __restrict__ offset,
+                                                   const uint32_t* __restrict__ count,
+                                                   const uint32_t* __restrict__ skip,
+                                                   const double* __restrict__ scratch, double* __restrict__ out,
+                                                   uint16_t* __restrict__ out16, bool bf16, float* __restrict__ out32,
+                                                   unsigned* flags) {
+  const Zig z{zo_zig_ki, zo_zig_wi, zo_zig_fi};
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < C; c += warps) {
+    const uint32_t s = chunk_stream[c];
+    const StreamDesc& d = streams[s];
+    const uint64_t o = offset[c];
+    if (o >= d.n) continue;
+    double* dst = out + d.out_off;
+    uint16_t* d16 = out16 ? out16 + d.out_off : nullptr;
+    float* d32 = out32 ? out32 + d.out_off : nullptr;
+    const double scale = d.scale;
+    const bool scaled = d.apply_scale != 0;
+    const uint32_t sk = skip[c];
+    if (sk != ~0u) {
+      const uint64_t n = min((uint64_t)count[c], d.n - o);
+      const double* src = scratch + (size_t)c * CH + sk;
+      for (uint64_t i = lane; i < n; i += 32) {
+        const double x = src[i];
+        put_sample(dst, d16, bf16, d32, o + i, scaled ? __dmul_rn(scale, x) : x);
+      }
+      continue;
+    }
+    if (lane == 0) {
+      const uint64_t local = (uint64_t)(c - (int64_t)d.chunk_begin);
+      const uint64_t end = (local + 1) * CH;
+      const uint64_t entry = local == 0 ? 0 : exit_pos[c - 1];
+      Parser p;
+      p.init(keys[2 * s], keys[2 * s + 1], entry);
+      unsigned amb = 0;
+      double x;
+      uint64_t oo = o;
+      while (p.pos < end && oo < d.n) {
+        if (p.attempt(z, &x, &amb)) put_sample(dst, d16, bf16, d32, oo++, scaled ? __dmul_rn(scale, x) : x);
+      }
+      if (amb) atomicAdd(&flags[1], amb);
+    }
+    __syncwarp();
+  }
+}
+
 uint64_t sampler_chunks_for(uint64_t n) {
   // expected u64/sample ~1.025; + generous margin so the scan never runs short
   uint64_t pos = n + n / 8 + 4 * CH;
@@ -382,8 +464,20 @@ void sampler_launch(const SamplerPlan& P, uint64_t seed, const uint64_t* d_step,
   if (P.S == 0) return;
   k_keys<<<(P.S + 127) / 128, 128, 0, st>>>(P.d_streams, P.S, seed, d_step, nu, P.d_keys);
   unsigned grid = (unsigned)((P.C + 255) / 256);
-  k_spec<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_spec, P.d_count, P.d_flags);
-  k_scan<<<P.S, 1024, 0, st>>>(P.d_streams, P.d_keys, P.d_spec, P.d_exit, P.d_count, P.d_offset, P.d_flags);
+  const bool copy = P.d_scratch && P.d_skip;
+  k_spec<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_spec, P.d_count,
+                               copy ? P.d_scratch : nullptr, P.d_flags);
+  k_scan<<<P.S, 1024, 0, st>>>(P.d_streams, P.d_keys, P.d_spec, P.d_exit, P.d_count, P.d_offset,
+                               copy ? P.d_skip : nullptr, P.d_flags);
+  if (copy) {
+    // a warp per chunk: each chunk is a short dependent chain (stream -> offset -> copy), so
+    // occupancy, not a grid-stride loop, hides it
+    const unsigned cgrid = (unsigned)std::min<int64_t>((P.C + 7) / 8, (int64_t)1 << 30);
+    k_emit_copy<<<cgrid, 256, 0, st>>>(
+        P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_exit, P.d_offset, P.d_count, P.d_skip, P.d_scratch, out,
+        static_cast<uint16_t*>(P.out16), P.out16_bf16, P.out32, P.d_flags);
+    return;
+  }
   k_emit<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_exit, P.d_offset, out,
                                P.d_flags);
 }

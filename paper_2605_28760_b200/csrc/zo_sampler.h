@@ -34,6 +34,15 @@ struct SamplerPlan {
   uint32_t* d_count = nullptr;
   uint64_t* d_offset = nullptr;
   unsigned* d_flags = nullptr;  // [0] short stream, [1] exp ambiguity, [2] splice repairs
+  // optional: k_spec keeps every chunk's speculative samples (C x 128 doubles) and k_scan
+  // the number of leading samples to drop (d_skip; ~0u: re-parse), so the emit pass is a
+  // coalesced copy instead of a second Philox + ziggurat pass
+  double* d_scratch = nullptr;
+  uint32_t* d_skip = nullptr;
+  // optional extra outputs at the same offsets as `out`: a 16-bit (fp16 / bf16) and an fp32 copy
+  void* out16 = nullptr;
+  bool out16_bf16 = false;
+  float* out32 = nullptr;
 };
 
 uint64_t sampler_chunks_for(uint64_t n);

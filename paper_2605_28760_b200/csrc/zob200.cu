@@ -286,7 +286,7 @@ Matrix& find(zo_ctx* c, const char* lid) {
   throw Error(ZO_ERR_INPUT, std::string("unknown layer id ") + lid);
 }
 
-void build_sampler_plan(zo_ctx* c, SamplerPlan& P, std::vector<StreamDesc>& sd) {
+void build_sampler_plan(zo_ctx* c, SamplerPlan& P, std::vector<StreamDesc>& sd, bool scratch = false) {
   int64_t chunk = 0;
   std::vector<uint32_t> chunk_stream;
   for (size_t s = 0; s < sd.size(); ++s) {
@@ -305,6 +305,10 @@ void build_sampler_plan(zo_ctx* c, SamplerPlan& P, std::vector<StreamDesc>& sd) 
   P.d_count = c->mem.get<uint32_t>(chunk);
   P.d_offset = c->mem.get<uint64_t>(chunk);
   P.d_flags = c->flags;
+  if (scratch) {  // speculative samples kept for the copy emit (zo_sampler.h)
+    P.d_scratch = c->mem.get<double>((size_t)chunk * 128);
+    P.d_skip = c->mem.get<uint32_t>(chunk);
+  }
   ZO_CUDA_TRY(cudaMemcpy(P.d_streams, sd.data(), sd.size() * sizeof(StreamDesc), cudaMemcpyHostToDevice));
   ZO_CUDA_TRY(cudaMemcpy(P.d_chunk_stream, chunk_stream.data(), chunk_stream.size() * 4, cudaMemcpyHostToDevice));
 }
@@ -709,9 +713,10 @@ void set_step(zo_ctx* c, uint64_t step) {
 
 void launch_dense_update_dev(zo_ctx* c, double lr, const double* out4, const unsigned* abort_flag) {
   if (c->fast_update) {
-    // 16-bit operands of this step's directions, then one fused GEMM + RMW per matrix
-    launch_shadow(c->U, c->su, c->U16, c->bf16, c->st);
-    launch_shadow(c->V, c->sv, c->V16, c->bf16, c->st);
+    // 16-bit operands of this step's directions (written by the sampler's emit when its plans
+    // carry them, else converted here), then one fused GEMM + RMW per matrix
+    if (c->planU.out16 != c->U16) launch_shadow(c->U, c->su, c->U16, c->bf16, c->st);
+    if (c->planV.out16 != c->V16) launch_shadow(c->V, c->sv, c->V16, c->bf16, c->st);
     if (c->upd_plans.empty()) {
       c->upd_plans.resize(c->mats.size());
       for (size_t i = 0; i < c->mats.size(); ++i) {
@@ -1082,8 +1087,9 @@ int zo_create(zo_ctx** out, const zo_model_desc* desc) {
     sv.out_off = (uint64_t)m.v_off;
     c->streamsV.push_back(sv);
   }
-  build_sampler_plan(c.get(), c->planU, c->streamsU);
-  build_sampler_plan(c.get(), c->planV, c->streamsV);
+  // the direction plans emit by copy (one Philox pass per sample)
+  build_sampler_plan(c.get(), c->planU, c->streamsU, true);
+  build_sampler_plan(c.get(), c->planV, c->streamsV, true);
   if (c->dense) {
     // dense_direction(seed, step, lid, (m, n)) = sample_gaussian(key DENSE_Z, m, n) row-major
     for (auto& m : c->mats) {
@@ -1347,6 +1353,9 @@ int zo_set_slot(zo_ctx* c, int32_t which, const double* host, int64_t count) {
   check(which >= 0 && which <= 2, ZO_ERR_INPUT, "bad slot id");
   check(count == (which == 1 ? c->sv : c->su), ZO_ERR_DIMENSION, "slot arena size mismatch");
   ZO_CUDA_TRY(cudaMemcpyAsync(slot_ptr(c, which), host, (size_t)count * 8, cudaMemcpyHostToDevice, c->st));
+  // host directions: refresh the tensor update's 16-bit copies the sampler would have written
+  if (which == 0 && c->planU.out16) launch_shadow(c->U, c->su, c->U16, c->bf16, c->st);
+  if (which == 1 && c->planV.out16) launch_shadow(c->V, c->sv, c->V16, c->bf16, c->st);
   if (which == 1) {
     write_vext_all(c);
     // a host V carries no window key: the next step resamples V (folding A with THIS V
@@ -1375,6 +1384,10 @@ int zo_set_update_mode(zo_ctx* c, int32_t mode) {
       c->V16 = c->mem.get<uint16_t>((size_t)c->sv);
     }
   }
+  // tensor mode: the direction sampler writes the update's 16-bit U / V operands as it emits
+  c->planU.out16 = mode == 1 ? c->U16 : nullptr;
+  c->planV.out16 = mode == 1 ? c->V16 : nullptr;
+  c->planU.out16_bf16 = c->planV.out16_bf16 = c->bf16;
   if ((mode == 1) != c->master32) {
     if (!c->conv_tmp) c->conv_tmp = c->mem.get<float>(CONV_CHUNK);
     for (auto& m : c->mats) {
