@@ -1380,8 +1380,10 @@ int zo_set_update_mode(zo_ctx* c, int32_t mode) {
     check(c->r >= 16 && c->r % 16 == 0, ZO_ERR_CONFIG, "the tensor-core dense update needs rank >= 16, multiple of 16");
     check(!c->real32, ZO_ERR_CONFIG, "real32 keeps the exact float64 update");
     if (!c->U16) {
-      c->U16 = c->mem.get<uint16_t>((size_t)c->su);
-      c->V16 = c->mem.get<uint16_t>((size_t)c->sv);
+      // + 256 rows of padding: an update GEMM's A-operand tensor map spans the matrix's rows
+      // rounded up to the 128-row tile, so the last matrix's box reads past its slice
+      c->U16 = c->mem.get<uint16_t>((size_t)c->su + (size_t)256 * c->r);
+      c->V16 = c->mem.get<uint16_t>((size_t)c->sv + (size_t)256 * c->r);
     }
   }
   // tensor mode: the direction sampler writes the update's 16-bit U / V operands as it emits
