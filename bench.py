@@ -136,8 +136,12 @@ def ncu_traffic(model):
     """DRAM bytes (read + write) of one launch of each of the four layer GEMMs, from the
     committed `ncu --set full` capture (profiles/), or None when not captured for this model."""
     import csv
-    p = os.path.join(HERE, "profiles", "r01g_ncu_gemm_opt13b.csv")
-    if model != "opt-13b" or not os.path.exists(p):
+    if model != "opt-13b":
+        return None
+    # the newest committed capture (profiles/capture.sh)
+    cands = [os.path.join(HERE, "profiles", n) for n in ("r02_final/ncu_gemm_opt13b.csv", "r01g_ncu_gemm_opt13b.csv")]
+    p = next((c for c in cands if os.path.exists(c)), None)
+    if p is None:
         return None
     tot = 0.0
     with open(p) as f:

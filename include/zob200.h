@@ -115,6 +115,12 @@ int zo_sample_stream(zo_ctx* ctx, uint64_t seed, uint64_t step, uint64_t lid_has
  * chained into u_digest after the matrices, zo_engine.py:256-260) */
 int zo_slot_count(const zo_ctx* ctx, int32_t which, int64_t* count);
 int zo_get_slot(zo_ctx* ctx, int32_t which, double* host, int64_t count);
+/* asynchronous U (0) / V (1) arena snapshot into pinned host ring slot `slot` (0..3): a
+ * device copy in stream order, then the host copy on a side stream overlapping the next
+ * step (the host digests of run_serving_path); _wait blocks until the slot has landed and
+ * returns its (engine-owned) host pointer.  A slot must be waited on before it is reused. */
+int zo_slot_snapshot(zo_ctx* ctx, int32_t which, int32_t slot);
+int zo_slot_snapshot_wait(zo_ctx* ctx, int32_t which, int32_t slot, const double** host);
 int zo_set_slot(zo_ctx* ctx, int32_t which, const double* host, int64_t count);
 /* declare which window start the V arena holds (a host upload of V leaves it
  * unknown, so the next step would fold A and resample V): resuming mid-window

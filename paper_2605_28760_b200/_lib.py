@@ -58,6 +58,8 @@ SIGNATURES = [
     ("zo_set_window", _c.c_int, [_P, _c.c_int64]),
     ("zo_set_update_mode", _c.c_int, [_P, _c.c_int32]),
     ("zo_set_schedule", _c.c_int, [_P, _c.c_int32]),
+    ("zo_slot_snapshot", _c.c_int, [_P, _c.c_int32, _c.c_int32]),
+    ("zo_slot_snapshot_wait", _c.c_int, [_P, _c.c_int32, _c.c_int32, _P]),
     ("zo_sampler_flags", _c.c_int, [_P, _c.POINTER(_c.c_uint32)]),
     ("zo_prepare_probe", _c.c_int, [_P, _c.c_double, _c.c_int32]),
     ("zo_score", _c.c_int, [_P, _P, _P, _c.c_int32, _c.c_int32, _P]),

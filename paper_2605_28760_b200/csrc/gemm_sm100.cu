@@ -1095,6 +1095,8 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
     return !e || std::atoi(e) != 0;
   }();
   g.cg = (cg2_on && N > 128 && bn >= 128 && M >= 512) ? 2 : 1;
+  // the update kernel's master-block ring leaves no room for 256-wide single-CTA operand tiles
+  if (epi == EPI_UPDATE64 && g.cg == 1 && bn > 128) g.bn = bn = 128;
   // N=128 pair tiles measured 1.4-1.5x slower (A re-reads, fixed costs), 192-wide no
   // faster than 256 on the ragged 13B shapes (they re-read A 33% more)
   if (g.cg == 2) g.bn = bn = 256;

@@ -229,6 +229,14 @@ struct zo_ctx {
     int kernels = 0;
   };
   GraphSlot gs_score, gs_apply, gs_qscore, gs_qapply;
+  // asynchronous slot snapshots (zo_slot_snapshot): U / V -> a device copy (in stream order)
+  // -> pinned host ring on a side stream, overlapping the next step
+  static constexpr int SNAP_RING = 4;
+  cudaStream_t snap_st = nullptr;
+  double* snap_dev[2] = {nullptr, nullptr};
+  double* snap_host[2][SNAP_RING] = {};
+  cudaEvent_t snap_ready[2][SNAP_RING] = {}, snap_done[2][SNAP_RING] = {};
+  cudaEvent_t snap_last[2] = {nullptr, nullptr};  // the last D2H out of snap_dev[which]
   uint64_t* d_base = nullptr;  // q-direction macro-step base step (t * G), set before the apply graph
   void drop_graphs() {
     gkey_valid = false;
@@ -239,6 +247,13 @@ struct zo_ctx {
     if (gexec) cudaGraphExecDestroy(gexec);
     for (GraphSlot* g : {&gs_score, &gs_apply, &gs_qscore, &gs_qapply})
       if (g->exec) cudaGraphExecDestroy(g->exec);
+    for (int w = 0; w < 2; ++w)
+      for (int k = 0; k < SNAP_RING; ++k) {
+        if (snap_host[w][k]) cudaFreeHost(snap_host[w][k]);
+        if (snap_ready[w][k]) cudaEventDestroy(snap_ready[w][k]);
+        if (snap_done[w][k]) cudaEventDestroy(snap_done[w][k]);
+      }
+    if (snap_st) cudaStreamDestroy(snap_st);
     if (cap_st) cudaStreamDestroy(cap_st);
     if (h_tok) cudaFreeHost(h_tok);
     if (h_gold) cudaFreeHost(h_gold);
@@ -1344,6 +1359,46 @@ int zo_get_slot(zo_ctx* c, int32_t which, double* host, int64_t count) {
   check(count == slot_size(c, which), ZO_ERR_DIMENSION, "slot arena size mismatch");
   ZO_CUDA_TRY(cudaMemcpyAsync(host, slot_ptr(c, which), (size_t)count * 8, cudaMemcpyDeviceToHost, c->st));
   ZO_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return ZO_OK;
+  ZO_API_END
+}
+
+// Snapshot the U (0) or V (1) arena into pinned host ring slot `slot` without blocking the
+// step stream: a device-to-device copy in stream order (the next step's sampler may then
+// overwrite the arena), then the device-to-host copy on a side stream that overlaps the next
+// step.  zo_slot_snapshot_wait blocks until that slot's copy has landed and returns it.
+int zo_slot_snapshot(zo_ctx* c, int32_t which, int32_t slot) {
+  ZO_API_BEGIN
+  check(which == 0 || which == 1, ZO_ERR_INPUT, "snapshots cover the U and V arenas");
+  check(slot >= 0 && slot < zo_ctx::SNAP_RING, ZO_ERR_INPUT, "snapshot slot out of range");
+  const size_t n = which == 1 ? (size_t)c->sv : (size_t)c->su;
+  if (!c->snap_st) ZO_CUDA_TRY(cudaStreamCreateWithFlags(&c->snap_st, cudaStreamNonBlocking));
+  if (!c->snap_dev[which]) c->snap_dev[which] = c->mem.get<double>(n);
+  if (!c->snap_host[which][slot]) {
+    ZO_CUDA_TRY(cudaMallocHost(&c->snap_host[which][slot], n * 8));
+    ZO_CUDA_TRY(cudaEventCreateWithFlags(&c->snap_ready[which][slot], cudaEventDisableTiming));
+    ZO_CUDA_TRY(cudaEventCreateWithFlags(&c->snap_done[which][slot], cudaEventDisableTiming));
+  }
+  // the previous D2H out of the device copy must be done before it is overwritten, and this
+  // host slot's previous copy must have been consumed (the caller waited on it)
+  if (c->snap_last[which]) ZO_CUDA_TRY(cudaStreamWaitEvent(c->st, c->snap_last[which], 0));
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->snap_dev[which], slot_ptr(c, which), n * 8, cudaMemcpyDeviceToDevice, c->st));
+  ZO_CUDA_TRY(cudaEventRecord(c->snap_ready[which][slot], c->st));
+  ZO_CUDA_TRY(cudaStreamWaitEvent(c->snap_st, c->snap_ready[which][slot], 0));
+  ZO_CUDA_TRY(cudaMemcpyAsync(c->snap_host[which][slot], c->snap_dev[which], n * 8, cudaMemcpyDeviceToHost,
+                              c->snap_st));
+  ZO_CUDA_TRY(cudaEventRecord(c->snap_done[which][slot], c->snap_st));
+  c->snap_last[which] = c->snap_done[which][slot];
+  return ZO_OK;
+  ZO_API_END
+}
+
+int zo_slot_snapshot_wait(zo_ctx* c, int32_t which, int32_t slot, const double** host) {
+  ZO_API_BEGIN
+  check((which == 0 || which == 1) && slot >= 0 && slot < zo_ctx::SNAP_RING && c->snap_host[which][slot],
+        ZO_ERR_INPUT, "no such snapshot");
+  ZO_CUDA_TRY(cudaEventSynchronize(c->snap_done[which][slot]));
+  *host = c->snap_host[which][slot];
   return ZO_OK;
   ZO_API_END
 }

@@ -185,6 +185,19 @@ class ZoEngine:
         check(lib().zo_get_slot(self._h, which, out.ctypes.data, n))
         return out
 
+    def snapshot(self, which: int, slot: int) -> None:
+        """Start an asynchronous copy of the U / V arena into host ring slot `slot` (zob200.h
+        zo_slot_snapshot); read it with snapshot_wait."""
+        check(lib().zo_slot_snapshot(self._h, which, slot))
+
+    def snapshot_wait(self, which: int, slot: int) -> np.ndarray:
+        """The landed snapshot (a view of engine-owned pinned memory, valid until the slot is
+        reused)."""
+        p = ctypes.c_void_p()
+        check(lib().zo_slot_snapshot_wait(self._h, which, slot, ctypes.byref(p)))
+        n = self.sv if which == V else self.su
+        return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)), shape=(n,))
+
     def set_slot(self, which: int, arena: np.ndarray) -> None:
         a = np.ascontiguousarray(arena, dtype=np.float64).reshape(-1)
         n = self.sv if which == V else self.su

@@ -63,6 +63,29 @@ class ServingRun:
     extra: dict = field(default_factory=dict)
 
 
+SNAP_RING = 4  # zob200.h zo_slot_snapshot ring depth
+
+
+class _SnapRing:
+    """Pinned host ring of asynchronous U / V arena snapshots (zob200.h zo_slot_snapshot): the
+    device copy is stream-ordered, the host copy overlaps the next step, and a slot is reused
+    only after the digest reading it has finished."""
+
+    def __init__(self, eng, which: int):
+        self.eng, self.which, self.next, self.busy = eng, which, 0, [None] * SNAP_RING
+
+    def digest(self, pool, z_arena=None):
+        slot = self.next
+        self.next = (slot + 1) % SNAP_RING
+        if self.busy[slot] is not None:
+            self.busy[slot].result()
+        self.eng.snapshot(self.which, slot)
+        eng, which = self.eng, self.which
+        fut = pool.submit(lambda: eng.digest(which, eng.snapshot_wait(which, slot), z_arena))
+        self.busy[slot] = fut
+        return fut
+
+
 def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: int, precision: str = "real64",
                      eval_every: int = 50, fold_on_eval: bool = False, abort_at: int | None = None,
                      params=None, digests: bool = True, compute_param_digests: bool = True,
@@ -98,6 +121,7 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
     meter = CostMeter()
     step_fn = lozo_step if zcfg.estimator == "lozo_lazy" else factorized_step
     pool = cf.ThreadPoolExecutor(max_workers=4) if digests else None
+    rings = {SLOT_U: _SnapRing(eng, SLOT_U), SLOT_V: _SnapRing(eng, SLOT_V)}
     pending: list[tuple[ZoStepRecord, cf.Future, cf.Future | None]] = []
     vfut = {"key": None, "fut": None}
     trajectory: list[ZoStepRecord] = []
@@ -134,12 +158,14 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
         meter.scoring_calls += 2
         meter.scoring_cost_units += 2 * zcfg.batch_size
         if pool is not None and (t - start_step) % digest_every == 0:
-            u_arena = eng.get_slot(SLOT_U)
+            # U (and a new window's V) leave through asynchronous snapshots into a pinned ring:
+            # the device copy is stream-ordered, the host copy overlaps the next step, and the
+            # digest thread waits for it (a ring slot is reused only after its digest is done)
             z_arena = eng.get_slot(SLOT_Z) if zcfg.scope == "full" else None
-            ufut = pool.submit(eng.digest, SLOT_U, u_arena, z_arena)
+            ufut = rings[SLOT_U].digest(pool, z_arena)
             wkey = (t // zcfg.nu) * zcfg.nu if zcfg.estimator == "lozo_lazy" else t
             if vfut["key"] != wkey:
-                vfut["key"], vfut["fut"] = wkey, pool.submit(eng.digest, SLOT_V, eng.get_slot(SLOT_V))
+                vfut["key"], vfut["fut"] = wkey, rings[SLOT_V].digest(pool)
             pending.append((rec, ufut, vfut["fut"]))
         trajectory.append(rec)
         done = t + 1
