@@ -398,10 +398,12 @@ __device__ __forceinline__ void put_sample(double* dst, uint16_t* d16, bool bf16
   if (d32) d32[o] = (float)v;
 }
 
-// warp per chunk (grid-stride): copy the chunk's speculative samples [skip, skip + count) to
-// their offsets (lanes along the samples: coalesced), or re-parse it on lane 0 when
-// skip == ~0u -- with the ziggurat tables read from global memory (the rare path; staging
-// them in shared memory per CTA would cost more than the copy itself)
+// Copy emit: a warp takes 32 consecutive chunks at a time -- lane l loads chunk l's metadata
+// (stream, offset, skip, count) so the dependent loads are paid once per 32 chunks -- then
+// copies each chunk's speculative samples [skip, skip + count) with all 32 lanes (coalesced),
+// writing the optional 16-bit / fp32 copies in the same pass.  A chunk whose entry fell
+// inside a speculative attempt (skip == ~0u, rare) is re-parsed by its own lane afterwards,
+// with the ziggurat tables read from global memory.
 __global__ void __launch_bounds__(256) k_emit_copy(const StreamDesc* __restrict__ streams,
                                                    const uint32_t* __restrict__ chunk_stream, int64_t C,
                                                    const uint64_t* __restrict__ keys,
@@ -415,27 +417,46 @@ __global__ void __launch_bounds__(256) k_emit_copy(const StreamDesc* __restrict_
   const Zig z{zo_zig_ki, zo_zig_wi, zo_zig_fi};
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); c < C; c += warps) {
-    const uint32_t s = chunk_stream[c];
-    const StreamDesc& d = streams[s];
-    const uint64_t o = offset[c];
-    if (o >= d.n) continue;
-    double* dst = out + d.out_off;
-    uint16_t* d16 = out16 ? out16 + d.out_off : nullptr;
-    float* d32 = out32 ? out32 + d.out_off : nullptr;
-    const double scale = d.scale;
-    const bool scaled = d.apply_scale != 0;
-    const uint32_t sk = skip[c];
-    if (sk != ~0u) {
-      const uint64_t n = min((uint64_t)count[c], d.n - o);
-      const double* src = scratch + (size_t)c * CH + sk;
+  for (int64_t c0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; c0 < C; c0 += warps * 32) {
+    // lane-owned metadata of chunk c0 + lane
+    const int64_t c = c0 + lane;
+    uint64_t o = ~0ull, dn = 0, doff = 0;
+    uint32_t sk = 0, cnt = 0, s = 0;
+    double scale = 1.0;
+    int scaled = 0;
+    if (c < C) {
+      s = chunk_stream[c];
+      const StreamDesc& d = streams[s];
+      o = offset[c];
+      dn = d.n;
+      doff = d.out_off;
+      scale = d.scale;
+      scaled = d.apply_scale != 0;
+      sk = skip[c];
+      cnt = count[c];
+    }
+    const int nj = (int)min((int64_t)32, C - c0);
+    for (int j = 0; j < nj; ++j) {
+      const uint64_t oj = __shfl_sync(0xffffffffu, o, j);
+      const uint64_t dnj = __shfl_sync(0xffffffffu, dn, j);
+      const uint32_t skj = __shfl_sync(0xffffffffu, sk, j);
+      if (oj >= dnj || skj == ~0u) continue;  // past the stream's end / re-parsed below
+      const uint64_t doffj = __shfl_sync(0xffffffffu, doff, j);
+      const double scj = __shfl_sync(0xffffffffu, scale, j);
+      const int sdj = __shfl_sync(0xffffffffu, scaled, j);
+      const uint64_t n = min((uint64_t)__shfl_sync(0xffffffffu, cnt, j), dnj - oj);
+      const double* src = scratch + (size_t)(c0 + j) * CH + skj;
+      double* dst = out + doffj;
+      uint16_t* d16 = out16 ? out16 + doffj : nullptr;
+      float* d32 = out32 ? out32 + doffj : nullptr;
+#pragma unroll 4
       for (uint64_t i = lane; i < n; i += 32) {
         const double x = src[i];
-        put_sample(dst, d16, bf16, d32, o + i, scaled ? __dmul_rn(scale, x) : x);
+        put_sample(dst, d16, bf16, d32, oj + i, sdj ? __dmul_rn(scj, x) : x);
       }
-      continue;
     }
-    if (lane == 0) {
+    if (c < C && sk == ~0u && o < dn) {  // rare: re-parse this lane's chunk from its true entry
+      const StreamDesc& d = streams[s];
       const uint64_t local = (uint64_t)(c - (int64_t)d.chunk_begin);
       const uint64_t end = (local + 1) * CH;
       const uint64_t entry = local == 0 ? 0 : exit_pos[c - 1];
@@ -444,7 +465,10 @@ __global__ void __launch_bounds__(256) k_emit_copy(const StreamDesc* __restrict_
       unsigned amb = 0;
       double x;
       uint64_t oo = o;
-      while (p.pos < end && oo < d.n) {
+      double* dst = out + doff;
+      uint16_t* d16 = out16 ? out16 + doff : nullptr;
+      float* d32 = out32 ? out32 + doff : nullptr;
+      while (p.pos < end && oo < dn) {
         if (p.attempt(z, &x, &amb)) put_sample(dst, d16, bf16, d32, oo++, scaled ? __dmul_rn(scale, x) : x);
       }
       if (amb) atomicAdd(&flags[1], amb);
@@ -470,9 +494,8 @@ void sampler_launch(const SamplerPlan& P, uint64_t seed, const uint64_t* d_step,
   k_scan<<<P.S, 1024, 0, st>>>(P.d_streams, P.d_keys, P.d_spec, P.d_exit, P.d_count, P.d_offset,
                                copy ? P.d_skip : nullptr, P.d_flags);
   if (copy) {
-    // a warp per chunk: each chunk is a short dependent chain (stream -> offset -> copy), so
-    // occupancy, not a grid-stride loop, hides it
-    const unsigned cgrid = (unsigned)std::min<int64_t>((P.C + 7) / 8, (int64_t)1 << 30);
+    // grid-stride over groups of 32 chunks per warp, up to 16 CTAs per SM
+    const unsigned cgrid = (unsigned)std::min<int64_t>((P.C + 255) / 256, 148 * 16);
     k_emit_copy<<<cgrid, 256, 0, st>>>(
         P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_exit, P.d_offset, P.d_count, P.d_skip, P.d_scratch, out,
         static_cast<uint16_t*>(P.out16), P.out16_bf16, P.out32, P.d_flags);
