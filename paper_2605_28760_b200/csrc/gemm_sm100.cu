@@ -216,7 +216,7 @@ __device__ __forceinline__ float unpack16(uint32_t w, int hi) {
   else return __half2float(__ushort_as_half(h));
 }
 
-template <int BN, int CG = 1, bool UPD = false>
+template <int BN, int CG = 1, bool UPD = false, bool RES = false>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;  // rows per CTA; a CTA pair (CG = 2) covers 256
   static constexpr int A_BYTES = BM * BK * 2;
@@ -228,9 +228,13 @@ struct GemmCfg {
   static constexpr int W_SLOTS = UPD ? 4 : 0;
   static constexpr int W_NBAR = 2 * W_SLOTS;  // barrier pairs (the fp32 ring's slot count)
   static constexpr int W_BYTES = 32 * BM * 8;
-  static constexpr int STAGES = UPD ? 3 : ((196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES);
+  // EPI_RESID32: per epilogue warp two 32 x 32 fp32 staging boxes for the TMA reduce-add of
+  // the residual (4 warps x 2 x 4 KB), paid for with one operand stage
+  static constexpr int O_BYTES = RES ? 4 * 2 * 32 * 32 * 4 : 0;
+  static constexpr int STAGES_MAX = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = UPD ? 3 : (RES && STAGES_MAX * STAGE_BYTES + O_BYTES > 200 * 1024 ? STAGES_MAX - 1 : STAGES_MAX);
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + W_SLOTS * W_BYTES + 512;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + W_SLOTS * W_BYTES + O_BYTES + 512;
 };
 
 struct GemmParams {
@@ -269,6 +273,7 @@ struct GemmParams {
   int upd_ld64, upd_ld16, upd_transposed;
   int upd_m32;  // the master holds fp32 values (zo_set_update_mode 1): half the master bytes
   int upd_shadow_rm;  // transposed update whose 16-bit shadow is row-major [i][j] (the embedding)
+  int res_tma;  // EPI_RESID32: the residual add as a TMA reduce-add through tmO
   const double* upd_out4;
   double upd_lr, upd_scale;
   const unsigned* upd_abort;
@@ -350,14 +355,15 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 template <int BN, int EPI, int DT, int XR, int CG>
 __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ? 320 : 192, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-           const __grid_constant__ CUtensorMap tmB2, GemmParams p) {
+           const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmO, GemmParams p) {
   // EPI_UPDATE32: EPI_UPDATE64 over an fp32 master (fp32 arithmetic, its own register budget)
   constexpr bool UPD = EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32, M32 = EPI == EPI_UPDATE32;
   // epilogue warp groups: the update variants run two groups of 4 warps (320 threads) -- their
   // epilogue is the whole kernel (a read-modify-write of every master block), latency-bound
   // at one warp per scheduler; group g takes the master-block rounds / column chunks = g mod 2
   constexpr int EGRP = UPD ? 2 : 1;
-  using C = GemmCfg<BN, CG, UPD>;
+  constexpr bool RES = EPI == EPI_RESID32;
+  using C = GemmCfg<BN, CG, UPD, RES>;
   constexpr bool BF16 = DT == 1, TF32 = DT == 2;
   constexpr int KE = TF32 ? 32 : 64;  // K elements per 128-byte block
   constexpr uint32_t FMT = TF32 ? 2u : BF16 ? 1u : 0u;  // instruction-descriptor a/b format
@@ -369,7 +375,8 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sW = smem + C::STAGES * C::STAGE_BYTES;  // EPI_UPDATE64 master-block ring
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sW + C::W_SLOTS * C::W_BYTES);
+  uint8_t* sO = sW + C::W_SLOTS * C::W_BYTES;  // EPI_RESID32 staging boxes (1024-aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sO + C::O_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4 + 2 * C::W_NBAR);
   // TMA-streamed master update (EPI_UPDATE64 on a projection): W64 blocks in/out through sW
   const bool wtma = UPD && p.upd_transposed;
@@ -386,6 +393,7 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     if (p.half_n || wtma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
+    if (RES && p.res_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmO)) : "memory");
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
@@ -529,6 +537,7 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
     const bool storer = ((warp - 2) & 3) == 0 && lane == 0;  // UPD: the group's TMA-store thread
     int wround_e = 0;        // EPI_UPDATE64: master blocks consumed so far (all groups, global order)
     int wprev = -1;          // EPI_UPDATE64: this group's previous round (its slot is released next)
+    int obuf = 0;            // EPI_RESID32 (TMA path): this warp's staging box to fill next
     const int erow = q * 32 + lane;  // row within the 128-row tile
     int it = 0;
     SegIter si;
@@ -846,6 +855,48 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
         goto tile_done;
       }
       if constexpr (EPI == EPI_RESID32) {
+        if (p.res_tma) {
+          // x32 += acc as a TMA reduce-add: each warp stages its 32 rows x 32 columns in a
+          // SWIZZLE_128B box (lane = row, 16-byte chunk j at j ^ (row & 7): 4-way banked,
+          // the minimum for 512 B) and one lane issues cp.reduce.async.bulk .add.f32 -- the
+          // residual read-modify-write happens in L2 (one fp32 round-to-nearest add per
+          // element, as before), none of it through the SM's load/store path.  Two boxes per
+          // warp alternate; a box is refilled once its previous reduce has read it.  Rows
+          // past M and columns past N are clipped by the tensor map.
+          uint8_t* box0 = sO + (size_t)(warp - 2) * 2 * 4096;
+#pragma unroll 1
+          for (int c = 0; c < bnc; c += 32) {
+            float v[32];
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+            if (split) add_partials(v, c);
+            const int col0 = n0 + c;
+            if (bb) {
+              if (col0 + 32 <= p.N)
+                add_bias(v, c);
+              else
+                for (int i = 0; i < 32; ++i)
+                  if (col0 + i < p.N) v[i] += bb[c + i];
+            }
+            uint8_t* box = box0 + obuf * 4096;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            __syncwarp();
+            float4* rowp = reinterpret_cast<float4*>(box + lane * 128);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) rowp[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0 && col0 < p.N) {
+              asm volatile(
+                  "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                      reinterpret_cast<uint64_t>(&tmO)),
+                  "r"(col0), "r"(m0 + q * 32), "r"(smem_u32(box))
+                  : "memory");
+              asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            obuf ^= 1;
+          }
+          goto tile_done;
+        }
         // fast path: whole tile row in range -> residual loads for chunk c+1 are in
         // flight while chunk c is added and stored
         const size_t lin0 = (size_t)row * p.ldo + n0;
@@ -999,6 +1050,8 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
   }
   if constexpr (UPD)
     if (wtma && warp >= 2 && ((warp - 2) & 3) == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if constexpr (RES)
+    if (p.res_tma && warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();
   if constexpr (CG == 2) cluster_sync_all();  // the pair's MMAs/epilogues are done before TMEM is freed
@@ -1109,6 +1162,24 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
   make_tmap_2d(&g.tmB, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg), dtype);
   make_tmap_2d(&g.tmB2, B, (uint64_t)N, (uint64_t)ldb, (uint64_t)ldb, (uint32_t)(bn / g.cg / 2), dtype);
   g.half_dp = g.half_n = 0;
+  // EPI_RESID32: the residual x32[M, N] (row stride ldo) as a TMA reduce-add target, 32 x 32
+  // fp32 boxes, SWIZZLE_128B (ZO_RES_TMA=0 keeps the load/add/store epilogue)
+  static const bool res_tma_on = [] {
+    const char* e = std::getenv("ZO_RES_TMA");
+    return !e || std::atoi(e) != 0;
+  }();
+  g.res_tma = 0;
+  if (epi == EPI_RESID32 && res_tma_on && ((size_t)ldo * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0) {
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)ldo * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&g.tmO, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, out, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(ZO_ERR_CUDA, "cuTensorMapEncodeTiled (residual) failed");
+    g.res_tma = 1;
+  }
 }
 
 static int max_pair_units(int num_sms);
@@ -1135,7 +1206,7 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms) {
 
 template <int BN, int EPI, int BF16, int XR, int CG>
 static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = -1, int last_ksteps = -1) {
-  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32>;
+  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32, EPI == EPI_RESID32>;
   constexpr int NT = (EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ? 320 : 192;  // k_gemm's launch bounds
   static bool attr_set = false;
   if (!attr_set) {
@@ -1181,12 +1252,13 @@ static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = 
   p.upd_transposed = g.upd_transposed;
   p.upd_m32 = g.upd_m32;
   p.upd_shadow_rm = g.upd_shadow_rm;
+  p.res_tma = g.res_tma;
   p.upd_out4 = g.upd_out4;
   p.upd_lr = g.upd_lr;
   p.upd_scale = g.upd_scale;
   p.upd_abort = g.upd_abort;
   if constexpr (CG == 1) {
-    launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(NT), C::SMEM, st, g.tmA, g.tmB, g.tmB2, p);
+    launch_pdl(k_gemm<BN, EPI, BF16, XR, 1>, dim3(g.grid), dim3(NT), C::SMEM, st, g.tmA, g.tmB, g.tmB2, g.tmO, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g.grid);
@@ -1202,7 +1274,7 @@ static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = 
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    ZO_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm<BN, EPI, BF16, XR, 2>, g.tmA, g.tmB, g.tmB2, p));
+    ZO_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gemm<BN, EPI, BF16, XR, 2>, g.tmA, g.tmB, g.tmB2, g.tmO, p));
   }
 }
 

@@ -25,6 +25,7 @@ struct GemmDesc {
   CUtensorMap tmA;
   CUtensorMap tmB;
   CUtensorMap tmB2;  // B with a half-height box: the half-width tail tiles (gemm_enable_halftail)
+  CUtensorMap tmO;   // EPI_RESID32: the residual as a TMA reduce-add target (res_tma)
   int M = 0, N = 0;
   int num_kb = 0;       // 64-wide K blocks
   int last_ksteps = 4;  // 16-wide UMMA steps issued in the last K block (trims the LoRA extension)
@@ -53,7 +54,8 @@ struct GemmDesc {
   void* upd_w16 = nullptr;
   int upd_ld64 = 0, upd_ld16 = 0, upd_transposed = 0;
   int upd_m32 = 0;  // upd_w64 actually holds fp32 values (the fast update mode's fp32 master)
-  int upd_shadow_rm = 0;  // upd_transposed with a row-major shadow W16[i][j] (the embedding, fp32 master)
+  int upd_shadow_rm = 0;
+  int res_tma = 0;  // EPI_RESID32 through cp.reduce.async.bulk (tmO), set by gemm_plan  // upd_transposed with a row-major shadow W16[i][j] (the embedding, fp32 master)
   const double* upd_out4 = nullptr;
   double upd_lr = 0.0, upd_scale = 1.0;
   const unsigned* upd_abort = nullptr;
