@@ -866,10 +866,13 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
           uint8_t* box0 = sO + (size_t)(warp - 2) * 2 * 4096;
 #pragma unroll 1
           for (int c = 0; c < bnc; c += 32) {
+            const int col0 = n0 + c;
+            // columns past N (a partial last tile): nothing to add -- and no staging write, which
+            // could overwrite the box the last issued reduce is still reading
+            if (col0 >= p.N) break;
             float v[32];
             tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
             if (split) add_partials(v, c);
-            const int col0 = n0 + c;
             if (bb) {
               if (col0 + 32 <= p.N)
                 add_bias(v, c);
@@ -885,7 +888,7 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
             for (int j = 0; j < 8; ++j) rowp[j ^ (lane & 7)] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0 && col0 < p.N) {
+            if (lane == 0) {
               asm volatile(
                   "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                       reinterpret_cast<uint64_t>(&tmO)),
