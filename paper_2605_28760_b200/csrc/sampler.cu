@@ -413,13 +413,13 @@ __global__ void __launch_bounds__(256) k_emit_copy(const StreamDesc* __restrict_
                                                    const uint32_t* __restrict__ skip,
                                                    const double* __restrict__ scratch, double* __restrict__ out,
                                                    uint16_t* __restrict__ out16, bool bf16, float* __restrict__ out32,
-                                                   unsigned* flags) {
+                                                   int G, unsigned* flags) {
   const Zig z{zo_zig_ki, zo_zig_wi, zo_zig_fi};
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t c0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; c0 < C; c0 += warps * 32) {
-    // lane-owned metadata of chunk c0 + lane
-    const int64_t c = c0 + lane;
+  for (int64_t c0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * G; c0 < C; c0 += warps * G) {
+    // lane-owned metadata of chunk c0 + lane (lanes < G)
+    const int64_t c = lane < G ? c0 + lane : C;
     uint64_t o = ~0ull, dn = 0, doff = 0;
     uint32_t sk = 0, cnt = 0, s = 0;
     double scale = 1.0;
@@ -435,7 +435,7 @@ __global__ void __launch_bounds__(256) k_emit_copy(const StreamDesc* __restrict_
       sk = skip[c];
       cnt = count[c];
     }
-    const int nj = (int)min((int64_t)32, C - c0);
+    const int nj = (int)min((int64_t)G, C - c0);
     for (int j = 0; j < nj; ++j) {
       const uint64_t oj = __shfl_sync(0xffffffffu, o, j);
       const uint64_t dnj = __shfl_sync(0xffffffffu, dn, j);
@@ -494,11 +494,16 @@ void sampler_launch(const SamplerPlan& P, uint64_t seed, const uint64_t* d_step,
   k_scan<<<P.S, 1024, 0, st>>>(P.d_streams, P.d_keys, P.d_spec, P.d_exit, P.d_count, P.d_offset,
                                copy ? P.d_skip : nullptr, P.d_flags);
   if (copy) {
-    // grid-stride over groups of 32 chunks per warp, up to 16 CTAs per SM
-    const unsigned cgrid = (unsigned)std::min<int64_t>((P.C + 255) / 256, 148 * 16);
+    // G chunks per warp (metadata loaded once per group): 32 for the large plans, fewer when
+    // that would leave the GPU under-filled (r = 2: 23 K chunks -> 8 per warp); grid-stride,
+    // up to 16 CTAs of 8 warps per SM
+    int G = 32;
+    while (G > 4 && (P.C + G - 1) / G < 148 * 16 * 8) G /= 2;
+    const int64_t warps = (P.C + G - 1) / G;
+    const unsigned cgrid = (unsigned)std::min<int64_t>((warps + 7) / 8, 148 * 16);
     k_emit_copy<<<cgrid, 256, 0, st>>>(
         P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_exit, P.d_offset, P.d_count, P.d_skip, P.d_scratch, out,
-        static_cast<uint16_t*>(P.out16), P.out16_bf16, P.out32, P.d_flags);
+        static_cast<uint16_t*>(P.out16), P.out16_bf16, P.out32, G, P.d_flags);
     return;
   }
   k_emit<<<grid, 256, 0, st>>>(P.d_streams, P.d_chunk_stream, P.C, P.d_keys, P.d_exit, P.d_offset, out,
