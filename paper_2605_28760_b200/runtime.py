@@ -140,8 +140,14 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
     done = start_step
     loop_t0 = time.perf_counter()
     eval_in_loop = 0.0
+    # the next step's minibatch is drawn on a host thread while the device runs this step (the
+    # engine call releases the GIL); the draw is a pure function of (seed, step)
+    prefetch = cf.ThreadPoolExecutor(max_workers=1)
+    nxt = prefetch.submit(sample_minibatch, task, "train", zcfg.seed, start_step, zcfg.batch_size)
     for t in range(start_step, start_step + steps):
-        batch = sample_minibatch(task, "train", zcfg.seed, t, zcfg.batch_size)
+        batch = nxt.result()
+        if t + 1 < start_step + steps:
+            nxt = prefetch.submit(sample_minibatch, task, "train", zcfg.seed, t + 1, zcfg.batch_size)
         t0 = time.perf_counter()
         try:
             if abort_at is not None and t == abort_at:
@@ -181,6 +187,7 @@ def run_serving_path(mcfg: ModelConfig, task: TaskData, zcfg: ZoConfig, steps: i
             do_eval(t + 1)
             eval_in_loop += time.perf_counter() - e0
     loop_wall = time.perf_counter() - loop_t0 - eval_in_loop
+    prefetch.shutdown(wait=False)
     if not aborted and final_fold and zcfg.estimator == "lozo_lazy":
         f0 = time.perf_counter()
         eng.fold()
