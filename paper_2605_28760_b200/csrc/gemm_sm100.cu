@@ -222,12 +222,11 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // EPI_UPDATE64: a short operand ring (K = rank) and a ring of float64 master blocks
-  // [32 rows][128 cols] streamed in and out by TMA: W_SLOTS x 32 KB for a float64 master, or
-  // 2 W_SLOTS x 16 KB for an fp32 master (the ring is latency-bound: twice the blocks in flight)
-  static constexpr int W_SLOTS = UPD ? 4 : 0;
-  static constexpr int W_NBAR = 2 * W_SLOTS;  // barrier pairs (the fp32 ring's slot count)
-  static constexpr int W_BYTES = 32 * BM * 8;
+  // EPI_UPDATE32: a short operand ring (K = rank) and a ring of fp32 master blocks
+  // [32 rows][128 cols] TMA-loaded (8 x 16 KB in flight); even slot count: a slot always serves
+  // the same epilogue warp group
+  static constexpr int W_SLOTS = UPD ? 8 : 0;
+  static constexpr int W_BYTES = 32 * BM * 4;
   // EPI_RESID32: per epilogue warp two 32 x 32 fp32 staging boxes for the TMA reduce-add of
   // the residual (4 warps x 2 x 4 KB), paid for with one operand stage
   static constexpr int O_BYTES = RES ? 4 * 2 * 32 * 32 * 4 : 0;
@@ -267,7 +266,7 @@ struct GemmParams {
   int bias_rps;
   long bias_vstride;
   int relu;
-  // EPI_UPDATE64 (see zo_gemm.h)
+  // EPI_UPDATE64 plans / EPI_UPDATE32 kernel (see zo_gemm.h)
   double* upd_w64;
   void* upd_w16;
   int upd_ld64, upd_ld16, upd_transposed;
@@ -353,11 +352,11 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // per MMA), 2 tf32 (kind::tf32 on fp32 storage, 32 elements per K block, K = 8 per MMA; the
 // same 32 bytes per MMA step, so the smem ring and descriptors are shared)
 template <int BN, int EPI, int DT, int XR, int CG>
-__global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ? 320 : 192, 1)
+__global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmO, GemmParams p) {
-  // EPI_UPDATE32: EPI_UPDATE64 over an fp32 master (fp32 arithmetic, its own register budget)
-  constexpr bool UPD = EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32, M32 = EPI == EPI_UPDATE32;
+  // EPI_UPDATE32: the tensor update over fp32 masters (the kernel variant of EPI_UPDATE64 plans)
+  constexpr bool UPD = EPI == EPI_UPDATE32, M32 = UPD;
   // epilogue warp groups: the update variants run two groups of 4 warps (320 threads) -- their
   // epilogue is the whole kernel (a read-modify-write of every master block), latency-bound
   // at one warp per scheduler; group g takes the master-block rounds / column chunks = g mod 2
@@ -374,16 +373,16 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint8_t* sW = smem + C::STAGES * C::STAGE_BYTES;  // EPI_UPDATE64 master-block ring
+  uint8_t* sW = smem + C::STAGES * C::STAGE_BYTES;  // EPI_UPDATE32 master-block ring
   uint8_t* sO = sW + C::W_SLOTS * C::W_BYTES;  // EPI_RESID32 staging boxes (1024-aligned)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sO + C::O_BYTES);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4 + 2 * C::W_NBAR);
-  // TMA-streamed master update (EPI_UPDATE64 on a projection): W64 blocks in/out through sW
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4 + 2 * C::W_SLOTS);
+  // the tensor update (EPI_UPDATE32): fp32 master blocks TMA-loaded through the sW ring
   const bool wtma = UPD && p.upd_transposed;
-  const uint32_t wfull0 = smem_u32(bars + 2 * C::STAGES + 4), wempty0 = wfull0 + 8 * C::W_NBAR;
+  const uint32_t wfull0 = smem_u32(bars + 2 * C::STAGES + 4), wempty0 = wfull0 + 8 * C::W_SLOTS;
   // master-block ring geometry: fp32 masters use twice the slots at half the size
-  constexpr int wslots = M32 ? C::W_NBAR : C::W_SLOTS;
-  constexpr uint32_t wbytes = M32 ? C::W_BYTES / 2 : C::W_BYTES;
+  constexpr int wslots = C::W_SLOTS;
+  constexpr uint32_t wbytes = C::W_BYTES;
   const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + C::STAGES);
   const uint32_t tfull0 = smem_u32(bars + 2 * C::STAGES), tempty0 = smem_u32(bars + 2 * C::STAGES + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -402,9 +401,9 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
       mbar_init(tfull0 + 8 * a, 1);
       mbar_init(tempty0 + 8 * a, 4 * EGRP * CG);  // every epilogue warp of the pair arrives at the leader
     }
-    for (int w = 0; w < C::W_NBAR; ++w) {
+    for (int w = 0; w < C::W_SLOTS; ++w) {
       mbar_init(wfull0 + 8 * w, 1);
-      mbar_init(wempty0 + 8 * w, M32 ? 4 : 1);  // fp32: the group's 4 warps release; fp64: the storer
+      mbar_init(wempty0 + 8 * w, 4);  // the group's 4 warps release a slot
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -438,7 +437,7 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      int wround = 0;  // EPI_UPDATE64: master blocks issued so far
+      int wround = 0;  // EPI_UPDATE32: master blocks issued so far
       SegIter si;
       si.init(p, CG);
       int t, k0, k1;
@@ -534,9 +533,7 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
   } else {
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     const int grp = (warp - 2) >> 2;  // epilogue warp group (0 unless UPD)
-    const bool storer = ((warp - 2) & 3) == 0 && lane == 0;  // UPD: the group's TMA-store thread
-    int wround_e = 0;        // EPI_UPDATE64: master blocks consumed so far (all groups, global order)
-    int wprev = -1;          // EPI_UPDATE64: this group's previous round (its slot is released next)
+    int wround_e = 0;        // EPI_UPDATE32: master blocks consumed so far (all groups, global order)
     int obuf = 0;            // EPI_RESID32 (TMA path): this warp's staging box to fill next
     const int erow = q * 32 + lane;  // row within the 128-row tile
     int it = 0;
@@ -719,140 +716,7 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
           wround_e = rbase + BN / 32;
           goto tile_done;
         }
-      }
-      if constexpr (UPD) {
-        if (!M32 && wtma) {
-          // projection: the master block of round r ([32 input rows i][128 output cols j],
-          // this warp's 32 j columns) arrives by TMA; lane j updates its column in place in
-          // shared memory, writes its 32 shadow values W16T[j][i..i+31] (64 contiguous bytes),
-          // and one thread streams the block back with a TMA store.  A block's slot is
-          // returned to the producer once the store of the NEXT round has been issued and
-          // this one's shared-memory reads are complete (cp.async.bulk.wait_group.read 1).
-          const bool skip = p.upd_abort ? (*p.upd_abort != 0u)
-                                        : !(isfinite(p.upd_out4[0]) && isfinite(p.upd_out4[1]));
-          const double alpha = -(p.upd_lr * p.upd_out4[2]) * p.upd_scale;
-          const int rbase = wround_e;  // global index of this tile's first round (producer order)
-#pragma unroll 1
-          for (int r = grp; r < BN / 32; r += EGRP) {
-            const int gi = rbase + r;
-            const int ws = gi % wslots;
-            float v[32];
-            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + 32 * r, v);
-            mbar_wait(wfull0 + 8 * ws, (gi / wslots) & 1);
-            double* blk = reinterpret_cast<double*>(sW + ws * wbytes) + erow;  // column erow
-            float* blk32 = reinterpret_cast<float*>(sW + ws * wbytes) + erow;  // fp32 master
-            const int col0 = n0 + 32 * r;
-            if (!skip) {
-              using WT = std::conditional_t<M32, float, double>;
-              WT w[32];
-              if constexpr (M32) {  // fp32 master: one fp32 FMA per weight, rounded once
-                const float alpha32 = (float)alpha;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) w[i] = blk32[i * C::BM];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  w[i] = fmaf(alpha32, v[i], w[i]);
-                  blk32[i * C::BM] = w[i];
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) w[i] = blk[i * C::BM];
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                  w[i] = fma(alpha, (double)v[i], w[i]);
-                  blk[i * C::BM] = w[i];
-                }
-              }
-              if (row_ok && col0 < p.N) {
-                uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)row * p.upd_ld16 + col0;
-                if (col0 + 32 <= p.N && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
-#pragma unroll
-                  for (int j = 0; j < 4; ++j) {
-                    uint4 u;
-                    u.x = pack2<BF16>((float)w[8 * j], (float)w[8 * j + 1]);
-                    u.y = pack2<BF16>((float)w[8 * j + 2], (float)w[8 * j + 3]);
-                    u.z = pack2<BF16>((float)w[8 * j + 4], (float)w[8 * j + 5]);
-                    u.w = pack2<BF16>((float)w[8 * j + 6], (float)w[8 * j + 7]);
-                    __stcs(reinterpret_cast<uint4*>(o) + j, u);
-                  }
-                } else {
-#pragma unroll
-                  for (int i = 0; i < 32; ++i)
-                    if (col0 + i < p.N) o[i] = (uint16_t)(pack2<BF16>((float)w[i], 0.f) & 0xffffu);
-                }
-              }
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            }
-            named_bar_sync(2 + grp, 128);
-            if (storer) {
-              if (!skip) {
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                        reinterpret_cast<uint64_t>(&tmB2)),
-                    "r"(m0), "r"(col0), "r"(smem_u32(sW + ws * wbytes))
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-              }
-              // this group's previous round's store has finished reading its slot: hand it back
-              // (with an even slot count a slot always serves the same group)
-              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-              if (wprev >= 0) mbar_arrive(wempty0 + 8 * (wprev % wslots));
-            }
-            wprev = gi;
-          }
-          wround_e = rbase + BN / 32;
-          goto tile_done;
-        }
-        // W64 += alpha * D with the 16-bit shadow rewritten from the new value (the embedding's
-        // untransposed master; the kernel is HBM-latency-bound: 18 B per weight against 256
-        // MMA FLOPs).  Every lane runs the TMEM loads (.sync.aligned); memory ops are guarded
-        // per row / column.
-        const bool skip = p.upd_abort ? (*p.upd_abort != 0u)
-                                      : !(isfinite(p.upd_out4[0]) && isfinite(p.upd_out4[1]));
-        const double alpha = -(p.upd_lr * p.upd_out4[2]) * p.upd_scale;
-        const bool live = !skip && row_ok;
-#pragma unroll 1
-        for (int c = 32 * grp; c < bnc; c += 32 * EGRP) {
-          // 32 columns per round (the two warp groups alternate): the 32 master loads are in
-          // flight before the first is used
-          const int col0 = n0 + c;
-          const int nc = live ? max(0, min(32, p.N - col0)) : 0;
-          using WT = std::conditional_t<M32, float, double>;
-          WT w[32];
-          const size_t base = p.upd_transposed ? (size_t)col0 * p.upd_ld64 + row : (size_t)row * p.upd_ld64 + col0;
-          const size_t step = p.upd_transposed ? (size_t)p.upd_ld64 : 1;
-          WT* wp = reinterpret_cast<WT*>(p.upd_w64) + base;
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < nc) w[i] = __ldcs(wp + (size_t)i * step);
-          float v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < nc) {
-              if constexpr (M32) w[i] = fmaf((float)alpha, v[i], w[i]);
-              else w[i] = fma(alpha, (double)v[i], w[i]);
-              __stcs(wp + (size_t)i * step, w[i]);
-            }
-          if (nc == 0) continue;
-          uint16_t* o = reinterpret_cast<uint16_t*>(p.upd_w16) + (size_t)row * p.upd_ld16 + col0;
-          if (nc == 32 && (((size_t)row * p.upd_ld16 + col0) % 8) == 0) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              uint4 u;
-              u.x = pack2<BF16>((float)w[8 * j], (float)w[8 * j + 1]);
-              u.y = pack2<BF16>((float)w[8 * j + 2], (float)w[8 * j + 3]);
-              u.z = pack2<BF16>((float)w[8 * j + 4], (float)w[8 * j + 5]);
-              u.w = pack2<BF16>((float)w[8 * j + 6], (float)w[8 * j + 7]);
-              __stcs(reinterpret_cast<uint4*>(o) + j, u);
-            }
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < nc) o[i] = (uint16_t)(pack2<BF16>((float)w[i], 0.f) & 0xffffu);
-          }
-        }
-        goto tile_done;
+        __trap();  // update plans are transposed (gemm_set_update_master checks it)
       }
       if constexpr (EPI == EPI_RESID32) {
         if (p.res_tma) {
@@ -1051,8 +915,6 @@ __global__ void __launch_bounds__((EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ?
       }
     }
   }
-  if constexpr (UPD)
-    if (wtma && warp >= 2 && ((warp - 2) & 3) == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if constexpr (RES)
     if (p.res_tma && warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
@@ -1105,17 +967,19 @@ void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t co
 }
 
 void gemm_set_update_master(GemmDesc& g) {
-  // EPI_UPDATE64 on a projection: a float64 map over the master W64 [N (inputs), M (outputs)]
-  // (row stride upd_ld64), 32 x 128 boxes, no swizzle -- streamed through the kernel's
-  // master-block ring in place of the half-tile B map
-  if (g.epi != EPI_UPDATE64 || !g.upd_transposed) return;
+  // EPI_UPDATE64 plan (run by the EPI_UPDATE32 kernel): an fp32 map over the master
+  // W[N (inputs), M (outputs)] (row stride upd_ld64), 32 x 128 boxes, no swizzle -- streamed
+  // through the kernel's master-block ring in place of the half-tile B map
+  if (g.epi != EPI_UPDATE64) return;
+  if (!g.upd_m32 || !g.upd_transposed)
+    throw Error(ZO_ERR_INTERNAL, "tensor update: fp32 master, transposed plan (D = V U^T) only");
   if (g.cg != 1 && g.cg != 2) throw Error(ZO_ERR_INTERNAL, "bad CTA group");
   if (g.bn % 32 || g.half_n || g.sk) throw Error(ZO_ERR_INTERNAL, "update GEMM: plain tiles only");
   cuuint64_t dims[2] = {(cuuint64_t)g.M, (cuuint64_t)g.N};
-  cuuint64_t strides[1] = {(cuuint64_t)g.upd_ld64 * (g.upd_m32 ? 4 : 8)};
+  cuuint64_t strides[1] = {(cuuint64_t)g.upd_ld64 * 4};
   cuuint32_t box[2] = {128, 32};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = get_encode()(&g.tmB2, g.upd_m32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+  CUresult r = get_encode()(&g.tmB2, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                             g.upd_w64, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1209,8 +1073,8 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms) {
 
 template <int BN, int EPI, int BF16, int XR, int CG>
 static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = -1, int last_ksteps = -1) {
-  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32, EPI == EPI_RESID32>;
-  constexpr int NT = (EPI == EPI_UPDATE64 || EPI == EPI_UPDATE32) ? 320 : 192;  // k_gemm's launch bounds
+  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE32, EPI == EPI_RESID32>;
+  constexpr int NT = EPI == EPI_UPDATE32 ? 320 : 192;  // k_gemm's launch bounds
   static bool attr_set = false;
   if (!attr_set) {
     ZO_CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI, BF16, XR, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1319,9 +1183,8 @@ static void launch_e(const GemmDesc& g, cudaStream_t st) {
       else launch_t<BN, EPI_GELU16_EXT, BF16, 8, CG>(g, st);
       break;
     case EPI_RESID32: launch_t<BN, EPI_RESID32, BF16, 0, CG>(g, st); break;
-    case EPI_UPDATE64:
-      if (g.upd_m32) launch_t<BN, EPI_UPDATE32, BF16, 0, CG>(g, st);
-      else launch_t<BN, EPI_UPDATE64, BF16, 0, CG>(g, st);
+    case EPI_UPDATE64:  // fp32 master, transposed (gemm_set_update_master checked both)
+      launch_t<BN, EPI_UPDATE32, BF16, 0, CG>(g, st);
       break;
     default: launch_t<BN, EPI_STORE32, BF16, 0, CG>(g, st); break;
   }

@@ -13,11 +13,11 @@ enum EpiKind : int {
   EPI_STORE32 = 3,  // out32[r, c] = acc                       (LM-head logits rows)
   EPI_GELU16_EXT = 4,  // EPI_GELU16 + per-tile partial t_k = sum_c a16[r,c] P[c,k] for the
                        // next GEMM's LoRA K-extension (tpart[n_tile][r][k], deterministic)
-  EPI_UPDATE64 = 5,    // factorized dense update on the tensor cores (zo_engine.py:449-450):
-                       // W64 += alpha * acc (alpha = -(lr*c)*scale from the device coefficient,
-                       // skipped when the step aborted), 16-bit shadow rewritten in the same pass
-  EPI_UPDATE32 = 6,    // EPI_UPDATE64 on an fp32 master (kernel variant; plans say EPI_UPDATE64 +
-                       // upd_m32 = 1)
+  EPI_UPDATE64 = 5,    // factorized dense update on the tensor cores (zo_engine.py:449-450), the
+                       // plan-level kind: W += alpha * acc (alpha = -(lr*c)*scale from the device
+                       // coefficient, skipped when the step aborted) on an fp32 master, the
+                       // 16-bit shadow rewritten in the same pass; D = V U^T (upd_transposed)
+  EPI_UPDATE32 = 6,    // the kernel variant that runs EPI_UPDATE64 plans
 };
 
 // D[M, N] = A[M, Kp] * B[N, Kp]^T, both operands K-major 16-bit, fp32 accumulate.
@@ -47,13 +47,13 @@ struct GemmDesc {
   int bias_rps = 0;
   long bias_vstride = 0;
   int relu = 0;  // EPI_GELU16*: ReLU instead of GELU-tanh (OPT arch)
-  // EPI_UPDATE64: the float64 master (row stride upd_ld64) and its 16-bit shadow (row stride
-  // upd_ld16); upd_transposed = 1: D = V U^T, D[j, i] updates W64[i, j] and W16T[j, i]
-  // (projections); 0: D = U V^T, D[i, j] updates W64[i, j] and W16[i, j] (embedding)
+  // EPI_UPDATE64: the fp32 master (upd_w64 cast, row stride upd_ld64) and its 16-bit shadow
+  // (row stride upd_ld16); upd_transposed = 1 (required): D = V U^T, D[j, i] updates W[i, j]
+  // and W16T[j, i] (projections) or W16[i, j] (upd_shadow_rm: the embedding)
   double* upd_w64 = nullptr;
   void* upd_w16 = nullptr;
   int upd_ld64 = 0, upd_ld16 = 0, upd_transposed = 0;
-  int upd_m32 = 0;  // upd_w64 actually holds fp32 values (the fast update mode's fp32 master)
+  int upd_m32 = 0;  // upd_w64 holds fp32 values (required: the tensor update mode's fp32 master)
   int upd_shadow_rm = 0;
   int res_tma = 0;  // EPI_RESID32 through cp.reduce.async.bulk (tmO), set by gemm_plan  // upd_transposed with a row-major shadow W16[i][j] (the embedding, fp32 master)
   const double* upd_out4 = nullptr;
