@@ -21,6 +21,9 @@ M="--metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum -
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt
 timeout 900 python bench.py --model $MODEL > gpurun_out/${TAG}_bench.log 2>&1
 tail -1 gpurun_out/${TAG}_bench.log > gpurun_out/${TAG}_bench.json
+timeout 600 python bench.py --model $MODEL --estimator factorized_sqrt_r --rank 128 --dense-update tensor --no-cpu-baseline \
+  --no-materialising > gpurun_out/${TAG}_bench_fact.log 2>&1
+tail -1 gpurun_out/${TAG}_bench_fact.log > gpurun_out/${TAG}_bench_fact_tensor.json
 timeout 900 ncu $M -s 1200 -c 500 --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_launches.log 2>&1
 # layer GEMMs: skip step 0 + layer 0
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 165 -c 5 \
