@@ -1537,8 +1537,7 @@ int zo_score_options(zo_ctx* c, const int32_t* tokens, const int32_t* options, i
       stage_batch(c, tokens, gold.data(), B, 1);
       do_score(c, B, 1);  // logits of the scored rows stay in c->logits
     } else {
-      for (int32_t b = 0; b < B; ++b)
-        check(options[j] >= 0 && options[j] < c->d.vocab, ZO_ERR_INPUT, "gold token id out of range");
+      check(options[j] >= 0 && options[j] < c->d.vocab, ZO_ERR_INPUT, "gold token id out of range");
       ZO_CUDA_TRY(cudaStreamSynchronize(c->st));  // the pinned gold staging is reused
       std::memcpy(c->h_gold, gold.data(), (size_t)B * 4);
       std::memcpy(c->h_gold + B, gold.data(), (size_t)B * 4);
