@@ -35,6 +35,22 @@ def test_strict_compare_self_and_fault(golden_dir):
     assert len(record_deltas(recs)) == len(recs)
 
 
+def test_strict_compare_skips_unaudited_digests(golden_dir):
+    """run_serving_path(digest_every=k) leaves the records between audits with empty digests:
+    strict_compare compares the audited ones only, counts them, and still checks losses."""
+    t = read_trajectory(os.path.join(golden_dir, "traj_micro_lozo.jsonl"))
+    h, recs, fin = copy.deepcopy(t)
+    for i, r in enumerate(recs):
+        if i % 4:
+            r.u_digest = r.v_digest = ""
+    rep = strict_compare(t, (h, recs, fin))
+    assert rep.accepted == rep.steps and rep.digests_audited == len(range(0, len(recs), 4))
+    recs[4].u_digest = "0" * 16  # a wrong audited digest is still caught
+    recs[1].loss_minus += 1e-3   # and an unaudited step's loss is still compared
+    rep = strict_compare(t, (h, recs, fin), loss_tol=1e-6)
+    assert rep.digest_mismatch_steps == [recs[4].step] and rep.loss_mismatch_steps == [recs[1].step]
+
+
 def test_rank_check():
     g = np.random.default_rng(0)
     low = g.standard_normal((20, 2)) @ g.standard_normal((2, 30))
