@@ -273,6 +273,7 @@ struct GemmParams {
   int upd_m32;  // the master holds fp32 values (zo_set_update_mode 1): half the master bytes
   int upd_shadow_rm;  // transposed update whose 16-bit shadow is row-major [i][j] (the embedding)
   int res_tma;  // EPI_RESID32: the residual add as a TMA reduce-add through tmO
+  int relaxed_arrive;  // accumulator hand-back with a relaxed arrive (ZO_RELAXED_ARRIVE=0: release)
   const double* upd_out4;
   double upd_lr, upd_scale;
   const unsigned* upd_abort;
@@ -902,7 +903,10 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (M32) {  // the update's global stores need no ordering against the MMA
+        // the accumulator hand-back orders only the TMEM reads (tcgen05.fence::before_thread_sync
+        // above); the epilogue's global stores need no ordering against the next MMA, so a
+        // relaxed arrive -- a release arrive would first wait for them to be acknowledged
+        if (p.relaxed_arrive || M32) {
           if constexpr (CG == 2)
             mbar_arrive_remote_relaxed(tempty0 + 8 * acc, 0);
           else
@@ -1120,6 +1124,13 @@ static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = 
   p.upd_m32 = g.upd_m32;
   p.upd_shadow_rm = g.upd_shadow_rm;
   p.res_tma = g.res_tma;
+  {
+    static const int relaxed = [] {
+      const char* e = std::getenv("ZO_RELAXED_ARRIVE");
+      return (!e || std::atoi(e) != 0) ? 1 : 0;
+    }();
+    p.relaxed_arrive = relaxed;
+  }
   p.upd_out4 = g.upd_out4;
   p.upd_lr = g.upd_lr;
   p.upd_scale = g.upd_scale;
