@@ -991,7 +991,7 @@ void gemm_set_update_master(GemmDesc& g) {
 }
 
 void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used, int epi,
-               int dtype, void* out, int ldo, int num_sms) {
+               int dtype, void* out, int ldo, int num_sms, int bn_hint) {
   if (lda % 8 || ldb % 8) throw Error(ZO_ERR_DIMENSION, "GEMM leading dimensions must be multiples of 8");
   if (dtype == 2 && epi != EPI_STORE32 && epi != EPI_RESID32)
     throw Error(ZO_ERR_INTERNAL, "tf32 GEMM supports the fp32 epilogues only");
@@ -1012,6 +1012,7 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
     bn = 64;
   else if (N <= 128 || (int64_t)m_tiles * ((N + 255) / 256) < num_sms / 2)
     bn = (int64_t)m_tiles * ((N + 127) / 128) < num_sms / 2 ? 64 : 128;  // small M: spread the weight read
+  if (bn_hint) bn = bn_hint;  // the caller knows better (split-K skinny GEMMs: one N tile reads A once)
   g.bn = bn;
   // CTA pairs (M = 256 per tile) halve the per-CTA B traffic and double the stages
   static const bool cg2_on = [] {

@@ -85,8 +85,9 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms);
 void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
                   uint32_t box_rows, int dtype);
 // Fill a GemmDesc. A is [Mpad, lda] (lda >= Kp), B is [N, ldb]; dtype as make_tmap_2d.
+// bn_hint: force the tile width (64 / 128 / 256) instead of the occupancy heuristic.
 void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used,
-               int epi, int dtype, void* out, int ldo, int num_sms);
+               int epi, int dtype, void* out, int ldo, int num_sms, int bn_hint = 0);
 void gemm_launch(const GemmDesc& g, cudaStream_t st);
 // skinny GEMMs (few output tiles, long K -- the high-rank LoRA-extension t = a . P): split K over
 // `splits` CTAs per tile; partial s lands at out + s * split_stride (EPI_STORE32), summed by the

@@ -124,10 +124,33 @@ __global__ void __launch_bounds__(256) k_ext_finalize(const float* __restrict__ 
   }
 }
 
+// few tiles (the high-rank split-K partials): a thread per (row, k) pair sums its <= 16
+// partials in tile order (independent loads, unrolled) -- the grouped kernel's 32-pair CTAs
+// were thousands of tiny CTAs at M x r = 2016 x 128
+__global__ void __launch_bounds__(256) k_ext_finalize_flat(const float* __restrict__ tpart, int ntiles, int ld,
+                                                           int M, int r, void* __restrict__ a, int lda, int K,
+                                                           int ext_terms, bool bf16, int neg_from) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // = row * r + k
+  if (i >= (int64_t)M * r) return;
+  const float* src = tpart + i;
+  const size_t stride = (size_t)ld * r;
+  float t = 0.f;
+#pragma unroll 4
+  for (int j = 0; j < ntiles; ++j) t += src[(size_t)j * stride];
+  const int row = (int)(i / r), k = (int)(i % r);
+  if (neg_from >= 0 && row >= neg_from) t = -t;
+  write_ext(a, (size_t)row * lda + K, k, t, ext_terms, bf16);
+}
+
 void launch_ext_finalize(const float* tpart, int ntiles, int ld, int M, int r, void* a, int lda, int K,
                          int ext_terms, bool bf16, cudaStream_t st, int neg_from) {
   const int64_t pairs = (int64_t)M * r;
-  if (ntiles <= 16)
+  if (ntiles <= 16 && pairs >= 148 * 256)  // the high-rank split-K partials
+    launch_pdl(k_ext_finalize_flat, dim3((unsigned)((pairs + 255) / 256)), dim3(256), 0, st, tpart, ntiles, ld, M,
+               r, a, lda, K, ext_terms, bf16, neg_from);
+  else if (ntiles <= 16)
     launch_pdl(k_ext_finalize<8>, dim3((unsigned)((pairs + 31) / 32)), dim3(256), 0, st, tpart, ntiles, ld, M, r, a,
                lda, K, ext_terms, bf16, neg_from);
   else

@@ -399,8 +399,9 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
           uint16_t* a = static_cast<uint16_t*>(acts[i]) + (size_t)sg * rps * lds[i];
           GemmDesc& g = lp.ext[2 * i + sg];
           // t = a . P_s: a few output tiles over K = 5120 .. 20480 -- split K so every SM works
+          // one N tile per rank block (r <= 128: A read once, the split-K partials fill the SMs)
           gemm_plan(g, a, mext, lds[i], c->P16T + (size_t)sg * c->su + mm[i]->u_off, c->r, (int)mm[i]->m,
-                    (int)mm[i]->m, EPI_STORE32, c->bf16, c->xws, c->r, c->num_sms);
+                    (int)mm[i]->m, EPI_STORE32, c->bf16, c->xws, c->r, c->num_sms, c->r <= 128 ? 128 : 0);
           const int tiles = ((mext + 127) / 128) * ((c->r + g.bn - 1) / g.bn);
           gemm_enable_splitk(g, std::max(1, c->num_sms / tiles), (long)c->Mpad * c->r);
           lp.ext_a[2 * i + sg] = a;
