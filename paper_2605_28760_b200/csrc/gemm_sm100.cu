@@ -229,7 +229,7 @@ struct GemmCfg {
   static constexpr int W_BYTES = 32 * BM * 4;
   // EPI_RESID32: per epilogue warp two 32 x 32 fp32 staging boxes for the TMA reduce-add of
   // the residual (4 warps x 2 x 4 KB), paid for with one operand stage
-  static constexpr int O_BYTES = RES ? 4 * 2 * 32 * 32 * 4 : 0;
+  static constexpr int O_BYTES = RES ? 4 * 2 * 32 * 32 * 4 : 0;  // (also the 16-bit output boxes, OBOX)
   static constexpr int STAGES_MAX = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = UPD ? 3 : (RES && STAGES_MAX * STAGE_BYTES + O_BYTES > 200 * 1024 ? STAGES_MAX - 1 : STAGES_MAX);
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
@@ -363,7 +363,9 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
   // at one warp per scheduler; group g takes the master-block rounds / column chunks = g mod 2
   constexpr int EGRP = UPD ? 2 : 1;
   constexpr bool RES = EPI == EPI_RESID32;
-  using C = GemmCfg<BN, CG, UPD, RES>;
+  // TMA-staged epilogue outputs: the residual reduce-add (RES) and the 16-bit stores
+  constexpr bool OBOX = RES || EPI == EPI_STORE16 || EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT;
+  using C = GemmCfg<BN, CG, UPD, OBOX>;
   constexpr bool BF16 = DT == 1, TF32 = DT == 2;
   constexpr int KE = TF32 ? 32 : 64;  // K elements per 128-byte block
   constexpr uint32_t FMT = TF32 ? 2u : BF16 ? 1u : 0u;  // instruction-descriptor a/b format
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
     if (p.half_n || wtma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
-    if (RES && p.res_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmO)) : "memory");
+    if (OBOX && p.res_tma) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmO)) : "memory");
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, 1);
@@ -795,6 +797,76 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
           goto tile_done;
         }
       }
+      if constexpr (OUT16) {
+        if (p.res_tma) {
+          // 16-bit output through TMA stores: a warp packs 64 columns of its 32 rows into a
+          // SWIZZLE_128B box (two 32-column chunks, 16-byte piece j of row r at j ^ (r & 7)) and
+          // one lane stores it -- no row-per-lane global stores.  N % 64 == 0 (gemm_plan), so a
+          // box is either wholly in range or past N; rows past M are clipped by the map.
+          uint8_t* box0 = sO + (size_t)(warp - 2) * 2 * 4096;
+#pragma unroll 1
+          for (int c = 0; c < bnc; c += 32) {
+            const int col0 = n0 + c;
+            if (col0 >= p.N) break;
+            float v[32];
+            tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
+            if (split) add_partials(v, c);
+            if (bb) add_bias(v, c);
+            if constexpr (GELU) {
+              if (p.relu) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+              }
+            }
+            uint32_t pk[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pk[j] = pack2<BF16>(v[2 * j], v[2 * j + 1]);
+            if constexpr (EPI == EPI_GELU16_EXT) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float a = unpack16<BF16>(pk[i >> 1], i & 1);
+                if constexpr (XR < 8) {
+                  const float* pr = xP + (size_t)(col0 + i) * XR;
+#pragma unroll
+                  for (int k = 0; k < XR; ++k) tp[k] += a * pr[k];
+                } else {
+                  const float* pr = xP + (size_t)(col0 + i) * p.xr;
+#pragma unroll
+                  for (int k = 0; k < 8; ++k)
+                    if (k < p.xr) tp[k] += a * pr[k];
+                }
+              }
+            }
+            const int half = (c >> 5) & 1;
+            uint8_t* box = box0 + obuf * 4096;
+            if (half == 0) {
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              __syncwarp();
+            }
+            uint4* rowp = reinterpret_cast<uint4*>(box + lane * 128);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              rowp[(half * 4 + j) ^ (lane & 7)] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            if (half == 1) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                        reinterpret_cast<uint64_t>(&tmO)),
+                    "r"(col0 - 32), "r"(m0 + q * 32), "r"(smem_u32(box))
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+              }
+              obuf ^= 1;
+            }
+          }
+          goto tile_done;
+        }
+      }
 #pragma unroll 1
       for (int c = 0; c < bnc; c += 32) {
         float v[32];
@@ -919,7 +991,7 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
       }
     }
   }
-  if constexpr (RES)
+  if constexpr (OBOX)
     if (p.res_tma && warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   __syncthreads();
   if (tr && threadIdx.x == 0) tr[1] = globaltimer();
@@ -1041,6 +1113,24 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
     return !e || std::atoi(e) != 0;
   }();
   g.res_tma = 0;
+  static const bool out_tma_on = [] {
+    const char* e = std::getenv("ZO_OUT_TMA");
+    return !e || std::atoi(e) != 0;
+  }();
+  const bool out16 = epi == EPI_STORE16 || epi == EPI_GELU16 || epi == EPI_GELU16_EXT;
+  if (out16 && dtype != 2 && out_tma_on && N % 64 == 0 && ((size_t)ldo * 2) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(out) % 16) == 0) {
+    // 16-bit outputs through TMA stores: [M, N] (row stride ldo) in 32 x 64 boxes, SWIZZLE_128B
+    cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
+    cuuint64_t strides[1] = {(cuuint64_t)ldo * 2};
+    cuuint32_t box[2] = {64, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&g.tmO, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, out, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(ZO_ERR_CUDA, "cuTensorMapEncodeTiled (16-bit output) failed");
+    g.res_tma = 1;
+  }
   if (epi == EPI_RESID32 && res_tma_on && ((size_t)ldo * 4) % 16 == 0 && (reinterpret_cast<uintptr_t>(out) % 16) == 0) {
     cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)M};
     cuuint64_t strides[1] = {(cuuint64_t)ldo * 4};
@@ -1078,7 +1168,8 @@ void gemm_enable_halftail(GemmDesc& g, int num_sms) {
 
 template <int BN, int EPI, int BF16, int XR, int CG>
 static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = -1, int last_ksteps = -1) {
-  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE32, EPI == EPI_RESID32>;
+  using C = GemmCfg<BN, CG, EPI == EPI_UPDATE32,
+                    EPI == EPI_RESID32 || EPI == EPI_STORE16 || EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT>;
   constexpr int NT = EPI == EPI_UPDATE32 ? 320 : 192;  // k_gemm's launch bounds
   static bool attr_set = false;
   if (!attr_set) {

@@ -83,13 +83,15 @@ np.save({out!r}, nll)
 
 
 @pytest.mark.parametrize("env,dim,heads", [("ZO_HALFTAIL", 4096, 32), ("ZO_HALFTAIL", 5120, 40),
-                                           ("ZO_RES_TMA", 5120, 40), ("ZO_RES_TMA", 128, 2)])
+                                           ("ZO_RES_TMA", 5120, 40), ("ZO_RES_TMA", 128, 2),
+                                           ("ZO_OUT_TMA", 5120, 40), ("ZO_OUT_TMA", 128, 2)])
 def test_schedule_variants_bitwise(tmp_path, env, dim, heads):
     """Schedule variants that leave every output element's k-ordered accumulation unchanged
     give bit-identical scores (env switch read once per process, so one subprocess each):
     half-width tail tiles (gemm_enable_halftail: 6.7B qkv, 13B attn_out); the residual add of
     attn_out / ff_down as a TMA reduce-add in L2 vs the epilogue's load / add / store (one
-    fp32 round-to-nearest add per element either way)."""
+    fp32 round-to-nearest add per element either way); the 16-bit outputs of qkv / ff_up as
+    TMA-stored swizzled boxes vs row-per-lane stores (same packed values, another store path)."""
     import subprocess
     repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
