@@ -353,15 +353,21 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 // per MMA), 2 tf32 (kind::tf32 on fp32 storage, 32 elements per K block, K = 8 per MMA; the
 // same 32 bytes per MMA step, so the smem ring and descriptors are shared)
 template <int BN, int EPI, int DT, int XR, int CG>
-__global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
+__global__ void __launch_bounds__(EPI == EPI_UPDATE32 || EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT ? 320 : 192, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
            const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmO, GemmParams p) {
   // EPI_UPDATE32: the tensor update over fp32 masters (the kernel variant of EPI_UPDATE64 plans)
   constexpr bool UPD = EPI == EPI_UPDATE32, M32 = UPD;
-  // epilogue warp groups: the update variants run two groups of 4 warps (320 threads) -- their
-  // epilogue is the whole kernel (a read-modify-write of every master block), latency-bound
-  // at one warp per scheduler; group g takes the master-block rounds / column chunks = g mod 2
-  constexpr int EGRP = UPD ? 2 : 1;
+  // epilogue warp groups: the update and GELU variants run two groups of 4 warps (320 threads)
+  // -- one warp per scheduler leaves their epilogues latency-bound (the update's read-modify-
+  // write of every master block; GELU + the extension dot products, ~as long as a d = 2048
+  // tile's MMAs).  Update: group g takes the master-block rounds / column chunks = g mod 2;
+  // GELU: group g takes the tile's 128-column half g (all of a half-width or <= 128 tile).
+  constexpr bool GELU = (EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT);
+  constexpr int EGRP = (UPD || GELU) ? 2 : 1;
+  // the extension partials t += a . P are summed per 128-column slot (min(BN, 128)): a full
+  // tile, its two half-width tail tiles and either epilogue group give the same sums
+  constexpr int SLOT = BN < 128 ? BN : 128;
   constexpr bool RES = EPI == EPI_RESID32;
   // TMA-staged epilogue outputs: the residual reduce-add (RES) and the 16-bit stores
   constexpr bool OBOX = RES || EPI == EPI_STORE16 || EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT;
@@ -559,7 +565,7 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
         // [BN/4][128 rows] float4 layout: the 32 lanes of a store write 512 contiguous bytes
         float4* ws = reinterpret_cast<float4*>(p.sk_ws + (size_t)blockIdx.x * C::BM * BN) + erow;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 32 * grp; c < BN; c += 32 * EGRP) {
           float v[32];
           tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
 #pragma unroll
@@ -575,7 +581,7 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
             mbar_arrive(tempty0 + 8 * acc);
         }
         __threadfence();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 128 * EGRP);
         if (warp == 2 && lane == 0) st_release(p.sk_flags + blockIdx.x, 1u);
         continue;
       }
@@ -633,8 +639,10 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
           }
         }
       };
-      constexpr bool GELU = (EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT);
       constexpr bool OUT16 = (EPI == EPI_STORE16 || GELU);
+      // this warp's columns of the tile: group g of a GELU kernel its slot g, else all
+      const int cb = GELU ? grp * SLOT : 0;
+      const int ce = GELU ? (cb + SLOT < bnc ? cb + SLOT : bnc) : bnc;
       float tp[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) tp[k] = 0.f;
@@ -803,9 +811,11 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
           // SWIZZLE_128B box (two 32-column chunks, 16-byte piece j of row r at j ^ (r & 7)) and
           // one lane stores it -- no row-per-lane global stores.  N % 64 == 0 (gemm_plan), so a
           // box is either wholly in range or past N; rows past M are clipped by the map.
-          uint8_t* box0 = sO + (size_t)(warp - 2) * 2 * 4096;
+          // (one box per warp when two groups share the 32 KB of staging)
+          constexpr int NBOX = EGRP == 2 ? 1 : 2;
+          uint8_t* box0 = sO + (size_t)(warp - 2) * NBOX * 4096;
 #pragma unroll 1
-          for (int c = 0; c < bnc; c += 32) {
+          for (int c = cb; c < ce; c += 32) {
             const int col0 = n0 + c;
             if (col0 >= p.N) break;
             float v[32];
@@ -841,9 +851,14 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
               }
             }
             const int half = (c >> 5) & 1;
-            uint8_t* box = box0 + obuf * 4096;
+            uint8_t* box = box0 + (NBOX == 2 ? obuf : 0) * 4096;
             if (half == 0) {
-              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+              if (lane == 0) {
+                if constexpr (NBOX == 2)
+                  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                else
+                  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              }
               __syncwarp();
             }
             uint4* rowp = reinterpret_cast<uint4*>(box + lane * 128);
@@ -868,7 +883,7 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
         }
       }
 #pragma unroll 1
-      for (int c = 0; c < bnc; c += 32) {
+      for (int c = cb; c < ce; c += 32) {
         float v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c, v);
         if (split) add_partials(v, c);
@@ -962,13 +977,13 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 ? 320 : 192, 1)
     tile_done:
       if (tr && warp == 2 && lane == 0 && it < 15) tr[33 + 2 * it] = globaltimer();
       if (split) {
-        named_bar_sync(1, 128);
+        named_bar_sync(1, 128 * EGRP);
         if (warp == 2 && lane < jend - jfirst)  // re-arm the consumed flags for the next launch
           for (int j = jfirst + lane; j < jend; j += 32) p.sk_flags[j * CG + (int)rank] = 0u;
       }
       if constexpr (EPI == EPI_GELU16_EXT) {
-        if (row_ok) {
-          float* dst = p.tpart + ((size_t)(n0 / BN) * p.tpart_ld + row) * p.xr;
+        if (row_ok && cb < ce && n0 + cb < p.N) {
+          float* dst = p.tpart + ((size_t)((n0 + cb) / SLOT) * p.tpart_ld + row) * p.xr;
           for (int k = 0; k < p.xr && k < 8; ++k) dst[k] = tp[k];
         }
       }
@@ -1147,13 +1162,13 @@ void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N,
 static int max_pair_units(int num_sms);
 
 void gemm_enable_halftail(GemmDesc& g, int num_sms) {
-  // pair tiles only, no stream-K, and not the GELU epilogue (its extension partials are
-  // indexed per full tile)
+  // pair tiles only, no stream-K (the GELU epilogue's extension partials are per 128-column
+  // slot, so half-width tiles write whole slots)
   static const bool on = [] {
     const char* e = std::getenv("ZO_HALFTAIL");
     return !e || std::atoi(e) != 0;
   }();
-  if (!on || g.sk || g.cg != 2 || g.bn != 256 || g.epi == EPI_GELU16_EXT) return;
+  if (!on || g.sk || g.cg != 2 || g.bn != 256) return;
   int units = std::min(g.grid / 2, max_pair_units(num_sms));
   const int m_tiles = (g.M + 255) / 256, n_tiles = (g.N + 255) / 256;
   const int tiles = m_tiles * n_tiles;
@@ -1170,7 +1185,7 @@ template <int BN, int EPI, int BF16, int XR, int CG>
 static void launch_t(const GemmDesc& g, cudaStream_t st, int kb0 = 0, int nkb = -1, int last_ksteps = -1) {
   using C = GemmCfg<BN, CG, EPI == EPI_UPDATE32,
                     EPI == EPI_RESID32 || EPI == EPI_STORE16 || EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT>;
-  constexpr int NT = EPI == EPI_UPDATE32 ? 320 : 192;  // k_gemm's launch bounds
+  constexpr int NT = (EPI == EPI_UPDATE32 || EPI == EPI_GELU16 || EPI == EPI_GELU16_EXT) ? 320 : 192;  // k_gemm's launch bounds
   static bool attr_set = false;
   if (!attr_set) {
     ZO_CUDA_TRY(cudaFuncSetAttribute(k_gemm<BN, EPI, BF16, XR, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -11,8 +11,8 @@ enum EpiKind : int {
   EPI_GELU16 = 1,   // out16[r, c] = gelu_tanh(acc)            (ff_up, model.py:145-146,197)
   EPI_RESID32 = 2,  // x32[r, c] += acc                        (attn_out / ff_down residual)
   EPI_STORE32 = 3,  // out32[r, c] = acc                       (LM-head logits rows)
-  EPI_GELU16_EXT = 4,  // EPI_GELU16 + per-tile partial t_k = sum_c a16[r,c] P[c,k] for the
-                       // next GEMM's LoRA K-extension (tpart[n_tile][r][k], deterministic)
+  EPI_GELU16_EXT = 4,  // EPI_GELU16 + partial t_k = sum_c a16[r,c] P[c,k] per 128-column slot
+                       // for the next GEMM's LoRA K-extension (tpart[slot][r][k], deterministic)
   EPI_UPDATE64 = 5,    // factorized dense update on the tensor cores (zo_engine.py:449-450), the
                        // plan-level kind: W += alpha * acc (alpha = -(lr*c)*scale from the device
                        // coefficient, skipped when the step aborted) on an fp32 master, the
@@ -89,6 +89,11 @@ void make_tmap_2d(CUtensorMap* map, const void* base, uint64_t rows, uint64_t co
 void gemm_plan(GemmDesc& g, const void* A, int M, int lda, const void* B, int N, int ldb, int Kp_used,
                int epi, int dtype, void* out, int ldo, int num_sms, int bn_hint = 0);
 void gemm_launch(const GemmDesc& g, cudaStream_t st);
+// EPI_GELU16_EXT: the number of extension-partial slots (min(bn, 128) columns each) over N
+inline int gemm_ext_slots(const GemmDesc& g, int N) {
+  const int s = g.bn < 128 ? g.bn : 128;
+  return (N + s - 1) / s;
+}
 // skinny GEMMs (few output tiles, long K -- the high-rank LoRA-extension t = a . P): split K over
 // `splits` CTAs per tile; partial s lands at out + s * split_stride (EPI_STORE32), summed by the
 // caller in a fixed order.  Returns the number of splits used.

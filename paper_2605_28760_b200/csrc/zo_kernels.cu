@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(256) k_ln_ext_reg(const float* __restrict__ x3
 // bytes a row touches) are loaded once for the R rows, which also share each
 // block-reduction round.
 template <int NPT, int XR, int R>
-__global__ void __launch_bounds__(256) k_ln_row(const float* __restrict__ x32, const float* __restrict__ g,
+__global__ void __launch_bounds__(256, NPT <= 5 ? 4 : 2) k_ln_row(const float* __restrict__ x32, const float* __restrict__ g,
                                                 const float* __restrict__ bta, int d, void* __restrict__ out, int ldo,
                                                 bool bf16, const float* __restrict__ Pp, const float* __restrict__ Pm,
                                                 int rows_per_sign, int ext_terms, long vstride) {

@@ -368,7 +368,7 @@ RowPlan& row_plan(zo_ctx* c, int M, int nsign = 2) {
       lp.up.xrps = M / nsign;
       lp.up.tpart_ld = c->Mpad;
       lp.up.tpart = c->tpart;
-      check((4 * d + lp.up.bn - 1) / lp.up.bn <= c->tpart_tiles, ZO_ERR_INTERNAL, "tpart too small");
+      check(gemm_ext_slots(lp.up, 4 * d) <= c->tpart_tiles, ZO_ERR_INTERNAL, "tpart too small");
     }
     gemm_plan(lp.down, c->gA, M, ldg, w.W16, d, w.ldw, 4 * d + c->ext_used, EPI_RESID32, c->bf16, c->x32, d,
               c->num_sms);
@@ -666,7 +666,7 @@ void do_score(zo_ctx* c, int B, int nsign) {
       launch_ln_ext(c->x32S, c->ln2g[l], c->ln2b[l], S, d, c->hS, ldh, c->bf16, c->Pp + u.u_off, c->Pm + u.u_off,
                     c->r, S / nsign, c->ext_terms, c->vstride, c->st);
       gemm_launch(rp.last_up, c->st);
-      launch_ext_finalize(c->tpart, (4 * d + rp.last_up.bn - 1) / rp.last_up.bn, c->Mpad, S, c->r, c->gS, ldg,
+      launch_ext_finalize(c->tpart, gemm_ext_slots(rp.last_up, 4 * d), c->Mpad, S, c->r, c->gS, ldg,
                           4 * d, c->ext_terms, c->bf16, c->st);
       gemm_launch(rp.last_down, c->st);
       break;
@@ -686,7 +686,7 @@ void do_score(zo_ctx* c, int B, int nsign) {
     gemm_launch(lp.up, c->st);
     prof_mark(c, PK_EXT);
     if (c->fused_ext)
-      launch_ext_finalize(c->tpart, (4 * d + lp.up.bn - 1) / lp.up.bn, c->Mpad, M, c->r, c->gA, ldg, 4 * d,
+      launch_ext_finalize(c->tpart, gemm_ext_slots(lp.up, 4 * d), c->Mpad, M, c->r, c->gA, ldg, 4 * d,
                           c->ext_terms, c->bf16, c->st);
     else
       ext_gemm(lp, 3);
