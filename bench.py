@@ -527,7 +527,13 @@ def main():
             t_prof = t_first + args.steps
             eng.profile_step(zcfg.seed, t_prof, zcfg.nu, zcfg.epsilon, zcfg.learning_rate,
                              d_tok[0].data_ptr(), d_gold[0].data_ptr(), Bl)  # plans warm
-            fam = eng.profile_step(zcfg.seed, t_prof + 1, zcfg.nu, zcfg.epsilon, zcfg.learning_rate,
+            # a hot lead-in of captured steps queued right in front of the profiled step (no
+            # host sync between them), so it runs in the timed region's power / clock state
+            # -- a step started from an idle GPU runs ~10% faster under the power cap
+            lead = 20
+            for i in range(lead):
+                one_step(t_prof + 1 + i, d_tok[i % len(d_tok)].data_ptr(), d_gold[i % len(d_gold)].data_ptr())
+            fam = eng.profile_step(zcfg.seed, t_prof + 1 + lead, zcfg.nu, zcfg.epsilon, zcfg.learning_rate,
                                    d_tok[0].data_ptr(), d_gold[0].data_ptr(), Bl)
         else:
             fam = None
