@@ -235,6 +235,7 @@ struct zo_ctx {
   cudaStream_t snap_st = nullptr;
   double* snap_dev[2] = {nullptr, nullptr};
   double* snap_host[2][SNAP_RING] = {};
+  bool snap_taken[2][SNAP_RING] = {};  // a snapshot was started into the slot
   cudaEvent_t snap_ready[2][SNAP_RING] = {}, snap_done[2][SNAP_RING] = {};
   cudaEvent_t snap_last[2] = {nullptr, nullptr};  // the last D2H out of snap_dev[which]
   uint64_t* d_base = nullptr;  // q-direction macro-step base step (t * G), set before the apply graph
@@ -1376,9 +1377,14 @@ int zo_slot_snapshot(zo_ctx* c, int32_t which, int32_t slot) {
   if (!c->snap_st) ZO_CUDA_TRY(cudaStreamCreateWithFlags(&c->snap_st, cudaStreamNonBlocking));
   if (!c->snap_dev[which]) c->snap_dev[which] = c->mem.get<double>(n);
   if (!c->snap_host[which][slot]) {
-    ZO_CUDA_TRY(cudaMallocHost(&c->snap_host[which][slot], n * 8));
-    ZO_CUDA_TRY(cudaEventCreateWithFlags(&c->snap_ready[which][slot], cudaEventDisableTiming));
-    ZO_CUDA_TRY(cudaEventCreateWithFlags(&c->snap_done[which][slot], cudaEventDisableTiming));
+    // the whole ring at once (pinned allocations take milliseconds: none inside a run's
+    // steady state, e.g. at the first window boundary of a timed span)
+    for (int k = 0; k < zo_ctx::SNAP_RING; ++k) {
+      if (c->snap_host[which][k]) continue;
+      ZO_CUDA_TRY(cudaMallocHost(&c->snap_host[which][k], n * 8));
+      ZO_CUDA_TRY(cudaEventCreateWithFlags(&c->snap_ready[which][k], cudaEventDisableTiming));
+      ZO_CUDA_TRY(cudaEventCreateWithFlags(&c->snap_done[which][k], cudaEventDisableTiming));
+    }
   }
   // the previous D2H out of the device copy must be done before it is overwritten, and this
   // host slot's previous copy must have been consumed (the caller waited on it)
@@ -1390,13 +1396,14 @@ int zo_slot_snapshot(zo_ctx* c, int32_t which, int32_t slot) {
                               c->snap_st));
   ZO_CUDA_TRY(cudaEventRecord(c->snap_done[which][slot], c->snap_st));
   c->snap_last[which] = c->snap_done[which][slot];
+  c->snap_taken[which][slot] = true;
   return ZO_OK;
   ZO_API_END
 }
 
 int zo_slot_snapshot_wait(zo_ctx* c, int32_t which, int32_t slot, const double** host) {
   ZO_API_BEGIN
-  check((which == 0 || which == 1) && slot >= 0 && slot < zo_ctx::SNAP_RING && c->snap_host[which][slot],
+  check((which == 0 || which == 1) && slot >= 0 && slot < zo_ctx::SNAP_RING && c->snap_taken[which][slot],
         ZO_ERR_INPUT, "no such snapshot");
   ZO_CUDA_TRY(cudaEventSynchronize(c->snap_done[which][slot]));
   *host = c->snap_host[which][slot];

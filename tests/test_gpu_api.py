@@ -221,3 +221,29 @@ def test_step_directions_match_reference(golden_dir, name):
         assert set(d.vectors) == set(params.engine.vids)
     elif zcfg.scope == "full":
         assert all(v.shape == (mcfg.dim,) for v in d.vectors.values())
+
+
+def test_slot_snapshot_ring():
+    """zo_slot_snapshot / zo_slot_snapshot_wait (the digest path's asynchronous U / V copies):
+    a landed snapshot equals the arena at snapshot time even after the arena moves on, ring
+    slots are independent, and waiting on a slot never snapshotted is an InputError."""
+    from paper_2605_28760_b200.engine import ZoEngine, U, V
+    from paper_2605_28760_b200.errors import InputError
+    eng = ZoEngine(512, 128, 2, 2, 63, max_batch=16, rank=2)
+    eng.init_params(7, 0.02)
+    eng.sample_u(42, 0)
+    eng.sample_v(42, 0, 50)
+    u0, v0 = eng.get_slot(U), eng.get_slot(V)
+    eng.snapshot(U, 0)
+    eng.snapshot(V, 0)
+    eng.sample_u(42, 1)  # the arena moves on in stream order after the device copy
+    u1 = eng.get_slot(U)
+    assert not np.array_equal(u0, u1)
+    eng.snapshot(U, 1)
+    np.testing.assert_array_equal(eng.snapshot_wait(U, 0), u0)
+    np.testing.assert_array_equal(eng.snapshot_wait(U, 1), u1)
+    np.testing.assert_array_equal(eng.snapshot_wait(V, 0), v0)
+    with pytest.raises(InputError):
+        eng.snapshot_wait(U, 2)  # allocated with the ring, never written
+    with pytest.raises(InputError):
+        eng.snapshot(U, 4)  # past the ring depth (zob200.h SNAP_RING)
