@@ -216,7 +216,7 @@ __device__ __forceinline__ float unpack16(uint32_t w, int hi) {
   else return __half2float(__ushort_as_half(h));
 }
 
-template <int BN, int CG = 1, bool UPD = false, bool RES = false>
+template <int BN, int CG = 1, bool UPD = false, bool OBOX = false>
 struct GemmCfg {
   static constexpr int BM = 128, BK = 64;  // rows per CTA; a CTA pair (CG = 2) covers 256
   static constexpr int A_BYTES = BM * BK * 2;
@@ -227,11 +227,13 @@ struct GemmCfg {
   // the same epilogue warp group
   static constexpr int W_SLOTS = UPD ? 8 : 0;
   static constexpr int W_BYTES = 32 * BM * 4;
-  // EPI_RESID32: per epilogue warp two 32 x 32 fp32 staging boxes for the TMA reduce-add of
-  // the residual (4 warps x 2 x 4 KB), paid for with one operand stage
-  static constexpr int O_BYTES = RES ? 4 * 2 * 32 * 32 * 4 : 0;  // (also the 16-bit output boxes, OBOX)
+  // OBOX (the residual and 16-bit-output epilogues): 32 KB of 4 KB staging boxes for the TMA
+  // stores -- per epilogue warp two 32 x 32 fp32 boxes (the residual reduce-add) or 32 x 64
+  // 16-bit boxes (two per warp with one epilogue group, one with two) -- paid for with one
+  // operand stage when the ring would not fit beside them
+  static constexpr int O_BYTES = OBOX ? 4 * 2 * 32 * 32 * 4 : 0;
   static constexpr int STAGES_MAX = (196 * 1024) / STAGE_BYTES > 8 ? 8 : (196 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = UPD ? 3 : (RES && STAGES_MAX * STAGE_BYTES + O_BYTES > 200 * 1024 ? STAGES_MAX - 1 : STAGES_MAX);
+  static constexpr int STAGES = UPD ? 3 : (OBOX && STAGES_MAX * STAGE_BYTES + O_BYTES > 200 * 1024 ? STAGES_MAX - 1 : STAGES_MAX);
   static constexpr int TMEM_COLS = (2 * BN) <= 32 ? 32 : (2 * BN) <= 64 ? 64 : (2 * BN) <= 128 ? 128 : (2 * BN) <= 256 ? 256 : 512;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + W_SLOTS * W_BYTES + O_BYTES + 512;
 };
@@ -272,7 +274,8 @@ struct GemmParams {
   int upd_ld64, upd_ld16, upd_transposed;
   int upd_m32;  // the master holds fp32 values (zo_set_update_mode 1): half the master bytes
   int upd_shadow_rm;  // transposed update whose 16-bit shadow is row-major [i][j] (the embedding)
-  int res_tma;  // EPI_RESID32: the residual add as a TMA reduce-add through tmO
+  int res_tma;  // the epilogue output goes through tmO: the residual as a TMA reduce-add
+                // (EPI_RESID32), 16-bit outputs as TMA stores (EPI_STORE16 / GELU16 / GELU16_EXT)
   int relaxed_arrive;  // accumulator hand-back with a relaxed arrive (ZO_RELAXED_ARRIVE=0: release)
   const double* upd_out4;
   double upd_lr, upd_scale;
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(EPI == EPI_UPDATE32 || EPI == EPI_GELU16 || EP
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   uint8_t* sW = smem + C::STAGES * C::STAGE_BYTES;  // EPI_UPDATE32 master-block ring
-  uint8_t* sO = sW + C::W_SLOTS * C::W_BYTES;  // EPI_RESID32 staging boxes (1024-aligned)
+  uint8_t* sO = sW + C::W_SLOTS * C::W_BYTES;  // OBOX staging boxes (1024-aligned)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sO + C::O_BYTES);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::STAGES + 4 + 2 * C::W_SLOTS);
   // the tensor update (EPI_UPDATE32): fp32 master blocks TMA-loaded through the sW ring

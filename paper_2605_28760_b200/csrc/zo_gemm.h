@@ -25,7 +25,7 @@ struct GemmDesc {
   CUtensorMap tmA;
   CUtensorMap tmB;
   CUtensorMap tmB2;  // B with a half-height box: the half-width tail tiles (gemm_enable_halftail)
-  CUtensorMap tmO;   // EPI_RESID32: the residual as a TMA reduce-add target (res_tma)
+  CUtensorMap tmO;   // the epilogue output for TMA stores / reduce-adds (res_tma)
   int M = 0, N = 0;
   int num_kb = 0;       // 64-wide K blocks
   int last_ksteps = 4;  // 16-wide UMMA steps issued in the last K block (trims the LoRA extension)
@@ -54,8 +54,9 @@ struct GemmDesc {
   void* upd_w16 = nullptr;
   int upd_ld64 = 0, upd_ld16 = 0, upd_transposed = 0;
   int upd_m32 = 0;  // upd_w64 holds fp32 values (required: the tensor update mode's fp32 master)
-  int upd_shadow_rm = 0;
-  int res_tma = 0;  // EPI_RESID32 through cp.reduce.async.bulk (tmO), set by gemm_plan  // upd_transposed with a row-major shadow W16[i][j] (the embedding, fp32 master)
+  int upd_shadow_rm = 0;  // upd_transposed with a row-major shadow W16[i][j] (the embedding, fp32 master)
+  int res_tma = 0;  // the output goes through tmO (set by gemm_plan): EPI_RESID32 as a
+                    // cp.reduce.async.bulk add, the 16-bit epilogues as TMA stores
   const double* upd_out4 = nullptr;
   double upd_lr = 0.0, upd_scale = 1.0;
   const unsigned* upd_abort = nullptr;
