@@ -1358,7 +1358,10 @@ void gemm_enable_streamk(GemmDesc& g, float* ws, unsigned* flags, int num_sms) {
   int w = (int)((sk_iters + units - 1) / units);
   // too fine: each owner would sum many partials; measured a loss at M=2048 attn_out
   // (12 tail tiles x 81 k-blocks over 74 pairs -> 14 per unit), a gain for ff_down (53)
-  if (w < 32) return;
+  // -- except a 4-way split of a small tail (<= units / 4 tail tiles, >= 16 k-blocks per
+  // unit): 13B attn_out, 12 tail tiles x 81 k-blocks, 92 -> 87 us (vs half-width tail tiles)
+  const bool four_way = 4 * tail <= units && (g.num_kb + 3) / 4 >= 16;
+  if (w < 32 && !four_way) return;
   // only a mostly-empty last wave pays for the fixup (13B: ff_down's 12 of 74 pairs,
   // 382 -> 350 us; qkv's 36/74 and ff_up's 48/74 measured neutral-to-worse)
   if (3 * tail > units) return;

@@ -9,11 +9,11 @@ scoring the N slices one after the other with the same engine state.
   per-example NLLs of every slicing (N = 1, 2, 4, 8) are BITWISE equal -- so c
   and the update are too -- although M changes the tile width, the CTA pairing
   and the half-width tail of every GEMM.
-* ``fast`` schedule (the N = 1 default, stream-K tail on the 13B ff_down): the
-  tail's fp32 partial sums change the last bits of the residual stream, which flips
-  an occasional 16-bit rounding of the next LN output -- observed 2.7e-4 relative
-  (5.7e-3 absolute on NLLs of ~21) per-example NLL at N = 1 vs the row-invariant
-  schedule, i.e. the fp16 scorer's own noise; bounded at 1e-3 relative.
+* ``fast`` schedule (the N = 1 default, stream-K tails on the 13B ff_down and the 4-way
+  tails on attn_out / qkv): the tails' fp32 partial sums change the last bits of the
+  residual stream, which flips an occasional 16-bit rounding of the next LN output --
+  observed up to 1.2e-3 relative (2.5e-2 absolute on NLLs of ~21) per-example NLL vs the
+  row-invariant schedule, i.e. the fp16 scorer's own noise; bounded at 2.5e-3 relative.
 
 Shape: OPT-13B dims (d = 5120, H = 40), two decoder blocks (the first runs every row --
 the last block's attn_out / ff_up / ff_down only see the scored rows), B = 16, T = 64 -- the
@@ -28,7 +28,11 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 D, H, L, V, T, B = 5120, 40, 2, 4096, 64, 16
-FAST_REL = 1e-3  # fast vs row-invariant schedule, relative per-example NLL (observed 2.7e-4)
+# fast vs row-invariant schedule, relative per-example NLL: observed 2.7e-4 with the stream-K
+# tail on ff_down only, 1.2e-3 once the 4-way tail also covers qkv / attn_out (N = 2: 1008 rows)
+# -- fp16 rounding flips in differently-summed tail tiles, amplified by this random-init
+# model's NLLs of ~21 (the GEMMs themselves match fp32 torch, test_gemm_streamk_four_way_tail)
+FAST_REL = 2.5e-3
 
 
 @pytest.fixture(scope="module")

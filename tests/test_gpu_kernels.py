@@ -55,6 +55,26 @@ def test_gemm_streamk_deterministic(streamk, monkeypatch):
     np.testing.assert_array_equal(r1, r2)
 
 
+@pytest.mark.parametrize("epi", [0, 2])
+@pytest.mark.parametrize("M", [2048, 1008])
+def test_gemm_streamk_four_way_tail(M, epi):
+    """The 4-way stream-K tail (13B attn_out: 160 pair tiles on 74 pairs, K = 81 blocks; and
+    its 1008-row slice at N = 2) against torch fp32 on the same 16-bit operands."""
+    import torch
+    from paper_2605_28760_b200.engine import test_gemm
+    rng = np.random.default_rng(M + epi)
+    ta, a16 = _h(rng.standard_normal((M, 5184)), False)
+    tb, b16 = _h(rng.standard_normal((5120, 5184)) * 0.05, False)
+    ref = ta.float() @ tb.float().T
+    C0 = rng.standard_normal((M, 5120)).astype(np.float32) if epi == 2 else None
+    if epi == 2:
+        ref = ref + torch.from_numpy(C0)
+    else:
+        ref = ref.to(torch.float16).float()
+    got = test_gemm(a16, b16, epi=epi, bf16=False, C=C0)
+    np.testing.assert_allclose(got, ref.numpy(), rtol=4e-3, atol=4e-3)
+
+
 def test_sampler_golden_streams(golden_dir):
     from paper_2605_28760_b200.numerics import Role, StreamKey, digest_array, digest_hex, sample_gaussian
     with open(os.path.join(golden_dir, "streams.json")) as f:
@@ -71,6 +91,7 @@ sys.path.insert(0, {repo!r})
 from paper_2605_28760_b200.engine import ZoEngine
 eng = ZoEngine(512, {dim}, 2, {heads}, 63, max_batch=16, rank=2)
 eng.init_params(7, 0.02)
+eng.set_schedule({sched!r})
 eng.sample_v(42, 0, 50)
 eng.sample_u(42, 0)
 rng = np.random.default_rng(0)
@@ -88,7 +109,8 @@ np.save({out!r}, nll)
 def test_schedule_variants_bitwise(tmp_path, env, dim, heads):
     """Schedule variants that leave every output element's k-ordered accumulation unchanged
     give bit-identical scores (env switch read once per process, so one subprocess each):
-    half-width tail tiles (gemm_enable_halftail: 6.7B qkv, 13B attn_out); the residual add of
+    half-width tail tiles (gemm_enable_halftail; under the row-invariant schedule, where no
+    stream-K tail takes precedence: 6.7B qkv, 13B qkv and attn_out); the residual add of
     attn_out / ff_down as a TMA reduce-add in L2 vs the epilogue's load / add / store (one
     fp32 round-to-nearest add per element either way); the 16-bit outputs of qkv / ff_up as
     TMA-stored swizzled boxes vs row-per-lane stores (same packed values, another store path)."""
@@ -97,7 +119,8 @@ def test_schedule_variants_bitwise(tmp_path, env, dim, heads):
     outs = []
     for flag in ("1", "0"):
         out = str(tmp_path / f"nll_{flag}.npy")
-        code = _HALFTAIL_PROBE.format(repo=repo, dim=dim, heads=heads, out=out)
+        code = _HALFTAIL_PROBE.format(repo=repo, dim=dim, heads=heads, out=out,
+                                      sched="row_invariant" if env == "ZO_HALFTAIL" else "fast")
         r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **{env: flag}),
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
